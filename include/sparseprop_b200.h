@@ -1,0 +1,118 @@
+/*
+ * sparseprop_b200.h -- C-ABI of the B200 (sm_100a) e-prop training-step kernels.
+ *
+ * The reference (`sparseprop` 0.1.0, arXiv 2501.11407 artifact) is pure Python and has
+ * no FFI of its own; its hot path is one Python function,
+ *   eprop_sparse_gradient(net, x_seq, label, smooth=False) -> GradResult
+ *   (/root/reference/pkg/src/sparseprop/gradients.py:132-185),
+ * whose per-step loop (gradients.py:157-176) is what these entry points replace, one
+ * kernel per stage of SURVEY.md section 8(b).  The Python host package
+ * `paper_2501_11407_b200` binds them with ctypes (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer unless stated; every call is asynchronous on
+ *     `stream` (a cudaStream_t; 0 = legacy default stream) and never allocates;
+ *   - return 0 on success, 2 on a bad argument (ShapeMismatch / ValueError in Python),
+ *     3 on a launch failure; spb_last_error() returns the message (thread-local);
+ *   - sizes: B batch, n hidden neurons, k inputs, m classes, Tc time-chunk length
+ *     (multiple of 8), len <= Tc valid steps in this chunk, t0 global step of its first
+ *     row, T sequence length; n_pad = round_up(n,128), k_pad = round_up(k,64).
+ *   - spike inputs are uint8 event counts x[b][t][j] (binary for Poisson data,
+ *     small integers after channel pooling, datasets.py:138-159).
+ */
+#ifndef SPARSEPROP_B200_H
+#define SPARSEPROP_B200_H
+
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Library identification / error text. */
+const char* spb_last_error(void);
+int spb_version(void);
+int spb_device_sm(void); /* compute capability of the current device, e.g. 100 */
+
+/* K0  Compact one chunk of dense uint8 spike counts into per-(sample,step) event lists.
+ *     x[b*stride_b + s*k + j] for s < rows; ev[(b*ld_rows+s)*cap + q] = (j<<8)|count in
+ *     increasing j; nnz[b*ld_rows+s] = number of events.  cap >= k, ld_rows >= rows.
+ *     Replaces the dense `net.neuron.w @ x_t` operand preparation (gradients.py:125). */
+int spb_compact_events(const uint8_t* x, long long stride_b, int B, int rows, int ld_rows, int k,
+                       uint32_t* ev, int* nnz, int cap, cudaStream_t stream);
+
+/* K1  Fused forward over one time chunk: event gather of W x_t (fp64 accumulation),
+ *     ALIF/LIF state update, spike and surrogate derivative.
+ *     Replaces _step_state (gradients.py:118-129) + heaviside/surrogate_grad
+ *     (graph.py:40-52) + the readout spike filter (gradients.py:173-174).
+ *     wt      [k][n] transposed input weights, fp32 (w_is_f64=0) or fp64 (1)
+ *     u, a    [B][n] fp64 state, carried across chunks (zero at t=0)
+ *     pass 0 (A): zbar, zsum [B][n] fp64 carried; raster [B][T][ceil(n/32)] bit-packed
+ *                 spikes (optional, may be NULL).
+ *     pass 1 (B): wsig [B][n] = W_out^T g; ctab[T] readout gains c_t; psi2 [B][n] carry;
+ *                 coef [B][Tc][n] float2 (A'_t, Q'_t) for K6 (ALIF only);
+ *                 lp_hi/lp_lo [n][B*Tc] bf16 split of L_t psi_t, K index b*Tc+s. */
+int spb_forward_chunk(int pass, const void* wt, int w_is_f64, const uint32_t* ev, const int* nnz,
+                      int B, int n, int k, int cap, int Tc, int len, int t0, int T, double alpha,
+                      double theta, double slope, double beta, double rho, double kappa,
+                      int reset, int alif, double* u, double* a, double* zbar, double* zsum,
+                      uint32_t* raster, const float* wsig, const double* ctab, float* psi2,
+                      float* coef, void* lp_hi, void* lp_lo, cudaStream_t stream);
+
+/* K4  Presynaptic filter xbar_t = alpha*xbar_{t-1} + x_t (the factorised LIF trace G_u,
+ *     gradients.py:89-94 with H_I = alpha, F rows = x_t; test_gradients.py:81-91).
+ *     xbar_state [B][k] fp64 carry; xf [B][Tc+1][k_pad] fp32 (row 0 = xbar_{t0-1});
+ *     xh/xl [k_pad][B*Tc] bf16 hi/lo split (GEMM operand, K index b*Tc+s). */
+int spb_xbar_chunk(const uint8_t* x, long long stride_b, int B, int k, int k_pad, int Tc,
+                   int len, double alpha, double* xbar_state, float* xf, void* xh, void* xl,
+                   cudaStream_t stream);
+
+/* K3  Readout + loss: s_b = W_out zsum_b, loss_b = CE(s_b, y_b), g_b = softmax - onehot,
+ *     wsig_b = W_out^T g_b.  Replaces gradients.py:163-164,177-178 and
+ *     softmax_cross_entropy (gradients.py:66-75).  wout [m][n] fp64; labels int64 [B]
+ *     (checked in range by the host: LabelOutOfRange); correct[b] = argmax(s_b)==y_b. */
+int spb_readout_loss(const double* wout, const double* zsum, const long long* labels, int B, int n,
+                     int m, double* s_out, double* loss, double* g, float* wsig, int* correct,
+                     cudaStream_t stream);
+
+/* K7  gwo[c][i] += sum_b g[b][c] zsum[b][i]   (gradients.py:181, summed over the batch). */
+int spb_readout_grad(const double* g, const double* zsum, int B, int n, int m, double* gwo,
+                     cudaStream_t stream);
+
+/* K5  Factorised gradient GEMM on tcgen05 tensor cores (TMA-fed, bf16 hi/lo split, fp32
+ *     TMEM accumulation), split-K over `splits` CTAs per 128x128 tile:
+ *       partial[z][i][j] = sum_{K in split z} (Ah+Al)[i][K] (Bh+Bl)[j][K]  (i<M, j<ldp)
+ *     at partial + z*slice_stride (row stride ldp); every slice is written.
+ *     Replaces the xbar/xsum n x k accumulation of gradients.py:165-172,180 for the
+ *     factorisable LIF part G_u = 1 (x) xbar.  A* [M][K], B* [N_rows][K] bf16 K-major,
+ *     16-byte aligned, K % 8 == 0. */
+int spb_grad_gemm_partials(const void* ah, const void* al, const void* bh, const void* bl, int M,
+                           int N_rows, int K, int splits, float* partial, int ldp,
+                           long long slice_stride, cudaStream_t stream);
+
+/* K5s CUDA-core version of K5 on the same operands (test cross-check only). */
+int spb_grad_gemm_simt(const void* ah, const void* al, const void* bh, const void* bl, int M,
+                       int N, int K, double* grad, int ldg, cudaStream_t stream);
+
+/* K6  ALIF adaptation-trace chunk: eps~ state [B][n_pad][k_pad] fp32 (rescaled trace,
+ *     see elig.cu), coef from K1, xf from K4; the batch is split in `splits` contiguous
+ *     ranges, each writing partial[split][n_pad][k_pad].  load_eps=0 on the first
+ *     chunk (eps=0), store_eps=0 on the last.  Replaces the ALIF G_a block of
+ *     eprop_trace_update (gradients.py:89-94) and x_step (gradients.py:165-167). */
+int spb_alif_elig_chunk(const float* coef, const float* xf, float* eps, float* partial, int B,
+                        int n, int n_pad, int k_pad, int Tc, int len, int splits, int load_eps,
+                        int store_eps, cudaStream_t stream);
+
+/* grad[i][j] += sum_{s<splits} partial[s][i][j] in fixed order (fp64). */
+int spb_reduce_partials(const float* partial, int splits, int n, int n_pad, int k_pad,
+                        double* grad, cudaStream_t stream);
+
+/* out[r][c] = acc[r*ld + c] cast to fp32 (out_is_f64=0) or fp64. */
+int spb_finalize_grad(const double* acc, int rows, int cols, int ld, void* out, int out_is_f64,
+                      cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSEPROP_B200_H */

@@ -1,0 +1,60 @@
+// Shared helpers for the sparseprop-b200 kernels (sm_100a only).
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "sparseprop-b200 targets sm_100a (B200) only"
+#endif
+
+namespace spb {
+
+// Last error message of the C-ABI (thread-local, read by spb_last_error()).
+void set_error(const char* fmt, ...);
+
+#define SPB_CHECK_ARG(cond, ...)            \
+  do {                                      \
+    if (!(cond)) {                          \
+      ::spb::set_error(__VA_ARGS__);        \
+      return 2;                             \
+    }                                       \
+  } while (0)
+
+#define SPB_CHECK_LAUNCH(name)                                                  \
+  do {                                                                          \
+    cudaError_t e_ = cudaGetLastError();                                        \
+    if (e_ != cudaSuccess) {                                                    \
+      ::spb::set_error("%s launch failed: %s", name, cudaGetErrorString(e_));   \
+      return 3;                                                                 \
+    }                                                                           \
+  } while (0)
+
+__host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ inline int round_up(int a, int b) { return ceil_div(a, b) * b; }
+
+// Packed fp32x2 FMA (sm_100: FFMA2).  d = a*b + c elementwise on float2 pairs.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+// sigma'(d) = 1 / (1 + slope*|d|)^2  (reference graph.py:40-42), fp64, no contraction.
+__device__ __forceinline__ double surrogate_grad_f64(double d, double slope) {
+  double t = __dadd_rn(1.0, __dmul_rn(slope, fabs(d)));
+  return __ddiv_rn(1.0, __dmul_rn(t, t));
+}
+
+// bf16 hi/lo split of an fp32 value: x ~= hi + lo with |x - hi - lo| <= 2^-16 |x|.
+__device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(x);
+  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+}  // namespace spb

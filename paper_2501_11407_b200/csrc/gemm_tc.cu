@@ -1,0 +1,280 @@
+// K5: factorised e-prop gradient GEMM on 5th-generation tensor cores (tcgen05 + TMA).
+//
+//   grad[i][j] += sum_K A[i][K] * B[j][K],   A = L_t psi_t  (M = n neurons),
+//                                            B = xbar_t     (N = k inputs),
+//   K = (sample, step) pairs of one time chunk (K = B*Tc), so the LIF trace psi (x) xbar
+//   (gradients.py:165-172, G_u = 1 (x) xbar) is never materialised per sample.
+//
+// fp32 accuracy from bf16 tensor cores: every operand is split x = hi + lo (bf16 each)
+// and D += Ah*Bh + Ah*Bl + Al*Bh (the lo*lo term is below fp32 rounding of the sum).
+//
+// Structure (one 128x128 output tile per CTA, split-K over blockIdx.z):
+//   warp 0   TMA producer: 4 tiles (Ah, Al, Bh, Bl; 128x64 bf16, SWIZZLE_128B) per stage
+//   warp 1   TMEM allocation + single-thread tcgen05.mma issue (12 MMAs of 128x128x16 per
+//            64-wide K block), tcgen05.commit releases smem stages / signals the epilogue
+//   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 -> fp32 partial tile (fixed-order reduce later)
+#include "common.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
+
+namespace spb {
+namespace tc {
+
+constexpr int BM = 128, BN = 128, BK = 64, STAGES = 3;
+constexpr int TILE_A = BM * BK * 2;  // bytes
+constexpr int TILE_B = BN * BK * 2;
+constexpr int STAGE_BYTES = 2 * TILE_A + 2 * TILE_B;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int THREADS = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t umma_desc_k_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;             // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;   // SBO
+  d |= (uint64_t)1u << 46;             // descriptor version (sm100)
+  d |= (uint64_t)2u << 61;             // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor: kind::f16, A/B bf16 K-major, D fp32, M=BM, N=BN.
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    grad_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_ah,
+                        const __grid_constant__ CUtensorMap tm_al,
+                        const __grid_constant__ CUtensorMap tm_bh,
+                        const __grid_constant__ CUtensorMap tm_bl, int M, int N, int K,
+                        int kb_per_split, float* __restrict__ partial, int ldp,
+                        long long slice_stride) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = bars;                   // [STAGES]
+  uint64_t* empty = bars + STAGES;         // [STAGES]
+  uint64_t* tmem_full = bars + 2 * STAGES; // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nkb = (K + BK - 1) / BK;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int kb1 = min(nkb, kb0 + kb_per_split);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    mbar_init(smem_u32(tmem_full), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_ah)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_al)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_bh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_bl)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+        const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t fb = smem_u32(&full[s]);
+        mbar_expect_tx(fb, STAGE_BYTES);
+        tma_load_2d(st, &tm_ah, fb, kb * BK, m0);
+        tma_load_2d(st + TILE_A, &tm_al, fb, kb * BK, m0);
+        tma_load_2d(st + 2 * TILE_A, &tm_bh, fb, kb * BK, n0);
+        tma_load_2d(st + 2 * TILE_A + TILE_B, &tm_bl, fb, kb * BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(smem_u32(&full[s]), ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t sah = st, sal = st + TILE_A, sbh = st + 2 * TILE_A,
+                       sbl = st + 2 * TILE_A + TILE_B;
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint32_t off = kk * 32;  // 16 bf16 along K inside the 128-byte swizzle row
+          const uint64_t dah = umma_desc_k_sw128(sah + off), dal = umma_desc_k_sw128(sal + off);
+          const uint64_t dbh = umma_desc_k_sw128(sbh + off), dbl = umma_desc_k_sw128(sbl + off);
+          umma_bf16(tmem_base, dah, dbh, (kb > kb0 || kk > 0) ? 1u : 0u);
+          umma_bf16(tmem_base, dah, dbl, 1u);
+          umma_bf16(tmem_base, dal, dbh, 1u);
+        }
+        umma_commit(smem_u32(&empty[s]));
+      }
+      umma_commit(smem_u32(tmem_full));
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
+    const int q = warp & 3;
+    const int row = m0 + q * 32 + lane;
+    const bool have_work = kb1 > kb0;
+    if (have_work) {
+      mbar_wait(smem_u32(tmem_full), 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    float* prow = partial + (long long)blockIdx.z * slice_stride + (long long)row * ldp;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+            "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+            "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+            "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+            "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < M) {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int col = n0 + c0 + v * 4;
+          if (col < ldp) {
+            float4 o;
+            o.x = have_work ? __uint_as_float(r[v * 4 + 0]) : 0.f;
+            o.y = have_work ? __uint_as_float(r[v * 4 + 1]) : 0.f;
+            o.z = have_work ? __uint_as_float(r[v * 4 + 2]) : 0.f;
+            o.w = have_work ? __uint_as_float(r[v * 4 + 3]) : 0.f;
+            *reinterpret_cast<float4*>(prow + col) = o;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(BN));
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 K-major operand [rows][K] with a 64 x box_rows box, 128-byte swizzle.
+static bool make_map(CUtensorMap* map, const void* ptr, int K, int rows, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace tc
+}  // namespace spb
+
+using namespace spb;
+
+extern "C" {
+
+// Split-K tensor-core GEMM writing fp32 partial tiles:
+//   partial[z][i][j] = sum_{K in split z} (Ah+Al)[i][K] (Bh+Bl)[j][K]   (lo*lo dropped)
+// for i < M, j < ldp; every one of the `splits` slices is written (empty K ranges give 0).
+// Reduced in fixed order with spb_reduce_partials.
+int spb_grad_gemm_partials(const void* ah, const void* al, const void* bh, const void* bl, int M,
+                           int N_rows, int K, int splits, float* partial, int ldp,
+                           long long slice_stride, cudaStream_t stream) {
+  SPB_CHECK_ARG(ah && al && bh && bl && partial, "spb_grad_gemm_partials: null pointer");
+  SPB_CHECK_ARG(M > 0 && N_rows > 0 && K > 0 && K % 8 == 0 && splits > 0 && ldp >= 1,
+                "spb_grad_gemm_partials: bad sizes M=%d N=%d K=%d", M, N_rows, K);
+  SPB_CHECK_ARG((reinterpret_cast<uintptr_t>(ah) | reinterpret_cast<uintptr_t>(al) |
+                 reinterpret_cast<uintptr_t>(bh) | reinterpret_cast<uintptr_t>(bl)) % 16 == 0,
+                "spb_grad_gemm_partials: operands must be 16-byte aligned");
+  CUtensorMap mah, mal, mbh, mbl;
+  if (!tc::make_map(&mah, ah, K, M, tc::BM) || !tc::make_map(&mal, al, K, M, tc::BM) ||
+      !tc::make_map(&mbh, bh, K, N_rows, tc::BN) || !tc::make_map(&mbl, bl, K, N_rows, tc::BN)) {
+    set_error("spb_grad_gemm_partials: cuTensorMapEncodeTiled failed");
+    return 3;
+  }
+  const int nkb = ceil_div(K, tc::BK);
+  const int kbps = ceil_div(nkb, splits);
+  cudaFuncSetAttribute(tc::grad_gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       tc::SMEM_BYTES);
+  dim3 grid(ceil_div(ldp, tc::BN), ceil_div(M, tc::BM), splits);
+  tc::grad_gemm_tc_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, stream>>>(
+      mah, mal, mbh, mbl, M, N_rows, K, kbps, partial, ldp, slice_stride);
+  SPB_CHECK_LAUNCH("grad_gemm_tc");
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// Readout, loss and learning signal (sm_100a):
+//   K3  spb_readout_loss  -- s = W_out zsum (the time-summed leaky readout,
+//                            gradients.py:163-164), softmax cross-entropy
+//                            (gradients.py:66-75), g = softmax - onehot,
+//                            w_sig = W_out^T g (gradients.py:178)
+//   K7  spb_readout_grad  -- grad W_out = sum_b g_b (x) zsum_b (gradients.py:181)
+//   --  spb_finalize_grad -- fp64 gradient accumulator -> caller dtype, padding dropped
+#include "common.cuh"
+
+namespace spb {
+
+__global__ void readout_loss_kernel(const double* __restrict__ wout, const double* __restrict__ zsum,
+                                    const long long* __restrict__ labels, int n, int m,
+                                    double* __restrict__ s_out, double* __restrict__ loss,
+                                    double* __restrict__ g_out, float* __restrict__ wsig,
+                                    int* __restrict__ correct) {
+  extern __shared__ double sm[];  // [m] logits + [m] g + [32] scratch
+  double* s = sm;
+  double* g = sm + m;
+  double* red = sm + 2 * m;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const double* z = zsum + (long long)b * n;
+  for (int c = 0; c < m; ++c) {
+    double acc = 0.0;
+    for (int i = tid; i < n; i += blockDim.x) acc = fma(wout[(long long)c * n + i], z[i], acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nwarps; ++w) t += red[w];
+      s[c] = t;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const int y = (int)labels[b];
+    double mx = s[0];
+    int arg = 0;
+    for (int c = 1; c < m; ++c)
+      if (s[c] > mx) { mx = s[c]; arg = c; }
+    double se = 0.0;
+    for (int c = 0; c < m; ++c) se += exp(s[c] - mx);
+    const double logz = log(se);
+    loss[b] = logz - (s[y] - mx);
+    for (int c = 0; c < m; ++c) {
+      g[c] = exp((s[c] - mx) - logz);
+      s_out[(long long)b * m + c] = s[c];
+    }
+    g[y] -= 1.0;
+    for (int c = 0; c < m; ++c) g_out[(long long)b * m + c] = g[c];
+    if (correct) correct[b] = (arg == y) ? 1 : 0;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < m; ++c) acc = fma(wout[(long long)c * n + i], g[c], acc);
+    wsig[(long long)b * n + i] = (float)acc;
+  }
+}
+
+__global__ void readout_grad_kernel(const double* __restrict__ g, const double* __restrict__ zsum,
+                                    int B, int n, int m, double* __restrict__ gwo) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (int b = 0; b < B; ++b) acc = fma(g[(long long)b * m + c], zsum[(long long)b * n + i], acc);
+  gwo[(long long)c * n + i] += acc;
+}
+
+template <typename OT>
+__global__ void finalize_kernel(const double* __restrict__ acc, int rows, int cols, int ld,
+                                OT* __restrict__ out) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)rows * cols) return;
+  const int r = (int)(idx / cols), c = (int)(idx % cols);
+  out[idx] = (OT)acc[(long long)r * ld + c];
+}
+
+}  // namespace spb
+
+using namespace spb;
+
+extern "C" {
+
+int spb_readout_loss(const double* wout, const double* zsum, const long long* labels, int B, int n,
+                     int m, double* s_out, double* loss, double* g, float* wsig, int* correct,
+                     cudaStream_t stream) {
+  SPB_CHECK_ARG(wout && zsum && labels && s_out && loss && g && wsig,
+                "spb_readout_loss: null pointer");
+  SPB_CHECK_ARG(B > 0 && n > 0 && m > 0 && m <= 4096, "spb_readout_loss: bad sizes");
+  const size_t smem = (size_t)(2 * m + 32) * sizeof(double);
+  readout_loss_kernel<<<B, 256, smem, stream>>>(wout, zsum, labels, n, m, s_out, loss, g, wsig,
+                                                correct);
+  SPB_CHECK_LAUNCH("readout_loss");
+  return 0;
+}
+
+int spb_readout_grad(const double* g, const double* zsum, int B, int n, int m, double* gwo,
+                     cudaStream_t stream) {
+  SPB_CHECK_ARG(g && zsum && gwo, "spb_readout_grad: null pointer");
+  SPB_CHECK_ARG(B > 0 && n > 0 && m > 0, "spb_readout_grad: bad sizes");
+  dim3 grid(ceil_div(n, 128), m);
+  readout_grad_kernel<<<grid, 128, 0, stream>>>(g, zsum, B, n, m, gwo);
+  SPB_CHECK_LAUNCH("readout_grad");
+  return 0;
+}
+
+int spb_finalize_grad(const double* acc, int rows, int cols, int ld, void* out, int out_is_f64,
+                      cudaStream_t stream) {
+  SPB_CHECK_ARG(acc && out && rows > 0 && cols > 0 && ld >= cols, "spb_finalize_grad: bad args");
+  const long long total = (long long)rows * cols;
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  if (out_is_f64)
+    finalize_kernel<double><<<blocks, 256, 0, stream>>>(acc, rows, cols, ld, (double*)out);
+  else
+    finalize_kernel<float><<<blocks, 256, 0, stream>>>(acc, rows, cols, ld, (float*)out);
+  SPB_CHECK_LAUNCH("finalize_grad");
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,274 @@
+"""Device-side e-prop engine: buffers and the chunked two-pass update.
+
+One ``EpropEngine`` owns every device buffer for a fixed problem shape
+(batch B, hidden n, inputs k, classes m, chunk length Tc) and replays the update
+
+    pass A  (forward only)         for each chunk: K0 compact -> K1 forward(A)
+    readout                        K3 loss / g / w_sig ; K7 grad W_out
+    pass B  (forward + traces)     for each chunk: K0 -> K1 forward(B) -> K4 xbar
+                                                  -> K5 tcgen05 GEMM (L psi) x xbar
+                                                  -> K6 ALIF eps chunk (ALIF only)
+                                                  -> fixed-order partial reduce
+
+which is the reference's per-sample online loop (gradients.py:157-176) restated for a
+batch: the learning signal L_t = c_t W_out^T (softmax - onehot) is only known after the
+whole sequence (gradients.py:177-182), so pass B recomputes the (deterministic)
+forward with L_t known (two-pass form).  Memory is independent of T:
+state is per (sample, neuron[, input]) and chunk buffers are sized by Tc.
+
+All work is enqueued on torch's current CUDA stream through the C-ABI (``_lib``); the
+engine never synchronises.  PyTorch provides allocation and streams only.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import LabelOutOfRange, ShapeMismatch
+
+SM_COUNT_DEFAULT = 148
+
+
+def _ptr(t):
+    return ctypes_void(t.data_ptr()) if t is not None else None
+
+
+def ctypes_void(p):
+    import ctypes
+    return ctypes.c_void_p(p)
+
+
+def _round_up(a, b):
+    return (a + b - 1) // b * b
+
+
+def readout_gains(T: int, kappa: float) -> np.ndarray:
+    """c_t = sum_{tau=t}^{T-1} kappa^(tau-t): the gain with which the time-summed leaky
+    readout (gradients.py:163-164) sees a spike at step t; the recurrence matches
+    bptt_gradient's c_t = 1 + kappa*c_{t+1} (gradients.py:218)."""
+    c = np.empty(T, dtype=np.float64)
+    acc = 0.0
+    for t in range(T - 1, -1, -1):
+        acc = 1.0 + kappa * acc
+        c[t] = acc
+    return c
+
+
+def _best_split(B: int, tiles: int, slots: int, min_per_split: int = 2) -> int:
+    """Batch split for K6: a divisor of B giving the best wave efficiency."""
+    best, best_eff = 1, -1.0
+    for d in range(1, B + 1):
+        if B % d or B // d < min_per_split and d != 1:
+            continue
+        ctas = tiles * d
+        waves = math.ceil(ctas / slots)
+        eff = ctas / (waves * slots)
+        # prefer >= 2 waves' worth of CTAs for load balance, then efficiency
+        score = eff + (0.05 if ctas >= 2 * slots else 0.0)
+        if score > best_eff + 1e-9:
+            best, best_eff = d, score
+    return best
+
+
+class EpropEngine:
+    """Buffers + launch sequence for one problem shape on one device."""
+
+    def __init__(self, n: int, k: int, m: int, B: int, *, alif: bool, w_f64: bool = False,
+                 chunk: int = 32, device=None, sm_count: int | None = None):
+        if chunk <= 0 or chunk % 8:
+            raise ValueError("chunk must be a positive multiple of 8")
+        if k >= (1 << 24):
+            raise ShapeMismatch("k too large")
+        self.lib = _lib.load()
+        self.n, self.k, self.m, self.B = int(n), int(k), int(m), int(B)
+        self.alif = bool(alif)
+        self.w_f64 = bool(w_f64)
+        self.Tc = int(chunk)
+        self.device = torch.device(device if device is not None else "cuda")
+        self.n_pad = _round_up(self.n, 128)
+        self.k_pad = _round_up(self.k, 64)
+        sms = sm_count or (torch.cuda.get_device_properties(self.device).multi_processor_count
+                           if self.device.type == "cuda" else SM_COUNT_DEFAULT)
+        self.sm_count = sms
+        dev = self.device
+        f32, f64 = torch.float32, torch.float64
+        Bn, Bk = (self.B, self.n), (self.B, self.k)
+        K = self.B * self.Tc
+        self.K = K
+        # K0 event lists
+        self.ev = torch.empty(self.B * self.Tc * self.k, dtype=torch.int32, device=dev)
+        self.nnz = torch.empty(self.B * self.Tc, dtype=torch.int32, device=dev)
+        # neuron state (fp64) and readout filters
+        self.u = torch.empty(Bn, dtype=f64, device=dev)
+        self.a = torch.empty(Bn, dtype=f64, device=dev)
+        self.zbar = torch.empty(Bn, dtype=f64, device=dev)
+        self.zsum = torch.empty(Bn, dtype=f64, device=dev)
+        self.psi2 = torch.empty(Bn, dtype=f32, device=dev)
+        # readout / loss
+        self.wsig = torch.empty(Bn, dtype=f32, device=dev)
+        self.s = torch.empty((self.B, self.m), dtype=f64, device=dev)
+        self.loss = torch.empty(self.B, dtype=f64, device=dev)
+        self.g = torch.empty((self.B, self.m), dtype=f64, device=dev)
+        self.correct = torch.empty(self.B, dtype=torch.int32, device=dev)
+        # pass-B chunk buffers
+        self.coef = (torch.empty((self.B, self.Tc, self.n, 2), dtype=f32, device=dev)
+                     if self.alif else None)
+        self.lp_hi = torch.empty((self.n, K), dtype=torch.bfloat16, device=dev)
+        self.lp_lo = torch.empty((self.n, K), dtype=torch.bfloat16, device=dev)
+        self.xbar_state = torch.empty(Bk, dtype=f64, device=dev)
+        self.xf = torch.empty((self.B, self.Tc + 1, self.k_pad), dtype=f32, device=dev)
+        self.xh = torch.empty((self.k_pad, K), dtype=torch.bfloat16, device=dev)
+        self.xl = torch.empty((self.k_pad, K), dtype=torch.bfloat16, device=dev)
+        # split-K / batch-split partial slices, reduced in fixed order
+        tiles5 = math.ceil(self.k_pad / 128) * math.ceil(self.n / 128)
+        nkb = math.ceil(K / 64)
+        self.splits5 = max(1, min(nkb, round(sms / tiles5)))
+        if self.alif:
+            tiles6 = (self.k_pad // 64) * (self.n_pad // 128)
+            self.splits6 = _best_split(self.B, tiles6, 2 * sms)
+            self.eps = torch.empty((self.B, self.n_pad, self.k_pad), dtype=f32, device=dev)
+        else:
+            self.splits6 = 0
+            self.eps = None
+        self.partial = torch.empty((self.splits6 + self.splits5, self.n_pad, self.k_pad),
+                                   dtype=f32, device=dev)
+        self.grad_w_acc = torch.empty((self.n, self.k_pad), dtype=f64, device=dev)
+        self.grad_wout = torch.empty((self.m, self.n), dtype=f64, device=dev)
+        # weights
+        self.wt = torch.empty((self.k, self.n), dtype=f64 if self.w_f64 else f32, device=dev)
+        self.wout = torch.empty((self.m, self.n), dtype=f64, device=dev)
+        self._ctab_T = None
+        self.ctab = None
+        self.launches = 0
+
+    # ----------------------------------------------------------------------------------
+    def set_weights(self, w, w_out):
+        """Upload input weights (as W^T [k, n]) and readout weights (fp64)."""
+        w = torch.as_tensor(w)
+        w_out = torch.as_tensor(w_out)
+        if tuple(w.shape) != (self.n, self.k) or tuple(w_out.shape) != (self.m, self.n):
+            raise ShapeMismatch(f"weights {tuple(w.shape)}/{tuple(w_out.shape)} do not match "
+                                f"engine (n={self.n}, k={self.k}, m={self.m})")
+        self.wt.copy_(w.t().to(self.wt.dtype), non_blocking=True)
+        self.wout.copy_(w_out.to(torch.float64), non_blocking=True)
+
+    def _gains(self, T, kappa):
+        if self._ctab_T != (T, kappa):
+            self.ctab = torch.as_tensor(readout_gains(T, kappa), device=self.device)
+            self._ctab_T = (T, kappa)
+        return self.ctab
+
+    # ----------------------------------------------------------------------------------
+    def run(self, x: torch.Tensor, labels: torch.Tensor, *, alpha=0.95, theta=1.0, slope=10.0,
+            beta=0.8, rho=0.96, kappa=0.95, reset=False, raster: torch.Tensor | None = None,
+            stream=None):
+        """One full e-prop update on device-resident inputs.
+
+        x       uint8 [B, T, k] spike counts (CUDA, contiguous)
+        labels  int64 [B] (CUDA)
+        raster  optional int32 [B, T, ceil(n/32)] bit-packed spike output (pass A)
+        Results stay on device: ``grad_w_acc`` (fp64 [n, k_pad]), ``grad_wout``,
+        ``loss``, ``s`` (readout sums), ``correct``.
+        """
+        if reset:
+            raise NotImplementedError(
+                "reset=True makes G_u non-factorisable (SURVEY.md 8(f)-3); not on the B200 path yet")
+        if x.dtype != torch.uint8 or x.dim() != 3 or x.shape[0] != self.B or x.shape[2] != self.k:
+            raise ShapeMismatch(f"x must be uint8 [B={self.B}, T, k={self.k}], got "
+                                f"{tuple(x.shape)} {x.dtype}")
+        if not x.is_contiguous():
+            raise ShapeMismatch("x must be contiguous")
+        T = int(x.shape[1])
+        if T <= 0:
+            raise ShapeMismatch("T must be positive")
+        lib, call = self.lib, _lib.call
+        st = ctypes_void(stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream)
+        if not self.alif:
+            beta_e, rho_e = 0.0, 0.0
+        else:
+            beta_e, rho_e = float(beta), float(rho)
+        B, n, k, m, Tc, K = self.B, self.n, self.k, self.m, self.Tc, self.K
+        ctab = self._gains(T, float(kappa))
+        nchunks = (T + Tc - 1) // Tc
+        strideb = T * k
+        self.launches = 0
+        v = ctypes_void
+        # ---------------- pass A ----------------
+        self.u.zero_(); self.a.zero_(); self.zbar.zero_(); self.zsum.zero_()
+        for c in range(nchunks):
+            t0 = c * Tc
+            ln = min(Tc, T - t0)
+            xp = x.data_ptr() + t0 * k
+            call("spb_compact_events", v(xp), strideb, B, ln, Tc, k, v(self.ev.data_ptr()),
+                 v(self.nnz.data_ptr()), k, st)
+            call("spb_forward_chunk", 0, v(self.wt.data_ptr()), int(self.w_f64),
+                 v(self.ev.data_ptr()), v(self.nnz.data_ptr()), B, n, k, k, Tc, ln, t0, T,
+                 float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
+                 int(self.alif), v(self.u.data_ptr()), v(self.a.data_ptr()),
+                 v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
+                 v(raster.data_ptr()) if raster is not None else None,
+                 None, None, None, None, None, None, st)
+            self.launches += 2
+        # ---------------- readout / loss ----------------
+        call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
+             v(labels.data_ptr()), B, n, m, v(self.s.data_ptr()), v(self.loss.data_ptr()),
+             v(self.g.data_ptr()), v(self.wsig.data_ptr()), v(self.correct.data_ptr()), st)
+        self.grad_wout.zero_()
+        call("spb_readout_grad", v(self.g.data_ptr()), v(self.zsum.data_ptr()), B, n, m,
+             v(self.grad_wout.data_ptr()), st)
+        self.launches += 2
+        # ---------------- pass B ----------------
+        self.u.zero_(); self.a.zero_(); self.psi2.fill_(1.0); self.xbar_state.zero_()
+        self.grad_w_acc.zero_()
+        slice_stride = self.n_pad * self.k_pad
+        part5 = self.partial.data_ptr() + self.splits6 * slice_stride * 4
+        for c in range(nchunks):
+            t0 = c * Tc
+            ln = min(Tc, T - t0)
+            xp = x.data_ptr() + t0 * k
+            call("spb_compact_events", v(xp), strideb, B, ln, Tc, k, v(self.ev.data_ptr()),
+                 v(self.nnz.data_ptr()), k, st)
+            call("spb_forward_chunk", 1, v(self.wt.data_ptr()), int(self.w_f64),
+                 v(self.ev.data_ptr()), v(self.nnz.data_ptr()), B, n, k, k, Tc, ln, t0, T,
+                 float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
+                 int(self.alif), v(self.u.data_ptr()), v(self.a.data_ptr()), None, None, None,
+                 v(self.wsig.data_ptr()), v(ctab.data_ptr()), v(self.psi2.data_ptr()),
+                 v(self.coef.data_ptr()) if self.alif else None,
+                 v(self.lp_hi.data_ptr()), v(self.lp_lo.data_ptr()), st)
+            call("spb_xbar_chunk", v(xp), strideb, B, k, self.k_pad, Tc, ln, float(alpha),
+                 v(self.xbar_state.data_ptr()), v(self.xf.data_ptr()), v(self.xh.data_ptr()),
+                 v(self.xl.data_ptr()), st)
+            call("spb_grad_gemm_partials", v(self.lp_hi.data_ptr()), v(self.lp_lo.data_ptr()),
+                 v(self.xh.data_ptr()), v(self.xl.data_ptr()), n, self.k_pad, K, self.splits5,
+                 v(part5), self.k_pad, slice_stride, st)
+            self.launches += 4
+            if self.alif:
+                call("spb_alif_elig_chunk", v(self.coef.data_ptr()), v(self.xf.data_ptr()),
+                     v(self.eps.data_ptr()), v(self.partial.data_ptr()), B, n, self.n_pad,
+                     self.k_pad, Tc, ln, self.splits6, int(c > 0), int(c < nchunks - 1), st)
+                self.launches += 1
+            call("spb_reduce_partials", v(self.partial.data_ptr()),
+                 self.splits6 + self.splits5, n, self.n_pad, self.k_pad,
+                 v(self.grad_w_acc.data_ptr()), st)
+            self.launches += 1
+        return self
+
+    def check_labels(self, labels_np):
+        labels_np = np.asarray(labels_np)
+        if labels_np.shape != (self.B,):
+            raise ShapeMismatch(f"labels must have shape ({self.B},)")
+        if labels_np.size and (labels_np.min() < 0 or labels_np.max() >= self.m):
+            bad = labels_np[(labels_np < 0) | (labels_np >= self.m)][0]
+            raise LabelOutOfRange(f"label {int(bad)} out of range for {self.m} classes")
+
+    def grad_w(self, dtype=torch.float32):
+        """Finalised input-weight gradient [n, k] in ``dtype`` (device tensor)."""
+        out = torch.empty((self.n, self.k), dtype=dtype, device=self.device)
+        st = ctypes_void(torch.cuda.current_stream(self.device).cuda_stream)
+        _lib.call("spb_finalize_grad", ctypes_void(self.grad_w_acc.data_ptr()), self.n, self.k,
+                  self.k_pad, ctypes_void(out.data_ptr()), int(dtype == torch.float64), st)
+        return out
