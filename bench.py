@@ -1,0 +1,357 @@
+"""Benchmark of the B200 e-prop training step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+Metric: e-prop train samples*timesteps/s on the SHD-shaped ALIF config (BASELINE.json
+configs[2]: 700 -> 1024 ALIF -> 20, T=250, batch 256 per GPU), synthetic Poisson spikes
+bit-identical to the reference generator, seeded reference initialisation.  One step
+= one full e-prop update (pass A, readout/loss, pass B with all eligibility kernels,
+gradient ready on device; for N>1 plus the single NCCL allreduce).  Weak scaling:
+each rank processes its own batch of 256 samples.
+
+Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events on the
+launching stream, with a 512 MiB L2 flush (> 126 MB L2) between timed steps outside
+the events; barrier + synchronize on both sides; max over ranks.  ``e2e`` repeats the
+step through the public engine API with pinned HOST inputs: H2D of the spike tensor
+and labels and D2H of the per-sample losses are inside the timed region.
+
+``--impl reference`` times the reference algorithm on the host CPU cores (the oracle
+port, oracle/cpu_bench.py) on a bounded sample of the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: kind, n, k, m, T, B (per GPU)
+    "c2": ("lif", 256, 700, 20, 250, 128),
+    "c3": ("alif", 1024, 700, 20, 250, 256),
+    "c4": ("alif", 2048, 700, 35, 500, 128),
+}
+CONFIG_DESC = {
+    "c2": "SHD-shaped LIF e-prop 700->256->20, T=250",
+    "c3": "SHD-shaped ALIF e-prop 700->1024->20, T=250",
+    "c4": "SSC-shaped ALIF e-prop 700->2048->35, T=500 (per-GPU shard of the 1024 batch at 8 GPUs)",
+}
+METRIC = "e-prop train samples·timesteps/s (SHD-shape ALIF); HBM GB/s vs roofline"
+UNIT = "samples*timesteps/s"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+FP32_PEAK_TFLOPS = 72.5  # FFMA/FFMA2 microbenchmark on this pool's B200 (tools/fp_microbench.cu)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def cpu_reference_line(args, cfg_name):
+    """--impl reference: the reference algorithm (oracle port) on the host cores."""
+    from oracle.cpu_bench import _pool, cores, time_cpu
+    kind, n, k, m, T, B = CONFIGS[cfg_name]
+    procs = cores()
+    T_sub = 25 if kind == "alif" else 100
+    pool = _pool(procs)
+    vals = []
+    try:
+        for i in range(args.warmup + args.steps):
+            v, wall, _ = time_cpu(kind, n, k, m, T_sub, procs, procs, pool=pool)
+            if i >= args.warmup:
+                vals.append(v)
+    finally:
+        pool.close()
+        pool.join()
+    value = float(np.mean(vals))
+    sample = (f"{procs} processes x 1 sample x {T_sub} steps per timed step "
+              f"(of the {B}x{T} workload), oracle port of gradients.py:132-185, "
+              "BLAS threads=1")
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": CONFIG_DESC[cfg_name], "batch_per_gpu": B, "seq_len": T,
+                   "n_hidden": n, "n_inputs": k, "n_classes": m},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--chunk", type=int, default=32)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="minimal run for ncu: no clocks, e2e or cpu baseline")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_env()
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(cpu_reference_line(args, args.config)), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200.parallel import GradPacker
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    kind, n, k, m, T, B = CONFIGS[args.config]
+    spec = P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=m, precision="f32", seed=0)
+    net = P.init_network(spec)
+    x_np, y_np = poisson_batch(B, k, T, m, seed=1000 + rank)
+    eng = EpropEngine(n, k, m, B, alif=kind == "alif", w_f64=False, chunk=args.chunk, device=dev)
+    eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+    xd = torch.from_numpy(x_np).to(dev)
+    yd = torch.from_numpy(y_np).to(dev)
+    packer = GradPacker(n, k, m, dev)
+    kw = dict(alpha=net.neuron.alpha, theta=net.neuron.theta, slope=net.neuron.slope,
+              kappa=net.readout.kappa)
+    if kind == "alif":
+        kw.update(beta=net.neuron.beta, rho=net.neuron.rho)
+
+    def step(x, y, timers=None):
+        eng.run(x, y, timers=timers, **kw)
+        packer.pack(eng.grad_w_acc, eng.grad_wout, eng.loss, eng.correct)
+        packer.allreduce()
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(xd, yd)
+    barrier()
+
+    clocks = ClockSampler(local) if not args.profile else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    timers = {}
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record()
+        step(xd, yd, timers=timers)
+        ev[i][1].record()
+    barrier()
+    launches_per_step = eng.launches  # kernels of libsparseprop_b200.so per step
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
+    clk = clocks.stop() if clocks else None
+
+    # kernel breakdown (CUDA events on the launching stream)
+    kern = {}
+    for name, lst in timers.items():
+        kern[name] = [(a.elapsed_time(b), meta) for a, b, meta in lst]
+
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * B * T / (ms_max * 1e-3)
+
+    # ---- e2e through the engine API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        xh = torch.from_numpy(x_np).pin_memory()
+        yh = torch.from_numpy(y_np).pin_memory()
+        loss_h = torch.empty(B, dtype=torch.float64).pin_memory()
+        xdev = torch.empty_like(xd)
+        ydev = torch.empty_like(yd)
+
+        def e2e_step():
+            xdev.copy_(xh, non_blocking=True)
+            ydev.copy_(yh, non_blocking=True)
+            step(xdev, ydev)
+            loss_h.copy_(eng.loss, non_blocking=True)
+
+        for _ in range(3):
+            e2e_step()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        n_e2e = max(5, args.steps // 2)
+        e0.record()
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record()
+        barrier()
+        e2e_ms = torch.tensor([e0.elapsed_time(e1) / n_e2e], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * B * T / (float(e2e_ms.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(x_np.nbytes + y_np.nbytes),
+               "d2h_bytes_per_step": int(B * 8),
+               "ms_per_step": float(e2e_ms.item())}
+
+    # ---- roofline of the dominant kernel ----
+    hbm_peak, bf16_peak, peak_kind = peaks()
+    roof = None
+    breakdown = {nm: float(sum(t for t, _ in v) / args.steps) for nm, v in kern.items()}
+    if "elig" in kern:
+        tot_t = sum(t for t, _ in kern["elig"]) * 1e-3
+        tot_b = 0.0
+        tot_f = 0.0
+        for _, (ln, ld, stv) in kern["elig"]:
+            tot_b += 4.0 * B * n * k * (int(ld) + int(stv))      # eps~ read / write
+            tot_b += 8.0 * B * ln * n + 4.0 * B * (ln + 1) * k    # staged (A',Q') and xbar
+            tot_f += 4.0 * B * ln * n * k                          # 2 FMA / synapse-step
+        ach = tot_b / tot_t / 1e9
+        fach = tot_f / tot_t / 1e12
+        roof = {"kernel": "alif_elig_kernel (K6)", "bound": "hbm", "achieved": ach,
+                "peak": hbm_peak, "peak_source": peak_kind, "unit": "GB/s",
+                "frac": ach / hbm_peak, "traffic": None,
+                "fp32": {"achieved": fach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": fach / FP32_PEAK_TFLOPS,
+                         "peak_source": "FFMA microbenchmark tools/fp_microbench.cu"},
+                "binding": "fp32" if fach / FP32_PEAK_TFLOPS > ach / hbm_peak else "hbm",
+                "kernel_ms_per_step": tot_t * 1e3 / args.steps,
+                "share_of_step": tot_t * 1e3 / args.steps / ms}
+    elif "gemm" in kern:
+        tot_t = sum(t for t, _ in kern["gemm"]) * 1e-3
+        tot_f = sum(6.0 * n * k * B * eng.Tc for _ in kern["gemm"])  # 3 bf16 MMAs
+        ach = tot_f / tot_t / 1e12
+        roof = {"kernel": "grad_gemm_tc_kernel (K5)", "bound": "tensor", "achieved": ach,
+                "peak": bf16_peak, "peak_source": peak_kind, "unit": "TFLOP/s",
+                "frac": ach / bf16_peak, "traffic": None,
+                "kernel_ms_per_step": tot_t * 1e3 / args.steps,
+                "share_of_step": tot_t * 1e3 / args.steps / ms}
+
+    # ---- CPU baseline (rank 0, N=1 only) ----
+    cpu = None
+    if world == 1 and not args.no_cpu and not args.profile:
+        from oracle.cpu_bench import cores, time_cpu
+        procs = cores()
+        T_sub = 100 if kind == "alif" else 250
+        v, wall, procs = time_cpu(kind, n, k, m, T_sub, 2 * procs, procs)
+        cpu = {"value": v, "unit": UNIT, "cores": procs, "kind": "port",
+               "sample": f"{2 * procs} single-sample tasks x {T_sub} steps of the {B}x{T} "
+                         f"workload on {procs} processes ({wall:.1f} s wall); oracle port "
+                         "of gradients.py:132-185, BLAS threads=1"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": CONFIG_DESC[args.config], "batch_per_gpu": B,
+                       "global_batch": B * world, "seq_len": T, "n_hidden": n, "n_inputs": k,
+                       "n_classes": m, "chunk": eng.Tc, "parallelism": f"dp{world}",
+                       "forward_precision": "fp64 state/current (bit-exact spikes)",
+                       "l2": "512 MiB flush between timed steps (outside events)"},
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": roof,
+            "kernel_ms_per_step": breakdown,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -51,14 +51,15 @@ int spb_compact_events(const uint8_t* x, long long stride_b, int B, int rows, in
  *     pass 0 (A): zbar, zsum [B][n] fp64 carried; raster [B][T][ceil(n/32)] bit-packed
  *                 spikes (optional, may be NULL).
  *     pass 1 (B): wsig [B][n] = W_out^T g; ctab[T] readout gains c_t; psi2 [B][n] carry;
- *                 coef [B][Tc][n] float2 (A'_t, Q'_t) for K6 (ALIF only);
+ *                 coef [B][Tc][coef_ld] float2 (A'_t, Q'_t) for K6 (ALIF only; rows
+ *                 i >= n are never written -- keep them zero);
  *                 lp_hi/lp_lo [n][B*Tc] bf16 split of L_t psi_t, K index b*Tc+s. */
 int spb_forward_chunk(int pass, const void* wt, int w_is_f64, const uint32_t* ev, const int* nnz,
                       int B, int n, int k, int cap, int Tc, int len, int t0, int T, double alpha,
                       double theta, double slope, double beta, double rho, double kappa,
                       int reset, int alif, double* u, double* a, double* zbar, double* zsum,
                       uint32_t* raster, const float* wsig, const double* ctab, float* psi2,
-                      float* coef, void* lp_hi, void* lp_lo, cudaStream_t stream);
+                      float* coef, int coef_ld, void* lp_hi, void* lp_lo, cudaStream_t stream);
 
 /* K4  Presynaptic filter xbar_t = alpha*xbar_{t-1} + x_t (the factorised LIF trace G_u,
  *     gradients.py:89-94 with H_I = alpha, F rows = x_t; test_gradients.py:81-91).
@@ -96,7 +97,8 @@ int spb_grad_gemm_simt(const void* ah, const void* al, const void* bh, const voi
                        int N, int K, double* grad, int ldg, cudaStream_t stream);
 
 /* K6  ALIF adaptation-trace chunk: eps~ state [B][n_pad][k_pad] fp32 (rescaled trace,
- *     see elig.cu), coef from K1, xf from K4; the batch is split in `splits` contiguous
+ *     see elig.cu), coef [B][Tc][n_pad] float2 from K1 (coef_ld = n_pad), xf from K4;
+ *     Tc in {8,16,32,64}; TMA-pipelined over samples; the batch is split in `splits` contiguous
  *     ranges, each writing partial[split][n_pad][k_pad].  load_eps=0 on the first
  *     chunk (eps=0), store_eps=0 on the last.  Replaces the ALIF G_a block of
  *     eprop_trace_update (gradients.py:89-94) and x_step (gradients.py:165-167). */

@@ -23,7 +23,7 @@ D = ctypes.c_double
 SIGNATURES = {
     "spb_compact_events": [P, LL, I, I, I, I, P, P, I, P],
     "spb_forward_chunk": [I, P, I, P, P, I, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I,
-                          P, P, P, P, P, P, P, P, P, P, P, P],
+                          P, P, P, P, P, P, P, P, P, I, P, P, P],
     "spb_xbar_chunk": [P, LL, I, I, I, I, I, D, P, P, P, P, P],
     "spb_readout_loss": [P, P, P, I, I, I, P, P, P, P, P, P],
     "spb_readout_grad": [P, P, I, I, I, P, P],

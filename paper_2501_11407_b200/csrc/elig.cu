@@ -15,32 +15,71 @@
 // i.e. exactly two FMAs per synapse-sample-step (one FFMA2 per synapse pair per step),
 // instead of FMUL+FFMA+FFMA for the literal form.  All terms of eps~ are non-negative for
 // non-negative inputs (A' > 0 when rho > beta), so the rescaling adds no cancellation.
-#include "common.cuh"
+#include "tma.cuh"
 
 namespace spb {
 
 constexpr int K6_TI = 128;   // neurons per CTA tile
 constexpr int K6_TJ = 64;    // inputs per CTA tile
-constexpr int K6_SC = 16;    // time steps staged per shared-memory fill
 constexpr int K6_THREADS = 256;
+constexpr int K6_MAX_TC = 64;
 
-__global__ void __launch_bounds__(K6_THREADS, 2) alif_elig_kernel(
-    const float2* __restrict__ coef,  // [B][Tc][n]  (A', Q')
-    const float* __restrict__ xf,     // [B][Tc+1][k_pad]  row s = xbar_{t0-1+s}
-    float* __restrict__ eps,          // [B][n_pad][k_pad] eps~ state
-    float* __restrict__ partial,      // [S][n_pad][k_pad]
-    int B, int n, int n_pad, int k_pad, int Tc, int len, int b_per_split, int load_eps,
-    int store_eps) {
-  __shared__ __align__(16) float2 coefS[K6_SC][K6_TI];
-  __shared__ __align__(16) float xS[K6_SC][K6_TJ];
+// Shared-memory stage for one sample: eps~ tile, (A',Q') rows and xbar rows of the chunk.
+template <int TC>
+struct K6Stage {
+  static constexpr int EPS_BYTES = K6_TI * K6_TJ * 4;              // 32 KB
+  static constexpr int COEF_BYTES = TC * K6_TI * 8;                // TC KB
+  static constexpr int XB_BYTES = ((TC + 1) * K6_TJ * 4 + 127) / 128 * 128;
+  static constexpr int BYTES = EPS_BYTES + COEF_BYTES + XB_BYTES;
+};
+
+// TMA-pipelined sweep.  Each CTA owns a 128x64 synapse tile and a contiguous range of
+// samples; per sample, one elected thread TMA-loads the sample's eps~ tile, its chunk of
+// (A',Q') and xbar rows into a shared-memory stage (STAGES-deep ring), the 256 threads
+// sweep the chunk from registers (4 neurons x 8 inputs each, FFMA2), and write eps~ back
+// with plain stores.  The gradient tile stays in registers across the sample loop.
+template <int TC, int STAGES>
+__global__ void __launch_bounds__(K6_THREADS, 1) alif_elig_tma_kernel(
+    const __grid_constant__ CUtensorMap tm_eps, const __grid_constant__ CUtensorMap tm_coef,
+    const __grid_constant__ CUtensorMap tm_xb, float* __restrict__ eps,
+    float* __restrict__ partial, int B, int n_pad, int k_pad, int len, int b_per_split,
+    int load_eps, int store_eps) {
+  using S = K6Stage<TC>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                             ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::BYTES);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int li = lane >> 3, lj = lane & 7;
   const int j0 = blockIdx.x * K6_TJ, i0 = blockIdx.y * K6_TI;
-  const int split = blockIdx.z;
-  const int b_begin = split * b_per_split;
-  const int b_end = min(B, b_begin + b_per_split);
-  const int row0 = warp * 16 + li * 4;  // first of this thread's 4 neurons (tile-local)
+  const int b_begin = blockIdx.z * b_per_split;
+  const int nb = max(0, min(B, b_begin + b_per_split) - b_begin);
+  const int row0 = warp * 16 + li * 4;
   const int cA = lj * 4, cB = 32 + lj * 4;
+  const uint32_t stage_bytes =
+      (load_eps ? S::EPS_BYTES : 0) + S::COEF_BYTES + (TC + 1) * K6_TJ * 4;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&full[s]), 1);
+    mbar_fence_init();
+    tma_prefetch_desc(&tm_eps);
+    tma_prefetch_desc(&tm_coef);
+    tma_prefetch_desc(&tm_xb);
+  }
+  __syncthreads();
+
+  auto issue = [&](int it) {
+    const int s = it % STAGES;
+    const int b = b_begin + it;
+    uint8_t* st = smem + s * S::BYTES;
+    const uint32_t fb = smem_u32(&full[s]);
+    mbar_expect_tx(fb, stage_bytes);
+    if (load_eps) tma_load_2d(smem_u32(st), &tm_eps, fb, j0, b * n_pad + i0);
+    tma_load_2d(smem_u32(st + S::EPS_BYTES), &tm_coef, fb, 2 * i0, b * TC);
+    tma_load_2d(smem_u32(st + S::EPS_BYTES + S::COEF_BYTES), &tm_xb, fb, j0, b * (TC + 1));
+  };
+  if (tid == 0)
+    for (int it = 0; it < min(nb, STAGES - 1); ++it) issue(it);
 
   float2 g2[4][4];
 #pragma unroll
@@ -48,14 +87,20 @@ __global__ void __launch_bounds__(K6_THREADS, 2) alif_elig_kernel(
 #pragma unroll
     for (int p = 0; p < 4; ++p) g2[r][p] = make_float2(0.f, 0.f);
 
-  for (int b = b_begin; b < b_end; ++b) {
+  for (int it = 0; it < nb; ++it) {
+    const int s = it % STAGES;
+    if (tid == 0 && it + STAGES - 1 < nb) issue(it + STAGES - 1);
+    mbar_wait(smem_u32(&full[s]), (it / STAGES) & 1);
+    const uint8_t* st = smem + s * S::BYTES;
+    const float* es = reinterpret_cast<const float*>(st);
+    const float2* cs = reinterpret_cast<const float2*>(st + S::EPS_BYTES);
+    const float* xs = reinterpret_cast<const float*>(st + S::EPS_BYTES + S::COEF_BYTES);
     float2 e2[4][4];
-    float* ebase = eps + ((long long)b * n_pad + i0 + row0) * k_pad + j0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       if (load_eps) {
-        const float4 va = *reinterpret_cast<const float4*>(ebase + (long long)r * k_pad + cA);
-        const float4 vb = *reinterpret_cast<const float4*>(ebase + (long long)r * k_pad + cB);
+        const float4 va = *reinterpret_cast<const float4*>(es + (row0 + r) * K6_TJ + cA);
+        const float4 vb = *reinterpret_cast<const float4*>(es + (row0 + r) * K6_TJ + cB);
         e2[r][0] = make_float2(va.x, va.y);
         e2[r][1] = make_float2(va.z, va.w);
         e2[r][2] = make_float2(vb.x, vb.y);
@@ -65,45 +110,29 @@ __global__ void __launch_bounds__(K6_THREADS, 2) alif_elig_kernel(
         for (int p = 0; p < 4; ++p) e2[r][p] = make_float2(0.f, 0.f);
       }
     }
-    for (int s0 = 0; s0 < len; s0 += K6_SC) {
-      const int steps = min(K6_SC, len - s0);
-      // stage (A',Q') for TI neurons and xbar_{t-1} for TJ inputs, `steps` rows each
-      for (int idx = tid; idx < K6_SC * K6_TI; idx += K6_THREADS) {
-        const int ss = idx / K6_TI, c = idx % K6_TI;
-        float2 v = make_float2(0.f, 0.f);
-        if (ss < steps && i0 + c < n) v = coef[((long long)b * Tc + s0 + ss) * n + i0 + c];
-        coefS[ss][c] = v;
-      }
-      for (int idx = tid; idx < K6_SC * K6_TJ; idx += K6_THREADS) {
-        const int ss = idx / K6_TJ, c = idx % K6_TJ;
-        float v = 0.f;
-        if (ss < steps) v = xf[((long long)b * (Tc + 1) + s0 + ss) * k_pad + j0 + c];
-        xS[ss][c] = v;
-      }
-      __syncthreads();
-      for (int ss = 0; ss < steps; ++ss) {
-        const float4 xa = *reinterpret_cast<const float4*>(&xS[ss][cA]);
-        const float4 xb = *reinterpret_cast<const float4*>(&xS[ss][cB]);
-        const float2 x2[4] = {make_float2(xa.x, xa.y), make_float2(xa.z, xa.w),
-                              make_float2(xb.x, xb.y), make_float2(xb.z, xb.w)};
-        const float4 c01 = *reinterpret_cast<const float4*>(&coefS[ss][row0]);
-        const float4 c23 = *reinterpret_cast<const float4*>(&coefS[ss][row0 + 2]);
-        const float Ar[4] = {c01.x, c01.z, c23.x, c23.z};
-        const float Qr[4] = {c01.y, c01.w, c23.y, c23.w};
+#pragma unroll 2
+    for (int ss = 0; ss < len; ++ss) {
+      const float4 xa = *reinterpret_cast<const float4*>(xs + ss * K6_TJ + cA);
+      const float4 xb = *reinterpret_cast<const float4*>(xs + ss * K6_TJ + cB);
+      const float2 x2[4] = {make_float2(xa.x, xa.y), make_float2(xa.z, xa.w),
+                            make_float2(xb.x, xb.y), make_float2(xb.z, xb.w)};
+      const float4 c01 = *reinterpret_cast<const float4*>(cs + ss * K6_TI + row0);
+      const float4 c23 = *reinterpret_cast<const float4*>(cs + ss * K6_TI + row0 + 2);
+      const float Ar[4] = {c01.x, c01.z, c23.x, c23.z};
+      const float Qr[4] = {c01.y, c01.w, c23.y, c23.w};
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const float2 A2 = make_float2(Ar[r], Ar[r]);
-          const float2 Q2 = make_float2(Qr[r], Qr[r]);
+      for (int r = 0; r < 4; ++r) {
+        const float2 A2 = make_float2(Ar[r], Ar[r]);
+        const float2 Q2 = make_float2(Qr[r], Qr[r]);
 #pragma unroll
-          for (int p = 0; p < 4; ++p) {
-            e2[r][p] = ffma2(A2, e2[r][p], x2[p]);
-            g2[r][p] = ffma2(Q2, e2[r][p], g2[r][p]);
-          }
+        for (int p = 0; p < 4; ++p) {
+          e2[r][p] = ffma2(A2, e2[r][p], x2[p]);
+          g2[r][p] = ffma2(Q2, e2[r][p], g2[r][p]);
         }
       }
-      __syncthreads();
     }
     if (store_eps) {
+      float* ebase = eps + ((long long)(b_begin + it) * n_pad + i0 + row0) * k_pad + j0;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         *reinterpret_cast<float4*>(ebase + (long long)r * k_pad + cA) =
@@ -112,8 +141,9 @@ __global__ void __launch_bounds__(K6_THREADS, 2) alif_elig_kernel(
             make_float4(e2[r][2].x, e2[r][2].y, e2[r][3].x, e2[r][3].y);
       }
     }
+    __syncthreads();  // stage s may be refilled by the next issue
   }
-  float* pbase = partial + ((long long)split * n_pad + i0 + row0) * k_pad + j0;
+  float* pbase = partial + ((long long)blockIdx.z * n_pad + i0 + row0) * k_pad + j0;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     *reinterpret_cast<float4*>(pbase + (long long)r * k_pad + cA) =
@@ -198,13 +228,40 @@ int spb_alif_elig_chunk(const float* coef, const float* xf, float* eps, float* p
   SPB_CHECK_ARG(n_pad % K6_TI == 0 && k_pad % K6_TJ == 0 && n <= n_pad,
                 "spb_alif_elig_chunk: n_pad must be a multiple of %d and k_pad of %d", K6_TI,
                 K6_TJ);
+  SPB_CHECK_ARG(Tc == 8 || Tc == 16 || Tc == 32 || Tc == 64,
+                "spb_alif_elig_chunk: chunk length must be 8, 16, 32 or 64 (got %d)", Tc);
   SPB_CHECK_ARG(B > 0 && splits > 0 && splits <= B && len >= 0 && len <= Tc,
                 "spb_alif_elig_chunk: bad sizes B=%d splits=%d len=%d Tc=%d", B, splits, len, Tc);
+  CUtensorMap m_eps, m_coef, m_xb;
+  const bool ok =
+      make_tmap_2d(&m_eps, eps, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, k_pad, (uint64_t)B * n_pad,
+                   (uint64_t)k_pad * 4, K6_TJ, K6_TI, CU_TENSOR_MAP_SWIZZLE_NONE) &&
+      make_tmap_2d(&m_coef, coef, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2 * (uint64_t)n_pad,
+                   (uint64_t)B * Tc, (uint64_t)n_pad * 8, 2 * K6_TI, Tc,
+                   CU_TENSOR_MAP_SWIZZLE_NONE) &&
+      make_tmap_2d(&m_xb, xf, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, k_pad, (uint64_t)B * (Tc + 1),
+                   (uint64_t)k_pad * 4, K6_TJ, Tc + 1, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (!ok) {
+    set_error("spb_alif_elig_chunk: cuTensorMapEncodeTiled failed");
+    return 3;
+  }
   const int bps = ceil_div(B, splits);
   dim3 grid(k_pad / K6_TJ, n_pad / K6_TI, splits);
-  alif_elig_kernel<<<grid, K6_THREADS, 0, stream>>>(reinterpret_cast<const float2*>(coef), xf,
-                                                    eps, partial, B, n, n_pad, k_pad, Tc, len,
-                                                    bps, load_eps, store_eps);
+#define SPB_K6_LAUNCH(TC, ST)                                                                   \
+  do {                                                                                          \
+    auto kfn = alif_elig_tma_kernel<TC, ST>;                                                    \
+    const int smem = ST * K6Stage<TC>::BYTES + 128 + 64;                                       \
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);               \
+    kfn<<<grid, K6_THREADS, smem, stream>>>(m_eps, m_coef, m_xb, eps, partial, B, n_pad, k_pad, \
+                                            len, bps, load_eps, store_eps);                     \
+  } while (0)
+  switch (Tc) {
+    case 8: SPB_K6_LAUNCH(8, 4); break;
+    case 16: SPB_K6_LAUNCH(16, 3); break;
+    case 32: SPB_K6_LAUNCH(32, 3); break;
+    default: SPB_K6_LAUNCH(64, 2); break;
+  }
+#undef SPB_K6_LAUNCH
   SPB_CHECK_LAUNCH("alif_elig");
   return 0;
 }

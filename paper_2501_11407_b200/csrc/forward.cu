@@ -50,13 +50,13 @@ __global__ void compact_events_kernel(const uint8_t* __restrict__ x, long long s
 // explicit round-to-nearest intrinsics (no FMA contraction).
 // ------------------------------------------------------------------------------------
 struct FwdParams {
-  int B, n, k, cap, Tc, len, t0, T;
+  int B, n, k, cap, Tc, len, t0, T, coef_ld;
   double alpha, theta, slope, beta, rho, kappa;
   int reset, alif, pass;  // pass 0 = A, 1 = B
 };
 
 template <typename WT, bool SMEM_W>
-__global__ void __launch_bounds__(512) forward_chunk_kernel(
+__global__ void __launch_bounds__(1024) forward_chunk_kernel(
     FwdParams P, const WT* __restrict__ wt, const uint32_t* __restrict__ ev,
     const int* __restrict__ nnz, double* __restrict__ u_st, double* __restrict__ a_st,
     double* __restrict__ zbar_st, double* __restrict__ zsum_st, uint32_t* __restrict__ raster,
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(512) forward_chunk_kernel(
     float2* __restrict__ coef, __nv_bfloat16* __restrict__ lp_hi,
     __nv_bfloat16* __restrict__ lp_lo) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WT* ws = reinterpret_cast<WT*>(smem_raw);
+  double* ws = reinterpret_cast<double*>(smem_raw);  // fp64 tile: no conversion in the gather
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i0 = blockIdx.x * 32;
   const int i = i0 + lane;
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(512) forward_chunk_kernel(
   if (SMEM_W) {
     for (int idx = threadIdx.x; idx < P.k * 32; idx += blockDim.x) {
       const int j = idx >> 5, c = idx & 31;
-      ws[idx] = (i0 + c < P.n) ? wt[(long long)j * P.n + i0 + c] : WT(0);
+      ws[idx] = (i0 + c < P.n) ? (double)wt[(long long)j * P.n + i0 + c] : 0.0;
     }
     __syncthreads();
   }
@@ -115,22 +115,25 @@ __global__ void __launch_bounds__(512) forward_chunk_kernel(
           const int j0 = e0 >> 8, j1 = e1 >> 8;
           double w0, w1;
           if (SMEM_W) {
-            w0 = (double)ws[j0 * 32 + lane];
-            w1 = (double)ws[j1 * 32 + lane];
+            w0 = ws[j0 * 32 + lane];
+            w1 = ws[j1 * 32 + lane];
           } else {
             w0 = valid_i ? (double)wt[(long long)j0 * P.n + i] : 0.0;
             w1 = valid_i ? (double)wt[(long long)j1 * P.n + i] : 0.0;
           }
-          I0 = fma((double)(e0 & 0xffu), w0, I0);
-          I1 = fma((double)(e1 & 0xffu), w1, I1);
+          // counts are warp-uniform (broadcast event); binary spikes take the add path
+          const uint32_t c0 = e0 & 0xffu, c1 = e1 & 0xffu;
+          I0 = (c0 == 1u) ? __dadd_rn(I0, w0) : fma((double)c0, w0, I0);
+          I1 = (c1 == 1u) ? __dadd_rn(I1, w1) : fma((double)c1, w1, I1);
         }
         if (q < mcnt) {
           const uint32_t e0 = __shfl_sync(0xffffffffu, e, q);
           const int j0 = e0 >> 8;
           double w0;
-          if (SMEM_W) w0 = (double)ws[j0 * 32 + lane];
+          if (SMEM_W) w0 = ws[j0 * 32 + lane];
           else w0 = valid_i ? (double)wt[(long long)j0 * P.n + i] : 0.0;
-          I0 = fma((double)(e0 & 0xffu), w0, I0);
+          const uint32_t c0 = e0 & 0xffu;
+          I0 = (c0 == 1u) ? __dadd_rn(I0, w0) : fma((double)c0, w0, I0);
         }
       }
       const double I = __dadd_rn(I0, I1);
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(512) forward_chunk_kernel(
           const float A = (float)(P.rho - P.beta * (double)psi1);
           const float Ap = (t == 0) ? 0.0f : A * (psi2 / fmaxf(psi1, 1e-30f));
           const float Qp = -(float)P.beta * lpsi * psi1;
-          if (valid_i) coef[(long long)row * P.n + i] = make_float2(Ap, Qp);
+          if (valid_i) coef[(long long)row * P.coef_ld + i] = make_float2(Ap, Qp);
         }
         psi2 = psi1;
         split_bf16(lpsi, hv[u8], lv[u8]);
@@ -242,9 +245,9 @@ static int launch_forward(const FwdParams& P, const WT* wt, const uint32_t* ev, 
                           double* u, double* a, double* zbar, double* zsum, uint32_t* raster,
                           const float* wsig, const double* ctab, float* psi2, float2* coef,
                           __nv_bfloat16* lph, __nv_bfloat16* lpl, cudaStream_t stream) {
-  const int wpb = 16;
+  const int wpb = 32;
   dim3 grid(ceil_div(P.n, 32), ceil_div(P.B, wpb));
-  const size_t smem = (size_t)P.k * 32 * sizeof(WT);
+  const size_t smem = (size_t)P.k * 32 * sizeof(double);
   if ((long long)smem <= (long long)fwd_smem_limit()) {
     auto kfn = forward_chunk_kernel<WT, true>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -284,15 +287,16 @@ int spb_forward_chunk(int pass, const void* wt, int w_is_f64, const uint32_t* ev
                       double theta, double slope, double beta, double rho, double kappa,
                       int reset, int alif, double* u, double* a, double* zbar, double* zsum,
                       uint32_t* raster, const float* wsig, const double* ctab, float* psi2,
-                      float* coef, void* lp_hi, void* lp_lo, cudaStream_t stream) {
+                      float* coef, int coef_ld, void* lp_hi, void* lp_lo, cudaStream_t stream) {
   SPB_CHECK_ARG(pass == 0 || pass == 1, "spb_forward_chunk: pass must be 0 (A) or 1 (B)");
   SPB_CHECK_ARG(wt && ev && nnz && u && a, "spb_forward_chunk: null pointer");
   SPB_CHECK_ARG(B > 0 && n > 0 && k > 0 && Tc > 0 && Tc % 8 == 0 && len >= 0 && len <= Tc,
                 "spb_forward_chunk: bad sizes B=%d n=%d k=%d Tc=%d len=%d", B, n, k, Tc, len);
   SPB_CHECK_ARG(pass == 0 ? (zbar && zsum) : (wsig && ctab && psi2 && lp_hi && lp_lo),
                 "spb_forward_chunk: missing pass-%c buffers", pass ? 'B' : 'A');
-  SPB_CHECK_ARG(!(pass == 1 && alif && !coef), "spb_forward_chunk: ALIF pass B needs coef");
-  FwdParams P{B, n, k, cap, Tc, len, t0, T, alpha, theta, slope, beta, rho, kappa,
+  SPB_CHECK_ARG(!(pass == 1 && alif && (!coef || coef_ld < n)),
+                "spb_forward_chunk: ALIF pass B needs coef with coef_ld >= n");
+  FwdParams P{B, n, k, cap, Tc, len, t0, T, coef_ld, alpha, theta, slope, beta, rho, kappa,
               reset, alif, pass};
   auto lph = reinterpret_cast<__nv_bfloat16*>(lp_hi);
   auto lpl = reinterpret_cast<__nv_bfloat16*>(lp_lo);

@@ -33,10 +33,6 @@ from .errors import LabelOutOfRange, ShapeMismatch
 SM_COUNT_DEFAULT = 148
 
 
-def _ptr(t):
-    return ctypes_void(t.data_ptr()) if t is not None else None
-
-
 def ctypes_void(p):
     import ctypes
     return ctypes.c_void_p(p)
@@ -58,11 +54,11 @@ def readout_gains(T: int, kappa: float) -> np.ndarray:
     return c
 
 
-def _best_split(B: int, tiles: int, slots: int, min_per_split: int = 2) -> int:
+def _best_split(B: int, tiles: int, slots: int, min_per_split: int = 16) -> int:
     """Batch split for K6: a divisor of B giving the best wave efficiency."""
     best, best_eff = 1, -1.0
     for d in range(1, B + 1):
-        if B % d or B // d < min_per_split and d != 1:
+        if B % d or (B // d < min_per_split and d != 1):
             continue
         ctas = tiles * d
         waves = math.ceil(ctas / slots)
@@ -81,6 +77,8 @@ class EpropEngine:
                  chunk: int = 32, device=None, sm_count: int | None = None):
         if chunk <= 0 or chunk % 8:
             raise ValueError("chunk must be a positive multiple of 8")
+        if alif and chunk not in (8, 16, 32, 64):
+            raise ValueError("ALIF chunk length must be 8, 16, 32 or 64")
         if k >= (1 << 24):
             raise ShapeMismatch("k too large")
         self.lib = _lib.load()
@@ -115,7 +113,8 @@ class EpropEngine:
         self.g = torch.empty((self.B, self.m), dtype=f64, device=dev)
         self.correct = torch.empty(self.B, dtype=torch.int32, device=dev)
         # pass-B chunk buffers
-        self.coef = (torch.empty((self.B, self.Tc, self.n, 2), dtype=f32, device=dev)
+        # rows i >= n stay zero forever (K1 writes only real neurons; K6 TMA reads n_pad)
+        self.coef = (torch.zeros((self.B, self.Tc, self.n_pad, 2), dtype=f32, device=dev)
                      if self.alif else None)
         self.lp_hi = torch.empty((self.n, K), dtype=torch.bfloat16, device=dev)
         self.lp_lo = torch.empty((self.n, K), dtype=torch.bfloat16, device=dev)
@@ -130,7 +129,7 @@ class EpropEngine:
         if self.alif:
             tiles6 = (self.k_pad // 64) * (self.n_pad // 128)
             self.splits6 = _best_split(self.B, tiles6, 2 * sms)
-            self.eps = torch.empty((self.B, self.n_pad, self.k_pad), dtype=f32, device=dev)
+            self.eps = torch.zeros((self.B, self.n_pad, self.k_pad), dtype=f32, device=dev)
         else:
             self.splits6 = 0
             self.eps = None
@@ -165,7 +164,7 @@ class EpropEngine:
     # ----------------------------------------------------------------------------------
     def run(self, x: torch.Tensor, labels: torch.Tensor, *, alpha=0.95, theta=1.0, slope=10.0,
             beta=0.8, rho=0.96, kappa=0.95, reset=False, raster: torch.Tensor | None = None,
-            stream=None):
+            stream=None, timers: dict | None = None):
         """One full e-prop update on device-resident inputs.
 
         x       uint8 [B, T, k] spike counts (CUDA, contiguous)
@@ -173,6 +172,8 @@ class EpropEngine:
         raster  optional int32 [B, T, ceil(n/32)] bit-packed spike output (pass A)
         Results stay on device: ``grad_w_acc`` (fp64 [n, k_pad]), ``grad_wout``,
         ``loss``, ``s`` (readout sums), ``correct``.
+        timers  optional dict; CUDA event pairs are appended per launch of the main
+                kernels under "forward", "gemm", "elig" with their chunk length.
         """
         if reset:
             raise NotImplementedError(
@@ -197,6 +198,18 @@ class EpropEngine:
         strideb = T * k
         self.launches = 0
         v = ctypes_void
+
+        def timed(name, ln, fn, *args):
+            if timers is None:
+                return call(fn, *args)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rc = call(fn, *args)
+            e1.record()
+            timers.setdefault(name, []).append((e0, e1, ln))
+            return rc
+
         # ---------------- pass A ----------------
         self.u.zero_(); self.a.zero_(); self.zbar.zero_(); self.zsum.zero_()
         for c in range(nchunks):
@@ -211,7 +224,7 @@ class EpropEngine:
                  int(self.alif), v(self.u.data_ptr()), v(self.a.data_ptr()),
                  v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
                  v(raster.data_ptr()) if raster is not None else None,
-                 None, None, None, None, None, None, st)
+                 None, None, None, None, 0, None, None, st)
             self.launches += 2
         # ---------------- readout / loss ----------------
         call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
@@ -232,22 +245,24 @@ class EpropEngine:
             xp = x.data_ptr() + t0 * k
             call("spb_compact_events", v(xp), strideb, B, ln, Tc, k, v(self.ev.data_ptr()),
                  v(self.nnz.data_ptr()), k, st)
-            call("spb_forward_chunk", 1, v(self.wt.data_ptr()), int(self.w_f64),
+            timed("forward", ln, "spb_forward_chunk", 1, v(self.wt.data_ptr()), int(self.w_f64),
                  v(self.ev.data_ptr()), v(self.nnz.data_ptr()), B, n, k, k, Tc, ln, t0, T,
                  float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
                  int(self.alif), v(self.u.data_ptr()), v(self.a.data_ptr()), None, None, None,
                  v(self.wsig.data_ptr()), v(ctab.data_ptr()), v(self.psi2.data_ptr()),
-                 v(self.coef.data_ptr()) if self.alif else None,
+                 v(self.coef.data_ptr()) if self.alif else None, self.n_pad,
                  v(self.lp_hi.data_ptr()), v(self.lp_lo.data_ptr()), st)
             call("spb_xbar_chunk", v(xp), strideb, B, k, self.k_pad, Tc, ln, float(alpha),
                  v(self.xbar_state.data_ptr()), v(self.xf.data_ptr()), v(self.xh.data_ptr()),
                  v(self.xl.data_ptr()), st)
-            call("spb_grad_gemm_partials", v(self.lp_hi.data_ptr()), v(self.lp_lo.data_ptr()),
+            timed("gemm", ln, "spb_grad_gemm_partials", v(self.lp_hi.data_ptr()),
+                  v(self.lp_lo.data_ptr()),
                  v(self.xh.data_ptr()), v(self.xl.data_ptr()), n, self.k_pad, K, self.splits5,
                  v(part5), self.k_pad, slice_stride, st)
             self.launches += 4
             if self.alif:
-                call("spb_alif_elig_chunk", v(self.coef.data_ptr()), v(self.xf.data_ptr()),
+                timed("elig", (ln, c > 0, c < nchunks - 1), "spb_alif_elig_chunk",
+                      v(self.coef.data_ptr()), v(self.xf.data_ptr()),
                      v(self.eps.data_ptr()), v(self.partial.data_ptr()), B, n, self.n_pad,
                      self.k_pad, Tc, ln, self.splits6, int(c > 0), int(c < nchunks - 1), st)
                 self.launches += 1

@@ -1,0 +1,176 @@
+"""Host-side tests (CPU only): the C-ABI library loads and exports every declared entry
+point, the ctypes signatures match include/sparseprop_b200.h, the engine's launch
+sequence is well-formed (dry run with a recording stub), API validation errors."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2501_11407_b200 as P
+from paper_2501_11407_b200 import _lib
+from paper_2501_11407_b200.engine import EpropEngine, readout_gains, _best_split
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sparseprop_b200.h")
+
+
+def _header_decls():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    decls = {}
+    for m in re.finditer(r"\b(?:int|const char\*)\s+(spb_\w+)\s*\(([^)]*)\)\s*;", txt):
+        args = [a.strip() for a in m.group(2).split(",") if a.strip() and a.strip() != "void"]
+        decls[m.group(1)] = args
+    return decls
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    decls = _header_decls()
+    assert len(decls) >= 12
+    for name in decls:
+        assert hasattr(lib, name), name
+
+
+def test_ctypes_signatures_match_header():
+    decls = _header_decls()
+    for name, args in _lib.SIGNATURES.items():
+        assert name in decls, name
+        hargs = decls[name]
+        assert len(args) == len(hargs), (name, len(args), len(hargs))
+        for ct, h in zip(args, hargs):
+            is_ptr = "*" in h or "cudaStream_t" in h
+            if is_ptr:
+                assert ct is ctypes.c_void_p, (name, h)
+            elif "double" in h:
+                assert ct is ctypes.c_double, (name, h)
+            elif "long long" in h:
+                assert ct is ctypes.c_longlong, (name, h)
+            else:
+                assert ct is ctypes.c_int, (name, h)
+
+
+def test_version_and_error_text():
+    lib = _lib.load()
+    assert lib.spb_version() == 1
+    assert isinstance(lib.spb_last_error(), bytes)
+
+
+def test_bad_arguments_are_rejected_without_gpu():
+    # argument validation happens before any CUDA call -> works on a CPU-only host
+    with pytest.raises(P.ShapeMismatch):
+        _lib.call("spb_forward_chunk", 2, None, 0, None, None, 1, 1, 1, 1, 8, 1, 0, 1,
+                  0.95, 1.0, 10.0, 0.0, 0.0, 0.95, 0, 0, None, None, None, None, None, None,
+                  None, None, None, 0, None, None, None)
+    with pytest.raises(P.ShapeMismatch):
+        _lib.call("spb_alif_elig_chunk", None, None, None, None, 1, 1, 128, 64, 32, 32, 1,
+                  0, 0, None)
+
+
+class _Recorder:
+    def __init__(self):
+        self.calls = []
+
+    def __call__(self, name, *args):
+        sig = _lib.SIGNATURES[name]
+        assert len(args) == len(sig), (name, len(args), len(sig))
+        for a, t in zip(args, sig):
+            if t is ctypes.c_void_p:
+                assert a is None or isinstance(a, (ctypes.c_void_p, int)), (name, a)
+            elif t is ctypes.c_double:
+                assert isinstance(a, float), (name, a)
+            else:
+                assert isinstance(a, (int, np.integer)) and not isinstance(a, bool) or \
+                    isinstance(a, bool), (name, a)
+        self.calls.append((name, args))
+        return 0
+
+
+@pytest.mark.parametrize("alif,T,chunk", [(True, 77, 16), (False, 50, 24), (True, 64, 64)])
+def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
+    rec = _Recorder()
+    monkeypatch.setattr(_lib, "call", rec)
+    monkeypatch.setattr(torch.cuda, "current_stream", lambda *a, **k: type("S", (), {"cuda_stream": 0})())
+    eng = EpropEngine(40, 30, 3, 6, alif=alif, chunk=chunk, device="cpu", sm_count=148)
+    x = torch.zeros((6, T, 30), dtype=torch.uint8)
+    y = torch.zeros(6, dtype=torch.int64)
+    eng.run(x, y)
+    names = [c[0] for c in rec.calls]
+    nch = (T + chunk - 1) // chunk
+    assert names.count("spb_forward_chunk") == 2 * nch
+    assert names.count("spb_compact_events") == 2 * nch
+    assert names.count("spb_xbar_chunk") == nch
+    assert names.count("spb_grad_gemm_partials") == nch
+    assert names.count("spb_alif_elig_chunk") == (nch if alif else 0)
+    assert names.count("spb_readout_loss") == 1
+    # first ALIF chunk starts from eps = 0, last chunk does not write eps back
+    el = [c[1] for c in rec.calls if c[0] == "spb_alif_elig_chunk"]
+    if el:
+        assert el[0][11] == 0 and el[-1][12] == 0
+        assert all(e[11] == 1 for e in el[1:]) and all(e[12] == 1 for e in el[:-1])
+        assert sum(e[9] for e in el) == T
+    assert eng.launches == len(rec.calls) - 0
+
+
+def test_engine_rejects_bad_inputs():
+    eng = EpropEngine(8, 5, 2, 3, alif=False, chunk=8, device="cpu", sm_count=148)
+    with pytest.raises(P.ShapeMismatch):
+        eng.run(torch.zeros((3, 10, 4), dtype=torch.uint8), torch.zeros(3, dtype=torch.int64))
+    with pytest.raises(P.ShapeMismatch):
+        eng.run(torch.zeros((3, 10, 5), dtype=torch.float32), torch.zeros(3, dtype=torch.int64))
+    with pytest.raises(NotImplementedError):
+        eng.run(torch.zeros((3, 10, 5), dtype=torch.uint8), torch.zeros(3, dtype=torch.int64),
+                reset=True)
+    with pytest.raises(ValueError):
+        EpropEngine(8, 5, 2, 3, alif=True, chunk=24, device="cpu")
+
+
+def test_readout_gains_match_bptt_recurrence():
+    c = readout_gains(6, 0.9)
+    acc, ref = 0.0, []
+    for _ in range(6):
+        acc = 1.0 + 0.9 * acc
+        ref.append(acc)
+    assert np.allclose(c, ref[::-1])
+
+
+def test_best_split_divides_batch():
+    for B in (1, 7, 64, 256, 1000):
+        d = _best_split(B, 88, 296)
+        assert B % d == 0 and (d == 1 or B // d >= 16)
+
+
+def test_param_validation_mirrors_reference():
+    with pytest.raises(ValueError):
+        P.LIFParams(np.zeros((1, 1)), alpha=1.5)
+    with pytest.raises(ValueError):
+        P.LIFParams(np.zeros((1, 1)), theta=0.0)
+    with pytest.raises(ValueError):
+        P.ALIFParams(np.zeros((1, 1)), beta=-0.1)
+    with pytest.raises(ValueError):
+        P.ALIFParams(np.zeros((1, 1)), rho=1.0)
+    with pytest.raises(ValueError):
+        P.ReadoutParams(np.zeros((1, 1)), kappa=0.0)
+
+
+def test_init_network_matches_oracle_and_reference_seed_stream():
+    from oracle.eprop_ref import init_network_arrays
+    net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=17, n_inputs=9, n_classes=4,
+                                       precision="f32", seed=3))
+    w, wo = init_network_arrays(17, 9, 4, seed=3, dtype=np.float32)
+    assert np.array_equal(net.neuron.w, w) and np.array_equal(net.readout.w_out, wo)
+    assert net.is_alif and net.n == 17 and net.k == 9 and net.m == 4
+
+
+def test_input_count_conversion():
+    from paper_2501_11407_b200.gradients import _as_counts
+    x = np.array([[0.0, 1.0, 3.0]])
+    assert _as_counts(x).dtype == np.uint8
+    with pytest.raises(ValueError):
+        _as_counts(np.array([[0.5]]))
+    with pytest.raises(ValueError):
+        _as_counts(np.array([[-1.0]]))

@@ -83,7 +83,7 @@ SMALL = ["c1_lif_f64", "c1_alif_f64", "c1_lif_f32", "c1_alif_f32", "mid_alif_f64
 
 
 @pytest.mark.parametrize("name", SMALL)
-@pytest.mark.parametrize("chunk", [8, 32, 104])
+@pytest.mark.parametrize("chunk", [8, 32, 64])
 def test_small_configs_vs_reference(name, chunk):
     _need_gpu()
     g = load_golden(name)
