@@ -36,11 +36,12 @@ int spb_version(void);
 int spb_device_sm(void); /* compute capability of the current device, e.g. 100 */
 
 /* K0  Compact one chunk of dense uint8 spike counts into per-(sample,step) event lists.
- *     x[b*stride_b + s*k + j] for s < rows; ev[(b*ld_rows+s)*cap + q] = (j<<8)|count in
- *     increasing j; nnz[b*ld_rows+s] = number of events.  cap >= k, ld_rows >= rows.
+ *     x[b*stride_b + s*k + j] for s < rows; ev[(b*ld_rows+s)*cap + q] = 32*j, each channel
+ *     repeated `count` times, increasing j; nnz[b*ld_rows+s] = number of events (<= cap).
+ *     A row with more than `cap` events sets *overflow = 1 (may be NULL).
  *     Replaces the dense `net.neuron.w @ x_t` operand preparation (gradients.py:125). */
 int spb_compact_events(const uint8_t* x, long long stride_b, int B, int rows, int ld_rows, int k,
-                       uint32_t* ev, int* nnz, int cap, cudaStream_t stream);
+                       uint32_t* ev, int* nnz, int cap, int* overflow, cudaStream_t stream);
 
 /* K1  Fused forward over one time chunk: event gather of W x_t (fp64 accumulation),
  *     ALIF/LIF state update, spike and surrogate derivative.

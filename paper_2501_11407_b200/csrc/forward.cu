@@ -15,11 +15,14 @@ namespace spb {
 
 // ------------------------------------------------------------------------------------
 // K0: one warp per (sample, step) row; increasing channel order (deterministic).
-// Event word = (channel << 8) | count.
-// ------------------------------------------------------------------------------------
+// Each input event is emitted `count` times as the word j*32 (the row offset of channel j
+// in K1's weight tile), so the gather is a pure add: sum_j count_j * W[i][j] exactly as
+// repeated fp64 additions of the same weight.  A row whose total count exceeds `cap`
+// is truncated and flagged in *overflow (the host raises).
 __global__ void compact_events_kernel(const uint8_t* __restrict__ x, long long stride_b,
                                       int k, int rows_per_b, int ld_rows, int B,
-                                      uint32_t* __restrict__ ev, int* __restrict__ nnz, int cap) {
+                                      uint32_t* __restrict__ ev, int* __restrict__ nnz, int cap,
+                                      int* __restrict__ overflow) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= B * rows_per_b) return;
@@ -30,15 +33,23 @@ __global__ void compact_events_kernel(const uint8_t* __restrict__ x, long long s
   int count = 0;
   for (int q0 = 0; q0 < k; q0 += 32) {
     const int j = q0 + lane;
-    const uint32_t c = (j < k) ? row[j] : 0u;
-    const unsigned m = __ballot_sync(0xffffffffu, c != 0u);
-    if (c != 0u) {
-      const int pos = count + __popc(m & ((1u << lane) - 1u));
-      out[pos] = ((uint32_t)j << 8) | c;
+    const int c = (j < k) ? (int)row[j] : 0;
+    // inclusive warp scan of the counts
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
-    count += __popc(m);
+    const int base = count + incl - c;
+    for (int r = 0; r < c; ++r)
+      if (base + r < cap) out[base + r] = (uint32_t)j * 32u;
+    count += __shfl_sync(0xffffffffu, incl, 31);
   }
-  if (lane == 0) nnz[orow] = count;
+  if (lane == 0) {
+    nnz[orow] = min(count, cap);
+    if (count > cap && overflow) atomicExch(overflow, 1);
+  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -105,6 +116,7 @@ __global__ void __launch_bounds__(1024) forward_chunk_kernel(
       const int nz = nnz[row];
       const uint32_t* list = ev + (long long)row * P.cap;
       double I0 = 0.0, I1 = 0.0;
+      const double* wl = ws + lane;
       for (int q0 = 0; q0 < nz; q0 += 32) {
         const uint32_t e = (q0 + lane < nz) ? list[q0 + lane] : 0u;
         const int mcnt = min(32, nz - q0);
@@ -112,28 +124,23 @@ __global__ void __launch_bounds__(1024) forward_chunk_kernel(
         for (; q + 1 < mcnt; q += 2) {
           const uint32_t e0 = __shfl_sync(0xffffffffu, e, q);
           const uint32_t e1 = __shfl_sync(0xffffffffu, e, q + 1);
-          const int j0 = e0 >> 8, j1 = e1 >> 8;
           double w0, w1;
           if (SMEM_W) {
-            w0 = ws[j0 * 32 + lane];
-            w1 = ws[j1 * 32 + lane];
+            w0 = wl[e0];
+            w1 = wl[e1];
           } else {
-            w0 = valid_i ? (double)wt[(long long)j0 * P.n + i] : 0.0;
-            w1 = valid_i ? (double)wt[(long long)j1 * P.n + i] : 0.0;
+            w0 = valid_i ? (double)wt[(long long)(e0 >> 5) * P.n + i] : 0.0;
+            w1 = valid_i ? (double)wt[(long long)(e1 >> 5) * P.n + i] : 0.0;
           }
-          // counts are warp-uniform (broadcast event); binary spikes take the add path
-          const uint32_t c0 = e0 & 0xffu, c1 = e1 & 0xffu;
-          I0 = (c0 == 1u) ? __dadd_rn(I0, w0) : fma((double)c0, w0, I0);
-          I1 = (c1 == 1u) ? __dadd_rn(I1, w1) : fma((double)c1, w1, I1);
+          I0 = __dadd_rn(I0, w0);
+          I1 = __dadd_rn(I1, w1);
         }
         if (q < mcnt) {
           const uint32_t e0 = __shfl_sync(0xffffffffu, e, q);
-          const int j0 = e0 >> 8;
           double w0;
-          if (SMEM_W) w0 = ws[j0 * 32 + lane];
-          else w0 = valid_i ? (double)wt[(long long)j0 * P.n + i] : 0.0;
-          const uint32_t c0 = e0 & 0xffu;
-          I0 = (c0 == 1u) ? __dadd_rn(I0, w0) : fma((double)c0, w0, I0);
+          if (SMEM_W) w0 = wl[e0];
+          else w0 = valid_i ? (double)wt[(long long)(e0 >> 5) * P.n + i] : 0.0;
+          I0 = __dadd_rn(I0, w0);
         }
       }
       const double I = __dadd_rn(I0, I1);
@@ -268,16 +275,16 @@ using namespace spb;
 extern "C" {
 
 int spb_compact_events(const uint8_t* x, long long stride_b, int B, int rows, int ld_rows, int k,
-                       uint32_t* ev, int* nnz, int cap, cudaStream_t stream) {
+                       uint32_t* ev, int* nnz, int cap, int* overflow, cudaStream_t stream) {
   SPB_CHECK_ARG(x && ev && nnz, "spb_compact_events: null pointer");
-  SPB_CHECK_ARG(B >= 0 && rows >= 0 && ld_rows >= rows && k > 0 && cap >= k && k < (1 << 24),
+  SPB_CHECK_ARG(B >= 0 && rows >= 0 && ld_rows >= rows && k > 0 && cap >= 1 && k < (1 << 24),
                 "spb_compact_events: bad sizes B=%d rows=%d k=%d cap=%d", B, rows, k, cap);
   const long long warps = (long long)B * rows;
   if (warps == 0) return 0;
   const int threads = 256;
   const long long blocks = (warps * 32 + threads - 1) / threads;
   compact_events_kernel<<<(unsigned)blocks, threads, 0, stream>>>(x, stride_b, k, rows, ld_rows,
-                                                                  B, ev, nnz, cap);
+                                                                  B, ev, nnz, cap, overflow);
   SPB_CHECK_LAUNCH("compact_events");
   return 0;
 }

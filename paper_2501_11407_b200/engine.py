@@ -74,7 +74,7 @@ class EpropEngine:
     """Buffers + launch sequence for one problem shape on one device."""
 
     def __init__(self, n: int, k: int, m: int, B: int, *, alif: bool, w_f64: bool = False,
-                 chunk: int = 32, device=None, sm_count: int | None = None):
+                 chunk: int = 32, device=None, sm_count: int | None = None, max_count: int = 1):
         if chunk <= 0 or chunk % 8:
             raise ValueError("chunk must be a positive multiple of 8")
         if alif and chunk not in (8, 16, 32, 64):
@@ -97,9 +97,15 @@ class EpropEngine:
         Bn, Bk = (self.B, self.n), (self.B, self.k)
         K = self.B * self.Tc
         self.K = K
-        # K0 event lists
-        self.ev = torch.empty(self.B * self.Tc * self.k, dtype=torch.int32, device=dev)
+        # K0 event lists: every input event repeated `count` times, so a row holds at
+        # most k * max_count entries (max_count = 1 for binary spike trains)
+        self.max_count = int(max_count)
+        if not 1 <= self.max_count <= 255:
+            raise ValueError("max_count must be in [1, 255]")
+        self.cap = self.k * self.max_count
+        self.ev = torch.empty(self.B * self.Tc * self.cap, dtype=torch.int32, device=dev)
         self.nnz = torch.empty(self.B * self.Tc, dtype=torch.int32, device=dev)
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=dev)
         # neuron state (fp64) and readout filters
         self.u = torch.empty(Bn, dtype=f64, device=dev)
         self.a = torch.empty(Bn, dtype=f64, device=dev)
@@ -217,9 +223,9 @@ class EpropEngine:
             ln = min(Tc, T - t0)
             xp = x.data_ptr() + t0 * k
             call("spb_compact_events", v(xp), strideb, B, ln, Tc, k, v(self.ev.data_ptr()),
-                 v(self.nnz.data_ptr()), k, st)
+                 v(self.nnz.data_ptr()), self.cap, v(self.overflow.data_ptr()), st)
             call("spb_forward_chunk", 0, v(self.wt.data_ptr()), int(self.w_f64),
-                 v(self.ev.data_ptr()), v(self.nnz.data_ptr()), B, n, k, k, Tc, ln, t0, T,
+                 v(self.ev.data_ptr()), v(self.nnz.data_ptr()), B, n, k, self.cap, Tc, ln, t0, T,
                  float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
                  int(self.alif), v(self.u.data_ptr()), v(self.a.data_ptr()),
                  v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
@@ -244,9 +250,9 @@ class EpropEngine:
             ln = min(Tc, T - t0)
             xp = x.data_ptr() + t0 * k
             call("spb_compact_events", v(xp), strideb, B, ln, Tc, k, v(self.ev.data_ptr()),
-                 v(self.nnz.data_ptr()), k, st)
+                 v(self.nnz.data_ptr()), self.cap, v(self.overflow.data_ptr()), st)
             timed("forward", ln, "spb_forward_chunk", 1, v(self.wt.data_ptr()), int(self.w_f64),
-                 v(self.ev.data_ptr()), v(self.nnz.data_ptr()), B, n, k, k, Tc, ln, t0, T,
+                 v(self.ev.data_ptr()), v(self.nnz.data_ptr()), B, n, k, self.cap, Tc, ln, t0, T,
                  float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
                  int(self.alif), v(self.u.data_ptr()), v(self.a.data_ptr()), None, None, None,
                  v(self.wsig.data_ptr()), v(ctab.data_ptr()), v(self.psi2.data_ptr()),
@@ -271,6 +277,13 @@ class EpropEngine:
                  v(self.grad_w_acc.data_ptr()), st)
             self.launches += 1
         return self
+
+    def check_overflow(self):
+        """Synchronising check that no (sample, step) had more than k*max_count events."""
+        if int(self.overflow.item()):
+            self.overflow.zero_()
+            raise ValueError(f"spike counts exceed max_count={self.max_count}; "
+                             "rebuild the engine with a larger max_count")
 
     def check_labels(self, labels_np):
         labels_np = np.asarray(labels_np)

@@ -210,3 +210,19 @@ def test_label_out_of_range_raises():
         P.eprop_sparse_gradient(net, np.zeros((5, 4)), 3)
     with pytest.raises(P.ShapeMismatch):
         P.eprop_sparse_gradient(net, np.zeros((5, 5)), 0)
+
+
+def test_pooled_count_inputs_vs_oracle():
+    """Integer event counts (pool_channels, datasets.py:138-159) through the drop-in API."""
+    _need_gpu()
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    x, labels = poisson_batch(6, 700, 45, 5, seed=3)
+    xp = x.reshape(6, 45, 140, 5).sum(-1).astype(np.float64)   # factor-5 pooling, counts <= 5
+    assert xp.max() > 1
+    net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=160, n_inputs=140, n_classes=5,
+                                       precision="f64", seed=2))
+    r = P.eprop_batch_gradient(net, xp, labels, chunk=16)
+    ref = O.eprop_two_pass_batch(net.neuron.w, net.readout.w_out, O.Params(alif=True), xp, labels)
+    assert _rel(r.grads["w"], ref.grad_w) <= REL_TOL
+    assert np.allclose(r.loss, ref.loss, rtol=1e-9)
