@@ -35,19 +35,28 @@ const char* spb_last_error(void);
 int spb_version(void);
 int spb_device_sm(void); /* compute capability of the current device, e.g. 100 */
 
-/* K0  Compact one chunk of dense uint8 spike counts into per-(sample,step) event lists.
- *     x[b*stride_b + s*k + j] for s < rows; ev[(b*ld_rows+s)*cap + q] = 32*j, each channel
- *     repeated `count` times, increasing j; nnz[b*ld_rows+s] = number of events (<= cap).
- *     A row with more than `cap` events sets *overflow = 1 (may be NULL).
- *     Replaces the dense `net.neuron.w @ x_t` operand preparation (gradients.py:125). */
-int spb_compact_events(const uint8_t* x, long long stride_b, int B, int rows, int ld_rows, int k,
-                       uint32_t* ev, int* nnz, int cap, int* overflow, cudaStream_t stream);
+/* K2  Exact input projection on INT8 tensor cores (proj.cu).  The weights are sliced
+ *     once per update into P signed 7-bit digits per entry (P=7 for fp32 weights, 8 for
+ *     fp64) with a per-neuron power-of-two scale; spikes are uint8 counts; tcgen05
+ *     kind::i8 accumulates exactly in int32 and the digits are recombined in int64, so
+ *     I = W x_t is exact up to one final fp64 rounding.  Replaces `net.neuron.w @ x_t`
+ *     (gradients.py:125).
+ *   spb_slice_weights: w [n][k] fp32 (w_is_f64=0) / fp64 -> wq [P][n_pad32][Kpad] int8,
+ *                      sexp [n] int32 (n_pad32 = round_up(n,32), Kpad = round_up(k,128)).
+ *   spb_pack_spikes:   x[b*stride_b + s*k + j] (s < len) -> xq [B*Tc][Kpad] uint8, zero padded.
+ *   spb_input_proj:    cur[row][i] = sum_j xq[row][j] W[i][j] for row < M (= B*Tc), fp64;
+ *                      persistent grid of min(tiles, sm_count) CTAs. */
+int spb_slice_weights(const void* w, int w_is_f64, int n, int k, int Kpad, int n_pad32, int P,
+                      int8_t* wq, int* sexp, cudaStream_t stream);
+int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int len, int Tc, int Kpad,
+                    uint8_t* xq, cudaStream_t stream);
+int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
+                   int Kpad, int P, double* cur, int sm_count, cudaStream_t stream);
 
-/* K1  Fused forward over one time chunk: event gather of W x_t (fp64 accumulation),
- *     ALIF/LIF state update, spike and surrogate derivative.
+/* K1  Neuron dynamics over one time chunk from the exact current cur [B*Tc][n] (row
+ *     b*Tc+s): ALIF/LIF state update, spike and surrogate derivative.
  *     Replaces _step_state (gradients.py:118-129) + heaviside/surrogate_grad
  *     (graph.py:40-52) + the readout spike filter (gradients.py:173-174).
- *     wt      [k][n] transposed input weights, fp32 (w_is_f64=0) or fp64 (1)
  *     u, a    [B][n] fp64 state, carried across chunks (zero at t=0)
  *     pass 0 (A): zbar, zsum [B][n] fp64 carried; raster [B][T][ceil(n/32)] bit-packed
  *                 spikes (optional, may be NULL).
@@ -55,12 +64,12 @@ int spb_compact_events(const uint8_t* x, long long stride_b, int B, int rows, in
  *                 coef [B][Tc][coef_ld] float2 (A'_t, Q'_t) for K6 (ALIF only; rows
  *                 i >= n are never written -- keep them zero);
  *                 lp_hi/lp_lo [n][B*Tc] bf16 split of L_t psi_t, K index b*Tc+s. */
-int spb_forward_chunk(int pass, const void* wt, int w_is_f64, const uint32_t* ev, const int* nnz,
-                      int B, int n, int k, int cap, int Tc, int len, int t0, int T, double alpha,
-                      double theta, double slope, double beta, double rho, double kappa,
-                      int reset, int alif, double* u, double* a, double* zbar, double* zsum,
-                      uint32_t* raster, const float* wsig, const double* ctab, float* psi2,
-                      float* coef, int coef_ld, void* lp_hi, void* lp_lo, cudaStream_t stream);
+int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int len, int t0, int T,
+                      double alpha, double theta, double slope, double beta, double rho,
+                      double kappa, int reset, int alif, double* u, double* a, double* zbar,
+                      double* zsum, uint32_t* raster, const float* wsig, const double* ctab,
+                      float* psi2, float* coef, int coef_ld, void* lp_hi, void* lp_lo,
+                      cudaStream_t stream);
 
 /* K4  Presynaptic filter xbar_t = alpha*xbar_{t-1} + x_t (the factorised LIF trace G_u,
  *     gradients.py:89-94 with H_I = alpha, F rows = x_t; test_gradients.py:81-91).

@@ -1,8 +1,8 @@
 // Forward-side kernels of the e-prop update (sm_100a):
-//   K0  spb_compact_events  -- dense uint8 spike counts -> per-(sample,step) event lists
-//   K1  spb_forward_chunk   -- fused input gather + LIF/ALIF dynamics + surrogate over a
-//                              time chunk; pass A (spike raster, zsum) or pass B (learning-
-//                              signal-weighted surrogate, eligibility coefficients)
+//   K1  spb_forward_chunk   -- LIF/ALIF dynamics + surrogate over a time chunk from the
+//                              exact input current of K2 (proj.cu); pass A (spike raster,
+//                              zsum) or pass B (learning-signal-weighted surrogate,
+//                              eligibility coefficients)
 //   K4  spb_xbar_chunk      -- presynaptic filter xbar_t = alpha*xbar_{t-1} + x_t
 //
 // Reference semantics: _step_state (gradients.py:118-129), heaviside/surrogate_grad
@@ -14,79 +14,27 @@
 namespace spb {
 
 // ------------------------------------------------------------------------------------
-// K0: one warp per (sample, step) row; increasing channel order (deterministic).
-// Each input event is emitted `count` times as the word j*32 (the row offset of channel j
-// in K1's weight tile), so the gather is a pure add: sum_j count_j * W[i][j] exactly as
-// repeated fp64 additions of the same weight.  A row whose total count exceeds `cap`
-// is truncated and flagged in *overflow (the host raises).
-__global__ void compact_events_kernel(const uint8_t* __restrict__ x, long long stride_b,
-                                      int k, int rows_per_b, int ld_rows, int B,
-                                      uint32_t* __restrict__ ev, int* __restrict__ nnz, int cap,
-                                      int* __restrict__ overflow) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= B * rows_per_b) return;
-  const int b = warp / rows_per_b, s = warp % rows_per_b;
-  const uint8_t* row = x + (long long)b * stride_b + (long long)s * k;
-  const long long orow = (long long)b * ld_rows + s;
-  uint32_t* out = ev + orow * cap;
-  int count = 0;
-  for (int q0 = 0; q0 < k; q0 += 32) {
-    const int j = q0 + lane;
-    const int c = (j < k) ? (int)row[j] : 0;
-    // inclusive warp scan of the counts
-    int incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int base = count + incl - c;
-    for (int r = 0; r < c; ++r)
-      if (base + r < cap) out[base + r] = (uint32_t)j * 32u;
-    count += __shfl_sync(0xffffffffu, incl, 31);
-  }
-  if (lane == 0) {
-    nnz[orow] = min(count, cap);
-    if (count > cap && overflow) atomicExch(overflow, 1);
-  }
-}
-
-// ------------------------------------------------------------------------------------
-// K1: fused forward chunk.  Warp = 32 consecutive neurons of one sample; the CTA's
-// input-weight tile W^T[:, i0:i0+32] is staged in shared memory once and gathered by
-// event index (x is a spike-count train, ~10% dense on SHD-shaped data).  State u, a
-// and the input current are fp64 so spike decisions match the f64 reference
-// (SURVEY.md 7.3); every multiply/add mirrors the reference's operation order with
-// explicit round-to-nearest intrinsics (no FMA contraction).
+// K1: neuron dynamics over one time chunk, reading the exact input current I (fp64,
+// produced by the INT8 tensor-core projection K2, proj.cu).  Warp = 32 consecutive
+// neurons of one sample.  State u, a and I are fp64 so spike decisions match the f64
+// reference; every multiply/add mirrors the reference's operation order
+// with explicit round-to-nearest intrinsics (no FMA contraction).
 // ------------------------------------------------------------------------------------
 struct FwdParams {
-  int B, n, k, cap, Tc, len, t0, T, coef_ld;
+  int B, n, Tc, len, t0, T, coef_ld;
   double alpha, theta, slope, beta, rho, kappa;
   int reset, alif, pass;  // pass 0 = A, 1 = B
 };
 
-template <typename WT, bool SMEM_W>
-__global__ void __launch_bounds__(1024) forward_chunk_kernel(
-    FwdParams P, const WT* __restrict__ wt, const uint32_t* __restrict__ ev,
-    const int* __restrict__ nnz, double* __restrict__ u_st, double* __restrict__ a_st,
-    double* __restrict__ zbar_st, double* __restrict__ zsum_st, uint32_t* __restrict__ raster,
-    const float* __restrict__ wsig, const double* __restrict__ ctab, float* __restrict__ psi2_st,
-    float2* __restrict__ coef, __nv_bfloat16* __restrict__ lp_hi,
+__global__ void __launch_bounds__(256) forward_chunk_kernel(
+    FwdParams P, const double* __restrict__ cur, double* __restrict__ u_st,
+    double* __restrict__ a_st, double* __restrict__ zbar_st, double* __restrict__ zsum_st,
+    uint32_t* __restrict__ raster, const float* __restrict__ wsig, const double* __restrict__ ctab,
+    float* __restrict__ psi2_st, float2* __restrict__ coef, __nv_bfloat16* __restrict__ lp_hi,
     __nv_bfloat16* __restrict__ lp_lo) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* ws = reinterpret_cast<double*>(smem_raw);  // fp64 tile: no conversion in the gather
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i0 = blockIdx.x * 32;
-  const int i = i0 + lane;
+  const int i = blockIdx.x * 32 + lane;
   const bool valid_i = i < P.n;
-  if (SMEM_W) {
-    for (int idx = threadIdx.x; idx < P.k * 32; idx += blockDim.x) {
-      const int j = idx >> 5, c = idx & 31;
-      ws[idx] = (i0 + c < P.n) ? (double)wt[(long long)j * P.n + i0 + c] : 0.0;
-    }
-    __syncthreads();
-  }
   const int b = blockIdx.y * (blockDim.x >> 5) + warp;
   if (b >= P.B) return;
   const long long bi = (long long)b * P.n + i;
@@ -106,81 +54,54 @@ __global__ void __launch_bounds__(1024) forward_chunk_kernel(
   const double theta = P.theta, beta = P.beta;
   const int K = P.B * P.Tc;
   const int nw = (P.n + 31) >> 5;
+  const double* crow = cur + (long long)b * P.Tc * P.n + i;
   __nv_bfloat16 hv[8], lv[8];
   for (int s8 = 0; s8 < P.Tc; s8 += 8) {
+    double Ib[8];
 #pragma unroll
-  for (int u8 = 0; u8 < 8; ++u8) {
-    const int s = s8 + u8;
-    if (s < P.len) {
-      const int row = b * P.Tc + s;
-      const int nz = nnz[row];
-      const uint32_t* list = ev + (long long)row * P.cap;
-      double I0 = 0.0, I1 = 0.0;
-      const double* wl = ws + lane;
-      for (int q0 = 0; q0 < nz; q0 += 32) {
-        const uint32_t e = (q0 + lane < nz) ? list[q0 + lane] : 0u;
-        const int mcnt = min(32, nz - q0);
-        int q = 0;
-        for (; q + 1 < mcnt; q += 2) {
-          const uint32_t e0 = __shfl_sync(0xffffffffu, e, q);
-          const uint32_t e1 = __shfl_sync(0xffffffffu, e, q + 1);
-          double w0, w1;
-          if (SMEM_W) {
-            w0 = wl[e0];
-            w1 = wl[e1];
-          } else {
-            w0 = valid_i ? (double)wt[(long long)(e0 >> 5) * P.n + i] : 0.0;
-            w1 = valid_i ? (double)wt[(long long)(e1 >> 5) * P.n + i] : 0.0;
+    for (int u8 = 0; u8 < 8; ++u8)
+      Ib[u8] = (valid_i && s8 + u8 < P.len) ? crow[(long long)(s8 + u8) * P.n] : 0.0;
+#pragma unroll
+    for (int u8 = 0; u8 < 8; ++u8) {
+      const int s = s8 + u8;
+      if (s < P.len) {
+        const int row = b * P.Tc + s;
+        const double I = Ib[u8];
+        // gradients.py:121-129 (u - theta - beta*a evaluates as (u - theta) - (beta*a))
+        const double d_prev = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
+        const double z_prev = d_prev >= 0.0 ? 1.0 : 0.0;
+        a = __dadd_rn(__dmul_rn(P.rho, a), z_prev);
+        u = __dadd_rn(__dmul_rn(P.alpha, u), I);
+        if (P.reset) u = __dsub_rn(u, __dmul_rn(theta, z_prev));
+        const double d = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
+        const bool z = d >= 0.0;
+        const int t = P.t0 + s;
+        if (P.pass == 0) {
+          // readout filter of the spikes (gradients.py:173-174)
+          zbar = __dadd_rn(__dmul_rn(P.kappa, zbar), z ? 1.0 : 0.0);
+          zsum = __dadd_rn(zsum, zbar);
+          const unsigned bal = __ballot_sync(0xffffffffu, z && valid_i);
+          if (raster != nullptr && lane == 0)
+            raster[((long long)b * P.T + t) * nw + blockIdx.x] = bal;
+        } else {
+          const double psi_d = surrogate_grad_f64(d, P.slope);
+          const float psi1 = (float)surrogate_grad_f64(d_prev, P.slope);  // psi_{t-1}
+          const float lpsi = (float)(ctab[t] * (double)w_sig * psi_d);    // L_t * psi_t
+          if (P.alif && coef != nullptr) {
+            // eps~_t = A'_t eps~_{t-1} + xbar_{t-1}; grad += Q'_t eps~_t (eps = psi_{t-1} eps~)
+            const float A = (float)(P.rho - P.beta * (double)psi1);
+            const float Ap = (t == 0) ? 0.0f : A * (psi2 / fmaxf(psi1, 1e-30f));
+            const float Qp = -(float)P.beta * lpsi * psi1;
+            if (valid_i) coef[(long long)row * P.coef_ld + i] = make_float2(Ap, Qp);
           }
-          I0 = __dadd_rn(I0, w0);
-          I1 = __dadd_rn(I1, w1);
+          psi2 = psi1;
+          split_bf16(lpsi, hv[u8], lv[u8]);
         }
-        if (q < mcnt) {
-          const uint32_t e0 = __shfl_sync(0xffffffffu, e, q);
-          double w0;
-          if (SMEM_W) w0 = wl[e0];
-          else w0 = valid_i ? (double)wt[(long long)(e0 >> 5) * P.n + i] : 0.0;
-          I0 = __dadd_rn(I0, w0);
-        }
+      } else if (P.pass == 1) {
+        hv[u8] = __float2bfloat16_rn(0.0f);
+        lv[u8] = __float2bfloat16_rn(0.0f);
       }
-      const double I = __dadd_rn(I0, I1);
-      // gradients.py:121-129 (u - theta - beta*a evaluates as (u - theta) - (beta*a))
-      const double d_prev = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
-      const double z_prev = d_prev >= 0.0 ? 1.0 : 0.0;
-      a = __dadd_rn(__dmul_rn(P.rho, a), z_prev);
-      u = __dadd_rn(__dmul_rn(P.alpha, u), I);
-      if (P.reset) u = __dsub_rn(u, __dmul_rn(theta, z_prev));
-      const double d = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
-      const bool z = d >= 0.0;
-      const int t = P.t0 + s;
-      if (P.pass == 0) {
-        // readout filter of the spikes (gradients.py:173-174)
-        zbar = __dadd_rn(__dmul_rn(P.kappa, zbar), z ? 1.0 : 0.0);
-        zsum = __dadd_rn(zsum, zbar);
-        const unsigned bal = __ballot_sync(0xffffffffu, z && valid_i);
-        if (raster != nullptr && lane == 0)
-          raster[((long long)b * P.T + t) * nw + blockIdx.x] = bal;
-      } else {
-        const double psi_d = surrogate_grad_f64(d, P.slope);
-        const float psi = (float)psi_d;
-        const float psi1 = (float)surrogate_grad_f64(d_prev, P.slope);  // psi_{t-1}
-        const float lpsi = (float)(ctab[t] * (double)w_sig * psi_d);    // L_t * psi_t
-        if (P.alif && coef != nullptr) {
-          // eps~_t = A'_t eps~_{t-1} + xbar_{t-1};  grad += Q'_t eps~_t   (eps = psi_{t-1} eps~)
-          const float A = (float)(P.rho - P.beta * (double)psi1);
-          const float Ap = (t == 0) ? 0.0f : A * (psi2 / fmaxf(psi1, 1e-30f));
-          const float Qp = -(float)P.beta * lpsi * psi1;
-          if (valid_i) coef[(long long)row * P.coef_ld + i] = make_float2(Ap, Qp);
-        }
-        psi2 = psi1;
-        split_bf16(lpsi, hv[u8], lv[u8]);
-        (void)psi;
-      }
-    } else if (P.pass == 1) {
-      hv[u8] = __float2bfloat16_rn(0.0f);
-      lv[u8] = __float2bfloat16_rn(0.0f);
     }
-  }
     if (P.pass == 1 && valid_i) {
       const long long off = (long long)i * K + (long long)b * P.Tc + s8;
       *reinterpret_cast<uint4*>(lp_hi + off) = *reinterpret_cast<uint4*>(hv);
@@ -239,80 +160,32 @@ __global__ void xbar_chunk_kernel(const uint8_t* __restrict__ x, long long strid
 
 }  // namespace spb
 
-namespace spb {
-static int fwd_smem_limit() {
-  int dev = 0, lim = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  return lim;
-}
-
-template <typename WT>
-static int launch_forward(const FwdParams& P, const WT* wt, const uint32_t* ev, const int* nnz,
-                          double* u, double* a, double* zbar, double* zsum, uint32_t* raster,
-                          const float* wsig, const double* ctab, float* psi2, float2* coef,
-                          __nv_bfloat16* lph, __nv_bfloat16* lpl, cudaStream_t stream) {
-  const int wpb = 32;
-  dim3 grid(ceil_div(P.n, 32), ceil_div(P.B, wpb));
-  const size_t smem = (size_t)P.k * 32 * sizeof(double);
-  if ((long long)smem <= (long long)fwd_smem_limit()) {
-    auto kfn = forward_chunk_kernel<WT, true>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kfn<<<grid, wpb * 32, smem, stream>>>(P, wt, ev, nnz, u, a, zbar, zsum, raster, wsig, ctab,
-                                          psi2, coef, lph, lpl);
-  } else {
-    forward_chunk_kernel<WT, false><<<grid, wpb * 32, 0, stream>>>(
-        P, wt, ev, nnz, u, a, zbar, zsum, raster, wsig, ctab, psi2, coef, lph, lpl);
-  }
-  SPB_CHECK_LAUNCH("forward_chunk");
-  return 0;
-}
-
-}  // namespace spb
-
 using namespace spb;
 
 extern "C" {
 
-int spb_compact_events(const uint8_t* x, long long stride_b, int B, int rows, int ld_rows, int k,
-                       uint32_t* ev, int* nnz, int cap, int* overflow, cudaStream_t stream) {
-  SPB_CHECK_ARG(x && ev && nnz, "spb_compact_events: null pointer");
-  SPB_CHECK_ARG(B >= 0 && rows >= 0 && ld_rows >= rows && k > 0 && cap >= 1 && k < (1 << 24),
-                "spb_compact_events: bad sizes B=%d rows=%d k=%d cap=%d", B, rows, k, cap);
-  const long long warps = (long long)B * rows;
-  if (warps == 0) return 0;
-  const int threads = 256;
-  const long long blocks = (warps * 32 + threads - 1) / threads;
-  compact_events_kernel<<<(unsigned)blocks, threads, 0, stream>>>(x, stride_b, k, rows, ld_rows,
-                                                                  B, ev, nnz, cap, overflow);
-  SPB_CHECK_LAUNCH("compact_events");
-  return 0;
-}
-
-int spb_forward_chunk(int pass, const void* wt, int w_is_f64, const uint32_t* ev, const int* nnz,
-                      int B, int n, int k, int cap, int Tc, int len, int t0, int T, double alpha,
-                      double theta, double slope, double beta, double rho, double kappa,
-                      int reset, int alif, double* u, double* a, double* zbar, double* zsum,
-                      uint32_t* raster, const float* wsig, const double* ctab, float* psi2,
-                      float* coef, int coef_ld, void* lp_hi, void* lp_lo, cudaStream_t stream) {
+int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int len, int t0, int T,
+                      double alpha, double theta, double slope, double beta, double rho,
+                      double kappa, int reset, int alif, double* u, double* a, double* zbar,
+                      double* zsum, uint32_t* raster, const float* wsig, const double* ctab,
+                      float* psi2, float* coef, int coef_ld, void* lp_hi, void* lp_lo,
+                      cudaStream_t stream) {
   SPB_CHECK_ARG(pass == 0 || pass == 1, "spb_forward_chunk: pass must be 0 (A) or 1 (B)");
-  SPB_CHECK_ARG(wt && ev && nnz && u && a, "spb_forward_chunk: null pointer");
-  SPB_CHECK_ARG(B > 0 && n > 0 && k > 0 && Tc > 0 && Tc % 8 == 0 && len >= 0 && len <= Tc,
-                "spb_forward_chunk: bad sizes B=%d n=%d k=%d Tc=%d len=%d", B, n, k, Tc, len);
+  SPB_CHECK_ARG(cur && u && a, "spb_forward_chunk: null pointer");
+  SPB_CHECK_ARG(B > 0 && n > 0 && Tc > 0 && Tc % 8 == 0 && len >= 0 && len <= Tc,
+                "spb_forward_chunk: bad sizes B=%d n=%d Tc=%d len=%d", B, n, Tc, len);
   SPB_CHECK_ARG(pass == 0 ? (zbar && zsum) : (wsig && ctab && psi2 && lp_hi && lp_lo),
                 "spb_forward_chunk: missing pass-%c buffers", pass ? 'B' : 'A');
   SPB_CHECK_ARG(!(pass == 1 && alif && (!coef || coef_ld < n)),
                 "spb_forward_chunk: ALIF pass B needs coef with coef_ld >= n");
-  FwdParams P{B, n, k, cap, Tc, len, t0, T, coef_ld, alpha, theta, slope, beta, rho, kappa,
+  FwdParams P{B, n, Tc, len, t0, T, coef_ld, alpha, theta, slope, beta, rho, kappa,
               reset, alif, pass};
-  auto lph = reinterpret_cast<__nv_bfloat16*>(lp_hi);
-  auto lpl = reinterpret_cast<__nv_bfloat16*>(lp_lo);
-  auto cf = reinterpret_cast<float2*>(coef);
-  if (w_is_f64)
-    return launch_forward<double>(P, (const double*)wt, ev, nnz, u, a, zbar, zsum, raster, wsig,
-                                  ctab, psi2, cf, lph, lpl, stream);
-  return launch_forward<float>(P, (const float*)wt, ev, nnz, u, a, zbar, zsum, raster, wsig,
-                               ctab, psi2, cf, lph, lpl, stream);
+  dim3 grid(ceil_div(n, 32), ceil_div(B, 8));
+  forward_chunk_kernel<<<grid, 256, 0, stream>>>(
+      P, cur, u, a, zbar, zsum, raster, wsig, ctab, psi2, reinterpret_cast<float2*>(coef),
+      reinterpret_cast<__nv_bfloat16*>(lp_hi), reinterpret_cast<__nv_bfloat16*>(lp_lo));
+  SPB_CHECK_LAUNCH("forward_chunk");
+  return 0;
 }
 
 int spb_xbar_chunk(const uint8_t* x, long long stride_b, int B, int k, int k_pad, int Tc,

@@ -1,0 +1,335 @@
+// K2: exact input projection I = W x_t on 5th-generation INT8 tensor cores (tcgen05).
+//
+// The reference computes the input current with a float matvec (`net.neuron.w @ x_t`,
+// gradients.py:125) in f64.  Spike decisions must match it bit for bit (margins go
+// down to ~1e-7), so the projection has to be exact to fp64 level.
+// Inputs are spike counts (uint8), so we slice the weights instead of rounding them:
+//
+//   W[i][j] = sum_{p<P} q_p[i][j] * 2^(s_i - 6 - 7p) + r,   q_p in [-64, 64] (int8),
+//   |r| <= 2^(s_i - 7P),  s_i = exponent of max_j |W[i][j]|
+//
+// P = 7 slices (48 bits) for fp32 weights -- exact for every weight >= 2^-24 of the row
+// maximum -- and P = 8 (55 bits) for fp64 weights.  x (u8) * q_p (s8) is accumulated by
+// tcgen05.mma.kind::i8 in int32 TMEM (exact: |acc| <= k*255*64 < 2^31), the slices are
+// recombined in int64 (exact) and converted to fp64 once: the result is the (weight-
+// truncated) exact sum rounded once, independent of summation order.
+//
+// Kernels:
+//   spb_pack_spikes      x chunk [B][len][k] -> xq [B*Tc][Kpad] (TMA-able, zero padded)
+//   spb_slice_weights    W [n][k] fp32/fp64  -> Wq [P][n_pad32][Kpad] int8, s [n] int32
+//   spb_input_proj       persistent warp-specialised tcgen05 GEMM -> I [B*Tc][n] fp64
+#include "tma.cuh"
+
+namespace spb {
+namespace proj {
+
+constexpr int BM = 128;       // (sample, step) rows per tile
+constexpr int NT = 32;        // neurons per tile (per slice)
+constexpr int BK = 128;       // bytes (= int8 elements) of K per stage: one 128B swizzle row
+constexpr int STAGES = 4;
+constexpr int THREADS = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int TILE_A = BM * BK;
+
+template <int P>
+struct Cfg {
+  static constexpr int N = P * NT;             // MMA N (224 or 256)
+  static constexpr int TILE_B = N * BK;
+  static constexpr int STAGE = TILE_A + TILE_B;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  // kind::i8: D s32 (c_format 2), A u8 (a_format 0), B s8 (b_format 1), both K-major
+  static constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (1u << 10) |
+                                    ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+};
+
+__device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ double pow2(int e) {  // 2^e for -1022 <= e <= 1023
+  return __longlong_as_double((long long)(e + 1023) << 52);
+}
+
+template <int P>
+__global__ void __launch_bounds__(THREADS, 1)
+    input_proj_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+                      const int* __restrict__ sexp, double* __restrict__ out, int M, int n,
+                      int n_pad32, int nkb) {
+  using C = Cfg<P>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;       // [2]
+  uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m_tiles = (M + BM - 1) / BM;
+  const int n_tiles = (n + NT - 1) / NT;
+  const int num_tiles = m_tiles * n_tiles;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(&tfull[a]), 1);
+      mbar_init(smem_u32(&tempty[a]), 4);  // one arrive per epilogue warp
+    }
+    mbar_fence_init();
+    tma_prefetch_desc(&tm_x);
+    tma_prefetch_desc(&tm_w);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int nt = t / m_tiles, mt = t % m_tiles;  // consecutive tiles share W slices
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(smem_u32(&empty[s]), ((it / STAGES) & 1) ^ 1);
+          const uint32_t st = smem_u32(smem + s * C::STAGE);
+          const uint32_t fb = smem_u32(&full[s]);
+          mbar_expect_tx(fb, C::STAGE);
+          tma_load_2d(st, &tm_x, fb, kb * BK, mt * BM);
+#pragma unroll
+          for (int p = 0; p < P; ++p)
+            tma_load_2d(st + TILE_A + p * NT * BK, &tm_w, fb, kb * BK, p * n_pad32 + nt * NT);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int it = 0, lt = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+        const int a = lt & 1;
+        mbar_wait(smem_u32(&tempty[a]), ((lt >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dacc = tmem_base + (uint32_t)(a * 256);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(smem_u32(&full[s]), (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t st = smem_u32(smem + s * C::STAGE);
+#pragma unroll
+          for (int kk = 0; kk < BK / 32; ++kk)
+            mma_i8(dacc, desc_k_sw128(st + kk * 32), desc_k_sw128(st + TILE_A + kk * 32),
+                   C::IDESC, (kb | kk) ? 1u : 0u);
+          commit(smem_u32(&empty[s]));
+        }
+        commit(smem_u32(&tfull[a]));
+      }
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    int lt = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+      const int nt = t / m_tiles, mt = t % m_tiles;
+      const int a = lt & 1;
+      mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256);
+      long long g0[NT], g1[NT];
+      int32_t r[32];
+#pragma unroll
+      for (int c = 0; c < NT; ++c) g0[c] = g1[c] = 0;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        tmem_ld32(tbase + p * NT, r);
+#pragma unroll
+        for (int c = 0; c < NT; ++c) {
+          if (p < 3) g0[c] = g0[c] * 128 + r[c];
+          else g1[c] = g1[c] * 128 + r[c];
+        }
+      }
+      // TMEM stage a is free once every epilogue warp has pulled its lanes
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&tempty[a]));
+      const int row = mt * BM + q * 32 + lane;
+      if (row < M) {
+        double* orow = out + (long long)row * n + nt * NT;
+        const int i0 = nt * NT;
+#pragma unroll
+        for (int c = 0; c < NT; c += 2) {
+          double v[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = i0 + c + h;
+            const int se = (i < n) ? __ldg(sexp + i) : 0;
+            // I = g0 * 2^(s-6-14) + g1 * 2^(s-6-7(P-1))  (both conversions exact)
+            v[h] = fma((double)g0[c + h], pow2(se - 20), (double)g1[c + h] * pow2(se - 6 - 7 * (P - 1)));
+          }
+          if (i0 + c + 1 < n) {
+            *reinterpret_cast<double2*>(orow + c) = make_double2(v[0], v[1]);
+          } else if (i0 + c < n) {
+            orow[c] = v[0];
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
+// x chunk -> zero-padded K-major operand rows (16-byte aligned rows for TMA).
+__global__ void pack_spikes_kernel(const uint8_t* __restrict__ x, long long stride_b, int k, int len,
+                                   int Tc, int Kpad, int B, uint8_t* __restrict__ xq) {
+  const long long total = (long long)B * Tc * Kpad;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx % Kpad);
+    const long long row = idx / Kpad;
+    const int s = (int)(row % Tc);
+    const int b = (int)(row / Tc);
+    uint8_t v = 0;
+    if (j < k && s < len) v = x[(long long)b * stride_b + (long long)s * k + j];
+    xq[idx] = v;
+  }
+}
+
+// One warp per neuron row: exponent of the row maximum, then P signed 7-bit digits.
+template <typename WT>
+__global__ void slice_weights_kernel(const WT* __restrict__ w, int n, int k, int Kpad, int n_pad32,
+                                     int P, int8_t* __restrict__ wq, int* __restrict__ sexp) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n_pad32) return;
+  double mx = 0.0;
+  if (i < n)
+    for (int j = lane; j < k; j += 32) mx = fmax(mx, fabs((double)w[(long long)i * k + j]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int s = 0;
+  if (mx > 0.0) frexp(mx, &s);  // mx = f * 2^s, f in [0.5, 1)  =>  |w| < 2^s
+  if (lane == 0 && i < n) sexp[i] = s;
+  for (int j = lane; j < Kpad; j += 32) {
+    double r = (i < n && j < k) ? ldexp((double)w[(long long)i * k + j], -s) : 0.0;
+    for (int p = 0; p < P; ++p) {
+      const double t = r * (p == 0 ? 64.0 : 128.0);
+      const double qv = rint(t);
+      r = t - qv;
+      wq[((long long)p * n_pad32 + i) * Kpad + j] = (int8_t)(int)qv;
+    }
+  }
+}
+
+}  // namespace proj
+}  // namespace spb
+
+using namespace spb;
+
+extern "C" {
+
+int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int len, int Tc, int Kpad,
+                    uint8_t* xq, cudaStream_t stream) {
+  SPB_CHECK_ARG(x && xq && B > 0 && k > 0 && Kpad >= k && Kpad % proj::BK == 0 && len >= 0 &&
+                    len <= Tc,
+                "spb_pack_spikes: bad args (Kpad must be a multiple of %d)", proj::BK);
+  const long long total = (long long)B * Tc * Kpad;
+  const long long want = (total + 255) / 256;
+  const int blocks = (int)(want < 148LL * 16 ? want : 148LL * 16);
+  proj::pack_spikes_kernel<<<blocks, 256, 0, stream>>>(x, stride_b, k, len, Tc, Kpad, B, xq);
+  SPB_CHECK_LAUNCH("pack_spikes");
+  return 0;
+}
+
+int spb_slice_weights(const void* w, int w_is_f64, int n, int k, int Kpad, int n_pad32, int P,
+                      int8_t* wq, int* sexp, cudaStream_t stream) {
+  SPB_CHECK_ARG(w && wq && sexp && n > 0 && k > 0 && Kpad >= k && n_pad32 >= n &&
+                    n_pad32 % proj::NT == 0 && (P == 7 || P == 8),
+                "spb_slice_weights: bad args");
+  const int blocks = ceil_div(n_pad32 * 32, 256);
+  if (w_is_f64)
+    proj::slice_weights_kernel<double><<<blocks, 256, 0, stream>>>((const double*)w, n, k, Kpad,
+                                                                   n_pad32, P, wq, sexp);
+  else
+    proj::slice_weights_kernel<float><<<blocks, 256, 0, stream>>>((const float*)w, n, k, Kpad,
+                                                                  n_pad32, P, wq, sexp);
+  SPB_CHECK_LAUNCH("slice_weights");
+  return 0;
+}
+
+int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
+                   int Kpad, int P, double* out, int sm_count, cudaStream_t stream) {
+  SPB_CHECK_ARG(xq && wq && sexp && out && M > 0 && n > 0 && n_pad32 >= n &&
+                    n_pad32 % proj::NT == 0 && Kpad % proj::BK == 0 && (P == 7 || P == 8),
+                "spb_input_proj: bad args");
+  SPB_CHECK_ARG((reinterpret_cast<uintptr_t>(xq) | reinterpret_cast<uintptr_t>(wq)) % 16 == 0,
+                "spb_input_proj: operands must be 16-byte aligned");
+  CUtensorMap mx, mw;
+  const bool ok =
+      make_tmap_2d(&mx, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, Kpad, M, Kpad, proj::BK, proj::BM,
+                   CU_TENSOR_MAP_SWIZZLE_128B) &&
+      make_tmap_2d(&mw, wq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, Kpad, (uint64_t)P * n_pad32, Kpad,
+                   proj::BK, proj::NT, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!ok) {
+    set_error("spb_input_proj: cuTensorMapEncodeTiled failed");
+    return 3;
+  }
+  const int tiles = ceil_div(M, proj::BM) * ceil_div(n, proj::NT);
+  const int grid = max(1, min(tiles, sm_count > 0 ? sm_count : 148));
+  const int nkb = Kpad / proj::BK;
+  if (P == 7) {
+    auto kfn = proj::input_proj_kernel<7>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, proj::Cfg<7>::SMEM);
+    kfn<<<grid, proj::THREADS, proj::Cfg<7>::SMEM, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);
+  } else {
+    auto kfn = proj::input_proj_kernel<8>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, proj::Cfg<8>::SMEM);
+    kfn<<<grid, proj::THREADS, proj::Cfg<8>::SMEM, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);
+  }
+  SPB_CHECK_LAUNCH("input_proj");
+  return 0;
+}
+
+}  // extern "C"

@@ -3,9 +3,11 @@
 One ``EpropEngine`` owns every device buffer for a fixed problem shape
 (batch B, hidden n, inputs k, classes m, chunk length Tc) and replays the update
 
-    pass A  (forward only)         for each chunk: K0 compact -> K1 forward(A)
+    weights                        K2s slice W into int8 digits (once per update)
+    pass A  (forward only)         for each chunk: pack x -> K2 int8 tcgen05 I = W x
+                                                  -> K1 dynamics(A)
     readout                        K3 loss / g / w_sig ; K7 grad W_out
-    pass B  (forward + traces)     for each chunk: K0 -> K1 forward(B) -> K4 xbar
+    pass B  (forward + traces)     for each chunk: pack -> K2 -> K1 dynamics(B) -> K4 xbar
                                                   -> K5 tcgen05 GEMM (L psi) x xbar
                                                   -> K6 ALIF eps chunk (ALIF only)
                                                   -> fixed-order partial reduce
@@ -74,7 +76,7 @@ class EpropEngine:
     """Buffers + launch sequence for one problem shape on one device."""
 
     def __init__(self, n: int, k: int, m: int, B: int, *, alif: bool, w_f64: bool = False,
-                 chunk: int = 32, device=None, sm_count: int | None = None, max_count: int = 1):
+                 chunk: int = 32, device=None, sm_count: int | None = None):
         if chunk <= 0 or chunk % 8:
             raise ValueError("chunk must be a positive multiple of 8")
         if alif and chunk not in (8, 16, 32, 64):
@@ -97,15 +99,14 @@ class EpropEngine:
         Bn, Bk = (self.B, self.n), (self.B, self.k)
         K = self.B * self.Tc
         self.K = K
-        # K0 event lists: every input event repeated `count` times, so a row holds at
-        # most k * max_count entries (max_count = 1 for binary spike trains)
-        self.max_count = int(max_count)
-        if not 1 <= self.max_count <= 255:
-            raise ValueError("max_count must be in [1, 255]")
-        self.cap = self.k * self.max_count
-        self.ev = torch.empty(self.B * self.Tc * self.cap, dtype=torch.int32, device=dev)
-        self.nnz = torch.empty(self.B * self.Tc, dtype=torch.int32, device=dev)
-        self.overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+        # K2 exact INT8 tensor-core projection: x chunk operand, sliced weights, current
+        self.Kpad = _round_up(self.k, 128)
+        self.n_pad32 = _round_up(self.n, 32)
+        self.P = 8 if self.w_f64 else 7
+        self.xq = torch.zeros((self.B * self.Tc, self.Kpad), dtype=torch.uint8, device=dev)
+        self.cur = torch.empty((self.B * self.Tc, self.n), dtype=f64, device=dev)
+        self.wq = torch.zeros((self.P, self.n_pad32, self.Kpad), dtype=torch.int8, device=dev)
+        self.sexp = torch.zeros(self.n, dtype=torch.int32, device=dev)
         # neuron state (fp64) and readout filters
         self.u = torch.empty(Bn, dtype=f64, device=dev)
         self.a = torch.empty(Bn, dtype=f64, device=dev)
@@ -144,22 +145,36 @@ class EpropEngine:
         self.grad_w_acc = torch.empty((self.n, self.k_pad), dtype=f64, device=dev)
         self.grad_wout = torch.empty((self.m, self.n), dtype=f64, device=dev)
         # weights
-        self.wt = torch.empty((self.k, self.n), dtype=f64 if self.w_f64 else f32, device=dev)
+        self.w = torch.empty((self.n, self.k), dtype=f64 if self.w_f64 else f32, device=dev)
         self.wout = torch.empty((self.m, self.n), dtype=f64, device=dev)
         self._ctab_T = None
         self.ctab = None
         self.launches = 0
 
     # ----------------------------------------------------------------------------------
-    def set_weights(self, w, w_out):
-        """Upload input weights (as W^T [k, n]) and readout weights (fp64)."""
+    def set_weights(self, w, w_out, stream=None):
+        """Upload input weights and readout weights (fp64) and slice W into the INT8
+        digits of the exact tensor-core projection (K2)."""
         w = torch.as_tensor(w)
         w_out = torch.as_tensor(w_out)
         if tuple(w.shape) != (self.n, self.k) or tuple(w_out.shape) != (self.m, self.n):
             raise ShapeMismatch(f"weights {tuple(w.shape)}/{tuple(w_out.shape)} do not match "
                                 f"engine (n={self.n}, k={self.k}, m={self.m})")
-        self.wt.copy_(w.t().to(self.wt.dtype), non_blocking=True)
+        self.w.copy_(w.to(self.w.dtype), non_blocking=True)
         self.wout.copy_(w_out.to(torch.float64), non_blocking=True)
+        self.slice_weights(stream)
+
+    def slice_weights(self, stream=None):
+        """Re-derive the INT8 weight digits from ``self.w`` (after an in-place update)."""
+        st = ctypes_void(stream if stream is not None else self._stream())
+        _lib.call("spb_slice_weights", ctypes_void(self.w.data_ptr()), int(self.w_f64), self.n,
+                  self.k, self.Kpad, self.n_pad32, self.P, ctypes_void(self.wq.data_ptr()),
+                  ctypes_void(self.sexp.data_ptr()), st)
+
+    def _stream(self):
+        if self.device.type != "cuda":
+            return 0
+        return torch.cuda.current_stream(self.device).cuda_stream
 
     def _gains(self, T, kappa):
         if self._ctab_T != (T, kappa):
@@ -193,7 +208,7 @@ class EpropEngine:
         if T <= 0:
             raise ShapeMismatch("T must be positive")
         lib, call = self.lib, _lib.call
-        st = ctypes_void(stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream)
+        st = ctypes_void(stream if stream is not None else self._stream())
         if not self.alif:
             beta_e, rho_e = 0.0, 0.0
         else:
@@ -222,16 +237,14 @@ class EpropEngine:
             t0 = c * Tc
             ln = min(Tc, T - t0)
             xp = x.data_ptr() + t0 * k
-            call("spb_compact_events", v(xp), strideb, B, ln, Tc, k, v(self.ev.data_ptr()),
-                 v(self.nnz.data_ptr()), self.cap, v(self.overflow.data_ptr()), st)
-            call("spb_forward_chunk", 0, v(self.wt.data_ptr()), int(self.w_f64),
-                 v(self.ev.data_ptr()), v(self.nnz.data_ptr()), B, n, k, self.cap, Tc, ln, t0, T,
+            self._project(xp, strideb, ln, st)
+            call("spb_forward_chunk", 0, v(self.cur.data_ptr()), B, n, Tc, ln, t0, T,
                  float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
                  int(self.alif), v(self.u.data_ptr()), v(self.a.data_ptr()),
                  v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
                  v(raster.data_ptr()) if raster is not None else None,
                  None, None, None, None, 0, None, None, st)
-            self.launches += 2
+            self.launches += 3
         # ---------------- readout / loss ----------------
         call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
              v(labels.data_ptr()), B, n, m, v(self.s.data_ptr()), v(self.loss.data_ptr()),
@@ -249,15 +262,13 @@ class EpropEngine:
             t0 = c * Tc
             ln = min(Tc, T - t0)
             xp = x.data_ptr() + t0 * k
-            call("spb_compact_events", v(xp), strideb, B, ln, Tc, k, v(self.ev.data_ptr()),
-                 v(self.nnz.data_ptr()), self.cap, v(self.overflow.data_ptr()), st)
-            timed("forward", ln, "spb_forward_chunk", 1, v(self.wt.data_ptr()), int(self.w_f64),
-                 v(self.ev.data_ptr()), v(self.nnz.data_ptr()), B, n, k, self.cap, Tc, ln, t0, T,
-                 float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
-                 int(self.alif), v(self.u.data_ptr()), v(self.a.data_ptr()), None, None, None,
-                 v(self.wsig.data_ptr()), v(ctab.data_ptr()), v(self.psi2.data_ptr()),
-                 v(self.coef.data_ptr()) if self.alif else None, self.n_pad,
-                 v(self.lp_hi.data_ptr()), v(self.lp_lo.data_ptr()), st)
+            self._project(xp, strideb, ln, st, timed)
+            timed("forward", ln, "spb_forward_chunk", 1, v(self.cur.data_ptr()), B, n, Tc, ln,
+                  t0, T, float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
+                  int(self.alif), v(self.u.data_ptr()), v(self.a.data_ptr()), None, None, None,
+                  v(self.wsig.data_ptr()), v(ctab.data_ptr()), v(self.psi2.data_ptr()),
+                  v(self.coef.data_ptr()) if self.alif else None, self.n_pad,
+                  v(self.lp_hi.data_ptr()), v(self.lp_lo.data_ptr()), st)
             call("spb_xbar_chunk", v(xp), strideb, B, k, self.k_pad, Tc, ln, float(alpha),
                  v(self.xbar_state.data_ptr()), v(self.xf.data_ptr()), v(self.xh.data_ptr()),
                  v(self.xl.data_ptr()), st)
@@ -265,7 +276,7 @@ class EpropEngine:
                   v(self.lp_lo.data_ptr()),
                  v(self.xh.data_ptr()), v(self.xl.data_ptr()), n, self.k_pad, K, self.splits5,
                  v(part5), self.k_pad, slice_stride, st)
-            self.launches += 4
+            self.launches += 5
             if self.alif:
                 timed("elig", (ln, c > 0, c < nchunks - 1), "spb_alif_elig_chunk",
                       v(self.coef.data_ptr()), v(self.xf.data_ptr()),
@@ -278,12 +289,18 @@ class EpropEngine:
             self.launches += 1
         return self
 
-    def check_overflow(self):
-        """Synchronising check that no (sample, step) had more than k*max_count events."""
-        if int(self.overflow.item()):
-            self.overflow.zero_()
-            raise ValueError(f"spike counts exceed max_count={self.max_count}; "
-                             "rebuild the engine with a larger max_count")
+    def _project(self, xp, strideb, ln, st, timed=None):
+        """K2: pack the chunk's spikes and compute cur = W x_t exactly on INT8 tensor cores."""
+        v = ctypes_void
+        _lib.call("spb_pack_spikes", v(xp), strideb, self.B, self.k, ln, self.Tc, self.Kpad,
+                  v(self.xq.data_ptr()), st)
+        args = ("spb_input_proj", v(self.xq.data_ptr()), v(self.wq.data_ptr()),
+                v(self.sexp.data_ptr()), self.B * self.Tc, self.n, self.n_pad32, self.Kpad,
+                self.P, v(self.cur.data_ptr()), self.sm_count, st)
+        if timed is not None:
+            timed("proj", ln, *args)
+        else:
+            _lib.call(*args)
 
     def check_labels(self, labels_np):
         labels_np = np.asarray(labels_np)

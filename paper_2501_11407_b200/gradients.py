@@ -83,22 +83,17 @@ def _default_chunk(T: int) -> int:
 
 
 def get_engine(net: Network, B: int, *, chunk: int | None = None, T: int | None = None,
-               device=None, max_count: int = 1) -> EpropEngine:
-    """Engine cache keyed by shape, neuron kind, weight precision, chunk, event
-    multiplicity and device."""
+               device=None) -> EpropEngine:
+    """Engine cache keyed by shape, neuron kind, weight precision, chunk and device."""
     dev = torch.device(device if device is not None else "cuda")
     if chunk is None:
         chunk = _default_chunk(T or 32)
-    mc = 1
-    while mc < max_count:
-        mc *= 2
-    mc = min(mc, 255)
     w_f64 = net.neuron.w.dtype == np.float64
-    key = (net.n, net.k, net.m, B, net.is_alif, w_f64, chunk, mc, str(dev))
+    key = (net.n, net.k, net.m, B, net.is_alif, w_f64, chunk, str(dev))
     eng = _ENGINES.get(key)
     if eng is None:
         eng = EpropEngine(net.n, net.k, net.m, B, alif=net.is_alif, w_f64=w_f64, chunk=chunk,
-                          device=dev, max_count=mc)
+                          device=dev)
         _ENGINES[key] = eng
     return eng
 
@@ -144,15 +139,13 @@ def eprop_batch_gradient(net: Network, x, labels, *, chunk: int | None = None,
         bad = labels[(labels < 0) | (labels >= net.m)][0]
         raise LabelOutOfRange(f"label {int(bad)} out of range for {net.m} classes")
     xc = np.ascontiguousarray(_as_counts(x))
-    eng = get_engine(net, B, chunk=chunk, T=T, device=device,
-                     max_count=int(xc.max()) if xc.size else 1)
+    eng = get_engine(net, B, chunk=chunk, T=T, device=device)
     dev = eng.device
     xd = torch.from_numpy(xc).to(dev)
     ld = torch.from_numpy(labels).to(dev)
     eng.set_weights(torch.from_numpy(np.ascontiguousarray(net.neuron.w)),
                     torch.from_numpy(np.ascontiguousarray(net.readout.w_out)))
     eng.run(xd, ld, **_neuron_kwargs(net))
-    eng.check_overflow()
     wdt = torch.float64 if net.neuron.w.dtype == np.float64 else torch.float32
     gw = eng.grad_w(wdt)
     gwo = eng.grad_wout.to(wdt)

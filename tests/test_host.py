@@ -63,9 +63,11 @@ def test_version_and_error_text():
 def test_bad_arguments_are_rejected_without_gpu():
     # argument validation happens before any CUDA call -> works on a CPU-only host
     with pytest.raises(P.ShapeMismatch):
-        _lib.call("spb_forward_chunk", 2, None, 0, None, None, 1, 1, 1, 1, 8, 1, 0, 1,
+        _lib.call("spb_forward_chunk", 2, None, 1, 1, 8, 1, 0, 1,
                   0.95, 1.0, 10.0, 0.0, 0.0, 0.95, 0, 0, None, None, None, None, None, None,
                   None, None, None, 0, None, None, None)
+    with pytest.raises(P.ShapeMismatch):
+        _lib.call("spb_input_proj", None, None, None, 1, 1, 32, 100, 7, None, 148, None)
     with pytest.raises(P.ShapeMismatch):
         _lib.call("spb_alif_elig_chunk", None, None, None, None, 1, 1, 128, 64, 32, 32, 1,
                   0, 0, None)
@@ -102,7 +104,9 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     names = [c[0] for c in rec.calls]
     nch = (T + chunk - 1) // chunk
     assert names.count("spb_forward_chunk") == 2 * nch
-    assert names.count("spb_compact_events") == 2 * nch
+    assert names.count("spb_pack_spikes") == 2 * nch
+    assert names.count("spb_input_proj") == 2 * nch
+    assert names.count("spb_slice_weights") == 0
     assert names.count("spb_xbar_chunk") == nch
     assert names.count("spb_grad_gemm_partials") == nch
     assert names.count("spb_alif_elig_chunk") == (nch if alif else 0)
