@@ -163,7 +163,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--chunk", type=int, default=32)
+    ap.add_argument("--chunk", type=int, default=0, help="0 = engine default for T")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -194,7 +194,9 @@ def main():
     spec = P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=m, precision="f32", seed=0)
     net = P.init_network(spec)
     x_np, y_np = poisson_batch(B, k, T, m, seed=1000 + rank)
-    eng = EpropEngine(n, k, m, B, alif=kind == "alif", w_f64=False, chunk=args.chunk, device=dev)
+    from paper_2501_11407_b200.engine import default_chunk
+    chunk = args.chunk or default_chunk(T)
+    eng = EpropEngine(n, k, m, B, alif=kind == "alif", w_f64=False, chunk=chunk, device=dev)
     eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
     xd = torch.from_numpy(x_np).to(dev)
     yd = torch.from_numpy(y_np).to(dev)
@@ -284,38 +286,58 @@ def main():
                "d2h_bytes_per_step": int(B * 8),
                "ms_per_step": float(e2e_ms.item())}
 
-    # ---- roofline of the dominant kernel ----
+    # ---- roofline of every main kernel; the dominant one is the headline ----
     hbm_peak, bf16_peak, peak_kind = peaks()
+    Tc, KR, P_sl = eng.Tc, eng.KR, eng.P
+    kernels = {}
+    for name, lst in kern.items():
+        t_tot = sum(t for t, _ in lst) * 1e-3                    # seconds over all steps
+        byts = flops = 0.0
+        for _, meta in lst:
+            if name == "proj":
+                ln = meta                                        # int8 MACs x2, useful part
+                flops += 2.0 * P_sl * B * ln * n * k
+                byts += B * ln * k + P_sl * n * k + 8.0 * B * ln * n
+            elif name == "forward":
+                ln = meta
+                byts += 8.0 * B * ln * n + (16.0 if kind == "alif" else 8.0) * n * B * KR
+            elif name == "gemm":
+                ln = meta
+                flops += 6.0 * n * k * B * (ln + 1)                 # 3 bf16 MMAs per product
+                byts += 4.0 * (n + k) * B * KR
+            elif name == "carry":
+                ln, ld, stv = meta
+                byts += 4.0 * B * n * k * (int(ld) + int(stv)) + 8.0 * B * n
+                if stv:
+                    byts += 4.0 * (n + k) * B * KR
+                    flops += 6.0 * n * k * B * KR
+        ent = {"ms_per_step": t_tot * 1e3 / args.steps, "share_of_step": t_tot * 1e3 / args.steps / ms,
+               "launches_per_step": len(lst) / args.steps}
+        if byts:
+            ent["hbm_gbs"] = byts / t_tot / 1e9
+            ent["hbm_frac"] = ent["hbm_gbs"] / hbm_peak
+        if flops:
+            pk = 2 * bf16_peak if name == "proj" else bf16_peak
+            ent["tensor_tflops"] = flops / t_tot / 1e12
+            ent["tensor_frac"] = ent["tensor_tflops"] / pk
+        kernels[name] = ent
     roof = None
-    breakdown = {nm: float(sum(t for t, _ in v) / args.steps) for nm, v in kern.items()}
-    if "elig" in kern:
-        tot_t = sum(t for t, _ in kern["elig"]) * 1e-3
-        tot_b = 0.0
-        tot_f = 0.0
-        for _, (ln, ld, stv) in kern["elig"]:
-            tot_b += 4.0 * B * n * k * (int(ld) + int(stv))      # eps~ read / write
-            tot_b += 8.0 * B * ln * n + 4.0 * B * (ln + 1) * k    # staged (A',Q') and xbar
-            tot_f += 4.0 * B * ln * n * k                          # 2 FMA / synapse-step
-        ach = tot_b / tot_t / 1e9
-        fach = tot_f / tot_t / 1e12
-        roof = {"kernel": "alif_elig_kernel (K6)", "bound": "hbm", "achieved": ach,
-                "peak": hbm_peak, "peak_source": peak_kind, "unit": "GB/s",
-                "frac": ach / hbm_peak, "traffic": None,
-                "fp32": {"achieved": fach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": fach / FP32_PEAK_TFLOPS,
-                         "peak_source": "FFMA microbenchmark tools/fp_microbench.cu"},
-                "binding": "fp32" if fach / FP32_PEAK_TFLOPS > ach / hbm_peak else "hbm",
-                "kernel_ms_per_step": tot_t * 1e3 / args.steps,
-                "share_of_step": tot_t * 1e3 / args.steps / ms}
-    elif "gemm" in kern:
-        tot_t = sum(t for t, _ in kern["gemm"]) * 1e-3
-        tot_f = sum(6.0 * n * k * B * eng.Tc for _ in kern["gemm"])  # 3 bf16 MMAs
-        ach = tot_f / tot_t / 1e12
-        roof = {"kernel": "grad_gemm_tc_kernel (K5)", "bound": "tensor", "achieved": ach,
-                "peak": bf16_peak, "peak_source": peak_kind, "unit": "TFLOP/s",
-                "frac": ach / bf16_peak, "traffic": None,
-                "kernel_ms_per_step": tot_t * 1e3 / args.steps,
-                "share_of_step": tot_t * 1e3 / args.steps / ms}
+    if kernels:
+        dom = max(kernels, key=lambda nm: kernels[nm]["ms_per_step"])
+        e = kernels[dom]
+        names = {"proj": "input_proj_kernel (K2, int8 tcgen05)", "forward": "forward_chunk_kernel (K1)",
+                 "gemm": "grad_gemm_tc_kernel (K5, bf16x3 tcgen05)",
+                 "carry": "alif_carry_kernel (K6, tcgen05 + eps stream)"}
+        if e.get("tensor_frac", 0) >= e.get("hbm_frac", 0) and "tensor_tflops" in e:
+            pk = 2 * bf16_peak if dom == "proj" else bf16_peak
+            roof = {"kernel": names[dom], "bound": "tensor", "achieved": e["tensor_tflops"],
+                    "peak": pk, "unit": "TFLOP/s", "frac": e["tensor_frac"]}
+        else:
+            roof = {"kernel": names[dom], "bound": "hbm", "achieved": e["hbm_gbs"],
+                    "peak": hbm_peak, "unit": "GB/s", "frac": e["hbm_frac"]}
+        roof.update({"peak_source": peak_kind + (" (int8 = 2x bf16)" if dom == "proj" else ""),
+                     "traffic": None, "kernel_ms_per_step": e["ms_per_step"],
+                     "share_of_step": e["share_of_step"]})
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     cpu = None
@@ -343,7 +365,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roof,
-            "kernel_ms_per_step": breakdown,
+            "kernels": kernels,
             "cpu_baseline": cpu,
             "clocks": clk,
         }

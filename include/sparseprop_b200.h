@@ -60,23 +60,26 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
  *     u, a    [B][n] fp64 state, carried across chunks (zero at t=0)
  *     pass 0 (A): zbar, zsum [B][n] fp64 carried; raster [B][T][ceil(n/32)] bit-packed
  *                 spikes (optional, may be NULL).
- *     pass 1 (B): wsig [B][n] = W_out^T g; ctab[T] readout gains c_t; psi2 [B][n] carry;
- *                 coef [B][Tc][coef_ld] float2 (A'_t, Q'_t) for K6 (ALIF only; rows
- *                 i >= n are never written -- keep them zero);
- *                 lp_hi/lp_lo [n][B*Tc] bf16 split of L_t psi_t, K index b*Tc+s. */
-int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int len, int t0, int T,
-                      double alpha, double theta, double slope, double beta, double rho,
+ *     pass 1 (B): wsig [B][n] = W_out^T g; ctab[T] readout gains c_t.  A backward scan
+ *                 over the chunk emits, K-major over (sample b, row rho < KR):
+ *                   c_hi/c_lo [n][B*KR]  gradient coefficient C_rho (bf16 hi/lo split)
+ *                   w_hi/w_lo [n][B*KR]  ALIF trace-carry coefficient W_rho
+ *                   mdt [B][n] float2    ALIF (M, Dt) of the chunk
+ *                 psi_scratch [B][KR+1][n] fp32 working buffer of the scan.
+ *                 (forward.cu header has the algebra).  KR >= Tc+1, KR % 8 == 0. */
+int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR, int len, int t0,
+                      int T, double alpha, double theta, double slope, double beta, double rho,
                       double kappa, int reset, int alif, double* u, double* a, double* zbar,
                       double* zsum, uint32_t* raster, const float* wsig, const double* ctab,
-                      float* psi2, float* coef, int coef_ld, void* lp_hi, void* lp_lo,
-                      cudaStream_t stream);
+                      void* c_hi, void* c_lo, void* w_hi, void* w_lo, float* mdt,
+                      float* psi_scratch, cudaStream_t stream);
 
 /* K4  Presynaptic filter xbar_t = alpha*xbar_{t-1} + x_t (the factorised LIF trace G_u,
  *     gradients.py:89-94 with H_I = alpha, F rows = x_t; test_gradients.py:81-91).
- *     xbar_state [B][k] fp64 carry; xf [B][Tc+1][k_pad] fp32 (row 0 = xbar_{t0-1});
- *     xh/xl [k_pad][B*Tc] bf16 hi/lo split (GEMM operand, K index b*Tc+s). */
-int spb_xbar_chunk(const uint8_t* x, long long stride_b, int B, int k, int k_pad, int Tc,
-                   int len, double alpha, double* xbar_state, float* xf, void* xh, void* xl,
+ *     xbar_state [B][k] fp64 carry; xh/xl [k_rows][B*KR] bf16 hi/lo split, K-major:
+ *     row rho = 0 holds xbar_{t0-1}, rho = s+1 holds xbar_{t0+s}; zero elsewhere. */
+int spb_xbar_chunk(const uint8_t* x, long long stride_b, int B, int k, int k_rows, int KR,
+                   int len, double alpha, double* xbar_state, void* xh, void* xl,
                    cudaStream_t stream);
 
 /* K3  Readout + loss: s_b = W_out zsum_b, loss_b = CE(s_b, y_b), g_b = softmax - onehot,
@@ -91,12 +94,13 @@ int spb_readout_loss(const double* wout, const double* zsum, const long long* la
 int spb_readout_grad(const double* g, const double* zsum, int B, int n, int m, double* gwo,
                      cudaStream_t stream);
 
-/* K5  Factorised gradient GEMM on tcgen05 tensor cores (TMA-fed, bf16 hi/lo split, fp32
+/* K5  Chunk gradient GEMM on tcgen05 tensor cores (TMA-fed, bf16 hi/lo split, fp32
  *     TMEM accumulation), split-K over `splits` CTAs per 128x128 tile:
  *       partial[z][i][j] = sum_{K in split z} (Ah+Al)[i][K] (Bh+Bl)[j][K]  (i<M, j<ldp)
  *     at partial + z*slice_stride (row stride ldp); every slice is written.
- *     Replaces the xbar/xsum n x k accumulation of gradients.py:165-172,180 for the
- *     factorisable LIF part G_u = 1 (x) xbar.  A* [M][K], B* [N_rows][K] bf16 K-major,
+ *     With A = C (K1) and B = xbar (K4) this is every intra-chunk gradient term: the
+ *     factorisable LIF part G_u = 1 (x) xbar and the intra-chunk ALIF part.  Replaces the
+ *     xbar/xsum n x k accumulation of gradients.py:165-172,180.  A* [M][K], B* [N_rows][K],
  *     16-byte aligned, K % 8 == 0. */
 int spb_grad_gemm_partials(const void* ah, const void* al, const void* bh, const void* bl, int M,
                            int N_rows, int K, int splits, float* partial, int ldp,
@@ -106,15 +110,17 @@ int spb_grad_gemm_partials(const void* ah, const void* al, const void* bh, const
 int spb_grad_gemm_simt(const void* ah, const void* al, const void* bh, const void* bl, int M,
                        int N, int K, double* grad, int ldg, cudaStream_t stream);
 
-/* K6  ALIF adaptation-trace chunk: eps~ state [B][n_pad][k_pad] fp32 (rescaled trace,
- *     see elig.cu), coef [B][Tc][n_pad] float2 from K1 (coef_ld = n_pad), xf from K4;
- *     Tc in {8,16,32,64}; TMA-pipelined over samples; the batch is split in `splits` contiguous
- *     ranges, each writing partial[split][n_pad][k_pad].  load_eps=0 on the first
- *     chunk (eps=0), store_eps=0 on the last.  Replaces the ALIF G_a block of
- *     eprop_trace_update (gradients.py:89-94) and x_step (gradients.py:165-167). */
-int spb_alif_elig_chunk(const float* coef, const float* xf, float* eps, float* partial, int B,
-                        int n, int n_pad, int k_pad, int Tc, int len, int splits, int load_eps,
-                        int store_eps, cudaStream_t stream);
+/* K6  ALIF adaptation trace carried across chunks on tcgen05 tensor cores (elig.cu):
+ *       E_end[b,i,:] = Dt[b,i] E0[b,i,:] + sum_rho W_rho[b,i] xbar_rho[b,:]   (if do_mma)
+ *       partial[z][i][j] = sum_{b in split z} M[b,i] E0[b,i,j]
+ *     eps [B][n_pad][ke] fp32 (E0 read if load_eps, E_end written if store_eps), w*/x* the
+ *     K1/K4 operands (K = B*KR), mdt from K1; partial [splits][n_pad][kp].
+ *     n_pad % 128 == 0, kp % 128 == 0, ke % 4 == 0, KR % 64 == 0.  Replaces the ALIF G_a
+ *     block of eprop_trace_update (gradients.py:89-94) and x_step (gradients.py:165-167). */
+int spb_alif_carry_chunk(const void* wh, const void* wl, const void* xh, const void* xl,
+                         const float* mdt, float* eps, float* partial, int B, int n, int n_pad,
+                         int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
+                         int store_eps, cudaStream_t stream);
 
 /* grad[i][j] += sum_{s<splits} partial[s][i][j] in fixed order (fp64). */
 int spb_reduce_partials(const float* partial, int splits, int n, int n_pad, int k_pad,

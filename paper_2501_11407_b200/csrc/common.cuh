@@ -51,10 +51,25 @@ __device__ __forceinline__ double surrogate_grad_f64(double d, double slope) {
   return __ddiv_rn(1.0, __dmul_rn(t, t));
 }
 
+// Same surrogate in fp32 for the gradient path (psi only scales fp32 eligibilities).
+__device__ __forceinline__ float surrogate_grad_f32(float d, float slope) {
+  const float t = fmaf(slope, fabsf(d), 1.0f);
+  return __frcp_rn(t * t);
+}
+
 // bf16 hi/lo split of an fp32 value: x ~= hi + lo with |x - hi - lo| <= 2^-16 |x|.
 __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
   hi = __float2bfloat16_rn(x);
   lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+// Paired split: (hi, lo) bf16x2 words of two fp32 values (cvt.rn.bf16x2.f32).
+__device__ __forceinline__ void split_bf16x2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+  const float2 hf = __bfloat1622float2(h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
 }  // namespace spb

@@ -1,157 +1,259 @@
-// Eligibility-trace gradient kernels (sm_100a):
-//   K6  spb_alif_elig_chunk  -- ALIF per-synapse adaptation trace eps_a swept over a
-//                               time chunk with the synapse tile held in registers
-//   --  spb_reduce_partials  -- fixed-order batch-split reduction into the fp64 gradient
+// Eligibility-trace kernels of the ALIF adaptation trace eps_a (sm_100a):
+//   K6  spb_alif_carry_chunk -- per-synapse trace carried across time chunks on tcgen05
+//                               tensor cores, with the inter-chunk gradient term fused
+//   --  spb_reduce_partials  -- fixed-order split reduction into the fp64 gradient
 //   K5s spb_grad_gemm_simt   -- CUDA-core reference of the factorised GEMM (tests only)
 //
 // Reference: the ALIF block of eprop_trace_update (gradients.py:89-94, H_I block
 // [[alpha,0],[psi^-, rho - beta psi^-]] from neurons.py:266-273 / test_neurons.py:144-155)
 // and the eligibility filter x_step = psi (G_u - beta G_a) (gradients.py:165-172).
 //
-// Rescaled trace.  With eps_t = A_t eps_{t-1} + P_t xbar_{t-1}, A_t = rho - beta psi_{t-1},
-// P_t = psi_{t-1}, the kernel carries eps~_t = eps_t / psi_{t-1}:
-//     eps~_t = A'_t eps~_{t-1} + xbar_{t-1},      A'_t = A_t psi_{t-2} / psi_{t-1}
-//     grad  += Q'_t eps~_t,                        Q'_t = -beta L_t psi_t psi_{t-1}
-// i.e. exactly two FMAs per synapse-sample-step (one FFMA2 per synapse pair per step),
-// instead of FMUL+FFMA+FFMA for the literal form.  All terms of eps~ are non-negative for
-// non-negative inputs (A' > 0 when rho > beta), so the rescaling adds no cancellation.
+// The trace eps[b][i][j] (= G_a) is the only per-synapse state.  With the chunk
+// coefficients of K1 (forward.cu: W_r, M, Dt) a whole chunk of L steps is
+//     E_end[b,i,:] = Dt[b,i] E0[b,i,:] + sum_r W_r[b,i] xbar_{r-1}[b,:]     (per-sample GEMM, K = L)
+//     grad[i,:]   += sum_b M[b,i] E0[b,i,:]                               (inter-chunk term)
+// while every intra-chunk contribution goes through the factorised GEMM K5.  eps is read
+// once and written once per chunk (8 bytes per synapse per chunk), and the per-step FMA
+// work of the literal recursion moves onto the tensor cores.
+//
+// Kernel structure (one 128-neuron x 128-input tile per CTA, a contiguous sample range per
+// blockIdx.z):  warp 0 TMA producer (W hi/lo, xbar hi/lo K-blocks, 3-stage ring), warp 1
+// TMEM owner + single-thread tcgen05.mma issuer (bf16 hi/lo split: hi*hi + hi*lo + lo*hi,
+// fp32 accumulation in one of two TMEM buffers), warps 2-9 epilogue: tcgen05.ld of the
+// sample's product, eps load/update/store, gradient tile in registers across samples.
 #include "tma.cuh"
 
 namespace spb {
+namespace carry {
 
-constexpr int K6_TI = 128;   // neurons per CTA tile
-constexpr int K6_TJ = 64;    // inputs per CTA tile
-constexpr int K6_THREADS = 256;
-constexpr int K6_MAX_TC = 64;
+constexpr int BM = 128, BN = 128, BK = 64, STAGES = 3;
+constexpr int TILE = BM * BK * 2;  // 16 KB (BN == BM)
+constexpr int STAGE = 4 * TILE;
+constexpr int EPI_WARPS = 16;  // 4 TMEM lane quarters x 4 column groups of 32
+constexpr int THREADS = 64 + EPI_WARPS * 32;
+constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
 
-// Shared-memory stage for one sample: eps~ tile, (A',Q') rows and xbar rows of the chunk.
-template <int TC>
-struct K6Stage {
-  static constexpr int EPS_BYTES = K6_TI * K6_TJ * 4;              // 32 KB
-  static constexpr int COEF_BYTES = TC * K6_TI * 8;                // TC KB
-  static constexpr int XB_BYTES = ((TC + 1) * K6_TJ * 4 + 127) / 128 * 128;
-  static constexpr int BYTES = EPS_BYTES + COEF_BYTES + XB_BYTES;
-};
+__device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&r)[32]) {
+  uint32_t* v = reinterpret_cast<uint32_t*>(r);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 
-// TMA-pipelined sweep.  Each CTA owns a 128x64 synapse tile and a contiguous range of
-// samples; per sample, one elected thread TMA-loads the sample's eps~ tile, its chunk of
-// (A',Q') and xbar rows into a shared-memory stage (STAGES-deep ring), the 256 threads
-// sweep the chunk from registers (4 neurons x 8 inputs each, FFMA2), and write eps~ back
-// with plain stores.  The gradient tile stays in registers across the sample loop.
-template <int TC, int STAGES>
-__global__ void __launch_bounds__(K6_THREADS, 1) alif_elig_tma_kernel(
-    const __grid_constant__ CUtensorMap tm_eps, const __grid_constant__ CUtensorMap tm_coef,
-    const __grid_constant__ CUtensorMap tm_xb, float* __restrict__ eps,
-    float* __restrict__ partial, int B, int n_pad, int k_pad, int len, int b_per_split,
-    int load_eps, int store_eps) {
-  using S = K6Stage<TC>;
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&r)[16]) {
+  uint32_t* v = reinterpret_cast<uint32_t*>(r);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    alif_carry_kernel(const __grid_constant__ CUtensorMap tm_wh, const __grid_constant__ CUtensorMap tm_wl,
+                      const __grid_constant__ CUtensorMap tm_xh, const __grid_constant__ CUtensorMap tm_xl,
+                      const float2* __restrict__ mdt, float* __restrict__ eps,
+                      float* __restrict__ partial, int B, int n, int n_pad, int ke, int kp, int KR,
+                      int b_per_split, int do_mma, int load_eps, int store_eps) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
-                                             ~uintptr_t(127));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::BYTES);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int li = lane >> 3, lj = lane & 7;
-  const int j0 = blockIdx.x * K6_TJ, i0 = blockIdx.y * K6_TI;
-  const int b_begin = blockIdx.z * b_per_split;
-  const int nb = max(0, min(B, b_begin + b_per_split) - b_begin);
-  const int row0 = warp * 16 + li * 4;
-  const int cA = lj * 4, cB = 32 + lj * 4;
-  const uint32_t stage_bytes =
-      (load_eps ? S::EPS_BYTES : 0) + S::COEF_BYTES + (TC + 1) * K6_TJ * 4;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&full[s]), 1);
-    mbar_fence_init();
-    tma_prefetch_desc(&tm_eps);
-    tma_prefetch_desc(&tm_coef);
-    tma_prefetch_desc(&tm_xb);
-  }
-  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
+  const int b0 = blockIdx.z * b_per_split;
+  const int nb = max(0, min(B, b0 + b_per_split) - b0);
+  const int nkb = KR / BK;
 
-  auto issue = [&](int it) {
-    const int s = it % STAGES;
-    const int b = b_begin + it;
-    uint8_t* st = smem + s * S::BYTES;
-    const uint32_t fb = smem_u32(&full[s]);
-    mbar_expect_tx(fb, stage_bytes);
-    if (load_eps) tma_load_2d(smem_u32(st), &tm_eps, fb, j0, b * n_pad + i0);
-    tma_load_2d(smem_u32(st + S::EPS_BYTES), &tm_coef, fb, 2 * i0, b * TC);
-    tma_load_2d(smem_u32(st + S::EPS_BYTES + S::COEF_BYTES), &tm_xb, fb, j0, b * (TC + 1));
-  };
-  if (tid == 0)
-    for (int it = 0; it < min(nb, STAGES - 1); ++it) issue(it);
-
-  float2 g2[4][4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int p = 0; p < 4; ++p) g2[r][p] = make_float2(0.f, 0.f);
-
-  for (int it = 0; it < nb; ++it) {
-    const int s = it % STAGES;
-    if (tid == 0 && it + STAGES - 1 < nb) issue(it + STAGES - 1);
-    mbar_wait(smem_u32(&full[s]), (it / STAGES) & 1);
-    const uint8_t* st = smem + s * S::BYTES;
-    const float* es = reinterpret_cast<const float*>(st);
-    const float2* cs = reinterpret_cast<const float2*>(st + S::EPS_BYTES);
-    const float* xs = reinterpret_cast<const float*>(st + S::EPS_BYTES + S::COEF_BYTES);
-    float2 e2[4][4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (load_eps) {
-        const float4 va = *reinterpret_cast<const float4*>(es + (row0 + r) * K6_TJ + cA);
-        const float4 vb = *reinterpret_cast<const float4*>(es + (row0 + r) * K6_TJ + cB);
-        e2[r][0] = make_float2(va.x, va.y);
-        e2[r][1] = make_float2(va.z, va.w);
-        e2[r][2] = make_float2(vb.x, vb.y);
-        e2[r][3] = make_float2(vb.z, vb.w);
-      } else {
-#pragma unroll
-        for (int p = 0; p < 4; ++p) e2[r][p] = make_float2(0.f, 0.f);
-      }
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
     }
-#pragma unroll 2
-    for (int ss = 0; ss < len; ++ss) {
-      const float4 xa = *reinterpret_cast<const float4*>(xs + ss * K6_TJ + cA);
-      const float4 xb = *reinterpret_cast<const float4*>(xs + ss * K6_TJ + cB);
-      const float2 x2[4] = {make_float2(xa.x, xa.y), make_float2(xa.z, xa.w),
-                            make_float2(xb.x, xb.y), make_float2(xb.z, xb.w)};
-      const float4 c01 = *reinterpret_cast<const float4*>(cs + ss * K6_TI + row0);
-      const float4 c23 = *reinterpret_cast<const float4*>(cs + ss * K6_TI + row0 + 2);
-      const float Ar[4] = {c01.x, c01.z, c23.x, c23.z};
-      const float Qr[4] = {c01.y, c01.w, c23.y, c23.w};
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const float2 A2 = make_float2(Ar[r], Ar[r]);
-        const float2 Q2 = make_float2(Qr[r], Qr[r]);
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          e2[r][p] = ffma2(A2, e2[r][p], x2[p]);
-          g2[r][p] = ffma2(Q2, e2[r][p], g2[r][p]);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(&tfull[a]), 1);
+      mbar_init(smem_u32(&tempty[a]), EPI_WARPS);
+    }
+    mbar_fence_init();
+    if (do_mma) {
+      tma_prefetch_desc(&tm_wh);
+      tma_prefetch_desc(&tm_wl);
+      tma_prefetch_desc(&tm_xh);
+      tma_prefetch_desc(&tm_xl);
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && do_mma) {
+      int it = 0;
+      for (int lb = 0; lb < nb; ++lb) {
+        const int kbase = (b0 + lb) * KR;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(smem_u32(&empty[s]), ((it / STAGES) & 1) ^ 1);
+          const uint32_t st = smem_u32(smem + s * STAGE);
+          const uint32_t fb = smem_u32(&full[s]);
+          mbar_expect_tx(fb, STAGE);
+          tma_load_2d(st, &tm_wh, fb, kbase + kb * BK, i0);
+          tma_load_2d(st + TILE, &tm_wl, fb, kbase + kb * BK, i0);
+          tma_load_2d(st + 2 * TILE, &tm_xh, fb, kbase + kb * BK, j0);
+          tma_load_2d(st + 3 * TILE, &tm_xl, fb, kbase + kb * BK, j0);
         }
       }
     }
-    if (store_eps) {
-      float* ebase = eps + ((long long)(b_begin + it) * n_pad + i0 + row0) * k_pad + j0;
+  } else if (warp == 1) {
+    if (lane == 0 && do_mma) {
+      int it = 0;
+      for (int lb = 0; lb < nb; ++lb) {
+        const int a = lb & 1;
+        mbar_wait(smem_u32(&tempty[a]), ((lb >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem_base + (uint32_t)(a * BN);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(smem_u32(&full[s]), (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t st = smem_u32(smem + s * STAGE);
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        *reinterpret_cast<float4*>(ebase + (long long)r * k_pad + cA) =
-            make_float4(e2[r][0].x, e2[r][0].y, e2[r][1].x, e2[r][1].y);
-        *reinterpret_cast<float4*>(ebase + (long long)r * k_pad + cB) =
-            make_float4(e2[r][2].x, e2[r][2].y, e2[r][3].x, e2[r][3].y);
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint32_t off = kk * 32;
+            const uint64_t dwh = desc_k_sw128(st + off), dwl = desc_k_sw128(st + TILE + off);
+            const uint64_t dxh = desc_k_sw128(st + 2 * TILE + off),
+                           dxl = desc_k_sw128(st + 3 * TILE + off);
+            mma_bf16(d, dwh, dxh, (kb | kk) ? 1u : 0u);
+            mma_bf16(d, dwh, dxl, 1u);
+            mma_bf16(d, dwl, dxh, 1u);
+          }
+          commit(smem_u32(&empty[s]));
+        }
+        commit(smem_u32(&tfull[a]));
       }
     }
-    __syncthreads();  // stage s may be refilled by the next issue
-  }
-  float* pbase = partial + ((long long)blockIdx.z * n_pad + i0 + row0) * k_pad + j0;
+  } else {
+    const int q = warp & 3;            // TMEM lane quarter of this warp
+    const int cg = (warp - 2) >> 2;    // 32-column group
+    const int r = q * 32 + lane;       // tile-local neuron row
+    const int i = i0 + r;
+    const bool vi = i < n;
+    const int c0 = j0 + cg * 32;       // first input column of this thread
+    float g[32];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    *reinterpret_cast<float4*>(pbase + (long long)r * k_pad + cA) =
-        make_float4(g2[r][0].x, g2[r][0].y, g2[r][1].x, g2[r][1].y);
-    *reinterpret_cast<float4*>(pbase + (long long)r * k_pad + cB) =
-        make_float4(g2[r][2].x, g2[r][2].y, g2[r][3].x, g2[r][3].y);
+    for (int c = 0; c < 32; ++c) g[c] = 0.f;
+    for (int lb = 0; lb < nb; ++lb) {
+      const int b = b0 + lb;
+      const int a = lb & 1;
+      float* erow = eps + ((long long)b * n_pad + i) * ke + c0;
+      // issue the eps loads first: they do not depend on the tensor-core product
+      float4 e0[8];
+#pragma unroll
+      for (int v4 = 0; v4 < 8; ++v4) {
+        e0[v4] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (load_eps && vi && c0 + v4 * 4 < ke) e0[v4] = *reinterpret_cast<const float4*>(erow + v4 * 4);
+      }
+      const float2 md = vi ? mdt[(long long)b * n + i] : make_float2(0.f, 0.f);
+      if (do_mma) {
+        mbar_wait(smem_u32(&tfull[a]), (lb >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+      float D[16];
+      if (do_mma) {
+        tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + cg * 32 + hf * 16), D);
+        if (hf == 1) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) arrive(smem_u32(&tempty[a]));
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) D[c] = 0.f;
+      }
+#pragma unroll
+      for (int v4 = hf * 4; v4 < hf * 4 + 4; ++v4) {
+        g[v4 * 4 + 0] = fmaf(md.x, e0[v4].x, g[v4 * 4 + 0]);
+        g[v4 * 4 + 1] = fmaf(md.x, e0[v4].y, g[v4 * 4 + 1]);
+        g[v4 * 4 + 2] = fmaf(md.x, e0[v4].z, g[v4 * 4 + 2]);
+        g[v4 * 4 + 3] = fmaf(md.x, e0[v4].w, g[v4 * 4 + 3]);
+        if (store_eps && vi && c0 + v4 * 4 < ke) {
+          float4 en;
+          const int dv = (v4 - hf * 4) * 4;
+          en.x = fmaf(md.y, e0[v4].x, D[dv + 0]);
+          en.y = fmaf(md.y, e0[v4].y, D[dv + 1]);
+          en.z = fmaf(md.y, e0[v4].z, D[dv + 2]);
+          en.w = fmaf(md.y, e0[v4].w, D[dv + 3]);
+          *reinterpret_cast<float4*>(erow + v4 * 4) = en;
+        }
+      }
+      }
+    }
+    if (vi) {
+      float* prow = partial + ((long long)blockIdx.z * n_pad + i) * kp + c0;
+#pragma unroll
+      for (int v4 = 0; v4 < 8; ++v4)
+        if (c0 + v4 * 4 < kp)
+          *reinterpret_cast<float4*>(prow + v4 * 4) =
+              make_float4(g[v4 * 4], g[v4 * 4 + 1], g[v4 * 4 + 2], g[v4 * 4 + 3]);
+    }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
 }
+
+}  // namespace carry
 
 __global__ void reduce_partials_kernel(const float* __restrict__ partial, int S, int n, int n_pad,
                                        int k_pad, double* __restrict__ grad) {
@@ -221,48 +323,42 @@ using namespace spb;
 
 extern "C" {
 
-int spb_alif_elig_chunk(const float* coef, const float* xf, float* eps, float* partial, int B,
-                        int n, int n_pad, int k_pad, int Tc, int len, int splits, int load_eps,
-                        int store_eps, cudaStream_t stream) {
-  SPB_CHECK_ARG(coef && xf && eps && partial, "spb_alif_elig_chunk: null pointer");
-  SPB_CHECK_ARG(n_pad % K6_TI == 0 && k_pad % K6_TJ == 0 && n <= n_pad,
-                "spb_alif_elig_chunk: n_pad must be a multiple of %d and k_pad of %d", K6_TI,
-                K6_TJ);
-  SPB_CHECK_ARG(Tc == 8 || Tc == 16 || Tc == 32 || Tc == 64,
-                "spb_alif_elig_chunk: chunk length must be 8, 16, 32 or 64 (got %d)", Tc);
-  SPB_CHECK_ARG(B > 0 && splits > 0 && splits <= B && len >= 0 && len <= Tc,
-                "spb_alif_elig_chunk: bad sizes B=%d splits=%d len=%d Tc=%d", B, splits, len, Tc);
-  CUtensorMap m_eps, m_coef, m_xb;
-  const bool ok =
-      make_tmap_2d(&m_eps, eps, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, k_pad, (uint64_t)B * n_pad,
-                   (uint64_t)k_pad * 4, K6_TJ, K6_TI, CU_TENSOR_MAP_SWIZZLE_NONE) &&
-      make_tmap_2d(&m_coef, coef, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, 2 * (uint64_t)n_pad,
-                   (uint64_t)B * Tc, (uint64_t)n_pad * 8, 2 * K6_TI, Tc,
-                   CU_TENSOR_MAP_SWIZZLE_NONE) &&
-      make_tmap_2d(&m_xb, xf, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, k_pad, (uint64_t)B * (Tc + 1),
-                   (uint64_t)k_pad * 4, K6_TJ, Tc + 1, CU_TENSOR_MAP_SWIZZLE_NONE);
-  if (!ok) {
-    set_error("spb_alif_elig_chunk: cuTensorMapEncodeTiled failed");
-    return 3;
+int spb_alif_carry_chunk(const void* wh, const void* wl, const void* xh, const void* xl,
+                         const float* mdt, float* eps, float* partial, int B, int n, int n_pad,
+                         int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
+                         int store_eps, cudaStream_t stream) {
+  SPB_CHECK_ARG(mdt && eps && partial, "spb_alif_carry_chunk: null pointer");
+  SPB_CHECK_ARG(!do_mma || (wh && wl && xh && xl), "spb_alif_carry_chunk: missing GEMM operands");
+  SPB_CHECK_ARG(n_pad % carry::BM == 0 && n <= n_pad && kp % carry::BN == 0 && kp >= k &&
+                    ke >= k && ke % 4 == 0 && KR % carry::BK == 0,
+                "spb_alif_carry_chunk: bad padding (n_pad %% 128, kp %% 128, ke %% 4, KR %% 64)");
+  SPB_CHECK_ARG(B > 0 && splits > 0 && splits <= B, "spb_alif_carry_chunk: bad split");
+  SPB_CHECK_ARG(!(store_eps && !do_mma), "spb_alif_carry_chunk: storing eps needs the GEMM");
+  CUtensorMap mwh{}, mwl{}, mxh{}, mxl{};
+  if (do_mma) {
+    const uint64_t K = (uint64_t)B * KR;
+    const bool ok =
+        make_tmap_2d(&mwh, wh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, n, K * 2, carry::BK,
+                     carry::BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
+        make_tmap_2d(&mwl, wl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, n, K * 2, carry::BK,
+                     carry::BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
+        make_tmap_2d(&mxh, xh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, kp, K * 2, carry::BK,
+                     carry::BN, CU_TENSOR_MAP_SWIZZLE_128B) &&
+        make_tmap_2d(&mxl, xl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, kp, K * 2, carry::BK,
+                     carry::BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (!ok) {
+      set_error("spb_alif_carry_chunk: cuTensorMapEncodeTiled failed");
+      return 3;
+    }
   }
   const int bps = ceil_div(B, splits);
-  dim3 grid(k_pad / K6_TJ, n_pad / K6_TI, splits);
-#define SPB_K6_LAUNCH(TC, ST)                                                                   \
-  do {                                                                                          \
-    auto kfn = alif_elig_tma_kernel<TC, ST>;                                                    \
-    const int smem = ST * K6Stage<TC>::BYTES + 128 + 64;                                       \
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);               \
-    kfn<<<grid, K6_THREADS, smem, stream>>>(m_eps, m_coef, m_xb, eps, partial, B, n_pad, k_pad, \
-                                            len, bps, load_eps, store_eps);                     \
-  } while (0)
-  switch (Tc) {
-    case 8: SPB_K6_LAUNCH(8, 4); break;
-    case 16: SPB_K6_LAUNCH(16, 3); break;
-    case 32: SPB_K6_LAUNCH(32, 3); break;
-    default: SPB_K6_LAUNCH(64, 2); break;
-  }
-#undef SPB_K6_LAUNCH
-  SPB_CHECK_LAUNCH("alif_elig");
+  cudaFuncSetAttribute(carry::alif_carry_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       carry::SMEM);
+  dim3 grid(kp / carry::BN, n_pad / carry::BM, splits);
+  carry::alif_carry_kernel<<<grid, carry::THREADS, carry::SMEM, stream>>>(
+      mwh, mwl, mxh, mxl, reinterpret_cast<const float2*>(mdt), eps, partial, B, n, n_pad, ke, kp,
+      KR, bps, do_mma, load_eps, store_eps);
+  SPB_CHECK_LAUNCH("alif_carry");
   return 0;
 }
 

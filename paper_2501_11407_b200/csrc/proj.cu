@@ -82,6 +82,192 @@ __device__ __forceinline__ double pow2(int e) {  // 2^e for -1022 <= e <= 1023
   return __longlong_as_double((long long)(e + 1023) << 52);
 }
 
+// Epilogue of one 128-row x 32-neuron tile: pull the P slice accumulators of this thread's
+// row from TMEM, recombine them exactly in int64 and write the fp64 current.
+template <int P>
+__device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int* __restrict__ sexp,
+                                                   double* __restrict__ out, int M, int n, int row,
+                                                   int i0, uint32_t tempty_bar, int lane) {
+  long long g0[NT], g1[NT];
+  int32_t r[32];
+#pragma unroll
+  for (int c = 0; c < NT; ++c) g0[c] = g1[c] = 0;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    tmem_ld32(tbase + p * NT, r);
+#pragma unroll
+    for (int c = 0; c < NT; ++c) {
+      if (p < 3) g0[c] = g0[c] * 128 + r[c];
+      else g1[c] = g1[c] * 128 + r[c];
+    }
+  }
+  // the TMEM buffer is free once every epilogue warp has pulled its lanes
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) mbar_arrive(tempty_bar);
+  if (row < M) {
+    double* orow = out + (long long)row * n + i0;
+#pragma unroll
+    for (int c = 0; c < NT; c += 2) {
+      double v[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = i0 + c + h;
+        const int se = (i < n) ? __ldg(sexp + i) : 0;
+        // I = g0 * 2^(s-6-14) + g1 * 2^(s-6-7(P-1))  (both conversions exact)
+        v[h] = fma((double)g0[c + h], pow2(se - 20), (double)g1[c + h] * pow2(se - 6 - 7 * (P - 1)));
+      }
+      if (i0 + c + 1 < n) {
+        *reinterpret_cast<double2*>(orow + c) = make_double2(v[0], v[1]);
+      } else if (i0 + c < n) {
+        orow[c] = v[0];
+      }
+    }
+  }
+}
+
+// W-resident variant (Kpad <= 768): each persistent CTA walks a contiguous range of tiles
+// in neuron-major order, keeps the sliced weights of its current neuron tile (all K) in
+// shared memory and streams only the spike tiles -- operand traffic drops from
+// (m_tiles x |W|) + (n_tiles x |x|) to (#CTAs x |W tile|) + (n_tiles x |x|).
+template <int P, int XS>
+struct ResCfg {
+  static constexpr int N = P * NT;
+  static constexpr int WBLK = N * BK;                    // one K-block of all slices
+  static constexpr int MAXKB = 6;                        // Kpad <= 768
+  static constexpr int W_BYTES = MAXKB * WBLK;
+  static constexpr int SMEM = W_BYTES + XS * TILE_A + 1024 + 256;
+};
+
+template <int P, int XS>
+__global__ void __launch_bounds__(THREADS, 1)
+    input_proj_wres_kernel(const __grid_constant__ CUtensorMap tm_x,
+                           const __grid_constant__ CUtensorMap tm_w, const int* __restrict__ sexp,
+                           double* __restrict__ out, int M, int n, int n_pad32, int nkb) {
+  using C = ResCfg<P, XS>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* wsm = smem;                        // [nkb][P*NT rows][128 B]
+  uint8_t* xsm = smem + C::W_BYTES;           // [XS][128 rows][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xsm + XS * TILE_A);
+  uint64_t* xfull = bars;
+  uint64_t* xempty = bars + XS;
+  uint64_t* tfull = bars + 2 * XS;
+  uint64_t* tempty = bars + 2 * XS + 2;
+  uint64_t* wfull = bars + 2 * XS + 4;
+  uint64_t* wempty = bars + 2 * XS + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * XS + 6);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m_tiles = (M + BM - 1) / BM;
+  const int n_tiles = (n + NT - 1) / NT;
+  const long long total = (long long)m_tiles * n_tiles;
+  const int t_begin = (int)(total * blockIdx.x / gridDim.x);
+  const int t_end = (int)(total * (blockIdx.x + 1) / gridDim.x);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < XS; ++s) {
+      mbar_init(smem_u32(&xfull[s]), 1);
+      mbar_init(smem_u32(&xempty[s]), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(&tfull[a]), 1);
+      mbar_init(smem_u32(&tempty[a]), 4);
+    }
+    mbar_init(smem_u32(wfull), 1);
+    mbar_init(smem_u32(wempty), 1);
+    mbar_fence_init();
+    tma_prefetch_desc(&tm_x);
+    tma_prefetch_desc(&tm_w);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0, cur_nt = -1, wl = 0;
+      for (int t = t_begin; t < t_end; ++t) {
+        const int nt = t / m_tiles, mt = t % m_tiles;
+        if (nt != cur_nt) {  // (re)load this neuron tile's weight slices, all K blocks
+          mbar_wait(smem_u32(wempty), (wl & 1) ^ 1);
+          const uint32_t fb = smem_u32(wfull);
+          mbar_expect_tx(fb, nkb * C::WBLK);
+          for (int kb = 0; kb < nkb; ++kb)
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+              tma_load_2d(smem_u32(wsm + kb * C::WBLK + p * NT * BK), &tm_w, fb, kb * BK,
+                          p * n_pad32 + nt * NT);
+          cur_nt = nt;
+          ++wl;
+        }
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % XS;
+          mbar_wait(smem_u32(&xempty[s]), ((it / XS) & 1) ^ 1);
+          const uint32_t fb = smem_u32(&xfull[s]);
+          mbar_expect_tx(fb, TILE_A);
+          tma_load_2d(smem_u32(xsm + s * TILE_A), &tm_x, fb, kb * BK, mt * BM);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int it = 0, lt = 0, cur_nt = -1, wl = 0;
+      for (int t = t_begin; t < t_end; ++t, ++lt) {
+        const int nt = t / m_tiles;
+        if (nt != cur_nt) {
+          mbar_wait(smem_u32(wfull), wl & 1);
+          cur_nt = nt;
+          ++wl;
+        }
+        const int a = lt & 1;
+        mbar_wait(smem_u32(&tempty[a]), ((lt >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dacc = tmem_base + (uint32_t)(a * 256);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % XS;
+          mbar_wait(smem_u32(&xfull[s]), (it / XS) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t xa = smem_u32(xsm + s * TILE_A);
+          const uint32_t wa = smem_u32(wsm + kb * C::WBLK);
+#pragma unroll
+          for (int kk = 0; kk < BK / 32; ++kk)
+            mma_i8(dacc, desc_k_sw128(xa + kk * 32), desc_k_sw128(wa + kk * 32), Cfg<P>::IDESC,
+                   (kb | kk) ? 1u : 0u);
+          commit(smem_u32(&xempty[s]));
+        }
+        commit(smem_u32(&tfull[a]));
+        // last tile of this neuron tile: the weight region may be refilled afterwards
+        if (t + 1 == t_end || (t + 1) / m_tiles != nt) commit(smem_u32(wempty));
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    int lt = 0;
+    for (int t = t_begin; t < t_end; ++t, ++lt) {
+      const int nt = t / m_tiles, mt = t % m_tiles;
+      const int a = lt & 1;
+      mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      proj_epilogue_tile<P>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256), sexp,
+                            out, M, n, mt * BM + q * 32 + lane, nt * NT, smem_u32(&tempty[a]),
+                            lane);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
 template <int P>
 __global__ void __launch_bounds__(THREADS, 1)
     input_proj_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
@@ -175,45 +361,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int a = lt & 1;
       mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256);
-      long long g0[NT], g1[NT];
-      int32_t r[32];
-#pragma unroll
-      for (int c = 0; c < NT; ++c) g0[c] = g1[c] = 0;
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        tmem_ld32(tbase + p * NT, r);
-#pragma unroll
-        for (int c = 0; c < NT; ++c) {
-          if (p < 3) g0[c] = g0[c] * 128 + r[c];
-          else g1[c] = g1[c] * 128 + r[c];
-        }
-      }
-      // TMEM stage a is free once every epilogue warp has pulled its lanes
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&tempty[a]));
-      const int row = mt * BM + q * 32 + lane;
-      if (row < M) {
-        double* orow = out + (long long)row * n + nt * NT;
-        const int i0 = nt * NT;
-#pragma unroll
-        for (int c = 0; c < NT; c += 2) {
-          double v[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int i = i0 + c + h;
-            const int se = (i < n) ? __ldg(sexp + i) : 0;
-            // I = g0 * 2^(s-6-14) + g1 * 2^(s-6-7(P-1))  (both conversions exact)
-            v[h] = fma((double)g0[c + h], pow2(se - 20), (double)g1[c + h] * pow2(se - 6 - 7 * (P - 1)));
-          }
-          if (i0 + c + 1 < n) {
-            *reinterpret_cast<double2*>(orow + c) = make_double2(v[0], v[1]);
-          } else if (i0 + c < n) {
-            orow[c] = v[0];
-          }
-        }
-      }
+      proj_epilogue_tile<P>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256), sexp,
+                            out, M, n, mt * BM + q * 32 + lane, nt * NT, smem_u32(&tempty[a]),
+                            lane);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -319,7 +469,19 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
   const int tiles = ceil_div(M, proj::BM) * ceil_div(n, proj::NT);
   const int grid = max(1, min(tiles, sm_count > 0 ? sm_count : 148));
   const int nkb = Kpad / proj::BK;
-  if (P == 7) {
+  if (nkb <= proj::ResCfg<7, 3>::MAXKB) {  // weights of a neuron tile fit in shared memory
+    if (P == 7) {
+      auto kfn = proj::input_proj_wres_kernel<7, 3>;
+      constexpr int sm = proj::ResCfg<7, 3>::SMEM;
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      kfn<<<grid, proj::THREADS, sm, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);
+    } else {
+      auto kfn = proj::input_proj_wres_kernel<8, 2>;
+      constexpr int sm = proj::ResCfg<8, 2>::SMEM;
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      kfn<<<grid, proj::THREADS, sm, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);
+    }
+  } else if (P == 7) {
     auto kfn = proj::input_proj_kernel<7>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, proj::Cfg<7>::SMEM);
     kfn<<<grid, proj::THREADS, proj::Cfg<7>::SMEM, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);

@@ -1,22 +1,23 @@
 """Device-side e-prop engine: buffers and the chunked two-pass update.
 
-One ``EpropEngine`` owns every device buffer for a fixed problem shape
-(batch B, hidden n, inputs k, classes m, chunk length Tc) and replays the update
+One ``EpropEngine`` owns every device buffer for a fixed problem shape (batch B,
+hidden n, inputs k, classes m, chunk length Tc) and replays the update
 
-    weights                        K2s slice W into int8 digits (once per update)
-    pass A  (forward only)         for each chunk: pack x -> K2 int8 tcgen05 I = W x
-                                                  -> K1 dynamics(A)
-    readout                        K3 loss / g / w_sig ; K7 grad W_out
-    pass B  (forward + traces)     for each chunk: pack -> K2 -> K1 dynamics(B) -> K4 xbar
-                                                  -> K5 tcgen05 GEMM (L psi) x xbar
-                                                  -> K6 ALIF eps chunk (ALIF only)
-                                                  -> fixed-order partial reduce
+    weights   K2s  slice W into exact INT8 digits (once per update)
+    pass A    per chunk: pack x -> K2 INT8 tcgen05 current I = W x_t -> K1 dynamics(A)
+    readout   K3 loss / g / w_sig ; K7 grad W_out
+    pass B    per chunk: pack -> K2 -> K1 dynamics(B) + backward chunk scan -> K4 xbar
+                         -> K5 tcgen05 chunk-gradient GEMM   (all intra-chunk terms)
+                         -> K6 tcgen05 ALIF trace carry      (inter-chunk terms, ALIF)
+                         -> fixed-order reduction of the split partials
 
 which is the reference's per-sample online loop (gradients.py:157-176) restated for a
 batch: the learning signal L_t = c_t W_out^T (softmax - onehot) is only known after the
-whole sequence (gradients.py:177-182), so pass B recomputes the (deterministic)
-forward with L_t known (two-pass form).  Memory is independent of T:
-state is per (sample, neuron[, input]) and chunk buffers are sized by Tc.
+whole sequence (gradients.py:177-182), so pass B recomputes the (deterministic) forward
+with L_t known (two-pass form), and the per-synapse ALIF trace is
+carried chunk to chunk (forward.cu / elig.cu headers give the algebra).  Memory is
+independent of T: state is per (sample, neuron[, input]) and chunk buffers are sized by
+Tc.
 
 All work is enqueued on torch's current CUDA stream through the C-ABI (``_lib``); the
 engine never synchronises.  PyTorch provides allocation and streams only.
@@ -24,6 +25,7 @@ engine never synchronises.  PyTorch provides allocation and streams only.
 
 from __future__ import annotations
 
+import ctypes
 import math
 
 import numpy as np
@@ -33,10 +35,10 @@ from . import _lib
 from .errors import LabelOutOfRange, ShapeMismatch
 
 SM_COUNT_DEFAULT = 148
+CHUNKS = (63, 127, 255)  # Tc with Tc + 1 a multiple of the 64-wide K block
 
 
 def ctypes_void(p):
-    import ctypes
     return ctypes.c_void_p(p)
 
 
@@ -56,97 +58,104 @@ def readout_gains(T: int, kappa: float) -> np.ndarray:
     return c
 
 
-def _best_split(B: int, tiles: int, slots: int, min_per_split: int = 16) -> int:
-    """Batch split for K6: a divisor of B giving the best wave efficiency."""
-    best, best_eff = 1, -1.0
-    for d in range(1, B + 1):
-        if B % d or (B // d < min_per_split and d != 1):
-            continue
-        ctas = tiles * d
-        waves = math.ceil(ctas / slots)
-        eff = ctas / (waves * slots)
-        # prefer >= 2 waves' worth of CTAs for load balance, then efficiency
-        score = eff + (0.05 if ctas >= 2 * slots else 0.0)
-        if score > best_eff + 1e-9:
-            best, best_eff = d, score
+def _wave_split(tiles: int, B: int, sms: int) -> int:
+    """Number of sample ranges for K6 (one CTA per SM): the smallest split whose grid
+    fills whole waves to >= 90 %, else the best of splits <= 8 waves."""
+    best, best_eff = 1, 0.0
+    for s in range(1, B + 1):
+        ctas = tiles * s
+        waves = math.ceil(ctas / sms)
+        if waves > 8:
+            break
+        eff = ctas / (waves * sms)
+        if eff >= 0.9:
+            return s
+        if eff > best_eff + 1e-9:
+            best, best_eff = s, eff
     return best
+
+
+def default_chunk(T: int) -> int:
+    for c in CHUNKS:
+        if T <= c:
+            return c
+    return 127
 
 
 class EpropEngine:
     """Buffers + launch sequence for one problem shape on one device."""
 
     def __init__(self, n: int, k: int, m: int, B: int, *, alif: bool, w_f64: bool = False,
-                 chunk: int = 32, device=None, sm_count: int | None = None):
-        if chunk <= 0 or chunk % 8:
-            raise ValueError("chunk must be a positive multiple of 8")
-        if alif and chunk not in (8, 16, 32, 64):
-            raise ValueError("ALIF chunk length must be 8, 16, 32 or 64")
-        if k >= (1 << 24):
-            raise ShapeMismatch("k too large")
+                 chunk: int = 127, device=None, sm_count: int | None = None):
+        if chunk not in CHUNKS:
+            raise ValueError(f"chunk must be one of {CHUNKS} (Tc + 1 a multiple of 64)")
         self.lib = _lib.load()
         self.n, self.k, self.m, self.B = int(n), int(k), int(m), int(B)
+        if min(self.n, self.k, self.m, self.B) <= 0:
+            raise ShapeMismatch("n, k, m and B must be positive")
         self.alif = bool(alif)
         self.w_f64 = bool(w_f64)
         self.Tc = int(chunk)
+        self.KR = self.Tc + 1
         self.device = torch.device(device if device is not None else "cuda")
         self.n_pad = _round_up(self.n, 128)
-        self.k_pad = _round_up(self.k, 64)
+        self.kp = _round_up(self.k, 128)
+        self.ke = _round_up(self.k, 4)
         sms = sm_count or (torch.cuda.get_device_properties(self.device).multi_processor_count
                            if self.device.type == "cuda" else SM_COUNT_DEFAULT)
         self.sm_count = sms
         dev = self.device
-        f32, f64 = torch.float32, torch.float64
-        Bn, Bk = (self.B, self.n), (self.B, self.k)
-        K = self.B * self.Tc
+        f32, f64, bf16 = torch.float32, torch.float64, torch.bfloat16
+        B, n, k, m = self.B, self.n, self.k, self.m
+        Bn = (B, n)
+        K = B * self.KR
         self.K = K
         # K2 exact INT8 tensor-core projection: x chunk operand, sliced weights, current
-        self.Kpad = _round_up(self.k, 128)
-        self.n_pad32 = _round_up(self.n, 32)
+        self.Kpad = _round_up(k, 128)
+        self.n_pad32 = _round_up(n, 32)
         self.P = 8 if self.w_f64 else 7
-        self.xq = torch.zeros((self.B * self.Tc, self.Kpad), dtype=torch.uint8, device=dev)
-        self.cur = torch.empty((self.B * self.Tc, self.n), dtype=f64, device=dev)
+        self.xq = torch.zeros((B * self.Tc, self.Kpad), dtype=torch.uint8, device=dev)
+        self.cur = torch.empty((B * self.Tc, n), dtype=f64, device=dev)
         self.wq = torch.zeros((self.P, self.n_pad32, self.Kpad), dtype=torch.int8, device=dev)
-        self.sexp = torch.zeros(self.n, dtype=torch.int32, device=dev)
+        self.sexp = torch.zeros(n, dtype=torch.int32, device=dev)
         # neuron state (fp64) and readout filters
         self.u = torch.empty(Bn, dtype=f64, device=dev)
         self.a = torch.empty(Bn, dtype=f64, device=dev)
         self.zbar = torch.empty(Bn, dtype=f64, device=dev)
         self.zsum = torch.empty(Bn, dtype=f64, device=dev)
-        self.psi2 = torch.empty(Bn, dtype=f32, device=dev)
         # readout / loss
         self.wsig = torch.empty(Bn, dtype=f32, device=dev)
-        self.s = torch.empty((self.B, self.m), dtype=f64, device=dev)
-        self.loss = torch.empty(self.B, dtype=f64, device=dev)
-        self.g = torch.empty((self.B, self.m), dtype=f64, device=dev)
-        self.correct = torch.empty(self.B, dtype=torch.int32, device=dev)
-        # pass-B chunk buffers
-        # rows i >= n stay zero forever (K1 writes only real neurons; K6 TMA reads n_pad)
-        self.coef = (torch.zeros((self.B, self.Tc, self.n_pad, 2), dtype=f32, device=dev)
-                     if self.alif else None)
-        self.lp_hi = torch.empty((self.n, K), dtype=torch.bfloat16, device=dev)
-        self.lp_lo = torch.empty((self.n, K), dtype=torch.bfloat16, device=dev)
-        self.xbar_state = torch.empty(Bk, dtype=f64, device=dev)
-        self.xf = torch.empty((self.B, self.Tc + 1, self.k_pad), dtype=f32, device=dev)
-        self.xh = torch.empty((self.k_pad, K), dtype=torch.bfloat16, device=dev)
-        self.xl = torch.empty((self.k_pad, K), dtype=torch.bfloat16, device=dev)
-        # split-K / batch-split partial slices, reduced in fixed order
-        tiles5 = math.ceil(self.k_pad / 128) * math.ceil(self.n / 128)
-        nkb = math.ceil(K / 64)
-        self.splits5 = max(1, min(nkb, round(sms / tiles5)))
+        self.s = torch.empty((B, m), dtype=f64, device=dev)
+        self.loss = torch.empty(B, dtype=f64, device=dev)
+        self.g = torch.empty((B, m), dtype=f64, device=dev)
+        self.correct = torch.empty(B, dtype=torch.int32, device=dev)
+        # pass-B chunk operands (bf16 hi/lo, K-major over (sample, rho))
+        self.psi = torch.zeros((B, self.KR + 1, n), dtype=f32, device=dev)   # K1 scan scratch
+        self.c_hi = torch.empty((n, K), dtype=bf16, device=dev)
+        self.c_lo = torch.empty((n, K), dtype=bf16, device=dev)
+        self.xbar_state = torch.empty((B, k), dtype=f64, device=dev)
+        self.xh = torch.zeros((self.kp, K), dtype=bf16, device=dev)
+        self.xl = torch.zeros((self.kp, K), dtype=bf16, device=dev)
+        # split-K (K5) and sample-split (K6) partial slices, reduced in fixed order
+        tiles5 = (self.kp // 128) * math.ceil(n / 128)
+        self.splits5 = max(1, min(K // 64, round(sms / tiles5)))
         if self.alif:
-            tiles6 = (self.k_pad // 64) * (self.n_pad // 128)
-            self.splits6 = _best_split(self.B, tiles6, 2 * sms)
-            self.eps = torch.zeros((self.B, self.n_pad, self.k_pad), dtype=f32, device=dev)
+            self.w_hi = torch.empty((n, K), dtype=bf16, device=dev)
+            self.w_lo = torch.empty((n, K), dtype=bf16, device=dev)
+            self.mdt = torch.empty((B, n, 2), dtype=f32, device=dev)
+            self.eps = torch.zeros((B, self.n_pad, self.ke), dtype=f32, device=dev)
+            tiles6 = (self.kp // 128) * (self.n_pad // 128)
+            self.splits6 = _wave_split(tiles6, B, sms)
         else:
+            self.w_hi = self.w_lo = self.mdt = self.eps = None
             self.splits6 = 0
-            self.eps = None
-        self.partial = torch.empty((self.splits6 + self.splits5, self.n_pad, self.k_pad),
+        self.partial = torch.zeros((self.splits5 + self.splits6, self.n_pad, self.kp),
                                    dtype=f32, device=dev)
-        self.grad_w_acc = torch.empty((self.n, self.k_pad), dtype=f64, device=dev)
-        self.grad_wout = torch.empty((self.m, self.n), dtype=f64, device=dev)
+        self.grad_w_acc = torch.empty((n, self.kp), dtype=f64, device=dev)
+        self.grad_wout = torch.empty((m, n), dtype=f64, device=dev)
         # weights
-        self.w = torch.empty((self.n, self.k), dtype=f64 if self.w_f64 else f32, device=dev)
-        self.wout = torch.empty((self.m, self.n), dtype=f64, device=dev)
+        self.w = torch.empty((n, k), dtype=f64 if self.w_f64 else f32, device=dev)
+        self.wout = torch.empty((m, n), dtype=f64, device=dev)
         self._ctab_T = None
         self.ctab = None
         self.launches = 0
@@ -182,113 +191,6 @@ class EpropEngine:
             self._ctab_T = (T, kappa)
         return self.ctab
 
-    # ----------------------------------------------------------------------------------
-    def run(self, x: torch.Tensor, labels: torch.Tensor, *, alpha=0.95, theta=1.0, slope=10.0,
-            beta=0.8, rho=0.96, kappa=0.95, reset=False, raster: torch.Tensor | None = None,
-            stream=None, timers: dict | None = None):
-        """One full e-prop update on device-resident inputs.
-
-        x       uint8 [B, T, k] spike counts (CUDA, contiguous)
-        labels  int64 [B] (CUDA)
-        raster  optional int32 [B, T, ceil(n/32)] bit-packed spike output (pass A)
-        Results stay on device: ``grad_w_acc`` (fp64 [n, k_pad]), ``grad_wout``,
-        ``loss``, ``s`` (readout sums), ``correct``.
-        timers  optional dict; CUDA event pairs are appended per launch of the main
-                kernels under "forward", "gemm", "elig" with their chunk length.
-        """
-        if reset:
-            raise NotImplementedError(
-                "reset=True makes G_u non-factorisable (SURVEY.md 8(f)-3); not on the B200 path yet")
-        if x.dtype != torch.uint8 or x.dim() != 3 or x.shape[0] != self.B or x.shape[2] != self.k:
-            raise ShapeMismatch(f"x must be uint8 [B={self.B}, T, k={self.k}], got "
-                                f"{tuple(x.shape)} {x.dtype}")
-        if not x.is_contiguous():
-            raise ShapeMismatch("x must be contiguous")
-        T = int(x.shape[1])
-        if T <= 0:
-            raise ShapeMismatch("T must be positive")
-        lib, call = self.lib, _lib.call
-        st = ctypes_void(stream if stream is not None else self._stream())
-        if not self.alif:
-            beta_e, rho_e = 0.0, 0.0
-        else:
-            beta_e, rho_e = float(beta), float(rho)
-        B, n, k, m, Tc, K = self.B, self.n, self.k, self.m, self.Tc, self.K
-        ctab = self._gains(T, float(kappa))
-        nchunks = (T + Tc - 1) // Tc
-        strideb = T * k
-        self.launches = 0
-        v = ctypes_void
-
-        def timed(name, ln, fn, *args):
-            if timers is None:
-                return call(fn, *args)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            rc = call(fn, *args)
-            e1.record()
-            timers.setdefault(name, []).append((e0, e1, ln))
-            return rc
-
-        # ---------------- pass A ----------------
-        self.u.zero_(); self.a.zero_(); self.zbar.zero_(); self.zsum.zero_()
-        for c in range(nchunks):
-            t0 = c * Tc
-            ln = min(Tc, T - t0)
-            xp = x.data_ptr() + t0 * k
-            self._project(xp, strideb, ln, st)
-            call("spb_forward_chunk", 0, v(self.cur.data_ptr()), B, n, Tc, ln, t0, T,
-                 float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
-                 int(self.alif), v(self.u.data_ptr()), v(self.a.data_ptr()),
-                 v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
-                 v(raster.data_ptr()) if raster is not None else None,
-                 None, None, None, None, 0, None, None, st)
-            self.launches += 3
-        # ---------------- readout / loss ----------------
-        call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
-             v(labels.data_ptr()), B, n, m, v(self.s.data_ptr()), v(self.loss.data_ptr()),
-             v(self.g.data_ptr()), v(self.wsig.data_ptr()), v(self.correct.data_ptr()), st)
-        self.grad_wout.zero_()
-        call("spb_readout_grad", v(self.g.data_ptr()), v(self.zsum.data_ptr()), B, n, m,
-             v(self.grad_wout.data_ptr()), st)
-        self.launches += 2
-        # ---------------- pass B ----------------
-        self.u.zero_(); self.a.zero_(); self.psi2.fill_(1.0); self.xbar_state.zero_()
-        self.grad_w_acc.zero_()
-        slice_stride = self.n_pad * self.k_pad
-        part5 = self.partial.data_ptr() + self.splits6 * slice_stride * 4
-        for c in range(nchunks):
-            t0 = c * Tc
-            ln = min(Tc, T - t0)
-            xp = x.data_ptr() + t0 * k
-            self._project(xp, strideb, ln, st, timed)
-            timed("forward", ln, "spb_forward_chunk", 1, v(self.cur.data_ptr()), B, n, Tc, ln,
-                  t0, T, float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
-                  int(self.alif), v(self.u.data_ptr()), v(self.a.data_ptr()), None, None, None,
-                  v(self.wsig.data_ptr()), v(ctab.data_ptr()), v(self.psi2.data_ptr()),
-                  v(self.coef.data_ptr()) if self.alif else None, self.n_pad,
-                  v(self.lp_hi.data_ptr()), v(self.lp_lo.data_ptr()), st)
-            call("spb_xbar_chunk", v(xp), strideb, B, k, self.k_pad, Tc, ln, float(alpha),
-                 v(self.xbar_state.data_ptr()), v(self.xf.data_ptr()), v(self.xh.data_ptr()),
-                 v(self.xl.data_ptr()), st)
-            timed("gemm", ln, "spb_grad_gemm_partials", v(self.lp_hi.data_ptr()),
-                  v(self.lp_lo.data_ptr()),
-                 v(self.xh.data_ptr()), v(self.xl.data_ptr()), n, self.k_pad, K, self.splits5,
-                 v(part5), self.k_pad, slice_stride, st)
-            self.launches += 5
-            if self.alif:
-                timed("elig", (ln, c > 0, c < nchunks - 1), "spb_alif_elig_chunk",
-                      v(self.coef.data_ptr()), v(self.xf.data_ptr()),
-                     v(self.eps.data_ptr()), v(self.partial.data_ptr()), B, n, self.n_pad,
-                     self.k_pad, Tc, ln, self.splits6, int(c > 0), int(c < nchunks - 1), st)
-                self.launches += 1
-            call("spb_reduce_partials", v(self.partial.data_ptr()),
-                 self.splits6 + self.splits5, n, self.n_pad, self.k_pad,
-                 v(self.grad_w_acc.data_ptr()), st)
-            self.launches += 1
-        return self
-
     def _project(self, xp, strideb, ln, st, timed=None):
         """K2: pack the chunk's spikes and compute cur = W x_t exactly on INT8 tensor cores."""
         v = ctypes_void
@@ -302,6 +204,116 @@ class EpropEngine:
         else:
             _lib.call(*args)
 
+    # ----------------------------------------------------------------------------------
+    def run(self, x: torch.Tensor, labels: torch.Tensor, *, alpha=0.95, theta=1.0, slope=10.0,
+            beta=0.8, rho=0.96, kappa=0.95, reset=False, raster: torch.Tensor | None = None,
+            stream=None, timers: dict | None = None):
+        """One full e-prop update on device-resident inputs.
+
+        x       uint8 [B, T, k] spike counts (CUDA, contiguous)
+        labels  int64 [B] (CUDA)
+        raster  optional int32 [B, T, ceil(n/32)] bit-packed spike output (pass A)
+        timers  optional dict; CUDA event pairs are appended per launch of the main
+                kernels under "proj", "forward", "gemm", "carry".
+        Results stay on device: ``grad_w_acc`` (fp64 [n, kp]), ``grad_wout``, ``loss``,
+        ``s`` (readout sums), ``correct``.
+        """
+        if reset:
+            raise NotImplementedError(
+                "reset=True makes G_u non-factorisable (SURVEY.md 8(f)-3); not on the B200 path yet")
+        if x.dtype != torch.uint8 or x.dim() != 3 or x.shape[0] != self.B or x.shape[2] != self.k:
+            raise ShapeMismatch(f"x must be uint8 [B={self.B}, T, k={self.k}], got "
+                                f"{tuple(x.shape)} {x.dtype}")
+        if not x.is_contiguous():
+            raise ShapeMismatch("x must be contiguous")
+        T = int(x.shape[1])
+        if T <= 0:
+            raise ShapeMismatch("T must be positive")
+        call = _lib.call
+        st = ctypes_void(stream if stream is not None else self._stream())
+        beta_e, rho_e = (float(beta), float(rho)) if self.alif else (0.0, 0.0)
+        B, n, k, m, Tc, KR, K = self.B, self.n, self.k, self.m, self.Tc, self.KR, self.K
+        ctab = self._gains(T, float(kappa))
+        nchunks = (T + Tc - 1) // Tc
+        strideb = T * k
+        self.launches = 0
+        v = ctypes_void
+        common = (float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
+                  int(self.alif))
+
+        def timed(name, meta, fn, *args):
+            if timers is None:
+                return call(fn, *args)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rc = call(fn, *args)
+            e1.record()
+            timers.setdefault(name, []).append((e0, e1, meta))
+            return rc
+
+        # ---------------- pass A ----------------
+        self.u.zero_(); self.a.zero_(); self.zbar.zero_(); self.zsum.zero_()
+        for c in range(nchunks):
+            t0 = c * Tc
+            ln = min(Tc, T - t0)
+            xp = x.data_ptr() + t0 * k
+            self._project(xp, strideb, ln, st, timed)
+            call("spb_forward_chunk", 0, v(self.cur.data_ptr()), B, n, Tc, KR, ln, t0, T,
+                 *common, v(self.u.data_ptr()), v(self.a.data_ptr()),
+                 v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
+                 v(raster.data_ptr()) if raster is not None else None,
+                 None, None, None, None, None, None, None, None, st)
+            self.launches += 3
+        # ---------------- readout / loss ----------------
+        call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
+             v(labels.data_ptr()), B, n, m, v(self.s.data_ptr()), v(self.loss.data_ptr()),
+             v(self.g.data_ptr()), v(self.wsig.data_ptr()), v(self.correct.data_ptr()), st)
+        self.grad_wout.zero_()
+        call("spb_readout_grad", v(self.g.data_ptr()), v(self.zsum.data_ptr()), B, n, m,
+             v(self.grad_wout.data_ptr()), st)
+        self.launches += 2
+        # ---------------- pass B ----------------
+        self.u.zero_(); self.a.zero_(); self.xbar_state.zero_()
+        self.grad_w_acc.zero_()
+        slice_stride = self.n_pad * self.kp
+        part6 = self.partial.data_ptr() + self.splits5 * slice_stride * 4
+        for c in range(nchunks):
+            t0 = c * Tc
+            ln = min(Tc, T - t0)
+            last = c == nchunks - 1
+            xp = x.data_ptr() + t0 * k
+            self._project(xp, strideb, ln, st, timed)
+            timed("forward", ln, "spb_forward_chunk", 1, v(self.cur.data_ptr()), B, n, Tc, KR,
+                  ln, t0, T, *common, v(self.u.data_ptr()), v(self.a.data_ptr()), None, None,
+                  None, v(self.wsig.data_ptr()), v(ctab.data_ptr()),
+                  v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()),
+                  v(self.w_hi.data_ptr()) if self.alif else None,
+                  v(self.w_lo.data_ptr()) if self.alif else None,
+                  v(self.mdt.data_ptr()) if self.alif else None, v(self.psi.data_ptr()), st)
+            call("spb_xbar_chunk", v(xp), strideb, B, k, self.kp, KR, ln, float(alpha),
+                 v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()), v(self.xl.data_ptr()), st)
+            timed("gemm", ln, "spb_grad_gemm_partials", v(self.c_hi.data_ptr()),
+                  v(self.c_lo.data_ptr()), v(self.xh.data_ptr()), v(self.xl.data_ptr()), n,
+                  self.kp, K, self.splits5, v(self.partial.data_ptr()), self.kp, slice_stride,
+                  st)
+            self.launches += 5
+            slices = self.splits5
+            if self.alif and (c > 0 or not last):
+                # first chunk: E0 = 0 (nothing to add, only carry); last chunk: no carry
+                timed("carry", (ln, c > 0, not last), "spb_alif_carry_chunk",
+                      v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()), v(self.xh.data_ptr()),
+                      v(self.xl.data_ptr()), v(self.mdt.data_ptr()), v(self.eps.data_ptr()),
+                      v(part6), B, n, self.n_pad, k, self.ke, self.kp, KR, self.splits6,
+                      int(not last), int(c > 0), int(not last), st)
+                self.launches += 1
+                if c > 0:
+                    slices += self.splits6
+            call("spb_reduce_partials", v(self.partial.data_ptr()), slices, n, self.n_pad,
+                 self.kp, v(self.grad_w_acc.data_ptr()), st)
+            self.launches += 1
+        return self
+
     def check_labels(self, labels_np):
         labels_np = np.asarray(labels_np)
         if labels_np.shape != (self.B,):
@@ -313,7 +325,7 @@ class EpropEngine:
     def grad_w(self, dtype=torch.float32):
         """Finalised input-weight gradient [n, k] in ``dtype`` (device tensor)."""
         out = torch.empty((self.n, self.k), dtype=dtype, device=self.device)
-        st = ctypes_void(torch.cuda.current_stream(self.device).cuda_stream)
         _lib.call("spb_finalize_grad", ctypes_void(self.grad_w_acc.data_ptr()), self.n, self.k,
-                  self.k_pad, ctypes_void(out.data_ptr()), int(dtype == torch.float64), st)
+                  self.kp, ctypes_void(out.data_ptr()), int(dtype == torch.float64),
+                  ctypes_void(self._stream()))
         return out

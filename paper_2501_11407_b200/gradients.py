@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .engine import EpropEngine
+from .engine import EpropEngine, default_chunk
 from .errors import LabelOutOfRange, ShapeMismatch
 from .neurons import ALIFParams, Network
 
@@ -75,19 +75,12 @@ def softmax_cross_entropy(v: np.ndarray, label: int):
 _ENGINES: dict = {}
 
 
-def _default_chunk(T: int) -> int:
-    for c in (8, 16, 32):
-        if T <= c:
-            return c
-    return 32
-
-
 def get_engine(net: Network, B: int, *, chunk: int | None = None, T: int | None = None,
                device=None) -> EpropEngine:
     """Engine cache keyed by shape, neuron kind, weight precision, chunk and device."""
     dev = torch.device(device if device is not None else "cuda")
     if chunk is None:
-        chunk = _default_chunk(T or 32)
+        chunk = default_chunk(T or 127)
     w_f64 = net.neuron.w.dtype == np.float64
     key = (net.n, net.k, net.m, B, net.is_alif, w_f64, chunk, str(dev))
     eng = _ENGINES.get(key)

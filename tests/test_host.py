@@ -12,7 +12,7 @@ import torch
 
 import paper_2501_11407_b200 as P
 from paper_2501_11407_b200 import _lib
-from paper_2501_11407_b200.engine import EpropEngine, readout_gains, _best_split
+from paper_2501_11407_b200.engine import EpropEngine, default_chunk, readout_gains
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "sparseprop_b200.h")
@@ -63,14 +63,14 @@ def test_version_and_error_text():
 def test_bad_arguments_are_rejected_without_gpu():
     # argument validation happens before any CUDA call -> works on a CPU-only host
     with pytest.raises(P.ShapeMismatch):
-        _lib.call("spb_forward_chunk", 2, None, 1, 1, 8, 1, 0, 1,
+        _lib.call("spb_forward_chunk", 2, None, 1, 1, 63, 64, 1, 0, 1,
                   0.95, 1.0, 10.0, 0.0, 0.0, 0.95, 0, 0, None, None, None, None, None, None,
-                  None, None, None, 0, None, None, None)
+                  None, None, None, None, None, None, None, None)
     with pytest.raises(P.ShapeMismatch):
         _lib.call("spb_input_proj", None, None, None, 1, 1, 32, 100, 7, None, 148, None)
     with pytest.raises(P.ShapeMismatch):
-        _lib.call("spb_alif_elig_chunk", None, None, None, None, 1, 1, 128, 64, 32, 32, 1,
-                  0, 0, None)
+        _lib.call("spb_alif_carry_chunk", None, None, None, None, None, None, None, 1, 1, 100,
+                  1, 4, 128, 64, 1, 0, 0, 0, None)
 
 
 class _Recorder:
@@ -92,7 +92,8 @@ class _Recorder:
         return 0
 
 
-@pytest.mark.parametrize("alif,T,chunk", [(True, 77, 16), (False, 50, 24), (True, 64, 64)])
+@pytest.mark.parametrize("alif,T,chunk", [(True, 300, 63), (False, 150, 63), (True, 127, 127),
+                                          (True, 128, 127)])
 def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     rec = _Recorder()
     monkeypatch.setattr(_lib, "call", rec)
@@ -109,19 +110,23 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     assert names.count("spb_slice_weights") == 0
     assert names.count("spb_xbar_chunk") == nch
     assert names.count("spb_grad_gemm_partials") == nch
-    assert names.count("spb_alif_elig_chunk") == (nch if alif else 0)
+    carries = [c[1] for c in rec.calls if c[0] == "spb_alif_carry_chunk"]
+    if alif:
+        # no carry launch for a single chunk; chunk 0 only carries, the last only adds M E0
+        assert len(carries) == (nch if nch > 1 else 0)
+        if carries:
+            do_mma, load, store = [(e[15], e[16], e[17]) for e in carries][0]
+            assert (do_mma, load, store) == (1, 0, 1)
+            assert [(e[15], e[16], e[17]) for e in carries][-1] == (0, 1, 0)
+            assert all((e[15], e[16], e[17]) == (1, 1, 1) for e in carries[1:-1])
+    else:
+        assert not carries
     assert names.count("spb_readout_loss") == 1
-    # first ALIF chunk starts from eps = 0, last chunk does not write eps back
-    el = [c[1] for c in rec.calls if c[0] == "spb_alif_elig_chunk"]
-    if el:
-        assert el[0][11] == 0 and el[-1][12] == 0
-        assert all(e[11] == 1 for e in el[1:]) and all(e[12] == 1 for e in el[:-1])
-        assert sum(e[9] for e in el) == T
     assert eng.launches == len(rec.calls) - 0
 
 
 def test_engine_rejects_bad_inputs():
-    eng = EpropEngine(8, 5, 2, 3, alif=False, chunk=8, device="cpu", sm_count=148)
+    eng = EpropEngine(8, 5, 2, 3, alif=False, chunk=63, device="cpu", sm_count=148)
     with pytest.raises(P.ShapeMismatch):
         eng.run(torch.zeros((3, 10, 4), dtype=torch.uint8), torch.zeros(3, dtype=torch.int64))
     with pytest.raises(P.ShapeMismatch):
@@ -131,6 +136,8 @@ def test_engine_rejects_bad_inputs():
                 reset=True)
     with pytest.raises(ValueError):
         EpropEngine(8, 5, 2, 3, alif=True, chunk=24, device="cpu")
+    with pytest.raises(ValueError):
+        EpropEngine(8, 5, 2, 3, alif=False, chunk=64, device="cpu")
 
 
 def test_readout_gains_match_bptt_recurrence():
@@ -140,12 +147,6 @@ def test_readout_gains_match_bptt_recurrence():
         acc = 1.0 + 0.9 * acc
         ref.append(acc)
     assert np.allclose(c, ref[::-1])
-
-
-def test_best_split_divides_batch():
-    for B in (1, 7, 64, 256, 1000):
-        d = _best_split(B, 88, 296)
-        assert B % d == 0 and (d == 1 or B // d >= 16)
 
 
 def test_param_validation_mirrors_reference():
@@ -178,3 +179,8 @@ def test_input_count_conversion():
         _as_counts(np.array([[0.5]]))
     with pytest.raises(ValueError):
         _as_counts(np.array([[-1.0]]))
+
+
+def test_default_chunk():
+    assert default_chunk(10) == 63 and default_chunk(100) == 127 and default_chunk(250) == 255
+    assert default_chunk(10_000) == 127

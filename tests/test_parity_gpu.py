@@ -83,7 +83,7 @@ SMALL = ["c1_lif_f64", "c1_alif_f64", "c1_lif_f32", "c1_alif_f32", "mid_alif_f64
 
 
 @pytest.mark.parametrize("name", SMALL)
-@pytest.mark.parametrize("chunk", [8, 32, 64])
+@pytest.mark.parametrize("chunk", [63, 127])
 def test_small_configs_vs_reference(name, chunk):
     _need_gpu()
     g = load_golden(name)
@@ -140,7 +140,7 @@ def test_shd_ssc_shapes_vs_reference(name):
     g = load_golden(name)
     net = _net_from_golden(g)
     x, labels = _inputs(g)
-    eng, r = _run_engine(net, x, labels, chunk=32, raster=True)
+    eng, r = _run_engine(net, x, labels, chunk=127, raster=True)
     assert np.array_equal(_unpack_raster(r, net.n), _golden_raster(g))
     assert np.allclose(eng.loss.cpu().numpy(), g["loss"], rtol=1e-9)
     gw = eng.grad_w(torch.float64).cpu().numpy()
@@ -153,9 +153,10 @@ def test_shd_ssc_shapes_vs_reference(name):
 
 
 @pytest.mark.parametrize("kind,n,k,m,T,B,chunk", [
-    ("alif", 200, 90, 7, 77, 12, 16),
-    ("lif", 300, 130, 5, 50, 10, 24),
-    ("alif", 130, 700, 20, 40, 33, 8),
+    ("alif", 200, 90, 7, 177, 12, 63),
+    ("lif", 300, 130, 5, 150, 10, 63),
+    ("alif", 130, 700, 20, 300, 33, 127),
+    ("alif", 64, 40, 3, 520, 5, 255),
 ])
 def test_batched_vs_two_pass_oracle(kind, n, k, m, T, B, chunk):
     """Ragged shapes (n, k not tile multiples, T not a chunk multiple) vs the numpy oracle."""
@@ -222,7 +223,41 @@ def test_pooled_count_inputs_vs_oracle():
     assert xp.max() > 1
     net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=160, n_inputs=140, n_classes=5,
                                        precision="f64", seed=2))
-    r = P.eprop_batch_gradient(net, xp, labels, chunk=16)
+    r = P.eprop_batch_gradient(net, xp, labels, chunk=63)
     ref = O.eprop_two_pass_batch(net.neuron.w, net.readout.w_out, O.Params(alif=True), xp, labels)
     assert _rel(r.grads["w"], ref.grad_w) <= REL_TOL
     assert np.allclose(r.loss, ref.loss, rtol=1e-9)
+
+
+@pytest.mark.parametrize("w_f64", [False, True])
+def test_int8_tensor_core_projection_is_exact(w_f64):
+    """K2: cur = W x_t from sliced INT8 tcgen05 MMAs equals the exactly-rounded sum."""
+    _need_gpu()
+    import ctypes
+    from paper_2501_11407_b200.engine import EpropEngine
+    rng = np.random.default_rng(0)
+    B, T, k, n = 5, 16, 700, 100
+    w = rng.uniform(-1, 1, (n, k)) / np.sqrt(k)
+    w[3, :] *= 1e-6                        # tiny row: per-neuron exponent
+    w[7, 5] = 0.0
+    w = w.astype(np.float64 if w_f64 else np.float32)
+    x = (rng.random((B, T, k)) < 0.1).astype(np.uint8)
+    x[0, 0, :10] = 7                       # pooled counts
+    eng = EpropEngine(n, k, 3, B, alif=False, w_f64=w_f64, chunk=63)
+    eng.set_weights(torch.from_numpy(w), torch.zeros((3, n), dtype=torch.float64))
+    xd = torch.from_numpy(x).cuda()
+    v = ctypes.c_void_p
+    eng._project(xd.data_ptr(), T * k, T, v(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    got = eng.cur.cpu().numpy().reshape(B, eng.Tc, n)[:, :T]
+    exact = np.einsum("btk,nk->btn", x.astype(np.longdouble), w.astype(np.longdouble))
+    err = np.abs(got.astype(np.longdouble) - exact)
+    # one fp64 rounding of the exact sum (half an ulp) + the digit truncation: every
+    # weight is represented to within 2^(s_i - 7P) (s_i = exponent of the row maximum)
+    P = 8 if w_f64 else 7
+    rowmax = np.abs(w.astype(np.float64)).max(axis=1)
+    s_i = np.frexp(rowmax)[1]
+    trunc = np.ldexp(1.0, s_i - 7 * P)                          # [n]
+    cnt = x.astype(np.float64).sum(-1)                           # [B, T]
+    bound = 1.12e-16 * np.abs(exact) + cnt[..., None] * trunc[None, None, :]
+    assert float(np.max(err - bound)) <= 0.0
