@@ -60,7 +60,7 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
  *     u, a    [B][n] fp64 state, carried across chunks (zero at t=0)
  *     pass 0 (A): zbar, zsum [B][n] fp64 carried; raster [B][T][ceil(n/32)] bit-packed
  *                 spikes (optional, may be NULL).
- *     pass 1 (B): wsig [B][n] = W_out^T g; ctab[T] readout gains c_t.  A backward scan
+ *     pass 1 (B): wsig [B][n] = W_out^T g; ctab[T] fp32 readout gains c_t.  A backward scan
  *                 over the chunk emits, K-major over (sample b, row rho < KR):
  *                   c_hi/c_lo [n][B*KR]  gradient coefficient C_rho (bf16 hi/lo split)
  *                   w_hi/w_lo [n][B*KR]  ALIF trace-carry coefficient W_rho
@@ -70,7 +70,7 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
 int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR, int len, int t0,
                       int T, double alpha, double theta, double slope, double beta, double rho,
                       double kappa, int reset, int alif, double* u, double* a, double* zbar,
-                      double* zsum, uint32_t* raster, const float* wsig, const double* ctab,
+                      double* zsum, uint32_t* raster, const float* wsig, const float* ctab,
                       void* c_hi, void* c_lo, void* w_hi, void* w_lo, float* mdt,
                       float* psi_scratch, cudaStream_t stream);
 

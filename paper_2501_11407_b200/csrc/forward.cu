@@ -47,7 +47,7 @@ constexpr int K1_THREADS = 128;  // 4 warps = 4 samples x 32 neurons
 __global__ void __launch_bounds__(K1_THREADS) forward_chunk_kernel(
     FwdParams P, const double* __restrict__ cur, double* __restrict__ u_st,
     double* __restrict__ a_st, double* __restrict__ zbar_st, double* __restrict__ zsum_st,
-    uint32_t* __restrict__ raster, const float* __restrict__ wsig, const double* __restrict__ ctab,
+    uint32_t* __restrict__ raster, const float* __restrict__ wsig, const float* __restrict__ ctab,
     __nv_bfloat16* __restrict__ c_hi, __nv_bfloat16* __restrict__ c_lo,
     __nv_bfloat16* __restrict__ w_hi, __nv_bfloat16* __restrict__ w_lo,
     float2* __restrict__ mdt, float* __restrict__ psis) {
@@ -143,11 +143,11 @@ __global__ void __launch_bounds__(K1_THREADS) forward_chunk_kernel(
       float cval = 0.0f, wval = 0.0f;
       if (r <= L) {
         const float psi_prev = pc[u8];  // psi_{r-1}
-        if (r >= 1) cval = (float)ctab[P.t0 + r - 1] * w_sig * psi_prev;  // Lpsi_{r-1}
+        if (r >= 1) cval = ctab[P.t0 + r - 1] * w_sig * psi_prev;  // Lpsi_{r-1}
         if (P.alif && r < L) {
           const float psi_r = pc[u8 + 1];
           const float A = fmaf(-beta_f, psi_prev, rho_f);
-          const float Q = -beta_f * ((float)ctab[P.t0 + r] * w_sig * psi_r);
+          const float Q = -beta_f * (ctab[P.t0 + r] * w_sig * psi_r);
           lam = fmaf(a_next, lam, Q);             // Lambda_r (Lambda_L = 0)
           cval = fmaf(psi_prev, lam, cval);       // + R_r
           wval = psi_prev * dcum;                 // W_r = P_r D(L-1, r)
@@ -222,7 +222,7 @@ extern "C" {
 int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR, int len, int t0,
                       int T, double alpha, double theta, double slope, double beta, double rho,
                       double kappa, int reset, int alif, double* u, double* a, double* zbar,
-                      double* zsum, uint32_t* raster, const float* wsig, const double* ctab,
+                      double* zsum, uint32_t* raster, const float* wsig, const float* ctab,
                       void* c_hi, void* c_lo, void* w_hi, void* w_lo, float* mdt,
                       float* psi_scratch, cudaStream_t stream) {
   SPB_CHECK_ARG(pass == 0 || pass == 1, "spb_forward_chunk: pass must be 0 (A) or 1 (B)");

@@ -85,7 +85,7 @@ __device__ __forceinline__ double pow2(int e) {  // 2^e for -1022 <= e <= 1023
 // Epilogue of one 128-row x 32-neuron tile: pull the P slice accumulators of this thread's
 // row from TMEM, recombine them exactly in int64 and write the fp64 current.
 template <int P>
-__device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int* __restrict__ sexp,
+__device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&se)[NT],
                                                    double* __restrict__ out, int M, int n, int row,
                                                    int i0, uint32_t tempty_bar, int lane) {
   long long g0[NT], g1[NT];
@@ -112,10 +112,9 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int* __
       double v[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int i = i0 + c + h;
-        const int se = (i < n) ? __ldg(sexp + i) : 0;
         // I = g0 * 2^(s-6-14) + g1 * 2^(s-6-7(P-1))  (both conversions exact)
-        v[h] = fma((double)g0[c + h], pow2(se - 20), (double)g1[c + h] * pow2(se - 6 - 7 * (P - 1)));
+        v[h] = fma((double)g0[c + h], pow2(se[c + h] - 20),
+                   (double)g1[c + h] * pow2(se[c + h] - 6 - 7 * (P - 1)));
       }
       if (i0 + c + 1 < n) {
         *reinterpret_cast<double2*>(orow + c) = make_double2(v[0], v[1]);
@@ -255,9 +254,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int t = t_begin; t < t_end; ++t, ++lt) {
       const int nt = t / m_tiles, mt = t % m_tiles;
       const int a = lt & 1;
+      int se[NT];  // per-neuron exponents, fetched before waiting on the tensor cores
+#pragma unroll
+      for (int c = 0; c < NT; ++c) se[c] = (nt * NT + c < n) ? __ldg(sexp + nt * NT + c) : 0;
       mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      proj_epilogue_tile<P>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256), sexp,
+      proj_epilogue_tile<P>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256), se,
                             out, M, n, mt * BM + q * 32 + lane, nt * NT, smem_u32(&tempty[a]),
                             lane);
     }
@@ -359,9 +361,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
       const int nt = t / m_tiles, mt = t % m_tiles;
       const int a = lt & 1;
+      int se[NT];  // per-neuron exponents, fetched before waiting on the tensor cores
+#pragma unroll
+      for (int c = 0; c < NT; ++c) se[c] = (nt * NT + c < n) ? __ldg(sexp + nt * NT + c) : 0;
       mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      proj_epilogue_tile<P>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256), sexp,
+      proj_epilogue_tile<P>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256), se,
                             out, M, n, mt * BM + q * 32 + lane, nt * NT, smem_u32(&tempty[a]),
                             lane);
     }

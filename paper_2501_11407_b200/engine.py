@@ -187,7 +187,8 @@ class EpropEngine:
 
     def _gains(self, T, kappa):
         if self._ctab_T != (T, kappa):
-            self.ctab = torch.as_tensor(readout_gains(T, kappa), device=self.device)
+            self.ctab = torch.as_tensor(readout_gains(T, kappa).astype(np.float32),
+                                        device=self.device)
             self._ctab_T = (T, kappa)
         return self.ctab
 
