@@ -253,30 +253,48 @@ def main():
     value = world * B * T / (ms_max * 1e-3)
 
     # ---- e2e through the engine API with pinned host buffers ----
+    # Each step's spikes/labels are copied H2D from pinned host memory on a copy stream
+    # (double-buffered: step i+1's copy overlaps step i's kernels) and the per-sample
+    # losses are read back D2H; every copy is inside the timed region.
     e2e = None
     if not args.no_e2e and not args.profile:
         xh = torch.from_numpy(x_np).pin_memory()
         yh = torch.from_numpy(y_np).pin_memory()
         loss_h = torch.empty(B, dtype=torch.float64).pin_memory()
-        xdev = torch.empty_like(xd)
-        ydev = torch.empty_like(yd)
+        xb = [torch.empty_like(xd) for _ in range(2)]
+        yb = [torch.empty_like(yd) for _ in range(2)]
+        cs = torch.cuda.Stream(device=dev)
+        main = torch.cuda.current_stream(dev)
+        copied = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
+        for e in consumed:
+            e.record(main)
 
-        def e2e_step():
-            xdev.copy_(xh, non_blocking=True)
-            ydev.copy_(yh, non_blocking=True)
-            step(xdev, ydev)
-            loss_h.copy_(eng.loss, non_blocking=True)
+        def prefetch(i):
+            with torch.cuda.stream(cs):
+                cs.wait_event(consumed[i % 2])
+                xb[i % 2].copy_(xh, non_blocking=True)
+                yb[i % 2].copy_(yh, non_blocking=True)
+                copied[i % 2].record(cs)
 
-        for _ in range(3):
-            e2e_step()
+        def run_e2e(nsteps):
+            prefetch(0)
+            for i in range(nsteps):
+                if i + 1 < nsteps:
+                    prefetch(i + 1)
+                main.wait_event(copied[i % 2])
+                step(xb[i % 2], yb[i % 2])
+                consumed[i % 2].record(main)
+                loss_h.copy_(eng.loss, non_blocking=True)
+
+        run_e2e(3)
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         n_e2e = max(5, args.steps // 2)
-        e0.record()
-        for _ in range(n_e2e):
-            e2e_step()
-        e1.record()
+        e0.record(main)
+        run_e2e(n_e2e)
+        e1.record(main)
         barrier()
         e2e_ms = torch.tensor([e0.elapsed_time(e1) / n_e2e], dtype=torch.float64, device=dev)
         if world > 1:
@@ -284,7 +302,8 @@ def main():
         e2e = {"value": world * B * T / (float(e2e_ms.item()) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(x_np.nbytes + y_np.nbytes),
                "d2h_bytes_per_step": int(B * 8),
-               "ms_per_step": float(e2e_ms.item())}
+               "ms_per_step": float(e2e_ms.item()),
+               "pipeline": "H2D of step i+1 on a copy stream overlaps step i (double buffer)"}
 
     # ---- roofline of every main kernel; the dominant one is the headline ----
     hbm_peak, bf16_peak, peak_kind = peaks()

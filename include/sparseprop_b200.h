@@ -61,17 +61,19 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
  *     pass 0 (A): zbar, zsum [B][n] fp64 carried; raster [B][T][ceil(n/32)] bit-packed
  *                 spikes (optional, may be NULL).
  *     pass 1 (B): wsig [B][n] = W_out^T g; ctab[T] fp32 readout gains c_t.  A backward scan
- *                 over the chunk emits, K-major over (sample b, row rho < KR):
- *                   c_hi/c_lo [n][B*KR]  gradient coefficient C_rho (bf16 hi/lo split)
- *                   w_hi/w_lo [n][B*KR]  ALIF trace-carry coefficient W_rho
- *                   mdt [B][n] float2    ALIF (M, Dt) of the chunk
+ *                 over the chunk (second kernel) emits, MN-major (neurons contiguous,
+ *                 row stride ldc >= n, ldc % 8 == 0) over (sample b, row rho < KR):
+ *                   c_hi/c_lo [B*KR][ldc]  gradient coefficient C_rho (bf16 hi/lo split)
+ *                   w_hi/w_lo [B*KR][ldc]  ALIF trace-carry coefficient W_rho (pass NULL
+ *                                          when no later chunk needs the trace)
+ *                   mdt [B][n] float2      ALIF (M, Dt) of the chunk (always, ALIF)
  *                 psi_scratch [B][KR+1][n] fp32 working buffer of the scan.
  *                 (forward.cu header has the algebra).  KR >= Tc+1, KR % 8 == 0. */
 int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR, int len, int t0,
                       int T, double alpha, double theta, double slope, double beta, double rho,
                       double kappa, int reset, int alif, double* u, double* a, double* zbar,
                       double* zsum, uint32_t* raster, const float* wsig, const float* ctab,
-                      void* c_hi, void* c_lo, void* w_hi, void* w_lo, float* mdt,
+                      void* c_hi, void* c_lo, void* w_hi, void* w_lo, int ldc, float* mdt,
                       float* psi_scratch, cudaStream_t stream);
 
 /* K4  Presynaptic filter xbar_t = alpha*xbar_{t-1} + x_t (the factorised LIF trace G_u,
@@ -96,28 +98,29 @@ int spb_readout_grad(const double* g, const double* zsum, int B, int n, int m, d
 
 /* K5  Chunk gradient GEMM on tcgen05 tensor cores (TMA-fed, bf16 hi/lo split, fp32
  *     TMEM accumulation), split-K over `splits` CTAs per 128x128 tile:
- *       partial[z][i][j] = sum_{K in split z} (Ah+Al)[i][K] (Bh+Bl)[j][K]  (i<M, j<ldp)
+ *       partial[z][i][j] = sum_{K in split z} (Ah+Al)[K][i] (Bh+Bl)[j][K]  (i<M, j<ldp)
  *     at partial + z*slice_stride (row stride ldp); every slice is written.
  *     With A = C (K1) and B = xbar (K4) this is every intra-chunk gradient term: the
  *     factorisable LIF part G_u = 1 (x) xbar and the intra-chunk ALIF part.  Replaces the
- *     xbar/xsum n x k accumulation of gradients.py:165-172,180.  A* [M][K], B* [N_rows][K],
- *     16-byte aligned, K % 8 == 0. */
-int spb_grad_gemm_partials(const void* ah, const void* al, const void* bh, const void* bl, int M,
-                           int N_rows, int K, int splits, float* partial, int ldp,
+ *     xbar/xsum n x k accumulation of gradients.py:165-172,180.  A* [K][lda] MN-major
+ *     (lda >= M, lda % 8 == 0), B* [N_rows][K] K-major; 16-byte aligned, K % 8 == 0. */
+int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* bh, const void* bl,
+                           int M, int N_rows, int K, int splits, float* partial, int ldp,
                            long long slice_stride, cudaStream_t stream);
 
 /* K5s CUDA-core version of K5 on the same operands (test cross-check only). */
-int spb_grad_gemm_simt(const void* ah, const void* al, const void* bh, const void* bl, int M,
-                       int N, int K, double* grad, int ldg, cudaStream_t stream);
+int spb_grad_gemm_simt(const void* ah, const void* al, int lda, const void* bh, const void* bl,
+                       int M, int N, int K, double* grad, int ldg, cudaStream_t stream);
 
 /* K6  ALIF adaptation trace carried across chunks on tcgen05 tensor cores (elig.cu):
  *       E_end[b,i,:] = Dt[b,i] E0[b,i,:] + sum_rho W_rho[b,i] xbar_rho[b,:]   (if do_mma)
  *       partial[z][i][j] = sum_{b in split z} M[b,i] E0[b,i,j]
- *     eps [B][n_pad][ke] fp32 (E0 read if load_eps, E_end written if store_eps), w*/x* the
- *     K1/K4 operands (K = B*KR), mdt from K1; partial [splits][n_pad][kp].
+ *     eps [B][n_pad][ke] fp32 (E0 read if load_eps, E_end written if store_eps), w* the K1s
+ *     operand [B*KR][ldw] (MN-major), x* the K4 operand [kp][B*KR], mdt from K1s;
+ *     partial [splits][n_pad][kp].
  *     n_pad % 128 == 0, kp % 128 == 0, ke % 4 == 0, KR % 64 == 0.  Replaces the ALIF G_a
  *     block of eprop_trace_update (gradients.py:89-94) and x_step (gradients.py:165-167). */
-int spb_alif_carry_chunk(const void* wh, const void* wl, const void* xh, const void* xl,
+int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh, const void* xl,
                          const float* mdt, float* eps, float* partial, int B, int n, int n_pad,
                          int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
                          int store_eps, cudaStream_t stream);

@@ -32,9 +32,19 @@ constexpr int STAGE = 4 * TILE;
 constexpr int EPI_WARPS = 16;  // 4 TMEM lane quarters x 4 column groups of 32
 constexpr int THREADS = 64 + EPI_WARPS * 32;
 constexpr int SMEM = STAGES * STAGE + 1024 + 256;
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+// A = W (MN-major: neurons contiguous, written by K1s), B = xbar (K-major)
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(8192u >> 4) << 16;   // LBO: next 64-wide MN block
+  d |= (uint64_t)(1024u >> 4) << 32;   // SBO: next 8-row K group
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
 __device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
@@ -145,8 +155,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t st = smem_u32(smem + s * STAGE);
           const uint32_t fb = smem_u32(&full[s]);
           mbar_expect_tx(fb, STAGE);
-          tma_load_2d(st, &tm_wh, fb, kbase + kb * BK, i0);
-          tma_load_2d(st + TILE, &tm_wl, fb, kbase + kb * BK, i0);
+          tma_load_2d(st, &tm_wh, fb, i0, kbase + kb * BK);
+          tma_load_2d(st + TILE / 2, &tm_wh, fb, i0 + 64, kbase + kb * BK);
+          tma_load_2d(st + TILE, &tm_wl, fb, i0, kbase + kb * BK);
+          tma_load_2d(st + TILE + TILE / 2, &tm_wl, fb, i0 + 64, kbase + kb * BK);
           tma_load_2d(st + 2 * TILE, &tm_xh, fb, kbase + kb * BK, j0);
           tma_load_2d(st + 3 * TILE, &tm_xl, fb, kbase + kb * BK, j0);
         }
@@ -167,8 +179,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t st = smem_u32(smem + s * STAGE);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint32_t off = kk * 32;
-            const uint64_t dwh = desc_k_sw128(st + off), dwl = desc_k_sw128(st + TILE + off);
+            const uint32_t off = kk * 32, offw = kk * 2048;
+            const uint64_t dwh = desc_mn_sw128(st + offw), dwl = desc_mn_sw128(st + TILE + offw);
             const uint64_t dxh = desc_k_sw128(st + 2 * TILE + off),
                            dxl = desc_k_sw128(st + 3 * TILE + off);
             mma_bf16(d, dwh, dxh, (kb | kk) ? 1u : 0u);
@@ -265,10 +277,10 @@ __global__ void reduce_partials_kernel(const float* __restrict__ partial, int S,
   grad[idx] += acc;
 }
 
-// CUDA-core GEMM on the same bf16 hi/lo K-major operands as the tensor-core path:
-// grad[i][j] += sum_K (Ah+Al)[i][K] * (Bh+Bl)[j][K]  (64x64 tiles, 4x4 per thread).
+// CUDA-core GEMM on the same bf16 hi/lo operands as the tensor-core path:
+// grad[i][j] += sum_K (Ah+Al)[K][i] * (Bh+Bl)[j][K]  (64x64 tiles, 4x4 per thread).
 __global__ void __launch_bounds__(256) grad_gemm_simt_kernel(
-    const __nv_bfloat16* __restrict__ ah, const __nv_bfloat16* __restrict__ al,
+    const __nv_bfloat16* __restrict__ ah, const __nv_bfloat16* __restrict__ al, int lda,
     const __nv_bfloat16* __restrict__ bh, const __nv_bfloat16* __restrict__ bl, int M, int N,
     int K, double* __restrict__ grad, int ldg) {
   __shared__ float As[32][65];
@@ -282,7 +294,7 @@ __global__ void __launch_bounds__(256) grad_gemm_simt_kernel(
       const int r = idx >> 5, kk = idx & 31;
       float va = 0.f, vb = 0.f;
       if (m0 + r < M && k0 + kk < K) {
-        const long long o = (long long)(m0 + r) * K + k0 + kk;
+        const long long o = (long long)(k0 + kk) * lda + m0 + r;
         va = __bfloat162float(ah[o]) + __bfloat162float(al[o]);
       }
       if (n0 + r < N && k0 + kk < K) {
@@ -323,7 +335,7 @@ using namespace spb;
 
 extern "C" {
 
-int spb_alif_carry_chunk(const void* wh, const void* wl, const void* xh, const void* xl,
+int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh, const void* xl,
                          const float* mdt, float* eps, float* partial, int B, int n, int n_pad,
                          int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
                          int store_eps, cudaStream_t stream) {
@@ -333,15 +345,16 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, const void* xh, const v
                     ke >= k && ke % 4 == 0 && KR % carry::BK == 0,
                 "spb_alif_carry_chunk: bad padding (n_pad %% 128, kp %% 128, ke %% 4, KR %% 64)");
   SPB_CHECK_ARG(B > 0 && splits > 0 && splits <= B, "spb_alif_carry_chunk: bad split");
+  SPB_CHECK_ARG(!do_mma || (ldw >= n && ldw % 8 == 0), "spb_alif_carry_chunk: bad ldw");
   SPB_CHECK_ARG(!(store_eps && !do_mma), "spb_alif_carry_chunk: storing eps needs the GEMM");
   CUtensorMap mwh{}, mwl{}, mxh{}, mxl{};
   if (do_mma) {
     const uint64_t K = (uint64_t)B * KR;
     const bool ok =
-        make_tmap_2d(&mwh, wh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, n, K * 2, carry::BK,
-                     carry::BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
-        make_tmap_2d(&mwl, wl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, n, K * 2, carry::BK,
-                     carry::BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
+        make_tmap_2d(&mwh, wh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, K, (uint64_t)ldw * 2, 64,
+                     carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
+        make_tmap_2d(&mwl, wl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, K, (uint64_t)ldw * 2, 64,
+                     carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
         make_tmap_2d(&mxh, xh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, kp, K * 2, carry::BK,
                      carry::BN, CU_TENSOR_MAP_SWIZZLE_128B) &&
         make_tmap_2d(&mxl, xl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, kp, K * 2, carry::BK,
@@ -373,13 +386,13 @@ int spb_reduce_partials(const float* partial, int splits, int n, int n_pad, int 
   return 0;
 }
 
-int spb_grad_gemm_simt(const void* ah, const void* al, const void* bh, const void* bl, int M,
-                       int N, int K, double* grad, int ldg, cudaStream_t stream) {
-  SPB_CHECK_ARG(ah && al && bh && bl && grad && M > 0 && N > 0 && K > 0 && ldg >= N,
+int spb_grad_gemm_simt(const void* ah, const void* al, int lda, const void* bh, const void* bl,
+                       int M, int N, int K, double* grad, int ldg, cudaStream_t stream) {
+  SPB_CHECK_ARG(ah && al && bh && bl && grad && M > 0 && N > 0 && K > 0 && ldg >= N && lda >= M,
                 "spb_grad_gemm_simt: bad args");
   dim3 grid(ceil_div(N, 64), ceil_div(M, 64));
   grad_gemm_simt_kernel<<<grid, 256, 0, stream>>>(
-      (const __nv_bfloat16*)ah, (const __nv_bfloat16*)al, (const __nv_bfloat16*)bh,
+      (const __nv_bfloat16*)ah, (const __nv_bfloat16*)al, lda, (const __nv_bfloat16*)bh,
       (const __nv_bfloat16*)bl, M, N, K, grad, ldg);
   SPB_CHECK_LAUNCH("grad_gemm_simt");
   return 0;

@@ -44,13 +44,10 @@ constexpr int K1_THREADS = 128;  // 4 warps = 4 samples x 32 neurons
 // kernel runs at full occupancy; the backward scan runs in fp32 (every quantity it
 // produces feeds the fp32 / bf16-split gradient path).
 // ------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(K1_THREADS) forward_chunk_kernel(
+__global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
     FwdParams P, const double* __restrict__ cur, double* __restrict__ u_st,
     double* __restrict__ a_st, double* __restrict__ zbar_st, double* __restrict__ zsum_st,
-    uint32_t* __restrict__ raster, const float* __restrict__ wsig, const float* __restrict__ ctab,
-    __nv_bfloat16* __restrict__ c_hi, __nv_bfloat16* __restrict__ c_lo,
-    __nv_bfloat16* __restrict__ w_hi, __nv_bfloat16* __restrict__ w_lo,
-    float2* __restrict__ mdt, float* __restrict__ psis) {
+    uint32_t* __restrict__ raster, const float* __restrict__ wsig, float* __restrict__ psis) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i = blockIdx.x * 32 + lane;
   const bool valid_i = i < P.n;
@@ -116,75 +113,114 @@ __global__ void __launch_bounds__(K1_THREADS) forward_chunk_kernel(
       zsum_st[bi] = zsum;
     }
   }
-  if (P.pass == 0) return;
-
-  // ---- backward scan over the chunk, emitting GEMM operands rho = KR-1 .. 0 ----
-  if (!valid_i) return;
-  const int L = P.len;
-  const long long K = (long long)P.B * P.KR;
-  const long long obase = (long long)i * K + (long long)b * P.KR;
-  const float beta_f = (float)beta, rho_f = (float)P.rho;
-  float lam = 0.f, dcum = 1.f, a_next = 0.f;
-  uint32_t ch[4], cl[4], wh[4], wl[4];  // bf16x2 pairs
-  // software-pipelined psi reads: rows r8 .. r8+8 of the group, next group prefetched
-  float pc[9];
-#pragma unroll
-  for (int q = 0; q < 9; ++q) pc[q] = prow[(long long)(P.KR - 8 + q) * P.n];
-  for (int r8 = P.KR - 8; r8 >= 0; r8 -= 8) {
-    float pn[8];
-    if (r8 >= 8) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) pn[q] = prow[(long long)(r8 - 8 + q) * P.n];
-    }
-    float cv[8], wv[8];
-#pragma unroll
-    for (int u8 = 7; u8 >= 0; --u8) {
-      const int r = r8 + u8;
-      float cval = 0.0f, wval = 0.0f;
-      if (r <= L) {
-        const float psi_prev = pc[u8];  // psi_{r-1}
-        if (r >= 1) cval = ctab[P.t0 + r - 1] * w_sig * psi_prev;  // Lpsi_{r-1}
-        if (P.alif && r < L) {
-          const float psi_r = pc[u8 + 1];
-          const float A = fmaf(-beta_f, psi_prev, rho_f);
-          const float Q = -beta_f * (ctab[P.t0 + r] * w_sig * psi_r);
-          lam = fmaf(a_next, lam, Q);             // Lambda_r (Lambda_L = 0)
-          cval = fmaf(psi_prev, lam, cval);       // + R_r
-          wval = psi_prev * dcum;                 // W_r = P_r D(L-1, r)
-          dcum *= A;
-          a_next = A;
-        }
-      }
-      cv[u8] = cval;
-      wv[u8] = wval;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      split_bf16x2(cv[2 * q], cv[2 * q + 1], ch[q], cl[q]);
-      if (P.alif) split_bf16x2(wv[2 * q], wv[2 * q + 1], wh[q], wl[q]);
-    }
-    *reinterpret_cast<uint4*>(c_hi + obase + r8) = *reinterpret_cast<uint4*>(ch);
-    *reinterpret_cast<uint4*>(c_lo + obase + r8) = *reinterpret_cast<uint4*>(cl);
-    if (P.alif) {
-      *reinterpret_cast<uint4*>(w_hi + obase + r8) = *reinterpret_cast<uint4*>(wh);
-      *reinterpret_cast<uint4*>(w_lo + obase + r8) = *reinterpret_cast<uint4*>(wl);
-    }
-    pc[8] = pc[0];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) pc[q] = pn[q];
-  }
-  if (P.alif) mdt[bi] = make_float2(a_next * lam, dcum);  // M = A_0 Lambda_0, Dt = prod A
 }
 
 // ------------------------------------------------------------------------------------
-// K4: xbar chunk.  Thread per (sample, channel); fp64 recurrence.  Writes the bf16 hi/lo
-// split, K-major over (sample, rho): xh/xl [k_rows][B*KR], rho = 0 -> xbar_{t0-1} (carry),
-// rho = s+1 -> xbar_{t0+s}, zero beyond the chunk.
+// K1s: backward scan over one chunk (pass B).  Thread = (sample, 2 neighbouring neurons):
+// it reads the psi rows K1 parked in the scratch (float2, coalesced, 4 rows prefetched)
+// from rho = L down to 0 and emits the GEMM operands MN-major -- C[b*KR + rho][i] and,
+// when the trace has to be carried to a next chunk, W -- as bf16x2 hi/lo pairs, i.e.
+// 128-byte coalesced stores per warp and row.  fp32 throughout (every output feeds the
+// fp32 / bf16-split gradient path).
 // ------------------------------------------------------------------------------------
-__global__ void xbar_chunk_kernel(const uint8_t* __restrict__ x, long long stride_b, int B,
-                                  int k, int k_rows, int KR, int len, double alpha,
-                                  double* __restrict__ xbar_st, __nv_bfloat16* __restrict__ xh,
-                                  __nv_bfloat16* __restrict__ xl) {
+constexpr int K1S_THREADS = 128;  // 4 warps = 4 samples x 64 neurons
+
+struct ScanLane {
+  float lam = 0.f, dcum = 1.f, a_next = 0.f;
+  // step r: psi_prev = psi_{r-1}, psi_r = psi_r; gains c_prev = c_{r-1}, c_r = c_r
+  __device__ __forceinline__ void step(int r, int L, bool alif, float psi_prev, float psi_r,
+                                       float c_prev, float c_r, float w_sig, float beta,
+                                       float rho, float& cval, float& wval) {
+    cval = 0.f;
+    wval = 0.f;
+    if (r >= 1) cval = c_prev * w_sig * psi_prev;  // L_{r-1} psi_{r-1}
+    if (alif && r < L) {
+      const float A = fmaf(-beta, psi_prev, rho);
+      const float Q = -beta * (c_r * w_sig * psi_r);
+      lam = fmaf(a_next, lam, Q);                  // Lambda_r (Lambda_L = 0)
+      cval = fmaf(psi_prev, lam, cval);            // + R_r
+      wval = psi_prev * dcum;                      // W_r = P_r D(L-1, r)
+      dcum *= A;
+      a_next = A;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
+    FwdParams P, const float* __restrict__ wsig, const float* __restrict__ ctab,
+    uint32_t* __restrict__ c_hi, uint32_t* __restrict__ c_lo, uint32_t* __restrict__ w_hi,
+    uint32_t* __restrict__ w_lo, int ldc, float2* __restrict__ mdt,
+    const float* __restrict__ psis) {
+  extern __shared__ float cs[];  // cs[r] = c_{t0+r-1}, r = 0..L
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int L = P.len;
+  for (int r = threadIdx.x; r <= L; r += K1S_THREADS)
+    cs[r] = (P.t0 + r - 1 >= 0) ? ctab[P.t0 + r - 1] : 0.f;
+  __syncthreads();
+  const int i = blockIdx.x * 64 + 2 * lane;  // this thread's neurons i, i+1
+  const int b = blockIdx.y * (K1S_THREADS / 32) + warp;
+  if (b >= P.B || i >= P.n) return;
+  const bool has2 = i + 1 < P.n;
+  const long long bi = (long long)b * P.n + i;
+  const float ws0 = wsig[bi], ws1 = has2 ? wsig[bi + 1] : 0.f;
+  const float beta = (float)P.beta, rho = (float)P.rho;
+  const bool carry = P.alif && w_hi != nullptr;
+  const float* prow = psis + (long long)b * (P.KR + 1) * P.n + i;
+  auto ldpsi = [&](int r) -> float2 {
+    if (r < 0) return make_float2(0.f, 0.f);
+    return has2 ? *reinterpret_cast<const float2*>(prow + (long long)r * P.n)
+                : make_float2(prow[(long long)r * P.n], 0.f);
+  };
+  const long long ld2 = ldc >> 1;  // row stride in bf16x2 words
+  uint32_t* chp = c_hi + (long long)b * P.KR * ld2 + (i >> 1);
+  uint32_t* clp = c_lo + (long long)b * P.KR * ld2 + (i >> 1);
+  uint32_t* whp = carry ? w_hi + (long long)b * P.KR * ld2 + (i >> 1) : nullptr;
+  uint32_t* wlp = carry ? w_lo + (long long)b * P.KR * ld2 + (i >> 1) : nullptr;
+  for (int r = P.KR - 1; r > L; --r) {  // rows past the chunk
+    chp[r * ld2] = 0u;
+    clp[r * ld2] = 0u;
+    if (carry) { whp[r * ld2] = 0u; wlp[r * ld2] = 0u; }
+  }
+  ScanLane s0, s1;
+  float2 q0 = ldpsi(L), q1 = ldpsi(L - 1), q2 = ldpsi(L - 2), q3 = ldpsi(L - 3);
+  float2 up = make_float2(0.f, 0.f);  // psi row r+1
+  for (int r = L; r >= 0; --r) {
+    const float2 cur = q0;  // psi row r = psi_{r-1}
+    q0 = q1;
+    q1 = q2;
+    q2 = q3;
+    q3 = ldpsi(r - 4);
+    const float c_prev = cs[r], c_r = (r < L) ? cs[r + 1] : 0.f;
+    float c0, w0, c1, w1;
+    s0.step(r, L, P.alif, cur.x, up.x, c_prev, c_r, ws0, beta, rho, c0, w0);
+    s1.step(r, L, P.alif, cur.y, up.y, c_prev, c_r, ws1, beta, rho, c1, w1);
+    uint32_t h, l;
+    split_bf16x2(c0, c1, h, l);
+    chp[r * ld2] = h;
+    clp[r * ld2] = l;
+    if (carry) {
+      split_bf16x2(w0, w1, h, l);
+      whp[r * ld2] = h;
+      wlp[r * ld2] = l;
+    }
+    up = cur;
+  }
+  if (P.alif && mdt != nullptr) {  // M also feeds the last chunk's inter-chunk term
+    mdt[bi] = make_float2(s0.a_next * s0.lam, s0.dcum);  // M = A_0 Lambda_0, Dt = prod A
+    if (has2) mdt[bi + 1] = make_float2(s1.a_next * s1.lam, s1.dcum);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K4: xbar chunk.  Thread per (sample, channel); fp64 recurrence; the 8 input bytes of a
+// group are loaded before the dependent chain.  Writes the bf16 hi/lo split, K-major over
+// (sample, rho): xh/xl [k_rows][B*KR], rho = 0 -> xbar_{t0-1} (carry), rho = s+1 ->
+// xbar_{t0+s}, zero beyond the chunk.
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) xbar_chunk_kernel(
+    const uint8_t* __restrict__ x, long long stride_b, int B, int k, int k_rows, int KR, int len,
+    double alpha, double* __restrict__ xbar_st, __nv_bfloat16* __restrict__ xh,
+    __nv_bfloat16* __restrict__ xl) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (j >= k_rows) return;
@@ -192,23 +228,33 @@ __global__ void xbar_chunk_kernel(const uint8_t* __restrict__ x, long long strid
   double xb = valid ? xbar_st[(long long)b * k + j] : 0.0;
   const long long K = (long long)B * KR;
   const uint8_t* xin = x + (long long)b * stride_b + j;
-  __nv_bfloat16 hv[8], lv[8];
+  uint4* oh = reinterpret_cast<uint4*>(xh + (long long)j * K + (long long)b * KR);
+  uint4* ol = reinterpret_cast<uint4*>(xl + (long long)j * K + (long long)b * KR);
   for (int r8 = 0; r8 < KR; r8 += 8) {
+    uint32_t xv[8];
 #pragma unroll
     for (int u8 = 0; u8 < 8; ++u8) {
       const int rho = r8 + u8;
-      float v = 0.0f;
-      if (rho == 0) {
-        v = (float)xb;
-      } else if (rho <= len) {
-        if (valid) xb = __dadd_rn(__dmul_rn(alpha, xb), (double)xin[(long long)(rho - 1) * k]);
-        v = (float)xb;
-      }
-      split_bf16(v, hv[u8], lv[u8]);
+      xv[u8] = (valid && rho >= 1 && rho <= len) ? xin[(long long)(rho - 1) * k] : 0u;
     }
-    const long long off = (long long)j * K + (long long)b * KR + r8;
-    *reinterpret_cast<uint4*>(xh + off) = *reinterpret_cast<uint4*>(hv);
-    *reinterpret_cast<uint4*>(xl + off) = *reinterpret_cast<uint4*>(lv);
+    float v[8];
+#pragma unroll
+    for (int u8 = 0; u8 < 8; ++u8) {
+      const int rho = r8 + u8;
+      float vv = 0.0f;
+      if (rho == 0) {
+        vv = (float)xb;
+      } else if (rho <= len) {
+        xb = __dadd_rn(__dmul_rn(alpha, xb), (double)xv[u8]);
+        vv = (float)xb;
+      }
+      v[u8] = vv;
+    }
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) split_bf16x2(v[2 * q], v[2 * q + 1], h[q], l[q]);
+    oh[r8 / 8] = make_uint4(h[0], h[1], h[2], h[3]);
+    ol[r8 / 8] = make_uint4(l[0], l[1], l[2], l[3]);
   }
   if (valid) xbar_st[(long long)b * k + j] = xb;
 }
@@ -223,7 +269,7 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
                       int T, double alpha, double theta, double slope, double beta, double rho,
                       double kappa, int reset, int alif, double* u, double* a, double* zbar,
                       double* zsum, uint32_t* raster, const float* wsig, const float* ctab,
-                      void* c_hi, void* c_lo, void* w_hi, void* w_lo, float* mdt,
+                      void* c_hi, void* c_lo, void* w_hi, void* w_lo, int ldc, float* mdt,
                       float* psi_scratch, cudaStream_t stream) {
   SPB_CHECK_ARG(pass == 0 || pass == 1, "spb_forward_chunk: pass must be 0 (A) or 1 (B)");
   SPB_CHECK_ARG(cur && u && a, "spb_forward_chunk: null pointer");
@@ -231,16 +277,23 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
                 "spb_forward_chunk: bad sizes B=%d n=%d Tc=%d KR=%d len=%d", B, n, Tc, KR, len);
   SPB_CHECK_ARG(pass == 0 ? (zbar && zsum) : (wsig && ctab && c_hi && c_lo && psi_scratch),
                 "spb_forward_chunk: missing pass-%c buffers", pass ? 'B' : 'A');
-  SPB_CHECK_ARG(!(pass == 1 && alif && (!w_hi || !w_lo || !mdt)),
-                "spb_forward_chunk: ALIF pass B needs w_hi, w_lo and mdt");
+  SPB_CHECK_ARG(!(pass == 1 && alif && (!mdt || (w_hi && !w_lo))),
+                "spb_forward_chunk: ALIF pass B needs mdt (and w_lo with w_hi)");
+  SPB_CHECK_ARG(pass == 0 || (ldc >= n && ldc % 8 == 0), "spb_forward_chunk: ldc must be >= n, %% 8");
   SPB_CHECK_ARG(!(pass == 1 && reset), "spb_forward_chunk: reset=True has no two-pass form");
   FwdParams P{B, n, Tc, KR, len, t0, T, alpha, theta, slope, beta, rho, kappa, reset, alif, pass};
   dim3 grid(ceil_div(n, 32), ceil_div(B, K1_THREADS / 32));
-  forward_chunk_kernel<<<grid, K1_THREADS, 0, stream>>>(
-      P, cur, u, a, zbar, zsum, raster, wsig, ctab, reinterpret_cast<__nv_bfloat16*>(c_hi),
-      reinterpret_cast<__nv_bfloat16*>(c_lo), reinterpret_cast<__nv_bfloat16*>(w_hi),
-      reinterpret_cast<__nv_bfloat16*>(w_lo), reinterpret_cast<float2*>(mdt), psi_scratch);
+  forward_chunk_kernel<<<grid, K1_THREADS, 0, stream>>>(P, cur, u, a, zbar, zsum, raster, wsig,
+                                                        psi_scratch);
   SPB_CHECK_LAUNCH("forward_chunk");
+  if (pass == 1) {
+    dim3 sgrid(ceil_div(n, 64), ceil_div(B, K1S_THREADS / 32));
+    chunk_scan_kernel<<<sgrid, K1S_THREADS, (len + 1) * sizeof(float), stream>>>(
+        P, wsig, ctab, reinterpret_cast<uint32_t*>(c_hi), reinterpret_cast<uint32_t*>(c_lo),
+        reinterpret_cast<uint32_t*>(w_hi), reinterpret_cast<uint32_t*>(w_lo), ldc,
+        reinterpret_cast<float2*>(mdt), psi_scratch);
+    SPB_CHECK_LAUNCH("chunk_scan");
+  }
   return 0;
 }
 

@@ -1,7 +1,8 @@
 // K5: factorised e-prop gradient GEMM on 5th-generation tensor cores (tcgen05 + TMA).
 //
-//   grad[i][j] += sum_K A[i][K] * B[j][K],   A = L_t psi_t  (M = n neurons),
-//                                            B = xbar_t     (N = k inputs),
+//   grad[i][j] += sum_K A[K][i] * B[j][K],   A = chunk coefficients C (M = n neurons,
+//                                            MN-major: neurons contiguous, as K1s writes)
+//                                            B = xbar_t     (N = k inputs, K-major),
 //   K = (sample, step) pairs of one time chunk (K = B*Tc), so the LIF trace psi (x) xbar
 //   (gradients.py:165-172, G_u = 1 (x) xbar) is never materialised per sample.
 //
@@ -9,7 +10,8 @@
 // and D += Ah*Bh + Ah*Bl + Al*Bh (the lo*lo term is below fp32 rounding of the sum).
 //
 // Structure (one 128x128 output tile per CTA, split-K over blockIdx.z):
-//   warp 0   TMA producer: 4 tiles (Ah, Al, Bh, Bl; 128x64 bf16, SWIZZLE_128B) per stage
+//   warp 0   TMA producer: Ah, Al (two 64x64 MN-major boxes each), Bh, Bl (128x64 K-major),
+//            all SWIZZLE_128B, per stage
 //   warp 1   TMEM allocation + single-thread tcgen05.mma issue (12 MMAs of 128x128x16 per
 //            64-wide K block), tcgen05.commit releases smem stages / signals the epilogue
 //   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 -> fp32 partial tile (fixed-order reduce later)
@@ -37,9 +39,20 @@ __device__ __forceinline__ uint64_t umma_desc_k_sw128(uint32_t saddr) {
   d |= (uint64_t)2u << 61;             // SWIZZLE_128B
   return d;
 }
-// Instruction descriptor: kind::f16, A/B bf16 K-major, D fp32, M=BM, N=BN.
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+// MN-major, SWIZZLE_128B: 64-element MN runs (128 B rows, one per K), 8-row K groups
+// 1024 B apart (SBO), the second 64-element MN half 8 KB further (LBO).
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(8192u >> 4) << 16;   // LBO: next 64-wide MN block
+  d |= (uint64_t)(1024u >> 4) << 32;   // SBO: next 8-row K group
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+// Instruction descriptor: kind::f16, A bf16 MN-major (bit 15), B bf16 K-major, D fp32.
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
@@ -107,8 +120,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
         const uint32_t fb = smem_u32(&full[s]);
         mbar_expect_tx(fb, STAGE_BYTES);
-        tma_load_2d(st, &tm_ah, fb, kb * BK, m0);
-        tma_load_2d(st + TILE_A, &tm_al, fb, kb * BK, m0);
+        tma_load_2d(st, &tm_ah, fb, m0, kb * BK);
+        tma_load_2d(st + TILE_A / 2, &tm_ah, fb, m0 + 64, kb * BK);
+        tma_load_2d(st + TILE_A, &tm_al, fb, m0, kb * BK);
+        tma_load_2d(st + TILE_A + TILE_A / 2, &tm_al, fb, m0 + 64, kb * BK);
         tma_load_2d(st + 2 * TILE_A, &tm_bh, fb, kb * BK, n0);
         tma_load_2d(st + 2 * TILE_A + TILE_B, &tm_bl, fb, kb * BK, n0);
       }
@@ -125,8 +140,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                        sbl = st + 2 * TILE_A + TILE_B;
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint32_t off = kk * 32;  // 16 bf16 along K inside the 128-byte swizzle row
-          const uint64_t dah = umma_desc_k_sw128(sah + off), dal = umma_desc_k_sw128(sal + off);
+          const uint32_t off = kk * 32;     // 16 bf16 along K inside the 128-byte swizzle row
+          const uint32_t offa = kk * 2048;  // 16 K rows of the MN-major A tile
+          const uint64_t dah = umma_desc_mn_sw128(sah + offa), dal = umma_desc_mn_sw128(sal + offa);
           const uint64_t dbh = umma_desc_k_sw128(sbh + off), dbl = umma_desc_k_sw128(sbl + off);
           umma_bf16(tmem_base, dah, dbh, (kb > kb0 || kk > 0) ? 1u : 0u);
           umma_bf16(tmem_base, dah, dbl, 1u);
@@ -189,6 +205,11 @@ static bool make_map(CUtensorMap* map, const void* ptr, int K, int rows, int box
   return make_tmap_2d(map, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)K, (uint64_t)rows,
                       (uint64_t)K * 2, BK, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
+// 2-D bf16 MN-major operand [K][ld] (M contiguous) with 64 x 64 boxes, 128-byte swizzle.
+static bool make_map_mn(CUtensorMap* map, const void* ptr, int M, int ld, int K) {
+  return make_tmap_2d(map, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)M, (uint64_t)K,
+                      (uint64_t)ld * 2, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B);
+}
 
 }  // namespace tc
 
@@ -229,20 +250,21 @@ using namespace spb;
 extern "C" {
 
 // Split-K tensor-core GEMM writing fp32 partial tiles:
-//   partial[z][i][j] = sum_{K in split z} (Ah+Al)[i][K] (Bh+Bl)[j][K]   (lo*lo dropped)
+//   partial[z][i][j] = sum_{K in split z} (Ah+Al)[K][i] (Bh+Bl)[j][K]   (lo*lo dropped)
 // for i < M, j < ldp; every one of the `splits` slices is written (empty K ranges give 0).
 // Reduced in fixed order with spb_reduce_partials.
-int spb_grad_gemm_partials(const void* ah, const void* al, const void* bh, const void* bl, int M,
-                           int N_rows, int K, int splits, float* partial, int ldp,
+int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* bh, const void* bl,
+                           int M, int N_rows, int K, int splits, float* partial, int ldp,
                            long long slice_stride, cudaStream_t stream) {
   SPB_CHECK_ARG(ah && al && bh && bl && partial, "spb_grad_gemm_partials: null pointer");
-  SPB_CHECK_ARG(M > 0 && N_rows > 0 && K > 0 && K % 8 == 0 && splits > 0 && ldp >= 1,
-                "spb_grad_gemm_partials: bad sizes M=%d N=%d K=%d", M, N_rows, K);
+  SPB_CHECK_ARG(M > 0 && N_rows > 0 && K > 0 && K % 8 == 0 && splits > 0 && ldp >= 1 &&
+                    lda >= M && lda % 8 == 0,
+                "spb_grad_gemm_partials: bad sizes M=%d lda=%d N=%d K=%d", M, lda, N_rows, K);
   SPB_CHECK_ARG((reinterpret_cast<uintptr_t>(ah) | reinterpret_cast<uintptr_t>(al) |
                  reinterpret_cast<uintptr_t>(bh) | reinterpret_cast<uintptr_t>(bl)) % 16 == 0,
                 "spb_grad_gemm_partials: operands must be 16-byte aligned");
   CUtensorMap mah, mal, mbh, mbl;
-  if (!tc::make_map(&mah, ah, K, M, tc::BM) || !tc::make_map(&mal, al, K, M, tc::BM) ||
+  if (!tc::make_map_mn(&mah, ah, M, lda, K) || !tc::make_map_mn(&mal, al, M, lda, K) ||
       !tc::make_map(&mbh, bh, K, N_rows, tc::BN) || !tc::make_map(&mbl, bl, K, N_rows, tc::BN)) {
     set_error("spb_grad_gemm_partials: cuTensorMapEncodeTiled failed");
     return 3;

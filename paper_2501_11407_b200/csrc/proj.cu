@@ -378,18 +378,36 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // x chunk -> zero-padded K-major operand rows (16-byte aligned rows for TMA).
+// One warp per output row (sample b, step s): 16-byte stores of the zero-padded row; the
+// source row (k bytes, any alignment) is read with 4-byte loads when k % 4 == 0.
 __global__ void pack_spikes_kernel(const uint8_t* __restrict__ x, long long stride_b, int k, int len,
                                    int Tc, int Kpad, int B, uint8_t* __restrict__ xq) {
-  const long long total = (long long)B * Tc * Kpad;
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(idx % Kpad);
-    const long long row = idx / Kpad;
+  const int lane = threadIdx.x & 31;
+  const long long rows = (long long)B * Tc;
+  const bool w4 = (k & 3) == 0 && (stride_b & 3) == 0 &&
+                  (reinterpret_cast<uintptr_t>(x) & 3) == 0;
+  for (long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += (long long)gridDim.x * (blockDim.x >> 5)) {
     const int s = (int)(row % Tc);
     const int b = (int)(row / Tc);
-    uint8_t v = 0;
-    if (j < k && s < len) v = x[(long long)b * stride_b + (long long)s * k + j];
-    xq[idx] = v;
+    const uint8_t* src = x + (long long)b * stride_b + (long long)s * k;
+    uint4* dst = reinterpret_cast<uint4*>(xq + row * Kpad);
+    const bool live = s < len;
+    for (int c = lane; c < Kpad / 16; c += 32) {
+      const int j0 = c * 16;
+      uint32_t wv[4] = {0u, 0u, 0u, 0u};
+      if (live) {
+        if (w4 && j0 + 16 <= k) {
+          const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src + j0);
+          wv[0] = s4[0]; wv[1] = s4[1]; wv[2] = s4[2]; wv[3] = s4[3];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (j0 + q < k) wv[q >> 2] |= (uint32_t)src[j0 + q] << (8 * (q & 3));
+        }
+      }
+      dst[c] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    }
   }
 }
 
@@ -430,8 +448,8 @@ int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int len,
   SPB_CHECK_ARG(x && xq && B > 0 && k > 0 && Kpad >= k && Kpad % proj::BK == 0 && len >= 0 &&
                     len <= Tc,
                 "spb_pack_spikes: bad args (Kpad must be a multiple of %d)", proj::BK);
-  const long long total = (long long)B * Tc * Kpad;
-  const long long want = (total + 255) / 256;
+  const long long rows = (long long)B * Tc;
+  const long long want = (rows + 7) / 8;
   const int blocks = (int)(want < 148LL * 16 ? want : 148LL * 16);
   proj::pack_spikes_kernel<<<blocks, 256, 0, stream>>>(x, stride_b, k, len, Tc, Kpad, B, xq);
   SPB_CHECK_LAUNCH("pack_spikes");

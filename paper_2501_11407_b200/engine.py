@@ -131,8 +131,9 @@ class EpropEngine:
         self.correct = torch.empty(B, dtype=torch.int32, device=dev)
         # pass-B chunk operands (bf16 hi/lo, K-major over (sample, rho))
         self.psi = torch.zeros((B, self.KR + 1, n), dtype=f32, device=dev)   # K1 scan scratch
-        self.c_hi = torch.empty((n, K), dtype=bf16, device=dev)
-        self.c_lo = torch.empty((n, K), dtype=bf16, device=dev)
+        self.ldc = _round_up(n, 8)   # C/W are MN-major [K][ldc] (neurons contiguous)
+        self.c_hi = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
+        self.c_lo = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
         self.xbar_state = torch.empty((B, k), dtype=f64, device=dev)
         self.xh = torch.zeros((self.kp, K), dtype=bf16, device=dev)
         self.xl = torch.zeros((self.kp, K), dtype=bf16, device=dev)
@@ -140,8 +141,8 @@ class EpropEngine:
         tiles5 = (self.kp // 128) * math.ceil(n / 128)
         self.splits5 = max(1, min(K // 64, round(sms / tiles5)))
         if self.alif:
-            self.w_hi = torch.empty((n, K), dtype=bf16, device=dev)
-            self.w_lo = torch.empty((n, K), dtype=bf16, device=dev)
+            self.w_hi = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
+            self.w_lo = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
             self.mdt = torch.empty((B, n, 2), dtype=f32, device=dev)
             self.eps = torch.zeros((B, self.n_pad, self.ke), dtype=f32, device=dev)
             tiles6 = (self.kp // 128) * (self.n_pad // 128)
@@ -264,7 +265,7 @@ class EpropEngine:
                  *common, v(self.u.data_ptr()), v(self.a.data_ptr()),
                  v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
                  v(raster.data_ptr()) if raster is not None else None,
-                 None, None, None, None, None, None, None, None, st)
+                 None, None, None, None, None, None, 0, None, None, st)
             self.launches += 3
         # ---------------- readout / loss ----------------
         call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
@@ -284,26 +285,28 @@ class EpropEngine:
             ln = min(Tc, T - t0)
             last = c == nchunks - 1
             xp = x.data_ptr() + t0 * k
-            self._project(xp, strideb, ln, st, timed)
+            if nchunks > 1:  # one chunk: cur of pass A is still valid (same W, same x)
+                self._project(xp, strideb, ln, st, timed)
+            carry_out = self.alif and not last   # the trace is only needed by a later chunk
             timed("forward", ln, "spb_forward_chunk", 1, v(self.cur.data_ptr()), B, n, Tc, KR,
                   ln, t0, T, *common, v(self.u.data_ptr()), v(self.a.data_ptr()), None, None,
                   None, v(self.wsig.data_ptr()), v(ctab.data_ptr()),
                   v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()),
-                  v(self.w_hi.data_ptr()) if self.alif else None,
-                  v(self.w_lo.data_ptr()) if self.alif else None,
+                  v(self.w_hi.data_ptr()) if carry_out else None,
+                  v(self.w_lo.data_ptr()) if carry_out else None, self.ldc,
                   v(self.mdt.data_ptr()) if self.alif else None, v(self.psi.data_ptr()), st)
             call("spb_xbar_chunk", v(xp), strideb, B, k, self.kp, KR, ln, float(alpha),
                  v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()), v(self.xl.data_ptr()), st)
             timed("gemm", ln, "spb_grad_gemm_partials", v(self.c_hi.data_ptr()),
-                  v(self.c_lo.data_ptr()), v(self.xh.data_ptr()), v(self.xl.data_ptr()), n,
+                  v(self.c_lo.data_ptr()), self.ldc, v(self.xh.data_ptr()), v(self.xl.data_ptr()), n,
                   self.kp, K, self.splits5, v(self.partial.data_ptr()), self.kp, slice_stride,
                   st)
-            self.launches += 5
+            self.launches += 6 if nchunks > 1 else 4
             slices = self.splits5
             if self.alif and (c > 0 or not last):
                 # first chunk: E0 = 0 (nothing to add, only carry); last chunk: no carry
                 timed("carry", (ln, c > 0, not last), "spb_alif_carry_chunk",
-                      v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()), v(self.xh.data_ptr()),
+                      v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()), self.ldc, v(self.xh.data_ptr()),
                       v(self.xl.data_ptr()), v(self.mdt.data_ptr()), v(self.eps.data_ptr()),
                       v(part6), B, n, self.n_pad, k, self.ke, self.kp, KR, self.splits6,
                       int(not last), int(c > 0), int(not last), st)

@@ -65,11 +65,11 @@ def test_bad_arguments_are_rejected_without_gpu():
     with pytest.raises(P.ShapeMismatch):
         _lib.call("spb_forward_chunk", 2, None, 1, 1, 63, 64, 1, 0, 1,
                   0.95, 1.0, 10.0, 0.0, 0.0, 0.95, 0, 0, None, None, None, None, None, None,
-                  None, None, None, None, None, None, None, None)
+                  None, None, None, None, None, 8, None, None, None)
     with pytest.raises(P.ShapeMismatch):
         _lib.call("spb_input_proj", None, None, None, 1, 1, 32, 100, 7, None, 148, None)
     with pytest.raises(P.ShapeMismatch):
-        _lib.call("spb_alif_carry_chunk", None, None, None, None, None, None, None, 1, 1, 100,
+        _lib.call("spb_alif_carry_chunk", None, None, 8, None, None, None, None, None, 1, 1, 100,
                   1, 4, 128, 64, 1, 0, 0, 0, None)
 
 
@@ -105,8 +105,9 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     names = [c[0] for c in rec.calls]
     nch = (T + chunk - 1) // chunk
     assert names.count("spb_forward_chunk") == 2 * nch
-    assert names.count("spb_pack_spikes") == 2 * nch
-    assert names.count("spb_input_proj") == 2 * nch
+    # a single chunk reuses pass A's current in pass B
+    assert names.count("spb_pack_spikes") == (2 * nch if nch > 1 else 1)
+    assert names.count("spb_input_proj") == (2 * nch if nch > 1 else 1)
     assert names.count("spb_slice_weights") == 0
     assert names.count("spb_xbar_chunk") == nch
     assert names.count("spb_grad_gemm_partials") == nch
@@ -115,14 +116,16 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
         # no carry launch for a single chunk; chunk 0 only carries, the last only adds M E0
         assert len(carries) == (nch if nch > 1 else 0)
         if carries:
-            do_mma, load, store = [(e[15], e[16], e[17]) for e in carries][0]
-            assert (do_mma, load, store) == (1, 0, 1)
-            assert [(e[15], e[16], e[17]) for e in carries][-1] == (0, 1, 0)
-            assert all((e[15], e[16], e[17]) == (1, 1, 1) for e in carries[1:-1])
+            flags = [(e[16], e[17], e[18]) for e in carries]   # do_mma, load_eps, store_eps
+            assert flags[0] == (1, 0, 1)
+            assert flags[-1] == (0, 1, 0)
+            assert all(f == (1, 1, 1) for f in flags[1:-1])
     else:
         assert not carries
     assert names.count("spb_readout_loss") == 1
-    assert eng.launches == len(rec.calls) - 0
+    # spb_forward_chunk pass B launches two kernels (dynamics + chunk scan)
+    passb = sum(1 for c in rec.calls if c[0] == "spb_forward_chunk" and c[1][0] == 1)
+    assert eng.launches == len(rec.calls) + passb
 
 
 def test_engine_rejects_bad_inputs():
