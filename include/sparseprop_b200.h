@@ -59,7 +59,11 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
  *     (graph.py:40-52) + the readout spike filter (gradients.py:173-174).
  *     u, a    [B][n] fp64 state, carried across chunks (zero at t=0)
  *     pass 0 (A): zbar, zsum [B][n] fp64 carried; raster [B][T][ceil(n/32)] bit-packed
- *                 spikes (optional, may be NULL).
+ *                 spikes (optional, may be NULL); psi_scratch optional: when given, the
+ *                 surrogate rows are parked exactly as pass B does (one-chunk sequences
+ *                 then run pass 2 instead of pass 1).
+ *     pass 2 (B scan only): the pass-B outputs below from a psi_scratch already filled
+ *                 by pass A of the same chunk (no dynamics kernel; cur/u/a unused).
  *     pass 1 (B): wsig [B][n] = W_out^T g; ctab[T] fp32 readout gains c_t.  A backward scan
  *                 over the chunk (second kernel) emits, MN-major (neurons contiguous,
  *                 row stride ldc >= n, ldc % 8 == 0) over (sample b, row rho < KR):
@@ -78,9 +82,10 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
 
 /* K4  Presynaptic filter xbar_t = alpha*xbar_{t-1} + x_t (the factorised LIF trace G_u,
  *     gradients.py:89-94 with H_I = alpha, F rows = x_t; test_gradients.py:81-91).
- *     xbar_state [B][k] fp64 carry; xh/xl [k_rows][B*KR] bf16 hi/lo split, K-major:
- *     row rho = 0 holds xbar_{t0-1}, rho = s+1 holds xbar_{t0+s}; zero elsewhere. */
-int spb_xbar_chunk(const uint8_t* x, long long stride_b, int B, int k, int k_rows, int KR,
+ *     xbar_state [B][k] fp64 carry; xh/xl [B*KR][kp] bf16 hi/lo split, MN-major (channels
+ *     contiguous, kp >= k, kp % 8 == 0): row b*KR + rho, rho = 0 holds xbar_{t0-1},
+ *     rho = s+1 holds xbar_{t0+s}; zero elsewhere. */
+int spb_xbar_chunk(const uint8_t* x, long long stride_b, int B, int k, int kp, int KR,
                    int len, double alpha, double* xbar_state, void* xh, void* xl,
                    cudaStream_t stream);
 
@@ -98,25 +103,26 @@ int spb_readout_grad(const double* g, const double* zsum, int B, int n, int m, d
 
 /* K5  Chunk gradient GEMM on tcgen05 tensor cores (TMA-fed, bf16 hi/lo split, fp32
  *     TMEM accumulation), split-K over `splits` CTAs per 128x128 tile:
- *       partial[z][i][j] = sum_{K in split z} (Ah+Al)[K][i] (Bh+Bl)[j][K]  (i<M, j<ldp)
+ *       partial[z][i][j] = sum_{K in split z} (Ah+Al)[K][i] (Bh+Bl)[K][j]  (i<M, j<ldp)
  *     at partial + z*slice_stride (row stride ldp); every slice is written.
  *     With A = C (K1) and B = xbar (K4) this is every intra-chunk gradient term: the
  *     factorisable LIF part G_u = 1 (x) xbar and the intra-chunk ALIF part.  Replaces the
  *     xbar/xsum n x k accumulation of gradients.py:165-172,180.  A* [K][lda] MN-major
- *     (lda >= M, lda % 8 == 0), B* [N_rows][K] K-major; 16-byte aligned, K % 8 == 0. */
+ *     (lda >= M, lda % 8 == 0), B* [K][ldb] MN-major (ldb >= N_rows, ldb % 8 == 0);
+ *     16-byte aligned, K % 8 == 0. */
 int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* bh, const void* bl,
-                           int M, int N_rows, int K, int splits, float* partial, int ldp,
+                           int ldb, int M, int N_rows, int K, int splits, float* partial, int ldp,
                            long long slice_stride, cudaStream_t stream);
 
 /* K5s CUDA-core version of K5 on the same operands (test cross-check only). */
 int spb_grad_gemm_simt(const void* ah, const void* al, int lda, const void* bh, const void* bl,
-                       int M, int N, int K, double* grad, int ldg, cudaStream_t stream);
+                       int ldb, int M, int N, int K, double* grad, int ldg, cudaStream_t stream);
 
 /* K6  ALIF adaptation trace carried across chunks on tcgen05 tensor cores (elig.cu):
  *       E_end[b,i,:] = Dt[b,i] E0[b,i,:] + sum_rho W_rho[b,i] xbar_rho[b,:]   (if do_mma)
  *       partial[z][i][j] = sum_{b in split z} M[b,i] E0[b,i,j]
  *     eps [B][n_pad][ke] fp32 (E0 read if load_eps, E_end written if store_eps), w* the K1s
- *     operand [B*KR][ldw] (MN-major), x* the K4 operand [kp][B*KR], mdt from K1s;
+ *     operand [B*KR][ldw] and x* the K4 operand [B*KR][kp] (both MN-major), mdt from K1s;
  *     partial [splits][n_pad][kp].
  *     n_pad % 128 == 0, kp % 128 == 0, ke % 4 == 0, KR % 64 == 0.  Replaces the ALIF G_a
  *     block of eprop_trace_update (gradients.py:89-94) and x_step (gradients.py:165-167). */

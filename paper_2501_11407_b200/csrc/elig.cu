@@ -32,8 +32,8 @@ constexpr int STAGE = 4 * TILE;
 constexpr int EPI_WARPS = 16;  // 4 TMEM lane quarters x 4 column groups of 32
 constexpr int THREADS = 64 + EPI_WARPS * 32;
 constexpr int SMEM = STAGES * STAGE + 1024 + 256;
-// A = W (MN-major: neurons contiguous, written by K1s), B = xbar (K-major)
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+// A = W, B = xbar, both MN-major (neurons / channels contiguous, written by K1s / K4)
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
 __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr) {
@@ -159,8 +159,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           tma_load_2d(st + TILE / 2, &tm_wh, fb, i0 + 64, kbase + kb * BK);
           tma_load_2d(st + TILE, &tm_wl, fb, i0, kbase + kb * BK);
           tma_load_2d(st + TILE + TILE / 2, &tm_wl, fb, i0 + 64, kbase + kb * BK);
-          tma_load_2d(st + 2 * TILE, &tm_xh, fb, kbase + kb * BK, j0);
-          tma_load_2d(st + 3 * TILE, &tm_xl, fb, kbase + kb * BK, j0);
+          tma_load_2d(st + 2 * TILE, &tm_xh, fb, j0, kbase + kb * BK);
+          tma_load_2d(st + 2 * TILE + TILE / 2, &tm_xh, fb, j0 + 64, kbase + kb * BK);
+          tma_load_2d(st + 3 * TILE, &tm_xl, fb, j0, kbase + kb * BK);
+          tma_load_2d(st + 3 * TILE + TILE / 2, &tm_xl, fb, j0 + 64, kbase + kb * BK);
         }
       }
     }
@@ -181,8 +183,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint32_t off = kk * 32, offw = kk * 2048;
             const uint64_t dwh = desc_mn_sw128(st + offw), dwl = desc_mn_sw128(st + TILE + offw);
-            const uint64_t dxh = desc_k_sw128(st + 2 * TILE + off),
-                           dxl = desc_k_sw128(st + 3 * TILE + off);
+            const uint64_t dxh = desc_mn_sw128(st + 2 * TILE + offw),
+                           dxl = desc_mn_sw128(st + 3 * TILE + offw);
             mma_bf16(d, dwh, dxh, (kb | kk) ? 1u : 0u);
             mma_bf16(d, dwh, dxl, 1u);
             mma_bf16(d, dwl, dxh, 1u);
@@ -278,11 +280,11 @@ __global__ void reduce_partials_kernel(const float* __restrict__ partial, int S,
 }
 
 // CUDA-core GEMM on the same bf16 hi/lo operands as the tensor-core path:
-// grad[i][j] += sum_K (Ah+Al)[K][i] * (Bh+Bl)[j][K]  (64x64 tiles, 4x4 per thread).
+// grad[i][j] += sum_K (Ah+Al)[K][i] * (Bh+Bl)[K][j]  (64x64 tiles, 4x4 per thread).
 __global__ void __launch_bounds__(256) grad_gemm_simt_kernel(
     const __nv_bfloat16* __restrict__ ah, const __nv_bfloat16* __restrict__ al, int lda,
-    const __nv_bfloat16* __restrict__ bh, const __nv_bfloat16* __restrict__ bl, int M, int N,
-    int K, double* __restrict__ grad, int ldg) {
+    const __nv_bfloat16* __restrict__ bh, const __nv_bfloat16* __restrict__ bl, int ldb, int M,
+    int N, int K, double* __restrict__ grad, int ldg) {
   __shared__ float As[32][65];
   __shared__ float Bs[32][65];
   const int tid = threadIdx.x;
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(256) grad_gemm_simt_kernel(
         va = __bfloat162float(ah[o]) + __bfloat162float(al[o]);
       }
       if (n0 + r < N && k0 + kk < K) {
-        const long long o = (long long)(n0 + r) * K + k0 + kk;
+        const long long o = (long long)(k0 + kk) * ldb + n0 + r;
         vb = __bfloat162float(bh[o]) + __bfloat162float(bl[o]);
       }
       As[kk][r] = va;
@@ -355,10 +357,10 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
                      carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
         make_tmap_2d(&mwl, wl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, K, (uint64_t)ldw * 2, 64,
                      carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
-        make_tmap_2d(&mxh, xh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, kp, K * 2, carry::BK,
-                     carry::BN, CU_TENSOR_MAP_SWIZZLE_128B) &&
-        make_tmap_2d(&mxl, xl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K, kp, K * 2, carry::BK,
-                     carry::BN, CU_TENSOR_MAP_SWIZZLE_128B);
+        make_tmap_2d(&mxh, xh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kp, K, (uint64_t)kp * 2, 64,
+                     carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
+        make_tmap_2d(&mxl, xl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kp, K, (uint64_t)kp * 2, 64,
+                     carry::BK, CU_TENSOR_MAP_SWIZZLE_128B);
     if (!ok) {
       set_error("spb_alif_carry_chunk: cuTensorMapEncodeTiled failed");
       return 3;
@@ -387,13 +389,14 @@ int spb_reduce_partials(const float* partial, int splits, int n, int n_pad, int 
 }
 
 int spb_grad_gemm_simt(const void* ah, const void* al, int lda, const void* bh, const void* bl,
-                       int M, int N, int K, double* grad, int ldg, cudaStream_t stream) {
-  SPB_CHECK_ARG(ah && al && bh && bl && grad && M > 0 && N > 0 && K > 0 && ldg >= N && lda >= M,
+                       int ldb, int M, int N, int K, double* grad, int ldg, cudaStream_t stream) {
+  SPB_CHECK_ARG(ah && al && bh && bl && grad && M > 0 && N > 0 && K > 0 && ldg >= N && lda >= M &&
+                    ldb >= N,
                 "spb_grad_gemm_simt: bad args");
   dim3 grid(ceil_div(N, 64), ceil_div(M, 64));
   grad_gemm_simt_kernel<<<grid, 256, 0, stream>>>(
       (const __nv_bfloat16*)ah, (const __nv_bfloat16*)al, lda, (const __nv_bfloat16*)bh,
-      (const __nv_bfloat16*)bl, M, N, K, grad, ldg);
+      (const __nv_bfloat16*)bl, ldb, M, N, K, grad, ldg);
   SPB_CHECK_LAUNCH("grad_gemm_simt");
   return 0;
 }

@@ -73,8 +73,11 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
   // expression from the same state, gradients.py:159): carry it.
   double d_prev = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
   const float slope = (float)P.slope;
-  float* prow = psis + (long long)b * (P.KR + 1) * P.n + i;  // pass B: psi of row rho at prow[rho*n]
-  if (P.pass == 1 && valid_i) prow[0] = surrogate_grad_f32((float)d_prev, slope);  // psi_{t0-1}
+  // psi of row rho at prow[rho*n] (pass B; optional in pass A, which lets a one-chunk
+  // sequence skip the pass-B dynamics entirely)
+  const bool park = psis != nullptr && valid_i;
+  float* prow = psis != nullptr ? psis + (long long)b * (P.KR + 1) * P.n + i : nullptr;
+  if (park) prow[0] = surrogate_grad_f32((float)d_prev, slope);  // psi_{t0-1}
   for (int s8 = 0; s8 < P.len; s8 += 8) {
     double Ib[8];
 #pragma unroll
@@ -97,10 +100,9 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
           const unsigned bal = __ballot_sync(0xffffffffu, z && valid_i);
           if (raster != nullptr && lane == 0)
             raster[((long long)b * P.T + P.t0 + s) * nw + blockIdx.x] = bal;
-        } else {
-          // the surrogate only scales fp32 eligibilities: evaluate it in fp32
-          if (valid_i) prow[(long long)(s + 1) * P.n] = surrogate_grad_f32((float)d, slope);
         }
+        // the surrogate only scales fp32 eligibilities: evaluate it in fp32
+        if (park) prow[(long long)(s + 1) * P.n] = surrogate_grad_f32((float)d, slope);
         d_prev = d;
       }
     }
@@ -212,51 +214,57 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
 }
 
 // ------------------------------------------------------------------------------------
-// K4: xbar chunk.  Thread per (sample, channel); fp64 recurrence; the 8 input bytes of a
-// group are loaded before the dependent chain.  Writes the bf16 hi/lo split, K-major over
-// (sample, rho): xh/xl [k_rows][B*KR], rho = 0 -> xbar_{t0-1} (carry), rho = s+1 ->
-// xbar_{t0+s}, zero beyond the chunk.
+// K4: xbar chunk.  Thread per (sample, 2 neighbouring channels); fp64 recurrences; the
+// input bytes of 8 steps are loaded ahead of the dependent chain.  Writes the bf16 hi/lo
+// split MN-major (channels contiguous): xh/xl [B*KR][kp], row b*KR + rho, rho = 0 ->
+// xbar_{t0-1} (carry), rho = s+1 -> xbar_{t0+s}, zero beyond the chunk -- one 128-byte
+// coalesced bf16x2 store per warp and row.
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) xbar_chunk_kernel(
-    const uint8_t* __restrict__ x, long long stride_b, int B, int k, int k_rows, int KR, int len,
-    double alpha, double* __restrict__ xbar_st, __nv_bfloat16* __restrict__ xh,
-    __nv_bfloat16* __restrict__ xl) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint8_t* __restrict__ x, long long stride_b, int B, int k, int kp, int KR, int len,
+    double alpha, double* __restrict__ xbar_st, uint32_t* __restrict__ xh,
+    uint32_t* __restrict__ xl) {
+  const int jp = blockIdx.x * blockDim.x + threadIdx.x;  // channel pair
+  const int j = 2 * jp;
   const int b = blockIdx.y;
-  if (j >= k_rows) return;
-  const bool valid = j < k;
-  double xb = valid ? xbar_st[(long long)b * k + j] : 0.0;
-  const long long K = (long long)B * KR;
+  if (j >= kp) return;
+  const bool v0 = j < k, v1 = j + 1 < k;
+  double xb0 = v0 ? xbar_st[(long long)b * k + j] : 0.0;
+  double xb1 = v1 ? xbar_st[(long long)b * k + j + 1] : 0.0;
   const uint8_t* xin = x + (long long)b * stride_b + j;
-  uint4* oh = reinterpret_cast<uint4*>(xh + (long long)j * K + (long long)b * KR);
-  uint4* ol = reinterpret_cast<uint4*>(xl + (long long)j * K + (long long)b * KR);
+  const long long ld2 = kp >> 1;
+  uint32_t* oh = xh + (long long)b * KR * ld2 + jp;
+  uint32_t* ol = xl + (long long)b * KR * ld2 + jp;
   for (int r8 = 0; r8 < KR; r8 += 8) {
-    uint32_t xv[8];
+    uint32_t x0[8], x1[8];
 #pragma unroll
     for (int u8 = 0; u8 < 8; ++u8) {
       const int rho = r8 + u8;
-      xv[u8] = (valid && rho >= 1 && rho <= len) ? xin[(long long)(rho - 1) * k] : 0u;
+      const bool live = rho >= 1 && rho <= len;
+      x0[u8] = (v0 && live) ? xin[(long long)(rho - 1) * k] : 0u;
+      x1[u8] = (v1 && live) ? xin[(long long)(rho - 1) * k + 1] : 0u;
     }
-    float v[8];
 #pragma unroll
     for (int u8 = 0; u8 < 8; ++u8) {
       const int rho = r8 + u8;
-      float vv = 0.0f;
+      float f0 = 0.f, f1 = 0.f;
       if (rho == 0) {
-        vv = (float)xb;
+        f0 = (float)xb0;
+        f1 = (float)xb1;
       } else if (rho <= len) {
-        xb = __dadd_rn(__dmul_rn(alpha, xb), (double)xv[u8]);
-        vv = (float)xb;
+        xb0 = __dadd_rn(__dmul_rn(alpha, xb0), (double)x0[u8]);
+        xb1 = __dadd_rn(__dmul_rn(alpha, xb1), (double)x1[u8]);
+        f0 = (float)xb0;
+        f1 = (float)xb1;
       }
-      v[u8] = vv;
+      uint32_t h, l;
+      split_bf16x2(f0, f1, h, l);
+      oh[(long long)rho * ld2] = h;
+      ol[(long long)rho * ld2] = l;
     }
-    uint32_t h[4], l[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) split_bf16x2(v[2 * q], v[2 * q + 1], h[q], l[q]);
-    oh[r8 / 8] = make_uint4(h[0], h[1], h[2], h[3]);
-    ol[r8 / 8] = make_uint4(l[0], l[1], l[2], l[3]);
   }
-  if (valid) xbar_st[(long long)b * k + j] = xb;
+  if (v0) xbar_st[(long long)b * k + j] = xb0;
+  if (v1) xbar_st[(long long)b * k + j + 1] = xb1;
 }
 
 }  // namespace spb
@@ -271,22 +279,26 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
                       double* zsum, uint32_t* raster, const float* wsig, const float* ctab,
                       void* c_hi, void* c_lo, void* w_hi, void* w_lo, int ldc, float* mdt,
                       float* psi_scratch, cudaStream_t stream) {
-  SPB_CHECK_ARG(pass == 0 || pass == 1, "spb_forward_chunk: pass must be 0 (A) or 1 (B)");
-  SPB_CHECK_ARG(cur && u && a, "spb_forward_chunk: null pointer");
+  SPB_CHECK_ARG(pass >= 0 && pass <= 2,
+                "spb_forward_chunk: pass must be 0 (A), 1 (B) or 2 (B scan only)");
+  SPB_CHECK_ARG(pass == 2 || (cur && u && a), "spb_forward_chunk: null pointer");
   SPB_CHECK_ARG(B > 0 && n > 0 && Tc > 0 && len >= 0 && len <= Tc && KR >= Tc + 1 && KR % 8 == 0,
                 "spb_forward_chunk: bad sizes B=%d n=%d Tc=%d KR=%d len=%d", B, n, Tc, KR, len);
   SPB_CHECK_ARG(pass == 0 ? (zbar && zsum) : (wsig && ctab && c_hi && c_lo && psi_scratch),
                 "spb_forward_chunk: missing pass-%c buffers", pass ? 'B' : 'A');
-  SPB_CHECK_ARG(!(pass == 1 && alif && (!mdt || (w_hi && !w_lo))),
+  SPB_CHECK_ARG(!(pass == 0 && psi_scratch && (u == nullptr)), "spb_forward_chunk: bad pass A");
+  SPB_CHECK_ARG(!(pass >= 1 && alif && (!mdt || (w_hi && !w_lo))),
                 "spb_forward_chunk: ALIF pass B needs mdt (and w_lo with w_hi)");
   SPB_CHECK_ARG(pass == 0 || (ldc >= n && ldc % 8 == 0), "spb_forward_chunk: ldc must be >= n, %% 8");
-  SPB_CHECK_ARG(!(pass == 1 && reset), "spb_forward_chunk: reset=True has no two-pass form");
+  SPB_CHECK_ARG(!(pass >= 1 && reset), "spb_forward_chunk: reset=True has no two-pass form");
   FwdParams P{B, n, Tc, KR, len, t0, T, alpha, theta, slope, beta, rho, kappa, reset, alif, pass};
   dim3 grid(ceil_div(n, 32), ceil_div(B, K1_THREADS / 32));
-  forward_chunk_kernel<<<grid, K1_THREADS, 0, stream>>>(P, cur, u, a, zbar, zsum, raster, wsig,
-                                                        psi_scratch);
-  SPB_CHECK_LAUNCH("forward_chunk");
-  if (pass == 1) {
+  if (pass <= 1) {
+    forward_chunk_kernel<<<grid, K1_THREADS, 0, stream>>>(P, cur, u, a, zbar, zsum, raster, wsig,
+                                                          psi_scratch);
+    SPB_CHECK_LAUNCH("forward_chunk");
+  }
+  if (pass >= 1) {
     dim3 sgrid(ceil_div(n, 64), ceil_div(B, K1S_THREADS / 32));
     chunk_scan_kernel<<<sgrid, K1S_THREADS, (len + 1) * sizeof(float), stream>>>(
         P, wsig, ctab, reinterpret_cast<uint32_t*>(c_hi), reinterpret_cast<uint32_t*>(c_lo),
@@ -297,16 +309,17 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
   return 0;
 }
 
-int spb_xbar_chunk(const uint8_t* x, long long stride_b, int B, int k, int k_rows, int KR,
+int spb_xbar_chunk(const uint8_t* x, long long stride_b, int B, int k, int kp, int KR,
                    int len, double alpha, double* xbar_state, void* xh, void* xl,
                    cudaStream_t stream) {
   SPB_CHECK_ARG(x && xbar_state && xh && xl, "spb_xbar_chunk: null pointer");
-  SPB_CHECK_ARG(B > 0 && k > 0 && k_rows >= k && KR > 0 && KR % 8 == 0 && len >= 0 && len < KR,
+  SPB_CHECK_ARG(B > 0 && k > 0 && kp >= k && kp % 8 == 0 && KR > 0 && KR % 8 == 0 && len >= 0 &&
+                    len < KR,
                 "spb_xbar_chunk: bad sizes");
-  dim3 grid(ceil_div(k_rows, 128), B);
-  xbar_chunk_kernel<<<grid, 128, 0, stream>>>(x, stride_b, B, k, k_rows, KR, len, alpha,
-                                              xbar_state, reinterpret_cast<__nv_bfloat16*>(xh),
-                                              reinterpret_cast<__nv_bfloat16*>(xl));
+  dim3 grid(ceil_div(kp / 2, 128), B);
+  xbar_chunk_kernel<<<grid, 128, 0, stream>>>(x, stride_b, B, k, kp, KR, len, alpha, xbar_state,
+                                              reinterpret_cast<uint32_t*>(xh),
+                                              reinterpret_cast<uint32_t*>(xl));
   SPB_CHECK_LAUNCH("xbar_chunk");
   return 0;
 }

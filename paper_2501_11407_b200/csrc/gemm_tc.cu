@@ -1,8 +1,8 @@
 // K5: factorised e-prop gradient GEMM on 5th-generation tensor cores (tcgen05 + TMA).
 //
-//   grad[i][j] += sum_K A[K][i] * B[j][K],   A = chunk coefficients C (M = n neurons,
-//                                            MN-major: neurons contiguous, as K1s writes)
-//                                            B = xbar_t     (N = k inputs, K-major),
+//   grad[i][j] += sum_K A[K][i] * B[K][j],   A = chunk coefficients C (M = n neurons)
+//                                            B = xbar_t     (N = k inputs)
+//   both MN-major (neurons / channels contiguous, as K1s / K4 write them),
 //   K = (sample, step) pairs of one time chunk (K = B*Tc), so the LIF trace psi (x) xbar
 //   (gradients.py:165-172, G_u = 1 (x) xbar) is never materialised per sample.
 //
@@ -10,8 +10,8 @@
 // and D += Ah*Bh + Ah*Bl + Al*Bh (the lo*lo term is below fp32 rounding of the sum).
 //
 // Structure (one 128x128 output tile per CTA, split-K over blockIdx.z):
-//   warp 0   TMA producer: Ah, Al (two 64x64 MN-major boxes each), Bh, Bl (128x64 K-major),
-//            all SWIZZLE_128B, per stage
+//   warp 0   TMA producer: Ah, Al, Bh, Bl, two 64x64 MN-major SWIZZLE_128B boxes each,
+//            per stage
 //   warp 1   TMEM allocation + single-thread tcgen05.mma issue (12 MMAs of 128x128x16 per
 //            64-wide K block), tcgen05.commit releases smem stages / signals the epilogue
 //   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 -> fp32 partial tile (fixed-order reduce later)
@@ -50,8 +50,8 @@ __device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t saddr) {
   d |= (uint64_t)2u << 61;
   return d;
 }
-// Instruction descriptor: kind::f16, A bf16 MN-major (bit 15), B bf16 K-major, D fp32.
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+// Instruction descriptor: kind::f16, A and B bf16 MN-major (bits 15, 16), D fp32.
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
@@ -124,8 +124,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma_load_2d(st + TILE_A / 2, &tm_ah, fb, m0 + 64, kb * BK);
         tma_load_2d(st + TILE_A, &tm_al, fb, m0, kb * BK);
         tma_load_2d(st + TILE_A + TILE_A / 2, &tm_al, fb, m0 + 64, kb * BK);
-        tma_load_2d(st + 2 * TILE_A, &tm_bh, fb, kb * BK, n0);
-        tma_load_2d(st + 2 * TILE_A + TILE_B, &tm_bl, fb, kb * BK, n0);
+        tma_load_2d(st + 2 * TILE_A, &tm_bh, fb, n0, kb * BK);
+        tma_load_2d(st + 2 * TILE_A + TILE_B / 2, &tm_bh, fb, n0 + 64, kb * BK);
+        tma_load_2d(st + 2 * TILE_A + TILE_B, &tm_bl, fb, n0, kb * BK);
+        tma_load_2d(st + 2 * TILE_A + TILE_B + TILE_B / 2, &tm_bl, fb, n0 + 64, kb * BK);
       }
     }
   } else if (warp == 1) {
@@ -140,10 +142,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                        sbl = st + 2 * TILE_A + TILE_B;
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint32_t off = kk * 32;     // 16 bf16 along K inside the 128-byte swizzle row
-          const uint32_t offa = kk * 2048;  // 16 K rows of the MN-major A tile
+          const uint32_t offa = kk * 2048;  // 16 K rows of the MN-major tiles
           const uint64_t dah = umma_desc_mn_sw128(sah + offa), dal = umma_desc_mn_sw128(sal + offa);
-          const uint64_t dbh = umma_desc_k_sw128(sbh + off), dbl = umma_desc_k_sw128(sbl + off);
+          const uint64_t dbh = umma_desc_mn_sw128(sbh + offa), dbl = umma_desc_mn_sw128(sbl + offa);
           umma_bf16(tmem_base, dah, dbh, (kb > kb0 || kk > 0) ? 1u : 0u);
           umma_bf16(tmem_base, dah, dbl, 1u);
           umma_bf16(tmem_base, dal, dbh, 1u);
@@ -254,18 +255,18 @@ extern "C" {
 // for i < M, j < ldp; every one of the `splits` slices is written (empty K ranges give 0).
 // Reduced in fixed order with spb_reduce_partials.
 int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* bh, const void* bl,
-                           int M, int N_rows, int K, int splits, float* partial, int ldp,
+                           int ldb, int M, int N_rows, int K, int splits, float* partial, int ldp,
                            long long slice_stride, cudaStream_t stream) {
   SPB_CHECK_ARG(ah && al && bh && bl && partial, "spb_grad_gemm_partials: null pointer");
   SPB_CHECK_ARG(M > 0 && N_rows > 0 && K > 0 && K % 8 == 0 && splits > 0 && ldp >= 1 &&
-                    lda >= M && lda % 8 == 0,
+                    lda >= M && lda % 8 == 0 && ldb >= N_rows && ldb % 8 == 0,
                 "spb_grad_gemm_partials: bad sizes M=%d lda=%d N=%d K=%d", M, lda, N_rows, K);
   SPB_CHECK_ARG((reinterpret_cast<uintptr_t>(ah) | reinterpret_cast<uintptr_t>(al) |
                  reinterpret_cast<uintptr_t>(bh) | reinterpret_cast<uintptr_t>(bl)) % 16 == 0,
                 "spb_grad_gemm_partials: operands must be 16-byte aligned");
   CUtensorMap mah, mal, mbh, mbl;
   if (!tc::make_map_mn(&mah, ah, M, lda, K) || !tc::make_map_mn(&mal, al, M, lda, K) ||
-      !tc::make_map(&mbh, bh, K, N_rows, tc::BN) || !tc::make_map(&mbl, bl, K, N_rows, tc::BN)) {
+      !tc::make_map_mn(&mbh, bh, N_rows, ldb, K) || !tc::make_map_mn(&mbl, bl, N_rows, ldb, K)) {
     set_error("spb_grad_gemm_partials: cuTensorMapEncodeTiled failed");
     return 3;
   }

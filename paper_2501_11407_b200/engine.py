@@ -135,8 +135,8 @@ class EpropEngine:
         self.c_hi = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
         self.c_lo = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
         self.xbar_state = torch.empty((B, k), dtype=f64, device=dev)
-        self.xh = torch.zeros((self.kp, K), dtype=bf16, device=dev)
-        self.xl = torch.zeros((self.kp, K), dtype=bf16, device=dev)
+        self.xh = torch.zeros((K, self.kp), dtype=bf16, device=dev)   # MN-major [K][kp]
+        self.xl = torch.zeros((K, self.kp), dtype=bf16, device=dev)
         # split-K (K5) and sample-split (K6) partial slices, reduced in fixed order
         tiles5 = (self.kp // 128) * math.ceil(n / 128)
         self.splits5 = max(1, min(K // 64, round(sms / tiles5)))
@@ -265,7 +265,8 @@ class EpropEngine:
                  *common, v(self.u.data_ptr()), v(self.a.data_ptr()),
                  v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
                  v(raster.data_ptr()) if raster is not None else None,
-                 None, None, None, None, None, None, 0, None, None, st)
+                 None, None, None, None, None, None, 0, None,
+                 v(self.psi.data_ptr()) if nchunks == 1 else None, st)
             self.launches += 3
         # ---------------- readout / loss ----------------
         call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
@@ -288,7 +289,9 @@ class EpropEngine:
             if nchunks > 1:  # one chunk: cur of pass A is still valid (same W, same x)
                 self._project(xp, strideb, ln, st, timed)
             carry_out = self.alif and not last   # the trace is only needed by a later chunk
-            timed("forward", ln, "spb_forward_chunk", 1, v(self.cur.data_ptr()), B, n, Tc, KR,
+            # one chunk: pass A already parked psi -> backward scan only (pass 2)
+            timed("forward", ln, "spb_forward_chunk", 1 if nchunks > 1 else 2,
+                  v(self.cur.data_ptr()), B, n, Tc, KR,
                   ln, t0, T, *common, v(self.u.data_ptr()), v(self.a.data_ptr()), None, None,
                   None, v(self.wsig.data_ptr()), v(ctab.data_ptr()),
                   v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()),
@@ -298,10 +301,11 @@ class EpropEngine:
             call("spb_xbar_chunk", v(xp), strideb, B, k, self.kp, KR, ln, float(alpha),
                  v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()), v(self.xl.data_ptr()), st)
             timed("gemm", ln, "spb_grad_gemm_partials", v(self.c_hi.data_ptr()),
-                  v(self.c_lo.data_ptr()), self.ldc, v(self.xh.data_ptr()), v(self.xl.data_ptr()), n,
+                  v(self.c_lo.data_ptr()), self.ldc, v(self.xh.data_ptr()), v(self.xl.data_ptr()),
+                  self.kp, n,
                   self.kp, K, self.splits5, v(self.partial.data_ptr()), self.kp, slice_stride,
                   st)
-            self.launches += 6 if nchunks > 1 else 4
+            self.launches += 6 if nchunks > 1 else 3
             slices = self.splits5
             if self.alif and (c > 0 or not last):
                 # first chunk: E0 = 0 (nothing to add, only carry); last chunk: no carry

@@ -125,6 +125,8 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     assert names.count("spb_readout_loss") == 1
     # spb_forward_chunk pass B launches two kernels (dynamics + chunk scan)
     passb = sum(1 for c in rec.calls if c[0] == "spb_forward_chunk" and c[1][0] == 1)
+    if nch == 1:  # pass A parks psi, pass B runs the scan only
+        assert [c[1][0] for c in rec.calls if c[0] == "spb_forward_chunk"] == [0, 2]
     assert eng.launches == len(rec.calls) + passb
 
 

@@ -189,15 +189,16 @@ def test_tcgen05_gemm_matches_cuda_core_gemm():
     at = torch.zeros(K, lda, device="cuda")
     at[:, :M] = a.t()                       # MN-major A operand [K][lda]
     ah = at.to(torch.bfloat16); al = (at - ah.float()).to(torch.bfloat16)
-    bh = b.to(torch.bfloat16); bl = (b - bh.float()).to(torch.bfloat16)
+    bt = b.t().contiguous()                 # MN-major B operand [K][N]
+    bh = bt.to(torch.bfloat16); bl = (bt - bh.float()).to(torch.bfloat16)
     splits = 3
     part = torch.zeros((splits, M, N), device="cuda")
     v = ctypes.c_void_p
     _lib.call("spb_grad_gemm_partials", v(ah.data_ptr()), v(al.data_ptr()), lda, v(bh.data_ptr()),
-              v(bl.data_ptr()), M, N, K, splits, v(part.data_ptr()), N, M * N, None)
+              v(bl.data_ptr()), N, M, N, K, splits, v(part.data_ptr()), N, M * N, None)
     ref = torch.zeros((M, N), dtype=torch.float64, device="cuda")
     _lib.call("spb_grad_gemm_simt", v(ah.data_ptr()), v(al.data_ptr()), lda, v(bh.data_ptr()),
-              v(bl.data_ptr()), M, N, K, v(ref.data_ptr()), N, None)
+              v(bl.data_ptr()), N, M, N, K, v(ref.data_ptr()), N, None)
     torch.cuda.synchronize()
     got = part.double().sum(0)
     exact = a.double() @ b.double().t()
