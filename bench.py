@@ -317,9 +317,15 @@ def main():
                 ln = meta                                        # int8 MACs x2, useful part
                 flops += 2.0 * P_sl * B * ln * n * k
                 byts += B * ln * k + P_sl * n * k + 8.0 * B * ln * n
-            elif name == "forward":
-                ln = meta
-                byts += 8.0 * B * ln * n + (16.0 if kind == "alif" else 8.0) * n * B * KR
+            elif name in ("forward", "forward_a"):
+                ln, pid, flag = meta
+                psi = 4.0 * B * (ln + 1) * n
+                if pid <= 1:                       # dynamics: read the fp64 current
+                    byts += 8.0 * B * ln * n
+                    if pid == 1 or flag:           # psi parked for the scan
+                        byts += psi
+                if pid >= 1:                       # scan: psi back, C (and W) out, bf16 hi/lo
+                    byts += psi + 4.0 * n * B * KR * (2 if flag else 1)
             elif name == "gemm":
                 ln = meta
                 flops += 6.0 * n * k * B * (ln + 1)                 # 3 bf16 MMAs per product
@@ -344,7 +350,8 @@ def main():
     if kernels:
         dom = max(kernels, key=lambda nm: kernels[nm]["ms_per_step"])
         e = kernels[dom]
-        names = {"proj": "input_proj_kernel (K2, int8 tcgen05)", "forward": "forward_chunk_kernel (K1)",
+        names = {"proj": "input_proj_kernel (K2, int8 tcgen05)", "forward": "forward_chunk + chunk_scan (K1 pass B)",
+                 "forward_a": "forward_chunk_kernel (K1 pass A)",
                  "gemm": "grad_gemm_tc_kernel (K5, bf16x3 tcgen05)",
                  "carry": "alif_carry_kernel (K6, tcgen05 + eps stream)"}
         if e.get("tensor_frac", 0) >= e.get("hbm_frac", 0) and "tensor_tflops" in e:

@@ -57,7 +57,7 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
  *     b*Tc+s): ALIF/LIF state update, spike and surrogate derivative.
  *     Replaces _step_state (gradients.py:118-129) + heaviside/surrogate_grad
  *     (graph.py:40-52) + the readout spike filter (gradients.py:173-174).
- *     u, a    [B][n] fp64 state, carried across chunks (zero at t=0)
+ *     u, a    [B][n] fp64 state, carried across chunks (t0 == 0: fresh zero state, not read)
  *     pass 0 (A): zbar, zsum [B][n] fp64 carried; raster [B][T][ceil(n/32)] bit-packed
  *                 spikes (optional, may be NULL); psi_scratch optional: when given, the
  *                 surrogate rows are parked exactly as pass B does (one-chunk sequences
@@ -82,11 +82,12 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
 
 /* K4  Presynaptic filter xbar_t = alpha*xbar_{t-1} + x_t (the factorised LIF trace G_u,
  *     gradients.py:89-94 with H_I = alpha, F rows = x_t; test_gradients.py:81-91).
- *     xbar_state [B][k] fp64 carry; xh/xl [B*KR][kp] bf16 hi/lo split, MN-major (channels
+ *     xbar_state [B][k] fp64 carry (fresh != 0: start from zero); xh/xl [B*KR][kp] bf16
+ *     hi/lo split, MN-major (channels
  *     contiguous, kp >= k, kp % 8 == 0): row b*KR + rho, rho = 0 holds xbar_{t0-1},
  *     rho = s+1 holds xbar_{t0+s}; zero elsewhere. */
 int spb_xbar_chunk(const uint8_t* x, long long stride_b, int B, int k, int kp, int KR,
-                   int len, double alpha, double* xbar_state, void* xh, void* xl,
+                   int len, int fresh, double alpha, double* xbar_state, void* xh, void* xl,
                    cudaStream_t stream);
 
 /* K3  Readout + loss: s_b = W_out zsum_b, loss_b = CE(s_b, y_b), g_b = softmax - onehot,
@@ -97,7 +98,7 @@ int spb_readout_loss(const double* wout, const double* zsum, const long long* la
                      int m, double* s_out, double* loss, double* g, float* wsig, int* correct,
                      cudaStream_t stream);
 
-/* K7  gwo[c][i] += sum_b g[b][c] zsum[b][i]   (gradients.py:181, summed over the batch). */
+/* K7  gwo[c][i] = sum_b g[b][c] zsum[b][i]   (gradients.py:181, summed over the batch). */
 int spb_readout_grad(const double* g, const double* zsum, int B, int n, int m, double* gwo,
                      cudaStream_t stream);
 
@@ -131,9 +132,10 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
                          int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
                          int store_eps, cudaStream_t stream);
 
-/* grad[i][j] += sum_{s<splits} partial[s][i][j] in fixed order (fp64). */
+/* grad[i][j] (+)= sum_{s<splits} partial[s][i][j] in fixed order (fp64); accumulate = 0
+ * overwrites. */
 int spb_reduce_partials(const float* partial, int splits, int n, int n_pad, int k_pad,
-                        double* grad, cudaStream_t stream);
+                        int accumulate, double* grad, cudaStream_t stream);
 
 /* out[r][c] = acc[r*ld + c] cast to fp32 (out_is_f64=0) or fp64. */
 int spb_finalize_grad(const double* acc, int rows, int cols, int ld, void* out, int out_is_f64,

@@ -270,13 +270,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 }  // namespace carry
 
 __global__ void reduce_partials_kernel(const float* __restrict__ partial, int S, int n, int n_pad,
-                                       int k_pad, double* __restrict__ grad) {
+                                       int k_pad, int accumulate, double* __restrict__ grad) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)n * k_pad) return;
   const long long stride = (long long)n_pad * k_pad;
   double acc = 0.0;
   for (int s = 0; s < S; ++s) acc += (double)partial[s * stride + idx];
-  grad[idx] += acc;
+  grad[idx] = accumulate ? grad[idx] + acc : acc;
 }
 
 // CUDA-core GEMM on the same bf16 hi/lo operands as the tensor-core path:
@@ -378,12 +378,12 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
 }
 
 int spb_reduce_partials(const float* partial, int splits, int n, int n_pad, int k_pad,
-                        double* grad, cudaStream_t stream) {
+                        int accumulate, double* grad, cudaStream_t stream) {
   SPB_CHECK_ARG(partial && grad && splits > 0 && n > 0 && n <= n_pad,
                 "spb_reduce_partials: bad args");
   const long long total = (long long)n * k_pad;
   reduce_partials_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(
-      partial, splits, n, n_pad, k_pad, grad);
+      partial, splits, n, n_pad, k_pad, accumulate, grad);
   SPB_CHECK_LAUNCH("reduce_partials");
   return 0;
 }

@@ -54,16 +54,13 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
   const int b = blockIdx.y * (K1_THREADS / 32) + warp;
   if (b >= P.B) return;  // warp-uniform; no block-level barriers below
   const long long bi = (long long)b * P.n + i;
-  double u = 0.0, a = 0.0, zbar = 0.0, zsum = 0.0;
-  float w_sig = 0.0f;
-  if (valid_i) {
+  double u = 0.0, a = 0.0, zbar = 0.0, zsum = 0.0;  // t0 == 0: fresh state (no read)
+  if (valid_i && P.t0 > 0) {
     u = u_st[bi];
     a = a_st[bi];
     if (P.pass == 0) {
       zbar = zbar_st[bi];
       zsum = zsum_st[bi];
-    } else {
-      w_sig = wsig[bi];
     }
   }
   const double theta = P.theta, beta = P.beta;
@@ -222,15 +219,15 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) xbar_chunk_kernel(
     const uint8_t* __restrict__ x, long long stride_b, int B, int k, int kp, int KR, int len,
-    double alpha, double* __restrict__ xbar_st, uint32_t* __restrict__ xh,
+    int fresh, double alpha, double* __restrict__ xbar_st, uint32_t* __restrict__ xh,
     uint32_t* __restrict__ xl) {
   const int jp = blockIdx.x * blockDim.x + threadIdx.x;  // channel pair
   const int j = 2 * jp;
   const int b = blockIdx.y;
   if (j >= kp) return;
   const bool v0 = j < k, v1 = j + 1 < k;
-  double xb0 = v0 ? xbar_st[(long long)b * k + j] : 0.0;
-  double xb1 = v1 ? xbar_st[(long long)b * k + j + 1] : 0.0;
+  double xb0 = (v0 && !fresh) ? xbar_st[(long long)b * k + j] : 0.0;
+  double xb1 = (v1 && !fresh) ? xbar_st[(long long)b * k + j + 1] : 0.0;
   const uint8_t* xin = x + (long long)b * stride_b + j;
   const long long ld2 = kp >> 1;
   uint32_t* oh = xh + (long long)b * KR * ld2 + jp;
@@ -310,14 +307,15 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
 }
 
 int spb_xbar_chunk(const uint8_t* x, long long stride_b, int B, int k, int kp, int KR,
-                   int len, double alpha, double* xbar_state, void* xh, void* xl,
+                   int len, int fresh, double alpha, double* xbar_state, void* xh, void* xl,
                    cudaStream_t stream) {
   SPB_CHECK_ARG(x && xbar_state && xh && xl, "spb_xbar_chunk: null pointer");
   SPB_CHECK_ARG(B > 0 && k > 0 && kp >= k && kp % 8 == 0 && KR > 0 && KR % 8 == 0 && len >= 0 &&
                     len < KR,
                 "spb_xbar_chunk: bad sizes");
   dim3 grid(ceil_div(kp / 2, 128), B);
-  xbar_chunk_kernel<<<grid, 128, 0, stream>>>(x, stride_b, B, k, kp, KR, len, alpha, xbar_state,
+  xbar_chunk_kernel<<<grid, 128, 0, stream>>>(x, stride_b, B, k, kp, KR, len, fresh, alpha,
+                                              xbar_state,
                                               reinterpret_cast<uint32_t*>(xh),
                                               reinterpret_cast<uint32_t*>(xl));
   SPB_CHECK_LAUNCH("xbar_chunk");

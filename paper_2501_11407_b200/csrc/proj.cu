@@ -27,7 +27,8 @@ constexpr int BM = 128;       // (sample, step) rows per tile
 constexpr int NT = 32;        // neurons per tile (per slice)
 constexpr int BK = 128;       // bytes (= int8 elements) of K per stage: one 128B swizzle row
 constexpr int STAGES = 4;
-constexpr int THREADS = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+constexpr int EPI_WARPS = 8;  // 4 TMEM lane quarters x 2 halves of the 32 neurons
 constexpr int TILE_A = BM * BK;
 
 template <int P>
@@ -78,27 +79,53 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, int32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ double pow2(int e) {  // 2^e for -1022 <= e <= 1023
   return __longlong_as_double((long long)(e + 1023) << 52);
 }
 
-// Epilogue of one 128-row x 32-neuron tile: pull the P slice accumulators of this thread's
-// row from TMEM, recombine them exactly in int64 and write the fp64 current.
+// Epilogue of one 128-row x 32-neuron tile, split over 8 warps: TMEM lane quarter q and
+// neuron half h (16 neurons).  Each thread pulls its row's P slice accumulators for its
+// 16 neurons in two batches (slices 0-2, then 3..P-1, one tcgen05.wait each), recombines
+// them exactly in int64 and writes 16 fp64 currents (128 contiguous bytes).
+constexpr int NH = NT / 2;
+
 template <int P>
-__device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&se)[NT],
+__device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&se)[NH],
                                                    double* __restrict__ out, int M, int n, int row,
                                                    int i0, uint32_t tempty_bar, int lane) {
-  long long g0[NT], g1[NT];
-  int32_t r[32];
+  long long g0[NH], g1[NH];
+  {
+    int32_t r[3][NH];
 #pragma unroll
-  for (int c = 0; c < NT; ++c) g0[c] = g1[c] = 0;
+    for (int p = 0; p < 3; ++p) tmem_ld16_nowait(tbase + p * NT, r[p]);
+    tmem_wait_ld();
 #pragma unroll
-  for (int p = 0; p < P; ++p) {
-    tmem_ld32(tbase + p * NT, r);
+    for (int c = 0; c < NH; ++c)
+      g0[c] = ((long long)r[0][c] * 128 + r[1][c]) * 128 + r[2][c];
+  }
+  {
+    int32_t r[P - 3][NH];
 #pragma unroll
-    for (int c = 0; c < NT; ++c) {
-      if (p < 3) g0[c] = g0[c] * 128 + r[c];
-      else g1[c] = g1[c] * 128 + r[c];
+    for (int p = 3; p < P; ++p) tmem_ld16_nowait(tbase + p * NT, r[p - 3]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < NH; ++c) {
+      long long v = r[0][c];
+#pragma unroll
+      for (int p = 1; p < P - 3; ++p) v = v * 128 + r[p][c];
+      g1[c] = v;
     }
   }
   // the TMEM buffer is free once every epilogue warp has pulled its lanes
@@ -108,7 +135,7 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&s
   if (row < M) {
     double* orow = out + (long long)row * n + i0;
 #pragma unroll
-    for (int c = 0; c < NT; c += 2) {
+    for (int c = 0; c < NH; c += 2) {
       double v[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -172,7 +199,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&tfull[a]), 1);
-      mbar_init(smem_u32(&tempty[a]), 4);
+      mbar_init(smem_u32(&tempty[a]), EPI_WARPS);
     }
     mbar_init(smem_u32(wfull), 1);
     mbar_init(smem_u32(wempty), 1);
@@ -249,18 +276,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else {
-    const int q = warp & 3;
+    const int q = warp & 3;          // TMEM lane quarter
+    const int hh = (warp - 2) >> 2;  // neuron half of the tile
     int lt = 0;
     for (int t = t_begin; t < t_end; ++t, ++lt) {
       const int nt = t / m_tiles, mt = t % m_tiles;
       const int a = lt & 1;
-      int se[NT];  // per-neuron exponents, fetched before waiting on the tensor cores
+      const int i0 = nt * NT + hh * NH;
+      int se[NH];  // per-neuron exponents, fetched before waiting on the tensor cores
 #pragma unroll
-      for (int c = 0; c < NT; ++c) se[c] = (nt * NT + c < n) ? __ldg(sexp + nt * NT + c) : 0;
+      for (int c = 0; c < NH; ++c) se[c] = (i0 + c < n) ? __ldg(sexp + i0 + c) : 0;
       mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      proj_epilogue_tile<P>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256), se,
-                            out, M, n, mt * BM + q * 32 + lane, nt * NT, smem_u32(&tempty[a]),
+      proj_epilogue_tile<P>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH),
+                            se, out, M, n, mt * BM + q * 32 + lane, i0, smem_u32(&tempty[a]),
                             lane);
     }
   }
@@ -298,7 +327,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&tfull[a]), 1);
-      mbar_init(smem_u32(&tempty[a]), 4);  // one arrive per epilogue warp
+      mbar_init(smem_u32(&tempty[a]), EPI_WARPS);  // one arrive per epilogue warp
     }
     mbar_fence_init();
     tma_prefetch_desc(&tm_x);
@@ -356,18 +385,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else {
-    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    const int q = warp & 3;          // TMEM lane quarter accessible to this warp
+    const int hh = (warp - 2) >> 2;  // neuron half of the tile
     int lt = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
       const int nt = t / m_tiles, mt = t % m_tiles;
       const int a = lt & 1;
-      int se[NT];  // per-neuron exponents, fetched before waiting on the tensor cores
+      const int i0 = nt * NT + hh * NH;
+      int se[NH];  // per-neuron exponents, fetched before waiting on the tensor cores
 #pragma unroll
-      for (int c = 0; c < NT; ++c) se[c] = (nt * NT + c < n) ? __ldg(sexp + nt * NT + c) : 0;
+      for (int c = 0; c < NH; ++c) se[c] = (i0 + c < n) ? __ldg(sexp + i0 + c) : 0;
       mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      proj_epilogue_tile<P>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256), se,
-                            out, M, n, mt * BM + q * 32 + lane, nt * NT, smem_u32(&tempty[a]),
+      proj_epilogue_tile<P>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH),
+                            se, out, M, n, mt * BM + q * 32 + lane, i0, smem_u32(&tempty[a]),
                             lane);
     }
   }

@@ -3,7 +3,7 @@
 //                            gradients.py:163-164), softmax cross-entropy
 //                            (gradients.py:66-75), g = softmax - onehot,
 //                            w_sig = W_out^T g (gradients.py:178)
-//   K7  spb_readout_grad  -- grad W_out = sum_b g_b (x) zsum_b (gradients.py:181)
+//   K7  spb_readout_grad  -- grad W_out = sum_b g_b (x) zsum_b (gradients.py:181), written
 //   --  spb_finalize_grad -- fp64 gradient accumulator -> caller dtype, padding dropped
 #include "common.cuh"
 
@@ -21,19 +21,22 @@ __global__ void readout_loss_kernel(const double* __restrict__ wout, const doubl
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const double* z = zsum + (long long)b * n;
-  for (int c = 0; c < m; ++c) {
-    double acc = 0.0;
-    for (int i = tid; i < n; i += blockDim.x) acc = fma(wout[(long long)c * n + i], z[i], acc);
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) red[warp] = acc;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int w = 0; w < nwarps; ++w) t += red[w];
-      s[c] = t;
+  // one warp per class (round robin): s_c = sum_i W_out[c][i] zsum[b][i], no block barriers
+  for (int c = warp; c < m; c += nwarps) {
+    const double* wr = wout + (long long)c * n;
+    double a0 = 0.0, a1 = 0.0;
+    int i = lane;
+    for (; i + 32 < n; i += 64) {
+      a0 = fma(wr[i], z[i], a0);
+      a1 = fma(wr[i + 32], z[i + 32], a1);
     }
-    __syncthreads();
+    if (i < n) a0 = fma(wr[i], z[i], a0);
+    double acc = a0 + a1;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) s[c] = acc;
   }
+  (void)red;
+  __syncthreads();
   if (tid == 0) {
     const int y = (int)labels[b];
     double mx = s[0];
@@ -65,9 +68,17 @@ __global__ void readout_grad_kernel(const double* __restrict__ g, const double* 
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (i >= n) return;
-  double acc = 0.0;
-  for (int b = 0; b < B; ++b) acc = fma(g[(long long)b * m + c], zsum[(long long)b * n + i], acc);
-  gwo[(long long)c * n + i] += acc;
+  // four interleaved accumulators (fixed order) to break the fp64 FMA dependency chain
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int b = 0;
+  for (; b + 3 < B; b += 4) {
+    a0 = fma(g[(long long)b * m + c], zsum[(long long)b * n + i], a0);
+    a1 = fma(g[(long long)(b + 1) * m + c], zsum[(long long)(b + 1) * n + i], a1);
+    a2 = fma(g[(long long)(b + 2) * m + c], zsum[(long long)(b + 2) * n + i], a2);
+    a3 = fma(g[(long long)(b + 3) * m + c], zsum[(long long)(b + 3) * n + i], a3);
+  }
+  for (; b < B; ++b) a0 = fma(g[(long long)b * m + c], zsum[(long long)b * n + i], a0);
+  gwo[(long long)c * n + i] = (a0 + a1) + (a2 + a3);
 }
 
 template <typename OT>

@@ -160,6 +160,13 @@ class EpropEngine:
         self._ctab_T = None
         self.ctab = None
         self.launches = 0
+        # side stream for work off the critical path (K4 xbar of a one-chunk sequence, K7)
+        if self.device.type == "cuda":
+            self.side = torch.cuda.Stream(device=dev)
+            self._ev = {nm: torch.cuda.Event() for nm in ("start", "xbar", "ro", "rg")}
+        else:
+            self.side = None
+            self._ev = None
 
     # ----------------------------------------------------------------------------------
     def set_weights(self, w, w_out, stream=None):
@@ -254,14 +261,29 @@ class EpropEngine:
             timers.setdefault(name, []).append((e0, e1, meta))
             return rc
 
+        use_side = self.side is not None and stream is None
+        sst = ctypes_void(self.side.cuda_stream) if use_side else st
+        main = torch.cuda.current_stream(self.device) if use_side else None
+        if use_side:
+            # the side stream must not run ahead of the previous update's consumers
+            self._ev["start"].record(main)
+            self.side.wait_event(self._ev["start"])
+        one = nchunks == 1
+        if one:  # K4 depends only on x: overlap it with pass A on the side stream
+            call("spb_xbar_chunk", v(x.data_ptr()), strideb, B, k, self.kp, KR, T, 1,
+                 float(alpha), v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()),
+                 v(self.xl.data_ptr()), sst)
+            self.launches += 1
+            if use_side:
+                self._ev["xbar"].record(self.side)
         # ---------------- pass A ----------------
-        self.u.zero_(); self.a.zero_(); self.zbar.zero_(); self.zsum.zero_()
-        for c in range(nchunks):
+        for c in range(nchunks):  # chunk 0 starts from fresh state inside the kernels
             t0 = c * Tc
             ln = min(Tc, T - t0)
             xp = x.data_ptr() + t0 * k
             self._project(xp, strideb, ln, st, timed)
-            call("spb_forward_chunk", 0, v(self.cur.data_ptr()), B, n, Tc, KR, ln, t0, T,
+            timed("forward_a", (ln, 0, nchunks == 1), "spb_forward_chunk", 0,
+                 v(self.cur.data_ptr()), B, n, Tc, KR, ln, t0, T,
                  *common, v(self.u.data_ptr()), v(self.a.data_ptr()),
                  v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
                  v(raster.data_ptr()) if raster is not None else None,
@@ -272,13 +294,15 @@ class EpropEngine:
         call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
              v(labels.data_ptr()), B, n, m, v(self.s.data_ptr()), v(self.loss.data_ptr()),
              v(self.g.data_ptr()), v(self.wsig.data_ptr()), v(self.correct.data_ptr()), st)
-        self.grad_wout.zero_()
+        if use_side:  # K7 is off the critical path
+            self._ev["ro"].record(main)
+            self.side.wait_event(self._ev["ro"])
         call("spb_readout_grad", v(self.g.data_ptr()), v(self.zsum.data_ptr()), B, n, m,
-             v(self.grad_wout.data_ptr()), st)
+             v(self.grad_wout.data_ptr()), sst)
+        if use_side:
+            self._ev["rg"].record(self.side)
         self.launches += 2
         # ---------------- pass B ----------------
-        self.u.zero_(); self.a.zero_(); self.xbar_state.zero_()
-        self.grad_w_acc.zero_()
         slice_stride = self.n_pad * self.kp
         part6 = self.partial.data_ptr() + self.splits5 * slice_stride * 4
         for c in range(nchunks):
@@ -290,7 +314,8 @@ class EpropEngine:
                 self._project(xp, strideb, ln, st, timed)
             carry_out = self.alif and not last   # the trace is only needed by a later chunk
             # one chunk: pass A already parked psi -> backward scan only (pass 2)
-            timed("forward", ln, "spb_forward_chunk", 1 if nchunks > 1 else 2,
+            pid = 1 if nchunks > 1 else 2
+            timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,
                   v(self.cur.data_ptr()), B, n, Tc, KR,
                   ln, t0, T, *common, v(self.u.data_ptr()), v(self.a.data_ptr()), None, None,
                   None, v(self.wsig.data_ptr()), v(ctab.data_ptr()),
@@ -298,14 +323,19 @@ class EpropEngine:
                   v(self.w_hi.data_ptr()) if carry_out else None,
                   v(self.w_lo.data_ptr()) if carry_out else None, self.ldc,
                   v(self.mdt.data_ptr()) if self.alif else None, v(self.psi.data_ptr()), st)
-            call("spb_xbar_chunk", v(xp), strideb, B, k, self.kp, KR, ln, float(alpha),
-                 v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()), v(self.xl.data_ptr()), st)
+            if not one:
+                call("spb_xbar_chunk", v(xp), strideb, B, k, self.kp, KR, ln, int(c == 0),
+                     float(alpha), v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()),
+                     v(self.xl.data_ptr()), st)
+                self.launches += 1
+            elif use_side:
+                main.wait_event(self._ev["xbar"])
             timed("gemm", ln, "spb_grad_gemm_partials", v(self.c_hi.data_ptr()),
                   v(self.c_lo.data_ptr()), self.ldc, v(self.xh.data_ptr()), v(self.xl.data_ptr()),
                   self.kp, n,
                   self.kp, K, self.splits5, v(self.partial.data_ptr()), self.kp, slice_stride,
                   st)
-            self.launches += 6 if nchunks > 1 else 3
+            self.launches += 5 if nchunks > 1 else 2
             slices = self.splits5
             if self.alif and (c > 0 or not last):
                 # first chunk: E0 = 0 (nothing to add, only carry); last chunk: no carry
@@ -318,8 +348,10 @@ class EpropEngine:
                 if c > 0:
                     slices += self.splits6
             call("spb_reduce_partials", v(self.partial.data_ptr()), slices, n, self.n_pad,
-                 self.kp, v(self.grad_w_acc.data_ptr()), st)
+                 self.kp, int(c > 0), v(self.grad_w_acc.data_ptr()), st)
             self.launches += 1
+        if use_side:
+            main.wait_event(self._ev["rg"])
         return self
 
     def check_labels(self, labels_np):
