@@ -137,6 +137,11 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
 int spb_reduce_partials(const float* partial, int splits, int n, int n_pad, int k_pad,
                         int accumulate, double* grad, cudaStream_t stream);
 
+/* Streaming inputs: copy rows of `row_bytes` from pinned host memory (pitch src_pitch)
+ * into a device chunk buffer (pitch dst_pitch) with cudaMemcpy2DAsync on `stream`. */
+int spb_copy_chunk_h2d(void* dst, long long dst_pitch, const void* src, long long src_pitch,
+                       long long row_bytes, int rows, cudaStream_t stream);
+
 /* out[r][c] = acc[r*ld + c] cast to fp32 (out_is_f64=0) or fp64. */
 int spb_finalize_grad(const double* acc, int rows, int cols, int ld, void* out, int out_is_f64,
                       cudaStream_t stream);

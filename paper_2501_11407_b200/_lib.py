@@ -34,6 +34,7 @@ SIGNATURES = {
     "spb_alif_carry_chunk": [P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I, I, P],
     "spb_reduce_partials": [P, I, I, I, I, I, P, P],
     "spb_finalize_grad": [P, I, I, I, P, I, P],
+    "spb_copy_chunk_h2d": [P, LL, P, LL, LL, I, P],
     "spb_version": [],
     "spb_device_sm": [],
 }

@@ -219,7 +219,10 @@ class EpropEngine:
             stream=None, timers: dict | None = None):
         """One full e-prop update on device-resident inputs.
 
-        x       uint8 [B, T, k] spike counts (CUDA, contiguous)
+        x       uint8 [B, T, k] spike counts, contiguous.  A CUDA tensor is used in place;
+                a CPU (ideally pinned) tensor is STREAMED: each time chunk is copied into
+                a double-buffered [2, B, Tc, k] device buffer on a copy stream, overlapped
+                with the previous chunk's kernels, so device memory is independent of T.
         labels  int64 [B] (CUDA)
         raster  optional int32 [B, T, ceil(n/32)] bit-packed spike output (pass A)
         timers  optional dict; CUDA event pairs are appended per launch of the main
@@ -235,6 +238,7 @@ class EpropEngine:
                                 f"{tuple(x.shape)} {x.dtype}")
         if not x.is_contiguous():
             raise ShapeMismatch("x must be contiguous")
+        streaming = x.device.type == "cpu" and self.device.type == "cuda"
         T = int(x.shape[1])
         if T <= 0:
             raise ShapeMismatch("T must be positive")
@@ -263,13 +267,54 @@ class EpropEngine:
 
         use_side = self.side is not None and stream is None
         sst = ctypes_void(self.side.cuda_stream) if use_side else st
-        main = torch.cuda.current_stream(self.device) if use_side else None
+        main = torch.cuda.current_stream(self.device) if self.device.type == "cuda" else None
         if use_side:
             # the side stream must not run ahead of the previous update's consumers
             self._ev["start"].record(main)
             self.side.wait_event(self._ev["start"])
         one = nchunks == 1
-        if one:  # K4 depends only on x: overlap it with pass A on the side stream
+        # ---- input access: resident (device tensor) or streamed chunk by chunk ----
+        if streaming:
+            if stream is not None:
+                raise ValueError("streamed inputs use the engine's own streams")
+            xs = self._stream_buffers()
+            uses = list(range(nchunks)) + ([] if one else list(range(nchunks)))
+            xhost = x.data_ptr()
+            for e in self._sev_free:
+                e.record(main)
+
+            def _copy(u):
+                cc = uses[u]
+                t0c = cc * Tc
+                lnc = min(Tc, T - t0c)
+                bb = u % 2
+                self._cs.wait_event(self._sev_free[bb])
+                call("spb_copy_chunk_h2d", v(xs[bb].data_ptr()), Tc * k, v(xhost + t0c * k),
+                     T * k, lnc * k, B, ctypes_void(self._cs.cuda_stream))
+                self._sev_ready[bb].record(self._cs)
+
+            state = {"u": 0}
+
+            def chunk_in(c):
+                u = state["u"]
+                if u == 0:
+                    _copy(0)
+                if u + 1 < len(uses):
+                    _copy(u + 1)
+                main.wait_event(self._sev_ready[u % 2])
+                return xs[u % 2].data_ptr(), Tc * k
+
+            def chunk_done():
+                self._sev_free[state["u"] % 2].record(main)
+                state["u"] += 1
+        else:
+            def chunk_in(c):
+                return x.data_ptr() + c * Tc * k, strideb
+
+            def chunk_done():
+                pass
+
+        if one and not streaming:  # K4 depends only on x: overlap it with pass A on the side stream
             call("spb_xbar_chunk", v(x.data_ptr()), strideb, B, k, self.kp, KR, T, 1,
                  float(alpha), v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()),
                  v(self.xl.data_ptr()), sst)
@@ -280,8 +325,10 @@ class EpropEngine:
         for c in range(nchunks):  # chunk 0 starts from fresh state inside the kernels
             t0 = c * Tc
             ln = min(Tc, T - t0)
-            xp = x.data_ptr() + t0 * k
-            self._project(xp, strideb, ln, st, timed)
+            xp, xstride = chunk_in(c)
+            self._project(xp, xstride, ln, st, timed)
+            if not (one and streaming):
+                chunk_done()
             timed("forward_a", (ln, 0, nchunks == 1), "spb_forward_chunk", 0,
                  v(self.cur.data_ptr()), B, n, Tc, KR, ln, t0, T,
                  *common, v(self.u.data_ptr()), v(self.a.data_ptr()),
@@ -309,9 +356,14 @@ class EpropEngine:
             t0 = c * Tc
             ln = min(Tc, T - t0)
             last = c == nchunks - 1
-            xp = x.data_ptr() + t0 * k
+            if one and streaming:
+                xp, xstride = xs[0].data_ptr(), Tc * k      # still holds the only chunk
+            elif one:
+                xp, xstride = x.data_ptr(), strideb
+            else:
+                xp, xstride = chunk_in(c)
             if nchunks > 1:  # one chunk: cur of pass A is still valid (same W, same x)
-                self._project(xp, strideb, ln, st, timed)
+                self._project(xp, xstride, ln, st, timed)
             carry_out = self.alif and not last   # the trace is only needed by a later chunk
             # one chunk: pass A already parked psi -> backward scan only (pass 2)
             pid = 1 if nchunks > 1 else 2
@@ -323,11 +375,12 @@ class EpropEngine:
                   v(self.w_hi.data_ptr()) if carry_out else None,
                   v(self.w_lo.data_ptr()) if carry_out else None, self.ldc,
                   v(self.mdt.data_ptr()) if self.alif else None, v(self.psi.data_ptr()), st)
-            if not one:
-                call("spb_xbar_chunk", v(xp), strideb, B, k, self.kp, KR, ln, int(c == 0),
+            if not one or streaming:
+                call("spb_xbar_chunk", v(xp), xstride, B, k, self.kp, KR, ln, int(c == 0),
                      float(alpha), v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()),
                      v(self.xl.data_ptr()), st)
                 self.launches += 1
+                chunk_done()
             elif use_side:
                 main.wait_event(self._ev["xbar"])
             timed("gemm", ln, "spb_grad_gemm_partials", v(self.c_hi.data_ptr()),
@@ -353,6 +406,16 @@ class EpropEngine:
         if use_side:
             main.wait_event(self._ev["rg"])
         return self
+
+    def _stream_buffers(self):
+        """Double-buffered device chunk of the input + copy stream (streaming mode)."""
+        if getattr(self, "_xs", None) is None:
+            self._xs = torch.empty((2, self.B, self.Tc, self.k), dtype=torch.uint8,
+                                   device=self.device)
+            self._cs = torch.cuda.Stream(device=self.device)
+            self._sev_free = [torch.cuda.Event() for _ in range(2)]
+            self._sev_ready = [torch.cuda.Event() for _ in range(2)]
+        return self._xs
 
     def check_labels(self, labels_np):
         labels_np = np.asarray(labels_np)

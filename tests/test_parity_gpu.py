@@ -264,3 +264,46 @@ def test_int8_tensor_core_projection_is_exact(w_f64):
     cnt = x.astype(np.float64).sum(-1)                           # [B, T]
     bound = 1.12e-16 * np.abs(exact) + cnt[..., None] * trunc[None, None, :]
     assert float(np.max(err - bound)) <= 0.0
+
+
+def test_streamed_inputs_match_resident_and_memory_is_flat_in_T():
+    """Streaming x chunk by chunk from pinned host memory gives bitwise the same update as
+    resident inputs, and peak device memory does not grow with T."""
+    _need_gpu()
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200.gradients import _neuron_kwargs
+    net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=256, n_inputs=700, n_classes=20,
+                                       precision="f32", seed=0))
+    kw = _neuron_kwargs(net)
+    B = 16
+    x, y = poisson_batch(B, 700, 300, 20, seed=5)
+    yd = torch.from_numpy(y).cuda()
+    res = {}
+    for mode in ("resident", "streamed"):
+        eng = EpropEngine(256, 700, 20, B, alif=True, chunk=127)
+        eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+        xin = torch.from_numpy(x).cuda() if mode == "resident" else torch.from_numpy(x).pin_memory()
+        eng.run(xin, yd, **kw)
+        torch.cuda.synchronize()
+        res[mode] = (eng.grad_w(torch.float64).cpu().numpy(), eng.loss.cpu().numpy(),
+                     eng.grad_wout.cpu().numpy())
+    for a, b in zip(res["resident"], res["streamed"]):
+        assert np.array_equal(a, b)
+    peaks = []
+    for T in (300, 3000):
+        x, y = poisson_batch(B, 700, T, 20, seed=6)
+        xh = torch.from_numpy(x).pin_memory()
+        yd = torch.from_numpy(y).cuda()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats()
+        base = torch.cuda.memory_allocated()
+        eng = EpropEngine(256, 700, 20, B, alif=True, chunk=127)
+        eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+        eng.run(xh, yd, **kw)
+        torch.cuda.synchronize()
+        peaks.append(torch.cuda.max_memory_allocated() - base)
+        del eng
+    assert peaks[1] <= 1.05 * peaks[0], peaks
