@@ -43,13 +43,15 @@ int spb_device_sm(void); /* compute capability of the current device, e.g. 100 *
  *     (gradients.py:125).
  *   spb_slice_weights: w [n][k] fp32 (w_is_f64=0) / fp64 -> wq [P][n_pad32][Kpad] int8,
  *                      sexp [n] int32 (n_pad32 = round_up(n,32), Kpad = round_up(k,128)).
- *   spb_pack_spikes:   x[b*stride_b + s*k + j] (s < len) -> xq [B*Tc][Kpad] uint8, zero padded.
+ *   spb_pack_spikes:   x row (b, s < len) at x + b*stride_b + s*kb -> xq [B*Tc][Kpad] uint8,
+ *                      zero padded; bits = 0: kb = k bytes (counts), bits = 1: kb = ceil(k/8)
+ *                      bytes, channel j = bit (j & 7) of byte j >> 3 (packbits, little). 
  *   spb_input_proj:    cur[row][i] = sum_j xq[row][j] W[i][j] for row < M (= B*Tc), fp64;
  *                      persistent grid of min(tiles, sm_count) CTAs. */
 int spb_slice_weights(const void* w, int w_is_f64, int n, int k, int Kpad, int n_pad32, int P,
                       int8_t* wq, int* sexp, cudaStream_t stream);
-int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int len, int Tc, int Kpad,
-                    uint8_t* xq, cudaStream_t stream);
+int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits, int len, int Tc,
+                    int Kpad, uint8_t* xq, cudaStream_t stream);
 int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
                    int Kpad, int P, double* cur, int sm_count, cudaStream_t stream);
 
@@ -82,13 +84,14 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
 
 /* K4  Presynaptic filter xbar_t = alpha*xbar_{t-1} + x_t (the factorised LIF trace G_u,
  *     gradients.py:89-94 with H_I = alpha, F rows = x_t; test_gradients.py:81-91).
+ *     x byte counts of (b, s) at x[b*stride_b + s*stride_t + j] (the K2 operand xq works);
  *     xbar_state [B][k] fp64 carry (fresh != 0: start from zero); xh/xl [B*KR][kp] bf16
  *     hi/lo split, MN-major (channels
  *     contiguous, kp >= k, kp % 8 == 0): row b*KR + rho, rho = 0 holds xbar_{t0-1},
  *     rho = s+1 holds xbar_{t0+s}; zero elsewhere. */
-int spb_xbar_chunk(const uint8_t* x, long long stride_b, int B, int k, int kp, int KR,
-                   int len, int fresh, double alpha, double* xbar_state, void* xh, void* xl,
-                   cudaStream_t stream);
+int spb_xbar_chunk(const uint8_t* x, long long stride_b, long long stride_t, int B, int k, int kp,
+                   int KR, int len, int fresh, double alpha, double* xbar_state, void* xh,
+                   void* xl, cudaStream_t stream);
 
 /* K3  Readout + loss: s_b = W_out zsum_b, loss_b = CE(s_b, y_b), g_b = softmax - onehot,
  *     wsig_b = W_out^T g_b.  Replaces gradients.py:163-164,177-178 and

@@ -218,9 +218,9 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
 // coalesced bf16x2 store per warp and row.
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) xbar_chunk_kernel(
-    const uint8_t* __restrict__ x, long long stride_b, int B, int k, int kp, int KR, int len,
-    int fresh, double alpha, double* __restrict__ xbar_st, uint32_t* __restrict__ xh,
-    uint32_t* __restrict__ xl) {
+    const uint8_t* __restrict__ x, long long stride_b, long long stride_t, int B, int k, int kp,
+    int KR, int len, int fresh, double alpha, double* __restrict__ xbar_st,
+    uint32_t* __restrict__ xh, uint32_t* __restrict__ xl) {
   const int jp = blockIdx.x * blockDim.x + threadIdx.x;  // channel pair
   const int j = 2 * jp;
   const int b = blockIdx.y;
@@ -238,8 +238,8 @@ __global__ void __launch_bounds__(128) xbar_chunk_kernel(
     for (int u8 = 0; u8 < 8; ++u8) {
       const int rho = r8 + u8;
       const bool live = rho >= 1 && rho <= len;
-      x0[u8] = (v0 && live) ? xin[(long long)(rho - 1) * k] : 0u;
-      x1[u8] = (v1 && live) ? xin[(long long)(rho - 1) * k + 1] : 0u;
+      x0[u8] = (v0 && live) ? xin[(long long)(rho - 1) * stride_t] : 0u;
+      x1[u8] = (v1 && live) ? xin[(long long)(rho - 1) * stride_t + 1] : 0u;
     }
 #pragma unroll
     for (int u8 = 0; u8 < 8; ++u8) {
@@ -306,16 +306,16 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
   return 0;
 }
 
-int spb_xbar_chunk(const uint8_t* x, long long stride_b, int B, int k, int kp, int KR,
-                   int len, int fresh, double alpha, double* xbar_state, void* xh, void* xl,
-                   cudaStream_t stream) {
+int spb_xbar_chunk(const uint8_t* x, long long stride_b, long long stride_t, int B, int k, int kp,
+                   int KR, int len, int fresh, double alpha, double* xbar_state, void* xh,
+                   void* xl, cudaStream_t stream) {
   SPB_CHECK_ARG(x && xbar_state && xh && xl, "spb_xbar_chunk: null pointer");
   SPB_CHECK_ARG(B > 0 && k > 0 && kp >= k && kp % 8 == 0 && KR > 0 && KR % 8 == 0 && len >= 0 &&
                     len < KR,
                 "spb_xbar_chunk: bad sizes");
   dim3 grid(ceil_div(kp / 2, 128), B);
-  xbar_chunk_kernel<<<grid, 128, 0, stream>>>(x, stride_b, B, k, kp, KR, len, fresh, alpha,
-                                              xbar_state,
+  xbar_chunk_kernel<<<grid, 128, 0, stream>>>(x, stride_b, stride_t, B, k, kp, KR, len, fresh,
+                                              alpha, xbar_state,
                                               reinterpret_cast<uint32_t*>(xh),
                                               reinterpret_cast<uint32_t*>(xl));
   SPB_CHECK_LAUNCH("xbar_chunk");

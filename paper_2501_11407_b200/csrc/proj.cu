@@ -15,7 +15,8 @@
 // truncated) exact sum rounded once, independent of summation order.
 //
 // Kernels:
-//   spb_pack_spikes      x chunk [B][len][k] -> xq [B*Tc][Kpad] (TMA-able, zero padded)
+//   spb_pack_spikes      x chunk [B][len][k] bytes or bits -> xq [B*Tc][Kpad] (TMA-able,
+//                        zero padded; also the row source of K4)
 //   spb_slice_weights    W [n][k] fp32/fp64  -> Wq [P][n_pad32][Kpad] int8, s [n] int32
 //   spb_input_proj       persistent warp-specialised tcgen05 GEMM -> I [B*Tc][n] fp64
 #include "tma.cuh"
@@ -409,26 +410,42 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // x chunk -> zero-padded K-major operand rows (16-byte aligned rows for TMA).
-// One warp per output row (sample b, step s): 16-byte stores of the zero-padded row; the
-// source row (k bytes, any alignment) is read with 4-byte loads when k % 4 == 0.
-__global__ void pack_spikes_kernel(const uint8_t* __restrict__ x, long long stride_b, int k, int len,
-                                   int Tc, int Kpad, int B, uint8_t* __restrict__ xq) {
+// One warp per output row (sample b, step s): 16-byte stores of the zero-padded row.
+// Byte input (bits == 0): the source row has k bytes (4-byte loads when aligned).  Bit
+// input (bits == 1): the source row has ceil(k/8) bytes, channel j = bit (j & 7) of byte
+// j >> 3 (numpy.packbits(..., bitorder="little")) -- 8x less host->device traffic for
+// binary spike trains.
+__device__ __forceinline__ uint32_t expand4(uint32_t nib) {  // 4 bits -> 4 bytes of 0/1
+  return (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+}
+
+__global__ void pack_spikes_kernel(const uint8_t* __restrict__ x, long long stride_b, int k,
+                                   int bits, int len, int Tc, int Kpad, int B,
+                                   uint8_t* __restrict__ xq) {
   const int lane = threadIdx.x & 31;
   const long long rows = (long long)B * Tc;
-  const bool w4 = (k & 3) == 0 && (stride_b & 3) == 0 &&
+  const int kb = bits ? (k + 7) / 8 : k;
+  const bool w4 = !bits && (k & 3) == 0 && (stride_b & 3) == 0 &&
                   (reinterpret_cast<uintptr_t>(x) & 3) == 0;
   for (long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
        row += (long long)gridDim.x * (blockDim.x >> 5)) {
     const int s = (int)(row % Tc);
     const int b = (int)(row / Tc);
-    const uint8_t* src = x + (long long)b * stride_b + (long long)s * k;
+    const uint8_t* src = x + (long long)b * stride_b + (long long)s * kb;
     uint4* dst = reinterpret_cast<uint4*>(xq + row * Kpad);
     const bool live = s < len;
     for (int c = lane; c < Kpad / 16; c += 32) {
       const int j0 = c * 16;
       uint32_t wv[4] = {0u, 0u, 0u, 0u};
       if (live) {
-        if (w4 && j0 + 16 <= k) {
+        if (bits) {
+          uint32_t v16 = 0u;
+          if (j0 < k) v16 = src[j0 >> 3];
+          if (j0 + 8 < k) v16 |= (uint32_t)src[(j0 >> 3) + 1] << 8;
+          if (j0 + 16 > k) v16 &= (k - j0 >= 16) ? 0xffffu : ((1u << (k - j0 > 0 ? k - j0 : 0)) - 1u);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) wv[q] = expand4((v16 >> (4 * q)) & 0xfu);
+        } else if (w4 && j0 + 16 <= k) {
           const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src + j0);
           wv[0] = s4[0]; wv[1] = s4[1]; wv[2] = s4[2]; wv[3] = s4[3];
         } else {
@@ -474,15 +491,16 @@ using namespace spb;
 
 extern "C" {
 
-int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int len, int Tc, int Kpad,
-                    uint8_t* xq, cudaStream_t stream) {
+int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits, int len, int Tc,
+                    int Kpad, uint8_t* xq, cudaStream_t stream) {
   SPB_CHECK_ARG(x && xq && B > 0 && k > 0 && Kpad >= k && Kpad % proj::BK == 0 && len >= 0 &&
                     len <= Tc,
                 "spb_pack_spikes: bad args (Kpad must be a multiple of %d)", proj::BK);
   const long long rows = (long long)B * Tc;
   const long long want = (rows + 7) / 8;
   const int blocks = (int)(want < 148LL * 16 ? want : 148LL * 16);
-  proj::pack_spikes_kernel<<<blocks, 256, 0, stream>>>(x, stride_b, k, len, Tc, Kpad, B, xq);
+  proj::pack_spikes_kernel<<<blocks, 256, 0, stream>>>(x, stride_b, k, bits, len, Tc, Kpad, B,
+                                                        xq);
   SPB_CHECK_LAUNCH("pack_spikes");
   return 0;
 }

@@ -200,11 +200,15 @@ class EpropEngine:
             self._ctab_T = (T, kappa)
         return self.ctab
 
-    def _project(self, xp, strideb, ln, st, timed=None):
-        """K2: pack the chunk's spikes and compute cur = W x_t exactly on INT8 tensor cores."""
+    def _pack(self, xp, strideb, bits, ln, st):
+        """Chunk spikes (bytes or bits) -> zero-padded K2 operand xq [B*Tc][Kpad] (also K4's
+        row source)."""
+        _lib.call("spb_pack_spikes", ctypes_void(xp), strideb, self.B, self.k, int(bits), ln,
+                  self.Tc, self.Kpad, ctypes_void(self.xq.data_ptr()), st)
+
+    def _project(self, ln, st, timed=None):
+        """K2: cur = W x_t exactly on INT8 tensor cores from the packed chunk."""
         v = ctypes_void
-        _lib.call("spb_pack_spikes", v(xp), strideb, self.B, self.k, ln, self.Tc, self.Kpad,
-                  v(self.xq.data_ptr()), st)
         args = ("spb_input_proj", v(self.xq.data_ptr()), v(self.wq.data_ptr()),
                 v(self.sexp.data_ptr()), self.B * self.Tc, self.n, self.n_pad32, self.Kpad,
                 self.P, v(self.cur.data_ptr()), self.sm_count, st)
@@ -216,25 +220,29 @@ class EpropEngine:
     # ----------------------------------------------------------------------------------
     def run(self, x: torch.Tensor, labels: torch.Tensor, *, alpha=0.95, theta=1.0, slope=10.0,
             beta=0.8, rho=0.96, kappa=0.95, reset=False, raster: torch.Tensor | None = None,
-            stream=None, timers: dict | None = None):
-        """One full e-prop update on device-resident inputs.
+            stream=None, timers: dict | None = None, bits: bool = False):
+        """One full e-prop update.
 
-        x       uint8 [B, T, k] spike counts, contiguous.  A CUDA tensor is used in place;
-                a CPU (ideally pinned) tensor is STREAMED: each time chunk is copied into
-                a double-buffered [2, B, Tc, k] device buffer on a copy stream, overlapped
-                with the previous chunk's kernels, so device memory is independent of T.
+        x       uint8 [B, T, k] spike counts, or with ``bits=True`` uint8 [B, T, ceil(k/8)]
+                bit-packed binary spikes (numpy.packbits(..., axis=-1, bitorder="little")).
+                A CUDA tensor is used in place; a CPU (ideally pinned) tensor is STREAMED:
+                each time chunk is copied into a double-buffered device chunk on a copy
+                stream, overlapped with the previous chunk's kernels, so device memory is
+                independent of T.
         labels  int64 [B] (CUDA)
         raster  optional int32 [B, T, ceil(n/32)] bit-packed spike output (pass A)
         timers  optional dict; CUDA event pairs are appended per launch of the main
-                kernels under "proj", "forward", "gemm", "carry".
+                kernels under "proj", "forward_a", "forward", "gemm", "carry".
         Results stay on device: ``grad_w_acc`` (fp64 [n, kp]), ``grad_wout``, ``loss``,
         ``s`` (readout sums), ``correct``.
         """
         if reset:
             raise NotImplementedError(
                 "reset=True makes G_u non-factorisable (SURVEY.md 8(f)-3); not on the B200 path yet")
-        if x.dtype != torch.uint8 or x.dim() != 3 or x.shape[0] != self.B or x.shape[2] != self.k:
-            raise ShapeMismatch(f"x must be uint8 [B={self.B}, T, k={self.k}], got "
+        kb = (self.k + 7) // 8 if bits else self.k
+        if x.dtype != torch.uint8 or x.dim() != 3 or x.shape[0] != self.B or x.shape[2] != kb:
+            raise ShapeMismatch(f"x must be uint8 [B={self.B}, T, {kb}] "
+                                f"({'bit-packed' if bits else 'counts'}), got "
                                 f"{tuple(x.shape)} {x.dtype}")
         if not x.is_contiguous():
             raise ShapeMismatch("x must be contiguous")
@@ -248,11 +256,13 @@ class EpropEngine:
         B, n, k, m, Tc, KR, K = self.B, self.n, self.k, self.m, self.Tc, self.KR, self.K
         ctab = self._gains(T, float(kappa))
         nchunks = (T + Tc - 1) // Tc
-        strideb = T * k
+        one = nchunks == 1
+        strideb = T * kb
         self.launches = 0
         v = ctypes_void
         common = (float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
                   int(self.alif))
+        xq_sb, xq_st = Tc * self.Kpad, self.Kpad          # K4 reads the packed operand
 
         def timed(name, meta, fn, *args):
             if timers is None:
@@ -272,13 +282,13 @@ class EpropEngine:
             # the side stream must not run ahead of the previous update's consumers
             self._ev["start"].record(main)
             self.side.wait_event(self._ev["start"])
-        one = nchunks == 1
+
         # ---- input access: resident (device tensor) or streamed chunk by chunk ----
         if streaming:
             if stream is not None:
                 raise ValueError("streamed inputs use the engine's own streams")
-            xs = self._stream_buffers()
-            uses = list(range(nchunks)) + ([] if one else list(range(nchunks)))
+            xs = self._stream_buffers(kb)
+            uses = list(range(nchunks)) * (1 if one else 2)
             xhost = x.data_ptr()
             for e in self._sev_free:
                 e.record(main)
@@ -289,53 +299,47 @@ class EpropEngine:
                 lnc = min(Tc, T - t0c)
                 bb = u % 2
                 self._cs.wait_event(self._sev_free[bb])
-                call("spb_copy_chunk_h2d", v(xs[bb].data_ptr()), Tc * k, v(xhost + t0c * k),
-                     T * k, lnc * k, B, ctypes_void(self._cs.cuda_stream))
+                call("spb_copy_chunk_h2d", v(xs[bb].data_ptr()), Tc * kb, v(xhost + t0c * kb),
+                     T * kb, lnc * kb, B, ctypes_void(self._cs.cuda_stream))
                 self._sev_ready[bb].record(self._cs)
 
             state = {"u": 0}
 
-            def chunk_in(c):
+            def pack_chunk(c, ln):
                 u = state["u"]
                 if u == 0:
                     _copy(0)
                 if u + 1 < len(uses):
                     _copy(u + 1)
                 main.wait_event(self._sev_ready[u % 2])
-                return xs[u % 2].data_ptr(), Tc * k
-
-            def chunk_done():
-                self._sev_free[state["u"] % 2].record(main)
+                self._pack(xs[u % 2].data_ptr(), Tc * kb, bits, ln, st)
+                self._sev_free[u % 2].record(main)
                 state["u"] += 1
         else:
-            def chunk_in(c):
-                return x.data_ptr() + c * Tc * k, strideb
+            def pack_chunk(c, ln):
+                self._pack(x.data_ptr() + c * Tc * kb, strideb, bits, ln, st)
 
-            def chunk_done():
-                pass
-
-        if one and not streaming:  # K4 depends only on x: overlap it with pass A on the side stream
-            call("spb_xbar_chunk", v(x.data_ptr()), strideb, B, k, self.kp, KR, T, 1,
-                 float(alpha), v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()),
-                 v(self.xl.data_ptr()), sst)
-            self.launches += 1
-            if use_side:
-                self._ev["xbar"].record(self.side)
         # ---------------- pass A ----------------
         for c in range(nchunks):  # chunk 0 starts from fresh state inside the kernels
             t0 = c * Tc
             ln = min(Tc, T - t0)
-            xp, xstride = chunk_in(c)
-            self._project(xp, xstride, ln, st, timed)
-            if not (one and streaming):
-                chunk_done()
-            timed("forward_a", (ln, 0, nchunks == 1), "spb_forward_chunk", 0,
-                 v(self.cur.data_ptr()), B, n, Tc, KR, ln, t0, T,
-                 *common, v(self.u.data_ptr()), v(self.a.data_ptr()),
-                 v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
-                 v(raster.data_ptr()) if raster is not None else None,
-                 None, None, None, None, None, None, 0, None,
-                 v(self.psi.data_ptr()) if nchunks == 1 else None, st)
+            pack_chunk(c, ln)
+            if one and use_side:  # K4 depends only on the packed x: overlap it with pass A
+                self._ev["xbar"].record(main)
+                self.side.wait_event(self._ev["xbar"])
+                call("spb_xbar_chunk", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
+                     ln, 1, float(alpha), v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()),
+                     v(self.xl.data_ptr()), sst)
+                self._ev["xbar"].record(self.side)
+                self.launches += 1
+            self._project(ln, st, timed)
+            timed("forward_a", (ln, 0, one), "spb_forward_chunk", 0,
+                  v(self.cur.data_ptr()), B, n, Tc, KR, ln, t0, T,
+                  *common, v(self.u.data_ptr()), v(self.a.data_ptr()),
+                  v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
+                  v(raster.data_ptr()) if raster is not None else None,
+                  None, None, None, None, None, None, 0, None,
+                  v(self.psi.data_ptr()) if one else None, st)
             self.launches += 3
         # ---------------- readout / loss ----------------
         call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
@@ -356,17 +360,13 @@ class EpropEngine:
             t0 = c * Tc
             ln = min(Tc, T - t0)
             last = c == nchunks - 1
-            if one and streaming:
-                xp, xstride = xs[0].data_ptr(), Tc * k      # still holds the only chunk
-            elif one:
-                xp, xstride = x.data_ptr(), strideb
-            else:
-                xp, xstride = chunk_in(c)
-            if nchunks > 1:  # one chunk: cur of pass A is still valid (same W, same x)
-                self._project(xp, xstride, ln, st, timed)
+            if not one:  # one chunk: xq and cur of pass A are still valid (same W, same x)
+                pack_chunk(c, ln)
+                self._project(ln, st, timed)
+                self.launches += 2
             carry_out = self.alif and not last   # the trace is only needed by a later chunk
             # one chunk: pass A already parked psi -> backward scan only (pass 2)
-            pid = 1 if nchunks > 1 else 2
+            pid = 2 if one else 1
             timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,
                   v(self.cur.data_ptr()), B, n, Tc, KR,
                   ln, t0, T, *common, v(self.u.data_ptr()), v(self.a.data_ptr()), None, None,
@@ -375,28 +375,27 @@ class EpropEngine:
                   v(self.w_hi.data_ptr()) if carry_out else None,
                   v(self.w_lo.data_ptr()) if carry_out else None, self.ldc,
                   v(self.mdt.data_ptr()) if self.alif else None, v(self.psi.data_ptr()), st)
-            if not one or streaming:
-                call("spb_xbar_chunk", v(xp), xstride, B, k, self.kp, KR, ln, int(c == 0),
-                     float(alpha), v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()),
-                     v(self.xl.data_ptr()), st)
-                self.launches += 1
-                chunk_done()
-            elif use_side:
+            self.launches += 1 if one else 2
+            if one and use_side:
                 main.wait_event(self._ev["xbar"])
+            else:
+                call("spb_xbar_chunk", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
+                     ln, int(c == 0), float(alpha), v(self.xbar_state.data_ptr()),
+                     v(self.xh.data_ptr()), v(self.xl.data_ptr()), st)
+                self.launches += 1
             timed("gemm", ln, "spb_grad_gemm_partials", v(self.c_hi.data_ptr()),
                   v(self.c_lo.data_ptr()), self.ldc, v(self.xh.data_ptr()), v(self.xl.data_ptr()),
-                  self.kp, n,
-                  self.kp, K, self.splits5, v(self.partial.data_ptr()), self.kp, slice_stride,
-                  st)
-            self.launches += 5 if nchunks > 1 else 2
+                  self.kp, n, self.kp, K, self.splits5, v(self.partial.data_ptr()), self.kp,
+                  slice_stride, st)
+            self.launches += 1
             slices = self.splits5
             if self.alif and (c > 0 or not last):
                 # first chunk: E0 = 0 (nothing to add, only carry); last chunk: no carry
                 timed("carry", (ln, c > 0, not last), "spb_alif_carry_chunk",
-                      v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()), self.ldc, v(self.xh.data_ptr()),
-                      v(self.xl.data_ptr()), v(self.mdt.data_ptr()), v(self.eps.data_ptr()),
-                      v(part6), B, n, self.n_pad, k, self.ke, self.kp, KR, self.splits6,
-                      int(not last), int(c > 0), int(not last), st)
+                      v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()), self.ldc,
+                      v(self.xh.data_ptr()), v(self.xl.data_ptr()), v(self.mdt.data_ptr()),
+                      v(self.eps.data_ptr()), v(part6), B, n, self.n_pad, k, self.ke, self.kp,
+                      KR, self.splits6, int(not last), int(c > 0), int(not last), st)
                 self.launches += 1
                 if c > 0:
                     slices += self.splits6
@@ -407,10 +406,10 @@ class EpropEngine:
             main.wait_event(self._ev["rg"])
         return self
 
-    def _stream_buffers(self):
+    def _stream_buffers(self, kb):
         """Double-buffered device chunk of the input + copy stream (streaming mode)."""
-        if getattr(self, "_xs", None) is None:
-            self._xs = torch.empty((2, self.B, self.Tc, self.k), dtype=torch.uint8,
+        if getattr(self, "_xs", None) is None or self._xs.shape[-1] != kb:
+            self._xs = torch.empty((2, self.B, self.Tc, kb), dtype=torch.uint8,
                                    device=self.device)
             self._cs = torch.cuda.Stream(device=self.device)
             self._sev_free = [torch.cuda.Event() for _ in range(2)]

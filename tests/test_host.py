@@ -105,7 +105,7 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     names = [c[0] for c in rec.calls]
     nch = (T + chunk - 1) // chunk
     assert names.count("spb_forward_chunk") == 2 * nch
-    # a single chunk reuses pass A's current in pass B
+    # a single chunk reuses pass A's packed spikes and current in pass B
     assert names.count("spb_pack_spikes") == (2 * nch if nch > 1 else 1)
     assert names.count("spb_input_proj") == (2 * nch if nch > 1 else 1)
     assert names.count("spb_slice_weights") == 0

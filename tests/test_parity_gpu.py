@@ -250,7 +250,9 @@ def test_int8_tensor_core_projection_is_exact(w_f64):
     eng.set_weights(torch.from_numpy(w), torch.zeros((3, n), dtype=torch.float64))
     xd = torch.from_numpy(x).cuda()
     v = ctypes.c_void_p
-    eng._project(xd.data_ptr(), T * k, T, v(torch.cuda.current_stream().cuda_stream))
+    st = v(torch.cuda.current_stream().cuda_stream)
+    eng._pack(xd.data_ptr(), T * k, False, T, st)
+    eng._project(T, st)
     torch.cuda.synchronize()
     got = eng.cur.cpu().numpy().reshape(B, eng.Tc, n)[:, :T]
     exact = np.einsum("btk,nk->btn", x.astype(np.longdouble), w.astype(np.longdouble))
@@ -307,3 +309,29 @@ def test_streamed_inputs_match_resident_and_memory_is_flat_in_T():
         peaks.append(torch.cuda.max_memory_allocated() - base)
         del eng
     assert peaks[1] <= 1.05 * peaks[0], peaks
+
+
+@pytest.mark.parametrize("k,T", [(700, 300), (37, 70)])
+def test_bit_packed_inputs_match_byte_inputs(k, T):
+    """Binary spikes given bit-packed (8x less H2D) give bitwise the same update."""
+    _need_gpu()
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200.gradients import _neuron_kwargs
+    net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=160, n_inputs=k, n_classes=5,
+                                       precision="f32", seed=1))
+    B = 6
+    x, y = poisson_batch(B, k, T, 5, seed=9)
+    xbits = np.packbits(x, axis=-1, bitorder="little")
+    yd = torch.from_numpy(y).cuda()
+    outs = []
+    for xin, bits in ((torch.from_numpy(x).cuda(), False), (torch.from_numpy(xbits).cuda(), True),
+                      (torch.from_numpy(xbits).pin_memory(), True)):
+        eng = EpropEngine(160, k, 5, B, alif=True, chunk=63)
+        eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+        eng.run(xin, yd, bits=bits, **_neuron_kwargs(net))
+        torch.cuda.synchronize()
+        outs.append((eng.grad_w(torch.float64).cpu().numpy(), eng.loss.cpu().numpy()))
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
