@@ -26,29 +26,24 @@
 namespace spb {
 namespace carry {
 
-constexpr int BM = 128, BN = 128, BK = 64, STAGES = 3;
-constexpr int TILE = BM * BK * 2;  // 16 KB (BN == BM)
-constexpr int STAGE = 4 * TILE;
-constexpr int EPI_WARPS = 16;  // 4 TMEM lane quarters x 4 column groups of 32
+// Tile: 128 neurons (TMEM lanes) x 128 inputs (TMEM columns); K blocks of 32 rows.
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
+constexpr int TILE = BM * BK * 2;               // 8 KB (two 64-wide MN-major boxes)
+constexpr int STAGE = 4 * TILE;                 // W hi/lo + xbar hi/lo
+constexpr int ETILE = BM * BN * 4;              // 64 KB eps tile (4 boxes of 128 x 32 fp32)
+constexpr int EPI_WARPS = 16;                   // 4 TMEM lane quarters x 4 column groups of 32
 constexpr int THREADS = 64 + EPI_WARPS * 32;
-constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+constexpr int SMEM = 2 * ETILE + STAGES * STAGE + 1024 + 256;
 // A = W, B = xbar, both MN-major (neurons / channels contiguous, written by K1s / K4)
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
-__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr) {
+// MN-major SWIZZLE_128B operand: 64-element MN runs (128 B rows, one per K), 8-row K
+// groups 1024 B apart (SBO), the second 64-element MN half one box (LBO) further.
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr, uint32_t lbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)(8192u >> 4) << 16;   // LBO: next 64-wide MN block
-  d |= (uint64_t)(1024u >> 4) << 32;   // SBO: next 8-row K group
-  d |= (uint64_t)1u << 46;
-  d |= (uint64_t)2u << 61;
-  return d;
-}
-__device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)(1024u >> 4) << 32;
   d |= (uint64_t)1u << 46;
   d |= (uint64_t)2u << 61;
@@ -68,20 +63,6 @@ __device__ __forceinline__ void commit(uint32_t bar) {
 __device__ __forceinline__ void arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&r)[32]) {
-  uint32_t* v = reinterpret_cast<uint32_t*>(r);
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&r)[16]) {
   uint32_t* v = reinterpret_cast<uint32_t*>(r);
   asm volatile(
@@ -94,21 +75,32 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Per CTA: one 128x128 synapse tile, a contiguous range of samples.  Warp 0 streams, per
+// sample, the sample's eps~ tile E0 (4 TMA boxes, SWIZZLE_128B, double-buffered so the next
+// sample's tile is in flight while this one is consumed) and the W / xbar K-blocks of the
+// per-sample GEMM (3-stage ring); warp 1 issues the tcgen05 MMAs into one of two TMEM
+// buffers; 16 epilogue warps combine E_end = Dt E0 + D (written back with plain stores)
+// and grad += M E0 (registers across samples).
 __global__ void __launch_bounds__(THREADS, 1)
     alif_carry_kernel(const __grid_constant__ CUtensorMap tm_wh, const __grid_constant__ CUtensorMap tm_wl,
                       const __grid_constant__ CUtensorMap tm_xh, const __grid_constant__ CUtensorMap tm_xl,
+                      const __grid_constant__ CUtensorMap tm_eps,
                       const float2* __restrict__ mdt, float* __restrict__ eps,
                       float* __restrict__ partial, int B, int n, int n_pad, int ke, int kp, int KR,
                       int b_per_split, int do_mma, int load_eps, int store_eps) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint8_t* esm = smem;                             // [2][4 boxes][128 rows][128 B]
+  uint8_t* osm = smem + 2 * ETILE;                 // [STAGES][4][TILE]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(osm + STAGES * STAGE);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint64_t* efull = bars + 2 * STAGES + 4;
+  uint64_t* eempty = bars + 2 * STAGES + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
@@ -124,6 +116,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&tfull[a]), 1);
       mbar_init(smem_u32(&tempty[a]), EPI_WARPS);
+      mbar_init(smem_u32(&efull[a]), 1);
+      mbar_init(smem_u32(&eempty[a]), EPI_WARPS);
     }
     mbar_fence_init();
     if (do_mma) {
@@ -132,6 +126,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tma_prefetch_desc(&tm_xh);
       tma_prefetch_desc(&tm_xl);
     }
+    if (load_eps) tma_prefetch_desc(&tm_eps);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -145,24 +140,38 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0 && do_mma) {
+    if (lane == 0) {
       int it = 0;
       for (int lb = 0; lb < nb; ++lb) {
-        const int kbase = (b0 + lb) * KR;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(smem_u32(&empty[s]), ((it / STAGES) & 1) ^ 1);
-          const uint32_t st = smem_u32(smem + s * STAGE);
-          const uint32_t fb = smem_u32(&full[s]);
-          mbar_expect_tx(fb, STAGE);
-          tma_load_2d(st, &tm_wh, fb, i0, kbase + kb * BK);
-          tma_load_2d(st + TILE / 2, &tm_wh, fb, i0 + 64, kbase + kb * BK);
-          tma_load_2d(st + TILE, &tm_wl, fb, i0, kbase + kb * BK);
-          tma_load_2d(st + TILE + TILE / 2, &tm_wl, fb, i0 + 64, kbase + kb * BK);
-          tma_load_2d(st + 2 * TILE, &tm_xh, fb, j0, kbase + kb * BK);
-          tma_load_2d(st + 2 * TILE + TILE / 2, &tm_xh, fb, j0 + 64, kbase + kb * BK);
-          tma_load_2d(st + 3 * TILE, &tm_xl, fb, j0, kbase + kb * BK);
-          tma_load_2d(st + 3 * TILE + TILE / 2, &tm_xl, fb, j0 + 64, kbase + kb * BK);
+        const int b = b0 + lb;
+        if (load_eps) {  // this sample's eps~ tile, 4 boxes of 32 columns
+          const int eb = lb & 1;
+          mbar_wait(smem_u32(&eempty[eb]), ((lb >> 1) & 1) ^ 1);
+          const uint32_t fb = smem_u32(&efull[eb]);
+          mbar_expect_tx(fb, ETILE);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            tma_load_2d(smem_u32(esm + eb * ETILE + q * (ETILE / 4)), &tm_eps, fb, j0 + 32 * q,
+                        b * n_pad + i0);
+        }
+        if (do_mma) {
+          const int kbase = b * KR;
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(smem_u32(&empty[s]), ((it / STAGES) & 1) ^ 1);
+            const uint32_t st = smem_u32(osm + s * STAGE);
+            const uint32_t fb = smem_u32(&full[s]);
+            mbar_expect_tx(fb, STAGE);
+            const int kr = kbase + kb * BK;
+            tma_load_2d(st, &tm_wh, fb, i0, kr);
+            tma_load_2d(st + TILE / 2, &tm_wh, fb, i0 + 64, kr);
+            tma_load_2d(st + TILE, &tm_wl, fb, i0, kr);
+            tma_load_2d(st + TILE + TILE / 2, &tm_wl, fb, i0 + 64, kr);
+            tma_load_2d(st + 2 * TILE, &tm_xh, fb, j0, kr);
+            tma_load_2d(st + 2 * TILE + TILE / 2, &tm_xh, fb, j0 + 64, kr);
+            tma_load_2d(st + 3 * TILE, &tm_xl, fb, j0, kr);
+            tma_load_2d(st + 3 * TILE + TILE / 2, &tm_xl, fb, j0 + 64, kr);
+          }
         }
       }
     }
@@ -178,13 +187,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int s = it % STAGES;
           mbar_wait(smem_u32(&full[s]), (it / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t st = smem_u32(smem + s * STAGE);
+          const uint32_t st = smem_u32(osm + s * STAGE);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint32_t off = kk * 32, offw = kk * 2048;
-            const uint64_t dwh = desc_mn_sw128(st + offw), dwl = desc_mn_sw128(st + TILE + offw);
-            const uint64_t dxh = desc_mn_sw128(st + 2 * TILE + offw),
-                           dxl = desc_mn_sw128(st + 3 * TILE + offw);
+            const uint32_t off = kk * 2048;  // 16 K rows of the MN-major tiles
+            const uint64_t dwh = desc_mn_sw128(st + off, TILE / 2),
+                           dwl = desc_mn_sw128(st + TILE + off, TILE / 2);
+            const uint64_t dxh = desc_mn_sw128(st + 2 * TILE + off, TILE / 2),
+                           dxl = desc_mn_sw128(st + 3 * TILE + off, TILE / 2);
             mma_bf16(d, dwh, dxh, (kb | kk) ? 1u : 0u);
             mma_bf16(d, dwh, dxl, 1u);
             mma_bf16(d, dwl, dxh, 1u);
@@ -196,7 +206,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     const int q = warp & 3;            // TMEM lane quarter of this warp
-    const int cg = (warp - 2) >> 2;    // 32-column group
+    const int cg = (warp - 2) >> 2;    // 32-column group = eps box
     const int r = q * 32 + lane;       // tile-local neuron row
     const int i = i0 + r;
     const bool vi = i < n;
@@ -207,50 +217,50 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int lb = 0; lb < nb; ++lb) {
       const int b = b0 + lb;
       const int a = lb & 1;
-      float* erow = eps + ((long long)b * n_pad + i) * ke + c0;
-      // issue the eps loads first: they do not depend on the tensor-core product
-      float4 e0[8];
-#pragma unroll
-      for (int v4 = 0; v4 < 8; ++v4) {
-        e0[v4] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (load_eps && vi && c0 + v4 * 4 < ke) e0[v4] = *reinterpret_cast<const float4*>(erow + v4 * 4);
-      }
+      const int eb = lb & 1;
       const float2 md = vi ? mdt[(long long)b * n + i] : make_float2(0.f, 0.f);
+      const uint8_t* erow = esm + eb * ETILE + cg * (ETILE / 4) + r * 128;
+      if (load_eps) mbar_wait(smem_u32(&efull[eb]), (lb >> 1) & 1);
       if (do_mma) {
         mbar_wait(smem_u32(&tfull[a]), (lb >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       }
+      float* grow = eps + ((long long)b * n_pad + i) * ke + c0;
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
-      float D[16];
+        float D[16];
+        if (do_mma) {
+          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + cg * 32 + hf * 16), D);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) D[c] = 0.f;
+        }
+#pragma unroll
+        for (int v4 = hf * 4; v4 < hf * 4 + 4; ++v4) {
+          float4 e0 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (load_eps)  // SWIZZLE_128B: 16-byte chunk v4 of row r sits at chunk v4 ^ (r & 7)
+            e0 = *reinterpret_cast<const float4*>(erow + ((v4 ^ (r & 7)) << 4));
+          g[v4 * 4 + 0] = fmaf(md.x, e0.x, g[v4 * 4 + 0]);
+          g[v4 * 4 + 1] = fmaf(md.x, e0.y, g[v4 * 4 + 1]);
+          g[v4 * 4 + 2] = fmaf(md.x, e0.z, g[v4 * 4 + 2]);
+          g[v4 * 4 + 3] = fmaf(md.x, e0.w, g[v4 * 4 + 3]);
+          if (store_eps && vi && c0 + v4 * 4 < ke) {
+            const int dv = (v4 - hf * 4) * 4;
+            float4 en;
+            en.x = fmaf(md.y, e0.x, D[dv + 0]);
+            en.y = fmaf(md.y, e0.y, D[dv + 1]);
+            en.z = fmaf(md.y, e0.z, D[dv + 2]);
+            en.w = fmaf(md.y, e0.w, D[dv + 3]);
+            *reinterpret_cast<float4*>(grow + v4 * 4) = en;
+          }
+        }
+      }
+      __syncwarp();
       if (do_mma) {
-        tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + cg * 32 + hf * 16), D);
-        if (hf == 1) {
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) arrive(smem_u32(&tempty[a]));
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 16; ++c) D[c] = 0.f;
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        if (lane == 0) arrive(smem_u32(&tempty[a]));
       }
-#pragma unroll
-      for (int v4 = hf * 4; v4 < hf * 4 + 4; ++v4) {
-        g[v4 * 4 + 0] = fmaf(md.x, e0[v4].x, g[v4 * 4 + 0]);
-        g[v4 * 4 + 1] = fmaf(md.x, e0[v4].y, g[v4 * 4 + 1]);
-        g[v4 * 4 + 2] = fmaf(md.x, e0[v4].z, g[v4 * 4 + 2]);
-        g[v4 * 4 + 3] = fmaf(md.x, e0[v4].w, g[v4 * 4 + 3]);
-        if (store_eps && vi && c0 + v4 * 4 < ke) {
-          float4 en;
-          const int dv = (v4 - hf * 4) * 4;
-          en.x = fmaf(md.y, e0[v4].x, D[dv + 0]);
-          en.y = fmaf(md.y, e0[v4].y, D[dv + 1]);
-          en.z = fmaf(md.y, e0[v4].z, D[dv + 2]);
-          en.w = fmaf(md.y, e0[v4].w, D[dv + 3]);
-          *reinterpret_cast<float4*>(erow + v4 * 4) = en;
-        }
-      }
-      }
+      if (load_eps && lane == 0) arrive(smem_u32(&eempty[eb]));
     }
     if (vi) {
       float* prow = partial + ((long long)blockIdx.z * n_pad + i) * kp + c0;
@@ -344,12 +354,18 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
   SPB_CHECK_ARG(mdt && eps && partial, "spb_alif_carry_chunk: null pointer");
   SPB_CHECK_ARG(!do_mma || (wh && wl && xh && xl), "spb_alif_carry_chunk: missing GEMM operands");
   SPB_CHECK_ARG(n_pad % carry::BM == 0 && n <= n_pad && kp % carry::BN == 0 && kp >= k &&
-                    ke >= k && ke % 4 == 0 && KR % carry::BK == 0,
+                    ke >= k && ke % 4 == 0 && KR % carry::BK == 0 && (kp / carry::BN) * carry::BN == kp,
                 "spb_alif_carry_chunk: bad padding (n_pad %% 128, kp %% 128, ke %% 4, KR %% 64)");
   SPB_CHECK_ARG(B > 0 && splits > 0 && splits <= B, "spb_alif_carry_chunk: bad split");
   SPB_CHECK_ARG(!do_mma || (ldw >= n && ldw % 8 == 0), "spb_alif_carry_chunk: bad ldw");
   SPB_CHECK_ARG(!(store_eps && !do_mma), "spb_alif_carry_chunk: storing eps needs the GEMM");
-  CUtensorMap mwh{}, mwl{}, mxh{}, mxl{};
+  CUtensorMap mwh{}, mwl{}, mxh{}, mxl{}, meps{};
+  if (load_eps &&
+      !make_tmap_2d(&meps, eps, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ke, (uint64_t)B * n_pad,
+                    (uint64_t)ke * 4, 32, carry::BM, CU_TENSOR_MAP_SWIZZLE_128B)) {
+    set_error("spb_alif_carry_chunk: cuTensorMapEncodeTiled (eps) failed");
+    return 3;
+  }
   if (do_mma) {
     const uint64_t K = (uint64_t)B * KR;
     const bool ok =
@@ -371,8 +387,8 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
                        carry::SMEM);
   dim3 grid(kp / carry::BN, n_pad / carry::BM, splits);
   carry::alif_carry_kernel<<<grid, carry::THREADS, carry::SMEM, stream>>>(
-      mwh, mwl, mxh, mxl, reinterpret_cast<const float2*>(mdt), eps, partial, B, n, n_pad, ke, kp,
-      KR, bps, do_mma, load_eps, store_eps);
+      mwh, mwl, mxh, mxl, meps, reinterpret_cast<const float2*>(mdt), eps, partial, B, n, n_pad,
+      ke, kp, KR, bps, do_mma, load_eps, store_eps);
   SPB_CHECK_LAUNCH("alif_carry");
   return 0;
 }
