@@ -59,6 +59,8 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
  *     b*Tc+s): ALIF/LIF state update, spike and surrogate derivative.
  *     Replaces _step_state (gradients.py:118-129) + heaviside/surrogate_grad
  *     (graph.py:40-52) + the readout spike filter (gradients.py:173-174).
+ *     smooth != 0: spikes are 0.5 + d/(1+slope|d|) (surrogate_smooth, graph.py:45-47; the
+ *             reference's smooth=True finite-difference mode), raster bit = z > 0.5.
  *     u, a    [B][n] fp64 state, carried across chunks (t0 == 0: fresh zero state, not read)
  *     pass 0 (A): zbar, zsum [B][n] fp64 carried; raster [B][T][ceil(n/32)] bit-packed
  *                 spikes (optional, may be NULL); psi_scratch optional: when given, the
@@ -77,10 +79,10 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
  *                 (forward.cu header has the algebra).  KR >= Tc+1, KR % 8 == 0. */
 int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR, int len, int t0,
                       int T, double alpha, double theta, double slope, double beta, double rho,
-                      double kappa, int reset, int alif, double* u, double* a, double* zbar,
-                      double* zsum, uint32_t* raster, const float* wsig, const float* ctab,
-                      void* c_hi, void* c_lo, void* w_hi, void* w_lo, int ldc, float* mdt,
-                      float* psi_scratch, cudaStream_t stream);
+                      double kappa, int reset, int alif, int smooth, double* u, double* a,
+                      double* zbar, double* zsum, uint32_t* raster, const float* wsig,
+                      const float* ctab, void* c_hi, void* c_lo, void* w_hi, void* w_lo, int ldc,
+                      float* mdt, float* psi_scratch, cudaStream_t stream);
 
 /* K4  Presynaptic filter xbar_t = alpha*xbar_{t-1} + x_t (the factorised LIF trace G_u,
  *     gradients.py:89-94 with H_I = alpha, F rows = x_t; test_gradients.py:81-91).
@@ -148,6 +150,19 @@ int spb_copy_chunk_h2d(void* dst, long long dst_pitch, const void* src, long lon
 /* out[r][c] = acc[r*ld + c] cast to fp32 (out_is_f64=0) or fp64. */
 int spb_finalize_grad(const double* acc, int rows, int cols, int ld, void* out, int out_is_f64,
                       cudaStream_t stream);
+
+/* Optimizer steps on device after the gradient / allreduce, restating
+ * sgd_update / adam_update (training.py:58-91) operation by operation in the parameter
+ * dtype (p_is_f64 ? fp64 : fp32).  p [rows][cols] (and Adam moments m, v, same dtype) are
+ * updated in place; the gradient is g [rows][ld_g] (fp64 accumulator or the packed
+ * allreduce buffer, g_is_f64), multiplied by g_scale (1/B for a batch mean) and rounded
+ * to the parameter dtype first; t >= 1 is the Adam step count after increment; mirror
+ * (optional, fp64 [rows][cols]) receives the updated parameter. */
+int spb_sgd_update(void* p, int p_is_f64, int rows, int cols, const void* g, int g_is_f64,
+                   int ld_g, double g_scale, double lr, double* mirror, cudaStream_t stream);
+int spb_adam_update(void* p, void* m, void* v, int p_is_f64, int rows, int cols, const void* g,
+                    int g_is_f64, int ld_g, double g_scale, double lr, double beta1, double beta2,
+                    double eps, int t, double* mirror, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

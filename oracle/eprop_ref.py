@@ -357,3 +357,67 @@ def poisson_batch(n_samples, n_channels, n_steps, n_classes, seed=0):
         labels[s] = label
         x[s] = rng.random((n_steps, n_channels)) < rates[label]        # datasets.py:65-67
     return x, labels
+
+
+# --------------------------------------------------------------------------------------
+# training loop (training.py:58-166) -- checker for the device trainer
+# --------------------------------------------------------------------------------------
+
+def sgd_update(params, grads, lr):
+    """p - lr*g per parameter, numpy weak-scalar promotion -- training.py:58-65."""
+    return {key: p - lr * grads[key] for key, p in params.items()}
+
+
+def adam_update(params, grads, lr, state, beta1=0.9, beta2=0.999, eps=1e-8):
+    """training.py:75-91; ``state`` is a dict {"m": {}, "v": {}, "t": int}."""
+    state["t"] += 1
+    out = {}
+    for key, p in params.items():
+        g = grads[key]
+        m = state["m"].get(key, np.zeros_like(p))
+        v = state["v"].get(key, np.zeros_like(p))
+        m = beta1 * m + (1 - beta1) * g
+        v = beta2 * v + (1 - beta2) * g * g
+        state["m"][key], state["v"][key] = m, v
+        m_hat = m / (1 - beta1 ** state["t"])
+        v_hat = v / (1 - beta2 ** state["t"])
+        out[key] = p - lr * m_hat / (np.sqrt(v_hat) + eps)
+    return out
+
+
+def train_online(w, w_out, p: Params, x, labels, optimizer="sgd", lr=0.01, epochs=1,
+                 max_updates=None, batch_size=1):
+    """Online e-prop training -- training.py:116-166 with eprop_forward_mode as the
+    engine.  ``batch_size > 1`` applies the batch-MEAN gradient, the
+    device trainer's batched mode.  Returns (w, w_out, [(epoch, loss, accuracy)])."""
+    dtype = w.dtype
+    w, w_out = w.copy(), w_out.copy()
+    state = {"m": {}, "v": {}, "t": 0}
+    rows, updates = [], 0
+    N = x.shape[0]
+    for epoch in range(epochs):
+        seen, correct = 0, 0
+        for s0 in range(0, N, batch_size):
+            nb = min(batch_size, N - s0)
+            gw = np.zeros_like(w, dtype=np.float64)
+            gwo = np.zeros_like(w_out, dtype=np.float64)
+            losses = []
+            for s in range(s0, s0 + nb):
+                r = eprop_forward_mode(w, w_out, p, x[s].astype(dtype), int(labels[s]))
+                gw += r.grad_w
+                gwo += r.grad_w_out
+                losses.append(r.loss)
+                correct += int(np.argmax(r.readout_sum) == labels[s])
+            grads = {"w": (gw / nb).astype(dtype), "w_out": (gwo / nb).astype(dtype)}
+            params = {"w": w, "w_out": w_out}
+            if optimizer == "adam":
+                params = adam_update(params, grads, lr, state)
+            else:
+                params = sgd_update(params, grads, lr)
+            w, w_out = params["w"].astype(dtype), params["w_out"].astype(dtype)
+            seen += nb
+            updates += 1
+            rows.append((epoch, float(np.mean(losses)), correct / seen))
+            if max_updates is not None and updates >= max_updates:
+                return w, w_out, rows
+    return w, w_out, rows

@@ -24,7 +24,7 @@ SIGNATURES = {
     "spb_slice_weights": [P, I, I, I, I, I, I, P, P, P],
     "spb_pack_spikes": [P, LL, I, I, I, I, I, I, P, P],
     "spb_input_proj": [P, P, P, I, I, I, I, I, P, I, P],
-    "spb_forward_chunk": [I, P, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I,
+    "spb_forward_chunk": [I, P, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I, I,
                           P, P, P, P, P, P, P, P, P, P, P, I, P, P, P],
     "spb_xbar_chunk": [P, LL, LL, I, I, I, I, I, I, D, P, P, P, P],
     "spb_readout_loss": [P, P, P, I, I, I, P, P, P, P, P, P],
@@ -35,6 +35,8 @@ SIGNATURES = {
     "spb_reduce_partials": [P, I, I, I, I, I, P, P],
     "spb_finalize_grad": [P, I, I, I, P, I, P],
     "spb_copy_chunk_h2d": [P, LL, P, LL, LL, I, P],
+    "spb_sgd_update": [P, I, I, I, P, I, I, D, D, P, P],
+    "spb_adam_update": [P, P, P, I, I, I, P, I, I, D, D, D, D, D, I, P, P],
     "spb_version": [],
     "spb_device_sm": [],
 }

@@ -31,7 +31,16 @@ struct FwdParams {
   int B, n, Tc, KR, len, t0, T;
   double alpha, theta, slope, beta, rho, kappa;
   int reset, alif, pass;  // pass 0 = A, 1 = B
+  int smooth;             // 1: spikes are surrogate_smooth(d) (graph.py:45-47), not Theta(d)
 };
+
+// z = spike(d): Theta(d) = [d >= 0] (graph.py:50-52) or, with smooth=True (the reference's
+// finite-difference mode, gradients.py:114-115), 0.5 + d / (1 + slope |d|) in the
+// reference's operation order.
+__device__ __forceinline__ double spike_value(double d, bool smooth, double slope) {
+  if (!smooth) return d >= 0.0 ? 1.0 : 0.0;
+  return __dadd_rn(0.5, __ddiv_rn(d, __dadd_rn(1.0, __dmul_rn(slope, fabs(d)))));
+}
 
 constexpr int K1_THREADS = 128;  // 4 warps = 4 samples x 32 neurons
 
@@ -70,6 +79,8 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
   // expression from the same state, gradients.py:159): carry it.
   double d_prev = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
   const float slope = (float)P.slope;
+  const double slope_d = P.slope;
+  const bool smooth = P.smooth != 0;
   // psi of row rho at prow[rho*n] (pass B; optional in pass A, which lets a one-chunk
   // sequence skip the pass-B dynamics entirely)
   const bool park = psis != nullptr && valid_i;
@@ -85,16 +96,17 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
       const int s = s8 + u8;
       if (s < P.len) {
         // gradients.py:121-129 (u - theta - beta*a evaluates as (u - theta) - (beta*a))
-        const double z_prev = d_prev >= 0.0 ? 1.0 : 0.0;
+        const double z_prev = spike_value(d_prev, smooth, slope_d);
         a = __dadd_rn(__dmul_rn(P.rho, a), z_prev);
         u = __dadd_rn(__dmul_rn(P.alpha, u), Ib[u8]);
         if (P.reset) u = __dsub_rn(u, __dmul_rn(theta, z_prev));
         const double d = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
-        const bool z = d >= 0.0;
         if (P.pass == 0) {
-          zbar = __dadd_rn(__dmul_rn(P.kappa, zbar), z ? 1.0 : 0.0);
+          const double zv = spike_value(d, smooth, slope_d);
+          zbar = __dadd_rn(__dmul_rn(P.kappa, zbar), zv);
           zsum = __dadd_rn(zsum, zbar);
-          const unsigned bal = __ballot_sync(0xffffffffu, z && valid_i);
+          // raster = z > 0.5 (gradients.py:362)
+          const unsigned bal = __ballot_sync(0xffffffffu, zv > 0.5 && valid_i);
           if (raster != nullptr && lane == 0)
             raster[((long long)b * P.T + P.t0 + s) * nw + blockIdx.x] = bal;
         }
@@ -272,10 +284,10 @@ extern "C" {
 
 int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR, int len, int t0,
                       int T, double alpha, double theta, double slope, double beta, double rho,
-                      double kappa, int reset, int alif, double* u, double* a, double* zbar,
-                      double* zsum, uint32_t* raster, const float* wsig, const float* ctab,
-                      void* c_hi, void* c_lo, void* w_hi, void* w_lo, int ldc, float* mdt,
-                      float* psi_scratch, cudaStream_t stream) {
+                      double kappa, int reset, int alif, int smooth, double* u, double* a,
+                      double* zbar, double* zsum, uint32_t* raster, const float* wsig,
+                      const float* ctab, void* c_hi, void* c_lo, void* w_hi, void* w_lo, int ldc,
+                      float* mdt, float* psi_scratch, cudaStream_t stream) {
   SPB_CHECK_ARG(pass >= 0 && pass <= 2,
                 "spb_forward_chunk: pass must be 0 (A), 1 (B) or 2 (B scan only)");
   SPB_CHECK_ARG(pass == 2 || (cur && u && a), "spb_forward_chunk: null pointer");
@@ -288,7 +300,8 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
                 "spb_forward_chunk: ALIF pass B needs mdt (and w_lo with w_hi)");
   SPB_CHECK_ARG(pass == 0 || (ldc >= n && ldc % 8 == 0), "spb_forward_chunk: ldc must be >= n, %% 8");
   SPB_CHECK_ARG(!(pass >= 1 && reset), "spb_forward_chunk: reset=True has no two-pass form");
-  FwdParams P{B, n, Tc, KR, len, t0, T, alpha, theta, slope, beta, rho, kappa, reset, alif, pass};
+  FwdParams P{B, n, Tc, KR, len, t0, T, alpha, theta, slope, beta, rho, kappa, reset, alif, pass,
+              smooth};
   dim3 grid(ceil_div(n, 32), ceil_div(B, K1_THREADS / 32));
   if (pass <= 1) {
     forward_chunk_kernel<<<grid, K1_THREADS, 0, stream>>>(P, cur, u, a, zbar, zsum, raster, wsig,

@@ -1,0 +1,154 @@
+// On-device optimizer steps fused after the gradient (and its allreduce): SURVEY.md 8(f)-1.
+//
+// Reference: sgd_update / adam_update (training.py:58-91).  The reference applies them to
+// numpy arrays in the network's dtype with Python-float hyper-parameters, i.e. every
+// operation is one IEEE operation in that dtype with the scalar first rounded to it
+// (numpy 2 weak-scalar promotion):
+//   sgd   p <- p - lr*g
+//   adam  m <- b1*m + (1-b1)*g ; v <- b2*v + ((1-b2)*g)*g
+//         p <- p - (lr*(m/(1-b1^t))) / (sqrt(v/(1-b2^t)) + eps)
+// The kernels restate exactly that operation order with explicit round-to-nearest
+// intrinsics (no FMA contraction), so a batch-1 run on the B200 applies the same update
+// to the same gradient as the reference.
+//
+// Gradients come straight from the engine's accumulator (fp64 [rows][ld_g], or the
+// packed fp32/fp64 allreduce buffer) and are scaled (1/B for a batch mean) and rounded
+// to the parameter dtype first -- the reference hands the optimizer grads already cast
+// to w.dtype (gradients.py:180-181).  `mirror` (optional) receives the updated parameter
+// in fp64 (the readout weights the loss kernel reads).  Elementwise, HBM-bound: one
+// thread per parameter, grid-stride.
+#include "common.cuh"
+
+namespace spb {
+
+template <typename T>
+struct Op;
+template <>
+struct Op<float> {
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+  static __device__ __forceinline__ float sqrt(float a) { return __fsqrt_rn(a); }
+};
+template <>
+struct Op<double> {
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+  static __device__ __forceinline__ double sqrt(double a) { return __dsqrt_rn(a); }
+};
+
+struct GradSrc {
+  const void* g;
+  int g_is_f64;
+  int ld;
+  double scale;
+};
+
+template <typename T>
+__device__ __forceinline__ T load_grad(const GradSrc& s, long long r, long long c) {
+  const long long o = r * s.ld + c;
+  const double v = s.g_is_f64 ? static_cast<const double*>(s.g)[o]
+                              : (double)static_cast<const float*>(s.g)[o];
+  return (T)(s.scale == 1.0 ? v : __dmul_rn(v, s.scale));
+}
+
+template <typename T>
+__global__ void sgd_kernel(T* __restrict__ p, GradSrc gs, int rows, int cols, T lr,
+                           double* __restrict__ mirror) {
+  using O = Op<T>;
+  const long long total = (long long)rows * cols;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long r = idx / cols, c = idx - r * cols;
+    const T g = load_grad<T>(gs, r, c);
+    const T v = O::sub(p[idx], O::mul(lr, g));
+    p[idx] = v;
+    if (mirror) mirror[idx] = (double)v;
+  }
+}
+
+template <typename T>
+struct AdamScalars {
+  T lr, b1, omb1, b2, omb2, bc1, bc2, eps;
+};
+
+template <typename T>
+__global__ void adam_kernel(T* __restrict__ p, T* __restrict__ m, T* __restrict__ v, GradSrc gs,
+                            int rows, int cols, AdamScalars<T> a, double* __restrict__ mirror) {
+  using O = Op<T>;
+  const long long total = (long long)rows * cols;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long r = idx / cols, c = idx - r * cols;
+    const T g = load_grad<T>(gs, r, c);
+    const T mn = O::add(O::mul(a.b1, m[idx]), O::mul(a.omb1, g));      // training.py:84
+    const T vn = O::add(O::mul(a.b2, v[idx]), O::mul(O::mul(a.omb2, g), g));  // :85
+    m[idx] = mn;
+    v[idx] = vn;
+    const T m_hat = O::div(mn, a.bc1);                                   // :87
+    const T v_hat = O::div(vn, a.bc2);                                   // :88
+    const T step = O::div(O::mul(a.lr, m_hat), O::add(O::sqrt(v_hat), a.eps));  // :89
+    const T pn = O::sub(p[idx], step);
+    p[idx] = pn;
+    if (mirror) mirror[idx] = (double)pn;
+  }
+}
+
+static int grid_for(long long total, int sm_count) {
+  const long long want = (total + 255) / 256;
+  const long long cap = (long long)(sm_count > 0 ? sm_count : 148) * 8;
+  return (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+}  // namespace spb
+
+using namespace spb;
+
+extern "C" {
+
+int spb_sgd_update(void* p, int p_is_f64, int rows, int cols, const void* g, int g_is_f64,
+                   int ld_g, double g_scale, double lr, double* mirror, cudaStream_t stream) {
+  SPB_CHECK_ARG(p && g && rows > 0 && cols > 0 && ld_g >= cols, "spb_sgd_update: bad args");
+  const GradSrc gs{g, g_is_f64, ld_g, g_scale};
+  const int grid = grid_for((long long)rows * cols, 148);
+  if (p_is_f64)
+    sgd_kernel<double><<<grid, 256, 0, stream>>>(static_cast<double*>(p), gs, rows, cols, lr,
+                                                 mirror);
+  else
+    sgd_kernel<float><<<grid, 256, 0, stream>>>(static_cast<float*>(p), gs, rows, cols,
+                                                (float)lr, mirror);
+  SPB_CHECK_LAUNCH("sgd_update");
+  return 0;
+}
+
+int spb_adam_update(void* p, void* m, void* v, int p_is_f64, int rows, int cols, const void* g,
+                    int g_is_f64, int ld_g, double g_scale, double lr, double beta1, double beta2,
+                    double eps, int t, double* mirror, cudaStream_t stream) {
+  SPB_CHECK_ARG(p && m && v && g && rows > 0 && cols > 0 && ld_g >= cols && t >= 1,
+                "spb_adam_update: bad args");
+  // Python-float scalars, computed in double exactly as the reference does, then
+  // rounded once to the parameter dtype (numpy weak-scalar promotion)
+  const double omb1 = 1.0 - beta1, omb2 = 1.0 - beta2;
+  const double bc1 = 1.0 - pow(beta1, (double)t), bc2 = 1.0 - pow(beta2, (double)t);
+  const GradSrc gs{g, g_is_f64, ld_g, g_scale};
+  const int grid = grid_for((long long)rows * cols, 148);
+  if (p_is_f64) {
+    AdamScalars<double> a{lr, beta1, omb1, beta2, omb2, bc1, bc2, eps};
+    adam_kernel<double><<<grid, 256, 0, stream>>>(static_cast<double*>(p), static_cast<double*>(m),
+                                                  static_cast<double*>(v), gs, rows, cols, a,
+                                                  mirror);
+  } else {
+    AdamScalars<float> a{(float)lr, (float)beta1, (float)omb1, (float)beta2,
+                         (float)omb2, (float)bc1, (float)bc2, (float)eps};
+    adam_kernel<float><<<grid, 256, 0, stream>>>(static_cast<float*>(p), static_cast<float*>(m),
+                                                 static_cast<float*>(v), gs, rows, cols, a,
+                                                 mirror);
+  }
+  SPB_CHECK_LAUNCH("adam_update");
+  return 0;
+}
+
+}  // extern "C"

@@ -220,7 +220,8 @@ class EpropEngine:
     # ----------------------------------------------------------------------------------
     def run(self, x: torch.Tensor, labels: torch.Tensor, *, alpha=0.95, theta=1.0, slope=10.0,
             beta=0.8, rho=0.96, kappa=0.95, reset=False, raster: torch.Tensor | None = None,
-            stream=None, timers: dict | None = None, bits: bool = False):
+            stream=None, timers: dict | None = None, bits: bool = False, smooth: bool = False,
+            forward_only: bool = False):
         """One full e-prop update.
 
         x       uint8 [B, T, k] spike counts, or with ``bits=True`` uint8 [B, T, ceil(k/8)]
@@ -233,6 +234,10 @@ class EpropEngine:
         raster  optional int32 [B, T, ceil(n/32)] bit-packed spike output (pass A)
         timers  optional dict; CUDA event pairs are appended per launch of the main
                 kernels under "proj", "forward_a", "forward", "gemm", "carry".
+        smooth  spikes are surrogate_smooth(d) instead of Theta(d) (the reference's
+                smooth=True mode, gradients.py:114-115); the trace algebra is unchanged.
+        forward_only  pass A + loss only (network_loss, gradients.py:349-365): no
+                gradients are computed (evaluate()).
         Results stay on device: ``grad_w_acc`` (fp64 [n, kp]), ``grad_wout``, ``loss``,
         ``s`` (readout sums), ``correct``.
         """
@@ -261,7 +266,7 @@ class EpropEngine:
         self.launches = 0
         v = ctypes_void
         common = (float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
-                  int(self.alif))
+                  int(self.alif), int(bool(smooth)))
         xq_sb, xq_st = Tc * self.Kpad, self.Kpad          # K4 reads the packed operand
 
         def timed(name, meta, fn, *args):
@@ -288,7 +293,7 @@ class EpropEngine:
             if stream is not None:
                 raise ValueError("streamed inputs use the engine's own streams")
             xs = self._stream_buffers(kb)
-            uses = list(range(nchunks)) * (1 if one else 2)
+            uses = list(range(nchunks)) * (1 if (one or forward_only) else 2)
             xhost = x.data_ptr()
             for e in self._sev_free:
                 e.record(main)
@@ -324,7 +329,7 @@ class EpropEngine:
             t0 = c * Tc
             ln = min(Tc, T - t0)
             pack_chunk(c, ln)
-            if one and use_side:  # K4 depends only on the packed x: overlap it with pass A
+            if one and use_side and not forward_only:  # K4 needs only x: overlap with pass A
                 self._ev["xbar"].record(main)
                 self.side.wait_event(self._ev["xbar"])
                 call("spb_xbar_chunk", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
@@ -339,12 +344,15 @@ class EpropEngine:
                   v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
                   v(raster.data_ptr()) if raster is not None else None,
                   None, None, None, None, None, None, 0, None,
-                  v(self.psi.data_ptr()) if one else None, st)
+                  v(self.psi.data_ptr()) if (one and not forward_only) else None, st)
             self.launches += 3
         # ---------------- readout / loss ----------------
         call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
              v(labels.data_ptr()), B, n, m, v(self.s.data_ptr()), v(self.loss.data_ptr()),
              v(self.g.data_ptr()), v(self.wsig.data_ptr()), v(self.correct.data_ptr()), st)
+        self.launches += 1
+        if forward_only:
+            return self
         if use_side:  # K7 is off the critical path
             self._ev["ro"].record(main)
             self.side.wait_event(self._ev["ro"])
@@ -352,7 +360,7 @@ class EpropEngine:
              v(self.grad_wout.data_ptr()), sst)
         if use_side:
             self._ev["rg"].record(self.side)
-        self.launches += 2
+        self.launches += 1
         # ---------------- pass B ----------------
         slice_stride = self.n_pad * self.kp
         part6 = self.partial.data_ptr() + self.splits5 * slice_stride * 4

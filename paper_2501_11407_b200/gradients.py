@@ -117,10 +117,10 @@ def eprop_batch_gradient(net: Network, x, labels, *, chunk: int | None = None,
     """Batched online e-prop on the B200: x [B, T, k] spike counts, labels [B].
 
     Returns per-sample losses and readout sums and the gradients SUMMED over the batch
-    (= sum of the reference's per-sample ``eprop_sparse_gradient`` grads).
+    (= sum of the reference's per-sample ``eprop_sparse_gradient`` grads).  ``smooth``
+    replaces the hard threshold by surrogate_smooth in the forward (graph.py:45-47), the
+    reference's finite-difference mode (gradients.py:114-115).
     """
-    if smooth:
-        raise NotImplementedError("smooth=True (finite-difference mode) is not on the B200 path")
     x = np.asarray(x)
     if x.ndim != 3 or x.shape[2] != net.k:
         raise ShapeMismatch(f"x must be [B, T, k={net.k}], got {x.shape}")
@@ -138,7 +138,7 @@ def eprop_batch_gradient(net: Network, x, labels, *, chunk: int | None = None,
     ld = torch.from_numpy(labels).to(dev)
     eng.set_weights(torch.from_numpy(np.ascontiguousarray(net.neuron.w)),
                     torch.from_numpy(np.ascontiguousarray(net.readout.w_out)))
-    eng.run(xd, ld, **_neuron_kwargs(net))
+    eng.run(xd, ld, smooth=smooth, **_neuron_kwargs(net))
     wdt = torch.float64 if net.neuron.w.dtype == np.float64 else torch.float32
     gw = eng.grad_w(wdt)
     gwo = eng.grad_wout.to(wdt)

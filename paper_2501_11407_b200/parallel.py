@@ -5,7 +5,7 @@ them one at a time), so the batch is sharded in contiguous ranges, every rank ke
 its own traces and state (engine.py), and the only collective is a single sum
 allreduce of the packed buffer
 
-    [ grad W (n*k) | grad W_out (m*n) | sum of losses | #correct ]      (fp32)
+    [ grad W (n*k) | grad W_out (m*n) | sum of losses | #correct ]      (fp32 or fp64)
 
 issued on the compute stream after the last chunk.
 """
@@ -29,10 +29,12 @@ def shard_range(batch: int, rank: int, world: int):
 class GradPacker:
     """Packs the per-rank results into one flat fp32 buffer and unpacks the reduced sum."""
 
-    def __init__(self, n: int, k: int, m: int, device):
+    def __init__(self, n: int, k: int, m: int, device, dtype=torch.float32):
         self.n, self.k, self.m = n, k, m
         self.size = n * k + m * n + 2
-        self.buf = torch.empty(self.size, dtype=torch.float32, device=device)
+        # fp32 for throughput runs (as the reference's f32 grads); fp64 when training an
+        # f64 network so the allreduce adds no rounding beyond the fp64 sum
+        self.buf = torch.empty(self.size, dtype=dtype, device=device)
 
     def views(self):
         n, k, m = self.n, self.k, self.m

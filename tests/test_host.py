@@ -64,7 +64,7 @@ def test_bad_arguments_are_rejected_without_gpu():
     # argument validation happens before any CUDA call -> works on a CPU-only host
     with pytest.raises(P.ShapeMismatch):
         _lib.call("spb_forward_chunk", 2, None, 1, 1, 63, 64, 1, 0, 1,
-                  0.95, 1.0, 10.0, 0.0, 0.0, 0.95, 0, 0, None, None, None, None, None, None,
+                  0.95, 1.0, 10.0, 0.0, 0.0, 0.95, 0, 0, 0, None, None, None, None, None, None,
                   None, None, None, None, None, 8, None, None, None)
     with pytest.raises(P.ShapeMismatch):
         _lib.call("spb_input_proj", None, None, None, 1, 1, 32, 100, 7, None, 148, None)
@@ -128,6 +128,22 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     if nch == 1:  # pass A parks psi, pass B runs the scan only
         assert [c[1][0] for c in rec.calls if c[0] == "spb_forward_chunk"] == [0, 2]
     assert eng.launches == len(rec.calls) + passb
+
+
+def test_engine_forward_only_dry_run(monkeypatch):
+    rec = _Recorder()
+    monkeypatch.setattr(_lib, "call", rec)
+    eng = EpropEngine(40, 30, 3, 6, alif=True, chunk=63, device="cpu", sm_count=148)
+    eng.run(torch.zeros((6, 150, 30), dtype=torch.uint8), torch.zeros(6, dtype=torch.int64),
+            forward_only=True, smooth=True)
+    names = [c[0] for c in rec.calls]
+    assert names.count("spb_forward_chunk") == 3 and names.count("spb_input_proj") == 3
+    assert names[-1] == "spb_readout_loss"
+    for n in ("spb_xbar_chunk", "spb_grad_gemm_partials", "spb_alif_carry_chunk",
+              "spb_readout_grad"):
+        assert n not in names
+    # smooth flag reaches the kernel (argument after `alif`)
+    assert all(c[1][17] == 1 for c in rec.calls if c[0] == "spb_forward_chunk")
 
 
 def test_engine_rejects_bad_inputs():
