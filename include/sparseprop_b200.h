@@ -76,13 +76,19 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
  *                                          when no later chunk needs the trace)
  *                   mdt [B][n] float2      ALIF (M, Dt) of the chunk (always, ALIF)
  *                 psi_scratch [B][KR+1][n] fp32 working buffer of the scan.
- *                 (forward.cu header has the algebra).  KR >= Tc+1, KR % 8 == 0. */
+ *                 (forward.cu header has the algebra).  KR >= Tc+1, KR % 8 == 0.
+ *     reset != 0 (pass B): the soft reset makes G_u per-synapse (neurons.py:266-271); the
+ *                 scan (K1r) then emits C for the RAW input operand (K4 with alpha = 0),
+ *                 w = W_u, ALIF also wa_hi/wa_lo = W_a, and in mdt: LIF float2
+ *                 (M_u, Dt_uu), ALIF float[8] (M_u, M_a, Dt_uu, Dt_ua, Dt_au, Dt_aa, 0, 0)
+ *                 per (sample, neuron) -- consumed by K6 (LIF) / K6r (ALIF). */
 int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR, int len, int t0,
                       int T, double alpha, double theta, double slope, double beta, double rho,
                       double kappa, int reset, int alif, int smooth, double* u, double* a,
                       double* zbar, double* zsum, uint32_t* raster, const float* wsig,
-                      const float* ctab, void* c_hi, void* c_lo, void* w_hi, void* w_lo, int ldc,
-                      float* mdt, float* psi_scratch, cudaStream_t stream);
+                      const float* ctab, void* c_hi, void* c_lo, void* w_hi, void* w_lo,
+                      void* wa_hi, void* wa_lo, int ldc, float* mdt, float* psi_scratch,
+                      cudaStream_t stream);
 
 /* K4  Presynaptic filter xbar_t = alpha*xbar_{t-1} + x_t (the factorised LIF trace G_u,
  *     gradients.py:89-94 with H_I = alpha, F rows = x_t; test_gradients.py:81-91).
@@ -136,6 +142,19 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
                          const float* mdt, float* eps, float* partial, int B, int n, int n_pad,
                          int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
                          int store_eps, cudaStream_t stream);
+
+/* K6r The ALIF trace PAIR (G_u, G_a) of reset=True carried across chunks on tcgen05
+ *     (elig_reset.cu): with (W_u, W_a), M, Dt from K1r and the raw input x (K4, alpha=0)
+ *       (E_u, E_a)_end = Dt (E_u, E_a)_0 + sum_rho (W_u, W_a)_rho x_rho   (if do_mma)
+ *       partial[z][i][j] = sum_{b in split z} (M_u E_u0 + M_a E_a0)[b,i,j]
+ *     eps_u / eps_a [B][n_pad][ke] fp32; coef [B][n][8]; layouts and padding as K6
+ *     (tiles of 128 neurons x 64 inputs).  Replaces the reset branch of the ALIF
+ *     eprop_trace_update (gradients.py:89-94, neurons.py:266-271). */
+int spb_reset_carry_chunk(const void* wu_hi, const void* wu_lo, const void* wa_hi,
+                          const void* wa_lo, int ldw, const void* xh, const float* coef,
+                          float* eps_u, float* eps_a, float* partial, int B, int n, int n_pad,
+                          int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
+                          int store_eps, cudaStream_t stream);
 
 /* grad[i][j] (+)= sum_{s<splits} partial[s][i][j] in fixed order (fp64); accumulate = 0
  * overwrites. */

@@ -25,13 +25,15 @@ SIGNATURES = {
     "spb_pack_spikes": [P, LL, I, I, I, I, I, I, P, P],
     "spb_input_proj": [P, P, P, I, I, I, I, I, P, I, P],
     "spb_forward_chunk": [I, P, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I, I,
-                          P, P, P, P, P, P, P, P, P, P, P, I, P, P, P],
+                          P, P, P, P, P, P, P, P, P, P, P, P, P, I, P, P, P],
     "spb_xbar_chunk": [P, LL, LL, I, I, I, I, I, I, D, P, P, P, P],
     "spb_readout_loss": [P, P, P, I, I, I, P, P, P, P, P, P],
     "spb_readout_grad": [P, P, I, I, I, P, P],
     "spb_grad_gemm_partials": [P, P, I, P, P, I, I, I, I, I, P, I, LL, P],
     "spb_grad_gemm_simt": [P, P, I, P, P, I, I, I, I, P, I, P],
     "spb_alif_carry_chunk": [P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I, I, P],
+    "spb_reset_carry_chunk": [P, P, P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I,
+                              I, P],
     "spb_reduce_partials": [P, I, I, I, I, I, P, P],
     "spb_finalize_grad": [P, I, I, I, P, I, P],
     "spb_copy_chunk_h2d": [P, LL, P, LL, LL, I, P],

@@ -223,6 +223,139 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
 }
 
 // ------------------------------------------------------------------------------------
+// K1r: backward scan of one chunk with reset=True (neurons.py:266-271: the soft reset makes
+// G_u per-synapse, h_uu = alpha - theta psi^-, and couples it to G_a, h_ua = theta beta
+// psi^-).  The trace g = (G_u, G_a) of one synapse obeys g_r = A_r g_{r-1} + e_u x_r with
+//   A_r = [[alpha - theta P_r, theta beta P_r], [P_r, rho - beta P_r]],  P_r = psi_{r-1}
+// (LIF: beta = rho = 0, only G_u lives), and step r adds q_r . g_r to the gradient with
+// q_r = Lpsi_r (1, -beta).  Backwards over the chunk:
+//   lambda_r = q_r + A_{r+1}^T lambda_{r+1}           -> C_{r+1} = lambda_r,u  (GEMM row of x_r)
+//   Phi_r    = A_{L-1} ... A_{r+1}                     -> W_{r+1} = Phi_r e_u   (carry rows)
+//   M = A_0^T lambda_0,  Dt = Phi_{-1}                  (boundary term M.E0, E_end = Dt E0 + D)
+// Row 0 (no x) is zero; the GEMM operand is the raw input (K4 with alpha = 0).  Outputs:
+// c (bf16 hi/lo), w_u = (w_hi, w_lo), ALIF also w_a = (wa_hi, wa_lo); coefficients: LIF
+// float2 (M_u, Dt_uu) in mdt, ALIF float[8] (M_u, M_a, Dt_uu, Dt_ua, Dt_au, Dt_aa, 0, 0).
+// ------------------------------------------------------------------------------------
+struct ResetLane {
+  float lu = 0.f, la = 0.f;                          // lambda_{r+1}
+  float nuu = 0.f, nua = 0.f, nau = 0.f, naa = 0.f;  // A_{r+1}
+  float puu = 1.f, pua = 0.f, pau = 0.f, paa = 1.f;  // Phi_r
+  __device__ __forceinline__ void step(float P, float lpsi, float alpha, float theta, float beta,
+                                       float rho, bool alif, float& cval, float& wu, float& wa) {
+    const float auu = fmaf(-theta, P, alpha);
+    const float aua = alif ? theta * beta * P : 0.f;
+    const float aau = alif ? P : 0.f;
+    const float aaa = alif ? fmaf(-beta, P, rho) : 0.f;
+    const float qa = alif ? -beta * lpsi : 0.f;
+    const float nlu = fmaf(nau, la, fmaf(nuu, lu, lpsi));
+    const float nla = fmaf(naa, la, fmaf(nua, lu, qa));
+    lu = nlu;
+    la = nla;
+    cval = lu;
+    wu = puu;
+    wa = pau;
+    const float quu = fmaf(pua, aau, puu * auu), qua = fmaf(pua, aaa, puu * aua);
+    const float qau = fmaf(paa, aau, pau * auu), qaa = fmaf(paa, aaa, pau * aua);
+    puu = quu; pua = qua; pau = qau; paa = qaa;
+    nuu = auu; nua = aua; nau = aau; naa = aaa;
+  }
+};
+
+__global__ void __launch_bounds__(K1S_THREADS) reset_scan_kernel(
+    FwdParams P, const float* __restrict__ wsig, const float* __restrict__ ctab,
+    uint32_t* __restrict__ c_hi, uint32_t* __restrict__ c_lo, uint32_t* __restrict__ w_hi,
+    uint32_t* __restrict__ w_lo, uint32_t* __restrict__ wa_hi, uint32_t* __restrict__ wa_lo,
+    int ldc, float* __restrict__ coef, const float* __restrict__ psis) {
+  extern __shared__ float cs[];  // cs[r] = c_{t0+r}, r = 0..L-1
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int L = P.len;
+  for (int r = threadIdx.x; r < L; r += K1S_THREADS) cs[r] = ctab[P.t0 + r];
+  __syncthreads();
+  const int i = blockIdx.x * 64 + 2 * lane;
+  const int b = blockIdx.y * (K1S_THREADS / 32) + warp;
+  if (b >= P.B || i >= P.n) return;
+  const bool has2 = i + 1 < P.n;
+  const bool alif = P.alif != 0;
+  const long long bi = (long long)b * P.n + i;
+  const float ws0 = wsig[bi], ws1 = has2 ? wsig[bi + 1] : 0.f;
+  const float alpha = (float)P.alpha, theta = (float)P.theta, beta = (float)P.beta,
+              rho = (float)P.rho;
+  const bool carry = w_hi != nullptr;
+  const float* prow = psis + (long long)b * (P.KR + 1) * P.n + i;
+  auto ldpsi = [&](int r) -> float2 {
+    if (r < 0) return make_float2(0.f, 0.f);
+    return has2 ? *reinterpret_cast<const float2*>(prow + (long long)r * P.n)
+                : make_float2(prow[(long long)r * P.n], 0.f);
+  };
+  const long long ld2 = ldc >> 1;
+  const long long base = (long long)b * P.KR * ld2 + (i >> 1);
+  uint32_t* chp = c_hi + base;
+  uint32_t* clp = c_lo + base;
+  for (int r = P.KR - 1; r > L; --r) {
+    chp[r * ld2] = 0u;
+    clp[r * ld2] = 0u;
+    if (carry) {
+      w_hi[base + r * ld2] = 0u;
+      w_lo[base + r * ld2] = 0u;
+      if (alif) { wa_hi[base + r * ld2] = 0u; wa_lo[base + r * ld2] = 0u; }
+    }
+  }
+  chp[0] = 0u;  // row 0 carries no input
+  clp[0] = 0u;
+  if (carry) {
+    w_hi[base] = 0u;
+    w_lo[base] = 0u;
+    if (alif) { wa_hi[base] = 0u; wa_lo[base] = 0u; }
+  }
+  ResetLane s0, s1;
+  // step r uses P_r = psi row r and Lpsi_r = c_r w_sig psi row r+1
+  float2 up = ldpsi(L);
+  float2 q0 = ldpsi(L - 1), q1 = ldpsi(L - 2), q2 = ldpsi(L - 3), q3 = ldpsi(L - 4);
+  for (int r = L - 1; r >= 0; --r) {
+    const float2 cur = q0;
+    q0 = q1;
+    q1 = q2;
+    q2 = q3;
+    q3 = ldpsi(r - 4);
+    const float cr = cs[r];
+    float c0, u0, a0, c1, u1, a1;
+    s0.step(cur.x, cr * ws0 * up.x, alpha, theta, beta, rho, alif, c0, u0, a0);
+    s1.step(cur.y, cr * ws1 * up.y, alpha, theta, beta, rho, alif, c1, u1, a1);
+    const long long o = (long long)(r + 1) * ld2;
+    uint32_t h, l;
+    split_bf16x2(c0, c1, h, l);
+    chp[o] = h;
+    clp[o] = l;
+    if (carry) {
+      split_bf16x2(u0, u1, h, l);
+      w_hi[base + o] = h;
+      w_lo[base + o] = l;
+      if (alif) {
+        split_bf16x2(a0, a1, h, l);
+        wa_hi[base + o] = h;
+        wa_lo[base + o] = l;
+      }
+    }
+    up = cur;
+  }
+  if (coef != nullptr) {
+    const ResetLane* sl[2] = {&s0, &s1};
+    for (int h = 0; h < (has2 ? 2 : 1); ++h) {
+      const ResetLane& s = *sl[h];
+      const float mu = fmaf(s.nau, s.la, s.nuu * s.lu);
+      const float ma = fmaf(s.naa, s.la, s.nua * s.lu);
+      if (alif) {
+        float4* cp = reinterpret_cast<float4*>(coef + (bi + h) * 8);
+        cp[0] = make_float4(mu, ma, s.puu, s.pua);
+        cp[1] = make_float4(s.pau, s.paa, 0.f, 0.f);
+      } else {
+        reinterpret_cast<float2*>(coef)[bi + h] = make_float2(mu, s.puu);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // K4: xbar chunk.  Thread per (sample, 2 neighbouring channels); fp64 recurrences; the
 // input bytes of 8 steps are loaded ahead of the dependent chain.  Writes the bf16 hi/lo
 // split MN-major (channels contiguous): xh/xl [B*KR][kp], row b*KR + rho, rho = 0 ->
@@ -286,8 +419,9 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
                       int T, double alpha, double theta, double slope, double beta, double rho,
                       double kappa, int reset, int alif, int smooth, double* u, double* a,
                       double* zbar, double* zsum, uint32_t* raster, const float* wsig,
-                      const float* ctab, void* c_hi, void* c_lo, void* w_hi, void* w_lo, int ldc,
-                      float* mdt, float* psi_scratch, cudaStream_t stream) {
+                      const float* ctab, void* c_hi, void* c_lo, void* w_hi, void* w_lo,
+                      void* wa_hi, void* wa_lo, int ldc, float* mdt, float* psi_scratch,
+                      cudaStream_t stream) {
   SPB_CHECK_ARG(pass >= 0 && pass <= 2,
                 "spb_forward_chunk: pass must be 0 (A), 1 (B) or 2 (B scan only)");
   SPB_CHECK_ARG(pass == 2 || (cur && u && a), "spb_forward_chunk: null pointer");
@@ -296,10 +430,13 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
   SPB_CHECK_ARG(pass == 0 ? (zbar && zsum) : (wsig && ctab && c_hi && c_lo && psi_scratch),
                 "spb_forward_chunk: missing pass-%c buffers", pass ? 'B' : 'A');
   SPB_CHECK_ARG(!(pass == 0 && psi_scratch && (u == nullptr)), "spb_forward_chunk: bad pass A");
-  SPB_CHECK_ARG(!(pass >= 1 && alif && (!mdt || (w_hi && !w_lo))),
+  SPB_CHECK_ARG(!(pass >= 1 && alif && !reset && (!mdt || (w_hi && !w_lo))),
                 "spb_forward_chunk: ALIF pass B needs mdt (and w_lo with w_hi)");
   SPB_CHECK_ARG(pass == 0 || (ldc >= n && ldc % 8 == 0), "spb_forward_chunk: ldc must be >= n, %% 8");
-  SPB_CHECK_ARG(!(pass >= 1 && reset), "spb_forward_chunk: reset=True has no two-pass form");
+  SPB_CHECK_ARG(!(pass >= 1 && reset && alif && w_hi && !(wa_hi && wa_lo)),
+                "spb_forward_chunk: ALIF reset carry needs wa_hi/wa_lo");
+  SPB_CHECK_ARG(!(pass >= 1 && reset && !mdt && w_hi),
+                "spb_forward_chunk: reset carry needs the coefficient buffer (mdt)");
   FwdParams P{B, n, Tc, KR, len, t0, T, alpha, theta, slope, beta, rho, kappa, reset, alif, pass,
               smooth};
   dim3 grid(ceil_div(n, 32), ceil_div(B, K1_THREADS / 32));
@@ -308,7 +445,15 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
                                                           psi_scratch);
     SPB_CHECK_LAUNCH("forward_chunk");
   }
-  if (pass >= 1) {
+  if (pass >= 1 && reset) {
+    dim3 sgrid(ceil_div(n, 64), ceil_div(B, K1S_THREADS / 32));
+    reset_scan_kernel<<<sgrid, K1S_THREADS, (len > 0 ? len : 1) * sizeof(float), stream>>>(
+        P, wsig, ctab, reinterpret_cast<uint32_t*>(c_hi), reinterpret_cast<uint32_t*>(c_lo),
+        reinterpret_cast<uint32_t*>(w_hi), reinterpret_cast<uint32_t*>(w_lo),
+        reinterpret_cast<uint32_t*>(wa_hi), reinterpret_cast<uint32_t*>(wa_lo), ldc, mdt,
+        psi_scratch);
+    SPB_CHECK_LAUNCH("reset_scan");
+  } else if (pass >= 1) {
     dim3 sgrid(ceil_div(n, 64), ceil_div(B, K1S_THREADS / 32));
     chunk_scan_kernel<<<sgrid, K1S_THREADS, (len + 1) * sizeof(float), stream>>>(
         P, wsig, ctab, reinterpret_cast<uint32_t*>(c_hi), reinterpret_cast<uint32_t*>(c_lo),

@@ -86,7 +86,8 @@ class EpropEngine:
     """Buffers + launch sequence for one problem shape on one device."""
 
     def __init__(self, n: int, k: int, m: int, B: int, *, alif: bool, w_f64: bool = False,
-                 chunk: int = 127, device=None, sm_count: int | None = None):
+                 chunk: int = 127, device=None, sm_count: int | None = None,
+                 reset: bool = False):
         if chunk not in CHUNKS:
             raise ValueError(f"chunk must be one of {CHUNKS} (Tc + 1 a multiple of 64)")
         self.lib = _lib.load()
@@ -94,6 +95,10 @@ class EpropEngine:
         if min(self.n, self.k, self.m, self.B) <= 0:
             raise ShapeMismatch("n, k, m and B must be positive")
         self.alif = bool(alif)
+        # carried per-synapse traces: ALIF G_a (reset=False); LIF G_u (reset=True, the soft
+        # reset makes G_u non-factorisable); ALIF (G_u, G_a) pair (reset=True)
+        self.reset = bool(reset)
+        self.ntr = (2 if self.reset else 1) if self.alif else (1 if self.reset else 0)
         self.w_f64 = bool(w_f64)
         self.Tc = int(chunk)
         self.KR = self.Tc + 1
@@ -140,12 +145,20 @@ class EpropEngine:
         # split-K (K5) and sample-split (K6) partial slices, reduced in fixed order
         tiles5 = (self.kp // 128) * math.ceil(n / 128)
         self.splits5 = max(1, min(K // 64, round(sms / tiles5)))
-        if self.alif:
+        self.wa_hi = self.wa_lo = self.eps2 = None
+        if self.ntr:
             self.w_hi = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
             self.w_lo = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
-            self.mdt = torch.empty((B, n, 2), dtype=f32, device=dev)
+            # chunk coefficients: (M, Dt) per (sample, neuron); the reset pair needs
+            # (M_u, M_a, Dt 2x2) padded to 8 floats
+            self.mdt = torch.empty((B, n, 2 if self.ntr == 1 else 8), dtype=f32, device=dev)
             self.eps = torch.zeros((B, self.n_pad, self.ke), dtype=f32, device=dev)
-            tiles6 = (self.kp // 128) * (self.n_pad // 128)
+            if self.ntr == 2:
+                self.wa_hi = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
+                self.wa_lo = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
+                self.eps2 = torch.zeros((B, self.n_pad, self.ke), dtype=f32, device=dev)
+            bn6 = 128 if self.ntr == 1 else 64
+            tiles6 = (self.kp // bn6) * (self.n_pad // 128)
             self.splits6 = _wave_split(tiles6, B, sms)
         else:
             self.w_hi = self.w_lo = self.mdt = self.eps = None
@@ -241,9 +254,8 @@ class EpropEngine:
         Results stay on device: ``grad_w_acc`` (fp64 [n, kp]), ``grad_wout``, ``loss``,
         ``s`` (readout sums), ``correct``.
         """
-        if reset:
-            raise NotImplementedError(
-                "reset=True makes G_u non-factorisable (SURVEY.md 8(f)-3); not on the B200 path yet")
+        if bool(reset) != self.reset:
+            raise ValueError(f"engine built for reset={self.reset}, called with reset={reset}")
         kb = (self.k + 7) // 8 if bits else self.k
         if x.dtype != torch.uint8 or x.dim() != 3 or x.shape[0] != self.B or x.shape[2] != kb:
             raise ShapeMismatch(f"x must be uint8 [B={self.B}, T, {kb}] "
@@ -265,9 +277,12 @@ class EpropEngine:
         strideb = T * kb
         self.launches = 0
         v = ctypes_void
-        common = (float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa), 0,
-                  int(self.alif), int(bool(smooth)))
+        common = (float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa),
+                  int(self.reset), int(self.alif), int(bool(smooth)))
         xq_sb, xq_st = Tc * self.Kpad, self.Kpad          # K4 reads the packed operand
+        # K5/K6 operand: the filtered input xbar (reset=False: G_u = 1 (x) xbar), or with
+        # reset=True the raw input (G_u is carried per synapse; K4 with alpha = 0 = copy)
+        x_alpha = 0.0 if self.reset else float(alpha)
 
         def timed(name, meta, fn, *args):
             if timers is None:
@@ -333,7 +348,7 @@ class EpropEngine:
                 self._ev["xbar"].record(main)
                 self.side.wait_event(self._ev["xbar"])
                 call("spb_xbar_chunk", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
-                     ln, 1, float(alpha), v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()),
+                     ln, 1, x_alpha, v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()),
                      v(self.xl.data_ptr()), sst)
                 self._ev["xbar"].record(self.side)
                 self.launches += 1
@@ -343,7 +358,7 @@ class EpropEngine:
                   *common, v(self.u.data_ptr()), v(self.a.data_ptr()),
                   v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
                   v(raster.data_ptr()) if raster is not None else None,
-                  None, None, None, None, None, None, 0, None,
+                  None, None, None, None, None, None, None, None, 0, None,
                   v(self.psi.data_ptr()) if (one and not forward_only) else None, st)
             self.launches += 3
         # ---------------- readout / loss ----------------
@@ -372,7 +387,7 @@ class EpropEngine:
                 pack_chunk(c, ln)
                 self._project(ln, st, timed)
                 self.launches += 2
-            carry_out = self.alif and not last   # the trace is only needed by a later chunk
+            carry_out = bool(self.ntr) and not last   # only a later chunk needs the trace
             # one chunk: pass A already parked psi -> backward scan only (pass 2)
             pid = 2 if one else 1
             timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,
@@ -381,14 +396,16 @@ class EpropEngine:
                   None, v(self.wsig.data_ptr()), v(ctab.data_ptr()),
                   v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()),
                   v(self.w_hi.data_ptr()) if carry_out else None,
-                  v(self.w_lo.data_ptr()) if carry_out else None, self.ldc,
-                  v(self.mdt.data_ptr()) if self.alif else None, v(self.psi.data_ptr()), st)
+                  v(self.w_lo.data_ptr()) if carry_out else None,
+                  v(self.wa_hi.data_ptr()) if carry_out and self.ntr == 2 else None,
+                  v(self.wa_lo.data_ptr()) if carry_out and self.ntr == 2 else None, self.ldc,
+                  v(self.mdt.data_ptr()) if self.ntr else None, v(self.psi.data_ptr()), st)
             self.launches += 1 if one else 2
             if one and use_side:
                 main.wait_event(self._ev["xbar"])
             else:
                 call("spb_xbar_chunk", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
-                     ln, int(c == 0), float(alpha), v(self.xbar_state.data_ptr()),
+                     ln, int(c == 0 or self.reset), x_alpha, v(self.xbar_state.data_ptr()),
                      v(self.xh.data_ptr()), v(self.xl.data_ptr()), st)
                 self.launches += 1
             timed("gemm", ln, "spb_grad_gemm_partials", v(self.c_hi.data_ptr()),
@@ -397,13 +414,23 @@ class EpropEngine:
                   slice_stride, st)
             self.launches += 1
             slices = self.splits5
-            if self.alif and (c > 0 or not last):
+            if self.ntr and (c > 0 or not last):
                 # first chunk: E0 = 0 (nothing to add, only carry); last chunk: no carry
-                timed("carry", (ln, c > 0, not last), "spb_alif_carry_chunk",
-                      v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()), self.ldc,
-                      v(self.xh.data_ptr()), v(self.xl.data_ptr()), v(self.mdt.data_ptr()),
-                      v(self.eps.data_ptr()), v(part6), B, n, self.n_pad, k, self.ke, self.kp,
-                      KR, self.splits6, int(not last), int(c > 0), int(not last), st)
+                if self.ntr == 1:
+                    timed("carry", (ln, c > 0, not last), "spb_alif_carry_chunk",
+                          v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()), self.ldc,
+                          v(self.xh.data_ptr()), v(self.xl.data_ptr()), v(self.mdt.data_ptr()),
+                          v(self.eps.data_ptr()), v(part6), B, n, self.n_pad, k, self.ke,
+                          self.kp, KR, self.splits6, int(not last), int(c > 0), int(not last),
+                          st)
+                else:
+                    timed("carry", (ln, c > 0, not last), "spb_reset_carry_chunk",
+                          v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()),
+                          v(self.wa_hi.data_ptr()), v(self.wa_lo.data_ptr()), self.ldc,
+                          v(self.xh.data_ptr()), v(self.mdt.data_ptr()), v(self.eps.data_ptr()),
+                          v(self.eps2.data_ptr()), v(part6), B, n, self.n_pad, k, self.ke,
+                          self.kp, KR, self.splits6, int(not last), int(c > 0), int(not last),
+                          st)
                 self.launches += 1
                 if c > 0:
                     slices += self.splits6

@@ -82,11 +82,12 @@ def get_engine(net: Network, B: int, *, chunk: int | None = None, T: int | None 
     if chunk is None:
         chunk = default_chunk(T or 127)
     w_f64 = net.neuron.w.dtype == np.float64
-    key = (net.n, net.k, net.m, B, net.is_alif, w_f64, chunk, str(dev))
+    reset = bool(net.neuron.reset)
+    key = (net.n, net.k, net.m, B, net.is_alif, w_f64, chunk, str(dev), reset)
     eng = _ENGINES.get(key)
     if eng is None:
         eng = EpropEngine(net.n, net.k, net.m, B, alif=net.is_alif, w_f64=w_f64, chunk=chunk,
-                          device=dev)
+                          device=dev, reset=reset)
         _ENGINES[key] = eng
     return eng
 

@@ -191,7 +191,7 @@ class DeviceTrainer:
         if eng is None:
             net = self.net
             eng = EpropEngine(net.n, net.k, net.m, B, alif=net.is_alif, w_f64=self.is_f64,
-                              chunk=self.chunk, device=self.device)
+                              chunk=self.chunk, device=self.device, reset=net.neuron.reset)
             self._engines[B] = eng
         # every engine shares the trainer's parameters: point its W at the master
         # copy and refresh its fp64 W_out mirror + INT8 digits when they changed
@@ -313,7 +313,7 @@ def evaluate(net: Network, dataset, *, batch_size: int = 256, device=None):
         if eng is None:
             eng = EpropEngine(net.n, net.k, net.m, B, alif=net.is_alif,
                               w_f64=net.neuron.w.dtype == np.float64,
-                              chunk=default_chunk(T), device=dev)
+                              chunk=default_chunk(T), device=dev, reset=net.neuron.reset)
             eng.set_weights(w, wo)
             engines[B] = eng
         eng.run(xs[s0:s0 + B], ld[s0:s0 + B], bits=bits, forward_only=True, **kw)

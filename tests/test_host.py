@@ -64,7 +64,7 @@ def test_bad_arguments_are_rejected_without_gpu():
     # argument validation happens before any CUDA call -> works on a CPU-only host
     with pytest.raises(P.ShapeMismatch):
         _lib.call("spb_forward_chunk", 2, None, 1, 1, 63, 64, 1, 0, 1,
-                  0.95, 1.0, 10.0, 0.0, 0.0, 0.95, 0, 0, 0, None, None, None, None, None, None,
+                  0.95, 1.0, 10.0, 0.0, 0.0, 0.95, 0, 0, 0, None, None, None, None, None, None, None, None,
                   None, None, None, None, None, 8, None, None, None)
     with pytest.raises(P.ShapeMismatch):
         _lib.call("spb_input_proj", None, None, None, 1, 1, 32, 100, 7, None, 148, None)
@@ -130,6 +130,28 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     assert eng.launches == len(rec.calls) + passb
 
 
+@pytest.mark.parametrize("alif", [False, True])
+def test_engine_reset_dry_run(monkeypatch, alif):
+    """reset=True: raw-input operand (K4 alpha = 0, fresh every chunk), the reset scan
+    and one (LIF: G_u) or two (ALIF: G_u, G_a) carried traces."""
+    rec = _Recorder()
+    monkeypatch.setattr(_lib, "call", rec)
+    eng = EpropEngine(40, 30, 3, 6, alif=alif, chunk=63, device="cpu", sm_count=148, reset=True)
+    x = torch.zeros((6, 200, 30), dtype=torch.uint8)
+    with pytest.raises(ValueError):
+        eng.run(x, torch.zeros(6, dtype=torch.int64), reset=False)
+    eng.run(x, torch.zeros(6, dtype=torch.int64), reset=True)
+    xb = [c[1] for c in rec.calls if c[0] == "spb_xbar_chunk"]
+    assert xb and all(a[8] == 1 and a[9] == 0.0 for a in xb)      # fresh, alpha = 0
+    fw = [c[1] for c in rec.calls if c[0] == "spb_forward_chunk"]
+    assert all(a[15] == 1 for a in fw)                              # reset flag
+    carry = "spb_reset_carry_chunk" if alif else "spb_alif_carry_chunk"
+    other = "spb_alif_carry_chunk" if alif else "spb_reset_carry_chunk"
+    names = [c[0] for c in rec.calls]
+    assert names.count(carry) == 4 and names.count(other) == 0     # 4 chunks
+    assert eng.mdt.shape[-1] == (8 if alif else 2)
+
+
 def test_engine_forward_only_dry_run(monkeypatch):
     rec = _Recorder()
     monkeypatch.setattr(_lib, "call", rec)
@@ -152,7 +174,7 @@ def test_engine_rejects_bad_inputs():
         eng.run(torch.zeros((3, 10, 4), dtype=torch.uint8), torch.zeros(3, dtype=torch.int64))
     with pytest.raises(P.ShapeMismatch):
         eng.run(torch.zeros((3, 10, 5), dtype=torch.float32), torch.zeros(3, dtype=torch.int64))
-    with pytest.raises(NotImplementedError):
+    with pytest.raises(ValueError):
         eng.run(torch.zeros((3, 10, 5), dtype=torch.uint8), torch.zeros(3, dtype=torch.int64),
                 reset=True)
     with pytest.raises(ValueError):
