@@ -66,6 +66,7 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+INT8_KERNELS = ("proj", "fused_a", "fused_b")
 FP32_PEAK_TFLOPS = 72.5  # FFMA/FFMA2 microbenchmark on this pool's B200 (tools/fp_microbench.cu)
 
 
@@ -321,6 +322,14 @@ def main():
                 ln = meta                                        # int8 MACs x2, useful part
                 flops += 2.0 * P_sl * B * ln * n * k
                 byts += B * ln * k + P_sl * n * k + 8.0 * B * ln * n
+            elif name in ("fused_a", "fused_b"):
+                ln, pid, parked = meta                           # K21: projection + dynamics
+                flops += 2.0 * P_sl * B * ln * n * k
+                byts += B * ln * k + P_sl * n * k + 16.0 * B * n * 2   # spikes, digits, state
+                if parked:
+                    byts += 4.0 * B * (ln + 1) * n                     # psi for the scan
+                if pid == 0:
+                    byts += B * ln * n / 8.0 + 16.0 * B * n           # raster, zbar/zsum
             elif name in ("forward", "forward_a"):
                 ln, pid, flag = meta
                 psi = 4.0 * B * (ln + 1) * n
@@ -346,7 +355,7 @@ def main():
             ent["hbm_gbs"] = byts / t_tot / 1e9
             ent["hbm_frac"] = ent["hbm_gbs"] / hbm_peak
         if flops:
-            pk = 2 * bf16_peak if name == "proj" else bf16_peak
+            pk = 2 * bf16_peak if name in INT8_KERNELS else bf16_peak
             ent["tensor_tflops"] = flops / t_tot / 1e12
             ent["tensor_frac"] = ent["tensor_tflops"] / pk
         kernels[name] = ent
@@ -355,17 +364,19 @@ def main():
         dom = max(kernels, key=lambda nm: kernels[nm]["ms_per_step"])
         e = kernels[dom]
         names = {"proj": "input_proj_kernel (K2, int8 tcgen05)", "forward": "forward_chunk + chunk_scan (K1 pass B)",
+                 "fused_a": "fused_forward_kernel (K21 pass A: int8 tcgen05 projection + fp64 dynamics)",
+                 "fused_b": "fused_forward_kernel (K21 pass B: projection + dynamics, psi)",
                  "forward_a": "forward_chunk_kernel (K1 pass A)",
                  "gemm": "grad_gemm_tc_kernel (K5, bf16x3 tcgen05)",
                  "carry": "alif_carry_kernel (K6, tcgen05 + eps stream)"}
         if e.get("tensor_frac", 0) >= e.get("hbm_frac", 0) and "tensor_tflops" in e:
-            pk = 2 * bf16_peak if dom == "proj" else bf16_peak
+            pk = 2 * bf16_peak if dom in INT8_KERNELS else bf16_peak
             roof = {"kernel": names[dom], "bound": "tensor", "achieved": e["tensor_tflops"],
                     "peak": pk, "unit": "TFLOP/s", "frac": e["tensor_frac"]}
         else:
             roof = {"kernel": names[dom], "bound": "hbm", "achieved": e["hbm_gbs"],
                     "peak": hbm_peak, "unit": "GB/s", "frac": e["hbm_frac"]}
-        roof.update({"peak_source": peak_kind + (" (int8 = 2x bf16)" if dom == "proj" else ""),
+        roof.update({"peak_source": peak_kind + (" (int8 = 2x bf16)" if dom in INT8_KERNELS else ""),
                      "traffic": None, "kernel_ms_per_step": e["ms_per_step"],
                      "share_of_step": e["share_of_step"]})
 
@@ -391,6 +402,7 @@ def main():
                        "global_batch": B * world, "seq_len": T, "n_hidden": n, "n_inputs": k,
                        "n_classes": m, "chunk": eng.Tc, "parallelism": f"dp{world}",
                        "forward_precision": "fp64 state/current (bit-exact spikes)",
+                       "forward_kernel": "K21 fused projection+dynamics" if eng.fused else "K2 projection + K1 dynamics",
                        "l2": "512 MiB flush between timed steps (outside events)"},
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,

@@ -45,15 +45,41 @@ int spb_device_sm(void); /* compute capability of the current device, e.g. 100 *
  *                      sexp [n] int32 (n_pad32 = round_up(n,32), Kpad = round_up(k,128)).
  *   spb_pack_spikes:   x row (b, s < len) at x + b*stride_b + s*kb -> xq [B*Tc][Kpad] uint8,
  *                      zero padded; bits = 0: kb = k bytes (counts), bits = 1: kb = ceil(k/8)
- *                      bytes, channel j = bit (j & 7) of byte j >> 3 (packbits, little). 
+ *                      bytes, channel j = bit (j & 7) of byte j >> 3 (packbits, little);
+ *                      output row b*Tc + s, or s*B + b with time_major != 0 (K21). 
  *   spb_input_proj:    cur[row][i] = sum_j xq[row][j] W[i][j] for row < M (= B*Tc), fp64;
  *                      persistent grid of min(tiles, sm_count) CTAs. */
 int spb_slice_weights(const void* w, int w_is_f64, int n, int k, int Kpad, int n_pad32, int P,
                       int8_t* wq, int* sexp, cudaStream_t stream);
 int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits, int len, int Tc,
-                    int Kpad, uint8_t* xq, cudaStream_t stream);
+                    int Kpad, int time_major, uint8_t* xq, cudaStream_t stream);
 int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
                    int Kpad, int P, double* cur, int sm_count, cudaStream_t stream);
+
+/* K21 Fused exact projection + neuron dynamics (fused.cu): the K2 tensor-core sums of a
+ *     (128-sample block, 16-neuron tile) at one step land in TMEM and the epilogue thread
+ *     that owns the sample integrates K1's dynamics in registers, step after step; the
+ *     fp64 current never reaches HBM.  Same arithmetic as K2 + K1 (identical spikes).
+ *     xq: TIME-MAJOR operand [Tc*B][Kpad] (spb_pack_spikes time_major=1), Kpad <= 768;
+ *     wq/sexp from spb_slice_weights.  pass 0 (A): zbar, zsum, raster (uint8 view of the
+ *     [B][T][ceil(n/32)] uint32 raster, optional, must be ZERO-initialised: bits are
+ *     OR-ed in), psi optional; pass 1 (B): psi required
+ *     (then spb_forward_chunk pass 2 runs the scan).  State u, a as K1. */
+int spb_fused_forward(int pass, const uint8_t* xq, const int8_t* wq, const int* sexp, int B,
+                      int n, int n_pad32, int Kpad, int P, int Tc, int KR, int len, int t0, int T,
+                      double alpha, double theta, double slope, double beta, double rho,
+                      double kappa, int reset, int smooth, double* u, double* a, double* zbar,
+                      double* zsum, uint8_t* raster, float* psi_scratch, int sm_count,
+                      cudaStream_t stream);
+
+/* Profiling variant of spb_fused_forward: probe bit 0 skips the dynamics (MMA + TMEM
+ * reads only), bit 1 skips the psi stores; probe = 0 is the production kernel. */
+int spb_fused_forward_probe(int pass, const uint8_t* xq, const int8_t* wq, const int* sexp, int B,
+                            int n, int n_pad32, int Kpad, int P, int Tc, int KR, int len, int t0,
+                            int T, double alpha, double theta, double slope, double beta,
+                            double rho, double kappa, int reset, int smooth, double* u, double* a,
+                            double* zbar, double* zsum, uint8_t* raster, float* psi_scratch,
+                            int sm_count, int probe, cudaStream_t stream);
 
 /* K1  Neuron dynamics over one time chunk from the exact current cur [B*Tc][n] (row
  *     b*Tc+s): ALIF/LIF state update, spike and surrogate derivative.

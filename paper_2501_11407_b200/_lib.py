@@ -22,7 +22,11 @@ D = ctypes.c_double
 # name -> argtypes (every function returns int status)
 SIGNATURES = {
     "spb_slice_weights": [P, I, I, I, I, I, I, P, P, P],
-    "spb_pack_spikes": [P, LL, I, I, I, I, I, I, P, P],
+    "spb_pack_spikes": [P, LL, I, I, I, I, I, I, I, P, P],
+    "spb_fused_forward_probe": [I, P, P, P, I, I, I, I, I, I, I, I, I, I, D, D, D, D, D, D, I,
+                                I, P, P, P, P, P, P, I, I, P],
+    "spb_fused_forward": [I, P, P, P, I, I, I, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I,
+                          P, P, P, P, P, P, I, P],
     "spb_input_proj": [P, P, P, I, I, I, I, I, P, I, P],
     "spb_forward_chunk": [I, P, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I, I,
                           P, P, P, P, P, P, P, P, P, P, P, P, P, I, P, P, P],

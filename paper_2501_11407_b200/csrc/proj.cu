@@ -420,7 +420,7 @@ __device__ __forceinline__ uint32_t expand4(uint32_t nib) {  // 4 bits -> 4 byte
 }
 
 __global__ void pack_spikes_kernel(const uint8_t* __restrict__ x, long long stride_b, int k,
-                                   int bits, int len, int Tc, int Kpad, int B,
+                                   int bits, int len, int Tc, int Kpad, int B, int tmajor,
                                    uint8_t* __restrict__ xq) {
   const int lane = threadIdx.x & 31;
   const long long rows = (long long)B * Tc;
@@ -429,8 +429,9 @@ __global__ void pack_spikes_kernel(const uint8_t* __restrict__ x, long long stri
                   (reinterpret_cast<uintptr_t>(x) & 3) == 0;
   for (long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
        row += (long long)gridDim.x * (blockDim.x >> 5)) {
-    const int s = (int)(row % Tc);
-    const int b = (int)(row / Tc);
+    // sample-major rows b*Tc + s (K2) or time-major rows s*B + b (fused K21)
+    const int s = tmajor ? (int)(row / B) : (int)(row % Tc);
+    const int b = tmajor ? (int)(row % B) : (int)(row / Tc);
     const uint8_t* src = x + (long long)b * stride_b + (long long)s * kb;
     uint4* dst = reinterpret_cast<uint4*>(xq + row * Kpad);
     const bool live = s < len;
@@ -492,7 +493,7 @@ using namespace spb;
 extern "C" {
 
 int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits, int len, int Tc,
-                    int Kpad, uint8_t* xq, cudaStream_t stream) {
+                    int Kpad, int time_major, uint8_t* xq, cudaStream_t stream) {
   SPB_CHECK_ARG(x && xq && B > 0 && k > 0 && Kpad >= k && Kpad % proj::BK == 0 && len >= 0 &&
                     len <= Tc,
                 "spb_pack_spikes: bad args (Kpad must be a multiple of %d)", proj::BK);
@@ -500,7 +501,7 @@ int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits
   const long long want = (rows + 7) / 8;
   const int blocks = (int)(want < 148LL * 16 ? want : 148LL * 16);
   proj::pack_spikes_kernel<<<blocks, 256, 0, stream>>>(x, stride_b, k, bits, len, Tc, Kpad, B,
-                                                        xq);
+                                                        time_major, xq);
   SPB_CHECK_LAUNCH("pack_spikes");
   return 0;
 }

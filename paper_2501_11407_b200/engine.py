@@ -87,7 +87,7 @@ class EpropEngine:
 
     def __init__(self, n: int, k: int, m: int, B: int, *, alif: bool, w_f64: bool = False,
                  chunk: int = 127, device=None, sm_count: int | None = None,
-                 reset: bool = False):
+                 reset: bool = False, fused: bool | None = None):
         if chunk not in CHUNKS:
             raise ValueError(f"chunk must be one of {CHUNKS} (Tc + 1 a multiple of 64)")
         self.lib = _lib.load()
@@ -119,8 +119,19 @@ class EpropEngine:
         self.Kpad = _round_up(k, 128)
         self.n_pad32 = _round_up(n, 32)
         self.P = 8 if self.w_f64 else 7
+        # K21 (fused.cu) = K2 + K1 in one kernel: the fp64 current never leaves the SM
+        # (needs Kpad <= 768).  Opt-in: measured on B200 it is bitwise identical to K2 + K1
+        # but not faster at C3/C4 (its N = 112 MMAs keep the tensor pipe ~26 % busy and the
+        # per-step epilogue sits on the critical path), so K2 then K1 is the default.
+        fusable = self.Kpad <= 768
+        if fused is None:
+            fused = False
+        if fused and not fusable:
+            raise ValueError("the fused projection needs k <= 768")
+        self.fused = bool(fused)
         self.xq = torch.zeros((B * self.Tc, self.Kpad), dtype=torch.uint8, device=dev)
-        self.cur = torch.empty((B * self.Tc, n), dtype=f64, device=dev)
+        self.cur = (None if self.fused else
+                    torch.empty((B * self.Tc, n), dtype=f64, device=dev))
         self.wq = torch.zeros((self.P, self.n_pad32, self.Kpad), dtype=torch.int8, device=dev)
         self.sexp = torch.zeros(n, dtype=torch.int32, device=dev)
         # neuron state (fp64) and readout filters
@@ -214,10 +225,24 @@ class EpropEngine:
         return self.ctab
 
     def _pack(self, xp, strideb, bits, ln, st):
-        """Chunk spikes (bytes or bits) -> zero-padded K2 operand xq [B*Tc][Kpad] (also K4's
-        row source)."""
+        """Chunk spikes (bytes or bits) -> zero-padded projection operand xq [B*Tc][Kpad]
+        (rows b*Tc + s for K2, time-major s*B + b for K21; also K4's row source)."""
         _lib.call("spb_pack_spikes", ctypes_void(xp), strideb, self.B, self.k, int(bits), ln,
-                  self.Tc, self.Kpad, ctypes_void(self.xq.data_ptr()), st)
+                  self.Tc, self.Kpad, int(self.fused), ctypes_void(self.xq.data_ptr()), st)
+
+    def _fused(self, pass_id, ln, t0, T, common, raster, psi, st, timed, meta):
+        """K21: exact INT8 projection + dynamics in one kernel (pass 0: raster, zsum and
+        optionally psi; pass 1: psi for the backward scan)."""
+        v = ctypes_void
+        alpha, theta, slope, beta, rho, kappa, reset, _alif, smooth = common
+        timed("fused_a" if pass_id == 0 else "fused_b", meta, "spb_fused_forward", pass_id,
+              v(self.xq.data_ptr()), v(self.wq.data_ptr()), v(self.sexp.data_ptr()), self.B,
+              self.n, self.n_pad32, self.Kpad, self.P, self.Tc, self.KR, ln, t0, T, alpha,
+              theta, slope, beta, rho, kappa, reset, smooth, v(self.u.data_ptr()),
+              v(self.a.data_ptr()), v(self.zbar.data_ptr()) if pass_id == 0 else None,
+              v(self.zsum.data_ptr()) if pass_id == 0 else None,
+              v(raster.data_ptr()) if raster is not None else None,
+              v(psi.data_ptr()) if psi is not None else None, self.sm_count, st)
 
     def _project(self, ln, st, timed=None):
         """K2: cur = W x_t exactly on INT8 tensor cores from the packed chunk."""
@@ -279,7 +304,8 @@ class EpropEngine:
         v = ctypes_void
         common = (float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa),
                   int(self.reset), int(self.alif), int(bool(smooth)))
-        xq_sb, xq_st = Tc * self.Kpad, self.Kpad          # K4 reads the packed operand
+        # K4 reads the packed operand (sample-major for K2, time-major for K21)
+        xq_sb, xq_st = ((self.Kpad, B * self.Kpad) if self.fused else (Tc * self.Kpad, self.Kpad))
         # K5/K6 operand: the filtered input xbar (reset=False: G_u = 1 (x) xbar), or with
         # reset=True the raw input (G_u is carried per synapse; K4 with alpha = 0 = copy)
         x_alpha = 0.0 if self.reset else float(alpha)
@@ -339,6 +365,8 @@ class EpropEngine:
             def pack_chunk(c, ln):
                 self._pack(x.data_ptr() + c * Tc * kb, strideb, bits, ln, st)
 
+        if raster is not None and self.fused:
+            raster.zero_()  # K21 ORs the spike bits into the words
         # ---------------- pass A ----------------
         for c in range(nchunks):  # chunk 0 starts from fresh state inside the kernels
             t0 = c * Tc
@@ -352,6 +380,12 @@ class EpropEngine:
                      v(self.xl.data_ptr()), sst)
                 self._ev["xbar"].record(self.side)
                 self.launches += 1
+            if self.fused:
+                self._fused(0, ln, t0, T, common, raster,
+                            self.psi if (one and not forward_only) else None, st, timed,
+                            (ln, 0, one and not forward_only))
+                self.launches += 2
+                continue
             self._project(ln, st, timed)
             timed("forward_a", (ln, 0, one), "spb_forward_chunk", 0,
                   v(self.cur.data_ptr()), B, n, Tc, KR, ln, t0, T,
@@ -383,15 +417,19 @@ class EpropEngine:
             t0 = c * Tc
             ln = min(Tc, T - t0)
             last = c == nchunks - 1
+            carry_out = bool(self.ntr) and not last   # only a later chunk needs the trace
             if not one:  # one chunk: xq and cur of pass A are still valid (same W, same x)
                 pack_chunk(c, ln)
-                self._project(ln, st, timed)
+                if self.fused:
+                    self._fused(1, ln, t0, T, common, None, self.psi, st, timed,
+                                (ln, 1, carry_out))
+                else:
+                    self._project(ln, st, timed)
                 self.launches += 2
-            carry_out = bool(self.ntr) and not last   # only a later chunk needs the trace
-            # one chunk: pass A already parked psi -> backward scan only (pass 2)
-            pid = 2 if one else 1
+            # one chunk (pass A parked psi) or K21 (parks psi itself): backward scan only
+            pid = 2 if (one or self.fused) else 1
             timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,
-                  v(self.cur.data_ptr()), B, n, Tc, KR,
+                  v(self.cur.data_ptr()) if self.cur is not None else None, B, n, Tc, KR,
                   ln, t0, T, *common, v(self.u.data_ptr()), v(self.a.data_ptr()), None, None,
                   None, v(self.wsig.data_ptr()), v(ctab.data_ptr()),
                   v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()),
@@ -400,7 +438,7 @@ class EpropEngine:
                   v(self.wa_hi.data_ptr()) if carry_out and self.ntr == 2 else None,
                   v(self.wa_lo.data_ptr()) if carry_out and self.ntr == 2 else None, self.ldc,
                   v(self.mdt.data_ptr()) if self.ntr else None, v(self.psi.data_ptr()), st)
-            self.launches += 1 if one else 2
+            self.launches += 1 if pid == 2 else 2
             if one and use_side:
                 main.wait_event(self._ev["xbar"])
             else:

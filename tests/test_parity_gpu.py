@@ -246,7 +246,7 @@ def test_int8_tensor_core_projection_is_exact(w_f64):
     w = w.astype(np.float64 if w_f64 else np.float32)
     x = (rng.random((B, T, k)) < 0.1).astype(np.uint8)
     x[0, 0, :10] = 7                       # pooled counts
-    eng = EpropEngine(n, k, 3, B, alif=False, w_f64=w_f64, chunk=63)
+    eng = EpropEngine(n, k, 3, B, alif=False, w_f64=w_f64, chunk=63, fused=False)
     eng.set_weights(torch.from_numpy(w), torch.zeros((3, n), dtype=torch.float64))
     xd = torch.from_numpy(x).cuda()
     v = ctypes.c_void_p

@@ -1,18 +1,34 @@
-"""Top SASS instructions by warp-stall samples from an ncu report (source page)."""
-import csv, io, subprocess, sys
+"""Top SASS instructions of an ncu report (source page): by warp-stall samples and by
+executed instructions; plus the opcode mix of the executed instructions."""
+import collections, csv, io, subprocess, sys
+
 
 def main(path, top=25):
     raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr = rows[1]
-    data = [r for r in rows[2:] if len(r) == len(hdr)]
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "Address"][0]
+    hdr = rows[hi]
+    data = [r for r in rows[hi + 1:] if len(r) == len(hdr)]
     si = hdr.index("Warp Stall Sampling (All Samples)")
-    tot = sum(float(r[si]) for r in data) or 1.0
-    data.sort(key=lambda r: -float(r[si]))
-    print(f"{path}: {int(tot)} samples")
-    for r in data[:top]:
-        print(f"{100*float(r[si])/tot:5.1f}%  {r[0][-5:]}  {r[1].strip()[:90]}")
+    ei = hdr.index("Instructions Executed")
+    val = lambda r, i: float(r[i]) if r[i] not in ("", "-") else 0.0
+    tot = sum(val(r, si) for r in data) or 1.0
+    etot = sum(val(r, ei) for r in data) or 1.0
+    print(f"{path}: {int(tot)} stall samples, {int(etot)} warp instructions")
+    for r in sorted(data, key=lambda r: -val(r, si))[:top]:
+        print(f"{100*val(r, si)/tot:5.1f}%  {r[0][-5:]}  {r[1].strip()[:90]}")
+    mix = collections.Counter()
+    for r in data:
+        op = r[1].strip().split()
+        if not op:
+            continue
+        o = op[1] if op[0].startswith("@") and len(op) > 1 else op[0]
+        mix[o.split(".")[0]] += val(r, ei)
+    print("opcode mix (executed):")
+    for o, c in mix.most_common(20):
+        print(f"  {o:12s} {100*c/etot:5.1f}%")
+
 
 if __name__ == "__main__":
     main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)
