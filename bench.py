@@ -196,7 +196,7 @@ def main():
     net = P.init_network(spec)
     x_np, y_np = poisson_batch(B, k, T, m, seed=1000 + rank)
     from paper_2501_11407_b200.engine import default_chunk
-    chunk = args.chunk or default_chunk(T)
+    chunk = args.chunk or default_chunk(T, B, n, k, kind == "alif")
     eng = EpropEngine(n, k, m, B, alif=kind == "alif", w_f64=False, chunk=chunk, device=dev)
     eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
     xd = torch.from_numpy(x_np).to(dev)

@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int a = lb & 1;
       const int eb = lb & 1;
       const float2 md = vi ? mdt[(long long)b * n + i] : make_float2(0.f, 0.f);
-      const uint8_t* erow = esm + eb * ETILE + cg * (ETILE / 4) + r * 128;
+      const uint32_t erow = smem_u32(esm + eb * ETILE + cg * (ETILE / 4) + r * 128);
       if (load_eps) mbar_wait(smem_u32(&efull[eb]), (lb >> 1) & 1);
       if (do_mma) {
         mbar_wait(smem_u32(&tfull[a]), (lb >> 1) & 1);
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int v4 = hf * 4; v4 < hf * 4 + 4; ++v4) {
           float4 e0 = make_float4(0.f, 0.f, 0.f, 0.f);
           if (load_eps)  // SWIZZLE_128B: 16-byte chunk v4 of row r sits at chunk v4 ^ (r & 7)
-            e0 = *reinterpret_cast<const float4*>(erow + ((v4 ^ (r & 7)) << 4));
+            e0 = lds_f4(erow + ((v4 ^ (r & 7)) << 4));
           g[v4 * 4 + 0] = fmaf(md.x, e0.x, g[v4 * 4 + 0]);
           g[v4 * 4 + 1] = fmaf(md.x, e0.y, g[v4 * 4 + 1]);
           g[v4 * 4 + 2] = fmaf(md.x, e0.z, g[v4 * 4 + 2]);

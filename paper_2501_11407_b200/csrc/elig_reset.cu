@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         k0 = coef[((long long)b * n + i) * 2];      // M_u, M_a, Dt_uu, Dt_ua
         k1 = coef[((long long)b * n + i) * 2 + 1];  // Dt_au, Dt_aa
       }
-      const uint8_t* eu_row = esm + eb * ESET + box * (ETR / 2) + r * 128;
-      const uint8_t* ea_row = eu_row + ETR;
+      const uint32_t eu_row = smem_u32(esm + eb * ESET + box * (ETR / 2) + r * 128);
+      const uint32_t ea_row = eu_row + ETR;
       if (load_eps) mbar_wait(smem_u32(&efull[eb]), (lb >> 1) & 1);
       float Du[16], Da[16];
       if (do_mma) {
@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         float4 eu = make_float4(0.f, 0.f, 0.f, 0.f), ea = eu;
         if (load_eps) {  // SWIZZLE_128B: chunk c of row r at c ^ (r & 7)
           const int chk = (ch0 + v4) ^ (r & 7);
-          eu = *reinterpret_cast<const float4*>(eu_row + (chk << 4));
-          ea = *reinterpret_cast<const float4*>(ea_row + (chk << 4));
+          eu = lds_f4(eu_row + (chk << 4));
+          ea = lds_f4(ea_row + (chk << 4));
         }
         const float e_u[4] = {eu.x, eu.y, eu.z, eu.w}, e_a[4] = {ea.x, ea.y, ea.z, ea.w};
         float nu[4], na[4];

@@ -35,7 +35,7 @@ from . import _lib
 from .errors import LabelOutOfRange, ShapeMismatch
 
 SM_COUNT_DEFAULT = 148
-CHUNKS = (63, 127, 255)  # Tc with Tc + 1 a multiple of the 64-wide K block
+CHUNKS = (63, 127, 255, 511)  # Tc with Tc + 1 a multiple of the 64-wide K block
 
 
 def ctypes_void(p):
@@ -75,11 +75,31 @@ def _wave_split(tiles: int, B: int, sms: int) -> int:
     return best
 
 
-def default_chunk(T: int) -> int:
+def chunk_bytes(Tc: int, B: int, n: int, k: int, alif: bool = True) -> int:
+    """Device bytes of the Tc-sized chunk buffers of an engine (current, packed spikes,
+    psi scratch, C/W operands, xbar operands): the part of the footprint that grows with
+    the chunk length (none of it grows with T)."""
+    KR = Tc + 1
+    kp = _round_up(k, 128)
+    ldc = _round_up(n, 8)
+    ops = 2 * (2 if alif else 1) * 2 * B * KR * ldc
+    return (8 * B * Tc * n + B * Tc * kp + 4 * B * (KR + 1) * n + ops + 4 * B * KR * kp)
+
+
+def default_chunk(T: int, B: int | None = None, n: int | None = None, k: int | None = None,
+                  alif: bool = True, budget: int = 24 << 30) -> int:
+    """Chunk length Tc for a sequence of T steps: the smallest Tc covering the whole
+    sequence, else the longest one whose chunk buffers fit ``budget`` bytes.  Longer
+    chunks are strictly less work (the per-synapse ALIF trace makes one HBM round trip per
+    chunk, K6) and memory stays independent of T."""
     for c in CHUNKS:
-        if T <= c:
+        if T <= c and (B is None or chunk_bytes(c, B, n, k, alif) <= budget):
             return c
-    return 127
+    best = CHUNKS[0]
+    for c in CHUNKS:
+        if B is None or chunk_bytes(c, B, n, k, alif) <= budget:
+            best = c
+    return best
 
 
 class EpropEngine:

@@ -80,7 +80,7 @@ def get_engine(net: Network, B: int, *, chunk: int | None = None, T: int | None 
     """Engine cache keyed by shape, neuron kind, weight precision, chunk and device."""
     dev = torch.device(device if device is not None else "cuda")
     if chunk is None:
-        chunk = default_chunk(T or 127)
+        chunk = default_chunk(T or 127, B, net.n, net.k, net.is_alif)
     w_f64 = net.neuron.w.dtype == np.float64
     reset = bool(net.neuron.reset)
     key = (net.n, net.k, net.m, B, net.is_alif, w_f64, chunk, str(dev), reset)

@@ -163,7 +163,8 @@ class DeviceTrainer:
         self.lr, self.beta1, self.beta2, self.eps = float(lr), float(beta1), float(beta2), float(eps)
         self.device = torch.device(device if device is not None else "cuda")
         self.group = group
-        self.chunk = chunk if chunk is not None else default_chunk(T or 127)
+        self.chunk = chunk if chunk is not None else default_chunk(T or 127, None, net.n, net.k,
+                                                                   net.is_alif)
         self.is_f64 = net.neuron.w.dtype == np.float64
         tdt = torch.float64 if self.is_f64 else torch.float32
         self.tdt = tdt
@@ -313,7 +314,8 @@ def evaluate(net: Network, dataset, *, batch_size: int = 256, device=None):
         if eng is None:
             eng = EpropEngine(net.n, net.k, net.m, B, alif=net.is_alif,
                               w_f64=net.neuron.w.dtype == np.float64,
-                              chunk=default_chunk(T), device=dev, reset=net.neuron.reset)
+                              chunk=default_chunk(T, B, net.n, net.k, net.is_alif), device=dev,
+                              reset=net.neuron.reset)
             eng.set_weights(w, wo)
             engines[B] = eng
         eng.run(xs[s0:s0 + B], ld[s0:s0 + B], bits=bits, forward_only=True, **kw)

@@ -83,7 +83,7 @@ SMALL = ["c1_lif_f64", "c1_alif_f64", "c1_lif_f32", "c1_alif_f32", "mid_alif_f64
 
 
 @pytest.mark.parametrize("name", SMALL)
-@pytest.mark.parametrize("chunk", [63, 127])
+@pytest.mark.parametrize("chunk", [63, 127, 511])
 def test_small_configs_vs_reference(name, chunk):
     _need_gpu()
     g = load_golden(name)
@@ -135,12 +135,13 @@ def test_drop_in_single_sample_api(name):
 
 
 @pytest.mark.parametrize("name", ["c2_lif_f64", "c3_alif_f64", "c4_alif_f64"])
-def test_shd_ssc_shapes_vs_reference(name):
+@pytest.mark.parametrize("chunk", [127, None])   # None = the engine's default (255 / 511)
+def test_shd_ssc_shapes_vs_reference(name, chunk):
     _need_gpu()
     g = load_golden(name)
     net = _net_from_golden(g)
     x, labels = _inputs(g)
-    eng, r = _run_engine(net, x, labels, chunk=127, raster=True)
+    eng, r = _run_engine(net, x, labels, chunk=chunk, raster=True)
     assert np.array_equal(_unpack_raster(r, net.n), _golden_raster(g))
     assert np.allclose(eng.loss.cpu().numpy(), g["loss"], rtol=1e-9)
     gw = eng.grad_w(torch.float64).cpu().numpy()
@@ -157,6 +158,8 @@ def test_shd_ssc_shapes_vs_reference(name):
     ("lif", 300, 130, 5, 150, 10, 63),
     ("alif", 130, 700, 20, 300, 33, 127),
     ("alif", 64, 40, 3, 520, 5, 255),
+    ("alif", 96, 60, 4, 1300, 4, 511),      # 3 chunks of 511 (the long-sequence default)
+    ("lif", 70, 50, 3, 600, 6, 511),
 ])
 def test_batched_vs_two_pass_oracle(kind, n, k, m, T, B, chunk):
     """Ragged shapes (n, k not tile multiples, T not a chunk multiple) vs the numpy oracle."""
@@ -293,6 +296,9 @@ def test_streamed_inputs_match_resident_and_memory_is_flat_in_T():
                      eng.grad_wout.cpu().numpy())
     for a, b in zip(res["resident"], res["streamed"]):
         assert np.array_equal(a, b)
+    del eng, xin  # measure the next engines from a clean base
+    import gc
+    gc.collect()
     peaks = []
     for T in (300, 3000):
         x, y = poisson_batch(B, 700, T, 20, seed=6)
