@@ -39,11 +39,13 @@ CONFIGS = {
     "c2": ("lif", 256, 700, 20, 250, 128),
     "c3": ("alif", 1024, 700, 20, 250, 256),
     "c4": ("alif", 2048, 700, 35, 500, 128),
+    "c5": ("alif", 1024, 700, 20, 2000, 256),
 }
 CONFIG_DESC = {
     "c2": "SHD-shaped LIF e-prop 700->256->20, T=250",
     "c3": "SHD-shaped ALIF e-prop 700->1024->20, T=250",
     "c4": "SSC-shaped ALIF e-prop 700->2048->35, T=500 (per-GPU shard of the 1024 batch at 8 GPUs)",
+    "c5": "C5 sweep point: ALIF e-prop 700->1024->20, T=2000 (4 chunks: per-synapse trace carried)",
 }
 METRIC = "e-prop train samples·timesteps/s (SHD-shape ALIF); HBM GB/s vs roofline"
 UNIT = "samples*timesteps/s"

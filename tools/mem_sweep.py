@@ -23,7 +23,7 @@ def main():
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--hidden", default="256,1024,4096,8192")
     ap.add_argument("--T", default="100,1000,10000")
-    ap.add_argument("--chunk", type=int, default=127)
+    ap.add_argument("--chunk", type=int, default=0, help="0 = engine default (memory-budgeted)")
     args = ap.parse_args()
     B, k, m = args.batch, 700, 20
     for n in [int(v) for v in args.hidden.split(",")]:
@@ -31,7 +31,12 @@ def main():
                                            precision="f32", seed=0))
         kw = _neuron_kwargs(net)
         rows = []
-        for T in [int(v) for v in args.T.split(",")]:
+        Ts = [int(v) for v in args.T.split(",")]
+        from paper_2501_11407_b200.engine import default_chunk
+        # one chunk length for the whole sweep (the one the longest T gets), so the
+        # footprint comparison is across T only
+        chunk = args.chunk or default_chunk(max(Ts), B, n, k)
+        for T in Ts:
             x, y = poisson_batch(B, k, T, m, seed=1)
             xh = torch.from_numpy(x).pin_memory()
             yd = torch.from_numpy(y).cuda()
@@ -39,7 +44,7 @@ def main():
             torch.cuda.empty_cache()
             torch.cuda.reset_peak_memory_stats()
             base = torch.cuda.memory_allocated()
-            eng = EpropEngine(n, k, m, B, alif=True, chunk=args.chunk)
+            eng = EpropEngine(n, k, m, B, alif=True, chunk=chunk)
             eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
             eng.run(xh, yd, **kw)                      # warm-up
             torch.cuda.synchronize()
@@ -52,7 +57,8 @@ def main():
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / reps
             peak = torch.cuda.max_memory_allocated() - base
-            rows.append({"n_hidden": n, "T": T, "batch": B, "peak_device_bytes": int(peak),
+            rows.append({"n_hidden": n, "T": T, "batch": B, "chunk": chunk,
+                         "peak_device_bytes": int(peak),
                          "ms_per_update": ms, "samples_timesteps_per_s": B * T / (ms * 1e-3),
                          "inputs": "streamed from pinned host memory (H2D inside the timing)"})
             del eng
