@@ -196,6 +196,14 @@ int spb_copy_chunk_h2d(void* dst, long long dst_pitch, const void* src, long lon
 int spb_finalize_grad(const double* acc, int rows, int cols, int ld, void* out, int out_is_f64,
                       cudaStream_t stream);
 
+/* On-device synthetic spikes (poisson.cu): out[b*stride_b + t*ceil(k/8) + (j>>3)] bit (j&7)
+ * = 1 with probability rates[labels[b]][j] for t < T, global step t0+t, Philox4x32-10
+ * keyed by `seed`, counter (byte, step, sample) -- reproducible in any chunking; the
+ * distribution of sample_events (datasets.py:65-67), not numpy's bits. */
+int spb_poisson_bits(const float* rates, const long long* labels, int B, int T, int k, int t0,
+                     unsigned long long seed, uint8_t* out, long long stride_b,
+                     cudaStream_t stream);
+
 /* Optimizer steps on device after the gradient / allreduce, restating
  * sgd_update / adam_update (training.py:58-91) operation by operation in the parameter
  * dtype (p_is_f64 ? fp64 : fp32).  p [rows][cols] (and Adam moments m, v, same dtype) are

@@ -28,8 +28,8 @@ constexpr int BM = 128;       // (sample, step) rows per tile
 constexpr int NT = 32;        // neurons per tile (per slice)
 constexpr int BK = 128;       // bytes (= int8 elements) of K per stage: one 128B swizzle row
 constexpr int STAGES = 4;
-constexpr int THREADS = 576;  // warp 0 TMA, warp 1 MMA, warps 2-17 epilogue
-constexpr int EPI_WARPS = 16; // 4 TMEM lane quarters x 4 groups of 8 of the 32 neurons
+constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+constexpr int EPI_WARPS = 8;  // 4 TMEM lane quarters x 2 halves of the 32 neurons
 constexpr int TILE_A = BM * BK;
 
 template <int P>
@@ -102,11 +102,11 @@ __device__ __forceinline__ double pow2(int e) {  // 2^e for -1022 <= e <= 1023
   return __longlong_as_double((long long)(e + 1023) << 52);
 }
 
-// Epilogue of one 128-row x 32-neuron tile, split over 16 warps: TMEM lane quarter q and
-// neuron group h (8 neurons).  Each thread pulls its row's P slice accumulators for its
-// 8 neurons in two batches (slices 0-2, then 3..P-1, one tcgen05.wait each), recombines
-// them exactly in int64 and writes 8 fp64 currents (64 contiguous bytes).
-constexpr int NH = NT / 4;  // neurons per epilogue thread
+// Epilogue of one 128-row x 32-neuron tile, split over 8 warps: TMEM lane quarter q and
+// neuron half h (16 neurons).  Each thread pulls its row's P slice accumulators for its
+// 16 neurons in two batches (slices 0-2, then 3..P-1, one tcgen05.wait each), recombines
+// them exactly in int64 and writes 16 fp64 currents (128 contiguous bytes).
+constexpr int NH = NT / 2;  // neurons per epilogue thread (16 epilogue warps measured slower)
 
 template <int P>
 __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&se)[NH],
@@ -116,7 +116,7 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&s
   {
     int32_t r[3][NH];
 #pragma unroll
-    for (int p = 0; p < 3; ++p) tmem_ld8_nowait(tbase + p * NT, r[p]);
+    for (int p = 0; p < 3; ++p) tmem_ld16_nowait(tbase + p * NT, r[p]);
     tmem_wait_ld();
 #pragma unroll
     for (int c = 0; c < NH; ++c)
@@ -125,7 +125,7 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&s
   {
     int32_t r[P - 3][NH];
 #pragma unroll
-    for (int p = 3; p < P; ++p) tmem_ld8_nowait(tbase + p * NT, r[p - 3]);
+    for (int p = 3; p < P; ++p) tmem_ld16_nowait(tbase + p * NT, r[p - 3]);
     tmem_wait_ld();
 #pragma unroll
     for (int c = 0; c < NH; ++c) {
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     const int q = warp & 3;          // TMEM lane quarter
-    const int hh = (warp - 2) >> 2;  // 8-neuron group of the tile
+    const int hh = (warp - 2) >> 2;  // neuron half of the tile
     int lt = 0;
     for (int t = t_begin; t < t_end; ++t, ++lt) {
       const int nt = t / m_tiles, mt = t % m_tiles;
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     const int q = warp & 3;          // TMEM lane quarter accessible to this warp
-    const int hh = (warp - 2) >> 2;  // 8-neuron group of the tile
+    const int hh = (warp - 2) >> 2;  // neuron half of the tile
     int lt = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
       const int nt = t / m_tiles, mt = t % m_tiles;

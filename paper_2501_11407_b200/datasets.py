@@ -255,6 +255,50 @@ def poisson_batch(n_samples: int, n_channels: int, n_steps: int, n_classes: int,
     return x, labels
 
 
+class DevicePoisson:
+    """Synthetic Poisson spike batches generated ON the device.
+
+    Per-class rates come from ``sample_rate_patterns`` with ``numpy.random.default_rng(
+    seed)`` exactly as the reference draws them (datasets.py:60-62, 75); labels per batch
+    from a numpy generator; the Bernoulli grid itself is drawn by the kernel
+    ``spb_poisson_bits`` (Philox4x32-10, counter = (channel byte, step, sample)), so a
+    batch never crosses PCIe.  Same distribution as ``sample_events``, not numpy's bits --
+    parity runs use ``poisson_batch``.  ``batch(B, T)`` returns (bits uint8 [B, T,
+    ceil(k/8)] on the device, labels int64 [B] on the device) for ``engine.run(...,
+    bits=True)``.
+    """
+
+    def __init__(self, n_classes: int, n_channels: int, seed: int = 0, device=None):
+        import torch
+        self.torch = torch
+        self.k, self.m = int(n_channels), int(n_classes)
+        rng = np.random.default_rng(seed)
+        self.rates_np = sample_rate_patterns(n_classes, n_channels, rng)
+        self.device = torch.device(device if device is not None else "cuda")
+        self.rates = torch.from_numpy(self.rates_np.astype(np.float32)).to(self.device)
+        self.seed = int(seed)
+        self._label_rng = rng
+        self._calls = 0
+
+    def batch(self, B: int, T: int, out=None, labels=None):
+        from . import _lib
+        torch = self.torch
+        if labels is None:
+            lab = self._label_rng.integers(self.m, size=B).astype(np.int64)
+            labels = torch.from_numpy(lab).to(self.device)
+        kb = (self.k + 7) // 8
+        if out is None:
+            out = torch.empty((B, T, kb), dtype=torch.uint8, device=self.device)
+        key = (self.seed * 0x9E3779B97F4A7C15 + self._calls) & 0xFFFFFFFFFFFFFFFF
+        self._calls += 1
+        import ctypes
+        _lib.call("spb_poisson_bits", ctypes.c_void_p(self.rates.data_ptr()),
+                  ctypes.c_void_p(labels.data_ptr()), B, T, self.k, 0, key,
+                  ctypes.c_void_p(out.data_ptr()), T * kb,
+                  ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+        return out, labels
+
+
 # --------------------------------------------------------------------------------------
 # SPIKES v1 I/O (datasets.py:86-135)
 # --------------------------------------------------------------------------------------

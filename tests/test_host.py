@@ -48,6 +48,8 @@ def test_ctypes_signatures_match_header():
                 assert ct is ctypes.c_void_p, (name, h)
             elif "double" in h:
                 assert ct is ctypes.c_double, (name, h)
+            elif "unsigned long long" in h:
+                assert ct is ctypes.c_ulonglong, (name, h)
             elif "long long" in h:
                 assert ct is ctypes.c_longlong, (name, h)
             else:

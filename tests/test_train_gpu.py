@@ -190,3 +190,29 @@ def test_smooth_mode_vs_reference(name, chunk):
     # the drop-in accepts smooth=True as the reference does
     res = P.eprop_batch_gradient(net, x, y, smooth=True)
     assert _rel(res.grads["w"], ref) <= 1e-4
+
+
+def test_device_poisson_generator():
+    """spb_poisson_bits: per-class/channel firing rates match sample_events' distribution,
+    deterministic per seed, no stray bits past k, and the engine trains on it directly."""
+    _need_gpu()
+    from paper_2501_11407_b200.datasets import DevicePoisson
+    k, m, B, T = 37, 3, 64, 400
+    gen = DevicePoisson(m, k, seed=3)
+    bits, labels = gen.batch(B, T)
+    x = np.unpackbits(bits.cpu().numpy(), axis=-1, bitorder="little")
+    assert np.all(x[..., k:] == 0)
+    x = x[..., :k].astype(np.float64)
+    lab = labels.cpu().numpy()
+    for c in range(m):
+        sel = x[lab == c]
+        if len(sel) < 4:
+            continue
+        emp = sel.mean(axis=(0, 1))
+        p = gen.rates_np[c]
+        sd = np.sqrt(p * (1 - p) / (sel.shape[0] * T))
+        assert np.all(np.abs(emp - p) <= 5 * sd + 1e-9)
+    again = DevicePoisson(m, k, seed=3).batch(B, T)[0]
+    assert torch.equal(again, bits)
+    other = DevicePoisson(m, k, seed=4).batch(B, T)[0]
+    assert not torch.equal(other, bits)

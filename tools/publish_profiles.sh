@@ -1,0 +1,21 @@
+#!/bin/bash
+# Copy the judged evidence of a capture (tools/capture_profiles.sh) from gpurun_out/<tag>
+# to profiles/<tag>: bench lines, launch lists (+ per-kernel shares), ncu summaries and
+# SASS hot spots (the .ncu-rep files themselves stay in gpurun_out: too large for git).
+set -u
+TAG=${1:-r1}
+S=gpurun_out/$TAG
+D=profiles/$TAG
+mkdir -p $D
+cp $S/gpu.txt $S/bench_*.json $S/mem_sweep_c5.jsonl $D/ 2>/dev/null
+[ -f $S/mma_microbench.txt ] && cp $S/mma_microbench.txt $D/
+for f in $S/launches_*.csv; do
+  b=$(basename $f .csv)
+  cp $f $D/
+  python tools/launch_summary.py $f > $D/$b.summary.txt
+done
+for r in $S/ncu_*.ncu-rep; do
+  b=$(basename $r .ncu-rep)
+  { python tools/ncu_summary.py $r; python tools/ncu_hotspots.py $r 20; } > $D/$b.summary.txt 2>&1
+done
+ls -la $D
