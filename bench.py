@@ -210,7 +210,8 @@ def main():
         kw.update(beta=net.neuron.beta, rho=net.neuron.rho)
 
     def step(x, y, timers=None, bits=False):
-        eng.run(x, y, timers=timers, bits=bits, **kw)
+        # the synthetic Poisson inputs are 0/1 spikes: promise it (K2 single-int64 path)
+        eng.run(x, y, timers=timers, bits=bits, binary=True, **kw)
         packer.pack(eng.grad_w_acc, eng.grad_wout, eng.loss, eng.correct)
         packer.allreduce()
 

@@ -48,13 +48,20 @@ int spb_device_sm(void); /* compute capability of the current device, e.g. 100 *
  *                      bytes, channel j = bit (j & 7) of byte j >> 3 (packbits, little);
  *                      output row b*Tc + s, or s*B + b with time_major != 0 (K21). 
  *   spb_input_proj:    cur[row][i] = sum_j xq[row][j] W[i][j] for row < M (= B*Tc), fp64;
- *                      persistent grid of min(tiles, sm_count) CTAs. */
+ *                      persistent grid of min(tiles, sm_count) CTAs.  binary != 0 promises
+ *                      0/1 spikes (and k <= 16384): the 7 digit sums then recombine in one
+ *                      int64 (same bits, half the fp64 work). */
 int spb_slice_weights(const void* w, int w_is_f64, int n, int k, int Kpad, int n_pad32, int P,
                       int8_t* wq, int* sexp, cudaStream_t stream);
 int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits, int len, int Tc,
                     int Kpad, int time_major, uint8_t* xq, cudaStream_t stream);
 int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
-                   int Kpad, int P, double* cur, int sm_count, cudaStream_t stream);
+                   int Kpad, int P, double* cur, int sm_count, int binary, cudaStream_t stream);
+/* Profiling variant of spb_input_proj (W-resident kernel): probe bit 0 skips the epilogue,
+ * bit 1 the spike-operand loads; probe = 0 is the production kernel. */
+int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
+                         int n_pad32, int Kpad, int P, double* cur, int sm_count, int binary,
+                         int probe, cudaStream_t stream);
 
 /* K21 Fused exact projection + neuron dynamics (fused.cu): the K2 tensor-core sums of a
  *     (128-sample block, 16-neuron tile) at one step land in TMEM and the epilogue thread

@@ -108,10 +108,15 @@ __device__ __forceinline__ double pow2(int e) {  // 2^e for -1022 <= e <= 1023
 // them exactly in int64 and writes 16 fp64 currents (128 contiguous bytes).
 constexpr int NH = NT / 2;  // neurons per epilogue thread (16 epilogue warps measured slower)
 
-template <int P>
+// BIN (binary spikes, k <= 16384): every digit sum |S_p| < 2^20, so all P = 7 digits
+// recombine into ONE int64 g = sum_p S_p 128^(6-p) (|g| < 2^63) and I = (double)g *
+// 2^(s-48): one rounding of the exact sum, bitwise the value of the two-part path below,
+// with half the fp64-pipe work.
+template <int P, bool BIN>
 __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&se)[NH],
                                                    double* __restrict__ out, int M, int n, int row,
-                                                   int i0, uint32_t tempty_bar, int lane) {
+                                                   int i0, uint32_t tempty_bar, int lane,
+                                                   int probe = 0) {
   long long g0[NH], g1[NH];
   {
     int32_t r[3][NH];
@@ -139,21 +144,57 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&s
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncwarp();
   if (lane == 0) mbar_arrive(tempty_bar);
-  if (row < M) {
-    double* orow = out + (long long)row * n + i0;
+  // values of this thread's row: 16 doubles = 8 double2 chunks
+  double2 ch[NH / 2];
 #pragma unroll
-    for (int c = 0; c < NH; c += 2) {
-      double v[2];
+  for (int c = 0; c < NH; c += 2) {
+    double v[2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < 2; ++h) {
+      if constexpr (BIN && P == 7) {
+        const long long g = (g0[c + h] << 28) + g1[c + h];
+        v[h] = (double)g * pow2(se[c + h] - 48);
+      } else {
         // I = g0 * 2^(s-6-14) + g1 * 2^(s-6-7(P-1))  (both conversions exact)
         v[h] = fma((double)g0[c + h], pow2(se[c + h] - 20),
                    (double)g1[c + h] * pow2(se[c + h] - 6 - 7 * (P - 1)));
       }
-      if (i0 + c + 1 < n) {
-        *reinterpret_cast<double2*>(orow + c) = make_double2(v[0], v[1]);
-      } else if (i0 + c < n) {
-        orow[c] = v[0];
+    }
+    ch[c / 2] = make_double2(v[0], v[1]);
+  }
+  if (probe & 4) {  // profiling probe: no global stores
+    if (ch[0].x == 1.2345e-300 && row < M) out[(long long)row * n + i0] = ch[0].y;
+    return;
+  }
+  // 8x8 transpose of 16-byte chunks inside each group of 8 lanes (3 xor-butterfly
+  // stages): afterwards lane p of the group holds chunk p of the group's 8 rows, so each
+  // store instruction writes 4 rows x 128 contiguous bytes (full lines) instead of 32
+  // rows x 16 bytes -- the uncoalesced row stores were the epilogue's bottleneck.
+  const int p8 = lane & 7;
+#pragma unroll
+  for (int sh = 4; sh >= 1; sh >>= 1) {
+    const bool up = (p8 & sh) != 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k & sh) continue;
+      const double2 send = up ? ch[k] : ch[k | sh];
+      double2 recv;
+      recv.x = __shfl_xor_sync(0xffffffffu, send.x, sh);
+      recv.y = __shfl_xor_sync(0xffffffffu, send.y, sh);
+      if (up) ch[k] = recv; else ch[k | sh] = recv;
+    }
+  }
+  const int row0 = row - p8;           // first row of this lane's group of 8
+  const int col = i0 + 2 * p8;         // this lane's chunk (2 neurons)
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int r = row0 + k;
+    if (r < M) {
+      double* o = out + (long long)r * n + col;
+      if (col + 1 < n) {
+        *reinterpret_cast<double2*>(o) = ch[k];
+      } else if (col < n) {
+        o[0] = ch[k].x;
       }
     }
   }
@@ -172,11 +213,12 @@ struct ResCfg {
   static constexpr int SMEM = W_BYTES + XS * TILE_A + 1024 + 256;
 };
 
-template <int P, int XS>
+template <int P, int XS, bool BIN>
 __global__ void __launch_bounds__(THREADS, 1)
     input_proj_wres_kernel(const __grid_constant__ CUtensorMap tm_x,
                            const __grid_constant__ CUtensorMap tm_w, const int* __restrict__ sexp,
-                           double* __restrict__ out, int M, int n, int n_pad32, int nkb) {
+                           double* __restrict__ out, int M, int n, int n_pad32, int nkb,
+                           int probe) {
   using C = ResCfg<P, XS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -246,6 +288,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int s = it % XS;
           mbar_wait(smem_u32(&xempty[s]), ((it / XS) & 1) ^ 1);
           const uint32_t fb = smem_u32(&xfull[s]);
+          if (probe & 2) {  // profiling probe: no spike-operand traffic
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
+            continue;
+          }
           mbar_expect_tx(fb, TILE_A);
           tma_load_2d(smem_u32(xsm + s * TILE_A), &tm_x, fb, kb * BK, mt * BM);
         }
@@ -295,9 +341,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int c = 0; c < NH; ++c) se[c] = (i0 + c < n) ? __ldg(sexp + i0 + c) : 0;
       mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      proj_epilogue_tile<P>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH),
+      if (probe & 1) {  // profiling probe: no epilogue (TMEM reads, recombination, stores)
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&tempty[a]));
+        continue;
+      }
+      proj_epilogue_tile<P, BIN>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH),
                             se, out, M, n, mt * BM + q * 32 + lane, i0, smem_u32(&tempty[a]),
-                            lane);
+                            lane, probe);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -306,7 +358,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
 }
 
-template <int P>
+template <int P, bool BIN>
 __global__ void __launch_bounds__(THREADS, 1)
     input_proj_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                       const int* __restrict__ sexp, double* __restrict__ out, int M, int n,
@@ -404,7 +456,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int c = 0; c < NH; ++c) se[c] = (i0 + c < n) ? __ldg(sexp + i0 + c) : 0;
       mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      proj_epilogue_tile<P>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH),
+      proj_epilogue_tile<P, BIN>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH),
                             se, out, M, n, mt * BM + q * 32 + lane, i0, smem_u32(&tempty[a]),
                             lane);
     }
@@ -528,8 +580,22 @@ int spb_slice_weights(const void* w, int w_is_f64, int n, int k, int Kpad, int n
   return 0;
 }
 
+int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
+                         int n_pad32, int Kpad, int P, double* out, int sm_count, int binary,
+                         int probe, cudaStream_t stream);
+
 int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
-                   int Kpad, int P, double* out, int sm_count, cudaStream_t stream) {
+                   int Kpad, int P, double* out, int sm_count, int binary, cudaStream_t stream) {
+  return spb_input_proj_probe(xq, wq, sexp, M, n, n_pad32, Kpad, P, out, sm_count, binary, 0,
+                              stream);
+}
+
+// spb_input_proj with a profiling probe for the W-resident kernel: bit 0 skips the
+// epilogue, bit 1 the spike-operand loads (probe = 0 is the production kernel).
+int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
+                         int n_pad32, int Kpad, int P, double* out, int sm_count, int binary,
+                         int probe, cudaStream_t stream) {
+  const bool bin = binary != 0 && P == 7 && Kpad <= 16384;
   SPB_CHECK_ARG(xq && wq && sexp && out && M > 0 && n > 0 && n_pad32 >= n &&
                     n_pad32 % proj::NT == 0 && Kpad % proj::BK == 0 && (P == 7 || P == 8),
                 "spb_input_proj: bad args");
@@ -550,22 +616,22 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
   const int nkb = Kpad / proj::BK;
   if (nkb <= proj::ResCfg<7, 3>::MAXKB) {  // weights of a neuron tile fit in shared memory
     if (P == 7) {
-      auto kfn = proj::input_proj_wres_kernel<7, 3>;
+      auto kfn = bin ? proj::input_proj_wres_kernel<7, 3, true> : proj::input_proj_wres_kernel<7, 3, false>;
       constexpr int sm = proj::ResCfg<7, 3>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      kfn<<<grid, proj::THREADS, sm, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);
+      kfn<<<grid, proj::THREADS, sm, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
     } else {
-      auto kfn = proj::input_proj_wres_kernel<8, 2>;
+      auto kfn = proj::input_proj_wres_kernel<8, 2, false>;
       constexpr int sm = proj::ResCfg<8, 2>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      kfn<<<grid, proj::THREADS, sm, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);
+      kfn<<<grid, proj::THREADS, sm, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
     }
   } else if (P == 7) {
-    auto kfn = proj::input_proj_kernel<7>;
+    auto kfn = bin ? proj::input_proj_kernel<7, true> : proj::input_proj_kernel<7, false>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, proj::Cfg<7>::SMEM);
     kfn<<<grid, proj::THREADS, proj::Cfg<7>::SMEM, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);
   } else {
-    auto kfn = proj::input_proj_kernel<8>;
+    auto kfn = proj::input_proj_kernel<8, false>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, proj::Cfg<8>::SMEM);
     kfn<<<grid, proj::THREADS, proj::Cfg<8>::SMEM, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);
   }

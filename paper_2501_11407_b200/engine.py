@@ -264,12 +264,13 @@ class EpropEngine:
               v(raster.data_ptr()) if raster is not None else None,
               v(psi.data_ptr()) if psi is not None else None, self.sm_count, st)
 
-    def _project(self, ln, st, timed=None):
-        """K2: cur = W x_t exactly on INT8 tensor cores from the packed chunk."""
+    def _project(self, ln, st, timed=None, binary=False):
+        """K2: cur = W x_t exactly on INT8 tensor cores from the packed chunk (binary:
+        0/1 spikes, single-int64 digit recombination)."""
         v = ctypes_void
         args = ("spb_input_proj", v(self.xq.data_ptr()), v(self.wq.data_ptr()),
                 v(self.sexp.data_ptr()), self.B * self.Tc, self.n, self.n_pad32, self.Kpad,
-                self.P, v(self.cur.data_ptr()), self.sm_count, st)
+                self.P, v(self.cur.data_ptr()), self.sm_count, int(bool(binary)), st)
         if timed is not None:
             timed("proj", ln, *args)
         else:
@@ -279,7 +280,7 @@ class EpropEngine:
     def run(self, x: torch.Tensor, labels: torch.Tensor, *, alpha=0.95, theta=1.0, slope=10.0,
             beta=0.8, rho=0.96, kappa=0.95, reset=False, raster: torch.Tensor | None = None,
             stream=None, timers: dict | None = None, bits: bool = False, smooth: bool = False,
-            forward_only: bool = False):
+            forward_only: bool = False, binary: bool | None = None):
         """One full e-prop update.
 
         x       uint8 [B, T, k] spike counts, or with ``bits=True`` uint8 [B, T, ceil(k/8)]
@@ -296,9 +297,13 @@ class EpropEngine:
                 smooth=True mode, gradients.py:114-115); the trace algebra is unchanged.
         forward_only  pass A + loss only (network_loss, gradients.py:349-365): no
                 gradients are computed (evaluate()).
+        binary  promise that every input count is 0 or 1 (default: True for bit-packed
+                input); K2 then recombines its digit sums in one int64 (same bits).
         Results stay on device: ``grad_w_acc`` (fp64 [n, kp]), ``grad_wout``, ``loss``,
         ``s`` (readout sums), ``correct``.
         """
+        if binary is None:
+            binary = bits
         if bool(reset) != self.reset:
             raise ValueError(f"engine built for reset={self.reset}, called with reset={reset}")
         kb = (self.k + 7) // 8 if bits else self.k
@@ -406,7 +411,7 @@ class EpropEngine:
                             (ln, 0, one and not forward_only))
                 self.launches += 2
                 continue
-            self._project(ln, st, timed)
+            self._project(ln, st, timed, binary)
             timed("forward_a", (ln, 0, one), "spb_forward_chunk", 0,
                   v(self.cur.data_ptr()), B, n, Tc, KR, ln, t0, T,
                   *common, v(self.u.data_ptr()), v(self.a.data_ptr()),
@@ -444,7 +449,7 @@ class EpropEngine:
                     self._fused(1, ln, t0, T, common, None, self.psi, st, timed,
                                 (ln, 1, carry_out))
                 else:
-                    self._project(ln, st, timed)
+                    self._project(ln, st, timed, binary)
                 self.launches += 2
             # one chunk (pass A parked psi) or K21 (parks psi itself): backward scan only
             pid = 2 if (one or self.fused) else 1

@@ -271,6 +271,35 @@ def test_int8_tensor_core_projection_is_exact(w_f64):
     assert float(np.max(err - bound)) <= 0.0
 
 
+@pytest.mark.parametrize("k", [700, 2000])   # W-resident and streamed-W kernels
+def test_binary_recombination_is_bitwise_the_two_part_path(k):
+    """K2 with binary=1 (one int64 per output) gives the same bits as binary=0."""
+    _need_gpu()
+    import ctypes
+    from paper_2501_11407_b200.engine import EpropEngine
+    rng = np.random.default_rng(1)
+    B, T, n = 6, 40, 200
+    w = (rng.uniform(-1, 1, (n, k)) / np.sqrt(k)).astype(np.float32)
+    w[5, :] *= 1e-5
+    x = (rng.random((B, T, k)) < 0.15).astype(np.uint8)
+    eng = EpropEngine(n, k, 3, B, alif=False, chunk=63, fused=False)
+    eng.set_weights(torch.from_numpy(w), torch.zeros((3, n), dtype=torch.float64))
+    xd = torch.from_numpy(x).cuda()
+    v = ctypes.c_void_p
+    st = v(torch.cuda.current_stream().cuda_stream)
+    eng._pack(xd.data_ptr(), T * k, False, T, st)
+    outs = []
+    for binary in (False, True):
+        eng.cur.zero_()
+        eng._project(T, st, binary=binary)
+        torch.cuda.synchronize()
+        outs.append(eng.cur.cpu().numpy().copy())
+    assert np.array_equal(outs[0], outs[1])
+    exact = np.einsum("btk,nk->btn", x.astype(np.longdouble), w.astype(np.longdouble))
+    got = outs[1].reshape(B, eng.Tc, n)[:, :T]
+    assert np.max(np.abs(got - exact.astype(np.float64))) <= 2.3e-16 * np.max(np.abs(exact))
+
+
 def test_streamed_inputs_match_resident_and_memory_is_flat_in_T():
     """Streaming x chunk by chunk from pinned host memory gives bitwise the same update as
     resident inputs, and peak device memory does not grow with T."""

@@ -1,0 +1,35 @@
+"""Time K2 (W-resident INT8 projection) at the C3 shape with the epilogue and/or the
+spike-operand loads switched off (spb_input_proj_probe) to locate its bottleneck."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2501_11407_b200 as P
+from paper_2501_11407_b200 import _lib
+from paper_2501_11407_b200.engine import EpropEngine
+from paper_2501_11407_b200.datasets import poisson_batch
+
+B, n, k, T = int(sys.argv[1]) if len(sys.argv) > 1 else 256, 1024, 700, 250
+net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=n, n_inputs=k, n_classes=20, precision="f32"))
+x, y = poisson_batch(B, k, T, 20, seed=1)
+eng = EpropEngine(n, k, 20, B, alif=True, chunk=255)
+eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+eng.run(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+torch.cuda.synchronize()
+v = ctypes.c_void_p
+st = v(torch.cuda.current_stream().cuda_stream)
+for binary, probe in ((0, 0), (1, 0), (0, 1), (0, 2), (0, 3), (0, 4), (1, 4)):
+    ts = []
+    for rep in range(8):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.call("spb_input_proj_probe", v(eng.xq.data_ptr()), v(eng.wq.data_ptr()),
+                  v(eng.sexp.data_ptr()), B * eng.Tc, n, eng.n_pad32, eng.Kpad, eng.P,
+                  v(eng.cur.data_ptr()), eng.sm_count, binary, probe, st)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ops = 2.0 * eng.P * B * eng.Tc * n * eng.Kpad
+    ms = float(np.median(ts[2:]))
+    print(f"binary={binary} probe={probe} (bit0: no epilogue, bit1: no x loads, bit2: no stores): {ms:.4f} ms, "
+          f"{ops / ms / 1e9:.0f} TOPS issued", flush=True)
