@@ -86,11 +86,21 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
   const bool park = psis != nullptr && valid_i;
   float* prow = psis != nullptr ? psis + (long long)b * (P.KR + 1) * P.n + i : nullptr;
   if (park) prow[0] = surrogate_grad_f32((float)d_prev, slope);  // psi_{t0-1}
+  // software pipeline: the current of steps s8+8..s8+15 is in flight while steps
+  // s8..s8+7 integrate (16 outstanding 8-byte loads per thread; the kernel is HBM-bound)
+  double In[8];
+#pragma unroll
+  for (int u8 = 0; u8 < 8; ++u8)
+    In[u8] = (valid_i && u8 < P.len) ? __ldcs(crow + (long long)u8 * P.n) : 0.0;
   for (int s8 = 0; s8 < P.len; s8 += 8) {
     double Ib[8];
 #pragma unroll
-    for (int u8 = 0; u8 < 8; ++u8)
-      Ib[u8] = (valid_i && s8 + u8 < P.len) ? crow[(long long)(s8 + u8) * P.n] : 0.0;
+    for (int u8 = 0; u8 < 8; ++u8) Ib[u8] = In[u8];
+#pragma unroll
+    for (int u8 = 0; u8 < 8; ++u8) {
+      const int sn = s8 + 8 + u8;
+      In[u8] = (valid_i && sn < P.len) ? __ldcs(crow + (long long)sn * P.n) : 0.0;
+    }
 #pragma unroll
     for (int u8 = 0; u8 < 8; ++u8) {
       const int s = s8 + u8;
