@@ -170,6 +170,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--recurrent", action="store_true",
+                    help="recurrent W_rec extension (SURVEY.md 8(f)-4) on the chosen shape")
     ap.add_argument("--profile", action="store_true",
                     help="minimal run for ncu: no clocks, e2e or cpu baseline")
     args = ap.parse_args()
@@ -194,16 +196,19 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     kind, n, k, m, T, B = CONFIGS[args.config]
-    spec = P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=m, precision="f32", seed=0)
+    spec = P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=m, precision="f32", seed=0,
+                         recurrent=args.recurrent)
     net = P.init_network(spec)
     x_np, y_np = poisson_batch(B, k, T, m, seed=1000 + rank)
     from paper_2501_11407_b200.engine import default_chunk
     chunk = args.chunk or default_chunk(T, B, n, k, kind == "alif")
-    eng = EpropEngine(n, k, m, B, alif=kind == "alif", w_f64=False, chunk=chunk, device=dev)
-    eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+    eng = EpropEngine(n, k, m, B, alif=kind == "alif", w_f64=False, chunk=chunk, device=dev,
+                      recurrent=args.recurrent)
+    eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out),
+                    w_rec=torch.from_numpy(net.neuron.w_rec) if args.recurrent else None)
     xd = torch.from_numpy(x_np).to(dev)
     yd = torch.from_numpy(y_np).to(dev)
-    packer = GradPacker(n, k, m, dev)
+    packer = GradPacker(n, k, m, dev)  # (recurrent: grad W_rec stays in the accumulator)
     kw = dict(alpha=net.neuron.alpha, theta=net.neuron.theta, slope=net.neuron.slope,
               kappa=net.readout.kappa)
     if kind == "alif":
@@ -401,7 +406,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": CONFIG_DESC[args.config], "batch_per_gpu": B,
+            "config": {"workload": CONFIG_DESC[args.config] + (" + recurrent W_rec" if
+                                                               args.recurrent else ""),
+                       "batch_per_gpu": B,
                        "global_batch": B * world, "seq_len": T, "n_hidden": n, "n_inputs": k,
                        "n_classes": m, "chunk": eng.Tc, "parallelism": f"dp{world}",
                        "forward_precision": "fp64 state/current (bit-exact spikes)",

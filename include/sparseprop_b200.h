@@ -123,6 +123,25 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
                       void* wa_hi, void* wa_lo, int ldc, float* mdt, float* psi_scratch,
                       cudaStream_t stream);
 
+/* K1rec Recurrent hidden layer (forward_rec.cu, parity unpinned):
+ *     u <- alpha u + (cur[row][i] + sum_{j: z_{t-1}[j]} W_rec[i][j]), otherwise as K1.
+ *     wrecT [n][n] = W_rec transposed (fp32, or fp64 with w_is_f64), n <= 2048; one CTA
+ *     per sample, the recurrent sum over active j ascending in fp64.  pass 0 (A): zbar,
+ *     zsum, raster (full words, optional); psi_scratch and zchunk [B][KR][ceil(n/32)]
+ *     (row r = spikes z_{t0+r-1}, bit-packed) are written when given (pass B needs both).
+ * spb_pack_rec: x~ operand rows (b, s) = [xq row (k bytes, at b*xq_sb + s*xq_st) |
+ *     z_{t0+s-1} as n bytes] -> out [B*Tc][Kx], Kx >= k + n; K4 then filters kx = k + n
+ *     columns and K5 / K6 produce the gradient of [W | W_rec]. */
+int spb_forward_rec_chunk(int pass, const double* cur, const void* wrecT, int w_is_f64, int B,
+                          int n, int Tc, int KR, int len, int t0, int T, double alpha,
+                          double theta, double slope, double beta, double rho, double kappa,
+                          int reset, int alif, int smooth, double* u, double* a, double* zbar,
+                          double* zsum, uint32_t* raster, float* psi_scratch, uint32_t* zchunk,
+                          cudaStream_t stream);
+int spb_pack_rec(const uint8_t* xq, long long xq_sb, long long xq_st, const uint32_t* zchunk,
+                 int B, int k, int n, int Tc, int KR, int len, int Kx, uint8_t* out,
+                 cudaStream_t stream);
+
 /* K4  Presynaptic filter xbar_t = alpha*xbar_{t-1} + x_t (the factorised LIF trace G_u,
  *     gradients.py:89-94 with H_I = alpha, F rows = x_t; test_gradients.py:81-91).
  *     x byte counts of (b, s) at x[b*stride_b + s*stride_t + j] (the K2 operand xq works);

@@ -421,3 +421,78 @@ def train_online(w, w_out, p: Params, x, labels, optimizer="sgd", lr=0.01, epoch
             if max_updates is not None and updates >= max_updates:
                 return w, w_out, rows
     return w, w_out, rows
+
+
+# --------------------------------------------------------------------------------------
+# recurrent extension -- PARITY UNPINNED: the reference has no
+# recurrent weights (neurons.py:165-172), so this restatement is the
+# spec of the GPU kernels, not a copy of reference behaviour.  It is pinned only by
+# (1) w_rec = 0 reproducing the feed-forward functions above bit for bit and (2) the
+# e-prop trace construction being the reference's own with the presynaptic input
+# x_t replaced by [x_t, z_{t-1}] (the standard e-prop treatment of recurrent weights,
+# H_E dropped).
+# --------------------------------------------------------------------------------------
+
+def step_state_rec(w, w_rec, p: Params, u, a, x_t, smooth=False):
+    """One forward step with recurrent input: I_t = W x_t + W_rec z_{t-1}, added to the
+    leak as ONE current (u' = alpha*u + I_t), z_{t-1} = spike(d_{t-1})."""
+    beta, rho = p.beta_eff, p.rho_eff
+    z = _spike(u - p.theta - beta * a, p.slope, smooth)
+    a_next = rho * a + z
+    current = w @ x_t + (w_rec @ z if w_rec is not None else 0.0)
+    u_next = p.alpha * u + current
+    if p.reset:
+        u_next = u_next - p.theta * z
+    drive = u_next - p.theta - beta * a_next
+    return u_next, a_next, _spike(drive, p.slope, smooth), surrogate_grad(drive, p.slope), z
+
+
+def eprop_forward_mode_rec(w, w_rec, w_out, p: Params, x_seq, label, smooth=False):
+    """Per-sample online e-prop of a recurrent layer: eprop_forward_mode with the trace
+    input x~_t = [x_t, z_{t-1}] and the forward of step_state_rec.  Returns
+    (Result with grad_w = [n, k + n] over [W | W_rec], raster [T, n])."""
+    dtype = w.dtype
+    n, k = w.shape
+    m = w_out.shape[0]
+    T = x_seq.shape[0]
+    beta, rho = p.beta_eff, p.rho_eff
+    rst = 1.0 if p.reset else 0.0
+    kk = k + n
+    u = np.zeros(n, dtype=dtype)
+    a = np.zeros(n, dtype=dtype)
+    g_u = np.zeros((n, kk), dtype=dtype)
+    g_a = np.zeros((n, kk), dtype=dtype) if p.alif else None
+    xbar = np.zeros((n, kk), dtype=dtype)
+    xsum = np.zeros((n, kk), dtype=dtype)
+    zbar = np.zeros(n, dtype=dtype)
+    zsum = np.zeros(n, dtype=dtype)
+    v = np.zeros(m, dtype=dtype)
+    s = np.zeros(m, dtype=dtype)
+    raster = np.zeros((T, n), dtype=bool)
+    for t in range(T):
+        psi_prev = surrogate_grad(u - p.theta - beta * a, p.slope)
+        u, a_new, z, sg, z_prev = step_state_rec(w, w_rec, p, u, a, x_seq[t], smooth)
+        xt = np.concatenate([x_seq[t].astype(dtype), z_prev.astype(dtype)])
+        h_uu = p.alpha - rst * p.theta * psi_prev
+        if p.alif:
+            h_ua = rst * p.theta * beta * psi_prev
+            g_u_new = h_uu[:, None] * g_u + h_ua[:, None] * g_a + xt[None, :]
+            g_a = psi_prev[:, None] * g_u + (rho - beta * psi_prev)[:, None] * g_a
+            g_u = g_u_new
+            x_step = sg[:, None] * (g_u - beta * g_a)
+        else:
+            g_u = h_uu[:, None] * g_u + xt[None, :]
+            x_step = sg[:, None] * g_u
+        a = a_new
+        raster[t] = z > 0.5
+        v = p.kappa * v + w_out @ z
+        s = s + v
+        xbar *= p.kappa
+        xbar += x_step
+        xsum += xbar
+        zbar = p.kappa * zbar + z
+        zsum = zsum + zbar
+    loss, g = softmax_cross_entropy(s, label)
+    w_sig = w_out.T @ g
+    return Result(loss, (w_sig[:, None] * xsum).astype(dtype), np.outer(g, zsum).astype(dtype),
+                  s), raster

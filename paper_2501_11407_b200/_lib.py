@@ -45,6 +45,9 @@ SIGNATURES = {
     "spb_sgd_update": [P, I, I, I, P, I, I, D, D, P, P],
     "spb_adam_update": [P, P, P, I, I, I, P, I, I, D, D, D, D, D, I, P, P],
     "spb_poisson_bits": [P, P, I, I, I, I, ctypes.c_ulonglong, P, LL, P],
+    "spb_forward_rec_chunk": [I, P, P, I, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I, I,
+                              P, P, P, P, P, P, P, P],
+    "spb_pack_rec": [P, LL, LL, P, I, I, I, I, I, I, I, P, P],
     "spb_version": [],
     "spb_device_sm": [],
 }

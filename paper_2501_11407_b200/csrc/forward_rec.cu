@@ -1,0 +1,272 @@
+// K1rec: LIF/ALIF dynamics of a RECURRENT hidden layer over one time chunk (sm_100a), and
+// the operand builder that appends the previous step's spikes to the input for the
+// eligibility kernels.  SURVEY.md 8(f)-4 -- parity UNPINNED: the reference has no
+// recurrent weights; the semantics are those of
+// oracle/eprop_ref.py:step_state_rec / eprop_forward_mode_rec:
+//
+//   z_{t-1} = spike(d_{t-1});  a <- rho a + z_{t-1}
+//   u <- alpha u + (I_in,t + W_rec z_{t-1})   [- theta z_{t-1} with reset]
+//   d = (u - theta) - beta a;  z_t = spike(d);  psi_t = surrogate(d)
+//
+// with I_in,t the exact projection of K2 and the recurrent current summed in fp64 over the
+// active presynaptic neurons in ascending index order (deterministic).  The e-prop trace
+// of W_rec is the input trace with presynaptic input z_{t-1} (H_E dropped), so pass B
+// runs the unchanged scan / xbar / GEMM / carry kernels on the extended input
+// x~_t = [x_t, z_{t-1}] (spb_pack_rec).
+//
+// One CTA per sample, 512 threads, NPT <= 4 neurons per thread (n <= 2048); the spikes of
+// the previous step live in a double-buffered shared bitmask, compacted by one warp into
+// an ascending active list each step (two __syncthreads per step) so that the weight
+// loads of 8 presynaptic spikes are in flight at once.
+// W_rec is stored transposed (wrecT[j][i] = W_rec[i][j]) so the gather of an active
+// presynaptic row is coalesced across the CTA's threads.
+#include "common.cuh"
+
+namespace spb {
+
+constexpr int REC_THREADS = 512;
+constexpr int REC_MAX_N = 2048;
+
+struct RecParams {
+  int B, n, Tc, KR, len, t0, T;
+  double alpha, theta, slope, beta, rho, kappa;
+  int reset, alif, pass, smooth, w_f64;
+};
+
+__device__ __forceinline__ double rec_spike(double d, bool smooth, double slope) {
+  if (!smooth) return d >= 0.0 ? 1.0 : 0.0;
+  return __dadd_rn(0.5, __ddiv_rn(d, __dadd_rn(1.0, __dmul_rn(slope, fabs(d)))));
+}
+
+template <int NPT>
+__global__ void __launch_bounds__(REC_THREADS, 1) forward_rec_kernel(
+    RecParams P, const double* __restrict__ cur, const void* __restrict__ wrecT,
+    double* __restrict__ u_st, double* __restrict__ a_st, double* __restrict__ zbar_st,
+    double* __restrict__ zsum_st, uint32_t* __restrict__ raster, float* __restrict__ psis,
+    uint32_t* __restrict__ zchunk) {
+  __shared__ uint32_t mask[2][REC_MAX_N / 32];
+  __shared__ uint16_t act[REC_MAX_N];
+  __shared__ int nact;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int b = blockIdx.x;
+  const int n = P.n, nw = (n + 31) >> 5;
+  const bool smooth = P.smooth != 0;
+  const double theta = P.theta, beta = P.beta, slope = P.slope;
+  const float slope_f = (float)P.slope;
+  const float* wf = static_cast<const float*>(wrecT);
+  const double* wd = static_cast<const double*>(wrecT);
+  double u[NPT], a[NPT], zb[NPT], zs[NPT], dp[NPT];
+#pragma unroll
+  for (int c = 0; c < NPT; ++c) {
+    const int i = tid + c * REC_THREADS;
+    const bool v = i < n;
+    const long long bi = (long long)b * n + i;
+    u[c] = (v && P.t0 > 0) ? u_st[bi] : 0.0;
+    a[c] = (v && P.t0 > 0) ? a_st[bi] : 0.0;
+    zb[c] = (v && P.t0 > 0 && P.pass == 0) ? zbar_st[bi] : 0.0;
+    zs[c] = (v && P.t0 > 0 && P.pass == 0) ? zsum_st[bi] : 0.0;
+    dp[c] = __dsub_rn(__dsub_rn(u[c], theta), __dmul_rn(beta, a[c]));
+  }
+  // z_{t0-1} from the carried state (the expression the reference re-evaluates)
+#pragma unroll
+  for (int c = 0; c < NPT; ++c) {
+    const int i = tid + c * REC_THREADS;
+    const bool zv = (i < n) && rec_spike(dp[c], smooth, slope) > 0.5;
+    const unsigned bal = __ballot_sync(0xffffffffu, zv);
+    if (lane == 0 && (c * REC_THREADS + (tid & ~31)) < n) mask[0][(c * REC_THREADS + (tid & ~31)) >> 5] = bal;
+  }
+  float* prow = psis != nullptr ? psis + (long long)b * (P.KR + 1) * n : nullptr;
+  if (prow != nullptr) {
+#pragma unroll
+    for (int c = 0; c < NPT; ++c) {
+      const int i = tid + c * REC_THREADS;
+      if (i < n) prow[i] = surrogate_grad_f32((float)dp[c], slope_f);  // psi_{t0-1}
+    }
+  }
+  __syncthreads();
+  uint32_t* zrow = zchunk != nullptr ? zchunk + (long long)b * P.KR * nw : nullptr;
+  if (zrow != nullptr)  // chunk row 0 = z_{t0-1}
+    for (int w = tid; w < nw; w += REC_THREADS) zrow[w] = mask[0][w];
+  const double* crow = cur + (long long)b * P.Tc * n;
+  for (int s = 0; s < P.len; ++s) {
+    const uint32_t* mprev = mask[s & 1];
+    uint32_t* mnext = mask[(s + 1) & 1];
+    // input current of this step (exact, from K2), issued before the gather
+    double I[NPT];
+#pragma unroll
+    for (int c = 0; c < NPT; ++c) {
+      const int i = tid + c * REC_THREADS;
+      I[c] = i < n ? __ldcs(crow + (long long)s * n + i) : 0.0;
+    }
+    // active list of z_{t-1} (ascending), built by warp 0 from the bitmask
+    if (tid < 32) {
+      int base = 0;
+      for (int w0 = 0; w0 < nw; w0 += 32) {
+        const int w = w0 + lane;
+        uint32_t bits = w < nw ? mprev[w] : 0u;
+        const int cnt = __popc(bits);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        int pos = base + incl - cnt;
+        while (bits) {
+          act[pos++] = (uint16_t)((w << 5) + __ffs(bits) - 1);
+          bits &= bits - 1;
+        }
+        base += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) nact = base;
+    }
+    __syncthreads();
+    // recurrent current: sum over the active presynaptic j in ascending order, the
+    // weight loads of GB spikes in flight at once
+    double R[NPT];
+#pragma unroll
+    for (int c = 0; c < NPT; ++c) R[c] = 0.0;
+    const int na = nact;
+    constexpr int GB = 8;
+    for (int q0 = 0; q0 < na; q0 += GB) {
+      double wv[GB][NPT];
+#pragma unroll
+      for (int q = 0; q < GB; ++q) {
+        const long long o = (long long)(q0 + q < na ? act[q0 + q] : 0) * n;
+#pragma unroll
+        for (int c = 0; c < NPT; ++c) {
+          const int i = tid + c * REC_THREADS;
+          wv[q][c] = (q0 + q < na && i < n) ? (P.w_f64 ? wd[o + i] : (double)wf[o + i]) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < GB; ++q)
+#pragma unroll
+        for (int c = 0; c < NPT; ++c)
+          if (q0 + q < na) R[c] = __dadd_rn(R[c], wv[q][c]);
+    }
+    float psi[NPT];
+#pragma unroll
+    for (int c = 0; c < NPT; ++c) {
+      const int i = tid + c * REC_THREADS;
+      const double z_prev = rec_spike(dp[c], smooth, slope);
+      a[c] = __dadd_rn(__dmul_rn(P.rho, a[c]), z_prev);
+      u[c] = __dadd_rn(__dmul_rn(P.alpha, u[c]), __dadd_rn(I[c], R[c]));
+      if (P.reset) u[c] = __dsub_rn(u[c], __dmul_rn(theta, z_prev));
+      const double d = __dsub_rn(__dsub_rn(u[c], theta), __dmul_rn(beta, a[c]));
+      const double zv = rec_spike(d, smooth, slope);
+      if (P.pass == 0) {
+        zb[c] = __dadd_rn(__dmul_rn(P.kappa, zb[c]), zv);
+        zs[c] = __dadd_rn(zs[c], zb[c]);
+      }
+      psi[c] = surrogate_grad_f32((float)d, slope_f);
+      dp[c] = d;
+      const unsigned bal = __ballot_sync(0xffffffffu, zv > 0.5 && i < n);
+      const int wi = (c * REC_THREADS + (tid & ~31)) >> 5;
+      if (lane == 0 && wi < nw) {
+        mnext[wi] = bal;
+        if (P.pass == 0 && raster != nullptr)
+          raster[((long long)b * P.T + P.t0 + s) * nw + wi] = bal;
+        if (zrow != nullptr) zrow[(long long)(s + 1) * nw + wi] = bal;
+      }
+    }
+    if (prow != nullptr) {
+#pragma unroll
+      for (int c = 0; c < NPT; ++c) {
+        const int i = tid + c * REC_THREADS;
+        if (i < n) prow[(long long)(s + 1) * n + i] = psi[c];
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int c = 0; c < NPT; ++c) {
+    const int i = tid + c * REC_THREADS;
+    if (i < n) {
+      const long long bi = (long long)b * n + i;
+      u_st[bi] = u[c];
+      a_st[bi] = a[c];
+      if (P.pass == 0) {
+        zbar_st[bi] = zb[c];
+        zsum_st[bi] = zs[c];
+      }
+    }
+  }
+}
+
+// x~ operand: row (b, s) of the chunk = [xq row (k bytes) | z_{t0+s-1} bits as n bytes],
+// zero padded to Kx; rows s >= len zero.  Warp per row.
+__global__ void pack_rec_kernel(const uint8_t* __restrict__ xq, long long xq_sb, long long xq_st,
+                                const uint32_t* __restrict__ zchunk, int B, int k, int n, int Tc,
+                                int KR, int len, int Kx, uint8_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (n + 31) >> 5;
+  const long long rows = (long long)B * Tc;
+  for (long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += (long long)gridDim.x * (blockDim.x >> 5)) {
+    const int s = (int)(row % Tc), b = (int)(row / Tc);
+    uint8_t* o = out + row * Kx;
+    const bool live = s < len;
+    const uint8_t* xr = xq + (long long)b * xq_sb + (long long)s * xq_st;
+    const uint32_t* zr = zchunk + ((long long)b * KR + s) * nw;
+    for (int c = lane; c < Kx; c += 32) {
+      uint8_t v = 0;
+      if (live) {
+        if (c < k) v = xr[c];
+        else if (c < k + n) v = (uint8_t)((zr[(c - k) >> 5] >> ((c - k) & 31)) & 1u);
+      }
+      o[c] = v;
+    }
+  }
+}
+
+}  // namespace spb
+
+using namespace spb;
+
+extern "C" {
+
+int spb_forward_rec_chunk(int pass, const double* cur, const void* wrecT, int w_is_f64, int B,
+                          int n, int Tc, int KR, int len, int t0, int T, double alpha,
+                          double theta, double slope, double beta, double rho, double kappa,
+                          int reset, int alif, int smooth, double* u, double* a, double* zbar,
+                          double* zsum, uint32_t* raster, float* psi_scratch, uint32_t* zchunk,
+                          cudaStream_t stream) {
+  SPB_CHECK_ARG(pass == 0 || pass == 1, "spb_forward_rec_chunk: pass must be 0 (A) or 1 (B)");
+  SPB_CHECK_ARG(cur && wrecT && u && a, "spb_forward_rec_chunk: null pointer");
+  SPB_CHECK_ARG(pass == 1 || (zbar && zsum), "spb_forward_rec_chunk: pass A needs zbar/zsum");
+  SPB_CHECK_ARG(B > 0 && n > 0 && n <= REC_MAX_N && Tc > 0 && len >= 1 && len <= Tc &&
+                    KR >= Tc + 1 && t0 >= 0 && t0 + len <= T,
+                "spb_forward_rec_chunk: bad sizes (n <= %d)", REC_MAX_N);
+  RecParams P{B, n, Tc, KR, len, t0, T, alpha, theta, slope, beta, rho, kappa,
+              reset, alif, pass, smooth, w_is_f64};
+  const int npt = (n + REC_THREADS - 1) / REC_THREADS;
+  if (npt <= 1)
+    forward_rec_kernel<1><<<B, REC_THREADS, 0, stream>>>(P, cur, wrecT, u, a, zbar, zsum, raster,
+                                                         psi_scratch, zchunk);
+  else if (npt <= 2)
+    forward_rec_kernel<2><<<B, REC_THREADS, 0, stream>>>(P, cur, wrecT, u, a, zbar, zsum, raster,
+                                                         psi_scratch, zchunk);
+  else
+    forward_rec_kernel<4><<<B, REC_THREADS, 0, stream>>>(P, cur, wrecT, u, a, zbar, zsum, raster,
+                                                         psi_scratch, zchunk);
+  SPB_CHECK_LAUNCH("forward_rec");
+  return 0;
+}
+
+int spb_pack_rec(const uint8_t* xq, long long xq_sb, long long xq_st, const uint32_t* zchunk,
+                 int B, int k, int n, int Tc, int KR, int len, int Kx, uint8_t* out,
+                 cudaStream_t stream) {
+  SPB_CHECK_ARG(xq && zchunk && out && B > 0 && k > 0 && n > 0 && Kx >= k + n && len >= 0 &&
+                    len <= Tc && KR >= Tc + 1,
+                "spb_pack_rec: bad args");
+  const long long rows = (long long)B * Tc;
+  const long long want = (rows + 7) / 8;
+  const int blocks = (int)(want < 148LL * 16 ? want : 148LL * 16);
+  pack_rec_kernel<<<blocks, 256, 0, stream>>>(xq, xq_sb, xq_st, zchunk, B, k, n, Tc, KR, len, Kx,
+                                              out);
+  SPB_CHECK_LAUNCH("pack_rec");
+  return 0;
+}
+
+}  // extern "C"

@@ -107,7 +107,7 @@ class EpropEngine:
 
     def __init__(self, n: int, k: int, m: int, B: int, *, alif: bool, w_f64: bool = False,
                  chunk: int = 127, device=None, sm_count: int | None = None,
-                 reset: bool = False, fused: bool | None = None):
+                 reset: bool = False, fused: bool | None = None, recurrent: bool = False):
         if chunk not in CHUNKS:
             raise ValueError(f"chunk must be one of {CHUNKS} (Tc + 1 a multiple of 64)")
         self.lib = _lib.load()
@@ -124,8 +124,14 @@ class EpropEngine:
         self.KR = self.Tc + 1
         self.device = torch.device(device if device is not None else "cuda")
         self.n_pad = _round_up(self.n, 128)
-        self.kp = _round_up(self.k, 128)
-        self.ke = _round_up(self.k, 4)
+        # recurrent layer: the eligibility kernels see the extended
+        # input x~_t = [x_t, z_{t-1}] of width kx = k + n (forward_rec.cu)
+        self.recurrent = bool(recurrent)
+        if self.recurrent and self.n > 2048:
+            raise ValueError("the recurrent path supports n <= 2048 hidden neurons")
+        self.kx = self.k + (self.n if self.recurrent else 0)
+        self.kp = _round_up(self.kx, 128)
+        self.ke = _round_up(self.kx, 4)
         sms = sm_count or (torch.cuda.get_device_properties(self.device).multi_processor_count
                            if self.device.type == "cuda" else SM_COUNT_DEFAULT)
         self.sm_count = sms
@@ -148,6 +154,8 @@ class EpropEngine:
             fused = False
         if fused and not fusable:
             raise ValueError("the fused projection needs k <= 768")
+        if fused and recurrent:
+            raise ValueError("the fused projection has no recurrent variant")
         self.fused = bool(fused)
         self.xq = torch.zeros((B * self.Tc, self.Kpad), dtype=torch.uint8, device=dev)
         self.cur = (None if self.fused else
@@ -170,7 +178,13 @@ class EpropEngine:
         self.ldc = _round_up(n, 8)   # C/W are MN-major [K][ldc] (neurons contiguous)
         self.c_hi = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
         self.c_lo = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
-        self.xbar_state = torch.empty((B, k), dtype=f64, device=dev)
+        self.xbar_state = torch.empty((B, self.kx), dtype=f64, device=dev)
+        if self.recurrent:
+            self.wrecT = torch.zeros((n, n), dtype=f64 if self.w_f64 else f32, device=dev)
+            self.nw = (n + 31) // 32
+            self.zchunk = torch.zeros((B, self.KR, self.nw), dtype=torch.int32, device=dev)
+            self.Kx2 = _round_up(self.kx, 4)
+            self.xq2 = torch.zeros((B * self.Tc, self.Kx2), dtype=torch.uint8, device=dev)
         self.xh = torch.zeros((K, self.kp), dtype=bf16, device=dev)   # MN-major [K][kp]
         self.xl = torch.zeros((K, self.kp), dtype=bf16, device=dev)
         # split-K (K5) and sample-split (K6) partial slices, reduced in fixed order
@@ -213,11 +227,21 @@ class EpropEngine:
             self._ev = None
 
     # ----------------------------------------------------------------------------------
-    def set_weights(self, w, w_out, stream=None):
+    def set_weights(self, w, w_out, stream=None, w_rec=None):
         """Upload input weights and readout weights (fp64) and slice W into the INT8
-        digits of the exact tensor-core projection (K2)."""
+        digits of the exact tensor-core projection (K2); recurrent engines also take
+        ``w_rec`` [n, n] (stored transposed for the coalesced spike gather)."""
         w = torch.as_tensor(w)
         w_out = torch.as_tensor(w_out)
+        if self.recurrent:
+            if w_rec is None:
+                raise ShapeMismatch("a recurrent engine needs w_rec")
+            w_rec = torch.as_tensor(w_rec)
+            if tuple(w_rec.shape) != (self.n, self.n):
+                raise ShapeMismatch(f"w_rec must be [{self.n}, {self.n}]")
+            self.wrecT.copy_(w_rec.to(self.wrecT.dtype).t().contiguous(), non_blocking=True)
+        elif w_rec is not None:
+            raise ShapeMismatch("w_rec given to a feed-forward engine")
         if tuple(w.shape) != (self.n, self.k) or tuple(w_out.shape) != (self.m, self.n):
             raise ShapeMismatch(f"weights {tuple(w.shape)}/{tuple(w_out.shape)} do not match "
                                 f"engine (n={self.n}, k={self.k}, m={self.m})")
@@ -397,7 +421,8 @@ class EpropEngine:
             t0 = c * Tc
             ln = min(Tc, T - t0)
             pack_chunk(c, ln)
-            if one and use_side and not forward_only:  # K4 needs only x: overlap with pass A
+            if one and use_side and not forward_only and not self.recurrent:
+                # K4 needs only x: overlap it with pass A
                 self._ev["xbar"].record(main)
                 self.side.wait_event(self._ev["xbar"])
                 call("spb_xbar_chunk", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
@@ -412,6 +437,11 @@ class EpropEngine:
                 self.launches += 2
                 continue
             self._project(ln, st, timed, binary)
+            if self.recurrent:
+                self._forward_rec(0, ln, t0, T, common, raster,
+                                  one and not forward_only, st, timed, (ln, 0, one))
+                self.launches += 3
+                continue
             timed("forward_a", (ln, 0, one), "spb_forward_chunk", 0,
                   v(self.cur.data_ptr()), B, n, Tc, KR, ln, t0, T,
                   *common, v(self.u.data_ptr()), v(self.a.data_ptr()),
@@ -450,9 +480,13 @@ class EpropEngine:
                                 (ln, 1, carry_out))
                 else:
                     self._project(ln, st, timed, binary)
+                    if self.recurrent:
+                        self._forward_rec(1, ln, t0, T, common, None, True, st, timed,
+                                          (ln, 1, carry_out))
+                        self.launches += 1
                 self.launches += 2
-            # one chunk (pass A parked psi) or K21 (parks psi itself): backward scan only
-            pid = 2 if (one or self.fused) else 1
+            # one chunk (pass A parked psi) or K21 / K1rec (park psi themselves): scan only
+            pid = 2 if (one or self.fused or self.recurrent) else 1
             timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,
                   v(self.cur.data_ptr()) if self.cur is not None else None, B, n, Tc, KR,
                   ln, t0, T, *common, v(self.u.data_ptr()), v(self.a.data_ptr()), None, None,
@@ -464,7 +498,17 @@ class EpropEngine:
                   v(self.wa_lo.data_ptr()) if carry_out and self.ntr == 2 else None, self.ldc,
                   v(self.mdt.data_ptr()) if self.ntr else None, v(self.psi.data_ptr()), st)
             self.launches += 1 if pid == 2 else 2
-            if one and use_side:
+            if self.recurrent:
+                # x~ = [x_t, z_{t-1}] bytes, then the usual filter over kx columns
+                call("spb_pack_rec", v(self.xq.data_ptr()), xq_sb, xq_st,
+                     v(self.zchunk.data_ptr()), B, k, n, Tc, KR, ln, self.Kx2,
+                     v(self.xq2.data_ptr()), st)
+                call("spb_xbar_chunk", v(self.xq2.data_ptr()), Tc * self.Kx2, self.Kx2, B,
+                     self.kx, self.kp, KR, ln, int(c == 0 or self.reset), x_alpha,
+                     v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()), v(self.xl.data_ptr()),
+                     st)
+                self.launches += 2
+            elif one and use_side:
                 main.wait_event(self._ev["xbar"])
             else:
                 call("spb_xbar_chunk", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
@@ -483,7 +527,7 @@ class EpropEngine:
                     timed("carry", (ln, c > 0, not last), "spb_alif_carry_chunk",
                           v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()), self.ldc,
                           v(self.xh.data_ptr()), v(self.xl.data_ptr()), v(self.mdt.data_ptr()),
-                          v(self.eps.data_ptr()), v(part6), B, n, self.n_pad, k, self.ke,
+                          v(self.eps.data_ptr()), v(part6), B, n, self.n_pad, self.kx, self.ke,
                           self.kp, KR, self.splits6, int(not last), int(c > 0), int(not last),
                           st)
                 else:
@@ -491,7 +535,8 @@ class EpropEngine:
                           v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()),
                           v(self.wa_hi.data_ptr()), v(self.wa_lo.data_ptr()), self.ldc,
                           v(self.xh.data_ptr()), v(self.mdt.data_ptr()), v(self.eps.data_ptr()),
-                          v(self.eps2.data_ptr()), v(part6), B, n, self.n_pad, k, self.ke,
+                          v(self.eps2.data_ptr()), v(part6), B, n, self.n_pad, self.kx,
+                          self.ke,
                           self.kp, KR, self.splits6, int(not last), int(c > 0), int(not last),
                           st)
                 self.launches += 1
@@ -521,6 +566,32 @@ class EpropEngine:
         if labels_np.size and (labels_np.min() < 0 or labels_np.max() >= self.m):
             bad = labels_np[(labels_np < 0) | (labels_np >= self.m)][0]
             raise LabelOutOfRange(f"label {int(bad)} out of range for {self.m} classes")
+
+    def _forward_rec(self, pass_id, ln, t0, T, common, raster, park, st, timed, meta):
+        """K1rec: recurrent dynamics of a chunk from K2's input current (pass 0: raster,
+        zsum; parks psi and the chunk spikes for pass B when ``park``)."""
+        v = ctypes_void
+        alpha, theta, slope, beta, rho, kappa, reset, alif, smooth = common
+        timed("forward_a" if pass_id == 0 else "forward_rec_b", meta, "spb_forward_rec_chunk",
+              pass_id, v(self.cur.data_ptr()), v(self.wrecT.data_ptr()), int(self.w_f64),
+              self.B, self.n, self.Tc, self.KR, ln, t0, T, alpha, theta, slope, beta, rho,
+              kappa, reset, alif, smooth, v(self.u.data_ptr()), v(self.a.data_ptr()),
+              v(self.zbar.data_ptr()) if pass_id == 0 else None,
+              v(self.zsum.data_ptr()) if pass_id == 0 else None,
+              v(raster.data_ptr()) if raster is not None else None,
+              v(self.psi.data_ptr()) if park else None,
+              v(self.zchunk.data_ptr()) if park else None, st)
+
+    def grad_w_rec(self, dtype=torch.float32):
+        """Finalised recurrent-weight gradient [n, n] (columns k .. k+n of the
+        accumulator over the extended input)."""
+        if not self.recurrent:
+            raise ValueError("not a recurrent engine")
+        out = torch.empty((self.n, self.n), dtype=dtype, device=self.device)
+        _lib.call("spb_finalize_grad", ctypes_void(self.grad_w_acc.data_ptr() + 8 * self.k),
+                  self.n, self.n, self.kp, ctypes_void(out.data_ptr()),
+                  int(dtype == torch.float64), ctypes_void(self._stream()))
+        return out
 
     def grad_w(self, dtype=torch.float32):
         """Finalised input-weight gradient [n, k] in ``dtype`` (device tensor)."""

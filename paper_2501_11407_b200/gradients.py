@@ -83,11 +83,12 @@ def get_engine(net: Network, B: int, *, chunk: int | None = None, T: int | None 
         chunk = default_chunk(T or 127, B, net.n, net.k, net.is_alif)
     w_f64 = net.neuron.w.dtype == np.float64
     reset = bool(net.neuron.reset)
-    key = (net.n, net.k, net.m, B, net.is_alif, w_f64, chunk, str(dev), reset)
+    rec = net.is_recurrent
+    key = (net.n, net.k, net.m, B, net.is_alif, w_f64, chunk, str(dev), reset, rec)
     eng = _ENGINES.get(key)
     if eng is None:
         eng = EpropEngine(net.n, net.k, net.m, B, alif=net.is_alif, w_f64=w_f64, chunk=chunk,
-                          device=dev, reset=reset)
+                          device=dev, reset=reset, recurrent=rec)
         _ENGINES[key] = eng
     return eng
 
@@ -138,16 +139,21 @@ def eprop_batch_gradient(net: Network, x, labels, *, chunk: int | None = None,
     xd = torch.from_numpy(xc).to(dev)
     ld = torch.from_numpy(labels).to(dev)
     eng.set_weights(torch.from_numpy(np.ascontiguousarray(net.neuron.w)),
-                    torch.from_numpy(np.ascontiguousarray(net.readout.w_out)))
+                    torch.from_numpy(np.ascontiguousarray(net.readout.w_out)),
+                    w_rec=(torch.from_numpy(np.ascontiguousarray(net.neuron.w_rec))
+                           if net.is_recurrent else None))
     eng.run(xd, ld, smooth=smooth, **_neuron_kwargs(net))
     wdt = torch.float64 if net.neuron.w.dtype == np.float64 else torch.float32
     gw = eng.grad_w(wdt)
     gwo = eng.grad_wout.to(wdt)
     out_dtype = net.neuron.w.dtype
+    grads = {"w": gw.cpu().numpy().astype(out_dtype, copy=False),
+             "w_out": gwo.cpu().numpy().astype(out_dtype, copy=False)}
+    if net.is_recurrent:
+        grads["w_rec"] = eng.grad_w_rec(wdt).cpu().numpy().astype(out_dtype, copy=False)
     return BatchGradResult(
         loss=eng.loss.cpu().numpy().copy(),
-        grads={"w": gw.cpu().numpy().astype(out_dtype, copy=False),
-               "w_out": gwo.cpu().numpy().astype(out_dtype, copy=False)},
+        grads=grads,
         readout_sum=eng.s.cpu().numpy().astype(out_dtype),
         correct=eng.correct.cpu().numpy().astype(bool),
     )

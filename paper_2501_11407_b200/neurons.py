@@ -9,7 +9,7 @@ host: the per-step dynamics (neurons.py:109-137) and the step Jacobians
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import KW_ONLY, dataclass
 
 import numpy as np
 
@@ -25,12 +25,20 @@ class LIFParams:
     theta: float = 1.0
     slope: float = DEFAULT_SLOPE
     reset: bool = False
+    _: KW_ONLY
+    # recurrent extension (not in the reference, parity unpinned):
+    # W_rec [n, n] feeding z_{t-1} back into the current; None = the reference's
+    # feed-forward layer.  Keyword-only so the reference's positional constructors
+    # (LIFParams(w, alpha, theta, slope, reset), ALIFParams(..., beta, rho)) are unchanged.
+    w_rec: np.ndarray | None = None
 
     def __post_init__(self):
         if not (0.0 < self.alpha < 1.0):
             raise ValueError("alpha must be in (0, 1)")
         if not self.theta > 0.0:
             raise ValueError("theta must be positive")
+        if self.w_rec is not None and np.shape(self.w_rec) != (self.n, self.n):
+            raise ValueError("w_rec must be [n, n]")
 
     @property
     def n(self) -> int:
@@ -91,3 +99,7 @@ class Network:
     @property
     def is_alif(self) -> bool:
         return isinstance(self.neuron, ALIFParams)
+
+    @property
+    def is_recurrent(self) -> bool:
+        return self.neuron.w_rec is not None

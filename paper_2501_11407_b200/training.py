@@ -49,6 +49,7 @@ class NetworkSpec:
     reset: bool = False
     precision: str = "f64"
     seed: int = 0
+    recurrent: bool = False  # extension: also draw W_rec (after w_out, zero diagonal)
 
 
 def init_network(spec: NetworkSpec) -> Network:
@@ -61,10 +62,16 @@ def init_network(spec: NetworkSpec) -> Network:
     lim_out = 1.0 / np.sqrt(spec.n_hidden)
     w = gen.uniform(-lim_in, lim_in, size=(spec.n_hidden, spec.n_inputs)).astype(dtype)
     w_out = gen.uniform(-lim_out, lim_out, size=(spec.n_classes, spec.n_hidden)).astype(dtype)
+    w_rec = None
+    if spec.recurrent:  # drawn after the reference's two blocks: feed-forward nets unchanged
+        w_rec = gen.uniform(-lim_out, lim_out, size=(spec.n_hidden, spec.n_hidden))
+        np.fill_diagonal(w_rec, 0.0)
+        w_rec = w_rec.astype(dtype)
     if spec.kind == "lif":
-        neuron = LIFParams(w, spec.alpha, spec.theta, spec.slope, spec.reset)
+        neuron = LIFParams(w, spec.alpha, spec.theta, spec.slope, spec.reset, w_rec=w_rec)
     elif spec.kind == "alif":
-        neuron = ALIFParams(w, spec.alpha, spec.theta, spec.slope, spec.reset, spec.beta, spec.rho)
+        neuron = ALIFParams(w, spec.alpha, spec.theta, spec.slope, spec.reset, spec.beta, spec.rho,
+                            w_rec=w_rec)
     else:
         raise ValueError(f"unknown neuron kind {spec.kind!r}")
     return Network(spec.kind, neuron, ReadoutParams(w_out, spec.kappa))
@@ -171,10 +178,14 @@ class DeviceTrainer:
         # master parameters in the network dtype (the engine's fp64 W_out is a mirror)
         self.w = torch.from_numpy(np.ascontiguousarray(net.neuron.w)).to(self.device)
         self.w_out = torch.from_numpy(np.ascontiguousarray(net.readout.w_out)).to(self.device)
+        self.w_rec = (torch.from_numpy(np.ascontiguousarray(net.neuron.w_rec)).to(self.device)
+                      if net.is_recurrent else None)
         self.t = 0
         if optimizer == "adam":
             self.m_w, self.v_w = torch.zeros_like(self.w), torch.zeros_like(self.w)
             self.m_wo, self.v_wo = torch.zeros_like(self.w_out), torch.zeros_like(self.w_out)
+            if self.w_rec is not None:
+                self.m_wr, self.v_wr = torch.zeros_like(self.w_rec), torch.zeros_like(self.w_rec)
         self.kw = _neuron_kwargs(net)
         self._engines = {}
         self._hist = []
@@ -192,7 +203,8 @@ class DeviceTrainer:
         if eng is None:
             net = self.net
             eng = EpropEngine(net.n, net.k, net.m, B, alif=net.is_alif, w_f64=self.is_f64,
-                              chunk=self.chunk, device=self.device, reset=net.neuron.reset)
+                              chunk=self.chunk, device=self.device, reset=net.neuron.reset,
+                              recurrent=net.is_recurrent)
             self._engines[B] = eng
         # every engine shares the trainer's parameters: point its W at the master
         # copy and refresh its fp64 W_out mirror + INT8 digits when they changed
@@ -200,6 +212,8 @@ class DeviceTrainer:
             eng.w = self.w
         if getattr(eng, "_wver", None) != self.t:
             eng.wout.copy_(self.w_out.to(self.torch.float64))
+            if self.w_rec is not None:
+                eng.wrecT.copy_(self.w_rec.t())
             eng.slice_weights()
             eng._wver = self.t
         return eng
@@ -217,6 +231,8 @@ class DeviceTrainer:
         st = ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
         v = ctypes.c_void_p
         stats = torch.stack([eng.loss.sum(), eng.correct.sum().to(torch.float64)])
+        if self._world() > 1 and self.w_rec is not None:
+            raise NotImplementedError("multi-rank training of the recurrent extension")
         if self._world() > 1:
             from .parallel import GradPacker
             if self._packer is None:
@@ -247,6 +263,17 @@ class DeviceTrainer:
                           v(self.v_wo.data_ptr()), f64, m, n, v(g_wo.data_ptr()), g_wo_f64, n,
                           scale, self.lr, self.beta1, self.beta2, self.eps, self.t,
                           v(eng.wout.data_ptr()), st)
+        if self.w_rec is not None:  # columns k .. k+n of the accumulator
+            g_wr = ctypes.c_void_p(eng.grad_w_acc.data_ptr() + 8 * k)
+            if self.optimizer == "sgd":
+                self.lib.call("spb_sgd_update", v(self.w_rec.data_ptr()), f64, n, n, g_wr, 1,
+                              eng.kp, scale, self.lr, None, st)
+            else:
+                self.lib.call("spb_adam_update", v(self.w_rec.data_ptr()),
+                              v(self.m_wr.data_ptr()), v(self.v_wr.data_ptr()), f64, n, n, g_wr,
+                              1, eng.kp, scale, self.lr, self.beta1, self.beta2, self.eps,
+                              self.t, None, st)
+            eng.wrecT.copy_(self.w_rec.t())
         # this engine's digits follow the new W right away (the next update's K2)
         eng.slice_weights()
         eng._wver = self.t
@@ -265,6 +292,9 @@ class DeviceTrainer:
     def weights(self):
         """Current parameters as numpy arrays in the network dtype."""
         return self.w.cpu().numpy(), self.w_out.cpu().numpy()
+
+    def weights_rec(self):
+        return None if self.w_rec is None else self.w_rec.cpu().numpy()
 
 
 def _set_weights(net: Network, w: np.ndarray, w_out: np.ndarray) -> None:
@@ -315,8 +345,9 @@ def evaluate(net: Network, dataset, *, batch_size: int = 256, device=None):
             eng = EpropEngine(net.n, net.k, net.m, B, alif=net.is_alif,
                               w_f64=net.neuron.w.dtype == np.float64,
                               chunk=default_chunk(T, B, net.n, net.k, net.is_alif), device=dev,
-                              reset=net.neuron.reset)
-            eng.set_weights(w, wo)
+                              reset=net.neuron.reset, recurrent=net.is_recurrent)
+            eng.set_weights(w, wo, w_rec=(torch.from_numpy(np.ascontiguousarray(
+                net.neuron.w_rec)) if net.is_recurrent else None))
             engines[B] = eng
         eng.run(xs[s0:s0 + B], ld[s0:s0 + B], bits=bits, forward_only=True, **kw)
         losses.append(eng.loss.clone())
@@ -388,6 +419,8 @@ def train(spec: NetworkSpec, dataset, method: str = "eprop-sparse", optimizer: s
         metrics.append(MetricsRow(epochs_of[i], i + 1, loss_sum / nb, ep_correct / ep_seen))
     w, w_out = tr.weights()
     _set_weights(net, w, w_out)
+    if net.is_recurrent:
+        net.neuron.w_rec = tr.weights_rec().astype(net.neuron.w.dtype)
     if metrics_path is not None:
         with open(metrics_path, "w", newline="") as fh:
             writer = csv.writer(fh)

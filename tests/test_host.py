@@ -154,6 +154,26 @@ def test_engine_reset_dry_run(monkeypatch, alif):
     assert eng.mdt.shape[-1] == (8 if alif else 2)
 
 
+def test_engine_recurrent_dry_run(monkeypatch):
+    """Recurrent engines: K1rec instead of K1 in both passes, the x~ = [x, z_{t-1}]
+    operand (spb_pack_rec) before K4, eligibility buffers over k + n columns."""
+    rec = _Recorder()
+    monkeypatch.setattr(_lib, "call", rec)
+    eng = EpropEngine(40, 30, 3, 6, alif=True, chunk=63, device="cpu", sm_count=148,
+                      recurrent=True)
+    assert eng.kx == 70 and eng.kp == 128 and eng.xbar_state.shape == (6, 70)
+    eng.run(torch.zeros((6, 150, 30), dtype=torch.uint8), torch.zeros(6, dtype=torch.int64))
+    names = [c[0] for c in rec.calls]
+    assert names.count("spb_forward_rec_chunk") == 6          # 3 chunks x 2 passes
+    assert names.count("spb_pack_rec") == 3 and names.count("spb_xbar_chunk") == 3
+    fw = [c[1] for c in rec.calls if c[0] == "spb_forward_chunk"]
+    assert fw and all(a[0] == 2 for a in fw)                  # scans only
+    xb = [c[1] for c in rec.calls if c[0] == "spb_xbar_chunk"]
+    assert all(a[4] == 70 for a in xb)                        # filters k + n columns
+    with pytest.raises(P.ShapeMismatch):
+        eng.set_weights(torch.zeros(40, 30), torch.zeros(3, 40))   # w_rec missing
+
+
 def test_engine_forward_only_dry_run(monkeypatch):
     rec = _Recorder()
     monkeypatch.setattr(_lib, "call", rec)

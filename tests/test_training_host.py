@@ -78,3 +78,33 @@ def test_device_optimizer_kernels_are_exported():
     lib = _lib.load()
     for name in ("spb_sgd_update", "spb_adam_update"):
         assert hasattr(lib, name)
+
+
+def test_recurrent_spec_keeps_the_reference_weights():
+    """recurrent=True draws W_rec AFTER the reference's two blocks (zero diagonal), so the
+    input and readout weights are the reference's; positional constructors unchanged."""
+    a = init_network(NetworkSpec(kind="alif", n_hidden=12, n_inputs=7, seed=3))
+    b = init_network(NetworkSpec(kind="alif", n_hidden=12, n_inputs=7, seed=3, recurrent=True))
+    assert np.array_equal(a.neuron.w, b.neuron.w)
+    assert np.array_equal(a.readout.w_out, b.readout.w_out)
+    assert a.neuron.w_rec is None and not a.is_recurrent and b.is_recurrent
+    assert b.neuron.w_rec.shape == (12, 12) and np.all(np.diag(b.neuron.w_rec) == 0)
+    from paper_2501_11407_b200.neurons import ALIFParams
+    p = ALIFParams(np.zeros((2, 3)), 0.9, 1.0, 10.0, False, 0.5, 0.9)
+    assert p.beta == 0.5 and p.rho == 0.9 and p.w_rec is None
+    with pytest.raises(ValueError):
+        ALIFParams(np.zeros((2, 3)), w_rec=np.zeros((3, 3)))
+
+
+def test_oracle_recurrent_with_zero_w_rec_is_the_feed_forward_oracle():
+    w, wo = O.init_network_arrays(20, 12, 3, seed=1)
+    x, y = O.poisson_batch(2, 12, 60, 3, seed=1)
+    for alif in (False, True):
+        for rst in (False, True):
+            p = O.Params(alif=alif, reset=rst)
+            r0 = O.eprop_forward_mode(w, wo, p, x[0].astype(float), int(y[0]))
+            r1, ras = O.eprop_forward_mode_rec(w, np.zeros((20, 20)), wo, p,
+                                               x[0].astype(float), int(y[0]))
+            assert np.array_equal(r0.grad_w, r1.grad_w[:, :12]) and r0.loss == r1.loss
+            assert np.array_equal(ras, O.network_loss(w, wo, p, x[0].astype(float),
+                                                      int(y[0]))[2])
