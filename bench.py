@@ -69,6 +69,27 @@ def peaks():
 
 
 INT8_KERNELS = ("proj", "fused_a", "fused_b")
+
+
+def measured_traffic(cfg, kernel):
+    """DRAM bytes per launch (read + write) of ``kernel`` from the committed ncu capture of
+    this config (profiles/*/traffic.json, tools/traffic_json.py), or None."""
+    pdir = os.path.join(ROOT, "profiles")
+    try:
+        tags = sorted(d for d in os.listdir(pdir) if os.path.isdir(os.path.join(pdir, d)))
+    except OSError:
+        return None
+    for tag in reversed(tags):
+        try:
+            with open(os.path.join(pdir, tag, "traffic.json")) as f:
+                d = json.load(f)
+            ent = d.get(cfg, {}).get(kernel)
+            if ent:
+                return {"bytes_per_launch": ent["bytes_per_launch"],
+                        "source": f"profiles/{tag}/{ent['source']} (ncu, cold cache)"}
+        except (OSError, ValueError):
+            continue
+    return None
 FP32_PEAK_TFLOPS = 72.5  # FFMA/FFMA2 microbenchmark on this pool's B200 (tools/fp_microbench.cu)
 
 
@@ -384,8 +405,12 @@ def main():
         else:
             roof = {"kernel": names[dom], "bound": "hbm", "achieved": e["hbm_gbs"],
                     "peak": hbm_peak, "unit": "GB/s", "frac": e["hbm_frac"]}
+        tr = measured_traffic(args.config, dom)
         roof.update({"peak_source": peak_kind + (" (int8 = 2x bf16)" if dom in INT8_KERNELS else ""),
-                     "traffic": None, "kernel_ms_per_step": e["ms_per_step"],
+                     "traffic": (tr or {}).get("bytes_per_launch"),
+                     "traffic_unit": "bytes per launch (DRAM read + write)",
+                     "traffic_source": (tr or {}).get("source"),
+                     "kernel_ms_per_step": e["ms_per_step"],
                      "share_of_step": e["share_of_step"]})
 
     # ---- CPU baseline (rank 0, N=1 only) ----

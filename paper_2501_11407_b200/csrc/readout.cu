@@ -63,22 +63,36 @@ __global__ void readout_loss_kernel(const double* __restrict__ wout, const doubl
   }
 }
 
-__global__ void readout_grad_kernel(const double* __restrict__ g, const double* __restrict__ zsum,
-                                    int B, int n, int m, double* __restrict__ gwo) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// gwo[c][i] = sum_b g[b][c] zsum[b][i]: block = 32 neurons x 8 batch slices (contiguous
+// sample ranges), each slice summed in order, the 8 slice sums added in slice order --
+// deterministic, and 8x the parallelism of one thread per (c, i).
+constexpr int RG_SLICES = 8;
+__global__ void __launch_bounds__(32 * RG_SLICES) readout_grad_kernel(
+    const double* __restrict__ g, const double* __restrict__ zsum, int B, int n, int m,
+    double* __restrict__ gwo) {
+  __shared__ double part[RG_SLICES][33];
+  const int lane = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
   const int c = blockIdx.y;
-  if (i >= n) return;
-  // four interleaved accumulators (fixed order) to break the fp64 FMA dependency chain
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  int b = 0;
-  for (; b + 3 < B; b += 4) {
-    a0 = fma(g[(long long)b * m + c], zsum[(long long)b * n + i], a0);
-    a1 = fma(g[(long long)(b + 1) * m + c], zsum[(long long)(b + 1) * n + i], a1);
-    a2 = fma(g[(long long)(b + 2) * m + c], zsum[(long long)(b + 2) * n + i], a2);
-    a3 = fma(g[(long long)(b + 3) * m + c], zsum[(long long)(b + 3) * n + i], a3);
+  const int per = (B + RG_SLICES - 1) / RG_SLICES;
+  const int b0 = sl * per, b1 = min(B, b0 + per);
+  double a0 = 0.0, a1 = 0.0;
+  if (i < n) {
+    int b = b0;
+    for (; b + 1 < b1; b += 2) {
+      a0 = fma(g[(long long)b * m + c], zsum[(long long)b * n + i], a0);
+      a1 = fma(g[(long long)(b + 1) * m + c], zsum[(long long)(b + 1) * n + i], a1);
+    }
+    if (b < b1) a0 = fma(g[(long long)b * m + c], zsum[(long long)b * n + i], a0);
   }
-  for (; b < B; ++b) a0 = fma(g[(long long)b * m + c], zsum[(long long)b * n + i], a0);
-  gwo[(long long)c * n + i] = (a0 + a1) + (a2 + a3);
+  part[sl][lane] = a0 + a1;
+  __syncthreads();
+  if (sl == 0 && i < n) {
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < RG_SLICES; ++q) acc += part[q][lane];
+    gwo[(long long)c * n + i] = acc;
+  }
 }
 
 template <typename OT>
@@ -113,8 +127,8 @@ int spb_readout_grad(const double* g, const double* zsum, int B, int n, int m, d
                      cudaStream_t stream) {
   SPB_CHECK_ARG(g && zsum && gwo, "spb_readout_grad: null pointer");
   SPB_CHECK_ARG(B > 0 && n > 0 && m > 0, "spb_readout_grad: bad sizes");
-  dim3 grid(ceil_div(n, 128), m);
-  readout_grad_kernel<<<grid, 128, 0, stream>>>(g, zsum, B, n, m, gwo);
+  dim3 grid(ceil_div(n, 32), m);
+  readout_grad_kernel<<<grid, 32 * RG_SLICES, 0, stream>>>(g, zsum, B, n, m, gwo);
   SPB_CHECK_LAUNCH("readout_grad");
   return 0;
 }

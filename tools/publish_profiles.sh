@@ -18,4 +18,6 @@ for r in $S/ncu_*.ncu-rep; do
   b=$(basename $r .ncu-rep)
   { python tools/ncu_summary.py $r; python tools/ncu_hotspots.py $r 20; } > $D/$b.summary.txt 2>&1
 done
+
+python tools/traffic_json.py $S > $D/traffic.json
 ls -la $D
