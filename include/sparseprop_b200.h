@@ -57,6 +57,12 @@ int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits
                     int Kpad, int time_major, uint8_t* xq, cudaStream_t stream);
 int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
                    int Kpad, int P, double* cur, int sm_count, int binary, cudaStream_t stream);
+/* K2 on CTA pairs (proj2.cu): the same exact projection with tcgen05.mma.cta_group::2 --
+ *   each CTA of a 2-CTA cluster supplies its 128 spike rows and half of the weight digits
+ *   (P even: 6 or 8; Kpad <= 768); same output bits as spb_input_proj. */
+int spb_input_proj_pair(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
+                        int n_pad32, int Kpad, int P, double* cur, int sm_count, int binary,
+                        cudaStream_t stream);
 /* Profiling variant of spb_input_proj (W-resident kernel): probe bit 0 skips the epilogue,
  * bit 1 the spike-operand loads; probe = 0 is the production kernel. */
 int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,

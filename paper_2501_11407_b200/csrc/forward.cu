@@ -187,10 +187,12 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
   const float beta = (float)P.beta, rho = (float)P.rho;
   const bool carry = P.alif && w_hi != nullptr;
   const float* prow = psis + (long long)b * (P.KR + 1) * P.n + i;
+  const bool even_n = (P.n & 1) == 0;  // float2 rows are 8-byte aligned only for even n
   auto ldpsi = [&](int r) -> float2 {
     if (r < 0) return make_float2(0.f, 0.f);
-    return has2 ? *reinterpret_cast<const float2*>(prow + (long long)r * P.n)
-                : make_float2(prow[(long long)r * P.n], 0.f);
+    const float* q = prow + (long long)r * P.n;
+    if (has2 && even_n) return *reinterpret_cast<const float2*>(q);
+    return make_float2(q[0], has2 ? q[1] : 0.f);
   };
   const long long ld2 = ldc >> 1;  // row stride in bf16x2 words
   uint32_t* chp = c_hi + (long long)b * P.KR * ld2 + (i >> 1);
@@ -292,10 +294,12 @@ __global__ void __launch_bounds__(K1S_THREADS) reset_scan_kernel(
               rho = (float)P.rho;
   const bool carry = w_hi != nullptr;
   const float* prow = psis + (long long)b * (P.KR + 1) * P.n + i;
+  const bool even_n = (P.n & 1) == 0;  // float2 rows are 8-byte aligned only for even n
   auto ldpsi = [&](int r) -> float2 {
     if (r < 0) return make_float2(0.f, 0.f);
-    return has2 ? *reinterpret_cast<const float2*>(prow + (long long)r * P.n)
-                : make_float2(prow[(long long)r * P.n], 0.f);
+    const float* q = prow + (long long)r * P.n;
+    if (has2 && even_n) return *reinterpret_cast<const float2*>(q);
+    return make_float2(q[0], has2 ? q[1] : 0.f);
   };
   const long long ld2 = ldc >> 1;
   const long long base = (long long)b * P.KR * ld2 + (i >> 1);

@@ -25,6 +25,7 @@
 // owner + tcgen05.mma.kind::i8 issuer (double-buffered accumulators).  Warps 2..: epilogue,
 // thread = (sample row, 4 neurons).
 #include "tma.cuh"
+#include "digits.cuh"
 
 namespace spb {
 namespace fused {
@@ -278,12 +279,11 @@ __global__ void __launch_bounds__(Cfg<P, NT, XS>::THREADS, 1)
 #pragma unroll
         for (int c = 0; c < NPT; ++c) {
           // exact recombination of the digit sums (as proj_epilogue_tile)
-          const long long g0 = ((long long)dg[0][c] * 128 + dg[1][c]) * 128 + dg[2][c];
+          const long long g0 = digits_g0<P>(dg[0][c], dg[1][c], dg[2][c]);
           long long g1 = dg[3][c];
 #pragma unroll
-          for (int p = 4; p < P; ++p) g1 = g1 * 128 + dg[p][c];
-          const double I = fma((double)g0, pow2(se[c] - 20),
-                               (double)g1 * pow2(se[c] - 6 - 7 * (P - 1)));
+          for (int p = 4; p < P; ++p) g1 = (g1 << Digits<P>::RB) + dg[p][c];
+          const double I = digits_current<P, false>(g0, g1, se[c]);
           // gradients.py:121-129 (LIF: beta = rho = 0, so d = u - theta exactly)
           const double z_prev = spike_value(dp[c], smooth, slope);
           if (ALIF) as[c] = __dadd_rn(__dmul_rn(F.rho, as[c]), z_prev);
@@ -389,7 +389,7 @@ int spb_fused_forward_probe(int pass, const uint8_t* xq, const int8_t* wq, const
   SPB_CHECK_ARG(pass == 1 || (zbar && zsum), "spb_fused_forward: pass A needs zbar/zsum");
   SPB_CHECK_ARG(pass == 0 || psi_scratch, "spb_fused_forward: pass B needs psi_scratch");
   SPB_CHECK_ARG(B > 0 && n > 0 && n_pad32 >= n && n_pad32 % 32 == 0 && Kpad % fused::BK == 0 &&
-                    Kpad / fused::BK <= fused::MAXKB && (P == 7 || P == 8) && len >= 1 &&
+                    Kpad / fused::BK <= fused::MAXKB && (P >= 6 && P <= 8) && len >= 1 &&
                     len <= Tc && KR >= Tc + 1 && t0 >= 0 && t0 + len <= T,
                 "spb_fused_forward: bad sizes (Kpad <= %d, P in {7,8})", fused::MAXKB * fused::BK);
   SPB_CHECK_ARG((reinterpret_cast<uintptr_t>(xq) | reinterpret_cast<uintptr_t>(wq)) % 16 == 0,
@@ -414,10 +414,14 @@ int spb_fused_forward_probe(int pass, const uint8_t* xq, const int8_t* wq, const
     fused::launch<8, 16, 7, true>(mx, mw, sexp, F, u, a, zbar, zsum, raster, psi_scratch, grid, stream);
   else if (P == 8)
     fused::launch<8, 16, 7, false>(mx, mw, sexp, F, u, a, zbar, zsum, raster, psi_scratch, grid, stream);
-  else if (alif)
+  else if (P == 7 && alif)
     fused::launch<7, 16, 8, true>(mx, mw, sexp, F, u, a, zbar, zsum, raster, psi_scratch, grid, stream);
-  else
+  else if (P == 7)
     fused::launch<7, 16, 8, false>(mx, mw, sexp, F, u, a, zbar, zsum, raster, psi_scratch, grid, stream);
+  else if (alif)
+    fused::launch<6, 16, 8, true>(mx, mw, sexp, F, u, a, zbar, zsum, raster, psi_scratch, grid, stream);
+  else
+    fused::launch<6, 16, 8, false>(mx, mw, sexp, F, u, a, zbar, zsum, raster, psi_scratch, grid, stream);
   SPB_CHECK_LAUNCH("fused_forward");
   return 0;
 }

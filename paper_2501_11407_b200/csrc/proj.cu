@@ -20,6 +20,7 @@
 //   spb_slice_weights    W [n][k] fp32/fp64  -> Wq [P][n_pad32][Kpad] int8, s [n] int32
 //   spb_input_proj       persistent warp-specialised tcgen05 GEMM -> I [B*Tc][n] fp64
 #include "tma.cuh"
+#include "digits.cuh"
 
 namespace spb {
 namespace proj {
@@ -124,8 +125,7 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&s
     for (int p = 0; p < 3; ++p) tmem_ld16_nowait(tbase + p * NT, r[p]);
     tmem_wait_ld();
 #pragma unroll
-    for (int c = 0; c < NH; ++c)
-      g0[c] = ((long long)r[0][c] * 128 + r[1][c]) * 128 + r[2][c];
+    for (int c = 0; c < NH; ++c) g0[c] = digits_g0<P>(r[0][c], r[1][c], r[2][c]);
   }
   {
     int32_t r[P - 3][NH];
@@ -136,7 +136,7 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&s
     for (int c = 0; c < NH; ++c) {
       long long v = r[0][c];
 #pragma unroll
-      for (int p = 1; p < P - 3; ++p) v = v * 128 + r[p][c];
+      for (int p = 1; p < P - 3; ++p) v = (v << Digits<P>::RB) + r[p][c];
       g1[c] = v;
     }
   }
@@ -150,16 +150,7 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&s
   for (int c = 0; c < NH; c += 2) {
     double v[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if constexpr (BIN && P == 7) {
-        const long long g = (g0[c + h] << 28) + g1[c + h];
-        v[h] = (double)g * pow2(se[c + h] - 48);
-      } else {
-        // I = g0 * 2^(s-6-14) + g1 * 2^(s-6-7(P-1))  (both conversions exact)
-        v[h] = fma((double)g0[c + h], pow2(se[c + h] - 20),
-                   (double)g1[c + h] * pow2(se[c + h] - 6 - 7 * (P - 1)));
-      }
-    }
+    for (int h = 0; h < 2; ++h) v[h] = digits_current<P, BIN>(g0[c + h], g1[c + h], se[c + h]);
     ch[c / 2] = make_double2(v[0], v[1]);
   }
   if (probe & 4) {  // profiling probe: no global stores
@@ -191,10 +182,11 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&s
     const int r = row0 + k;
     if (r < M) {
       double* o = out + (long long)r * n + col;
-      if (col + 1 < n) {
+      if (col + 1 < n && (n & 1) == 0) {  // 16-byte aligned rows
         *reinterpret_cast<double2*>(o) = ch[k];
-      } else if (col < n) {
-        o[0] = ch[k].x;
+      } else {
+        if (col < n) o[0] = ch[k].x;
+        if (col + 1 < n) o[1] = ch[k].y;
       }
     }
   }
@@ -533,12 +525,24 @@ __global__ void slice_weights_kernel(const WT* __restrict__ w, int n, int k, int
   if (mx > 0.0) frexp(mx, &s);  // mx = f * 2^s, f in [0.5, 1)  =>  |w| < 2^s
   if (lane == 0 && i < n) sexp[i] = s;
   for (int j = lane; j < Kpad; j += 32) {
-    double r = (i < n && j < k) ? ldexp((double)w[(long long)i * k + j], -s) : 0.0;
-    for (int p = 0; p < P; ++p) {
-      const double t = r * (p == 0 ? 64.0 : 128.0);
-      const double qv = rint(t);
-      r = t - qv;
-      wq[((long long)p * n_pad32 + i) * Kpad + j] = (int8_t)(int)qv;
+    const double wv = (i < n && j < k) ? (double)w[(long long)i * k + j] : 0.0;
+    if (P == 6) {
+      // balanced radix-256 digits of R = rint(w 2^(46-s)), |R| < 2^46, least significant
+      // first: q = ((R + 128) mod 256) - 128 in [-128, 127], R <- (R - q) / 256 (exact)
+      long long R = (long long)rint(ldexp(wv, 46 - s));
+      for (int p = P - 1; p >= 0; --p) {
+        const long long q = ((R + 128) & 255) - 128;
+        R = (R - q) >> 8;
+        wq[((long long)p * n_pad32 + i) * Kpad + j] = (int8_t)q;
+      }
+    } else {
+      double r = ldexp(wv, -s);
+      for (int p = 0; p < P; ++p) {
+        const double t = r * (p == 0 ? 64.0 : 128.0);
+        const double qv = rint(t);
+        r = t - qv;
+        wq[((long long)p * n_pad32 + i) * Kpad + j] = (int8_t)(int)qv;
+      }
     }
   }
 }
@@ -567,7 +571,7 @@ int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits
 int spb_slice_weights(const void* w, int w_is_f64, int n, int k, int Kpad, int n_pad32, int P,
                       int8_t* wq, int* sexp, cudaStream_t stream) {
   SPB_CHECK_ARG(w && wq && sexp && n > 0 && k > 0 && Kpad >= k && n_pad32 >= n &&
-                    n_pad32 % proj::NT == 0 && (P == 7 || P == 8),
+                    n_pad32 % proj::NT == 0 && (P == 6 || P == 7 || P == 8),
                 "spb_slice_weights: bad args");
   const int blocks = ceil_div(n_pad32 * 32, 256);
   if (w_is_f64)
@@ -595,9 +599,9 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
 int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
                          int n_pad32, int Kpad, int P, double* out, int sm_count, int binary,
                          int probe, cudaStream_t stream) {
-  const bool bin = binary != 0 && P == 7 && Kpad <= 16384;
+  const bool bin = binary != 0 && P <= 7 && Kpad <= 8192;
   SPB_CHECK_ARG(xq && wq && sexp && out && M > 0 && n > 0 && n_pad32 >= n &&
-                    n_pad32 % proj::NT == 0 && Kpad % proj::BK == 0 && (P == 7 || P == 8),
+                    n_pad32 % proj::NT == 0 && Kpad % proj::BK == 0 && (P == 6 || P == 7 || P == 8),
                 "spb_input_proj: bad args");
   SPB_CHECK_ARG((reinterpret_cast<uintptr_t>(xq) | reinterpret_cast<uintptr_t>(wq)) % 16 == 0,
                 "spb_input_proj: operands must be 16-byte aligned");
@@ -615,7 +619,12 @@ int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, i
   const int grid = max(1, min(tiles, sm_count > 0 ? sm_count : 148));
   const int nkb = Kpad / proj::BK;
   if (nkb <= proj::ResCfg<7, 3>::MAXKB) {  // weights of a neuron tile fit in shared memory
-    if (P == 7) {
+    if (P == 6) {
+      auto kfn = bin ? proj::input_proj_wres_kernel<6, 5, true> : proj::input_proj_wres_kernel<6, 5, false>;
+      constexpr int sm = proj::ResCfg<6, 5>::SMEM;
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      kfn<<<grid, proj::THREADS, sm, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
+    } else if (P == 7) {
       auto kfn = bin ? proj::input_proj_wres_kernel<7, 3, true> : proj::input_proj_wres_kernel<7, 3, false>;
       constexpr int sm = proj::ResCfg<7, 3>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -626,6 +635,10 @@ int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, i
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       kfn<<<grid, proj::THREADS, sm, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
     }
+  } else if (P == 6) {
+    auto kfn = bin ? proj::input_proj_kernel<6, true> : proj::input_proj_kernel<6, false>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, proj::Cfg<6>::SMEM);
+    kfn<<<grid, proj::THREADS, proj::Cfg<6>::SMEM, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);
   } else if (P == 7) {
     auto kfn = bin ? proj::input_proj_kernel<7, true> : proj::input_proj_kernel<7, false>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, proj::Cfg<7>::SMEM);

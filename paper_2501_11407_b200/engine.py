@@ -107,7 +107,8 @@ class EpropEngine:
 
     def __init__(self, n: int, k: int, m: int, B: int, *, alif: bool, w_f64: bool = False,
                  chunk: int = 127, device=None, sm_count: int | None = None,
-                 reset: bool = False, fused: bool | None = None, recurrent: bool = False):
+                 reset: bool = False, fused: bool | None = None, recurrent: bool = False,
+                 pair: bool | None = None):
         if chunk not in CHUNKS:
             raise ValueError(f"chunk must be one of {CHUNKS} (Tc + 1 a multiple of 64)")
         self.lib = _lib.load()
@@ -144,7 +145,13 @@ class EpropEngine:
         # K2 exact INT8 tensor-core projection: x chunk operand, sliced weights, current
         self.Kpad = _round_up(k, 128)
         self.n_pad32 = _round_up(n, 32)
-        self.P = 8 if self.w_f64 else 7
+        self.P = 8 if self.w_f64 else 6   # digit format, csrc/digits.cuh
+        # K2 on CTA pairs (proj2.cu, cta_group::2): bitwise the single-CTA K2; opt-in --
+        # measured slower at C3 (0.347 vs 0.301 ms): the MMA issue loop, not the shared-
+        # memory operand port, bounds K2 (tools/proj_probe.py, tools/mma_pattern_bench.cu)
+        self.pair = False if pair is None else bool(pair)
+        if self.pair and self.Kpad > 768:
+            raise ValueError("the CTA-pair projection needs k <= 768")
         # K21 (fused.cu) = K2 + K1 in one kernel: the fp64 current never leaves the SM
         # (needs Kpad <= 768).  Opt-in: measured on B200 it is bitwise identical to K2 + K1
         # but not faster at C3/C4 (its N = 112 MMAs keep the tensor pipe ~26 % busy and the
@@ -292,9 +299,10 @@ class EpropEngine:
         """K2: cur = W x_t exactly on INT8 tensor cores from the packed chunk (binary:
         0/1 spikes, single-int64 digit recombination)."""
         v = ctypes_void
-        args = ("spb_input_proj", v(self.xq.data_ptr()), v(self.wq.data_ptr()),
-                v(self.sexp.data_ptr()), self.B * self.Tc, self.n, self.n_pad32, self.Kpad,
-                self.P, v(self.cur.data_ptr()), self.sm_count, int(bool(binary)), st)
+        args = ("spb_input_proj_pair" if self.pair else "spb_input_proj", v(self.xq.data_ptr()),
+                v(self.wq.data_ptr()), v(self.sexp.data_ptr()), self.B * self.Tc, self.n,
+                self.n_pad32, self.Kpad, self.P, v(self.cur.data_ptr()), self.sm_count,
+                int(bool(binary)), st)
         if timed is not None:
             timed("proj", ln, *args)
         else:

@@ -1,0 +1,116 @@
+// Microbenchmark of tcgen05 kind::i8 issue patterns at the K2 shape (M=128, N=192, K=32B):
+//   mode 0: back-to-back MMAs, fixed descriptors
+//   mode 1: descriptors walk 5 smem stages x 4 K-steps (distinct addresses, like K2)
+//   mode 2: mode 1 + tcgen05.commit to an mbarrier after every 4 MMAs (no waits)
+//   mode 3: mode 2 + a producer thread that waits each stage's commit and re-arms a "full"
+//           barrier the MMA thread waits on (the K2 ring without TMA), depth 5
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_pattern_bench tools/mma_pattern_bench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+__device__ __forceinline__ void mbar_init(uint32_t b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(c));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile("{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(bar), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+constexpr int XS = 5;
+__global__ void __launch_bounds__(128, 1) bench(int mode, int stages_total, unsigned long long* cyc, int N) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[XS], empty[XS], done;
+  __shared__ uint32_t slot;
+  const int tid = threadIdx.x;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+  for (int i = tid; i < 180 * 1024; i += blockDim.x) base[i] = 0;
+  if (tid == 0) {
+    for (int s = 0; s < XS; ++s) { mbar_init(su32(&full[s]), 1); mbar_init(su32(&empty[s]), 1); }
+    mbar_init(su32(&done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = slot;
+  const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const uint32_t xa0 = su32(base), wa0 = su32(base + XS * 16384);
+  if (tid == 0) {
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < stages_total; ++it) {
+      const int s = it % XS;
+      if (mode == 3) mbar_wait(su32(&full[s]), (it / XS) & 1);
+      const uint32_t xa = (mode == 0) ? xa0 : xa0 + s * 16384;
+      const uint32_t wa = (mode == 0) ? wa0 : wa0 + (it % 4) * (N * 128);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t off = (mode == 0) ? 0 : kk * 32;
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                     "l"(desc_k_sw128(xa + off)), "l"(desc_k_sw128(wa + off)), "r"(idesc), "r"(it | kk));
+      }
+      if (mode >= 2) commit(su32(&empty[s]));
+    }
+    commit(su32(&done));
+    mbar_wait(su32(&done), 0);
+    cyc[blockIdx.x] = clock64() - t0;
+  } else if (tid == 32 && mode == 3) {
+    for (int it = 0; it < stages_total; ++it) {
+      const int s = it % XS;
+      if (it >= XS) mbar_wait(su32(&empty[s]), ((it / XS) - 1) & 1);
+      arrive(su32(&full[s]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  unsigned long long* d;
+  cudaMalloc(&d, sms * sizeof(unsigned long long));
+  const int smem = 180 * 1024 + 1024;
+  cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int stages = 4000;
+  for (int N : {128, 192, 224, 256}) for (int mode = 0; mode < 4; ++mode) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float ms = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0);
+      bench<<<sms, 128, smem>>>(mode, stages, d, N);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+    }
+    unsigned long long c0 = 0;
+    cudaMemcpy(&c0, d, 8, cudaMemcpyDeviceToHost);
+    const double ops = 2.0 * 128 * N * 32 * 4.0 * stages * sms;
+    printf("N=%d mode %d: %.1f cyc/MMA, %.0f TOPS  err=%s\n", N, mode, (double)c0 / (4.0 * stages),
+           ops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}
