@@ -191,6 +191,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="eager launches instead of replaying the captured CUDA graph")
     ap.add_argument("--recurrent", action="store_true",
                     help="recurrent W_rec extension (SURVEY.md 8(f)-4) on the chosen shape")
     ap.add_argument("--profile", action="store_true",
@@ -252,6 +254,27 @@ def main():
         step(xd, yd)
     barrier()
 
+    # The whole update (every kernel, the side-stream fork/join, the gradient packing and
+    # the allreduce) is captured once in a CUDA graph and replayed per step: no host
+    # launch gaps on the device timeline.  Falls back to eager launches if capture fails.
+    graph = None
+    if args.graph and not args.profile:
+        try:
+            cs_ = torch.cuda.Stream(device=dev)
+            cs_.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(cs_):
+                step(xd, yd)                     # warm the capture stream
+            torch.cuda.current_stream(dev).wait_stream(cs_)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=cs_):
+                step(xd, yd)
+            graph.replay()
+            barrier()
+        except Exception as exc:  # noqa: BLE001
+            print(f"[bench] CUDA graph capture failed ({exc}); eager launches", file=sys.stderr)
+            graph = None
+            barrier()
+
     clocks = ClockSampler(local) if not args.profile else None
     if clocks:
         clocks.start()
@@ -263,13 +286,23 @@ def main():
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record()
-        step(xd, yd, timers=timers)
+        if graph is not None:
+            graph.replay()
+        else:
+            step(xd, yd, timers=timers)
         ev[i][1].record()
     barrier()
     launches_per_step = eng.launches  # kernels of libsparseprop_b200.so per step
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
     clk = clocks.stop() if clocks else None
+    if graph is not None:  # per-kernel breakdown from eager steps (events per launch)
+        n_bd = max(3, min(args.steps, 10))
+        for _ in range(n_bd):
+            flush.zero_()
+            step(xd, yd, timers=timers)
+        barrier()
+    steps_bd = n_bd if graph is not None else args.steps
 
     # kernel breakdown (CUDA events on the launching stream)
     kern = {}
@@ -378,8 +411,8 @@ def main():
                 if stv:
                     byts += 4.0 * (n + k) * B * KR
                     flops += 6.0 * n * k * B * KR
-        ent = {"ms_per_step": t_tot * 1e3 / args.steps, "share_of_step": t_tot * 1e3 / args.steps / ms,
-               "launches_per_step": len(lst) / args.steps}
+        ent = {"ms_per_step": t_tot * 1e3 / steps_bd, "share_of_step": t_tot * 1e3 / steps_bd / ms,
+               "launches_per_step": len(lst) / steps_bd}
         if byts:
             ent["hbm_gbs"] = byts / t_tot / 1e9
             ent["hbm_frac"] = ent["hbm_gbs"] / hbm_peak
@@ -438,7 +471,9 @@ def main():
                        "n_classes": m, "chunk": eng.Tc, "parallelism": f"dp{world}",
                        "forward_precision": "fp64 state/current (bit-exact spikes)",
                        "forward_kernel": "K21 fused projection+dynamics" if eng.fused else "K2 projection + K1 dynamics",
-                       "l2": "512 MiB flush between timed steps (outside events)"},
+                       "l2": "512 MiB flush between timed steps (outside events)",
+                       "launch": "CUDA graph replay of the whole update" if graph is not None
+                                 else "eager launches"},
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roof,
