@@ -557,6 +557,35 @@ class EpropEngine:
             main.wait_event(self._ev["rg"])
         return self
 
+    def graphed(self, x_like: torch.Tensor, labels_like: torch.Tensor, **run_kwargs):
+        """Capture one update on static device buffers shaped like ``x_like`` /
+        ``labels_like`` into a CUDA graph; returns ``step(x, labels)`` that copies the batch
+        into the static buffers and replays the graph (no per-kernel host launches).  The
+        results land in the engine's buffers as with ``run``."""
+        if self.device.type != "cuda":
+            raise ValueError("CUDA graphs need a CUDA engine")
+        xs = torch.empty_like(x_like, device=self.device)
+        ls = torch.empty_like(labels_like, device=self.device)
+        xs.copy_(x_like)
+        ls.copy_(labels_like)
+        cs = torch.cuda.Stream(device=self.device)
+        cs.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(cs):
+            self.run(xs, ls, **run_kwargs)       # first launches (attributes, descriptors)
+        torch.cuda.current_stream(self.device).wait_stream(cs)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cs):
+            self.run(xs, ls, **run_kwargs)
+
+        def step(x, labels):
+            xs.copy_(x, non_blocking=True)
+            ls.copy_(labels, non_blocking=True)
+            graph.replay()
+            return self
+
+        step.graph = graph
+        return step
+
     def _stream_buffers(self, kb):
         """Double-buffered device chunk of the input + copy stream (streaming mode)."""
         if getattr(self, "_xs", None) is None or self._xs.shape[-1] != kb:

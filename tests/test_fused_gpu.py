@@ -96,3 +96,31 @@ def test_fused_ragged_many_chunks(kind, reset, smooth, wdt, bits):
         _, _, ras = O.network_loss(w64, wo64, p, x[b].astype(np.float64), int(y[b]),
                                    smooth=smooth)
         assert np.array_equal(fu[0][b], ras)
+
+
+def test_graphed_update_equals_eager():
+    """EpropEngine.graphed: the captured CUDA graph replays the same update bit for bit."""
+    _need_gpu()
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200.gradients import _neuron_kwargs
+    net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=200, n_inputs=90, n_classes=5,
+                                       precision="f32", seed=4))
+    kw = _neuron_kwargs(net)
+    eng = EpropEngine(200, 90, 5, 12, alif=True, chunk=63)
+    eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+    outs = []
+    for seed in (1, 2):
+        x, y = poisson_batch(12, 90, 150, 5, seed=seed)
+        xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        eng.run(xd, yd, **kw)
+        torch.cuda.synchronize()
+        outs.append((eng.grad_w_acc.cpu().numpy().copy(), eng.loss.cpu().numpy().copy()))
+    step = eng.graphed(xd, yd, **kw)
+    for seed, (gw, ls) in zip((1, 2), outs):
+        x, y = poisson_batch(12, 90, 150, 5, seed=seed)
+        step(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+        torch.cuda.synchronize()
+        assert np.array_equal(eng.grad_w_acc.cpu().numpy(), gw)
+        assert np.array_equal(eng.loss.cpu().numpy(), ls)
