@@ -431,6 +431,8 @@ def main():
                  "forward_a": "forward_chunk_kernel (K1 pass A)",
                  "gemm": "grad_gemm_tc_kernel (K5, bf16x3 tcgen05)",
                  "carry": "alif_carry_kernel (K6, tcgen05 + eps stream)"}
+        if args.recurrent:
+            names["forward_a"] = "forward_rec_kernel (K1rec pass A: recurrent spike gather)"
         if e.get("tensor_frac", 0) >= e.get("hbm_frac", 0) and "tensor_tflops" in e:
             pk = 2 * bf16_peak if dom in INT8_KERNELS else bf16_peak
             roof = {"kernel": names[dom], "bound": "tensor", "achieved": e["tensor_tflops"],
@@ -438,7 +440,7 @@ def main():
         else:
             roof = {"kernel": names[dom], "bound": "hbm", "achieved": e["hbm_gbs"],
                     "peak": hbm_peak, "unit": "GB/s", "frac": e["hbm_frac"]}
-        tr = measured_traffic(args.config, dom)
+        tr = measured_traffic(args.config + ("_rec" if args.recurrent else ""), dom)
         roof.update({"peak_source": peak_kind + (" (int8 = 2x bf16)" if dom in INT8_KERNELS else ""),
                      "traffic": (tr or {}).get("bytes_per_launch"),
                      "traffic_unit": "bytes per launch (DRAM read + write)",

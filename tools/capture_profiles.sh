@@ -12,6 +12,9 @@ timeout 300 python bench.py --config c4 --no-cpu --steps 10 > $O/bench_c4.json 2
 timeout 300 python bench.py --config c2 --no-cpu --steps 20 > $O/bench_c2.json 2>&1
 timeout 300 python bench.py --config c5 --no-cpu --steps 5 > $O/bench_c5.json 2>&1
 timeout 300 python bench.py --impl reference --steps 3 > $O/bench_ref.json 2>&1
+timeout 300 python bench.py --recurrent --no-cpu --steps 5 > $O/bench_c3_recurrent.json 2>&1
+timeout 300 python tools/proj_probe.py > $O/proj_probe.txt 2>&1
+[ -x tools/mma_pattern_bench ] && ./tools/mma_pattern_bench > $O/mma_pattern_bench.txt 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $O/launches_c3.csv python bench.py --steps 2 --warmup 3 --profile > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
