@@ -86,15 +86,15 @@ __device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
 __device__ __forceinline__ void mma2_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                         uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 // arrive on the barrier at this offset in BOTH CTAs once the issued MMAs complete
 __device__ __forceinline__ void commit2(uint32_t bar) {
   asm volatile(
-      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      "{\n\t.reg .b16 m;\n\t.reg .pred e;\n\tmov.b16 m, 3;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
       " [%0], m;\n\t}" ::"r"(bar)
       : "memory");
 }
@@ -267,7 +267,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {  // whole warp, converged; elect.sync picks the issuer
       int it = 0, lt = 0, wl = 0, cur_nt = -1;
       for (int t = t_begin; t < t_end; ++t, ++lt) {
         const int nt = t / m2_tiles;

@@ -56,7 +56,27 @@ __global__ void __launch_bounds__(128, 1) bench(int mode, int stages_total, unsi
   const uint32_t tmem = slot;
   const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   const uint32_t xa0 = su32(base), wa0 = su32(base + XS * 16384);
-  if (tid == 0) {
+  if (mode == 4 && tid < 32) {
+    // warp-converged issue: every lane runs the loop, one elected lane issues (no R2UR /
+    // divergent-uniform loop around each tcgen05.mma)
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < stages_total; ++it) {
+      const int s = it % XS;
+      const uint32_t xa = xa0 + s * 16384;
+      const uint32_t wa = wa0 + (it % 4) * (N * 128);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "elect.sync _|e, 0xffffffff;\n\t"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                     "l"(desc_k_sw128(xa + kk * 32)), "l"(desc_k_sw128(wa + kk * 32)), "r"(idesc), "r"(it | kk));
+      }
+    }
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&done)) : "memory");
+    mbar_wait(su32(&done), 0);
+    if (tid == 0) cyc[blockIdx.x] = clock64() - t0;
+  } else if (tid == 0 && mode < 4) {
     const unsigned long long t0 = clock64();
     for (int it = 0; it < stages_total; ++it) {
       const int s = it % XS;
@@ -95,7 +115,7 @@ int main() {
   const int smem = 180 * 1024 + 1024;
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int stages = 4000;
-  for (int N : {128, 192, 224, 256}) for (int mode = 0; mode < 4; ++mode) {
+  for (int N : {128, 192}) for (int mode = 0; mode < 5; ++mode) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     float ms = 0;
