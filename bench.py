@@ -191,6 +191,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--microbatch", type=int, default=1,
+                    help="split the batch over this many concurrently streamed engines")
+    ap.add_argument("--mb-sms", type=int, default=0,
+                    help="SMs the persistent kernels of each micro-batch may occupy (0 = all)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="eager launches instead of replaying the captured CUDA graph")
     ap.add_argument("--recurrent", action="store_true",
@@ -225,8 +229,14 @@ def main():
     x_np, y_np = poisson_batch(B, k, T, m, seed=1000 + rank)
     from paper_2501_11407_b200.engine import default_chunk
     chunk = args.chunk or default_chunk(T, B, n, k, kind == "alif")
-    eng = EpropEngine(n, k, m, B, alif=kind == "alif", w_f64=False, chunk=chunk, device=dev,
-                      recurrent=args.recurrent)
+    if args.microbatch > 1:
+        from paper_2501_11407_b200.engine import MicroBatchEngine
+        eng = MicroBatchEngine(n, k, m, B, parts=args.microbatch, alif=kind == "alif",
+                               w_f64=False, chunk=chunk, device=dev, recurrent=args.recurrent,
+                               sm_count=args.mb_sms or None)
+    else:
+        eng = EpropEngine(n, k, m, B, alif=kind == "alif", w_f64=False, chunk=chunk,
+                          device=dev, recurrent=args.recurrent)
     eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out),
                     w_rec=torch.from_numpy(net.neuron.w_rec) if args.recurrent else None)
     xd = torch.from_numpy(x_np).to(dev)

@@ -637,3 +637,65 @@ class EpropEngine:
                   self.kp, ctypes_void(out.data_ptr()), int(dtype == torch.float64),
                   ctypes_void(self._stream()))
         return out
+
+
+class MicroBatchEngine:
+    """Two half-batch engines on two CUDA streams, so one half's HBM-bound kernels (K1,
+    the chunk scan) run while the other half's tensor-core kernels (K2, K5) run; the
+    gradient accumulators are added in a fixed order afterwards (deterministic).  Same
+    results as one engine over the whole batch up to the fp32 summation order of the
+    chunk GEMM's partials (each half's partials are reduced separately, in fp64).
+    Exposes the single engine's result buffers: grad_w_acc, grad_wout, loss, s, correct."""
+
+    def __init__(self, n, k, m, B, *, parts: int = 2, **kw):
+        if B < parts:
+            raise ValueError("batch smaller than the number of micro-batches")
+        dev = kw.get("device")
+        self.parts = int(parts)
+        base, extra = divmod(B, parts)
+        self.sizes = [base + (1 if i < extra else 0) for i in range(parts)]
+        self.engines = [EpropEngine(n, k, m, b, **kw) for b in self.sizes]
+        e0 = self.engines[0]
+        self.n, self.k, self.m, self.B = e0.n, e0.k, e0.m, int(B)
+        self.device, self.kp = e0.device, e0.kp
+        self.Tc, self.KR, self.P, self.fused = e0.Tc, e0.KR, e0.P, e0.fused
+        self.streams = [torch.cuda.Stream(device=self.device) for _ in range(parts)]
+        self.grad_w_acc = torch.empty_like(e0.grad_w_acc)
+        self.grad_wout = torch.empty_like(e0.grad_wout)
+        self.loss = torch.empty(B, dtype=e0.loss.dtype, device=self.device)
+        self.correct = torch.empty(B, dtype=e0.correct.dtype, device=self.device)
+        self.s = torch.empty((B, m), dtype=e0.s.dtype, device=self.device)
+        self.launches = 0
+
+    def set_weights(self, *a, **kw):
+        for e in self.engines:
+            e.set_weights(*a, **kw)
+
+    def run(self, x, labels, **kw):
+        main = torch.cuda.current_stream(self.device)
+        lo = 0
+        for e, st, b in zip(self.engines, self.streams, self.sizes):
+            st.wait_stream(main)
+            with torch.cuda.stream(st):
+                e.run(x[lo:lo + b], labels[lo:lo + b], **kw)
+            lo += b
+        for st in self.streams:
+            main.wait_stream(st)
+        # fixed-order combination (part 0 + part 1 + ...)
+        torch.add(self.engines[0].grad_w_acc, self.engines[1].grad_w_acc, out=self.grad_w_acc)
+        torch.add(self.engines[0].grad_wout, self.engines[1].grad_wout, out=self.grad_wout)
+        for e in self.engines[2:]:
+            self.grad_w_acc += e.grad_w_acc
+            self.grad_wout += e.grad_wout
+        torch.cat([e.loss for e in self.engines], out=self.loss)
+        torch.cat([e.correct for e in self.engines], out=self.correct)
+        torch.cat([e.s for e in self.engines], out=self.s)
+        self.launches = sum(e.launches for e in self.engines)
+        return self
+
+    def grad_w(self, dtype=torch.float32):
+        out = torch.empty((self.n, self.k), dtype=dtype, device=self.device)
+        _lib.call("spb_finalize_grad", ctypes_void(self.grad_w_acc.data_ptr()), self.n, self.k,
+                  self.kp, ctypes_void(out.data_ptr()), int(dtype == torch.float64),
+                  ctypes_void(torch.cuda.current_stream(self.device).cuda_stream))
+        return out

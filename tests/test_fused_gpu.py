@@ -124,3 +124,32 @@ def test_graphed_update_equals_eager():
         torch.cuda.synchronize()
         assert np.array_equal(eng.grad_w_acc.cpu().numpy(), gw)
         assert np.array_equal(eng.loss.cpu().numpy(), ls)
+
+
+@pytest.mark.parametrize("parts", [2, 3])
+def test_microbatch_engine_matches_single(parts):
+    """MicroBatchEngine (half batches on concurrent streams): losses/readouts bitwise, the
+    gradient up to the summation order of the per-part fp32 GEMM partials."""
+    _need_gpu()
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.engine import EpropEngine, MicroBatchEngine
+    from paper_2501_11407_b200.gradients import _neuron_kwargs
+    net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=150, n_inputs=80, n_classes=4,
+                                       precision="f32", seed=8))
+    kw = _neuron_kwargs(net)
+    x, y = poisson_batch(11, 80, 300, 4, seed=8)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    w, wo = torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out)
+    one = EpropEngine(150, 80, 4, 11, alif=True, chunk=127)
+    one.set_weights(w, wo)
+    one.run(xd, yd, **kw)
+    mb = MicroBatchEngine(150, 80, 4, 11, parts=parts, alif=True, chunk=127)
+    mb.set_weights(w, wo)
+    mb.run(xd, yd, **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(one.loss, mb.loss) and torch.equal(one.s, mb.s)
+    assert torch.equal(one.correct, mb.correct)
+    assert _rel(mb.grad_w(torch.float64).cpu().numpy(),
+                one.grad_w(torch.float64).cpu().numpy()) <= 1e-6
+    assert _rel(mb.grad_wout.cpu().numpy(), one.grad_wout.cpu().numpy()) <= 1e-12

@@ -76,6 +76,33 @@ __global__ void __launch_bounds__(128, 1) bench(int mode, int stages_total, unsi
                  "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&done)) : "memory");
     mbar_wait(su32(&done), 0);
     if (tid == 0) cyc[blockIdx.x] = clock64() - t0;
+  } else if (mode == 5 && tid < 32) {
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < stages_total; ++it) {
+      const int s = it % XS;
+      mbar_wait(su32(&full[s]), (it / XS) & 1);
+      const uint32_t xa = xa0 + s * 16384;
+      const uint32_t wa = wa0 + (it % 4) * (N * 128);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "elect.sync _|e, 0xffffffff;\n\t"
+                     "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                     "l"(desc_k_sw128(xa + kk * 32)), "l"(desc_k_sw128(wa + kk * 32)), "r"(idesc), "r"(it | kk));
+      }
+      asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                   "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&empty[s])) : "memory");
+    }
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&done)) : "memory");
+    mbar_wait(su32(&done), 0);
+    if (tid == 0) cyc[blockIdx.x] = clock64() - t0;
+  } else if (tid == 32 && mode == 5) {
+    for (int it = 0; it < stages_total; ++it) {
+      const int s = it % XS;
+      if (it >= XS) mbar_wait(su32(&empty[s]), ((it / XS) - 1) & 1);
+      arrive(su32(&full[s]));
+    }
   } else if (tid == 0 && mode < 4) {
     const unsigned long long t0 = clock64();
     for (int it = 0; it < stages_total; ++it) {
@@ -115,7 +142,7 @@ int main() {
   const int smem = 180 * 1024 + 1024;
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int stages = 4000;
-  for (int N : {128, 192}) for (int mode = 0; mode < 5; ++mode) {
+  for (int N : {128, 192}) for (int mode = 3; mode < 6; ++mode) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     float ms = 0;
