@@ -42,7 +42,7 @@ __device__ __forceinline__ double spike_value(double d, bool smooth, double slop
   return __dadd_rn(0.5, __ddiv_rn(d, __dadd_rn(1.0, __dmul_rn(slope, fabs(d)))));
 }
 
-constexpr int K1_THREADS = 128;  // 4 warps = 4 samples x 32 neurons
+constexpr int K1_THREADS = 128;  // 4 warps = 128 consecutive neurons of one sample
 
 // ------------------------------------------------------------------------------------
 // K1.  Warp = 32 consecutive neurons of one sample.  State u, a and the current are fp64
@@ -58,10 +58,13 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
     double* __restrict__ a_st, double* __restrict__ zbar_st, double* __restrict__ zsum_st,
     uint32_t* __restrict__ raster, const float* __restrict__ wsig, float* __restrict__ psis) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int i = blockIdx.x * 32 + lane;
+  // CTA = one sample x 128 consecutive neurons: every step it streams 1 KB of current
+  // and writes 512 B of psi contiguously (DRAM-friendly), warp = 32 neurons
+  const int wbase = blockIdx.x * K1_THREADS + warp * 32;
+  const int i = wbase + lane;
   const bool valid_i = i < P.n;
-  const int b = blockIdx.y * (K1_THREADS / 32) + warp;
-  if (b >= P.B) return;  // warp-uniform; no block-level barriers below
+  const int b = blockIdx.y;
+  if (wbase >= P.n) return;  // warp-uniform; no block-level barriers below
   const long long bi = (long long)b * P.n + i;
   double u = 0.0, a = 0.0, zbar = 0.0, zsum = 0.0;  // t0 == 0: fresh state (no read)
   if (valid_i && P.t0 > 0) {
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
           // raster = z > 0.5 (gradients.py:362)
           const unsigned bal = __ballot_sync(0xffffffffu, zv > 0.5 && valid_i);
           if (raster != nullptr && lane == 0)
-            raster[((long long)b * P.T + P.t0 + s) * nw + blockIdx.x] = bal;
+            raster[((long long)b * P.T + P.t0 + s) * nw + (wbase >> 5)] = bal;
         }
         // the surrogate only scales fp32 eligibilities: evaluate it in fp32
         if (park) prow[(long long)(s + 1) * P.n] = surrogate_grad_f32((float)d, slope);
@@ -144,7 +147,7 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
 // 128-byte coalesced stores per warp and row.  fp32 throughout (every output feeds the
 // fp32 / bf16-split gradient path).
 // ------------------------------------------------------------------------------------
-constexpr int K1S_THREADS = 128;  // 4 warps = 4 samples x 64 neurons
+constexpr int K1S_THREADS = 128;  // 4 warps = 256 consecutive neurons of one sample
 
 struct ScanLane {
   float lam = 0.f, dcum = 1.f, a_next = 0.f;
@@ -178,8 +181,8 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
   for (int r = threadIdx.x; r <= L; r += K1S_THREADS)
     cs[r] = (P.t0 + r - 1 >= 0) ? ctab[P.t0 + r - 1] : 0.f;
   __syncthreads();
-  const int i = blockIdx.x * 64 + 2 * lane;  // this thread's neurons i, i+1
-  const int b = blockIdx.y * (K1S_THREADS / 32) + warp;
+  const int i = blockIdx.x * 2 * K1S_THREADS + warp * 64 + 2 * lane;  // neurons i, i+1
+  const int b = blockIdx.y;
   if (b >= P.B || i >= P.n) return;
   const bool has2 = i + 1 < P.n;
   const long long bi = (long long)b * P.n + i;
@@ -283,8 +286,8 @@ __global__ void __launch_bounds__(K1S_THREADS) reset_scan_kernel(
   const int L = P.len;
   for (int r = threadIdx.x; r < L; r += K1S_THREADS) cs[r] = ctab[P.t0 + r];
   __syncthreads();
-  const int i = blockIdx.x * 64 + 2 * lane;
-  const int b = blockIdx.y * (K1S_THREADS / 32) + warp;
+  const int i = blockIdx.x * 2 * K1S_THREADS + warp * 64 + 2 * lane;
+  const int b = blockIdx.y;
   if (b >= P.B || i >= P.n) return;
   const bool has2 = i + 1 < P.n;
   const bool alif = P.alif != 0;
@@ -453,14 +456,14 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
                 "spb_forward_chunk: reset carry needs the coefficient buffer (mdt)");
   FwdParams P{B, n, Tc, KR, len, t0, T, alpha, theta, slope, beta, rho, kappa, reset, alif, pass,
               smooth};
-  dim3 grid(ceil_div(n, 32), ceil_div(B, K1_THREADS / 32));
+  dim3 grid(ceil_div(n, K1_THREADS), B);
   if (pass <= 1) {
     forward_chunk_kernel<<<grid, K1_THREADS, 0, stream>>>(P, cur, u, a, zbar, zsum, raster, wsig,
                                                           psi_scratch);
     SPB_CHECK_LAUNCH("forward_chunk");
   }
   if (pass >= 1 && reset) {
-    dim3 sgrid(ceil_div(n, 64), ceil_div(B, K1S_THREADS / 32));
+    dim3 sgrid(ceil_div(n, 2 * K1S_THREADS), B);
     reset_scan_kernel<<<sgrid, K1S_THREADS, (len > 0 ? len : 1) * sizeof(float), stream>>>(
         P, wsig, ctab, reinterpret_cast<uint32_t*>(c_hi), reinterpret_cast<uint32_t*>(c_lo),
         reinterpret_cast<uint32_t*>(w_hi), reinterpret_cast<uint32_t*>(w_lo),
@@ -468,7 +471,7 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
         psi_scratch);
     SPB_CHECK_LAUNCH("reset_scan");
   } else if (pass >= 1) {
-    dim3 sgrid(ceil_div(n, 64), ceil_div(B, K1S_THREADS / 32));
+    dim3 sgrid(ceil_div(n, 2 * K1S_THREADS), B);
     chunk_scan_kernel<<<sgrid, K1S_THREADS, (len + 1) * sizeof(float), stream>>>(
         P, wsig, ctab, reinterpret_cast<uint32_t*>(c_hi), reinterpret_cast<uint32_t*>(c_lo),
         reinterpret_cast<uint32_t*>(w_hi), reinterpret_cast<uint32_t*>(w_lo), ldc,

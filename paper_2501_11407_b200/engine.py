@@ -196,7 +196,8 @@ class EpropEngine:
         self.xl = torch.zeros((K, self.kp), dtype=bf16, device=dev)
         # split-K (K5) and sample-split (K6) partial slices, reduced in fixed order
         tiles5 = (self.kp // 128) * math.ceil(n / 128)
-        self.splits5 = max(1, min(K // 64, round(sms / tiles5)))
+        # split-K so the grid fills whole waves of SMs (C4: 96 tiles x 3 = 1.95 waves)
+        self.splits5 = _wave_split(tiles5, max(1, K // 64), sms)
         self.wa_hi = self.wa_lo = self.eps2 = None
         if self.ntr:
             self.w_hi = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
