@@ -268,7 +268,8 @@ def main():
     # the allreduce) is captured once in a CUDA graph and replayed per step: no host
     # launch gaps on the device timeline.  Falls back to eager launches if capture fails.
     graph = None
-    if args.graph and not args.profile:
+    # (single process only: the NCCL allreduce of a multi-rank step stays eager)
+    if args.graph and not args.profile and world == 1:
         try:
             cs_ = torch.cuda.Stream(device=dev)
             cs_.wait_stream(torch.cuda.current_stream(dev))
