@@ -195,6 +195,8 @@ def main():
                     help="split the batch over this many concurrently streamed engines")
     ap.add_argument("--mb-sms", type=int, default=0,
                     help="SMs the persistent kernels of each micro-batch may occupy (0 = all)")
+    ap.add_argument("--e2e-graph", action="store_true",
+                    help="replay a captured graph per step in the e2e loop too (measured no faster)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="eager launches instead of replaying the captured CUDA graph")
     ap.add_argument("--recurrent", action="store_true",
@@ -354,13 +356,30 @@ def main():
                 yb[i % 2].copy_(yh, non_blocking=True)
                 copied[i % 2].record(cs)
 
+        # one CUDA graph per input slot (EpropEngine.graphed on the double buffer itself)
+        gsteps = None
+        if args.e2e_graph and graph is not None and hasattr(eng, "graphed"):
+            try:
+                for i in range(2):
+                    xb[i].copy_(torch.from_numpy(x_bits).to(dev))
+                    yb[i].copy_(yd)
+                gsteps = [eng.graphed(xb[i], yb[i], static_inputs=True, bits=True, binary=True,
+                                      **kw) for i in range(2)]
+                barrier()
+            except Exception as exc:  # noqa: BLE001
+                print(f"[bench] e2e graph capture failed ({exc}); eager", file=sys.stderr)
+                gsteps = None
+
         def run_e2e(nsteps):
             prefetch(0)
             for i in range(nsteps):
                 if i + 1 < nsteps:
                     prefetch(i + 1)
                 main.wait_event(copied[i % 2])
-                step(xb[i % 2], yb[i % 2], bits=True)
+                if gsteps is not None:
+                    gsteps[i % 2]()
+                else:
+                    step(xb[i % 2], yb[i % 2], bits=True)
                 consumed[i % 2].record(main)
                 loss_h.copy_(eng.loss, non_blocking=True)
 
@@ -381,7 +400,9 @@ def main():
                "input_format": "bit-packed binary spikes (np.packbits, little), unpacked on device",
                "d2h_bytes_per_step": int(B * 8),
                "ms_per_step": float(e2e_ms.item()),
-               "pipeline": "H2D of step i+1 on a copy stream overlaps step i (double buffer)"}
+               "pipeline": "H2D of step i+1 on a copy stream overlaps step i (double buffer)"
+                           + ("; each step replays the update's CUDA graph (EpropEngine.graphed)"
+                              if gsteps is not None else "")}
 
     # ---- roofline of every main kernel; the dominant one is the headline ----
     hbm_peak, bf16_peak, peak_kind = peaks()

@@ -558,17 +558,23 @@ class EpropEngine:
             main.wait_event(self._ev["rg"])
         return self
 
-    def graphed(self, x_like: torch.Tensor, labels_like: torch.Tensor, **run_kwargs):
+    def graphed(self, x_like: torch.Tensor, labels_like: torch.Tensor, *,
+                static_inputs: bool = False, **run_kwargs):
         """Capture one update on static device buffers shaped like ``x_like`` /
         ``labels_like`` into a CUDA graph; returns ``step(x, labels)`` that copies the batch
-        into the static buffers and replays the graph (no per-kernel host launches).  The
+        into the static buffers and replays the graph (no per-kernel host launches).  With
+        ``static_inputs=True`` the given device tensors ARE the static buffers (the caller
+        refills them, e.g. by an async host-to-device copy; ``step()`` just replays).  The
         results land in the engine's buffers as with ``run``."""
         if self.device.type != "cuda":
             raise ValueError("CUDA graphs need a CUDA engine")
-        xs = torch.empty_like(x_like, device=self.device)
-        ls = torch.empty_like(labels_like, device=self.device)
-        xs.copy_(x_like)
-        ls.copy_(labels_like)
+        if static_inputs:
+            xs, ls = x_like, labels_like
+        else:
+            xs = torch.empty_like(x_like, device=self.device)
+            ls = torch.empty_like(labels_like, device=self.device)
+            xs.copy_(x_like)
+            ls.copy_(labels_like)
         cs = torch.cuda.Stream(device=self.device)
         cs.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(cs):
@@ -578,9 +584,11 @@ class EpropEngine:
         with torch.cuda.graph(graph, stream=cs):
             self.run(xs, ls, **run_kwargs)
 
-        def step(x, labels):
-            xs.copy_(x, non_blocking=True)
-            ls.copy_(labels, non_blocking=True)
+        def step(x=None, labels=None):
+            if x is not None:
+                xs.copy_(x, non_blocking=True)
+            if labels is not None:
+                ls.copy_(labels, non_blocking=True)
             graph.replay()
             return self
 
