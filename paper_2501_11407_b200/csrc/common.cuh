@@ -51,10 +51,14 @@ __device__ __forceinline__ double surrogate_grad_f64(double d, double slope) {
   return __ddiv_rn(1.0, __dmul_rn(t, t));
 }
 
-// Same surrogate in fp32 for the gradient path (psi only scales fp32 eligibilities).
+// Same surrogate in fp32 for the gradient path (psi only scales fp32 eligibilities):
+// 1/t^2 from the hardware reciprocal (MUFU.RCP, ~1 ulp; the IEEE-rounded __frcp_rn costs
+// a Newton fix-up sequence in the instruction-bound dynamics loop).
 __device__ __forceinline__ float surrogate_grad_f32(float d, float slope) {
   const float t = fmaf(slope, fabsf(d), 1.0f);
-  return __frcp_rn(t * t);
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t));
+  return r * r;
 }
 
 // bf16 hi/lo split of an fp32 value: x ~= hi + lo with |x - hi - lo| <= 2^-16 |x|.

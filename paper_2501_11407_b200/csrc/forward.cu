@@ -53,6 +53,10 @@ constexpr int K1_THREADS = 128;  // 4 warps = 128 consecutive neurons of one sam
 // kernel runs at full occupancy; the backward scan runs in fp32 (every quantity it
 // produces feeds the fp32 / bf16-split gradient path).
 // ------------------------------------------------------------------------------------
+// Templated on the per-launch flags so the per-step loop carries no flag branches and
+// walks its current / psi rows with pointer increments (the kernel is instruction-bound:
+// ~70 issued instructions per neuron-step before this specialisation).
+template <bool PASSA, bool PARK, bool RESET, bool SMOOTH>
 __global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
     FwdParams P, const double* __restrict__ cur, double* __restrict__ u_st,
     double* __restrict__ a_st, double* __restrict__ zbar_st, double* __restrict__ zsum_st,
@@ -70,61 +74,66 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
   if (valid_i && P.t0 > 0) {
     u = u_st[bi];
     a = a_st[bi];
-    if (P.pass == 0) {
+    if (PASSA) {
       zbar = zbar_st[bi];
       zsum = zsum_st[bi];
     }
   }
-  const double theta = P.theta, beta = P.beta;
-  const int nw = (P.n + 31) >> 5;
-  const double* crow = cur + (long long)b * P.Tc * P.n + i;
+  const double theta = P.theta, beta = P.beta, alpha = P.alpha, rho = P.rho, kappa = P.kappa;
+  const int n = P.n;
+  const int nw = (n + 31) >> 5;
+  // invalid lanes read a valid address (their own row start) and discard the value
+  const double* cp = cur + (long long)b * P.Tc * n + (valid_i ? i : wbase);
   // d_prev of step t is the drive d of step t-1 (the reference recomputes the same
   // expression from the same state, gradients.py:159): carry it.
   double d_prev = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
   const float slope = (float)P.slope;
   const double slope_d = P.slope;
-  const bool smooth = P.smooth != 0;
   // psi of row rho at prow[rho*n] (pass B; optional in pass A, which lets a one-chunk
   // sequence skip the pass-B dynamics entirely)
-  const bool park = psis != nullptr && valid_i;
-  float* prow = psis != nullptr ? psis + (long long)b * (P.KR + 1) * P.n + i : nullptr;
-  if (park) prow[0] = surrogate_grad_f32((float)d_prev, slope);  // psi_{t0-1}
+  const bool park = PARK && valid_i;
+  float* pp = PARK ? psis + (long long)b * (P.KR + 1) * n + (valid_i ? i : wbase) : nullptr;
+  if (park) pp[0] = surrogate_grad_f32((float)d_prev, slope);  // psi_{t0-1}
+  uint32_t* rp = (PASSA && raster != nullptr)
+                     ? raster + ((long long)b * P.T + P.t0) * nw + (wbase >> 5) : nullptr;
+  const int len = P.len;
   // software pipeline: the current of steps s8+8..s8+15 is in flight while steps
-  // s8..s8+7 integrate (16 outstanding 8-byte loads per thread; the kernel is HBM-bound)
+  // s8..s8+7 integrate (16 outstanding 8-byte loads per thread)
   double In[8];
 #pragma unroll
-  for (int u8 = 0; u8 < 8; ++u8)
-    In[u8] = (valid_i && u8 < P.len) ? __ldcs(crow + (long long)u8 * P.n) : 0.0;
-  for (int s8 = 0; s8 < P.len; s8 += 8) {
+  for (int u8 = 0; u8 < 8; ++u8) In[u8] = u8 < len ? __ldcs(cp + (long long)u8 * n) : 0.0;
+  const long long n8 = 8LL * n;
+  for (int s8 = 0; s8 < len; s8 += 8) {
     double Ib[8];
 #pragma unroll
     for (int u8 = 0; u8 < 8; ++u8) Ib[u8] = In[u8];
+    cp += n8;
+#pragma unroll
+    for (int u8 = 0; u8 < 8; ++u8)
+      In[u8] = (s8 + 8 + u8 < len) ? __ldcs(cp + (long long)u8 * n) : 0.0;
 #pragma unroll
     for (int u8 = 0; u8 < 8; ++u8) {
-      const int sn = s8 + 8 + u8;
-      In[u8] = (valid_i && sn < P.len) ? __ldcs(crow + (long long)sn * P.n) : 0.0;
-    }
-#pragma unroll
-    for (int u8 = 0; u8 < 8; ++u8) {
-      const int s = s8 + u8;
-      if (s < P.len) {
+      if (s8 + u8 < len) {
         // gradients.py:121-129 (u - theta - beta*a evaluates as (u - theta) - (beta*a))
-        const double z_prev = spike_value(d_prev, smooth, slope_d);
-        a = __dadd_rn(__dmul_rn(P.rho, a), z_prev);
-        u = __dadd_rn(__dmul_rn(P.alpha, u), Ib[u8]);
-        if (P.reset) u = __dsub_rn(u, __dmul_rn(theta, z_prev));
+        const double z_prev = spike_value(d_prev, SMOOTH, slope_d);
+        a = __dadd_rn(__dmul_rn(rho, a), z_prev);
+        u = __dadd_rn(__dmul_rn(alpha, u), Ib[u8]);
+        if (RESET) u = __dsub_rn(u, __dmul_rn(theta, z_prev));
         const double d = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
-        if (P.pass == 0) {
-          const double zv = spike_value(d, smooth, slope_d);
-          zbar = __dadd_rn(__dmul_rn(P.kappa, zbar), zv);
+        if (PASSA) {
+          const double zv = spike_value(d, SMOOTH, slope_d);
+          zbar = __dadd_rn(__dmul_rn(kappa, zbar), zv);
           zsum = __dadd_rn(zsum, zbar);
           // raster = z > 0.5 (gradients.py:362)
           const unsigned bal = __ballot_sync(0xffffffffu, zv > 0.5 && valid_i);
-          if (raster != nullptr && lane == 0)
-            raster[((long long)b * P.T + P.t0 + s) * nw + (wbase >> 5)] = bal;
+          if (rp != nullptr && lane == 0) rp[0] = bal;
+          if (rp != nullptr) rp += nw;
         }
         // the surrogate only scales fp32 eligibilities: evaluate it in fp32
-        if (park) prow[(long long)(s + 1) * P.n] = surrogate_grad_f32((float)d, slope);
+        if (PARK) {
+          pp += n;
+          if (park) pp[0] = surrogate_grad_f32((float)d, slope);
+        }
         d_prev = d;
       }
     }
@@ -132,11 +141,27 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
   if (valid_i) {
     u_st[bi] = u;
     a_st[bi] = a;
-    if (P.pass == 0) {
+    if (PASSA) {
       zbar_st[bi] = zbar;
       zsum_st[bi] = zsum;
     }
   }
+}
+
+template <bool PASSA, bool PARK>
+static void launch_forward(const FwdParams& P, dim3 grid, cudaStream_t stream, const double* cur,
+                           double* u, double* a, double* zbar, double* zsum, uint32_t* raster,
+                           const float* wsig, float* psis) {
+  const bool reset = P.reset != 0, smooth = P.smooth != 0;
+#define SPB_K1(R, S)                                                                          \
+  forward_chunk_kernel<PASSA, PARK, R, S><<<grid, K1_THREADS, 0, stream>>>(P, cur, u, a, zbar, \
+                                                                          zsum, raster, wsig, \
+                                                                          psis)
+  if (reset && smooth) SPB_K1(true, true);
+  else if (reset) SPB_K1(true, false);
+  else if (smooth) SPB_K1(false, true);
+  else SPB_K1(false, false);
+#undef SPB_K1
 }
 
 // ------------------------------------------------------------------------------------
@@ -458,8 +483,12 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
               smooth};
   dim3 grid(ceil_div(n, K1_THREADS), B);
   if (pass <= 1) {
-    forward_chunk_kernel<<<grid, K1_THREADS, 0, stream>>>(P, cur, u, a, zbar, zsum, raster, wsig,
-                                                          psi_scratch);
+    if (pass == 0 && psi_scratch)
+      launch_forward<true, true>(P, grid, stream, cur, u, a, zbar, zsum, raster, wsig, psi_scratch);
+    else if (pass == 0)
+      launch_forward<true, false>(P, grid, stream, cur, u, a, zbar, zsum, raster, wsig, nullptr);
+    else
+      launch_forward<false, true>(P, grid, stream, cur, u, a, zbar, zsum, raster, wsig, psi_scratch);
     SPB_CHECK_LAUNCH("forward_chunk");
   }
   if (pass >= 1 && reset) {
