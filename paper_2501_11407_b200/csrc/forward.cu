@@ -174,27 +174,8 @@ static void launch_forward(const FwdParams& P, dim3 grid, cudaStream_t stream, c
 // ------------------------------------------------------------------------------------
 constexpr int K1S_THREADS = 128;  // 4 warps = 256 consecutive neurons of one sample
 
-struct ScanLane {
-  float lam = 0.f, dcum = 1.f, a_next = 0.f;
-  // step r: psi_prev = psi_{r-1}, psi_r = psi_r; gains c_prev = c_{r-1}, c_r = c_r
-  __device__ __forceinline__ void step(int r, int L, bool alif, float psi_prev, float psi_r,
-                                       float c_prev, float c_r, float w_sig, float beta,
-                                       float rho, float& cval, float& wval) {
-    cval = 0.f;
-    wval = 0.f;
-    if (r >= 1) cval = c_prev * w_sig * psi_prev;  // L_{r-1} psi_{r-1}
-    if (alif && r < L) {
-      const float A = fmaf(-beta, psi_prev, rho);
-      const float Q = -beta * (c_r * w_sig * psi_r);
-      lam = fmaf(a_next, lam, Q);                  // Lambda_r (Lambda_L = 0)
-      cval = fmaf(psi_prev, lam, cval);            // + R_r
-      wval = psi_prev * dcum;                      // W_r = P_r D(L-1, r)
-      dcum *= A;
-      a_next = A;
-    }
-  }
-};
 
+template <bool ALIF, bool CARRY>
 __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
     FwdParams P, const float* __restrict__ wsig, const float* __restrict__ ctab,
     uint32_t* __restrict__ c_hi, uint32_t* __restrict__ c_lo, uint32_t* __restrict__ w_hi,
@@ -209,56 +190,81 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
   const int i = blockIdx.x * 2 * K1S_THREADS + warp * 64 + 2 * lane;  // neurons i, i+1
   const int b = blockIdx.y;
   if (b >= P.B || i >= P.n) return;
-  const bool has2 = i + 1 < P.n;
-  const long long bi = (long long)b * P.n + i;
+  const int n = P.n;
+  const bool has2 = i + 1 < n;
+  const long long bi = (long long)b * n + i;
   const float ws0 = wsig[bi], ws1 = has2 ? wsig[bi + 1] : 0.f;
   const float beta = (float)P.beta, rho = (float)P.rho;
-  const bool carry = P.alif && w_hi != nullptr;
-  const float* prow = psis + (long long)b * (P.KR + 1) * P.n + i;
-  const bool even_n = (P.n & 1) == 0;  // float2 rows are 8-byte aligned only for even n
+  const float* prow = psis + (long long)b * (P.KR + 1) * n + i;
+  const bool vec = has2 && (n & 1) == 0;  // float2 rows are 8-byte aligned only for even n
   auto ldpsi = [&](int r) -> float2 {
     if (r < 0) return make_float2(0.f, 0.f);
-    const float* q = prow + (long long)r * P.n;
-    if (has2 && even_n) return *reinterpret_cast<const float2*>(q);
-    return make_float2(q[0], has2 ? q[1] : 0.f);
+    const float* q = prow + (long long)r * n;
+    if (vec) return __ldcs(reinterpret_cast<const float2*>(q));
+    return make_float2(__ldcs(q), has2 ? __ldcs(q + 1) : 0.f);
   };
   const long long ld2 = ldc >> 1;  // row stride in bf16x2 words
-  uint32_t* chp = c_hi + (long long)b * P.KR * ld2 + (i >> 1);
-  uint32_t* clp = c_lo + (long long)b * P.KR * ld2 + (i >> 1);
-  uint32_t* whp = carry ? w_hi + (long long)b * P.KR * ld2 + (i >> 1) : nullptr;
-  uint32_t* wlp = carry ? w_lo + (long long)b * P.KR * ld2 + (i >> 1) : nullptr;
+  const long long row0 = (long long)b * P.KR * ld2 + (i >> 1);
+  uint32_t* chp = c_hi + row0;
+  uint32_t* clp = c_lo + row0;
+  uint32_t* whp = CARRY ? w_hi + row0 : nullptr;
+  uint32_t* wlp = CARRY ? w_lo + row0 : nullptr;
   for (int r = P.KR - 1; r > L; --r) {  // rows past the chunk
     chp[r * ld2] = 0u;
     clp[r * ld2] = 0u;
-    if (carry) { whp[r * ld2] = 0u; wlp[r * ld2] = 0u; }
+    if (CARRY) { whp[r * ld2] = 0u; wlp[r * ld2] = 0u; }
   }
-  ScanLane s0, s1;
-  float2 q0 = ldpsi(L), q1 = ldpsi(L - 1), q2 = ldpsi(L - 2), q3 = ldpsi(L - 3);
+  // walk the rows backwards with pointer decrements; PF psi rows in flight per thread
+  chp += L * ld2;
+  clp += L * ld2;
+  if (CARRY) { whp += L * ld2; wlp += L * ld2; }
+  float lam0 = 0.f, dcum0 = 1.f, an0 = 0.f, lam1 = 0.f, dcum1 = 1.f, an1 = 0.f;
+  constexpr int PF = 8;  // psi rows in flight per thread (16 measured slower)
+  float2 q[PF];
+#pragma unroll
+  for (int u = 0; u < PF; ++u) q[u] = ldpsi(L - u);
   float2 up = make_float2(0.f, 0.f);  // psi row r+1
   for (int r = L; r >= 0; --r) {
-    const float2 cur = q0;  // psi row r = psi_{r-1}
-    q0 = q1;
-    q1 = q2;
-    q2 = q3;
-    q3 = ldpsi(r - 4);
+    const float2 cur = q[0];  // psi row r = psi_{r-1}
+#pragma unroll
+    for (int u = 0; u < PF - 1; ++u) q[u] = q[u + 1];
+    q[PF - 1] = ldpsi(r - PF);
     const float c_prev = cs[r], c_r = (r < L) ? cs[r + 1] : 0.f;
-    float c0, w0, c1, w1;
-    s0.step(r, L, P.alif, cur.x, up.x, c_prev, c_r, ws0, beta, rho, c0, w0);
-    s1.step(r, L, P.alif, cur.y, up.y, c_prev, c_r, ws1, beta, rho, c1, w1);
+    // L_{r-1} psi_{r-1} (row r >= 1) [+ R_r = P_r Lambda_r, ALIF]; W_r = P_r D(L-1, r)
+    float c0 = r >= 1 ? c_prev * ws0 * cur.x : 0.f;
+    float c1 = r >= 1 ? c_prev * ws1 * cur.y : 0.f;
+    float w0 = 0.f, w1 = 0.f;
+    if (ALIF && r < L) {
+      const float A0 = fmaf(-beta, cur.x, rho), A1 = fmaf(-beta, cur.y, rho);
+      lam0 = fmaf(an0, lam0, -beta * (c_r * ws0 * up.x));
+      lam1 = fmaf(an1, lam1, -beta * (c_r * ws1 * up.y));
+      c0 = fmaf(cur.x, lam0, c0);
+      c1 = fmaf(cur.y, lam1, c1);
+      w0 = cur.x * dcum0;
+      w1 = cur.y * dcum1;
+      dcum0 *= A0;
+      dcum1 *= A1;
+      an0 = A0;
+      an1 = A1;
+    }
     uint32_t h, l;
     split_bf16x2(c0, c1, h, l);
-    chp[r * ld2] = h;
-    clp[r * ld2] = l;
-    if (carry) {
+    *chp = h;
+    *clp = l;
+    chp -= ld2;
+    clp -= ld2;
+    if (CARRY) {
       split_bf16x2(w0, w1, h, l);
-      whp[r * ld2] = h;
-      wlp[r * ld2] = l;
+      *whp = h;
+      *wlp = l;
+      whp -= ld2;
+      wlp -= ld2;
     }
     up = cur;
   }
-  if (P.alif && mdt != nullptr) {  // M also feeds the last chunk's inter-chunk term
-    mdt[bi] = make_float2(s0.a_next * s0.lam, s0.dcum);  // M = A_0 Lambda_0, Dt = prod A
-    if (has2) mdt[bi + 1] = make_float2(s1.a_next * s1.lam, s1.dcum);
+  if (ALIF && mdt != nullptr) {  // M also feeds the last chunk's inter-chunk term
+    mdt[bi] = make_float2(an0 * lam0, dcum0);  // M = A_0 Lambda_0, Dt = prod A
+    if (has2) mdt[bi + 1] = make_float2(an1 * lam1, dcum1);
   }
 }
 
@@ -501,7 +507,10 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
     SPB_CHECK_LAUNCH("reset_scan");
   } else if (pass >= 1) {
     dim3 sgrid(ceil_div(n, 2 * K1S_THREADS), B);
-    chunk_scan_kernel<<<sgrid, K1S_THREADS, (len + 1) * sizeof(float), stream>>>(
+    const bool carry = alif && w_hi != nullptr;
+    auto kfn = alif ? (carry ? chunk_scan_kernel<true, true> : chunk_scan_kernel<true, false>)
+                    : chunk_scan_kernel<false, false>;
+    kfn<<<sgrid, K1S_THREADS, (len + 1) * sizeof(float), stream>>>(
         P, wsig, ctab, reinterpret_cast<uint32_t*>(c_hi), reinterpret_cast<uint32_t*>(c_lo),
         reinterpret_cast<uint32_t*>(w_hi), reinterpret_cast<uint32_t*>(w_lo), ldc,
         reinterpret_cast<float2*>(mdt), psi_scratch);
