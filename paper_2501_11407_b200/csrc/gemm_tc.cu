@@ -22,7 +22,8 @@
 namespace spb {
 namespace tc {
 
-constexpr int BM = 128, BN = 128, BK = 64, STAGES = 3;
+constexpr int BM = 128, BN = 256, BK = 32, STAGES = 4;   // 128x256 tiles: 25% less L2 operand
+                                                          // traffic per output than 128x128
 constexpr int TILE_A = BM * BK * 2;  // bytes
 constexpr int TILE_B = BN * BK * 2;
 constexpr int STAGE_BYTES = 2 * TILE_A + 2 * TILE_B;
@@ -44,7 +45,7 @@ __device__ __forceinline__ uint64_t umma_desc_k_sw128(uint32_t saddr) {
 __device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)(8192u >> 4) << 16;   // LBO: next 64-wide MN block
+  d |= (uint64_t)((64u * BK * 2u) >> 4) << 16;   // LBO: next 64-wide MN block (one box)
   d |= (uint64_t)(1024u >> 4) << 32;   // SBO: next 8-row K group
   d |= (uint64_t)1u << 46;
   d |= (uint64_t)2u << 61;
@@ -125,10 +126,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma_load_2d(st + TILE_A / 2, &tm_ah, fb, m0 + 64, kb * BK);
         tma_load_2d(st + TILE_A, &tm_al, fb, m0, kb * BK);
         tma_load_2d(st + TILE_A + TILE_A / 2, &tm_al, fb, m0 + 64, kb * BK);
-        tma_load_2d(st + 2 * TILE_A, &tm_bh, fb, n0, kb * BK);
-        tma_load_2d(st + 2 * TILE_A + TILE_B / 2, &tm_bh, fb, n0 + 64, kb * BK);
-        tma_load_2d(st + 2 * TILE_A + TILE_B, &tm_bl, fb, n0, kb * BK);
-        tma_load_2d(st + 2 * TILE_A + TILE_B + TILE_B / 2, &tm_bl, fb, n0 + 64, kb * BK);
+#pragma unroll
+        for (int h = 0; h < BN / 64; ++h) {
+          tma_load_2d(st + 2 * TILE_A + h * (TILE_B / (BN / 64)), &tm_bh, fb, n0 + 64 * h, kb * BK);
+          tma_load_2d(st + 2 * TILE_A + TILE_B + h * (TILE_B / (BN / 64)), &tm_bl, fb, n0 + 64 * h,
+                      kb * BK);
+        }
       }
     }
   } else if (warp == 1) {

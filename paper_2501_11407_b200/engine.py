@@ -195,7 +195,7 @@ class EpropEngine:
         self.xh = torch.zeros((K, self.kp), dtype=bf16, device=dev)   # MN-major [K][kp]
         self.xl = torch.zeros((K, self.kp), dtype=bf16, device=dev)
         # split-K (K5) and sample-split (K6) partial slices, reduced in fixed order
-        tiles5 = (self.kp // 128) * math.ceil(n / 128)
+        tiles5 = math.ceil(self.kp / 256) * math.ceil(n / 128)   # K5 tiles are 128 x 256
         # split-K so the grid fills whole waves of SMs (C4: 96 tiles x 3 = 1.95 waves)
         self.splits5 = _wave_split(tiles5, max(1, K // 64), sms)
         self.wa_hi = self.wa_lo = self.eps2 = None
