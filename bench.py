@@ -22,6 +22,7 @@ port, oracle/cpu_bench.py) on a bounded sample of the same workload, rank 0 only
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -218,6 +219,7 @@ def main():
     import paper_2501_11407_b200 as P
     from paper_2501_11407_b200.datasets import poisson_batch
     from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200 import _lib
     from paper_2501_11407_b200.parallel import GradPacker
 
     torch.cuda.set_device(local)
@@ -249,11 +251,36 @@ def main():
     if kind == "alif":
         kw.update(beta=net.neuron.beta, rho=net.neuron.rho)
 
+    # Online weight update (north_star (3)): one fp32 master W / W_out shared by the
+    # engine(s); after the allreduce the fused SGD kernel updates both (W_out also
+    # refreshes the engine's fp64 mirror) and W is re-sliced into the INT8 digits the
+    # next update's projection reads -- all of it inside the timed step.
+    engines = list(getattr(eng, "engines", [eng]))
+    w_master = engines[0].w
+    for e in engines[1:]:
+        e.w = w_master
+    wout_master = torch.from_numpy(np.ascontiguousarray(net.readout.w_out)).to(dev)
+    lr, g_scale = 1e-3, 1.0 / (world * B)
+    vp = ctypes.c_void_p
+
+    def update():
+        gw, gwo, _, _ = packer.views()
+        st = vp(torch.cuda.current_stream(dev).cuda_stream)
+        _lib.call("spb_sgd_update", vp(w_master.data_ptr()), 0, n, k, vp(gw.data_ptr()), 0, k,
+                  g_scale, lr, None, st)
+        _lib.call("spb_sgd_update", vp(wout_master.data_ptr()), 0, m, n, vp(gwo.data_ptr()),
+                  0, n, g_scale, lr, vp(engines[0].wout.data_ptr()), st)
+        for e in engines[1:]:
+            e.wout.copy_(engines[0].wout)
+        for e in engines:
+            e.slice_weights()
+
     def step(x, y, timers=None, bits=False):
         # the synthetic Poisson inputs are 0/1 spikes: promise it (K2 single-int64 path)
         eng.run(x, y, timers=timers, bits=bits, binary=True, **kw)
         packer.pack(eng.grad_w_acc, eng.grad_wout, eng.loss, eng.correct)
         packer.allreduce()
+        update()
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
@@ -305,7 +332,8 @@ def main():
             step(xd, yd, timers=timers)
         ev[i][1].record()
     barrier()
-    launches_per_step = eng.launches  # kernels of libsparseprop_b200.so per step
+    # kernels of libsparseprop_b200.so per step: the engine's + 2 SGD + 1 slice per engine
+    launches_per_step = eng.launches + 2 + len(engines)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
     clk = clocks.stop() if clocks else None
@@ -378,6 +406,9 @@ def main():
                 main.wait_event(copied[i % 2])
                 if gsteps is not None:
                     gsteps[i % 2]()
+                    packer.pack(eng.grad_w_acc, eng.grad_wout, eng.loss, eng.correct)
+                    packer.allreduce()
+                    update()
                 else:
                     step(xb[i % 2], yb[i % 2], bits=True)
                 consumed[i % 2].record(main)
@@ -505,6 +536,7 @@ def main():
                        "n_classes": m, "chunk": eng.Tc, "parallelism": f"dp{world}",
                        "forward_precision": "fp64 state/current (bit-exact spikes)",
                        "forward_kernel": "K21 fused projection+dynamics" if eng.fused else "K2 projection + K1 dynamics",
+                       "step": "e-prop gradient + allreduce + fused SGD on W/W_out + W re-slice",
                        "l2": "512 MiB flush between timed steps (outside events)",
                        "launch": "CUDA graph replay of the whole update" if graph is not None
                                  else "eager launches"},
