@@ -26,6 +26,7 @@ engine never synchronises.  PyTorch provides allocation and streams only.
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 
 import numpy as np
@@ -226,6 +227,10 @@ class EpropEngine:
         self._ctab_T = None
         self.ctab = None
         self.launches = 0
+        # where K4 (xbar of a one-chunk sequence) runs: "fa" (default, measured best: C4
+        # 1.66 -> 1.59 ms) = side stream after K2, overlapping K1; "proj" = side stream from
+        # the start of pass A, overlapping K2; "main" = serially before K5
+        self.xbar_sched = os.environ.get("SPB_XBAR_SCHED", "fa")
         # side stream for work off the critical path (K4 xbar of a one-chunk sequence, K7)
         if self.device.type == "cuda":
             self.side = torch.cuda.Stream(device=dev)
@@ -430,7 +435,10 @@ class EpropEngine:
             t0 = c * Tc
             ln = min(Tc, T - t0)
             pack_chunk(c, ln)
-            if one and use_side and not forward_only and not self.recurrent:
+            side_x = one and use_side and not forward_only and not self.recurrent
+            if side_x and self.xbar_sched == "fa" and not self.fused:
+                self._project(ln, st, timed, binary)
+            if side_x and self.xbar_sched != "main":
                 # K4 needs only x: overlap it with pass A
                 self._ev["xbar"].record(main)
                 self.side.wait_event(self._ev["xbar"])
@@ -445,7 +453,8 @@ class EpropEngine:
                             (ln, 0, one and not forward_only))
                 self.launches += 2
                 continue
-            self._project(ln, st, timed, binary)
+            if not (side_x and self.xbar_sched == "fa"):
+                self._project(ln, st, timed, binary)
             if self.recurrent:
                 self._forward_rec(0, ln, t0, T, common, raster,
                                   one and not forward_only, st, timed, (ln, 0, one))
@@ -517,7 +526,7 @@ class EpropEngine:
                      v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()), v(self.xl.data_ptr()),
                      st)
                 self.launches += 2
-            elif one and use_side:
+            elif one and use_side and self.xbar_sched != "main":
                 main.wait_event(self._ev["xbar"])
             else:
                 call("spb_xbar_chunk", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
