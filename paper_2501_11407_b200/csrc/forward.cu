@@ -457,6 +457,63 @@ __global__ void __launch_bounds__(128) xbar_chunk_kernel(
   if (v1) xbar_st[(long long)b * k + j + 1] = xb1;
 }
 
+// K4 on 4 neighbouring channels per thread (row strides and x 4-byte aligned): one 32-bit
+// spike load and two 8-byte bf16x4 stores per step -- half the instructions per byte of
+// the 2-channel kernel above, same values.
+__global__ void __launch_bounds__(128) xbar_chunk4_kernel(
+    const uint8_t* __restrict__ x, long long stride_b, long long stride_t, int B, int k, int kp,
+    int KR, int len, int fresh, double alpha, double* __restrict__ xbar_st,
+    uint2* __restrict__ xh, uint2* __restrict__ xl) {
+  const int jq = blockIdx.x * blockDim.x + threadIdx.x;  // channel quad
+  const int j = 4 * jq;
+  const int b = blockIdx.y;
+  if (j >= kp) return;
+  double xb[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    xb[c] = (j + c < k && !fresh) ? xbar_st[(long long)b * k + j + c] : 0.0;
+  // channels >= k read padding bytes of the operand row (zero) or nothing at all
+  const bool any = j < k;
+  const uint32_t* xin = reinterpret_cast<const uint32_t*>(x + (long long)b * stride_b + j);
+  const long long st4 = stride_t >> 2;
+  const long long ld4 = kp >> 2;
+  uint2* oh = xh + (long long)b * KR * ld4 + jq;
+  uint2* ol = xl + (long long)b * KR * ld4 + jq;
+  const uint32_t keep = j + 4 <= k ? 0xffffffffu : (0xffffffffu >> (8 * (j + 4 - k)));
+  for (int r8 = 0; r8 < KR; r8 += 8) {
+    uint32_t xw[8];
+#pragma unroll
+    for (int u8 = 0; u8 < 8; ++u8) {
+      const int rho = r8 + u8;
+      const bool live = any && rho >= 1 && rho <= len;
+      xw[u8] = live ? (__ldg(xin + (long long)(rho - 1) * st4) & keep) : 0u;
+    }
+#pragma unroll
+    for (int u8 = 0; u8 < 8; ++u8) {
+      const int rho = r8 + u8;
+      float f[4] = {0.f, 0.f, 0.f, 0.f};
+      if (rho == 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) f[c] = (float)xb[c];
+      } else if (rho <= len) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          xb[c] = __dadd_rn(__dmul_rn(alpha, xb[c]), (double)((xw[u8] >> (8 * c)) & 0xffu));
+          f[c] = (float)xb[c];
+        }
+      }
+      uint2 h, l;
+      split_bf16x2(f[0], f[1], h.x, l.x);
+      split_bf16x2(f[2], f[3], h.y, l.y);
+      oh[(long long)rho * ld4] = h;
+      ol[(long long)rho * ld4] = l;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (j + c < k) xbar_st[(long long)b * k + j + c] = xb[c];
+}
+
 }  // namespace spb
 
 using namespace spb;
@@ -526,6 +583,15 @@ int spb_xbar_chunk(const uint8_t* x, long long stride_b, long long stride_t, int
   SPB_CHECK_ARG(B > 0 && k > 0 && kp >= k && kp % 8 == 0 && KR > 0 && KR % 8 == 0 && len >= 0 &&
                     len < KR,
                 "spb_xbar_chunk: bad sizes");
+  if ((stride_b | stride_t) % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0 &&
+      reinterpret_cast<uintptr_t>(xh) % 8 == 0 && reinterpret_cast<uintptr_t>(xl) % 8 == 0) {
+    dim3 grid4(ceil_div(kp / 4, 128), B);
+    xbar_chunk4_kernel<<<grid4, 128, 0, stream>>>(x, stride_b, stride_t, B, k, kp, KR, len, fresh,
+                                                  alpha, xbar_state, reinterpret_cast<uint2*>(xh),
+                                                  reinterpret_cast<uint2*>(xl));
+    SPB_CHECK_LAUNCH("xbar_chunk4");
+    return 0;
+  }
   dim3 grid(ceil_div(kp / 2, 128), B);
   xbar_chunk_kernel<<<grid, 128, 0, stream>>>(x, stride_b, stride_t, B, k, kp, KR, len, fresh,
                                               alpha, xbar_state,
