@@ -264,12 +264,16 @@ def main():
     vp = ctypes.c_void_p
 
     def update():
-        gw, gwo, _, _ = packer.views()
+        if world > 1:  # the allreduced fp32 payload
+            gw, gwo, _, _ = packer.views()
+            g64, ldw = 0, k
+        else:          # one rank: straight from the engine's fp64 accumulators
+            gw, gwo, g64, ldw = eng.grad_w_acc, eng.grad_wout, 1, eng.grad_w_acc.stride(0)
         st = vp(torch.cuda.current_stream(dev).cuda_stream)
-        _lib.call("spb_sgd_update", vp(w_master.data_ptr()), 0, n, k, vp(gw.data_ptr()), 0, k,
-                  g_scale, lr, None, st)
+        _lib.call("spb_sgd_update", vp(w_master.data_ptr()), 0, n, k, vp(gw.data_ptr()), g64,
+                  ldw, g_scale, lr, None, st)
         _lib.call("spb_sgd_update", vp(wout_master.data_ptr()), 0, m, n, vp(gwo.data_ptr()),
-                  0, n, g_scale, lr, vp(engines[0].wout.data_ptr()), st)
+                  g64, n, g_scale, lr, vp(engines[0].wout.data_ptr()), st)
         for e in engines[1:]:
             e.wout.copy_(engines[0].wout)
         for e in engines:
@@ -278,8 +282,9 @@ def main():
     def step(x, y, timers=None, bits=False):
         # the synthetic Poisson inputs are 0/1 spikes: promise it (K2 single-int64 path)
         eng.run(x, y, timers=timers, bits=bits, binary=True, **kw)
-        packer.pack(eng.grad_w_acc, eng.grad_wout, eng.loss, eng.correct)
-        packer.allreduce()
+        if world > 1:  # the update's single collective
+            packer.pack(eng.grad_w_acc, eng.grad_wout, eng.loss, eng.correct)
+            packer.allreduce()
         update()
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -333,7 +338,7 @@ def main():
         ev[i][1].record()
     barrier()
     # kernels of libsparseprop_b200.so per step: the engine's + 2 SGD + 1 slice per engine
-    launches_per_step = eng.launches + 2 + len(engines)
+    launches_per_step = eng.launches + 2 + len(engines) + (1 if world > 1 else 0)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
     clk = clocks.stop() if clocks else None
@@ -406,8 +411,9 @@ def main():
                 main.wait_event(copied[i % 2])
                 if gsteps is not None:
                     gsteps[i % 2]()
-                    packer.pack(eng.grad_w_acc, eng.grad_wout, eng.loss, eng.correct)
-                    packer.allreduce()
+                    if world > 1:
+                        packer.pack(eng.grad_w_acc, eng.grad_wout, eng.loss, eng.correct)
+                        packer.allreduce()
                     update()
                 else:
                     step(xb[i % 2], yb[i % 2], bits=True)
@@ -536,7 +542,7 @@ def main():
                        "n_classes": m, "chunk": eng.Tc, "parallelism": f"dp{world}",
                        "forward_precision": "fp64 state/current (bit-exact spikes)",
                        "forward_kernel": "K21 fused projection+dynamics" if eng.fused else "K2 projection + K1 dynamics",
-                       "step": "e-prop gradient + allreduce + fused SGD on W/W_out + W re-slice",
+                       "step": "e-prop gradient (+ allreduce when N > 1) + fused SGD on W/W_out + W re-slice",
                        "l2": "512 MiB flush between timed steps (outside events)",
                        "launch": "CUDA graph replay of the whole update" if graph is not None
                                  else "eager launches"},

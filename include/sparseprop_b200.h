@@ -228,6 +228,14 @@ int spb_copy_chunk_h2d(void* dst, long long dst_pitch, const void* src, long lon
 int spb_finalize_grad(const double* acc, int rows, int cols, int ld, void* out, int out_is_f64,
                       cudaStream_t stream);
 
+/* Data-parallel allreduce payload (parallel.py GradPacker) in one launch:
+ * out = [acc[:, :k] (n*k) | gwo (m*n) | sum_b loss[b] | sum_b correct[b]] in fp32
+ * (out_is_f64=0) or fp64; the two sums in sample order.  Replaces the host-side packing
+ * the reference never needed (it is single-process: reference/pkg/src/sparseprop/training.py). */
+int spb_pack_grads(const double* acc, int n, int k, int ld, const double* gwo, int m,
+                   const double* loss, const int* correct, int B, void* out, int out_is_f64,
+                   cudaStream_t stream);
+
 /* On-device synthetic spikes (poisson.cu): out[b*stride_b + t*ceil(k/8) + (j>>3)] bit (j&7)
  * = 1 with probability rates[labels[b]][j] for t < T, global step t0+t, Philox4x32-10
  * keyed by `seed`, counter (byte, step, sample) -- reproducible in any chunking; the

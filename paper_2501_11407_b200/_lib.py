@@ -42,6 +42,7 @@ SIGNATURES = {
                               I, P],
     "spb_reduce_partials": [P, I, I, I, I, I, P, P],
     "spb_finalize_grad": [P, I, I, I, P, I, P],
+    "spb_pack_grads": [P, I, I, I, P, I, P, P, I, P, I, P],
     "spb_copy_chunk_h2d": [P, LL, P, LL, LL, I, P],
     "spb_sgd_update": [P, I, I, I, P, I, I, D, D, P, P],
     "spb_adam_update": [P, P, P, I, I, I, P, I, I, D, D, D, D, D, I, P, P],

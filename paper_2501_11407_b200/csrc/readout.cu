@@ -5,6 +5,8 @@
 //                            w_sig = W_out^T g (gradients.py:178)
 //   K7  spb_readout_grad  -- grad W_out = sum_b g_b (x) zsum_b (gradients.py:181), written
 //   --  spb_finalize_grad -- fp64 gradient accumulator -> caller dtype, padding dropped
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace spb {
@@ -14,10 +16,9 @@ __global__ void readout_loss_kernel(const double* __restrict__ wout, const doubl
                                     double* __restrict__ s_out, double* __restrict__ loss,
                                     double* __restrict__ g_out, float* __restrict__ wsig,
                                     int* __restrict__ correct) {
-  extern __shared__ double sm[];  // [m] logits + [m] g + [32] scratch
+  extern __shared__ double sm[];  // [m] logits + [m] g (exps, then dL/ds)
   double* s = sm;
   double* g = sm + m;
-  double* red = sm + 2 * m;
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const double* z = zsum + (long long)b * n;
@@ -26,6 +27,7 @@ __global__ void readout_loss_kernel(const double* __restrict__ wout, const doubl
     const double* wr = wout + (long long)c * n;
     double a0 = 0.0, a1 = 0.0;
     int i = lane;
+#pragma unroll 4
     for (; i + 32 < n; i += 64) {
       a0 = fma(wr[i], z[i], a0);
       a1 = fma(wr[i + 32], z[i + 32], a1);
@@ -35,25 +37,36 @@ __global__ void readout_loss_kernel(const double* __restrict__ wout, const doubl
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) s[c] = acc;
   }
-  (void)red;
   __syncthreads();
-  if (tid == 0) {
+  // softmax cross-entropy: the exps run one class per lane; the max, the first argmax and
+  // the sum of exps are taken in class order by one lane (the reference's order)
+  if (warp == 0) {
     const int y = (int)labels[b];
     double mx = s[0];
     int arg = 0;
-    for (int c = 1; c < m; ++c)
-      if (s[c] > mx) { mx = s[c]; arg = c; }
-    double se = 0.0;
-    for (int c = 0; c < m; ++c) se += exp(s[c] - mx);
-    const double logz = log(se);
-    loss[b] = logz - (s[y] - mx);
-    for (int c = 0; c < m; ++c) {
-      g[c] = exp((s[c] - mx) - logz);
-      s_out[(long long)b * m + c] = s[c];
+    if (lane == 0) {
+      for (int c = 1; c < m; ++c)
+        if (s[c] > mx) { mx = s[c]; arg = c; }
     }
-    g[y] -= 1.0;
-    for (int c = 0; c < m; ++c) g_out[(long long)b * m + c] = g[c];
-    if (correct) correct[b] = (arg == y) ? 1 : 0;
+    mx = __shfl_sync(0xffffffffu, mx, 0);
+    for (int c = lane; c < m; c += 32) g[c] = exp(s[c] - mx);
+    __syncwarp();
+    double logz = 0.0;
+    if (lane == 0) {
+      double se = 0.0;
+      for (int c = 0; c < m; ++c) se += g[c];
+      logz = log(se);
+      loss[b] = logz - (s[y] - mx);
+      if (correct) correct[b] = (arg == y) ? 1 : 0;
+    }
+    logz = __shfl_sync(0xffffffffu, logz, 0);
+    __syncwarp();
+    for (int c = lane; c < m; c += 32) {
+      const double gc = exp((s[c] - mx) - logz) - (c == y ? 1.0 : 0.0);
+      g[c] = gc;
+      s_out[(long long)b * m + c] = s[c];
+      g_out[(long long)b * m + c] = gc;
+    }
   }
   __syncthreads();
   for (int i = tid; i < n; i += blockDim.x) {
@@ -104,6 +117,35 @@ __global__ void finalize_kernel(const double* __restrict__ acc, int rows, int co
   out[idx] = (OT)acc[(long long)r * ld + c];
 }
 
+// Allreduce payload in one launch: [grad W (acc[:, :k]) | grad W_out | sum loss | #correct]
+// in the payload dtype; block 0 also sums the B losses and correct flags in sample order.
+template <typename OT>
+__global__ void pack_grads_kernel(const double* __restrict__ acc, int n, int k, int ld,
+                                  const double* __restrict__ gwo, int m,
+                                  const double* __restrict__ loss, const int* __restrict__ correct,
+                                  int B, OT* __restrict__ out) {
+  const long long nk = (long long)n * k, total = nk + (long long)m * n;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    if (idx < nk) {
+      const int r = (int)(idx / k), c = (int)(idx - (long long)r * k);
+      out[idx] = (OT)acc[(long long)r * ld + c];
+    } else {
+      out[idx] = (OT)gwo[idx - nk];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double ls = 0.0;
+    long long nc = 0;
+    for (int b = 0; b < B; ++b) {
+      ls += loss[b];
+      nc += correct[b];
+    }
+    out[total] = (OT)ls;
+    out[total + 1] = (OT)nc;
+  }
+}
+
 }  // namespace spb
 
 using namespace spb;
@@ -130,6 +172,23 @@ int spb_readout_grad(const double* g, const double* zsum, int B, int n, int m, d
   dim3 grid(ceil_div(n, 32), m);
   readout_grad_kernel<<<grid, 32 * RG_SLICES, 0, stream>>>(g, zsum, B, n, m, gwo);
   SPB_CHECK_LAUNCH("readout_grad");
+  return 0;
+}
+
+int spb_pack_grads(const double* acc, int n, int k, int ld, const double* gwo, int m,
+                   const double* loss, const int* correct, int B, void* out, int out_is_f64,
+                   cudaStream_t stream) {
+  SPB_CHECK_ARG(acc && gwo && loss && correct && out && n > 0 && k > 0 && ld >= k && m > 0 && B > 0,
+                "spb_pack_grads: bad args");
+  const long long total = (long long)n * k + (long long)m * n;
+  const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 148 * 8);
+  if (out_is_f64)
+    pack_grads_kernel<double><<<blocks, 256, 0, stream>>>(acc, n, k, ld, gwo, m, loss, correct, B,
+                                                          (double*)out);
+  else
+    pack_grads_kernel<float><<<blocks, 256, 0, stream>>>(acc, n, k, ld, gwo, m, loss, correct, B,
+                                                         (float*)out);
+  SPB_CHECK_LAUNCH("pack_grads");
   return 0;
 }
 

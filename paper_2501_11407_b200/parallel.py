@@ -43,7 +43,21 @@ class GradPacker:
         return gw, gwo, self.buf[n * k + m * n], self.buf[n * k + m * n + 1]
 
     def pack(self, grad_w_acc, grad_wout, loss, correct):
-        """grad_w_acc may be column-padded ([n, k_pad]); only [:, :k] is packed."""
+        """grad_w_acc may be column-padded ([n, k_pad]); only [:, :k] is packed.  On CUDA
+        one fused kernel (spb_pack_grads) does it; elsewhere (gloo tests) torch ops."""
+        if (self.buf.is_cuda and grad_w_acc.dtype == torch.float64
+                and grad_wout.dtype == torch.float64 and loss.dtype == torch.float64
+                and correct.dtype == torch.int32 and grad_w_acc.stride(1) == 1
+                and grad_wout.is_contiguous()):
+            import ctypes
+            from . import _lib
+            v = ctypes.c_void_p
+            _lib.call("spb_pack_grads", v(grad_w_acc.data_ptr()), self.n, self.k,
+                      grad_w_acc.stride(0), v(grad_wout.data_ptr()), self.m,
+                      v(loss.data_ptr()), v(correct.data_ptr()), int(loss.shape[0]),
+                      v(self.buf.data_ptr()), int(self.buf.dtype == torch.float64),
+                      v(torch.cuda.current_stream(self.buf.device).cuda_stream))
+            return self.buf
         gw, gwo, ls, nc = self.views()
         gw.copy_(grad_w_acc[:, : self.k])
         gwo.copy_(grad_wout)
