@@ -470,6 +470,9 @@ def main():
                         byts += psi
                 if pid >= 1:                       # scan: psi back, C (and W) out, bf16 hi/lo
                     byts += psi + 4.0 * n * B * KR * (2 if flag else 1)
+            elif name == "forward_scan":
+                ln, _, _ = meta                    # K1f: current in, C out (psi stays in L2)
+                byts += 8.0 * B * ln * n + 4.0 * n * B * KR
             elif name == "gemm":
                 ln = meta
                 flops += 6.0 * n * k * B * (ln + 1)                 # 3 bf16 MMAs per product
@@ -498,6 +501,7 @@ def main():
                  "fused_a": "fused_forward_kernel (K21 pass A: int8 tcgen05 projection + fp64 dynamics)",
                  "fused_b": "fused_forward_kernel (K21 pass B: projection + dynamics, psi)",
                  "forward_a": "forward_chunk_kernel (K1 pass A)",
+                 "forward_scan": "forward_scan_kernel (K1f: dynamics + readout + chunk scan)",
                  "gemm": "grad_gemm_tc_kernel (K5, bf16x3 tcgen05)",
                  "carry": "alif_carry_kernel (K6, tcgen05 + eps stream)"}
         if args.recurrent:

@@ -129,6 +129,22 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
                       void* wa_hi, void* wa_lo, int ldc, float* mdt, float* psi_scratch,
                       cudaStream_t stream);
 
+/* K1f One-chunk update's per-neuron work in one kernel (forward.cu; replaces, for a
+ *     sequence that fits one chunk, reset = 0: spb_forward_chunk pass 0 with psi_scratch +
+ *     spb_readout_loss + spb_forward_chunk pass 2): the pass-A dynamics from a fresh state
+ *     (u, a, zbar, zsum, raster as K1), the readout loss of each sample (s, loss, g, correct
+ *     and wsig = W_out^T g as spb_readout_loss; wout [m][n] fp64, m <= 64, logits summed over
+ *     128-neuron partials) and the backward scan into c_hi/c_lo (as pass B; no carry).
+ *     sync: 1 + 2B uint32 words, zero before the first call (self-resetting); part:
+ *     B * ceil(n/128) * m doubles of scratch.  Reference: gradients.py:118-174 as K1 + K3. */
+int spb_forward_scan_chunk(const double* cur, int B, int n, int Tc, int KR, int len, int T,
+                           double alpha, double theta, double slope, double beta, double rho,
+                           double kappa, int alif, int smooth, double* u, double* a, double* zbar,
+                           double* zsum, uint32_t* raster, float* psi, const double* wout,
+                           const long long* labels, int m, double* s, double* loss, double* g,
+                           float* wsig, int* correct, const float* ctab, void* c_hi, void* c_lo,
+                           int ldc, unsigned* sync, double* part, cudaStream_t stream);
+
 /* K1rec Recurrent hidden layer (forward_rec.cu, parity unpinned):
  *     u <- alpha u + (cur[row][i] + sum_{j: z_{t-1}[j]} W_rec[i][j]), otherwise as K1.
  *     wrecT [n][n] = W_rec transposed (fp32, or fp64 with w_is_f64), n <= 2048; one CTA

@@ -32,6 +32,8 @@ SIGNATURES = {
     "spb_input_proj_pair": [P, P, P, I, I, I, I, I, P, I, I, P],
     "spb_forward_chunk": [I, P, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I, I,
                           P, P, P, P, P, P, P, P, P, P, P, P, P, I, P, P, P],
+    "spb_forward_scan_chunk": [P, I, I, I, I, I, I, D, D, D, D, D, D, I, I, P, P, P, P, P, P,
+                               P, P, I, P, P, P, P, P, P, P, P, I, P, P, P],
     "spb_xbar_chunk": [P, LL, LL, I, I, I, I, I, I, D, P, P, P, P],
     "spb_readout_loss": [P, P, P, I, I, I, P, P, P, P, P, P],
     "spb_readout_grad": [P, P, I, I, I, P, P],

@@ -183,6 +183,12 @@ class EpropEngine:
         self.correct = torch.empty(B, dtype=torch.int32, device=dev)
         # pass-B chunk operands (bf16 hi/lo, K-major over (sample, rho))
         self.psi = torch.zeros((B, self.KR + 1, n), dtype=f32, device=dev)   # K1 scan scratch
+        # K1f (one-chunk forward + readout + scan in one kernel): sample meeting words and
+        # the partial logits.  Opt-in (SPB_K1F=1 or engine.k1f = True): measured slower at C3
+        # (0.41 vs 0.29 ms for K1 + K3 + K1s: the live psi of ~900 resident CTAs overflows L2)
+        self.k1f = os.environ.get("SPB_K1F", "0") == "1" and m <= 64
+        self.kf_sync = torch.zeros(1 + 2 * B, dtype=torch.int32, device=dev)
+        self.kf_part = torch.empty(B * ((n + 127) // 128) * m, dtype=f64, device=dev)
         self.ldc = _round_up(n, 8)   # C/W are MN-major [K][ldc] (neurons contiguous)
         self.c_hi = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
         self.c_lo = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
@@ -362,6 +368,9 @@ class EpropEngine:
         ctab = self._gains(T, float(kappa))
         nchunks = (T + Tc - 1) // Tc
         one = nchunks == 1
+        # K1f: pass A + readout + scan of a one-chunk sequence in one kernel
+        kf = (one and self.k1f and not forward_only and not self.fused and not self.recurrent
+              and not self.reset and self.device.type == "cuda")
         strideb = T * kb
         self.launches = 0
         v = ctypes_void
@@ -455,6 +464,19 @@ class EpropEngine:
                 continue
             if not (side_x and self.xbar_sched == "fa"):
                 self._project(ln, st, timed, binary)
+            if kf:
+                timed("forward_scan", (ln, 3, one), "spb_forward_scan_chunk",
+                      v(self.cur.data_ptr()), B, n, Tc, KR, ln, T, *common[:6], int(self.alif),
+                      int(bool(smooth)), v(self.u.data_ptr()), v(self.a.data_ptr()),
+                      v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
+                      v(raster.data_ptr()) if raster is not None else None,
+                      v(self.psi.data_ptr()), v(self.wout.data_ptr()), v(labels.data_ptr()), m,
+                      v(self.s.data_ptr()), v(self.loss.data_ptr()), v(self.g.data_ptr()),
+                      v(self.wsig.data_ptr()), v(self.correct.data_ptr()), v(ctab.data_ptr()),
+                      v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()), self.ldc,
+                      v(self.kf_sync.data_ptr()), v(self.kf_part.data_ptr()), st)
+                self.launches += 3
+                continue
             if self.recurrent:
                 self._forward_rec(0, ln, t0, T, common, raster,
                                   one and not forward_only, st, timed, (ln, 0, one))
@@ -468,11 +490,12 @@ class EpropEngine:
                   None, None, None, None, None, None, None, None, 0, None,
                   v(self.psi.data_ptr()) if (one and not forward_only) else None, st)
             self.launches += 3
-        # ---------------- readout / loss ----------------
-        call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
-             v(labels.data_ptr()), B, n, m, v(self.s.data_ptr()), v(self.loss.data_ptr()),
-             v(self.g.data_ptr()), v(self.wsig.data_ptr()), v(self.correct.data_ptr()), st)
-        self.launches += 1
+        # ---------------- readout / loss (inside K1f when it ran) ----------------
+        if not kf:
+            call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
+                 v(labels.data_ptr()), B, n, m, v(self.s.data_ptr()), v(self.loss.data_ptr()),
+                 v(self.g.data_ptr()), v(self.wsig.data_ptr()), v(self.correct.data_ptr()), st)
+            self.launches += 1
         if forward_only:
             return self
         if use_side:  # K7 is off the critical path
@@ -505,17 +528,18 @@ class EpropEngine:
                 self.launches += 2
             # one chunk (pass A parked psi) or K21 / K1rec (park psi themselves): scan only
             pid = 2 if (one or self.fused or self.recurrent) else 1
-            timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,
-                  v(self.cur.data_ptr()) if self.cur is not None else None, B, n, Tc, KR,
-                  ln, t0, T, *common, v(self.u.data_ptr()), v(self.a.data_ptr()), None, None,
-                  None, v(self.wsig.data_ptr()), v(ctab.data_ptr()),
-                  v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()),
-                  v(self.w_hi.data_ptr()) if carry_out else None,
-                  v(self.w_lo.data_ptr()) if carry_out else None,
-                  v(self.wa_hi.data_ptr()) if carry_out and self.ntr == 2 else None,
-                  v(self.wa_lo.data_ptr()) if carry_out and self.ntr == 2 else None, self.ldc,
-                  v(self.mdt.data_ptr()) if self.ntr else None, v(self.psi.data_ptr()), st)
-            self.launches += 1 if pid == 2 else 2
+            if not kf:
+                timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,
+                      v(self.cur.data_ptr()) if self.cur is not None else None, B, n, Tc, KR,
+                      ln, t0, T, *common, v(self.u.data_ptr()), v(self.a.data_ptr()), None, None,
+                      None, v(self.wsig.data_ptr()), v(ctab.data_ptr()),
+                      v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()),
+                      v(self.w_hi.data_ptr()) if carry_out else None,
+                      v(self.w_lo.data_ptr()) if carry_out else None,
+                      v(self.wa_hi.data_ptr()) if carry_out and self.ntr == 2 else None,
+                      v(self.wa_lo.data_ptr()) if carry_out and self.ntr == 2 else None, self.ldc,
+                      v(self.mdt.data_ptr()) if self.ntr else None, v(self.psi.data_ptr()), st)
+                self.launches += 1 if pid == 2 else 2
             if self.recurrent:
                 # x~ = [x_t, z_{t-1}] bytes, then the usual filter over kx columns
                 call("spb_pack_rec", v(self.xq.data_ptr()), xq_sb, xq_st,

@@ -1,0 +1,71 @@
+"""K1f (csrc/forward.cu forward_scan_kernel: one-chunk pass A + readout + backward scan in
+one launch) against the three-launch path it replaces (K1 pass A, K3 readout, K1s scan).
+The dynamics are the same code, so rasters and spike counts are bitwise equal; the logits
+are summed over 128-neuron partials (losses equal to fp64 rounding) and the gradients
+follow to fp32 rounding."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    a = np.asarray(a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def _run(net, x, y, *, k1f, smooth=False, graph=False):
+    from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200.gradients import _neuron_kwargs
+    B, T, _ = x.shape
+    chunk = next(c for c in (63, 127, 255, 511) if T <= c)
+    eng = EpropEngine(net.n, net.k, net.m, B, alif=net.is_alif,
+                      w_f64=net.neuron.w.dtype == np.float64, chunk=chunk)
+    eng.k1f = k1f
+    eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+    r = torch.zeros((B, T, (net.n + 31) // 32), dtype=torch.int32, device="cuda")
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    kw = dict(raster=r, smooth=smooth, **_neuron_kwargs(net))
+    eng.run(xd, yd, **kw)
+    if graph:  # replays reuse the self-resetting sample-meeting words
+        for _ in range(3):
+            eng.run(xd, yd, **kw)
+    torch.cuda.synchronize()
+    return dict(raster=r.cpu().numpy().copy(), loss=eng.loss.cpu().numpy().copy(),
+                g=eng.g.cpu().numpy().copy(), correct=eng.correct.cpu().numpy().copy(),
+                wsig=eng.wsig.cpu().numpy().copy(), zsum=eng.zsum.cpu().numpy().copy(),
+                gw=eng.grad_w_acc.cpu().numpy().copy(), gwo=eng.grad_wout.cpu().numpy().copy())
+
+
+@pytest.mark.parametrize("kind,n,k,m,B,T,prec,smooth", [
+    ("alif", 1024, 700, 20, 16, 250, "f32", False),   # C3 shape, small batch
+    ("lif", 256, 700, 20, 24, 250, "f32", False),     # C2 shape
+    ("alif", 100, 37, 3, 5, 40, "f64", False),        # ragged warps (no L2 discard), f64
+    ("lif", 130, 64, 35, 7, 100, "f32", True),        # smooth spikes, two CTAs + 2 neurons
+    ("alif", 2048, 96, 64, 3, 60, "f32", False),      # 16 CTAs per sample, m at the limit
+])
+def test_k1f_matches_three_launch_path(kind, n, k, m, B, T, prec, smooth):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    net = P.init_network(P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=m,
+                                       precision=prec, seed=7))
+    x, y = poisson_batch(B, k, T, m, seed=11)
+    a = _run(net, x, y, k1f=True, smooth=smooth, graph=True)
+    b = _run(net, x, y, k1f=False, smooth=smooth)
+    assert np.array_equal(a["raster"], b["raster"])
+    assert np.array_equal(a["zsum"], b["zsum"])
+    assert np.array_equal(a["correct"], b["correct"])
+    np.testing.assert_allclose(a["loss"], b["loss"], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(a["g"], b["g"], rtol=1e-10, atol=1e-14)
+    assert _rel(a["wsig"], b["wsig"]) < 1e-6
+    assert _rel(a["gwo"], b["gwo"]) < 1e-10
+    assert _rel(a["gw"], b["gw"]) < 1e-5
+    cos = float(np.dot(a["gw"].ravel(), b["gw"].ravel()) /
+                (np.linalg.norm(a["gw"]) * np.linalg.norm(b["gw"]) + 1e-300))
+    assert cos > 0.99999
