@@ -270,13 +270,12 @@ def main():
         else:          # one rank: straight from the engine's fp64 accumulators
             gw, gwo, g64, ldw = eng.grad_w_acc, eng.grad_wout, 1, eng.grad_w_acc.stride(0)
         st = vp(torch.cuda.current_stream(dev).cuda_stream)
-        _lib.call("spb_sgd_update", vp(w_master.data_ptr()), 0, n, k, vp(gw.data_ptr()), g64,
-                  ldw, g_scale, lr, None, st)
+        # W: SGD fused with the re-slicing of the first engine's INT8 digits
+        engines[0].sgd_slice(gw, g64, ldw, g_scale, lr)
         _lib.call("spb_sgd_update", vp(wout_master.data_ptr()), 0, m, n, vp(gwo.data_ptr()),
                   g64, n, g_scale, lr, vp(engines[0].wout.data_ptr()), st)
         for e in engines[1:]:
             e.wout.copy_(engines[0].wout)
-        for e in engines:
             e.slice_weights()
 
     def step(x, y, timers=None, bits=False):
@@ -337,8 +336,9 @@ def main():
             step(xd, yd, timers=timers)
         ev[i][1].record()
     barrier()
-    # kernels of libsparseprop_b200.so per step: the engine's + 2 SGD + 1 slice per engine
-    launches_per_step = eng.launches + 2 + len(engines) + (1 if world > 1 else 0)
+    # kernels of libsparseprop_b200.so per step: the engine's + SGD(+slice) on W + SGD on
+    # W_out + a slice per further engine (+ the payload pack when N > 1)
+    launches_per_step = eng.launches + 2 + (len(engines) - 1) + (1 if world > 1 else 0)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
     clk = clocks.stop() if clocks else None

@@ -269,6 +269,12 @@ int spb_poisson_bits(const float* rates, const long long* labels, int B, int T, 
  * (optional, fp64 [rows][cols]) receives the updated parameter. */
 int spb_sgd_update(void* p, int p_is_f64, int rows, int cols, const void* g, int g_is_f64,
                    int ld_g, double g_scale, double lr, double* mirror, cudaStream_t stream);
+/* SGD on the input weights fused with their re-slicing (spb_slice_weights) for the next
+ * update's projection: w [n][k] (fp32 / fp64 by w_is_f64) <- w - lr*(g_scale*g) exactly as
+ * spb_sgd_update, then wq/sexp re-derived from the new w.  One launch instead of two. */
+int spb_sgd_slice_update(void* w, int w_is_f64, int n, int k, const void* g, int g_is_f64,
+                         int ld_g, double g_scale, double lr, int Kpad, int n_pad32, int P,
+                         int8_t* wq, int* sexp, cudaStream_t stream);
 int spb_adam_update(void* p, void* m, void* v, int p_is_f64, int rows, int cols, const void* g,
                     int g_is_f64, int ld_g, double g_scale, double lr, double beta1, double beta2,
                     double eps, int t, double* mirror, cudaStream_t stream);

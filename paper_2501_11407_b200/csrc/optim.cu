@@ -103,9 +103,103 @@ static int grid_for(long long total, int sm_count) {
   return (int)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
+// ------------------------------------------------------------------------------------
+// SGD on the input weights fused with their re-slicing into the INT8 projection digits
+// (K2s, proj.cu / digits.cuh): CTA = one row of W.  Pass 1 applies p <- p - lr*g (the
+// sgd_kernel arithmetic) and takes the row maximum; pass 2 re-reads the row (the warp's
+// CTA's own fresh writes, L1-hot) and emits the P digit planes, 4 inputs per thread so every
+// plane store is one 32-bit word.  do_sgd = 0 is plain slicing (spb_slice_weights).
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void slice_one(double wv, int s, int P, int8_t (&q)[8]) {
+  if (P == 6) {
+    // balanced radix-256 digits of R = rint(w 2^(46-s)), |R| < 2^46, least significant
+    // first: q = ((R + 128) mod 256) - 128 in [-128, 127], R <- (R - q) / 256 (exact)
+    long long R = (long long)rint(ldexp(wv, 46 - s));
+#pragma unroll
+    for (int p = 5; p >= 0; --p) {
+      const long long d = ((R + 128) & 255) - 128;
+      R = (R - d) >> 8;
+      q[p] = (int8_t)d;
+    }
+  } else {  // radix-128 digits (P = 7: f32, P = 8: f64 weights)
+    double r = ldexp(wv, -s);
+    for (int p = 0; p < P; ++p) {
+      const double t = r * (p == 0 ? 64.0 : 128.0);
+      const double qv = rint(t);
+      r = t - qv;
+      q[p] = (int8_t)(int)qv;
+    }
+  }
+}
+
+constexpr int SS_THREADS = 128;  // one CTA per row of W
+
+template <typename T>
+__global__ void __launch_bounds__(SS_THREADS) sgd_slice_kernel(T* __restrict__ w, GradSrc gs,
+                                                               int n, int k, T lr, int do_sgd,
+                                                               int Kpad, int n_pad32, int P,
+                                                               int8_t* __restrict__ wq,
+                                                               int* __restrict__ sexp) {
+  using O = Op<T>;
+  __shared__ double red[SS_THREADS / 32];
+  const int i = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  T* row = w + (long long)i * k;
+  double mx = 0.0;
+  if (i < n) {
+    for (int j = tid; j < k; j += SS_THREADS) {
+      T v = row[j];
+      if (do_sgd) {
+        v = O::sub(v, O::mul(lr, load_grad<T>(gs, i, j)));
+        row[j] = v;
+      }
+      mx = fmax(mx, fabs((double)v));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();  // also orders the row's updated values before pass 2 reads them
+#pragma unroll
+  for (int q = 0; q < SS_THREADS / 32; ++q) mx = fmax(mx, red[q]);
+  int s = 0;
+  if (mx > 0.0) frexp(mx, &s);  // mx = f * 2^s, f in [0.5, 1)  =>  |w| < 2^s
+  if (tid == 0 && i < n) sexp[i] = s;
+  for (int j0 = 4 * tid; j0 < Kpad; j0 += 4 * SS_THREADS) {
+    uint32_t word[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = j0 + e;
+      const double wv = (i < n && j < k) ? (double)row[j] : 0.0;
+      int8_t q[8];
+      slice_one(wv, s, P, q);
+      for (int p = 0; p < P; ++p) word[p] |= (uint32_t)(uint8_t)q[p] << (8 * e);
+    }
+    for (int p = 0; p < P; ++p)
+      *reinterpret_cast<uint32_t*>(wq + ((long long)p * n_pad32 + i) * Kpad + j0) = word[p];
+  }
+}
+
 }  // namespace spb
 
 using namespace spb;
+
+// shared by spb_slice_weights (proj.cu) and spb_sgd_slice_update
+extern "C" __attribute__((visibility("hidden"))) int spb_launch_sgd_slice(void* w, int w_is_f64, int n, int k, const void* g, int g_is_f64,
+                         int ld_g, double g_scale, double lr, int do_sgd, int Kpad, int n_pad32,
+                         int P, int8_t* wq, int* sexp, cudaStream_t stream) {
+  const GradSrc gs{g, g_is_f64, ld_g, g_scale};
+  const int blocks = n_pad32;
+  if (w_is_f64)
+    sgd_slice_kernel<double><<<blocks, SS_THREADS, 0, stream>>>(static_cast<double*>(w), gs, n, k, lr,
+                                                         do_sgd, Kpad, n_pad32, P, wq, sexp);
+  else
+    sgd_slice_kernel<float><<<blocks, SS_THREADS, 0, stream>>>(static_cast<float*>(w), gs, n, k,
+                                                        (float)lr, do_sgd, Kpad, n_pad32, P, wq,
+                                                        sexp);
+  SPB_CHECK_LAUNCH("sgd_slice");
+  return 0;
+}
 
 extern "C" {
 
@@ -122,6 +216,17 @@ int spb_sgd_update(void* p, int p_is_f64, int rows, int cols, const void* g, int
                                                 (float)lr, mirror);
   SPB_CHECK_LAUNCH("sgd_update");
   return 0;
+}
+
+int spb_sgd_slice_update(void* w, int w_is_f64, int n, int k, const void* g, int g_is_f64,
+                         int ld_g, double g_scale, double lr, int Kpad, int n_pad32, int P,
+                         int8_t* wq, int* sexp, cudaStream_t stream) {
+  SPB_CHECK_ARG(w && g && wq && sexp && n > 0 && k > 0 && ld_g >= k && Kpad >= k &&
+                    Kpad % 128 == 0 && n_pad32 >= n && n_pad32 % 32 == 0 &&
+                    (P == 6 || P == 7 || P == 8),
+                "spb_sgd_slice_update: bad args");
+  return spb_launch_sgd_slice(w, w_is_f64, n, k, g, g_is_f64, ld_g, g_scale, lr, 1, Kpad,
+                              n_pad32, P, wq, sexp, stream);
 }
 
 int spb_adam_update(void* p, void* m, void* v, int p_is_f64, int rows, int cols, const void* g,

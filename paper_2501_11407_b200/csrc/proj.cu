@@ -511,43 +511,6 @@ __global__ void pack_spikes_kernel(const uint8_t* __restrict__ x, long long stri
   }
 }
 
-// One warp per neuron row: exponent of the row maximum, then P signed 7-bit digits.
-template <typename WT>
-__global__ void slice_weights_kernel(const WT* __restrict__ w, int n, int k, int Kpad, int n_pad32,
-                                     int P, int8_t* __restrict__ wq, int* __restrict__ sexp) {
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (i >= n_pad32) return;
-  double mx = 0.0;
-  if (i < n)
-    for (int j = lane; j < k; j += 32) mx = fmax(mx, fabs((double)w[(long long)i * k + j]));
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  int s = 0;
-  if (mx > 0.0) frexp(mx, &s);  // mx = f * 2^s, f in [0.5, 1)  =>  |w| < 2^s
-  if (lane == 0 && i < n) sexp[i] = s;
-  for (int j = lane; j < Kpad; j += 32) {
-    const double wv = (i < n && j < k) ? (double)w[(long long)i * k + j] : 0.0;
-    if (P == 6) {
-      // balanced radix-256 digits of R = rint(w 2^(46-s)), |R| < 2^46, least significant
-      // first: q = ((R + 128) mod 256) - 128 in [-128, 127], R <- (R - q) / 256 (exact)
-      long long R = (long long)rint(ldexp(wv, 46 - s));
-      for (int p = P - 1; p >= 0; --p) {
-        const long long q = ((R + 128) & 255) - 128;
-        R = (R - q) >> 8;
-        wq[((long long)p * n_pad32 + i) * Kpad + j] = (int8_t)q;
-      }
-    } else {
-      double r = ldexp(wv, -s);
-      for (int p = 0; p < P; ++p) {
-        const double t = r * (p == 0 ? 64.0 : 128.0);
-        const double qv = rint(t);
-        r = t - qv;
-        wq[((long long)p * n_pad32 + i) * Kpad + j] = (int8_t)(int)qv;
-      }
-    }
-  }
-}
-
 }  // namespace proj
 }  // namespace spb
 
@@ -569,20 +532,19 @@ int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits
   return 0;
 }
 
+int spb_launch_sgd_slice(void* w, int w_is_f64, int n, int k, const void* g, int g_is_f64,
+                         int ld_g, double g_scale, double lr, int do_sgd, int Kpad, int n_pad32,
+                         int P, int8_t* wq, int* sexp, cudaStream_t stream);  // optim.cu
+
 int spb_slice_weights(const void* w, int w_is_f64, int n, int k, int Kpad, int n_pad32, int P,
                       int8_t* wq, int* sexp, cudaStream_t stream) {
   SPB_CHECK_ARG(w && wq && sexp && n > 0 && k > 0 && Kpad >= k && n_pad32 >= n &&
                     n_pad32 % proj::NT == 0 && (P == 6 || P == 7 || P == 8),
                 "spb_slice_weights: bad args");
-  const int blocks = ceil_div(n_pad32 * 32, 256);
-  if (w_is_f64)
-    proj::slice_weights_kernel<double><<<blocks, 256, 0, stream>>>((const double*)w, n, k, Kpad,
-                                                                   n_pad32, P, wq, sexp);
-  else
-    proj::slice_weights_kernel<float><<<blocks, 256, 0, stream>>>((const float*)w, n, k, Kpad,
-                                                                  n_pad32, P, wq, sexp);
-  SPB_CHECK_LAUNCH("slice_weights");
-  return 0;
+  SPB_CHECK_ARG(Kpad % 128 == 0, "spb_slice_weights: Kpad must be a multiple of 128");
+  // the slicing pass of the fused SGD + slice kernel (optim.cu), without the update
+  return spb_launch_sgd_slice(const_cast<void*>(w), w_is_f64, n, k, nullptr, 0, k, 1.0, 0.0, 0,
+                              Kpad, n_pad32, P, wq, sexp, stream);
 }
 
 int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,

@@ -275,6 +275,15 @@ class EpropEngine:
                   self.k, self.Kpad, self.n_pad32, self.P, ctypes_void(self.wq.data_ptr()),
                   ctypes_void(self.sexp.data_ptr()), st)
 
+    def sgd_slice(self, g, g_is_f64: bool, ld_g: int, g_scale: float, lr: float, stream=None):
+        """``self.w <- self.w - lr * g_scale * g`` (the fused SGD kernel's arithmetic) and
+        the INT8 digits re-derived from the new W, in one launch (spb_sgd_slice_update)."""
+        st = ctypes_void(stream if stream is not None else self._stream())
+        _lib.call("spb_sgd_slice_update", ctypes_void(self.w.data_ptr()), int(self.w_f64),
+                  self.n, self.k, ctypes_void(g.data_ptr()), int(g_is_f64), int(ld_g),
+                  float(g_scale), float(lr), self.Kpad, self.n_pad32, self.P,
+                  ctypes_void(self.wq.data_ptr()), ctypes_void(self.sexp.data_ptr()), st)
+
     def _stream(self):
         if self.device.type != "cuda":
             return 0

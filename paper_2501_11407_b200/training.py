@@ -250,8 +250,8 @@ class DeviceTrainer:
         n, k, m = eng.n, eng.k, eng.m
         f64 = int(self.is_f64)
         if self.optimizer == "sgd":
-            self.lib.call("spb_sgd_update", v(self.w.data_ptr()), f64, n, k, v(g_w.data_ptr()),
-                          g_w_f64, ld_w, scale, self.lr, None, st)
+            # W update fused with the re-slicing of this engine's INT8 digits (one launch)
+            eng.sgd_slice(g_w, g_w_f64, ld_w, scale, self.lr, stream=st.value)
             self.lib.call("spb_sgd_update", v(self.w_out.data_ptr()), f64, m, n,
                           v(g_wo.data_ptr()), g_wo_f64, n, scale, self.lr,
                           v(eng.wout.data_ptr()), st)
@@ -274,8 +274,10 @@ class DeviceTrainer:
                               1, eng.kp, scale, self.lr, self.beta1, self.beta2, self.eps,
                               self.t, None, st)
             eng.wrecT.copy_(self.w_rec.t())
-        # this engine's digits follow the new W right away (the next update's K2)
-        eng.slice_weights()
+        # this engine's digits follow the new W right away (the next update's K2; the
+        # SGD kernel above already re-sliced them)
+        if self.optimizer != "sgd":
+            eng.slice_weights()
         eng._wver = self.t
         self._hist.append((stats, nb))
         return eng
