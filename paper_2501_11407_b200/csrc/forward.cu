@@ -23,6 +23,8 @@
 // so the gradient of a chunk is ONE GEMM over (sample, rho) with coefficient
 //   C_rho = R_rho [rho < L] + Lpsi_{rho-1} [rho >= 1]          (LIF: R = 0)
 // plus the elementwise M E0 term, and the carried trace is a per-sample GEMM with W.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace spb {
@@ -501,6 +503,165 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
 }
 
 // ------------------------------------------------------------------------------------
+// K1s on time segments: the same outputs as chunk_scan_kernel with S = 4 warps per 64
+// neurons, warp s scanning rows [lo_s, hi_s] of the chunk -- 4x the warps in flight for
+// the same bytes (the one-warp-per-64-neurons scan is latency-bound at small B*n).  The
+// ALIF recursion lam_r = A_{r+1} lam_{r+1} + q_r is linear in the value entering a
+// segment, so a first sweep gives each segment its local bottom value (entry 0), the
+// product G of its A factors and the product D of its carry factors; the segments then
+// meet in shared memory (top segment first, fixed order) and a second sweep emits the
+// rows.  fp32 results equal the sequential scan's up to fp32 rounding.
+// ------------------------------------------------------------------------------------
+constexpr int SEG = 4;
+
+template <bool ALIF, bool CARRY>
+__global__ void __launch_bounds__(SEG * 32) chunk_scan_seg_kernel(
+    FwdParams P, const float* __restrict__ wsig, const float* __restrict__ ctab,
+    uint32_t* __restrict__ c_hi, uint32_t* __restrict__ c_lo, uint32_t* __restrict__ w_hi,
+    uint32_t* __restrict__ w_lo, int ldc, float2* __restrict__ mdt,
+    const float* __restrict__ psis) {
+  extern __shared__ float cs[];  // cs[r] = c_{t0+r-1}, r = 0..L
+  __shared__ float2 sh_l[SEG][32], sh_g[SEG][32], sh_d[SEG][32];
+  const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+  const int L = P.len;
+  for (int r = threadIdx.x; r <= L; r += SEG * 32)
+    cs[r] = (P.t0 + r - 1 >= 0) ? ctab[P.t0 + r - 1] : 0.f;
+  const int i = blockIdx.x * 64 + 2 * lane;  // neurons i, i+1
+  const int b = blockIdx.y;
+  const int n = P.n;
+  const bool live = i < n;
+  const bool has2 = i + 1 < n;
+  const long long bi = (long long)b * n + i;
+  const float ws0 = live ? wsig[bi] : 0.f, ws1 = has2 ? wsig[bi + 1] : 0.f;
+  const float beta = (float)P.beta, rho = (float)P.rho;
+  const float* prow = psis + (long long)b * (P.KR + 1) * n + (live ? i : 0);
+  const bool vec = has2 && (n & 1) == 0;
+  auto ldpsi = [&](int r) -> float2 {
+    if (r < 0 || r > L || !live) return make_float2(0.f, 0.f);
+    const float* q = prow + (long long)r * n;
+    if (vec) return __ldcg(reinterpret_cast<const float2*>(q));
+    return make_float2(__ldcg(q), has2 ? __ldcg(q + 1) : 0.f);
+  };
+  // rows [lo, hi] of this warp's segment (top segment ends at L)
+  const int per = (L + 1 + SEG - 1) / SEG;
+  const int lo = seg * per, hi = min(L, lo + per - 1);
+  const long long ld2 = ldc >> 1;
+  const long long row0 = (long long)b * P.KR * ld2 + (i >> 1);
+  // rows past the chunk: zero (spread over the warps)
+  for (int r = L + 1 + seg; r < P.KR; r += SEG)
+    if (live) {
+      c_hi[row0 + r * ld2] = 0u;
+      c_lo[row0 + r * ld2] = 0u;
+      if (CARRY) { w_hi[row0 + r * ld2] = 0u; w_lo[row0 + r * ld2] = 0u; }
+    }
+  // entry state of the segment: row hi+1's psi and A (none above the top row L)
+  const float2 up0 = (hi < L) ? ldpsi(hi + 1) : make_float2(0.f, 0.f);
+  const float an0_in = (ALIF && hi < L && hi + 1 < L) ? fmaf(-beta, up0.x, rho) : 0.f;
+  const float an1_in = (ALIF && hi < L && hi + 1 < L) ? fmaf(-beta, up0.y, rho) : 0.f;
+  float lam0 = 0.f, lam1 = 0.f, dcum0 = 1.f, dcum1 = 1.f;
+  __syncthreads();  // cs
+  if (ALIF && lo <= hi) {
+    // sweep 1: local bottom value, G = prod of the A's applied to the entry, D = prod A_r
+    float l0 = 0.f, l1 = 0.f, g0 = 1.f, g1 = 1.f, d0 = 1.f, d1 = 1.f;
+    float an0 = an0_in, an1 = an1_in;
+    float2 up = up0;
+    constexpr int PF1 = 8;
+    float2 pq[PF1];
+#pragma unroll
+    for (int u = 0; u < PF1; ++u) pq[u] = (hi - u >= lo) ? ldpsi(hi - u) : make_float2(0.f, 0.f);
+    for (int r = hi; r >= lo; --r) {
+      const float2 cur = pq[0];
+#pragma unroll
+      for (int u = 0; u < PF1 - 1; ++u) pq[u] = pq[u + 1];
+      pq[PF1 - 1] = (r - PF1 >= lo) ? ldpsi(r - PF1) : make_float2(0.f, 0.f);
+      if (r < L) {
+        const float c_r = cs[r + 1];
+        const float A0 = fmaf(-beta, cur.x, rho), A1 = fmaf(-beta, cur.y, rho);
+        l0 = fmaf(an0, l0, -beta * (c_r * ws0 * up.x));
+        l1 = fmaf(an1, l1, -beta * (c_r * ws1 * up.y));
+        g0 *= an0;
+        g1 *= an1;
+        d0 *= A0;
+        d1 *= A1;
+        an0 = A0;
+        an1 = A1;
+      }
+      up = cur;
+    }
+    sh_l[seg][lane] = make_float2(l0, l1);
+    sh_g[seg][lane] = make_float2(g0, g1);
+    sh_d[seg][lane] = make_float2(d0, d1);
+  }
+  if (ALIF) {
+    __syncthreads();
+    // entry of this segment: the segments above, top first (fixed order)
+    for (int q = SEG - 1; q > seg; --q) {
+      const int qlo = q * per, qhi = min(L, qlo + per - 1);
+      if (qlo > qhi) continue;
+      const float2 gl = sh_l[q][lane], gg = sh_g[q][lane], gd = sh_d[q][lane];
+      lam0 = fmaf(gg.x, lam0, gl.x);
+      lam1 = fmaf(gg.y, lam1, gl.y);
+      dcum0 *= gd.x;
+      dcum1 *= gd.y;
+    }
+  }
+  if (lo > hi) return;
+  // sweep 2: the rows, exactly the sequential scan's step from the segment's entry
+  uint32_t* chp = c_hi + row0 + (long long)hi * ld2;
+  uint32_t* clp = c_lo + row0 + (long long)hi * ld2;
+  uint32_t* whp = CARRY ? w_hi + row0 + (long long)hi * ld2 : nullptr;
+  uint32_t* wlp = CARRY ? w_lo + row0 + (long long)hi * ld2 : nullptr;
+  float an0 = an0_in, an1 = an1_in;
+  float2 up = up0;
+  constexpr int PF = 8;
+  float2 qv[PF];
+#pragma unroll
+  for (int u = 0; u < PF; ++u) qv[u] = (hi - u >= lo) ? ldpsi(hi - u) : make_float2(0.f, 0.f);
+  for (int r = hi; r >= lo; --r) {
+    const float2 cur = qv[0];
+#pragma unroll
+    for (int u = 0; u < PF - 1; ++u) qv[u] = qv[u + 1];
+    qv[PF - 1] = (r - PF >= lo) ? ldpsi(r - PF) : make_float2(0.f, 0.f);
+    const float c_prev = cs[r], c_r = (r < L) ? cs[r + 1] : 0.f;
+    float c0 = r >= 1 ? c_prev * ws0 * cur.x : 0.f;
+    float c1 = r >= 1 ? c_prev * ws1 * cur.y : 0.f;
+    float w0 = 0.f, w1 = 0.f;
+    if (ALIF && r < L) {
+      const float A0 = fmaf(-beta, cur.x, rho), A1 = fmaf(-beta, cur.y, rho);
+      lam0 = fmaf(an0, lam0, -beta * (c_r * ws0 * up.x));
+      lam1 = fmaf(an1, lam1, -beta * (c_r * ws1 * up.y));
+      c0 = fmaf(cur.x, lam0, c0);
+      c1 = fmaf(cur.y, lam1, c1);
+      w0 = cur.x * dcum0;
+      w1 = cur.y * dcum1;
+      dcum0 *= A0;
+      dcum1 *= A1;
+      an0 = A0;
+      an1 = A1;
+    }
+    if (live) {
+      uint32_t h, l;
+      split_bf16x2(c0, c1, h, l);
+      *chp = h;
+      *clp = l;
+      if (CARRY) {
+        split_bf16x2(w0, w1, h, l);
+        *whp = h;
+        *wlp = l;
+      }
+    }
+    chp -= ld2;
+    clp -= ld2;
+    if (CARRY) { whp -= ld2; wlp -= ld2; }
+    up = cur;
+  }
+  if (ALIF && mdt != nullptr && seg == 0 && live) {  // M = A_0 Lambda_0, Dt = prod A
+    mdt[bi] = make_float2(an0 * lam0, dcum0);
+    if (has2) mdt[bi + 1] = make_float2(an1 * lam1, dcum1);
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // K1r: backward scan of one chunk with reset=True (neurons.py:266-271: the soft reset makes
 // G_u per-synapse, h_uu = alpha - theta psi^-, and couples it to G_a, h_ua = theta beta
 // psi^-).  The trace g = (G_u, G_a) of one synapse obeys g_r = A_r g_{r-1} + e_u x_r with
@@ -750,6 +911,12 @@ __global__ void __launch_bounds__(128) xbar_chunk4_kernel(
 
 using namespace spb;
 
+// segmented scan selection (SPB_SCAN_SEG=0 restores the one-sweep scan, for A/B runs)
+static bool seg_scan() {
+  const char* e = getenv("SPB_SCAN_SEG");
+  return !(e && e[0] == '0');
+}
+
 extern "C" {
 
 int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR, int len, int t0,
@@ -799,6 +966,20 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
     const bool carry = alif && w_hi != nullptr;
     auto kfn = alif ? (carry ? chunk_scan_kernel<true, true> : chunk_scan_kernel<true, false>)
                     : chunk_scan_kernel<false, false>;
+    // segments pay off where the one-sweep grid is small (C2: 0.058 -> 0.031 ms); for
+    // ALIF they cost a second psi sweep, a loss once the grid fills the GPU (C3)
+    if (seg_scan() && (!alif || (long long)B * ceil_div(n, 2 * K1S_THREADS) < 2LL * 148)) {
+      auto sfn = alif ? (carry ? chunk_scan_seg_kernel<true, true>
+                               : chunk_scan_seg_kernel<true, false>)
+                      : chunk_scan_seg_kernel<false, false>;
+      dim3 g2(ceil_div(n, 64), B);
+      sfn<<<g2, SEG * 32, (len + 1) * sizeof(float), stream>>>(
+          P, wsig, ctab, reinterpret_cast<uint32_t*>(c_hi), reinterpret_cast<uint32_t*>(c_lo),
+          reinterpret_cast<uint32_t*>(w_hi), reinterpret_cast<uint32_t*>(w_lo), ldc,
+          reinterpret_cast<float2*>(mdt), psi_scratch);
+      SPB_CHECK_LAUNCH("chunk_scan_seg");
+      return 0;
+    }
     kfn<<<sgrid, K1S_THREADS, (len + 1) * sizeof(float), stream>>>(
         P, wsig, ctab, reinterpret_cast<uint32_t*>(c_hi), reinterpret_cast<uint32_t*>(c_lo),
         reinterpret_cast<uint32_t*>(w_hi), reinterpret_cast<uint32_t*>(w_lo), ldc,

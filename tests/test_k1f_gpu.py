@@ -69,3 +69,22 @@ def test_k1f_matches_three_launch_path(kind, n, k, m, B, T, prec, smooth):
     cos = float(np.dot(a["gw"].ravel(), b["gw"].ravel()) /
                 (np.linalg.norm(a["gw"]) * np.linalg.norm(b["gw"]) + 1e-300))
     assert cos > 0.99999
+
+
+@pytest.mark.parametrize("kind,n,B,T", [("lif", 256, 6, 100), ("alif", 192, 5, 120),
+                                         ("alif", 70, 3, 300)])
+def test_segmented_scan_matches_one_sweep(kind, n, B, T, monkeypatch):
+    """K1s on 4 time segments (chunk_scan_seg_kernel) vs the one-sweep scan."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    net = P.init_network(P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=50, n_classes=4,
+                                       precision="f32", seed=3))
+    x, y = poisson_batch(B, 50, T, 4, seed=5)
+    monkeypatch.setenv("SPB_SCAN_SEG", "1")
+    a = _run(net, x, y, k1f=False)
+    monkeypatch.setenv("SPB_SCAN_SEG", "0")
+    b = _run(net, x, y, k1f=False)
+    assert np.array_equal(a["raster"], b["raster"])
+    assert _rel(a["gw"], b["gw"]) < 1e-5
