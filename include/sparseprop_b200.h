@@ -174,6 +174,11 @@ int spb_pack_rec(const uint8_t* xq, long long xq_sb, long long xq_st, const uint
 int spb_xbar_chunk(const uint8_t* x, long long stride_b, long long stride_t, int B, int k, int kp,
                    int KR, int len, int fresh, double alpha, double* xbar_state, void* xh,
                    void* xl, cudaStream_t stream);
+/* Same contract as spb_xbar_chunk, computed on 64-row time segments (KR/64 x the threads;
+ * values equal up to fp64 rounding): for a K4 on the critical path (multi-chunk pass B). */
+int spb_xbar_chunk_seg(const uint8_t* x, long long stride_b, long long stride_t, int B, int k, int kp,
+                       int KR, int len, int fresh, double alpha, double* xbar_state, void* xh,
+                       void* xl, cudaStream_t stream);
 
 /* K3  Readout + loss: s_b = W_out zsum_b, loss_b = CE(s_b, y_b), g_b = softmax - onehot,
  *     wsig_b = W_out^T g_b.  Replaces gradients.py:163-164,177-178 and

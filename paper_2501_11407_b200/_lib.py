@@ -35,6 +35,7 @@ SIGNATURES = {
     "spb_forward_scan_chunk": [P, I, I, I, I, I, I, D, D, D, D, D, D, I, I, P, P, P, P, P, P,
                                P, P, I, P, P, P, P, P, P, P, P, I, P, P, P],
     "spb_xbar_chunk": [P, LL, LL, I, I, I, I, I, I, D, P, P, P, P],
+    "spb_xbar_chunk_seg": [P, LL, LL, I, I, I, I, I, I, D, P, P, P, P],
     "spb_readout_loss": [P, P, P, I, I, I, P, P, P, P, P, P],
     "spb_readout_grad": [P, P, I, I, I, P, P],
     "spb_grad_gemm_partials": [P, P, I, P, P, I, I, I, I, I, P, I, LL, P],

@@ -907,6 +907,117 @@ __global__ void __launch_bounds__(128) xbar_chunk4_kernel(
     if (j + c < k) xbar_st[(long long)b * k + j + c] = xb[c];
 }
 
+// K4 on time segments: warp s of a CTA filters rows rho in [64 s, 64 s + 63] of 128
+// channels (4 per lane) -- KR/64 x the threads of xbar_chunk4_kernel for the same bytes
+// (one 64-row segment per warp).  The filter is linear: sweep 1 runs each segment from a
+// zero entry (segment 0 from the true carry) to get its end value, the segments meet in
+// shared memory in time order (E <- alpha^len E + end), and sweep 2 re-reads the spike
+// bytes (L1/L2-hot) and writes the rows from the true entry.  fp64 throughout; the values
+// equal the sequential filter's up to fp64 rounding (they are then split to bf16 hi/lo).
+constexpr int XSEG_ROWS = 64;
+
+__global__ void __launch_bounds__(256) xbar_seg_kernel(
+    const uint8_t* __restrict__ x, long long stride_b, long long stride_t, int B, int k, int kp,
+    int KR, int len, int fresh, double alpha, double* __restrict__ xbar_st,
+    uint2* __restrict__ xh, uint2* __restrict__ xl) {
+  __shared__ double sh_end[8][32][4];
+  __shared__ double sh_pow[8];
+  const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+  const int nseg = blockDim.x >> 5;
+  const int jq = blockIdx.x * 32 + lane;  // channel quad
+  const int j = 4 * jq;
+  const int b = blockIdx.y;
+  const bool any = j < k;
+  const uint32_t keep = j + 4 <= k ? 0xffffffffu : (any ? (0xffffffffu >> (8 * (j + 4 - k))) : 0u);
+  const uint32_t* xin = reinterpret_cast<const uint32_t*>(x + (long long)b * stride_b + (any ? j : 0));
+  const long long st4 = stride_t >> 2;
+  double xb_in[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    xb_in[c] = (j + c < k && !fresh) ? xbar_st[(long long)b * k + j + c] : 0.0;
+  const int lo = seg * XSEG_ROWS, hi = lo + XSEG_ROWS - 1;
+  auto xword = [&](int rho) -> uint32_t {  // spikes of step rho - 1 (rows 1..len)
+    return (any && rho >= 1 && rho <= len) ? (__ldg(xin + (long long)(rho - 1) * st4) & keep) : 0u;
+  };
+  // ---- sweep 1: end value of this segment from a zero entry (segment 0: the carry) ----
+  if (seg + 1 < nseg) {
+    double y[4];
+    double apow = 1.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) y[c] = (seg == 0) ? xb_in[c] : 0.0;
+    for (int r8 = lo; r8 <= hi; r8 += 8) {
+      uint32_t w8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) w8[u] = xword(r8 + u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int rho = r8 + u;
+        if (rho >= 1 && rho <= len) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            y[c] = __dadd_rn(__dmul_rn(alpha, y[c]), (double)((w8[u] >> (8 * c)) & 0xffu));
+          apow = __dmul_rn(apow, alpha);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sh_end[seg][lane][c] = y[c];
+    if (lane == 0) sh_pow[seg] = apow;
+  }
+  __syncthreads();
+  // ---- entry of this segment: the segments before it, in time order ----
+  double xv[4];
+  if (seg == 0) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) xv[c] = xb_in[c];
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) xv[c] = 0.0;
+    for (int q = 0; q < seg; ++q) {
+      const double ap = sh_pow[q];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        xv[c] = (q == 0) ? sh_end[0][lane][c] : __dadd_rn(__dmul_rn(ap, xv[c]), sh_end[q][lane][c]);
+    }
+  }
+  if (jq >= (kp >> 2)) return;
+  // ---- sweep 2: the rows ----
+  const long long ld4 = kp >> 2;
+  uint2* oh = xh + ((long long)b * KR + lo) * ld4 + jq;
+  uint2* ol = xl + ((long long)b * KR + lo) * ld4 + jq;
+  for (int r8 = lo; r8 <= hi; r8 += 8) {
+    uint32_t w8[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) w8[u] = xword(r8 + u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int rho = r8 + u;
+      float f[4] = {0.f, 0.f, 0.f, 0.f};
+      if (rho == 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) f[c] = (float)xv[c];
+      } else if (rho <= len) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          xv[c] = __dadd_rn(__dmul_rn(alpha, xv[c]), (double)((w8[u] >> (8 * c)) & 0xffu));
+          f[c] = (float)xv[c];
+        }
+      }
+      uint2 h, l;
+      split_bf16x2(f[0], f[1], h.x, l.x);
+      split_bf16x2(f[2], f[3], h.y, l.y);
+      oh[(long long)(rho - lo) * ld4] = h;
+      ol[(long long)(rho - lo) * ld4] = l;
+    }
+    // the carried state xbar_{t0+len-1} lives in row len: its segment stores it
+    if (r8 <= len && len < r8 + 8) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (j + c < k) xbar_st[(long long)b * k + j + c] = xv[c];
+    }
+  }
+}
+
 }  // namespace spb
 
 using namespace spb;
@@ -1019,15 +1130,49 @@ int spb_forward_scan_chunk(const double* cur, int B, int n, int Tc, int KR, int 
   return 0;
 }
 
+static int xbar_launch(const uint8_t* x, long long stride_b, long long stride_t, int B, int k,
+                       int kp, int KR, int len, int fresh, double alpha, double* xbar_state,
+                       void* xh, void* xl, bool segmented, cudaStream_t stream);
+
 int spb_xbar_chunk(const uint8_t* x, long long stride_b, long long stride_t, int B, int k, int kp,
                    int KR, int len, int fresh, double alpha, double* xbar_state, void* xh,
                    void* xl, cudaStream_t stream) {
+  return xbar_launch(x, stride_b, stride_t, B, k, kp, KR, len, fresh, alpha, xbar_state, xh, xl,
+                     false, stream);
+}
+
+// K4 on 64-row time segments (more threads, for a K4 on the critical path; the one-chunk
+// K4 overlapped with K1 keeps the sequential kernel, measured better there).
+// SPB_XBAR_SEG=0 falls back to the sequential kernel (A/B runs, tests).
+int spb_xbar_chunk_seg(const uint8_t* x, long long stride_b, long long stride_t, int B, int k,
+                       int kp, int KR, int len, int fresh, double alpha, double* xbar_state,
+                       void* xh, void* xl, cudaStream_t stream) {
+  const char* es = getenv("SPB_XBAR_SEG");
+  return xbar_launch(x, stride_b, stride_t, B, k, kp, KR, len, fresh, alpha, xbar_state, xh, xl,
+                     !(es && es[0] == '0'), stream);
+}
+
+}  // extern "C"
+
+static int xbar_launch(const uint8_t* x, long long stride_b, long long stride_t, int B, int k,
+                       int kp, int KR, int len, int fresh, double alpha, double* xbar_state,
+                       void* xh, void* xl, bool segmented, cudaStream_t stream) {
   SPB_CHECK_ARG(x && xbar_state && xh && xl, "spb_xbar_chunk: null pointer");
   SPB_CHECK_ARG(B > 0 && k > 0 && kp >= k && kp % 8 == 0 && KR > 0 && KR % 8 == 0 && len >= 0 &&
                     len < KR,
                 "spb_xbar_chunk: bad sizes");
-  if ((stride_b | stride_t) % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0 &&
-      reinterpret_cast<uintptr_t>(xh) % 8 == 0 && reinterpret_cast<uintptr_t>(xl) % 8 == 0) {
+  const bool al4 = (stride_b | stride_t) % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0 &&
+                   reinterpret_cast<uintptr_t>(xh) % 8 == 0 &&
+                   reinterpret_cast<uintptr_t>(xl) % 8 == 0;
+  if (segmented && al4 && KR % XSEG_ROWS == 0 && KR / XSEG_ROWS <= 8) {
+    dim3 gs(ceil_div(kp / 4, 32), B);
+    xbar_seg_kernel<<<gs, 32 * (KR / XSEG_ROWS), 0, stream>>>(
+        x, stride_b, stride_t, B, k, kp, KR, len, fresh, alpha, xbar_state,
+        reinterpret_cast<uint2*>(xh), reinterpret_cast<uint2*>(xl));
+    SPB_CHECK_LAUNCH("xbar_seg");
+    return 0;
+  }
+  if (al4) {
     dim3 grid4(ceil_div(kp / 4, 128), B);
     xbar_chunk4_kernel<<<grid4, 128, 0, stream>>>(x, stride_b, stride_t, B, k, kp, KR, len, fresh,
                                                   alpha, xbar_state, reinterpret_cast<uint2*>(xh),
@@ -1044,4 +1189,4 @@ int spb_xbar_chunk(const uint8_t* x, long long stride_b, long long stride_t, int
   return 0;
 }
 
-}  // extern "C"
+

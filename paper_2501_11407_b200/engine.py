@@ -554,7 +554,7 @@ class EpropEngine:
                 call("spb_pack_rec", v(self.xq.data_ptr()), xq_sb, xq_st,
                      v(self.zchunk.data_ptr()), B, k, n, Tc, KR, ln, self.Kx2,
                      v(self.xq2.data_ptr()), st)
-                call("spb_xbar_chunk", v(self.xq2.data_ptr()), Tc * self.Kx2, self.Kx2, B,
+                call("spb_xbar_chunk_seg", v(self.xq2.data_ptr()), Tc * self.Kx2, self.Kx2, B,
                      self.kx, self.kp, KR, ln, int(c == 0 or self.reset), x_alpha,
                      v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()), v(self.xl.data_ptr()),
                      st)
@@ -562,7 +562,7 @@ class EpropEngine:
             elif one and use_side and self.xbar_sched != "main":
                 main.wait_event(self._ev["xbar"])
             else:
-                call("spb_xbar_chunk", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
+                call("spb_xbar_chunk_seg", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
                      ln, int(c == 0 or self.reset), x_alpha, v(self.xbar_state.data_ptr()),
                      v(self.xh.data_ptr()), v(self.xl.data_ptr()), st)
                 self.launches += 1

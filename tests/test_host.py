@@ -6,6 +6,8 @@ import ctypes
 import os
 import re
 
+XB = ("spb_xbar_chunk", "spb_xbar_chunk_seg")  # K4: sequential / time-segmented entry
+
 import numpy as np
 import pytest
 import torch
@@ -111,7 +113,7 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     assert names.count("spb_pack_spikes") == (2 * nch if nch > 1 else 1)
     assert names.count("spb_input_proj") == (2 * nch if nch > 1 else 1)
     assert names.count("spb_slice_weights") == 0
-    assert names.count("spb_xbar_chunk") == nch
+    assert sum(names.count(x) for x in XB) == nch
     assert names.count("spb_grad_gemm_partials") == nch
     carries = [c[1] for c in rec.calls if c[0] == "spb_alif_carry_chunk"]
     if alif:
@@ -143,7 +145,7 @@ def test_engine_reset_dry_run(monkeypatch, alif):
     with pytest.raises(ValueError):
         eng.run(x, torch.zeros(6, dtype=torch.int64), reset=False)
     eng.run(x, torch.zeros(6, dtype=torch.int64), reset=True)
-    xb = [c[1] for c in rec.calls if c[0] == "spb_xbar_chunk"]
+    xb = [c[1] for c in rec.calls if c[0] in XB]
     assert xb and all(a[8] == 1 and a[9] == 0.0 for a in xb)      # fresh, alpha = 0
     fw = [c[1] for c in rec.calls if c[0] == "spb_forward_chunk"]
     assert all(a[15] == 1 for a in fw)                              # reset flag
@@ -165,10 +167,10 @@ def test_engine_recurrent_dry_run(monkeypatch):
     eng.run(torch.zeros((6, 150, 30), dtype=torch.uint8), torch.zeros(6, dtype=torch.int64))
     names = [c[0] for c in rec.calls]
     assert names.count("spb_forward_rec_chunk") == 6          # 3 chunks x 2 passes
-    assert names.count("spb_pack_rec") == 3 and names.count("spb_xbar_chunk") == 3
+    assert names.count("spb_pack_rec") == 3 and sum(names.count(x) for x in XB) == 3
     fw = [c[1] for c in rec.calls if c[0] == "spb_forward_chunk"]
     assert fw and all(a[0] == 2 for a in fw)                  # scans only
-    xb = [c[1] for c in rec.calls if c[0] == "spb_xbar_chunk"]
+    xb = [c[1] for c in rec.calls if c[0] in XB]
     assert all(a[4] == 70 for a in xb)                        # filters k + n columns
     with pytest.raises(P.ShapeMismatch):
         eng.set_weights(torch.zeros(40, 30), torch.zeros(3, 40))   # w_rec missing
@@ -183,7 +185,7 @@ def test_engine_forward_only_dry_run(monkeypatch):
     names = [c[0] for c in rec.calls]
     assert names.count("spb_forward_chunk") == 3 and names.count("spb_input_proj") == 3
     assert names[-1] == "spb_readout_loss"
-    for n in ("spb_xbar_chunk", "spb_grad_gemm_partials", "spb_alif_carry_chunk",
+    for n in ("spb_xbar_chunk", "spb_xbar_chunk_seg", "spb_grad_gemm_partials", "spb_alif_carry_chunk",
               "spb_readout_grad"):
         assert n not in names
     # smooth flag reaches the kernel (argument after `alif`)

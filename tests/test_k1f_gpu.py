@@ -88,3 +88,33 @@ def test_segmented_scan_matches_one_sweep(kind, n, B, T, monkeypatch):
     b = _run(net, x, y, k1f=False)
     assert np.array_equal(a["raster"], b["raster"])
     assert _rel(a["gw"], b["gw"]) < 1e-5
+
+
+@pytest.mark.parametrize("kind,n,k,B,T,chunk", [("alif", 128, 700, 4, 250, 255),
+                                                 ("lif", 96, 37, 3, 300, 127),
+                                                 ("alif", 64, 130, 2, 700, 511)])
+def test_segmented_xbar_matches_sequential(kind, n, k, B, T, chunk, monkeypatch):
+    """K4 on 64-row time segments (xbar_seg_kernel) vs the sequential 4-channel filter,
+    one and several chunks (the carried fp64 filter state crosses chunk boundaries)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200.gradients import _neuron_kwargs
+    net = P.init_network(P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=4,
+                                       precision="f32", seed=9))
+    x, y = poisson_batch(B, k, T, 4, seed=2)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SPB_XBAR_SEG", flag)
+        eng = EpropEngine(n, k, 4, B, alif=net.is_alif, chunk=chunk)
+        eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+        eng.run(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), **_neuron_kwargs(net))
+        torch.cuda.synchronize()
+        out[flag] = (eng.grad_w_acc.cpu().numpy().copy(), eng.xbar_state.cpu().numpy().copy(),
+                     eng.xh.float().cpu().numpy().copy())
+    a, b = out["1"], out["0"]
+    np.testing.assert_allclose(a[1], b[1], rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(a[2], b[2], rtol=2 ** -7, atol=0)
+    assert _rel(a[0], b[0]) < 1e-6
