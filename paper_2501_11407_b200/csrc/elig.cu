@@ -17,23 +17,27 @@
 // work of the literal recursion moves onto the tensor cores.
 //
 // Kernel structure (one 128-neuron x 128-input tile per CTA, a contiguous sample range per
-// blockIdx.z):  warp 0 TMA producer (W hi/lo, xbar hi/lo K-blocks, 3-stage ring), warp 1
-// TMEM owner + single-thread tcgen05.mma issuer (bf16 hi/lo split: hi*hi + hi*lo + lo*hi,
-// fp32 accumulation in one of two TMEM buffers), warps 2-9 epilogue: tcgen05.ld of the
-// sample's product, eps load/update/store, gradient tile in registers across samples.
+// blockIdx.z):  warp 0 TMA producer of the W hi/lo, xbar hi/lo K-blocks (5-stage ring),
+// warp 1 TMEM owner + tcgen05.mma issuer (bf16 hi/lo split: hi*hi + hi*lo + lo*hi, fp32
+// accumulation in one of two TMEM buffers), warp 2 TMA producer of the eps tiles, warps
+// 3-18 epilogue: tcgen05.ld of the sample's product, eps update/store, gradient tile in
+// registers across samples.
 #include "tma.cuh"
 
 namespace spb {
 namespace carry {
 
 // Tile: 128 neurons (TMEM lanes) x 128 inputs (TMEM columns); K blocks of 32 rows.
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 5;
 constexpr int TILE = BM * BK * 2;               // 8 KB (two 64-wide MN-major boxes)
 constexpr int STAGE = 4 * TILE;                 // W hi/lo + xbar hi/lo
 constexpr int ETILE = BM * BN * 4;              // 64 KB eps tile (4 boxes of 128 x 32 fp32)
 constexpr int EPI_WARPS = 16;                   // 4 TMEM lane quarters x 4 column groups of 32
-constexpr int THREADS = 64 + EPI_WARPS * 32;
-constexpr int SMEM = 2 * ETILE + STAGES * STAGE + 1024 + 256;
+constexpr int EPI0 = 3;                         // warps 0-2: operand TMA, MMA, eps TMA
+constexpr int THREADS = EPI0 * 32 + EPI_WARPS * 32;
+// one eps tile (single-buffered: its own producer warp refills it while the next sample's
+// MMAs run) leaves room for 5 operand stages -- the L2 operand stream is latency-bound
+constexpr int SMEM = ETILE + STAGES * STAGE + 1024 + 256;
 // A = W, B = xbar, both MN-major (neurons / channels contiguous, written by K1s / K4)
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -76,12 +80,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Per CTA: one 128x128 synapse tile, a contiguous range of samples.  Warp 0 streams, per
-// sample, the sample's eps~ tile E0 (4 TMA boxes, SWIZZLE_128B, double-buffered so the next
-// sample's tile is in flight while this one is consumed) and the W / xbar K-blocks of the
-// per-sample GEMM (3-stage ring); warp 1 issues the tcgen05 MMAs into one of two TMEM
-// buffers; 16 epilogue warps combine E_end = Dt E0 + D (written back with plain stores)
-// and grad += M E0 (registers across samples).
+// Per CTA: one 128x128 synapse tile, a contiguous range of samples.  Warp 0 streams the
+// W / xbar K-blocks of each sample's GEMM (5-stage ring), warp 2 the sample's eps~ tile E0
+// (4 TMA boxes, SWIZZLE_128B, single-buffered: it is refilled as soon as the epilogue has
+// read it, while the next sample's MMAs run); warp 1 issues the tcgen05 MMAs into one of
+// two TMEM buffers; 16 epilogue warps combine E_end = Dt E0 + D (written back with plain
+// stores) and grad += M E0 (registers across samples).
 __global__ void __launch_bounds__(THREADS, 1)
     alif_carry_kernel(const __grid_constant__ CUtensorMap tm_wh, const __grid_constant__ CUtensorMap tm_wl,
                       const __grid_constant__ CUtensorMap tm_xh, const __grid_constant__ CUtensorMap tm_xl,
@@ -92,16 +96,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* esm = smem;                             // [2][4 boxes][128 rows][128 B]
-  uint8_t* osm = smem + 2 * ETILE;                 // [STAGES][4][TILE]
+  uint8_t* esm = smem;                             // [4 boxes][128 rows][128 B]
+  uint8_t* osm = smem + ETILE;                     // [STAGES][4][TILE]
   uint64_t* bars = reinterpret_cast<uint64_t*>(osm + STAGES * STAGE);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
   uint64_t* efull = bars + 2 * STAGES + 4;
-  uint64_t* eempty = bars + 2 * STAGES + 6;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 8);
+  uint64_t* eempty = bars + 2 * STAGES + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 6);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
@@ -117,9 +121,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&tfull[a]), 1);
       mbar_init(smem_u32(&tempty[a]), EPI_WARPS);
-      mbar_init(smem_u32(&efull[a]), 1);
-      mbar_init(smem_u32(&eempty[a]), EPI_WARPS);
     }
+    mbar_init(smem_u32(efull), 1);
+    mbar_init(smem_u32(eempty), EPI_WARPS);
     mbar_fence_init();
     if (do_mma) {
       tma_prefetch_desc(&tm_wh);
@@ -141,39 +145,38 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (lane == 0 && do_mma) {  // operand K-blocks of every sample's GEMM
       int it = 0;
       for (int lb = 0; lb < nb; ++lb) {
-        const int b = b0 + lb;
-        if (load_eps) {  // this sample's eps~ tile, 4 boxes of 32 columns
-          const int eb = lb & 1;
-          mbar_wait(smem_u32(&eempty[eb]), ((lb >> 1) & 1) ^ 1);
-          const uint32_t fb = smem_u32(&efull[eb]);
-          mbar_expect_tx(fb, ETILE);
+        const int kbase = (b0 + lb) * KR;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(smem_u32(&empty[s]), ((it / STAGES) & 1) ^ 1);
+          const uint32_t st = smem_u32(osm + s * STAGE);
+          const uint32_t fb = smem_u32(&full[s]);
+          mbar_expect_tx(fb, STAGE);
+          const int kr = kbase + kb * BK;
+          tma_load_2d(st, &tm_wh, fb, i0, kr);
+          tma_load_2d(st + TILE / 2, &tm_wh, fb, i0 + 64, kr);
+          tma_load_2d(st + TILE, &tm_wl, fb, i0, kr);
+          tma_load_2d(st + TILE + TILE / 2, &tm_wl, fb, i0 + 64, kr);
+          tma_load_2d(st + 2 * TILE, &tm_xh, fb, j0, kr);
+          tma_load_2d(st + 2 * TILE + TILE / 2, &tm_xh, fb, j0 + 64, kr);
+          tma_load_2d(st + 3 * TILE, &tm_xl, fb, j0, kr);
+          tma_load_2d(st + 3 * TILE + TILE / 2, &tm_xl, fb, j0 + 64, kr);
+        }
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0 && load_eps) {  // each sample's eps~ tile E0, 4 boxes of 32 columns
+      for (int lb = 0; lb < nb; ++lb) {
+        mbar_wait(smem_u32(eempty), (lb & 1) ^ 1);
+        const uint32_t fb = smem_u32(efull);
+        mbar_expect_tx(fb, ETILE);
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            tma_load_2d(smem_u32(esm + eb * ETILE + q * (ETILE / 4)), &tm_eps, fb, j0 + 32 * q,
-                        b * n_pad + i0);
-        }
-        if (do_mma) {
-          const int kbase = b * KR;
-          for (int kb = 0; kb < nkb; ++kb, ++it) {
-            const int s = it % STAGES;
-            mbar_wait(smem_u32(&empty[s]), ((it / STAGES) & 1) ^ 1);
-            const uint32_t st = smem_u32(osm + s * STAGE);
-            const uint32_t fb = smem_u32(&full[s]);
-            mbar_expect_tx(fb, STAGE);
-            const int kr = kbase + kb * BK;
-            tma_load_2d(st, &tm_wh, fb, i0, kr);
-            tma_load_2d(st + TILE / 2, &tm_wh, fb, i0 + 64, kr);
-            tma_load_2d(st + TILE, &tm_wl, fb, i0, kr);
-            tma_load_2d(st + TILE + TILE / 2, &tm_wl, fb, i0 + 64, kr);
-            tma_load_2d(st + 2 * TILE, &tm_xh, fb, j0, kr);
-            tma_load_2d(st + 2 * TILE + TILE / 2, &tm_xh, fb, j0 + 64, kr);
-            tma_load_2d(st + 3 * TILE, &tm_xl, fb, j0, kr);
-            tma_load_2d(st + 3 * TILE + TILE / 2, &tm_xl, fb, j0 + 64, kr);
-          }
-        }
+        for (int q = 0; q < 4; ++q)
+          tma_load_2d(smem_u32(esm + q * (ETILE / 4)), &tm_eps, fb, j0 + 32 * q,
+                      (b0 + lb) * n_pad + i0);
       }
     }
   } else if (warp == 1) {
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     const int q = warp & 3;            // TMEM lane quarter of this warp
-    const int cg = (warp - 2) >> 2;    // 32-column group = eps box
+    const int cg = (warp - EPI0) >> 2; // 32-column group = eps box
     const int r = q * 32 + lane;       // tile-local neuron row
     const int i = i0 + r;
     const bool vi = i < n;
@@ -218,10 +221,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int lb = 0; lb < nb; ++lb) {
       const int b = b0 + lb;
       const int a = lb & 1;
-      const int eb = lb & 1;
       const float2 md = vi ? mdt[(long long)b * n + i] : make_float2(0.f, 0.f);
-      const uint32_t erow = smem_u32(esm + eb * ETILE + cg * (ETILE / 4) + r * 128);
-      if (load_eps) mbar_wait(smem_u32(&efull[eb]), (lb >> 1) & 1);
+      const uint32_t erow = smem_u32(esm + cg * (ETILE / 4) + r * 128);
+      if (load_eps) mbar_wait(smem_u32(efull), lb & 1);
       if (do_mma) {
         mbar_wait(smem_u32(&tfull[a]), (lb >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         if (lane == 0) arrive(smem_u32(&tempty[a]));
       }
-      if (load_eps && lane == 0) arrive(smem_u32(&eempty[eb]));
+      if (load_eps && lane == 0) arrive(smem_u32(eempty));
     }
     if (vi) {
       float* prow = partial + ((long long)blockIdx.z * n_pad + i) * kp + c0;

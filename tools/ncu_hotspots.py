@@ -7,9 +7,11 @@ def main(path, top=25):
     raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hi = [i for i, r in enumerate(rows) if r and r[0] == "Address"][0]
+    his = [i for i, r in enumerate(rows) if r and r[0] == "Address"]
+    hi = his[0]  # first kernel of the report (a report may hold several launches)
     hdr = rows[hi]
-    data = [r for r in rows[hi + 1:] if len(r) == len(hdr)]
+    end = his[1] if len(his) > 1 else len(rows)
+    data = [r for r in rows[hi + 1:end] if len(r) == len(hdr) and r[0] != "Address"]
     si = hdr.index("Warp Stall Sampling (All Samples)")
     ei = hdr.index("Instructions Executed")
     val = lambda r, i: float(r[i]) if r[i] not in ("", "-") else 0.0
