@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(smem_u32(&tempty[a]), EPI_WARPS);
     }
     mbar_init(smem_u32(efull), 1);
-    mbar_init(smem_u32(eempty), EPI_WARPS);
+    mbar_init(smem_u32(eempty), 1);  // the epilogue's storing thread, once per sample
     mbar_fence_init();
     if (do_mma) {
       tma_prefetch_desc(&tm_wh);
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tma_prefetch_desc(&tm_xh);
       tma_prefetch_desc(&tm_xl);
     }
-    if (load_eps) tma_prefetch_desc(&tm_eps);
+    if (load_eps || store_eps) tma_prefetch_desc(&tm_eps);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -224,11 +224,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       const float2 md = vi ? mdt[(long long)b * n + i] : make_float2(0.f, 0.f);
       const uint32_t erow = smem_u32(esm + cg * (ETILE / 4) + r * 128);
       if (load_eps) mbar_wait(smem_u32(efull), lb & 1);
+      else if (store_eps && lb > 0) mbar_wait(smem_u32(eempty), (lb - 1) & 1);  // tile reusable
       if (do_mma) {
         mbar_wait(smem_u32(&tfull[a]), (lb >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       }
-      float* grow = eps + ((long long)b * n_pad + i) * ke + c0;
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         float D[16];
@@ -247,14 +247,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           g[v4 * 4 + 1] = fmaf(md.x, e0.y, g[v4 * 4 + 1]);
           g[v4 * 4 + 2] = fmaf(md.x, e0.z, g[v4 * 4 + 2]);
           g[v4 * 4 + 3] = fmaf(md.x, e0.w, g[v4 * 4 + 3]);
-          if (store_eps && vi && c0 + v4 * 4 < ke) {
+          if (store_eps) {  // E_end in place over E0 (same swizzled chunk), TMA-stored below
             const int dv = (v4 - hf * 4) * 4;
             float4 en;
             en.x = fmaf(md.y, e0.x, D[dv + 0]);
             en.y = fmaf(md.y, e0.y, D[dv + 1]);
             en.z = fmaf(md.y, e0.z, D[dv + 2]);
             en.w = fmaf(md.y, e0.w, D[dv + 3]);
-            *reinterpret_cast<float4*>(grow + v4 * 4) = en;
+            sts_f4(erow + ((v4 ^ (r & 7)) << 4), en);
           }
         }
       }
@@ -263,8 +263,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         if (lane == 0) arrive(smem_u32(&tempty[a]));
       }
-      if (load_eps && lane == 0) arrive(smem_u32(eempty));
+      if (load_eps || store_eps) {
+        // the whole tile is read (and rewritten): one thread stores it with 4 TMA boxes
+        // and frees it once the bulk copies have read the shared memory
+        if (store_eps) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(EPI_WARPS * 32) : "memory");
+        if (warp == EPI0 && lane == 0) {
+          if (store_eps) {
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4)
+              tma_store_2d(&tm_eps, smem_u32(esm + q4 * (ETILE / 4)), j0 + 32 * q4,
+                           b * n_pad + i0);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+          arrive(smem_u32(eempty));
+        }
+      }
     }
+    if (store_eps && warp == EPI0 && lane == 0)
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // E_end written
     if (vi) {
       float* prow = partial + ((long long)blockIdx.z * n_pad + i) * kp + c0;
 #pragma unroll
@@ -363,7 +381,7 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
   SPB_CHECK_ARG(!do_mma || (ldw >= n && ldw % 8 == 0), "spb_alif_carry_chunk: bad ldw");
   SPB_CHECK_ARG(!(store_eps && !do_mma), "spb_alif_carry_chunk: storing eps needs the GEMM");
   CUtensorMap mwh{}, mwl{}, mxh{}, mxl{}, meps{};
-  if (load_eps &&
+  if ((load_eps || store_eps) &&
       !make_tmap_2d(&meps, eps, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ke, (uint64_t)B * n_pad,
                     (uint64_t)ke * 4, 32, carry::BM, CU_TENSOR_MAP_SWIZZLE_128B)) {
     set_error("spb_alif_carry_chunk: cuTensorMapEncodeTiled (eps) failed");
