@@ -300,14 +300,45 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 }  // namespace carry
 
+// 4 consecutive elements per thread (float4 partial loads, all S slices in flight before
+// the fixed-order fp64 sums), k_pad % 4 == 0.
 __global__ void reduce_partials_kernel(const float* __restrict__ partial, int S, int n, int n_pad,
                                        int k_pad, int accumulate, double* __restrict__ grad) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long idx = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
   if (idx >= (long long)n * k_pad) return;
   const long long stride = (long long)n_pad * k_pad;
-  double acc = 0.0;
-  for (int s = 0; s < S; ++s) acc += (double)partial[s * stride + idx];
-  grad[idx] = accumulate ? grad[idx] + acc : acc;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int s = 0;
+  for (; s + 4 <= S; s += 4) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = __ldcs(reinterpret_cast<const float4*>(partial + (s + u) * stride + idx));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a0 += (double)v[u].x;
+      a1 += (double)v[u].y;
+      a2 += (double)v[u].z;
+      a3 += (double)v[u].w;
+    }
+  }
+  for (; s < S; ++s) {
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(partial + s * stride + idx));
+    a0 += (double)v.x;
+    a1 += (double)v.y;
+    a2 += (double)v.z;
+    a3 += (double)v.w;
+  }
+  double2* g2 = reinterpret_cast<double2*>(grad + idx);
+  if (accumulate) {
+    const double2 o0 = g2[0], o1 = g2[1];
+    a0 = o0.x + a0;
+    a1 = o0.y + a1;
+    a2 = o1.x + a2;
+    a3 = o1.y + a3;
+  }
+  g2[0] = make_double2(a0, a1);
+  g2[1] = make_double2(a2, a3);
 }
 
 // CUDA-core GEMM on the same bf16 hi/lo operands as the tensor-core path:
@@ -416,10 +447,10 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
 
 int spb_reduce_partials(const float* partial, int splits, int n, int n_pad, int k_pad,
                         int accumulate, double* grad, cudaStream_t stream) {
-  SPB_CHECK_ARG(partial && grad && splits > 0 && n > 0 && n <= n_pad,
-                "spb_reduce_partials: bad args");
+  SPB_CHECK_ARG(partial && grad && splits > 0 && n > 0 && n <= n_pad && k_pad % 4 == 0,
+                "spb_reduce_partials: bad args (k_pad %% 4 == 0)");
   const long long total = (long long)n * k_pad;
-  reduce_partials_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(
+  reduce_partials_kernel<<<(unsigned)((total / 4 + 255) / 256), 256, 0, stream>>>(
       partial, splits, n, n_pad, k_pad, accumulate, grad);
   SPB_CHECK_LAUNCH("reduce_partials");
   return 0;

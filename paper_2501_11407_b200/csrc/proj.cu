@@ -470,6 +470,35 @@ __device__ __forceinline__ uint32_t expand4(uint32_t nib) {  // 4 bits -> 4 byte
   return (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
 }
 
+// Byte-count rows with k, the row stride and x 4-byte aligned (the common case): CTA per 4
+// rows, thread per 4 output bytes of each -- each warp moves 128 contiguous bytes in and
+// out per row (coalesced u32), the 4 rows' loads in flight together.
+__global__ void __launch_bounds__(256) pack_bytes4_kernel(const uint8_t* __restrict__ x,
+                                                          long long stride_b, int k, int len,
+                                                          int Tc, int Kpad, int B, int tmajor,
+                                                          uint8_t* __restrict__ xq) {
+  const int wpr = Kpad >> 2;  // output words per row
+  const int rows = B * Tc;
+  constexpr int R = 4;        // rows per CTA, their loads issued together
+  const int row0 = blockIdx.x * R;
+  for (int w = threadIdx.x; w < wpr; w += blockDim.x) {
+    uint32_t v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int row = row0 + q;
+      const int s = tmajor ? row / B : row % Tc;
+      const int b = tmajor ? row % B : row / Tc;
+      v[q] = (row < rows && s < len && 4 * w < k)
+                 ? __ldg(reinterpret_cast<const uint32_t*>(x + (long long)b * stride_b +
+                                                           (long long)s * k) + w)
+                 : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (row0 + q < rows) reinterpret_cast<uint32_t*>(xq + (long long)(row0 + q) * Kpad)[w] = v[q];
+  }
+}
+
 __global__ void pack_spikes_kernel(const uint8_t* __restrict__ x, long long stride_b, int k,
                                    int bits, int len, int Tc, int Kpad, int B, int tmajor,
                                    uint8_t* __restrict__ xq) {
@@ -526,6 +555,14 @@ int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits
   const long long rows = (long long)B * Tc;
   const long long want = (rows + 7) / 8;
   const int blocks = (int)(want < 148LL * 16 ? want : 148LL * 16);
+  if (!bits && (k & 3) == 0 && (stride_b & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0) {
+    const int b4 = (int)((rows + 3) / 4);
+    const int t4 = std::min(256, ((Kpad / 4 + 31) / 32) * 32);
+    proj::pack_bytes4_kernel<<<b4, t4, 0, stream>>>(x, stride_b, k, len, Tc, Kpad, B, time_major,
+                                                     xq);
+    SPB_CHECK_LAUNCH("pack_bytes4");
+    return 0;
+  }
   proj::pack_spikes_kernel<<<blocks, 256, 0, stream>>>(x, stride_b, k, bits, len, Tc, Kpad, B,
                                                         time_major, xq);
   SPB_CHECK_LAUNCH("pack_spikes");

@@ -159,8 +159,10 @@ int spb_readout_loss(const double* wout, const double* zsum, const long long* la
                 "spb_readout_loss: null pointer");
   SPB_CHECK_ARG(B > 0 && n > 0 && m > 0 && m <= 4096, "spb_readout_loss: bad sizes");
   const size_t smem = (size_t)(2 * m + 32) * sizeof(double);
-  readout_loss_kernel<<<B, 256, smem, stream>>>(wout, zsum, labels, n, m, s_out, loss, g, wsig,
-                                                correct);
+  // one warp per class (up to 32 warps): the class dot products run in one round
+  const int threads = 32 * (m < 8 ? 8 : (m > 32 ? 32 : m));
+  readout_loss_kernel<<<B, threads, smem, stream>>>(wout, zsum, labels, n, m, s_out, loss, g,
+                                                    wsig, correct);
   SPB_CHECK_LAUNCH("readout_loss");
   return 0;
 }
