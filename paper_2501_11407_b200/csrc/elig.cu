@@ -24,6 +24,8 @@
 // registers across samples.
 #include "tma.cuh"
 
+#include <cstdlib>
+
 namespace spb {
 namespace carry {
 
@@ -92,7 +94,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                       const __grid_constant__ CUtensorMap tm_eps,
                       const float2* __restrict__ mdt, float* __restrict__ eps,
                       float* __restrict__ partial, int B, int n, int n_pad, int ke, int kp, int KR,
-                      int b_per_split, int do_mma, int load_eps, int store_eps) {
+                      int b_per_split, int do_mma, int load_eps, int store_eps,
+                      int probe) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -154,6 +157,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(smem_u32(&empty[s]), ((it / STAGES) & 1) ^ 1);
           const uint32_t st = smem_u32(osm + s * STAGE);
           const uint32_t fb = smem_u32(&full[s]);
+          if (probe & 1) {  // profiling probe: no operand traffic
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
+            continue;
+          }
           mbar_expect_tx(fb, STAGE);
           const int kr = kbase + kb * BK;
           tma_load_2d(st, &tm_wh, fb, i0, kr);
@@ -193,7 +200,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t st = smem_u32(osm + s * STAGE);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
+          for (int kk = 0; kk < ((probe & 2) ? 0 : BK / 16); ++kk) {  // probe bit 1: no MMAs
             const uint32_t off = kk * 2048;  // 16 K rows of the MN-major tiles
             const uint64_t dwh = desc_mn_sw128(st + off, TILE / 2),
                            dwl = desc_mn_sw128(st + TILE + off, TILE / 2);
@@ -397,6 +404,12 @@ __global__ void __launch_bounds__(256) grad_gemm_simt_kernel(
 
 using namespace spb;
 
+// SPB_CARRY_PROBE (profiling only): bit 0 drops the operand loads, bit 1 the MMAs
+static int carry_probe() {
+  const char* e = getenv("SPB_CARRY_PROBE");
+  return e ? atoi(e) : 0;
+}
+
 extern "C" {
 
 int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh, const void* xl,
@@ -440,7 +453,7 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
   dim3 grid(kp / carry::BN, n_pad / carry::BM, splits);
   carry::alif_carry_kernel<<<grid, carry::THREADS, carry::SMEM, stream>>>(
       mwh, mwl, mxh, mxl, meps, reinterpret_cast<const float2*>(mdt), eps, partial, B, n, n_pad,
-      ke, kp, KR, bps, do_mma, load_eps, store_eps);
+      ke, kp, KR, bps, do_mma, load_eps, store_eps, carry_probe());
   SPB_CHECK_LAUNCH("alif_carry");
   return 0;
 }
