@@ -1,0 +1,58 @@
+"""bench.py keeps the driver's JSON-line contract: the reference arm here on the CPU, the
+B200 arm (short run) on the GPU."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(*args, timeout=600):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT,
+                         capture_output=True, text=True, timeout=timeout)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+             "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e"}
+
+
+def _check_common(d):
+    assert BASE_KEYS <= set(d), BASE_KEYS - set(d)
+    assert d["metric"].startswith("e-prop train samples")
+    assert d["unit"] == "samples*timesteps/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["scaling"] == "weak" and d["data"] == "synthetic"
+    assert {"workload", "seq_len", "n_hidden", "n_inputs", "n_classes"} <= set(d["config"])
+    e = d["e2e"]
+    assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(e)
+    assert e["unit"] == d["unit"] and e["value"] > 0
+
+
+def test_reference_arm_contract():
+    d = _run("--impl", "reference", "--config", "c2", "--steps", "1", "--warmup", "0")
+    _check_common(d)
+    assert d["impl"] == "reference"
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_contract():
+    d = _run("--config", "c2", "--steps", "4", "--warmup", "3", "--no-cpu")
+    _check_common(d)
+    assert "impl" not in d or d["impl"] != "reference"
+    assert d["n_gpus"] == 1 and d["steps"] == 4 and d["warmup"] == 3
+    assert d["gpu_launches"] > 0
+    r = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
+    assert r["bound"] in ("hbm", "tensor") and 0 < r["frac"] < 2
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    c = d["clocks"]
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c)
