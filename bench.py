@@ -474,9 +474,9 @@ def main():
                 ln, _, _ = meta                    # K1f: current in, C out (psi stays in L2)
                 byts += 8.0 * B * ln * n + 4.0 * n * B * KR
             elif name == "gemm":
-                ln = meta
-                flops += 6.0 * n * k * B * (ln + 1)                 # 3 bf16 MMAs per product
-                byts += 4.0 * (n + k) * B * KR
+                ln, raw = meta                   # raw spikes (exact bf16): 2 MMAs, no B-lo
+                flops += (4.0 if raw else 6.0) * n * k * B * (ln + 1)
+                byts += 4.0 * n * B * KR + (2.0 if raw else 4.0) * k * B * KR
             elif name == "carry":
                 ln, ld, stv = meta
                 byts += 4.0 * B * n * k * (int(ld) + int(stv)) + 8.0 * B * n
@@ -502,7 +502,7 @@ def main():
                  "fused_b": "fused_forward_kernel (K21 pass B: projection + dynamics, psi)",
                  "forward_a": "forward_chunk_kernel (K1 pass A)",
                  "forward_scan": "forward_scan_kernel (K1f: dynamics + readout + chunk scan)",
-                 "gemm": "grad_gemm_tc_kernel (K5, bf16x3 tcgen05)",
+                 "gemm": "grad_gemm_tc_kernel (K5, bf16 hi/lo tcgen05)",
                  "carry": "alif_carry_kernel (K6, tcgen05 + eps stream)"}
         if args.recurrent:
             names["forward_a"] = "forward_rec_kernel (K1rec pass A: recurrent spike gather)"

@@ -364,7 +364,8 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_scan_kernel(
   clp += L * ld2;
   const bool disc = (n & 31) == 0;  // whole 128-byte psi lines per warp
   const float* wrow = psis + (long long)b * (P.KR + 1) * n + wbase;
-  float lam = 0.f, an = 0.f, up = 0.f;
+  float lam = 0.f, an = 0.f, up = 0.f, ft = 0.f;
+  const float falpha = (float)P.alpha;
   constexpr int PF = 8;
   float q[PF];
 #pragma unroll
@@ -383,6 +384,8 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_scan_kernel(
       an = A0;
     }
     up = cu;
+    ft = fmaf(falpha, ft, c0);  // input filter folded into C (as pass 3)
+    c0 = ft;
     const float c1 = __shfl_down_sync(0xffffffffu, c0, 1);
     if (st_ok) {
       uint32_t h, l;
@@ -409,7 +412,11 @@ __global__ void __launch_bounds__(K1_THREADS, 6) forward_scan_kernel(
 constexpr int K1S_THREADS = 128;  // 4 warps = 256 consecutive neurons of one sample
 
 
-template <bool ALIF, bool CARRY>
+// FILT (pass 3, one fresh chunk, reset = 0): the presynaptic filter is folded into the
+// coefficients -- sum_rho C_rho xbar_{rho-1} = sum_rho Ct_rho x_{rho-1} (+ Ct_0 xbar_{-1}
+// = 0) with Ct_rho = C_rho + alpha Ct_{rho+1} -- so the gradient GEMM runs on the RAW
+// spikes, exact in bf16 (2 MMAs instead of 3, half the operand bytes, no filter kernel).
+template <bool ALIF, bool CARRY, bool FILT = false>
 __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
     FwdParams P, const float* __restrict__ wsig, const float* __restrict__ ctab,
     uint32_t* __restrict__ c_hi, uint32_t* __restrict__ c_lo, uint32_t* __restrict__ w_hi,
@@ -453,6 +460,8 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
   clp += L * ld2;
   if (CARRY) { whp += L * ld2; wlp += L * ld2; }
   float lam0 = 0.f, dcum0 = 1.f, an0 = 0.f, lam1 = 0.f, dcum1 = 1.f, an1 = 0.f;
+  float ft0 = 0.f, ft1 = 0.f;  // FILT: running Ct
+  const float falpha = (float)P.alpha;
   constexpr int PF = 8;  // psi rows in flight per thread (16 measured slower)
   float2 q[PF];
 #pragma unroll
@@ -480,6 +489,12 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
       dcum1 *= A1;
       an0 = A0;
       an1 = A1;
+    }
+    if (FILT) {
+      ft0 = fmaf(falpha, ft0, c0);
+      ft1 = fmaf(falpha, ft1, c1);
+      c0 = ft0;
+      c1 = ft1;
     }
     uint32_t h, l;
     split_bf16x2(c0, c1, h, l);
@@ -514,7 +529,9 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
 // ------------------------------------------------------------------------------------
 constexpr int SEG = 4;
 
-template <bool ALIF, bool CARRY>
+// FILT as in chunk_scan_kernel (LIF only here: Ct is linear in the segment entry, so a
+// first sweep gives each segment its local bottom value and alpha^rows).
+template <bool ALIF, bool CARRY, bool FILT = false>
 __global__ void __launch_bounds__(SEG * 32) chunk_scan_seg_kernel(
     FwdParams P, const float* __restrict__ wsig, const float* __restrict__ ctab,
     uint32_t* __restrict__ c_hi, uint32_t* __restrict__ c_lo, uint32_t* __restrict__ w_hi,
@@ -592,6 +609,40 @@ __global__ void __launch_bounds__(SEG * 32) chunk_scan_seg_kernel(
     sh_g[seg][lane] = make_float2(g0, g1);
     sh_d[seg][lane] = make_float2(d0, d1);
   }
+  static_assert(!(FILT && ALIF), "segmented FILT scan is LIF only");
+  const float falpha = (float)P.alpha;
+  float ft0 = 0.f, ft1 = 0.f;
+  if (FILT) {
+    if (lo <= hi) {  // sweep 1: this segment's Ct at row lo from a zero entry, alpha^rows
+      float f0 = 0.f, f1 = 0.f, ap = 1.f;
+      constexpr int PF1 = 8;
+      float2 pq[PF1];
+#pragma unroll
+      for (int u = 0; u < PF1; ++u) pq[u] = (hi - u >= lo) ? ldpsi(hi - u) : make_float2(0.f, 0.f);
+      for (int r = hi; r >= lo; --r) {
+        const float2 cur = pq[0];
+#pragma unroll
+        for (int u = 0; u < PF1 - 1; ++u) pq[u] = pq[u + 1];
+        pq[PF1 - 1] = (r - PF1 >= lo) ? ldpsi(r - PF1) : make_float2(0.f, 0.f);
+        const float c_prev = cs[r];
+        const float c0 = r >= 1 ? c_prev * ws0 * cur.x : 0.f;
+        const float c1 = r >= 1 ? c_prev * ws1 * cur.y : 0.f;
+        f0 = fmaf(falpha, f0, c0);
+        f1 = fmaf(falpha, f1, c1);
+        ap *= falpha;
+      }
+      sh_l[seg][lane] = make_float2(f0, f1);
+      sh_g[seg][lane] = make_float2(ap, ap);
+    }
+    __syncthreads();
+    for (int q = SEG - 1; q > seg; --q) {  // the segments above, top first
+      const int qlo = q * per, qhi = min(L, qlo + per - 1);
+      if (qlo > qhi) continue;
+      const float2 gl = sh_l[q][lane], gg = sh_g[q][lane];
+      ft0 = fmaf(gg.x, ft0, gl.x);
+      ft1 = fmaf(gg.y, ft1, gl.y);
+    }
+  }
   if (ALIF) {
     __syncthreads();
     // entry of this segment: the segments above, top first (fixed order)
@@ -638,6 +689,12 @@ __global__ void __launch_bounds__(SEG * 32) chunk_scan_seg_kernel(
       dcum1 *= A1;
       an0 = A0;
       an1 = A1;
+    }
+    if (FILT) {
+      ft0 = fmaf(falpha, ft0, c0);
+      ft1 = fmaf(falpha, ft1, c1);
+      c0 = ft0;
+      c1 = ft1;
     }
     if (live) {
       uint32_t h, l;
@@ -817,7 +874,7 @@ __global__ void __launch_bounds__(128) xbar_chunk_kernel(
   const uint8_t* xin = x + (long long)b * stride_b + j;
   const long long ld2 = kp >> 1;
   uint32_t* oh = xh + (long long)b * KR * ld2 + jp;
-  uint32_t* ol = xl + (long long)b * KR * ld2 + jp;
+  uint32_t* ol = xl != nullptr ? xl + (long long)b * KR * ld2 + jp : nullptr;
   for (int r8 = 0; r8 < KR; r8 += 8) {
     uint32_t x0[8], x1[8];
 #pragma unroll
@@ -843,7 +900,7 @@ __global__ void __launch_bounds__(128) xbar_chunk_kernel(
       uint32_t h, l;
       split_bf16x2(f0, f1, h, l);
       oh[(long long)rho * ld2] = h;
-      ol[(long long)rho * ld2] = l;
+      if (xl != nullptr) ol[(long long)rho * ld2] = l;
     }
   }
   if (v0) xbar_st[(long long)b * k + j] = xb0;
@@ -871,7 +928,7 @@ __global__ void __launch_bounds__(128) xbar_chunk4_kernel(
   const long long st4 = stride_t >> 2;
   const long long ld4 = kp >> 2;
   uint2* oh = xh + (long long)b * KR * ld4 + jq;
-  uint2* ol = xl + (long long)b * KR * ld4 + jq;
+  uint2* ol = xl != nullptr ? xl + (long long)b * KR * ld4 + jq : nullptr;
   const uint32_t keep = j + 4 <= k ? 0xffffffffu : (0xffffffffu >> (8 * (j + 4 - k)));
   for (int r8 = 0; r8 < KR; r8 += 8) {
     uint32_t xw[8];
@@ -899,7 +956,7 @@ __global__ void __launch_bounds__(128) xbar_chunk4_kernel(
       split_bf16x2(f[0], f[1], h.x, l.x);
       split_bf16x2(f[2], f[3], h.y, l.y);
       oh[(long long)rho * ld4] = h;
-      ol[(long long)rho * ld4] = l;
+      if (xl != nullptr) ol[(long long)rho * ld4] = l;
     }
   }
 #pragma unroll
@@ -984,7 +1041,7 @@ __global__ void __launch_bounds__(256) xbar_seg_kernel(
   // ---- sweep 2: the rows ----
   const long long ld4 = kp >> 2;
   uint2* oh = xh + ((long long)b * KR + lo) * ld4 + jq;
-  uint2* ol = xl + ((long long)b * KR + lo) * ld4 + jq;
+  uint2* ol = xl != nullptr ? xl + ((long long)b * KR + lo) * ld4 + jq : nullptr;
   for (int r8 = lo; r8 <= hi; r8 += 8) {
     uint32_t w8[8];
 #pragma unroll
@@ -1007,7 +1064,7 @@ __global__ void __launch_bounds__(256) xbar_seg_kernel(
       split_bf16x2(f[0], f[1], h.x, l.x);
       split_bf16x2(f[2], f[3], h.y, l.y);
       oh[(long long)(rho - lo) * ld4] = h;
-      ol[(long long)(rho - lo) * ld4] = l;
+      if (xl != nullptr) ol[(long long)(rho - lo) * ld4] = l;
     }
     // the carried state xbar_{t0+len-1} lives in row len: its segment stores it
     if (r8 <= len && len < r8 + 8) {
@@ -1037,8 +1094,13 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
                       const float* ctab, void* c_hi, void* c_lo, void* w_hi, void* w_lo,
                       void* wa_hi, void* wa_lo, int ldc, float* mdt, float* psi_scratch,
                       cudaStream_t stream) {
-  SPB_CHECK_ARG(pass >= 0 && pass <= 2,
-                "spb_forward_chunk: pass must be 0 (A), 1 (B) or 2 (B scan only)");
+  SPB_CHECK_ARG(pass >= 0 && pass <= 3,
+                "spb_forward_chunk: pass must be 0 (A), 1 (B), 2 (B scan only) or 3 (B scan "
+                "only, input filter folded into C)");
+  SPB_CHECK_ARG(pass != 3 || (!reset && t0 == 0 && w_hi == nullptr),
+                "spb_forward_chunk: pass 3 is for one fresh chunk with reset = 0, no carry");
+  const bool filt = pass == 3;
+  if (filt) pass = 2;
   SPB_CHECK_ARG(pass == 2 || (cur && u && a), "spb_forward_chunk: null pointer");
   SPB_CHECK_ARG(B > 0 && n > 0 && Tc > 0 && len >= 0 && len <= Tc && KR >= Tc + 1 && KR % 8 == 0,
                 "spb_forward_chunk: bad sizes B=%d n=%d Tc=%d KR=%d len=%d", B, n, Tc, KR, len);
@@ -1075,14 +1137,18 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
   } else if (pass >= 1) {
     dim3 sgrid(ceil_div(n, 2 * K1S_THREADS), B);
     const bool carry = alif && w_hi != nullptr;
-    auto kfn = alif ? (carry ? chunk_scan_kernel<true, true> : chunk_scan_kernel<true, false>)
-                    : chunk_scan_kernel<false, false>;
+    auto kfn = alif ? (carry ? chunk_scan_kernel<true, true>
+                             : (filt ? chunk_scan_kernel<true, false, true>
+                                     : chunk_scan_kernel<true, false>))
+                    : (filt ? chunk_scan_kernel<false, false, true>
+                            : chunk_scan_kernel<false, false>);
     // segments pay off where the one-sweep grid is small (C2: 0.058 -> 0.031 ms); for
     // ALIF they cost a second psi sweep, a loss once the grid fills the GPU (C3)
-    if (seg_scan() && (!alif || (long long)B * ceil_div(n, 2 * K1S_THREADS) < 2LL * 148)) {
+    if (seg_scan() && (!alif || (!filt && (long long)B * ceil_div(n, 2 * K1S_THREADS) < 2LL * 148))) {
       auto sfn = alif ? (carry ? chunk_scan_seg_kernel<true, true>
                                : chunk_scan_seg_kernel<true, false>)
-                      : chunk_scan_seg_kernel<false, false>;
+                      : (filt ? chunk_scan_seg_kernel<false, false, true>
+                              : chunk_scan_seg_kernel<false, false>);
       dim3 g2(ceil_div(n, 64), B);
       sfn<<<g2, SEG * 32, (len + 1) * sizeof(float), stream>>>(
           P, wsig, ctab, reinterpret_cast<uint32_t*>(c_hi), reinterpret_cast<uint32_t*>(c_lo),
@@ -1157,7 +1223,8 @@ int spb_xbar_chunk_seg(const uint8_t* x, long long stride_b, long long stride_t,
 static int xbar_launch(const uint8_t* x, long long stride_b, long long stride_t, int B, int k,
                        int kp, int KR, int len, int fresh, double alpha, double* xbar_state,
                        void* xh, void* xl, bool segmented, cudaStream_t stream) {
-  SPB_CHECK_ARG(x && xbar_state && xh && xl, "spb_xbar_chunk: null pointer");
+  // xl = NULL: only the hi part is written (alpha = 0 raw-spike operand: lo is 0)
+  SPB_CHECK_ARG(x && xbar_state && xh && (xl || alpha == 0.0), "spb_xbar_chunk: null pointer");
   SPB_CHECK_ARG(B > 0 && k > 0 && kp >= k && kp % 8 == 0 && KR > 0 && KR % 8 == 0 && len >= 0 &&
                     len < KR,
                 "spb_xbar_chunk: bad sizes");

@@ -28,6 +28,11 @@ constexpr int TILE_A = BM * BK * 2;  // bytes
 constexpr int TILE_B = BN * BK * 2;
 constexpr int STAGE_BYTES = 2 * TILE_A + 2 * TILE_B;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+// B exact in bf16 (BLO = false: raw spike operand, lo = 0): 2 MMAs per K step, no B-lo
+// stream, the freed shared memory buys 2 more stages
+constexpr int STAGES_NL = 6;
+constexpr int STAGE_BYTES_NL = 2 * TILE_A + TILE_B;
+constexpr int SMEM_BYTES_NL = STAGES_NL * STAGE_BYTES_NL + 1024 + 256;
 constexpr int THREADS = 192;
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart.
@@ -68,6 +73,7 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
                : "memory");
 }
 
+template <bool BLO>
 __global__ void __launch_bounds__(THREADS, 1)
     grad_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_ah,
                         const __grid_constant__ CUtensorMap tm_al,
@@ -75,14 +81,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const __grid_constant__ CUtensorMap tm_bl, int M, int N, int K,
                         int kb_per_split, float* __restrict__ partial, int ldp,
                         long long slice_stride) {
+  constexpr int NST = BLO ? STAGES : STAGES_NL;
+  constexpr int SB = BLO ? STAGE_BYTES : STAGE_BYTES_NL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* full = bars;                   // [STAGES]
-  uint64_t* empty = bars + STAGES;         // [STAGES]
-  uint64_t* tmem_full = bars + 2 * STAGES; // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * SB);
+  uint64_t* full = bars;                   // [NST]
+  uint64_t* empty = bars + NST;            // [NST]
+  uint64_t* tmem_full = bars + 2 * NST;    // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
@@ -91,7 +99,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int kb1 = min(nkb, kb0 + kb_per_split);
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
@@ -100,7 +108,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_ah)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_al)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_bh)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_bl)) : "memory");
+    if (BLO)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_bl)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -116,12 +125,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
+        const int s = it % NST;
+        const uint32_t ph = (it / NST) & 1;
         mbar_wait(smem_u32(&empty[s]), ph ^ 1);
-        const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t st = smem_u32(smem + s * SB);
         const uint32_t fb = smem_u32(&full[s]);
-        mbar_expect_tx(fb, STAGE_BYTES);
+        mbar_expect_tx(fb, SB);
         tma_load_2d(st, &tm_ah, fb, m0, kb * BK);
         tma_load_2d(st + TILE_A / 2, &tm_ah, fb, m0 + 64, kb * BK);
         tma_load_2d(st + TILE_A, &tm_al, fb, m0, kb * BK);
@@ -129,19 +138,20 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int h = 0; h < BN / 64; ++h) {
           tma_load_2d(st + 2 * TILE_A + h * (TILE_B / (BN / 64)), &tm_bh, fb, n0 + 64 * h, kb * BK);
-          tma_load_2d(st + 2 * TILE_A + TILE_B + h * (TILE_B / (BN / 64)), &tm_bl, fb, n0 + 64 * h,
-                      kb * BK);
+          if (BLO)
+            tma_load_2d(st + 2 * TILE_A + TILE_B + h * (TILE_B / (BN / 64)), &tm_bl, fb,
+                        n0 + 64 * h, kb * BK);
         }
       }
     }
   } else if (warp == 1) {
     {  // the whole warp runs the issue loop (converged); elect.sync picks the issuer
       for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
+        const int s = it % NST;
+        const uint32_t ph = (it / NST) & 1;
         mbar_wait(smem_u32(&full[s]), ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t st = smem_u32(smem + s * SB);
         const uint32_t sah = st, sal = st + TILE_A, sbh = st + 2 * TILE_A,
                        sbl = st + 2 * TILE_A + TILE_B;
 #pragma unroll
@@ -150,7 +160,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint64_t dah = umma_desc_mn_sw128(sah + offa), dal = umma_desc_mn_sw128(sal + offa);
           const uint64_t dbh = umma_desc_mn_sw128(sbh + offa), dbl = umma_desc_mn_sw128(sbl + offa);
           umma_bf16(tmem_base, dah, dbh, (kb > kb0 || kk > 0) ? 1u : 0u);
-          umma_bf16(tmem_base, dah, dbl, 1u);
+          if (BLO) umma_bf16(tmem_base, dah, dbl, 1u);
           umma_bf16(tmem_base, dal, dbh, 1u);
         }
         umma_commit(smem_u32(&empty[s]));
@@ -256,12 +266,14 @@ extern "C" {
 
 // Split-K tensor-core GEMM writing fp32 partial tiles:
 //   partial[z][i][j] = sum_{K in split z} (Ah+Al)[K][i] (Bh+Bl)[j][K]   (lo*lo dropped)
+// bl = NULL: B is exact in bf16 (raw spikes), Bl = 0 -- 2 MMAs per step instead of 3.
 // for i < M, j < ldp; every one of the `splits` slices is written (empty K ranges give 0).
 // Reduced in fixed order with spb_reduce_partials.
 int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* bh, const void* bl,
                            int ldb, int M, int N_rows, int K, int splits, float* partial, int ldp,
                            long long slice_stride, cudaStream_t stream) {
-  SPB_CHECK_ARG(ah && al && bh && bl && partial, "spb_grad_gemm_partials: null pointer");
+  SPB_CHECK_ARG(ah && al && bh && partial, "spb_grad_gemm_partials: null pointer");
+  const bool blo = bl != nullptr;  // bl = NULL: B is exact in bf16 (no lo part), 2 MMAs
   SPB_CHECK_ARG(M > 0 && N_rows > 0 && K > 0 && K % 8 == 0 && splits > 0 && ldp >= 1 &&
                     lda >= M && lda % 8 == 0 && ldb >= N_rows && ldb % 8 == 0,
                 "spb_grad_gemm_partials: bad sizes M=%d lda=%d N=%d K=%d", M, lda, N_rows, K);
@@ -270,17 +282,25 @@ int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* 
                 "spb_grad_gemm_partials: operands must be 16-byte aligned");
   CUtensorMap mah, mal, mbh, mbl;
   if (!tc::make_map_mn(&mah, ah, M, lda, K) || !tc::make_map_mn(&mal, al, M, lda, K) ||
-      !tc::make_map_mn(&mbh, bh, N_rows, ldb, K) || !tc::make_map_mn(&mbl, bl, N_rows, ldb, K)) {
+      !tc::make_map_mn(&mbh, bh, N_rows, ldb, K) ||
+      !tc::make_map_mn(&mbl, blo ? bl : bh, N_rows, ldb, K)) {
     set_error("spb_grad_gemm_partials: cuTensorMapEncodeTiled failed");
     return 3;
   }
   const int nkb = ceil_div(K, tc::BK);
   const int kbps = ceil_div(nkb, splits);
-  cudaFuncSetAttribute(tc::grad_gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       tc::SMEM_BYTES);
   dim3 grid(ceil_div(ldp, tc::BN), ceil_div(M, tc::BM), splits);
-  tc::grad_gemm_tc_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, stream>>>(
-      mah, mal, mbh, mbl, M, N_rows, K, kbps, partial, ldp, slice_stride);
+  if (blo) {
+    cudaFuncSetAttribute(tc::grad_gemm_tc_kernel<true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+    tc::grad_gemm_tc_kernel<true><<<grid, tc::THREADS, tc::SMEM_BYTES, stream>>>(
+        mah, mal, mbh, mbl, M, N_rows, K, kbps, partial, ldp, slice_stride);
+  } else {
+    cudaFuncSetAttribute(tc::grad_gemm_tc_kernel<false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES_NL);
+    tc::grad_gemm_tc_kernel<false><<<grid, tc::THREADS, tc::SMEM_BYTES_NL, stream>>>(
+        mah, mal, mbh, mbl, M, N_rows, K, kbps, partial, ldp, slice_stride);
+  }
   SPB_CHECK_LAUNCH("grad_gemm_tc");
   return 0;
 }

@@ -187,6 +187,8 @@ class EpropEngine:
         # the partial logits.  Opt-in (SPB_K1F=1 or engine.k1f = True): measured slower at C3
         # (0.41 vs 0.29 ms for K1 + K3 + K1s: the live psi of ~900 resident CTAs overflows L2)
         self.k1f = os.environ.get("SPB_K1F", "0") == "1" and m <= 64
+        # fold the input filter into the one-chunk coefficients (SPB_FILT=0: xbar operand)
+        self.filt = os.environ.get("SPB_FILT", "1") != "0"
         self.kf_sync = torch.zeros(1 + 2 * B, dtype=torch.int32, device=dev)
         self.kf_part = torch.empty(B * ((n + 127) // 128) * m, dtype=f64, device=dev)
         self.ldc = _round_up(n, 8)   # C/W are MN-major [K][ldc] (neurons contiguous)
@@ -378,8 +380,8 @@ class EpropEngine:
         nchunks = (T + Tc - 1) // Tc
         one = nchunks == 1
         # K1f: pass A + readout + scan of a one-chunk sequence in one kernel
-        kf = (one and self.k1f and not forward_only and not self.fused and not self.recurrent
-              and not self.reset and self.device.type == "cuda")
+        kf = (one and self.k1f and self.filt and not forward_only and not self.fused
+              and not self.recurrent and not self.reset and self.device.type == "cuda")
         strideb = T * kb
         self.launches = 0
         v = ctypes_void
@@ -390,6 +392,15 @@ class EpropEngine:
         # K5/K6 operand: the filtered input xbar (reset=False: G_u = 1 (x) xbar), or with
         # reset=True the raw input (G_u is carried per synapse; K4 with alpha = 0 = copy)
         x_alpha = 0.0 if self.reset else float(alpha)
+        # one fresh chunk, reset=False: the input filter is folded into the coefficients
+        # (scan pass 3), so K5 too runs on the raw spikes (forward.cu FILT).  Raw-spike
+        # operands are exact in bf16: no lo part (K4 writes hi only, K5 does 2 MMAs).
+        filt = (one and not self.reset and not self.recurrent and not forward_only
+                and self.filt)
+        if filt:
+            x_alpha = 0.0
+        raw_x = (filt or self.reset) and not self.recurrent
+        xl_ptr = None if raw_x else v(self.xl.data_ptr())
 
         def timed(name, meta, fn, *args):
             if timers is None:
@@ -462,7 +473,7 @@ class EpropEngine:
                 self.side.wait_event(self._ev["xbar"])
                 call("spb_xbar_chunk", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
                      ln, 1, x_alpha, v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()),
-                     v(self.xl.data_ptr()), sst)
+                     xl_ptr, sst)
                 self._ev["xbar"].record(self.side)
                 self.launches += 1
             if self.fused:
@@ -537,6 +548,8 @@ class EpropEngine:
                 self.launches += 2
             # one chunk (pass A parked psi) or K21 / K1rec (park psi themselves): scan only
             pid = 2 if (one or self.fused or self.recurrent) else 1
+            if filt:
+                pid = 3
             if not kf:
                 timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,
                       v(self.cur.data_ptr()) if self.cur is not None else None, B, n, Tc, KR,
@@ -548,7 +561,7 @@ class EpropEngine:
                       v(self.wa_hi.data_ptr()) if carry_out and self.ntr == 2 else None,
                       v(self.wa_lo.data_ptr()) if carry_out and self.ntr == 2 else None, self.ldc,
                       v(self.mdt.data_ptr()) if self.ntr else None, v(self.psi.data_ptr()), st)
-                self.launches += 1 if pid == 2 else 2
+                self.launches += 1 if pid >= 2 else 2
             if self.recurrent:
                 # x~ = [x_t, z_{t-1}] bytes, then the usual filter over kx columns
                 call("spb_pack_rec", v(self.xq.data_ptr()), xq_sb, xq_st,
@@ -564,10 +577,10 @@ class EpropEngine:
             else:
                 call("spb_xbar_chunk_seg", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
                      ln, int(c == 0 or self.reset), x_alpha, v(self.xbar_state.data_ptr()),
-                     v(self.xh.data_ptr()), v(self.xl.data_ptr()), st)
+                     v(self.xh.data_ptr()), xl_ptr, st)
                 self.launches += 1
-            timed("gemm", ln, "spb_grad_gemm_partials", v(self.c_hi.data_ptr()),
-                  v(self.c_lo.data_ptr()), self.ldc, v(self.xh.data_ptr()), v(self.xl.data_ptr()),
+            timed("gemm", (ln, raw_x), "spb_grad_gemm_partials", v(self.c_hi.data_ptr()),
+                  v(self.c_lo.data_ptr()), self.ldc, v(self.xh.data_ptr()), xl_ptr,
                   self.kp, n, self.kp, K, self.splits5, v(self.partial.data_ptr()), self.kp,
                   slice_stride, st)
             self.launches += 1

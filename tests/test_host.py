@@ -129,8 +129,13 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     assert names.count("spb_readout_loss") == 1
     # spb_forward_chunk pass B launches two kernels (dynamics + chunk scan)
     passb = sum(1 for c in rec.calls if c[0] == "spb_forward_chunk" and c[1][0] == 1)
-    if nch == 1:  # pass A parks psi, pass B runs the scan only
-        assert [c[1][0] for c in rec.calls if c[0] == "spb_forward_chunk"] == [0, 2]
+    if nch == 1:  # pass A parks psi, pass B runs the scan only, input filter folded in
+        assert [c[1][0] for c in rec.calls if c[0] == "spb_forward_chunk"] == [0, 3]
+        # the raw-spike operand: K4 with alpha = 0 writes hi only, K5 gets no B-lo
+        xb = [c[1] for c in rec.calls if c[0] in XB]
+        assert all(a[9] == 0.0 and a[12] is None for a in xb)
+        gm = [c[1] for c in rec.calls if c[0] == "spb_grad_gemm_partials"]
+        assert all(a[4] is None for a in gm)
     assert eng.launches == len(rec.calls) + passb
 
 
