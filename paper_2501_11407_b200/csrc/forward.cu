@@ -462,16 +462,23 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
   float lam0 = 0.f, dcum0 = 1.f, an0 = 0.f, lam1 = 0.f, dcum1 = 1.f, an1 = 0.f;
   float ft0 = 0.f, ft1 = 0.f;  // FILT: running Ct
   const float falpha = (float)P.alpha;
-  constexpr int PF = 8;  // psi rows in flight per thread (16 measured slower)
-  float2 q[PF];
+  // rows in blocks of 8: the next block's 8 psi loads are issued before this block is
+  // processed (8-16 rows in flight per thread, no register shifting)
+  float2 nxt[8];
 #pragma unroll
-  for (int u = 0; u < PF; ++u) q[u] = ldpsi(L - u);
+  for (int u = 0; u < 8; ++u) nxt[u] = ldpsi(L - u);
   float2 up = make_float2(0.f, 0.f);  // psi row r+1
-  for (int r = L; r >= 0; --r) {
-    const float2 cur = q[0];  // psi row r = psi_{r-1}
+  for (int r8 = L; r8 >= 0; r8 -= 8) {
+    float2 blk[8];
 #pragma unroll
-    for (int u = 0; u < PF - 1; ++u) q[u] = q[u + 1];
-    q[PF - 1] = ldpsi(r - PF);
+    for (int u = 0; u < 8; ++u) blk[u] = nxt[u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) nxt[u] = ldpsi(r8 - 8 - u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+    const int r = r8 - u;
+    if (r < 0) break;
+    const float2 cur = blk[u];  // psi row r = psi_{r-1}
     const float c_prev = cs[r], c_r = (r < L) ? cs[r + 1] : 0.f;
     // L_{r-1} psi_{r-1} (row r >= 1) [+ R_r = P_r Lambda_r, ALIF]; W_r = P_r D(L-1, r)
     float c0 = r >= 1 ? c_prev * ws0 * cur.x : 0.f;
@@ -510,6 +517,7 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
       wlp -= ld2;
     }
     up = cur;
+    }
   }
   if (ALIF && mdt != nullptr) {  // M also feeds the last chunk's inter-chunk term
     mdt[bi] = make_float2(an0 * lam0, dcum0);  // M = A_0 Lambda_0, Dt = prod A
