@@ -672,15 +672,21 @@ __global__ void __launch_bounds__(SEG * 32) chunk_scan_seg_kernel(
   uint32_t* wlp = CARRY ? w_lo + row0 + (long long)hi * ld2 : nullptr;
   float an0 = an0_in, an1 = an1_in;
   float2 up = up0;
-  constexpr int PF = 8;
-  float2 qv[PF];
+  float2 nxt[8];
 #pragma unroll
-  for (int u = 0; u < PF; ++u) qv[u] = (hi - u >= lo) ? ldpsi(hi - u) : make_float2(0.f, 0.f);
-  for (int r = hi; r >= lo; --r) {
-    const float2 cur = qv[0];
+  for (int u = 0; u < 8; ++u) nxt[u] = (hi - u >= lo) ? ldpsi(hi - u) : make_float2(0.f, 0.f);
+  for (int r8 = hi; r8 >= lo; r8 -= 8) {
+    float2 blk[8];
 #pragma unroll
-    for (int u = 0; u < PF - 1; ++u) qv[u] = qv[u + 1];
-    qv[PF - 1] = (r - PF >= lo) ? ldpsi(r - PF) : make_float2(0.f, 0.f);
+    for (int u = 0; u < 8; ++u) blk[u] = nxt[u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      nxt[u] = (r8 - 8 - u >= lo) ? ldpsi(r8 - 8 - u) : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+    const int r = r8 - u;
+    if (r < lo) break;
+    const float2 cur = blk[u];
     const float c_prev = cs[r], c_r = (r < L) ? cs[r + 1] : 0.f;
     float c0 = r >= 1 ? c_prev * ws0 * cur.x : 0.f;
     float c1 = r >= 1 ? c_prev * ws1 * cur.y : 0.f;
@@ -719,6 +725,7 @@ __global__ void __launch_bounds__(SEG * 32) chunk_scan_seg_kernel(
     clp -= ld2;
     if (CARRY) { whp -= ld2; wlp -= ld2; }
     up = cur;
+    }
   }
   if (ALIF && mdt != nullptr && seg == 0 && live) {  // M = A_0 Lambda_0, Dt = prod A
     mdt[bi] = make_float2(an0 * lam0, dcum0);
@@ -816,13 +823,21 @@ __global__ void __launch_bounds__(K1S_THREADS) reset_scan_kernel(
   ResetLane s0, s1;
   // step r uses P_r = psi row r and Lpsi_r = c_r w_sig psi row r+1
   float2 up = ldpsi(L);
-  float2 q0 = ldpsi(L - 1), q1 = ldpsi(L - 2), q2 = ldpsi(L - 3), q3 = ldpsi(L - 4);
-  for (int r = L - 1; r >= 0; --r) {
-    const float2 cur = q0;
-    q0 = q1;
-    q1 = q2;
-    q2 = q3;
-    q3 = ldpsi(r - 4);
+  // rows in blocks of 8, the next block's loads in flight (as chunk_scan_kernel)
+  float2 nxt[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) nxt[u] = ldpsi(L - 1 - u);
+  for (int r8 = L - 1; r8 >= 0; r8 -= 8) {
+    float2 blk[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) blk[u] = nxt[u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) nxt[u] = ldpsi(r8 - 8 - u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+    const int r = r8 - u;
+    if (r < 0) break;
+    const float2 cur = blk[u];
     const float cr = cs[r];
     float c0, u0, a0, c1, u1, a1;
     s0.step(cur.x, cr * ws0 * up.x, alpha, theta, beta, rho, alif, c0, u0, a0);
@@ -843,6 +858,7 @@ __global__ void __launch_bounds__(K1S_THREADS) reset_scan_kernel(
       }
     }
     up = cur;
+    }
   }
   if (coef != nullptr) {
     const ResetLane* sl[2] = {&s0, &s1};
