@@ -590,15 +590,21 @@ __global__ void __launch_bounds__(SEG * 32) chunk_scan_seg_kernel(
     float l0 = 0.f, l1 = 0.f, g0 = 1.f, g1 = 1.f, d0 = 1.f, d1 = 1.f;
     float an0 = an0_in, an1 = an1_in;
     float2 up = up0;
-    constexpr int PF1 = 8;
-    float2 pq[PF1];
+    float2 nx1[8];
 #pragma unroll
-    for (int u = 0; u < PF1; ++u) pq[u] = (hi - u >= lo) ? ldpsi(hi - u) : make_float2(0.f, 0.f);
-    for (int r = hi; r >= lo; --r) {
-      const float2 cur = pq[0];
+    for (int u = 0; u < 8; ++u) nx1[u] = (hi - u >= lo) ? ldpsi(hi - u) : make_float2(0.f, 0.f);
+    for (int r8 = hi; r8 >= lo; r8 -= 8) {
+      float2 bk1[8];
 #pragma unroll
-      for (int u = 0; u < PF1 - 1; ++u) pq[u] = pq[u + 1];
-      pq[PF1 - 1] = (r - PF1 >= lo) ? ldpsi(r - PF1) : make_float2(0.f, 0.f);
+      for (int u = 0; u < 8; ++u) bk1[u] = nx1[u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        nx1[u] = (r8 - 8 - u >= lo) ? ldpsi(r8 - 8 - u) : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+      const int r = r8 - u;
+      if (r < lo) break;
+      const float2 cur = bk1[u];
       if (r < L) {
         const float c_r = cs[r + 1];
         const float A0 = fmaf(-beta, cur.x, rho), A1 = fmaf(-beta, cur.y, rho);
@@ -612,6 +618,7 @@ __global__ void __launch_bounds__(SEG * 32) chunk_scan_seg_kernel(
         an1 = A1;
       }
       up = cur;
+      }
     }
     sh_l[seg][lane] = make_float2(l0, l1);
     sh_g[seg][lane] = make_float2(g0, g1);
@@ -623,21 +630,28 @@ __global__ void __launch_bounds__(SEG * 32) chunk_scan_seg_kernel(
   if (FILT) {
     if (lo <= hi) {  // sweep 1: this segment's Ct at row lo from a zero entry, alpha^rows
       float f0 = 0.f, f1 = 0.f, ap = 1.f;
-      constexpr int PF1 = 8;
-      float2 pq[PF1];
+      float2 nx1[8];
 #pragma unroll
-      for (int u = 0; u < PF1; ++u) pq[u] = (hi - u >= lo) ? ldpsi(hi - u) : make_float2(0.f, 0.f);
-      for (int r = hi; r >= lo; --r) {
-        const float2 cur = pq[0];
+      for (int u = 0; u < 8; ++u) nx1[u] = (hi - u >= lo) ? ldpsi(hi - u) : make_float2(0.f, 0.f);
+      for (int r8 = hi; r8 >= lo; r8 -= 8) {
+        float2 bk1[8];
 #pragma unroll
-        for (int u = 0; u < PF1 - 1; ++u) pq[u] = pq[u + 1];
-        pq[PF1 - 1] = (r - PF1 >= lo) ? ldpsi(r - PF1) : make_float2(0.f, 0.f);
+        for (int u = 0; u < 8; ++u) bk1[u] = nx1[u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          nx1[u] = (r8 - 8 - u >= lo) ? ldpsi(r8 - 8 - u) : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+        const int r = r8 - u;
+        if (r < lo) break;
+        const float2 cur = bk1[u];
         const float c_prev = cs[r];
         const float c0 = r >= 1 ? c_prev * ws0 * cur.x : 0.f;
         const float c1 = r >= 1 ? c_prev * ws1 * cur.y : 0.f;
         f0 = fmaf(falpha, f0, c0);
         f1 = fmaf(falpha, f1, c1);
         ap *= falpha;
+        }
       }
       sh_l[seg][lane] = make_float2(f0, f1);
       sh_g[seg][lane] = make_float2(ap, ap);
