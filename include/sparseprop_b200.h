@@ -179,6 +179,13 @@ int spb_xbar_chunk(const uint8_t* x, long long stride_b, long long stride_t, int
 int spb_xbar_chunk_seg(const uint8_t* x, long long stride_b, long long stride_t, int B, int k, int kp,
                        int KR, int len, int fresh, double alpha, double* xbar_state, void* xh,
                        void* xl, cudaStream_t stream);
+/* Multi-chunk raw-spike operand: xh rows rho >= 1 = the raw spikes of the chunk (exact in
+ * bf16, no lo part), row 0 = 0; the fp64 filter state xbar_state is advanced with alpha
+ * (as spb_xbar_chunk) and the entry state xbar_{t0-1} is written to xs_hi/xs_lo [B][kp]
+ * (bf16 hi/lo) for the row-0 terms of K5 (a K = B GEMM) and K6 (epilogue). */
+int spb_xbar_chunk_raw(const uint8_t* x, long long stride_b, long long stride_t, int B, int k,
+                       int kp, int KR, int len, int fresh, double alpha, double* xbar_state,
+                       void* xh, void* xs_hi, void* xs_lo, cudaStream_t stream);
 
 /* K3  Readout + loss: s_b = W_out zsum_b, loss_b = CE(s_b, y_b), g_b = softmax - onehot,
  *     wsig_b = W_out^T g_b.  Replaces gradients.py:163-164,177-178 and
@@ -216,11 +223,16 @@ int spb_grad_gemm_simt(const void* ah, const void* al, int lda, const void* bh, 
  *     operand [B*KR][ldw] and x* the K4 operand [B*KR][kp] (both MN-major), mdt from K1s;
  *     partial [splits][n_pad][kp].
  *     n_pad % 128 == 0, kp % 128 == 0, ke % 4 == 0, KR % 64 == 0.  Replaces the ALIF G_a
- *     block of eprop_trace_update (gradients.py:89-94) and x_step (gradients.py:165-167). */
+ *     block of eprop_trace_update (gradients.py:89-94) and x_step (gradients.py:165-167).
+ *     xl = NULL: the raw-spike operand (rows rho >= 1 raw spikes, row 0 zero; W from scan
+ *     pass 3/4 with the input filter folded in), 2 MMAs per step; then xs_hi/xs_lo [B][kp]
+ *     (spb_xbar_chunk_raw's entry state, NULL for a fresh state) add the row-0 term
+ *     W_0[b,i] xbar_{t0-1}[b,j] to E_end in the epilogue. */
 int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh, const void* xl,
                          const float* mdt, float* eps, float* partial, int B, int n, int n_pad,
                          int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
-                         int store_eps, cudaStream_t stream);
+                         int store_eps, const void* xs_hi, const void* xs_lo,
+                         cudaStream_t stream);
 
 /* K6r The ALIF trace PAIR (G_u, G_a) of reset=True carried across chunks on tcgen05
  *     (elig_reset.cu): with (W_u, W_a), M, Dt from K1r and the raw input x (K4, alpha=0)

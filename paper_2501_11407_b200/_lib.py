@@ -36,11 +36,13 @@ SIGNATURES = {
                                P, P, I, P, P, P, P, P, P, P, P, I, P, P, P],
     "spb_xbar_chunk": [P, LL, LL, I, I, I, I, I, I, D, P, P, P, P],
     "spb_xbar_chunk_seg": [P, LL, LL, I, I, I, I, I, I, D, P, P, P, P],
+    "spb_xbar_chunk_raw": [P, LL, LL, I, I, I, I, I, I, D, P, P, P, P, P],
     "spb_readout_loss": [P, P, P, I, I, I, P, P, P, P, P, P],
     "spb_readout_grad": [P, P, I, I, I, P, P],
     "spb_grad_gemm_partials": [P, P, I, P, P, I, I, I, I, I, P, I, LL, P],
     "spb_grad_gemm_simt": [P, P, I, P, P, I, I, I, I, P, I, P],
-    "spb_alif_carry_chunk": [P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I, I, P],
+    "spb_alif_carry_chunk": [P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I, I, P, P,
+                             P],
     "spb_reset_carry_chunk": [P, P, P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I,
                               I, P],
     "spb_reduce_partials": [P, I, I, I, I, I, P, P],

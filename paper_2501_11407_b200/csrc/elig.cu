@@ -40,6 +40,10 @@ constexpr int THREADS = EPI0 * 32 + EPI_WARPS * 32;
 // one eps tile (single-buffered: its own producer warp refills it while the next sample's
 // MMAs run) leaves room for 5 operand stages -- the L2 operand stream is latency-bound
 constexpr int SMEM = ETILE + STAGES * STAGE + 1024 + 256;
+// raw-spike operand (RAW): no xbar-lo tiles, 2 MMAs per K step, 6 stages of 3 tiles
+constexpr int STAGES_R = 6;
+constexpr int STAGE_R = 3 * TILE;
+constexpr int SMEM_R = ETILE + STAGES_R * STAGE_R + 1024 + 256;
 // A = W, B = xbar, both MN-major (neurons / channels contiguous, written by K1s / K4)
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -88,6 +92,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&r)[16]) {
 // read it, while the next sample's MMAs run); warp 1 issues the tcgen05 MMAs into one of
 // two TMEM buffers; 16 epilogue warps combine E_end = Dt E0 + D (written back with plain
 // stores) and grad += M E0 (registers across samples).
+// RAW: the per-sample GEMM runs on the raw spikes (rows rho >= 1; row 0 zero) with the
+// input filter folded into W (forward.cu pass 3/4), and the entry-state term
+// Wt_0[b,i] xbar_{t0-1}[b,j] (xs = bf16 hi/lo [B][kp], Wt_0 = row 0 of W) is added in the
+// epilogue in fp32.
+template <bool RAW>
 __global__ void __launch_bounds__(THREADS, 1)
     alif_carry_kernel(const __grid_constant__ CUtensorMap tm_wh, const __grid_constant__ CUtensorMap tm_wl,
                       const __grid_constant__ CUtensorMap tm_xh, const __grid_constant__ CUtensorMap tm_xl,
@@ -95,20 +104,25 @@ __global__ void __launch_bounds__(THREADS, 1)
                       const float2* __restrict__ mdt, float* __restrict__ eps,
                       float* __restrict__ partial, int B, int n, int n_pad, int ke, int kp, int KR,
                       int b_per_split, int do_mma, int load_eps, int store_eps,
-                      int probe) {
+                      int probe, const __nv_bfloat16* __restrict__ wh_g,
+                      const __nv_bfloat16* __restrict__ wl_g, int ldw,
+                      const __nv_bfloat16* __restrict__ xs_hi,
+                      const __nv_bfloat16* __restrict__ xs_lo) {
+  constexpr int NST = RAW ? STAGES_R : STAGES;
+  constexpr int SB = RAW ? STAGE_R : STAGE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* esm = smem;                             // [4 boxes][128 rows][128 B]
-  uint8_t* osm = smem + ETILE;                     // [STAGES][4][TILE]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(osm + STAGES * STAGE);
+  uint8_t* osm = smem + ETILE;                     // [NST][4 or 3][TILE]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(osm + NST * SB);
   uint64_t* full = bars;
-  uint64_t* empty = bars + STAGES;
-  uint64_t* tfull = bars + 2 * STAGES;
-  uint64_t* tempty = bars + 2 * STAGES + 2;
-  uint64_t* efull = bars + 2 * STAGES + 4;
-  uint64_t* eempty = bars + 2 * STAGES + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 6);
+  uint64_t* empty = bars + NST;
+  uint64_t* tfull = bars + 2 * NST;
+  uint64_t* tempty = bars + 2 * NST + 2;
+  uint64_t* efull = bars + 2 * NST + 4;
+  uint64_t* eempty = bars + 2 * NST + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 6);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
@@ -117,7 +131,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int nkb = KR / BK;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
@@ -132,7 +146,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tma_prefetch_desc(&tm_wh);
       tma_prefetch_desc(&tm_wl);
       tma_prefetch_desc(&tm_xh);
-      tma_prefetch_desc(&tm_xl);
+      if (!RAW) tma_prefetch_desc(&tm_xl);
     }
     if (load_eps || store_eps) tma_prefetch_desc(&tm_eps);
   }
@@ -153,15 +167,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int lb = 0; lb < nb; ++lb) {
         const int kbase = (b0 + lb) * KR;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(smem_u32(&empty[s]), ((it / STAGES) & 1) ^ 1);
-          const uint32_t st = smem_u32(osm + s * STAGE);
+          const int s = it % NST;
+          mbar_wait(smem_u32(&empty[s]), ((it / NST) & 1) ^ 1);
+          const uint32_t st = smem_u32(osm + s * SB);
           const uint32_t fb = smem_u32(&full[s]);
           if (probe & 1) {  // profiling probe: no operand traffic
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
             continue;
           }
-          mbar_expect_tx(fb, STAGE);
+          mbar_expect_tx(fb, SB);
           const int kr = kbase + kb * BK;
           tma_load_2d(st, &tm_wh, fb, i0, kr);
           tma_load_2d(st + TILE / 2, &tm_wh, fb, i0 + 64, kr);
@@ -169,8 +183,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           tma_load_2d(st + TILE + TILE / 2, &tm_wl, fb, i0 + 64, kr);
           tma_load_2d(st + 2 * TILE, &tm_xh, fb, j0, kr);
           tma_load_2d(st + 2 * TILE + TILE / 2, &tm_xh, fb, j0 + 64, kr);
-          tma_load_2d(st + 3 * TILE, &tm_xl, fb, j0, kr);
-          tma_load_2d(st + 3 * TILE + TILE / 2, &tm_xl, fb, j0 + 64, kr);
+          if (!RAW) {
+            tma_load_2d(st + 3 * TILE, &tm_xl, fb, j0, kr);
+            tma_load_2d(st + 3 * TILE + TILE / 2, &tm_xl, fb, j0 + 64, kr);
+          }
         }
       }
     }
@@ -195,10 +211,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem_base + (uint32_t)(a * BN);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(smem_u32(&full[s]), (it / STAGES) & 1);
+          const int s = it % NST;
+          mbar_wait(smem_u32(&full[s]), (it / NST) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t st = smem_u32(osm + s * STAGE);
+          const uint32_t st = smem_u32(osm + s * SB);
 #pragma unroll
           for (int kk = 0; kk < ((probe & 2) ? 0 : BK / 16); ++kk) {  // probe bit 1: no MMAs
             const uint32_t off = kk * 2048;  // 16 K rows of the MN-major tiles
@@ -207,7 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint64_t dxh = desc_mn_sw128(st + 2 * TILE + off, TILE / 2),
                            dxl = desc_mn_sw128(st + 3 * TILE + off, TILE / 2);
             mma_bf16(d, dwh, dxh, (kb | kk) ? 1u : 0u);
-            mma_bf16(d, dwh, dxl, 1u);
+            if (!RAW) mma_bf16(d, dwh, dxl, 1u);
             mma_bf16(d, dwl, dxh, 1u);
           }
           commit(smem_u32(&empty[s]));
@@ -229,6 +245,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int b = b0 + lb;
       const int a = lb & 1;
       const float2 md = vi ? mdt[(long long)b * n + i] : make_float2(0.f, 0.f);
+      // RAW: entry-state term Wt_0[b,i] * xbar_{t0-1}[b, c0 + c] (xs may be absent: fresh)
+      float w0e = 0.f;
+      if (RAW && xs_hi != nullptr && vi) {
+        const long long o = (long long)b * KR * ldw + i;
+        w0e = __bfloat162float(wh_g[o]) + __bfloat162float(wl_g[o]);
+      }
       const uint32_t erow = smem_u32(esm + cg * (ETILE / 4) + r * 128);
       if (load_eps) mbar_wait(smem_u32(efull), lb & 1);
       else if (store_eps && lb > 0) mbar_wait(smem_u32(eempty), (lb - 1) & 1);  // tile reusable
@@ -261,6 +283,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             en.y = fmaf(md.y, e0.y, D[dv + 1]);
             en.z = fmaf(md.y, e0.z, D[dv + 2]);
             en.w = fmaf(md.y, e0.w, D[dv + 3]);
+            if (RAW && xs_hi != nullptr) {
+              const int cc = c0 + v4 * 4;
+              float xsv[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                xsv[e] = cc + e < kp ? __bfloat162float(xs_hi[(long long)b * kp + cc + e]) +
+                                           __bfloat162float(xs_lo[(long long)b * kp + cc + e])
+                                     : 0.f;
+              en.x = fmaf(w0e, xsv[0], en.x);
+              en.y = fmaf(w0e, xsv[1], en.y);
+              en.z = fmaf(w0e, xsv[2], en.z);
+              en.w = fmaf(w0e, xsv[3], en.w);
+            }
             sts_f4(erow + ((v4 ^ (r & 7)) << 4), en);
           }
         }
@@ -415,9 +450,14 @@ extern "C" {
 int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh, const void* xl,
                          const float* mdt, float* eps, float* partial, int B, int n, int n_pad,
                          int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
-                         int store_eps, cudaStream_t stream) {
+                         int store_eps, const void* xs_hi, const void* xs_lo,
+                         cudaStream_t stream) {
   SPB_CHECK_ARG(mdt && eps && partial, "spb_alif_carry_chunk: null pointer");
-  SPB_CHECK_ARG(!do_mma || (wh && wl && xh && xl), "spb_alif_carry_chunk: missing GEMM operands");
+  // xl = NULL: raw-spike operand (2 MMAs); xs = the entry-state term (NULL: fresh state)
+  const bool raw = xl == nullptr;
+  SPB_CHECK_ARG(!(xs_hi && !raw) && !(xs_hi && !xs_lo),
+                "spb_alif_carry_chunk: the entry-state term needs the raw operand (xl = NULL)");
+  SPB_CHECK_ARG(!do_mma || (wh && wl && xh), "spb_alif_carry_chunk: missing GEMM operands");
   SPB_CHECK_ARG(n_pad % carry::BM == 0 && n <= n_pad && kp % carry::BN == 0 && kp >= k &&
                     ke >= k && ke % 4 == 0 && KR % carry::BK == 0 && (kp / carry::BN) * carry::BN == kp,
                 "spb_alif_carry_chunk: bad padding (n_pad %% 128, kp %% 128, ke %% 4, KR %% 64)");
@@ -440,20 +480,34 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
                      carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
         make_tmap_2d(&mxh, xh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kp, K, (uint64_t)kp * 2, 64,
                      carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
-        make_tmap_2d(&mxl, xl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kp, K, (uint64_t)kp * 2, 64,
-                     carry::BK, CU_TENSOR_MAP_SWIZZLE_128B);
+        make_tmap_2d(&mxl, raw ? xh : xl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kp, K,
+                     (uint64_t)kp * 2, 64, carry::BK, CU_TENSOR_MAP_SWIZZLE_128B);
     if (!ok) {
       set_error("spb_alif_carry_chunk: cuTensorMapEncodeTiled failed");
       return 3;
     }
   }
   const int bps = ceil_div(B, splits);
-  cudaFuncSetAttribute(carry::alif_carry_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       carry::SMEM);
   dim3 grid(kp / carry::BN, n_pad / carry::BM, splits);
-  carry::alif_carry_kernel<<<grid, carry::THREADS, carry::SMEM, stream>>>(
-      mwh, mwl, mxh, mxl, meps, reinterpret_cast<const float2*>(mdt), eps, partial, B, n, n_pad,
-      ke, kp, KR, bps, do_mma, load_eps, store_eps, carry_probe());
+  const auto* whb = static_cast<const __nv_bfloat16*>(wh);
+  const auto* wlb = static_cast<const __nv_bfloat16*>(wl);
+  const auto* xsh = static_cast<const __nv_bfloat16*>(xs_hi);
+  const auto* xsl = static_cast<const __nv_bfloat16*>(xs_lo);
+  if (raw) {
+    cudaFuncSetAttribute(carry::alif_carry_kernel<true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, carry::SMEM_R);
+    carry::alif_carry_kernel<true><<<grid, carry::THREADS, carry::SMEM_R, stream>>>(
+        mwh, mwl, mxh, mxl, meps, reinterpret_cast<const float2*>(mdt), eps, partial, B, n,
+        n_pad, ke, kp, KR, bps, do_mma, load_eps, store_eps, carry_probe(), whb, wlb, ldw, xsh,
+        xsl);
+  } else {
+    cudaFuncSetAttribute(carry::alif_carry_kernel<false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, carry::SMEM);
+    carry::alif_carry_kernel<false><<<grid, carry::THREADS, carry::SMEM, stream>>>(
+        mwh, mwl, mxh, mxl, meps, reinterpret_cast<const float2*>(mdt), eps, partial, B, n,
+        n_pad, ke, kp, KR, bps, do_mma, load_eps, store_eps, carry_probe(), whb, wlb, ldw,
+        nullptr, nullptr);
+  }
   SPB_CHECK_LAUNCH("alif_carry");
   return 0;
 }

@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
   clp += L * ld2;
   if (CARRY) { whp += L * ld2; wlp += L * ld2; }
   float lam0 = 0.f, dcum0 = 1.f, an0 = 0.f, lam1 = 0.f, dcum1 = 1.f, an1 = 0.f;
-  float ft0 = 0.f, ft1 = 0.f;  // FILT: running Ct
+  float ft0 = 0.f, ft1 = 0.f, fw0 = 0.f, fw1 = 0.f;  // FILT: running Ct, Wt
   const float falpha = (float)P.alpha;
   // rows in blocks of 8: the next block's 8 psi loads are issued before this block is
   // processed (8-16 rows in flight per thread, no register shifting)
@@ -502,6 +502,12 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
       ft1 = fmaf(falpha, ft1, c1);
       c0 = ft0;
       c1 = ft1;
+      if (CARRY) {  // the carry GEMM runs on the raw spikes too
+        fw0 = fmaf(falpha, fw0, w0);
+        fw1 = fmaf(falpha, fw1, w1);
+        w0 = fw0;
+        w1 = fw1;
+      }
     }
     uint32_t h, l;
     split_bf16x2(c0, c1, h, l);
@@ -948,10 +954,14 @@ __global__ void __launch_bounds__(128) xbar_chunk_kernel(
 // K4 on 4 neighbouring channels per thread (row strides and x 4-byte aligned): one 32-bit
 // spike load and two 8-byte bf16x4 stores per step -- half the instructions per byte of
 // the 2-channel kernel above, same values.
+// raw != 0 (multi-chunk raw-spike operand): rows rho >= 1 hold the raw spikes, row 0 is
+// zero and the entry state xbar_{t0-1} goes to xs_hi/xs_lo [B][kp] instead (the GEMMs
+// add its term separately); the fp64 filter state is still advanced with alpha.
 __global__ void __launch_bounds__(128) xbar_chunk4_kernel(
     const uint8_t* __restrict__ x, long long stride_b, long long stride_t, int B, int k, int kp,
     int KR, int len, int fresh, double alpha, double* __restrict__ xbar_st,
-    uint2* __restrict__ xh, uint2* __restrict__ xl) {
+    uint2* __restrict__ xh, uint2* __restrict__ xl, int raw = 0,
+    uint2* __restrict__ xs_hi = nullptr, uint2* __restrict__ xs_lo = nullptr) {
   const int jq = blockIdx.x * blockDim.x + threadIdx.x;  // channel quad
   const int j = 4 * jq;
   const int b = blockIdx.y;
@@ -983,11 +993,21 @@ __global__ void __launch_bounds__(128) xbar_chunk4_kernel(
       if (rho == 0) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) f[c] = (float)xb[c];
+        if (raw) {  // entry state to xs, zero row
+          uint2 h, l;
+          split_bf16x2(f[0], f[1], h.x, l.x);
+          split_bf16x2(f[2], f[3], h.y, l.y);
+          xs_hi[(long long)b * ld4 + jq] = h;
+          xs_lo[(long long)b * ld4 + jq] = l;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) f[c] = 0.f;
+        }
       } else if (rho <= len) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          xb[c] = __dadd_rn(__dmul_rn(alpha, xb[c]), (double)((xw[u8] >> (8 * c)) & 0xffu));
-          f[c] = (float)xb[c];
+          const uint32_t xv = (xw[u8] >> (8 * c)) & 0xffu;
+          xb[c] = __dadd_rn(__dmul_rn(alpha, xb[c]), (double)xv);
+          f[c] = raw ? (float)xv : (float)xb[c];
         }
       }
       uint2 h, l;
@@ -1014,7 +1034,8 @@ constexpr int XSEG_ROWS = 64;
 __global__ void __launch_bounds__(256) xbar_seg_kernel(
     const uint8_t* __restrict__ x, long long stride_b, long long stride_t, int B, int k, int kp,
     int KR, int len, int fresh, double alpha, double* __restrict__ xbar_st,
-    uint2* __restrict__ xh, uint2* __restrict__ xl) {
+    uint2* __restrict__ xh, uint2* __restrict__ xl, int raw = 0,
+    uint2* __restrict__ xs_hi = nullptr, uint2* __restrict__ xs_lo = nullptr) {
   __shared__ double sh_end[8][32][4];
   __shared__ double sh_pow[8];
   const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
@@ -1091,11 +1112,21 @@ __global__ void __launch_bounds__(256) xbar_seg_kernel(
       if (rho == 0) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) f[c] = (float)xv[c];
+        if (raw) {  // entry state to xs, zero row (see xbar_chunk4_kernel)
+          uint2 h, l;
+          split_bf16x2(f[0], f[1], h.x, l.x);
+          split_bf16x2(f[2], f[3], h.y, l.y);
+          xs_hi[(long long)b * ld4 + jq] = h;
+          xs_lo[(long long)b * ld4 + jq] = l;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) f[c] = 0.f;
+        }
       } else if (rho <= len) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          xv[c] = __dadd_rn(__dmul_rn(alpha, xv[c]), (double)((w8[u] >> (8 * c)) & 0xffu));
-          f[c] = (float)xv[c];
+          const uint32_t xb8 = (w8[u] >> (8 * c)) & 0xffu;
+          xv[c] = __dadd_rn(__dmul_rn(alpha, xv[c]), (double)xb8);
+          f[c] = raw ? (float)xb8 : (float)xv[c];
         }
       }
       uint2 h, l;
@@ -1132,13 +1163,13 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
                       const float* ctab, void* c_hi, void* c_lo, void* w_hi, void* w_lo,
                       void* wa_hi, void* wa_lo, int ldc, float* mdt, float* psi_scratch,
                       cudaStream_t stream) {
-  SPB_CHECK_ARG(pass >= 0 && pass <= 3,
-                "spb_forward_chunk: pass must be 0 (A), 1 (B), 2 (B scan only) or 3 (B scan "
-                "only, input filter folded into C)");
-  SPB_CHECK_ARG(pass != 3 || (!reset && t0 == 0 && w_hi == nullptr),
-                "spb_forward_chunk: pass 3 is for one fresh chunk with reset = 0, no carry");
-  const bool filt = pass == 3;
-  if (filt) pass = 2;
+  SPB_CHECK_ARG(pass >= 0 && pass <= 4,
+                "spb_forward_chunk: pass must be 0 (A), 1 (B), 2 (B scan only), 3 (B scan only, "
+                "input filter folded into C / W) or 4 (B, input filter folded)");
+  SPB_CHECK_ARG(pass < 3 || !reset, "spb_forward_chunk: passes 3 / 4 need reset = 0");
+  const bool filt = pass >= 3;
+  if (pass == 3) pass = 2;
+  if (pass == 4) pass = 1;
   SPB_CHECK_ARG(pass == 2 || (cur && u && a), "spb_forward_chunk: null pointer");
   SPB_CHECK_ARG(B > 0 && n > 0 && Tc > 0 && len >= 0 && len <= Tc && KR >= Tc + 1 && KR % 8 == 0,
                 "spb_forward_chunk: bad sizes B=%d n=%d Tc=%d KR=%d len=%d", B, n, Tc, KR, len);
@@ -1175,7 +1206,8 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
   } else if (pass >= 1) {
     dim3 sgrid(ceil_div(n, 2 * K1S_THREADS), B);
     const bool carry = alif && w_hi != nullptr;
-    auto kfn = alif ? (carry ? chunk_scan_kernel<true, true>
+    auto kfn = alif ? (carry ? (filt ? chunk_scan_kernel<true, true, true>
+                                     : chunk_scan_kernel<true, true>)
                              : (filt ? chunk_scan_kernel<true, false, true>
                                      : chunk_scan_kernel<true, false>))
                     : (filt ? chunk_scan_kernel<false, false, true>
@@ -1236,7 +1268,8 @@ int spb_forward_scan_chunk(const double* cur, int B, int n, int Tc, int KR, int 
 
 static int xbar_launch(const uint8_t* x, long long stride_b, long long stride_t, int B, int k,
                        int kp, int KR, int len, int fresh, double alpha, double* xbar_state,
-                       void* xh, void* xl, bool segmented, cudaStream_t stream);
+                       void* xh, void* xl, bool segmented, cudaStream_t stream,
+                       void* xs_hi = nullptr, void* xs_lo = nullptr);
 
 int spb_xbar_chunk(const uint8_t* x, long long stride_b, long long stride_t, int B, int k, int kp,
                    int KR, int len, int fresh, double alpha, double* xbar_state, void* xh,
@@ -1256,13 +1289,30 @@ int spb_xbar_chunk_seg(const uint8_t* x, long long stride_b, long long stride_t,
                      !(es && es[0] == '0'), stream);
 }
 
+// Multi-chunk raw-spike operand (xh rows rho >= 1 = raw spikes, row 0 = 0, hi only) with
+// the fp64 filter state advanced by alpha and the entry state xbar_{t0-1} written to
+// xs_hi / xs_lo [B][kp] (bf16 hi/lo) for the GEMMs' row-0 terms.
+int spb_xbar_chunk_raw(const uint8_t* x, long long stride_b, long long stride_t, int B, int k,
+                       int kp, int KR, int len, int fresh, double alpha, double* xbar_state,
+                       void* xh, void* xs_hi, void* xs_lo, cudaStream_t stream) {
+  SPB_CHECK_ARG(xs_hi && xs_lo, "spb_xbar_chunk_raw: null entry-state buffer");
+  SPB_CHECK_ARG((stride_b | stride_t) % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0,
+                "spb_xbar_chunk_raw: the spike rows must be 4-byte aligned");
+  const char* es = getenv("SPB_XBAR_SEG");
+  return xbar_launch(x, stride_b, stride_t, B, k, kp, KR, len, fresh, alpha, xbar_state, xh,
+                     nullptr, !(es && es[0] == '0'), stream, xs_hi, xs_lo);
+}
+
 }  // extern "C"
 
 static int xbar_launch(const uint8_t* x, long long stride_b, long long stride_t, int B, int k,
                        int kp, int KR, int len, int fresh, double alpha, double* xbar_state,
-                       void* xh, void* xl, bool segmented, cudaStream_t stream) {
+                       void* xh, void* xl, bool segmented, cudaStream_t stream, void* xs_hi,
+                       void* xs_lo) {
+  const int raw = xs_hi != nullptr ? 1 : 0;
   // xl = NULL: only the hi part is written (alpha = 0 raw-spike operand: lo is 0)
-  SPB_CHECK_ARG(x && xbar_state && xh && (xl || alpha == 0.0), "spb_xbar_chunk: null pointer");
+  SPB_CHECK_ARG(x && xbar_state && xh && (xl || alpha == 0.0 || raw),
+                "spb_xbar_chunk: null pointer");
   SPB_CHECK_ARG(B > 0 && k > 0 && kp >= k && kp % 8 == 0 && KR > 0 && KR % 8 == 0 && len >= 0 &&
                     len < KR,
                 "spb_xbar_chunk: bad sizes");
@@ -1273,7 +1323,8 @@ static int xbar_launch(const uint8_t* x, long long stride_b, long long stride_t,
     dim3 gs(ceil_div(kp / 4, 32), B);
     xbar_seg_kernel<<<gs, 32 * (KR / XSEG_ROWS), 0, stream>>>(
         x, stride_b, stride_t, B, k, kp, KR, len, fresh, alpha, xbar_state,
-        reinterpret_cast<uint2*>(xh), reinterpret_cast<uint2*>(xl));
+        reinterpret_cast<uint2*>(xh), reinterpret_cast<uint2*>(xl), raw,
+        reinterpret_cast<uint2*>(xs_hi), reinterpret_cast<uint2*>(xs_lo));
     SPB_CHECK_LAUNCH("xbar_seg");
     return 0;
   }
@@ -1281,10 +1332,13 @@ static int xbar_launch(const uint8_t* x, long long stride_b, long long stride_t,
     dim3 grid4(ceil_div(kp / 4, 128), B);
     xbar_chunk4_kernel<<<grid4, 128, 0, stream>>>(x, stride_b, stride_t, B, k, kp, KR, len, fresh,
                                                   alpha, xbar_state, reinterpret_cast<uint2*>(xh),
-                                                  reinterpret_cast<uint2*>(xl));
+                                                  reinterpret_cast<uint2*>(xl), raw,
+                                                  reinterpret_cast<uint2*>(xs_hi),
+                                                  reinterpret_cast<uint2*>(xs_lo));
     SPB_CHECK_LAUNCH("xbar_chunk4");
     return 0;
   }
+  SPB_CHECK_ARG(!raw, "spb_xbar_chunk_raw: unaligned operand");
   dim3 grid(ceil_div(kp / 2, 128), B);
   xbar_chunk_kernel<<<grid, 128, 0, stream>>>(x, stride_b, stride_t, B, k, kp, KR, len, fresh,
                                               alpha, xbar_state,

@@ -274,7 +274,7 @@ int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* 
                            long long slice_stride, cudaStream_t stream) {
   SPB_CHECK_ARG(ah && al && bh && partial, "spb_grad_gemm_partials: null pointer");
   const bool blo = bl != nullptr;  // bl = NULL: B is exact in bf16 (no lo part), 2 MMAs
-  SPB_CHECK_ARG(M > 0 && N_rows > 0 && K > 0 && K % 8 == 0 && splits > 0 && ldp >= 1 &&
+  SPB_CHECK_ARG(M > 0 && N_rows > 0 && K > 0 && splits > 0 && ldp >= 1 &&
                     lda >= M && lda % 8 == 0 && ldb >= N_rows && ldb % 8 == 0,
                 "spb_grad_gemm_partials: bad sizes M=%d lda=%d N=%d K=%d", M, lda, N_rows, K);
   SPB_CHECK_ARG((reinterpret_cast<uintptr_t>(ah) | reinterpret_cast<uintptr_t>(al) |

@@ -203,6 +203,9 @@ class EpropEngine:
             self.xq2 = torch.zeros((B * self.Tc, self.Kx2), dtype=torch.uint8, device=dev)
         self.xh = torch.zeros((K, self.kp), dtype=bf16, device=dev)   # MN-major [K][kp]
         self.xl = torch.zeros((K, self.kp), dtype=bf16, device=dev)
+        # entry filter state xbar_{t0-1} of a later chunk (raw-spike operand), bf16 hi/lo
+        self.xs_hi = torch.zeros((B, self.kp), dtype=bf16, device=dev)
+        self.xs_lo = torch.zeros((B, self.kp), dtype=bf16, device=dev)
         # split-K (K5) and sample-split (K6) partial slices, reduced in fixed order
         tiles5 = math.ceil(self.kp / 256) * math.ceil(n / 128)   # K5 tiles are 128 x 256
         # split-K so the grid fills whole waves of SMs (C4: 96 tiles x 3 = 1.95 waves)
@@ -225,7 +228,8 @@ class EpropEngine:
         else:
             self.w_hi = self.w_lo = self.mdt = self.eps = None
             self.splits6 = 0
-        self.partial = torch.zeros((self.splits5 + self.splits6, self.n_pad, self.kp),
+        # partial slices: [K5 splits | K6 splits | 1 for the carried-filter row-0 GEMM]
+        self.partial = torch.zeros((self.splits5 + self.splits6 + 1, self.n_pad, self.kp),
                                    dtype=f32, device=dev)
         self.grad_w_acc = torch.empty((n, self.kp), dtype=f64, device=dev)
         self.grad_wout = torch.empty((m, n), dtype=f64, device=dev)
@@ -395,10 +399,12 @@ class EpropEngine:
         # one fresh chunk, reset=False: the input filter is folded into the coefficients
         # (scan pass 3), so K5 too runs on the raw spikes (forward.cu FILT).  Raw-spike
         # operands are exact in bf16: no lo part (K4 writes hi only, K5 does 2 MMAs).
-        filt = (one and not self.reset and not self.recurrent and not forward_only
-                and self.filt)
-        if filt:
-            x_alpha = 0.0
+        # Several chunks: the same on every chunk (scan pass 4 / 3), with the entry state
+        # xbar_{t0-1} of each later chunk handled apart -- K4 writes it to xs_hi/lo, a
+        # K = B GEMM adds Ct_0 (x) xbar_{t0-1} and K6 adds Wt_0 xbar_{t0-1} in its epilogue.
+        filt = (not self.reset and not self.recurrent and not forward_only and self.filt)
+        if filt and one:
+            x_alpha = 0.0   # K4 = byte -> bf16 copy (the filter state is never needed)
         raw_x = (filt or self.reset) and not self.recurrent
         xl_ptr = None if raw_x else v(self.xl.data_ptr())
 
@@ -549,7 +555,7 @@ class EpropEngine:
             # one chunk (pass A parked psi) or K21 / K1rec (park psi themselves): scan only
             pid = 2 if (one or self.fused or self.recurrent) else 1
             if filt:
-                pid = 3
+                pid = 3 if pid == 2 else 4
             if not kf:
                 timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,
                       v(self.cur.data_ptr()) if self.cur is not None else None, B, n, Tc, KR,
@@ -574,6 +580,12 @@ class EpropEngine:
                 self.launches += 2
             elif one and use_side and self.xbar_sched != "main":
                 main.wait_event(self._ev["xbar"])
+            elif filt and not one:
+                call("spb_xbar_chunk_raw", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp,
+                     KR, ln, int(c == 0), float(alpha), v(self.xbar_state.data_ptr()),
+                     v(self.xh.data_ptr()), v(self.xs_hi.data_ptr()), v(self.xs_lo.data_ptr()),
+                     st)
+                self.launches += 1
             else:
                 call("spb_xbar_chunk_seg", v(self.xq.data_ptr()), xq_sb, xq_st, B, k, self.kp, KR,
                      ln, int(c == 0 or self.reset), x_alpha, v(self.xbar_state.data_ptr()),
@@ -584,16 +596,25 @@ class EpropEngine:
                   self.kp, n, self.kp, K, self.splits5, v(self.partial.data_ptr()), self.kp,
                   slice_stride, st)
             self.launches += 1
+            entry = filt and not one and c > 0   # row-0 terms of the carried filter state
+            if entry:  # sum_b Ct_0[b,i] xbar_{t0-1}[b,j]: rows b*KR of C, K = B
+                call("spb_grad_gemm_partials", v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()),
+                     KR * self.ldc, v(self.xs_hi.data_ptr()), v(self.xs_lo.data_ptr()),
+                     self.kp, n, self.kp, B, 1,
+                     v(self.partial.data_ptr() + (self.splits5 + self.splits6) * slice_stride * 4),
+                     self.kp, slice_stride, st)
+                self.launches += 1
             slices = self.splits5
             if self.ntr and (c > 0 or not last):
                 # first chunk: E0 = 0 (nothing to add, only carry); last chunk: no carry
                 if self.ntr == 1:
                     timed("carry", (ln, c > 0, not last), "spb_alif_carry_chunk",
                           v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()), self.ldc,
-                          v(self.xh.data_ptr()), v(self.xl.data_ptr()), v(self.mdt.data_ptr()),
+                          v(self.xh.data_ptr()), xl_ptr, v(self.mdt.data_ptr()),
                           v(self.eps.data_ptr()), v(part6), B, n, self.n_pad, self.kx, self.ke,
                           self.kp, KR, self.splits6, int(not last), int(c > 0), int(not last),
-                          st)
+                          v(self.xs_hi.data_ptr()) if entry else None,
+                          v(self.xs_lo.data_ptr()) if entry else None, st)
                 else:
                     timed("carry", (ln, c > 0, not last), "spb_reset_carry_chunk",
                           v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()),
@@ -606,6 +627,8 @@ class EpropEngine:
                 self.launches += 1
                 if c > 0:
                     slices += self.splits6
+            if entry:  # the row-0 slice sits after K6's (layout [K5 | K6 | row 0])
+                slices = self.splits5 + self.splits6 + 1
             call("spb_reduce_partials", v(self.partial.data_ptr()), slices, n, self.n_pad,
                  self.kp, int(c > 0), v(self.grad_w_acc.data_ptr()), st)
             self.launches += 1

@@ -6,7 +6,7 @@ import ctypes
 import os
 import re
 
-XB = ("spb_xbar_chunk", "spb_xbar_chunk_seg")  # K4: sequential / time-segmented entry
+XB = ("spb_xbar_chunk", "spb_xbar_chunk_seg", "spb_xbar_chunk_raw")  # K4 entry points
 
 import numpy as np
 import pytest
@@ -74,7 +74,7 @@ def test_bad_arguments_are_rejected_without_gpu():
         _lib.call("spb_input_proj", None, None, None, 1, 1, 32, 100, 7, None, 148, 0, None)
     with pytest.raises(P.ShapeMismatch):
         _lib.call("spb_alif_carry_chunk", None, None, 8, None, None, None, None, None, 1, 1, 100,
-                  1, 4, 128, 64, 1, 0, 0, 0, None)
+                  1, 4, 128, 64, 1, 0, 0, 0, None, None, None)
 
 
 class _Recorder:
@@ -114,7 +114,8 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     assert names.count("spb_input_proj") == (2 * nch if nch > 1 else 1)
     assert names.count("spb_slice_weights") == 0
     assert sum(names.count(x) for x in XB) == nch
-    assert names.count("spb_grad_gemm_partials") == nch
+    # K5 per chunk, plus the K = B GEMM of the carried filter state for chunks after the first
+    assert names.count("spb_grad_gemm_partials") == nch + (nch - 1)
     carries = [c[1] for c in rec.calls if c[0] == "spb_alif_carry_chunk"]
     if alif:
         # no carry launch for a single chunk; chunk 0 only carries, the last only adds M E0

@@ -118,3 +118,32 @@ def test_segmented_xbar_matches_sequential(kind, n, k, B, T, chunk, monkeypatch)
     np.testing.assert_allclose(a[1], b[1], rtol=1e-13, atol=1e-13)
     np.testing.assert_allclose(a[2], b[2], rtol=2 ** -7, atol=0)
     assert _rel(a[0], b[0]) < 1e-6
+
+
+@pytest.mark.parametrize("kind,n,k,B,T,chunk", [("alif", 256, 130, 5, 300, 63),
+                                                 ("lif", 200, 64, 9, 400, 127),
+                                                 ("alif", 1024, 96, 40, 600, 255)])
+def test_raw_operand_multichunk_matches_xbar(kind, n, k, B, T, chunk, monkeypatch):
+    """Several chunks on the raw-spike operand (filter folded into C / W, the carried
+    filter state through the K = B row-0 GEMM and the K6 epilogue) vs the filtered-input
+    operand: the same sums in another order (gradient to fp32 rounding)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200.gradients import _neuron_kwargs
+    net = P.init_network(P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=5,
+                                       precision="f32", seed=21))
+    x, y = poisson_batch(B, k, T, 5, seed=22)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SPB_FILT", flag)
+        eng = EpropEngine(n, k, 5, B, alif=net.is_alif, chunk=chunk)
+        assert eng.filt == (flag == "1")
+        eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+        eng.run(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), **_neuron_kwargs(net))
+        torch.cuda.synchronize()
+        out[flag] = (eng.grad_w_acc.cpu().numpy().copy(), eng.loss.cpu().numpy().copy())
+    assert np.array_equal(out["1"][1], out["0"][1])
+    assert _rel(out["1"][0], out["0"][0]) < 1e-5
