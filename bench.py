@@ -463,6 +463,7 @@ def main():
                     byts += B * ln * n / 8.0 + 16.0 * B * n           # raster, zbar/zsum
             elif name in ("forward", "forward_a"):
                 ln, pid, flag = meta
+                pid = {3: 2, 4: 1}.get(pid, pid)   # raw-operand passes: same traffic
                 psi = 4.0 * B * (ln + 1) * n
                 if pid <= 1:                       # dynamics: read the fp64 current
                     byts += 8.0 * B * ln * n
