@@ -499,6 +499,40 @@ __global__ void __launch_bounds__(256) pack_bytes4_kernel(const uint8_t* __restr
   }
 }
 
+// Bit-packed rows (np.packbits little order): thread per input byte = 8 output bytes
+// (one 8-byte store), CTA per 4 rows with their loads in flight together.
+__global__ void __launch_bounds__(128) pack_bits8_kernel(const uint8_t* __restrict__ x,
+                                                         long long stride_b, int k, int len,
+                                                         int Tc, int Kpad, int B, int tmajor,
+                                                         uint8_t* __restrict__ xq) {
+  const int kb = (k + 7) >> 3;   // input bytes per row
+  const int wpr = Kpad >> 3;     // output 8-byte words per row
+  const int rows = B * Tc;
+  constexpr int R = 4;
+  const int row0 = blockIdx.x * R;
+  for (int w = threadIdx.x; w < wpr; w += blockDim.x) {
+    uint32_t v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int row = row0 + q;
+      const int s = tmajor ? row / B : row % Tc;
+      const int b = tmajor ? row % B : row / Tc;
+      uint32_t byte = 0u;
+      if (row < rows && s < len && w < kb) {
+        byte = __ldg(x + (long long)b * stride_b + (long long)s * kb + w);
+        const int left = k - 8 * w;  // valid channels in this byte
+        if (left < 8) byte &= (1u << left) - 1u;
+      }
+      v[q] = byte;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (row0 + q < rows)
+        reinterpret_cast<uint2*>(xq + (long long)(row0 + q) * Kpad)[w] =
+            make_uint2(expand4(v[q] & 0xfu), expand4(v[q] >> 4));
+  }
+}
+
 __global__ void pack_spikes_kernel(const uint8_t* __restrict__ x, long long stride_b, int k,
                                    int bits, int len, int Tc, int Kpad, int B, int tmajor,
                                    uint8_t* __restrict__ xq) {
@@ -561,6 +595,14 @@ int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits
     proj::pack_bytes4_kernel<<<b4, t4, 0, stream>>>(x, stride_b, k, len, Tc, Kpad, B, time_major,
                                                      xq);
     SPB_CHECK_LAUNCH("pack_bytes4");
+    return 0;
+  }
+  if (bits) {
+    const int b8 = (int)((rows + 3) / 4);
+    const int t8 = std::min(128, ((Kpad / 8 + 31) / 32) * 32);
+    proj::pack_bits8_kernel<<<b8, t8, 0, stream>>>(x, stride_b, k, len, Tc, Kpad, B, time_major,
+                                                    xq);
+    SPB_CHECK_LAUNCH("pack_bits8");
     return 0;
   }
   proj::pack_spikes_kernel<<<blocks, 256, 0, stream>>>(x, stride_b, k, bits, len, Tc, Kpad, B,
