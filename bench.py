@@ -223,10 +223,17 @@ def main():
     from paper_2501_11407_b200 import _lib
     from paper_2501_11407_b200.parallel import GradPacker
 
+    # one GPU per rank (NCCL); SPB_DIST_BACKEND=gloo lets several ranks share one GPU to
+    # exercise the multi-rank path (packing, allreduce, max over ranks) on a 1-GPU box
+    backend = os.environ.get("SPB_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     kind, n, k, m, T, B = CONFIGS[args.config]
     spec = P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=m, precision="f32", seed=0,
                          recurrent=args.recurrent)
