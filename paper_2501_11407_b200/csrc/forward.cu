@@ -429,7 +429,9 @@ __global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
     cs[r] = (P.t0 + r - 1 >= 0) ? ctab[P.t0 + r - 1] : 0.f;
   __syncthreads();
   const int i = blockIdx.x * 2 * K1S_THREADS + warp * 64 + 2 * lane;  // neurons i, i+1
-  const int b = blockIdx.y;
+  // samples in reverse launch order: K1 parked the psi of the last samples most recently,
+  // so the first scan CTAs find it in L2
+  const int b = (int)gridDim.y - 1 - (int)blockIdx.y;
   if (b >= P.B || i >= P.n) return;
   const int n = P.n;
   const bool has2 = i + 1 < n;
