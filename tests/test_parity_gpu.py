@@ -161,6 +161,10 @@ def test_shd_ssc_shapes_vs_reference(name, chunk):
     ("alif", 96, 60, 4, 1300, 4, 511),      # 3 chunks of 511 (the long-sequence default)
     ("alif", 333, 45, 3, 130, 5, 127),      # odd n: unaligned current rows
     ("lif", 70, 50, 3, 600, 6, 511),
+    ("alif", 33, 9, 2, 1, 3, 63),           # a single time step
+    ("alif", 40, 20, 3, 64, 2, 63),         # two chunks, the last one step long
+    ("lif", 1, 1, 2, 20, 1, 63),            # one neuron, one input, one sample
+    ("alif", 257, 129, 4, 255, 3, 255),     # T exactly one chunk, n / k one past a tile
 ])
 def test_batched_vs_two_pass_oracle(kind, n, k, m, T, B, chunk):
     """Ragged shapes (n, k not tile multiples, T not a chunk multiple) vs the numpy oracle."""
