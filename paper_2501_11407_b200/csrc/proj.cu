@@ -61,6 +61,23 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, 
       "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// The 4 MMAs of one 128-byte K block (K = 32 bytes each) under ONE elect.sync: the
+// descriptors of steps 1..3 are the step-0 descriptors + 2 (32 bytes in 16-byte units of
+// the start-address field, SW128 K-major), formed inside the block.
+__device__ __forceinline__ void mma_i8_x4(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                          uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a2, b2, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %3, 1;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc0));
+}
 __device__ __forceinline__ void commit(uint32_t bar) {
   asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
                "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
@@ -310,10 +327,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t xa = smem_u32(xsm + s * TILE_A);
           const uint32_t wa = smem_u32(wsm + kb * C::WBLK);
-#pragma unroll
-          for (int kk = 0; kk < BK / 32; ++kk)
-            mma_i8(dacc, desc_k_sw128(xa + kk * 32), desc_k_sw128(wa + kk * 32), Cfg<P>::IDESC,
-                   (kb | kk) ? 1u : 0u);
+          static_assert(BK / 32 == 4, "four K steps per block");
+          mma_i8_x4(dacc, desc_k_sw128(xa), desc_k_sw128(wa), Cfg<P>::IDESC, kb ? 1u : 0u);
           commit(smem_u32(&xempty[s]));
         }
         commit(smem_u32(&tfull[a]));
