@@ -98,7 +98,8 @@ def test_fused_ragged_many_chunks(kind, reset, smooth, wdt, bits):
         assert np.array_equal(fu[0][b], ras)
 
 
-def test_graphed_update_equals_eager():
+@pytest.mark.parametrize("T", [150, 60])   # three chunks / one chunk (side-stream K4)
+def test_graphed_update_equals_eager(T):
     """EpropEngine.graphed: the captured CUDA graph replays the same update bit for bit."""
     _need_gpu()
     import paper_2501_11407_b200 as P
@@ -112,14 +113,14 @@ def test_graphed_update_equals_eager():
     eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
     outs = []
     for seed in (1, 2):
-        x, y = poisson_batch(12, 90, 150, 5, seed=seed)
+        x, y = poisson_batch(12, 90, T, 5, seed=seed)
         xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
         eng.run(xd, yd, **kw)
         torch.cuda.synchronize()
         outs.append((eng.grad_w_acc.cpu().numpy().copy(), eng.loss.cpu().numpy().copy()))
     step = eng.graphed(xd, yd, **kw)
     for seed, (gw, ls) in zip((1, 2), outs):
-        x, y = poisson_batch(12, 90, 150, 5, seed=seed)
+        x, y = poisson_batch(12, 90, T, 5, seed=seed)
         step(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
         torch.cuda.synchronize()
         assert np.array_equal(eng.grad_w_acc.cpu().numpy(), gw)
