@@ -49,4 +49,16 @@ __device__ __forceinline__ double digits_current(long long g0, long long g1, int
   }
 }
 
+// the same with the per-neuron scale 2^(s - F) precomputed (one per neuron tile)
+template <int P, bool BIN>
+__device__ __forceinline__ double digits_current_scaled(long long g0, long long g1, double scale) {
+  using D = Digits<P>;
+  if constexpr (BIN && D::kSingleOk) {
+    const long long g = (g0 << D::HI) + g1;
+    return (double)g * scale;
+  } else {
+    return fma((double)g0, scale * (double)(1LL << D::HI), (double)g1 * scale);
+  }
+}
+
 }  // namespace spb

@@ -131,8 +131,9 @@ constexpr int NH = NT / 2;  // neurons per epilogue thread (16 epilogue warps me
 // recombine into ONE int64 g = sum_p S_p 128^(6-p) (|g| < 2^63) and I = (double)g *
 // 2^(s-48): one rounding of the exact sum, bitwise the value of the two-part path below,
 // with half the fp64-pipe work.
-template <int P, bool BIN>
-__device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&se)[NH],
+// SE: per-neuron exponents (int) or precomputed scales 2^(s-F) (double)
+template <int P, bool BIN, typename SE = int>
+__device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se)[NH],
                                                    double* __restrict__ out, int M, int n, int row,
                                                    int i0, uint32_t tempty_bar, int lane,
                                                    int probe = 0) {
@@ -168,7 +169,12 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const int (&s
   for (int c = 0; c < NH; c += 2) {
     double v[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) v[h] = digits_current<P, BIN>(g0[c + h], g1[c + h], se[c + h]);
+    for (int h = 0; h < 2; ++h) {
+      if constexpr (sizeof(SE) == sizeof(double))
+        v[h] = digits_current_scaled<P, BIN>(g0[c + h], g1[c + h], se[c + h]);
+      else
+        v[h] = digits_current<P, BIN>(g0[c + h], g1[c + h], se[c + h]);
+    }
     ch[c / 2] = make_double2(v[0], v[1]);
   }
   if (probe & 4) {  // profiling probe: no global stores
@@ -340,24 +346,32 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = warp & 3;          // TMEM lane quarter
     const int hh = (warp - 2) >> 2;  // neuron half of the tile
     int lt = 0;
+    // tile coordinates advanced incrementally (no per-tile division); the per-neuron
+    // scales 2^(s-F) change only with the neuron tile
+    int nt = t_begin / m_tiles, mt = t_begin % m_tiles, sc_nt = -1;
+    double sc[NH];
     for (int t = t_begin; t < t_end; ++t, ++lt) {
-      const int nt = t / m_tiles, mt = t % m_tiles;
       const int a = lt & 1;
       const int i0 = nt * NT + hh * NH;
-      int se[NH];  // per-neuron exponents, fetched before waiting on the tensor cores
+      if (nt != sc_nt) {
 #pragma unroll
-      for (int c = 0; c < NH; ++c) se[c] = (i0 + c < n) ? __ldg(sexp + i0 + c) : 0;
+        for (int c = 0; c < NH; ++c)
+          sc[c] = digits_pow2(((i0 + c < n) ? __ldg(sexp + i0 + c) : 0) - Digits<P>::F);
+        sc_nt = nt;
+      }
       mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (probe & 1) {  // profiling probe: no epilogue (TMEM reads, recombination, stores)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&tempty[a]));
+        if (++mt == m_tiles) { mt = 0; ++nt; }
         continue;
       }
       proj_epilogue_tile<P, BIN>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH),
-                            se, out, M, n, mt * BM + q * 32 + lane, i0, smem_u32(&tempty[a]),
+                            sc, out, M, n, mt * BM + q * 32 + lane, i0, smem_u32(&tempty[a]),
                             lane, probe);
+      if (++mt == m_tiles) { mt = 0; ++nt; }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
