@@ -416,8 +416,9 @@ constexpr int K1S_THREADS = 128;  // 4 warps = 256 consecutive neurons of one sa
 // coefficients -- sum_rho C_rho xbar_{rho-1} = sum_rho Ct_rho x_{rho-1} (+ Ct_0 xbar_{-1}
 // = 0) with Ct_rho = C_rho + alpha Ct_{rho+1} -- so the gradient GEMM runs on the RAW
 // spikes, exact in bf16 (2 MMAs instead of 3, half the operand bytes, no filter kernel).
+// (7 CTAs per SM, <= 73 registers: the C3 grid of B x n/256 = 1024 CTAs is one wave)
 template <bool ALIF, bool CARRY, bool FILT = false>
-__global__ void __launch_bounds__(K1S_THREADS) chunk_scan_kernel(
+__global__ void __launch_bounds__(K1S_THREADS, 7) chunk_scan_kernel(
     FwdParams P, const float* __restrict__ wsig, const float* __restrict__ ctab,
     uint32_t* __restrict__ c_hi, uint32_t* __restrict__ c_lo, uint32_t* __restrict__ w_hi,
     uint32_t* __restrict__ w_lo, int ldc, float2* __restrict__ mdt,
