@@ -397,15 +397,26 @@ def main():
                 yb[i % 2].copy_(yh, non_blocking=True)
                 copied[i % 2].record(cs)
 
-        # one CUDA graph per input slot (EpropEngine.graphed on the double buffer itself)
+        # one CUDA graph per input slot: the whole step (update included) on the double
+        # buffer itself, replayed once its host-to-device copy has landed
         gsteps = None
-        if args.e2e_graph and graph is not None and hasattr(eng, "graphed"):
+        if args.e2e_graph and graph is not None:
             try:
                 for i in range(2):
                     xb[i].copy_(torch.from_numpy(x_bits).to(dev))
                     yb[i].copy_(yd)
-                gsteps = [eng.graphed(xb[i], yb[i], static_inputs=True, bits=True, binary=True,
-                                      **kw) for i in range(2)]
+                torch.cuda.synchronize()
+                gsteps = []
+                for i in range(2):
+                    cs2 = torch.cuda.Stream(device=dev)
+                    cs2.wait_stream(torch.cuda.current_stream(dev))
+                    with torch.cuda.stream(cs2):
+                        step(xb[i], yb[i], bits=True)          # warm the capture stream
+                    torch.cuda.current_stream(dev).wait_stream(cs2)
+                    g_i = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g_i, stream=cs2):
+                        step(xb[i], yb[i], bits=True)
+                    gsteps.append(g_i.replay)
                 barrier()
             except Exception as exc:  # noqa: BLE001
                 print(f"[bench] e2e graph capture failed ({exc}); eager", file=sys.stderr)
@@ -419,10 +430,6 @@ def main():
                 main.wait_event(copied[i % 2])
                 if gsteps is not None:
                     gsteps[i % 2]()
-                    if world > 1:
-                        packer.pack(eng.grad_w_acc, eng.grad_wout, eng.loss, eng.correct)
-                        packer.allreduce()
-                    update()
                 else:
                     step(xb[i % 2], yb[i % 2], bits=True)
                 consumed[i % 2].record(main)
@@ -446,7 +453,7 @@ def main():
                "d2h_bytes_per_step": int(B * 8),
                "ms_per_step": float(e2e_ms.item()),
                "pipeline": "H2D of step i+1 on a copy stream overlaps step i (double buffer)"
-                           + ("; each step replays the update's CUDA graph (EpropEngine.graphed)"
+                           + ("; each step replays the whole update's CUDA graph"
                               if gsteps is not None else "")}
 
     # ---- roofline of every main kernel; the dominant one is the headline ----
