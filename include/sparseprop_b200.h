@@ -55,6 +55,11 @@ int spb_slice_weights(const void* w, int w_is_f64, int n, int k, int Kpad, int n
                       int8_t* wq, int* sexp, cudaStream_t stream);
 int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits, int len, int Tc,
                     int Kpad, int time_major, uint8_t* xq, cudaStream_t stream);
+/* spb_pack_spikes (sample-major) that also writes the one-chunk raw-spike GEMM operand of
+ * K5: xh bf16 [B*KR][Kpad], row b*KR + s + 1 = the spikes of step s (row 0 untouched,
+ * zero) -- K4 folded into the pack. */
+int spb_pack_spikes_xh(const uint8_t* x, long long stride_b, int B, int k, int bits, int len,
+                       int Tc, int Kpad, int KR, uint8_t* xq, void* xh, cudaStream_t stream);
 int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
                    int Kpad, int P, double* cur, int sm_count, int binary, cudaStream_t stream);
 /* K2 on CTA pairs (proj2.cu): the same exact projection with tcgen05.mma.cta_group::2 --

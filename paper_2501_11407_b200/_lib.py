@@ -23,6 +23,7 @@ D = ctypes.c_double
 SIGNATURES = {
     "spb_slice_weights": [P, I, I, I, I, I, I, P, P, P],
     "spb_pack_spikes": [P, LL, I, I, I, I, I, I, I, P, P],
+    "spb_pack_spikes_xh": [P, LL, I, I, I, I, I, I, I, P, P, P],
     "spb_fused_forward_probe": [I, P, P, P, I, I, I, I, I, I, I, I, I, I, D, D, D, D, D, D, I,
                                 I, P, P, P, P, P, P, I, I, P],
     "spb_fused_forward": [I, P, P, P, I, I, I, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I,

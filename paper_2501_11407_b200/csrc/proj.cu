@@ -502,10 +502,24 @@ __device__ __forceinline__ uint32_t expand4(uint32_t nib) {  // 4 bits -> 4 byte
 // Byte-count rows with k, the row stride and x 4-byte aligned (the common case): CTA per 4
 // rows, thread per 4 output bytes of each -- each warp moves 128 contiguous bytes in and
 // out per row (coalesced u32), the 4 rows' loads in flight together.
+// bf16 of four spike counts (0..255, exact): the upper halves of their fp32 encodings
+__device__ __forceinline__ uint2 bf16x4_of_bytes(uint32_t w) {
+  uint2 h;
+  h.x = (__float_as_uint((float)(w & 0xffu)) >> 16) |
+        (__float_as_uint((float)((w >> 8) & 0xffu)) & 0xffff0000u);
+  h.y = (__float_as_uint((float)((w >> 16) & 0xffu)) >> 16) |
+        (__float_as_uint((float)(w >> 24)) & 0xffff0000u);
+  return h;
+}
+
+// xh != NULL: also the raw-spike GEMM operand (bf16 [B*KR][Kpad], row b*KR + s + 1 =
+// spikes of step s; row 0 is left as is, zero) -- the one-chunk K4 folded into the pack.
 __global__ void __launch_bounds__(256) pack_bytes4_kernel(const uint8_t* __restrict__ x,
                                                           long long stride_b, int k, int len,
                                                           int Tc, int Kpad, int B, int tmajor,
-                                                          uint8_t* __restrict__ xq) {
+                                                          uint8_t* __restrict__ xq,
+                                                          uint2* __restrict__ xh = nullptr,
+                                                          int KR = 0) {
   const int wpr = Kpad >> 2;  // output words per row
   const int rows = B * Tc;
   constexpr int R = 4;        // rows per CTA, their loads issued together
@@ -525,6 +539,16 @@ __global__ void __launch_bounds__(256) pack_bytes4_kernel(const uint8_t* __restr
 #pragma unroll
     for (int q = 0; q < R; ++q)
       if (row0 + q < rows) reinterpret_cast<uint32_t*>(xq + (long long)(row0 + q) * Kpad)[w] = v[q];
+    if (xh != nullptr) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int row = row0 + q;
+        if (row < rows) {
+          const int s = row % Tc, b = row / Tc;
+          xh[((long long)b * KR + s + 1) * (Kpad >> 2) + w] = bf16x4_of_bytes(v[q]);
+        }
+      }
+    }
   }
 }
 
@@ -533,7 +557,9 @@ __global__ void __launch_bounds__(256) pack_bytes4_kernel(const uint8_t* __restr
 __global__ void __launch_bounds__(128) pack_bits8_kernel(const uint8_t* __restrict__ x,
                                                          long long stride_b, int k, int len,
                                                          int Tc, int Kpad, int B, int tmajor,
-                                                         uint8_t* __restrict__ xq) {
+                                                         uint8_t* __restrict__ xq,
+                                                         uint4* __restrict__ xh = nullptr,
+                                                         int KR = 0) {
   const int kb = (k + 7) >> 3;   // input bytes per row
   const int wpr = Kpad >> 3;     // output 8-byte words per row
   const int rows = B * Tc;
@@ -559,6 +585,22 @@ __global__ void __launch_bounds__(128) pack_bits8_kernel(const uint8_t* __restri
       if (row0 + q < rows)
         reinterpret_cast<uint2*>(xq + (long long)(row0 + q) * Kpad)[w] =
             make_uint2(expand4(v[q] & 0xfu), expand4(v[q] >> 4));
+    if (xh != nullptr) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int row = row0 + q;
+        if (row < rows) {
+          const int s = row % Tc, b = row / Tc;
+          // 8 spikes -> 8 bf16 (0x3F80 = 1.0)
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            o[e] = (((v[q] >> (2 * e)) & 1u) ? 0x3F80u : 0u) |
+                   (((v[q] >> (2 * e + 1)) & 1u) ? 0x3F800000u : 0u);
+          xh[((long long)b * KR + s + 1) * (Kpad >> 3) + w] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+      }
+    }
   }
 }
 
@@ -610,6 +652,9 @@ using namespace spb;
 
 extern "C" {
 
+int spb_pack_spikes_xh(const uint8_t* x, long long stride_b, int B, int k, int bits, int len,
+                       int Tc, int Kpad, int KR, uint8_t* xq, void* xh, cudaStream_t stream);
+
 int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits, int len, int Tc,
                     int Kpad, int time_major, uint8_t* xq, cudaStream_t stream) {
   SPB_CHECK_ARG(x && xq && B > 0 && k > 0 && Kpad >= k && Kpad % proj::BK == 0 && len >= 0 &&
@@ -637,6 +682,30 @@ int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits
   proj::pack_spikes_kernel<<<blocks, 256, 0, stream>>>(x, stride_b, k, bits, len, Tc, Kpad, B,
                                                         time_major, xq);
   SPB_CHECK_LAUNCH("pack_spikes");
+  return 0;
+}
+
+// spb_pack_spikes (sample-major) that also writes the one-chunk raw-spike GEMM operand
+// xh (bf16 [B*KR][Kpad], row b*KR + s + 1 = step s, row 0 untouched = zero).
+int spb_pack_spikes_xh(const uint8_t* x, long long stride_b, int B, int k, int bits, int len,
+                       int Tc, int Kpad, int KR, uint8_t* xq, void* xh, cudaStream_t stream) {
+  SPB_CHECK_ARG(x && xq && xh && B > 0 && k > 0 && Kpad >= k && Kpad % proj::BK == 0 &&
+                    len >= 0 && len <= Tc && KR >= Tc + 1,
+                "spb_pack_spikes_xh: bad args");
+  const long long rows = (long long)B * Tc;
+  if (bits) {
+    const int t8 = std::min(128, ((Kpad / 8 + 31) / 32) * 32);
+    proj::pack_bits8_kernel<<<(int)((rows + 3) / 4), t8, 0, stream>>>(
+        x, stride_b, k, len, Tc, Kpad, B, 0, xq, static_cast<uint4*>(xh), KR);
+    SPB_CHECK_LAUNCH("pack_bits8_xh");
+    return 0;
+  }
+  SPB_CHECK_ARG((k & 3) == 0 && (stride_b & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0,
+                "spb_pack_spikes_xh: byte rows must be 4-byte aligned");
+  const int t4 = std::min(256, ((Kpad / 4 + 31) / 32) * 32);
+  proj::pack_bytes4_kernel<<<(int)((rows + 3) / 4), t4, 0, stream>>>(
+      x, stride_b, k, len, Tc, Kpad, B, 0, xq, static_cast<uint2*>(xh), KR);
+  SPB_CHECK_LAUNCH("pack_bytes4_xh");
   return 0;
 }
 

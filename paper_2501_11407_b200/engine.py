@@ -189,6 +189,7 @@ class EpropEngine:
         self.k1f = os.environ.get("SPB_K1F", "0") == "1" and m <= 64
         # fold the input filter into the one-chunk coefficients (SPB_FILT=0: xbar operand)
         self.filt = os.environ.get("SPB_FILT", "1") != "0"
+        self.pack_xh = os.environ.get("SPB_PACK_XH", "1") != "0"
         self.kf_sync = torch.zeros(1 + 2 * B, dtype=torch.int32, device=dev)
         self.kf_part = torch.empty(B * ((n + 127) // 128) * m, dtype=f64, device=dev)
         self.ldc = _round_up(n, 8)   # C/W are MN-major [K][ldc] (neurons contiguous)
@@ -302,9 +303,15 @@ class EpropEngine:
             self._ctab_T = (T, kappa)
         return self.ctab
 
-    def _pack(self, xp, strideb, bits, ln, st):
+    def _pack(self, xp, strideb, bits, ln, st, xh=False):
         """Chunk spikes (bytes or bits) -> zero-padded projection operand xq [B*Tc][Kpad]
-        (rows b*Tc + s for K2, time-major s*B + b for K21; also K4's row source)."""
+        (rows b*Tc + s for K2, time-major s*B + b for K21; also K4's row source).  xh: also
+        write the one-chunk raw-spike GEMM operand (K4 folded into the pack)."""
+        if xh:
+            _lib.call("spb_pack_spikes_xh", ctypes_void(xp), strideb, self.B, self.k, int(bits),
+                      ln, self.Tc, self.Kpad, self.KR, ctypes_void(self.xq.data_ptr()),
+                      ctypes_void(self.xh.data_ptr()), st)
+            return
         _lib.call("spb_pack_spikes", ctypes_void(xp), strideb, self.B, self.k, int(bits), ln,
                   self.Tc, self.Kpad, int(self.fused), ctypes_void(self.xq.data_ptr()), st)
 
@@ -407,6 +414,9 @@ class EpropEngine:
             x_alpha = 0.0   # K4 = byte -> bf16 copy (the filter state is never needed)
         raw_x = (filt or self.reset) and not self.recurrent
         xl_ptr = None if raw_x else v(self.xl.data_ptr())
+        # one chunk: the pack writes the raw-spike GEMM operand itself (no K4 at all)
+        pack_xh = (filt and one and not self.fused and self.pack_xh
+                   and (bits or (self.k % 4 == 0 and x.data_ptr() % 4 == 0)))
 
         def timed(name, meta, fn, *args):
             if timers is None:
@@ -456,12 +466,12 @@ class EpropEngine:
                 if u + 1 < len(uses):
                     _copy(u + 1)
                 main.wait_event(self._sev_ready[u % 2])
-                self._pack(xs[u % 2].data_ptr(), Tc * kb, bits, ln, st)
+                self._pack(xs[u % 2].data_ptr(), Tc * kb, bits, ln, st, xh=pack_xh)
                 self._sev_free[u % 2].record(main)
                 state["u"] += 1
         else:
             def pack_chunk(c, ln):
-                self._pack(x.data_ptr() + c * Tc * kb, strideb, bits, ln, st)
+                self._pack(x.data_ptr() + c * Tc * kb, strideb, bits, ln, st, xh=pack_xh)
 
         if raster is not None and self.fused:
             raster.zero_()  # K21 ORs the spike bits into the words
@@ -471,6 +481,10 @@ class EpropEngine:
             ln = min(Tc, T - t0)
             pack_chunk(c, ln)
             side_x = one and use_side and not forward_only and not self.recurrent
+            if pack_xh:  # the pack wrote K5's raw operand: no K4 (pass B's wait is a no-op)
+                if use_side:
+                    self._ev["xbar"].record(main)
+                side_x = False
             if side_x and self.xbar_sched == "fa" and not self.fused:
                 self._project(ln, st, timed, binary)
             if side_x and self.xbar_sched != "main":
@@ -578,6 +592,8 @@ class EpropEngine:
                      v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()), v(self.xl.data_ptr()),
                      st)
                 self.launches += 2
+            elif pack_xh:
+                pass   # the pass-A pack wrote the raw-spike operand
             elif one and use_side and self.xbar_sched != "main":
                 main.wait_event(self._ev["xbar"])
             elif filt and not one:

@@ -110,10 +110,14 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     nch = (T + chunk - 1) // chunk
     assert names.count("spb_forward_chunk") == 2 * nch
     # a single chunk reuses pass A's packed spikes and current in pass B
-    assert names.count("spb_pack_spikes") == (2 * nch if nch > 1 else 1)
+    # one chunk: the pack also writes K5's raw-spike operand (spb_pack_spikes_xh, no K4)
+    packs = names.count("spb_pack_spikes") + names.count("spb_pack_spikes_xh")
+    assert packs == (2 * nch if nch > 1 else 1)
+    pack_xh = nch == 1 and 30 % 4 == 0          # byte rows must be 4-byte aligned (k = 30)
+    assert names.count("spb_pack_spikes_xh") == (1 if pack_xh else 0)
     assert names.count("spb_input_proj") == (2 * nch if nch > 1 else 1)
     assert names.count("spb_slice_weights") == 0
-    assert sum(names.count(x) for x in XB) == nch
+    assert sum(names.count(x) for x in XB) == (0 if pack_xh else nch)
     # K5 per chunk, plus the K = B GEMM of the carried filter state for chunks after the first
     assert names.count("spb_grad_gemm_partials") == nch + (nch - 1)
     carries = [c[1] for c in rec.calls if c[0] == "spb_alif_carry_chunk"]
@@ -132,9 +136,7 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     passb = sum(1 for c in rec.calls if c[0] == "spb_forward_chunk" and c[1][0] == 1)
     if nch == 1:  # pass A parks psi, pass B runs the scan only, input filter folded in
         assert [c[1][0] for c in rec.calls if c[0] == "spb_forward_chunk"] == [0, 3]
-        # the raw-spike operand: K4 with alpha = 0 writes hi only, K5 gets no B-lo
-        xb = [c[1] for c in rec.calls if c[0] in XB]
-        assert all(a[9] == 0.0 and a[12] is None for a in xb)
+        # the raw-spike operand: written by the pack, K5 gets no B-lo
         gm = [c[1] for c in rec.calls if c[0] == "spb_grad_gemm_partials"]
         assert all(a[4] is None for a in gm)
     assert eng.launches == len(rec.calls) + passb

@@ -106,6 +106,7 @@ def test_segmented_xbar_matches_sequential(kind, n, k, B, T, chunk, monkeypatch)
                                        precision="f32", seed=9))
     x, y = poisson_batch(B, k, T, 4, seed=2)
     out = {}
+    monkeypatch.setenv("SPB_PACK_XH", "0")   # keep K4 in the one-chunk case (it is tested here)
     for flag in ("1", "0"):
         monkeypatch.setenv("SPB_XBAR_SEG", flag)
         eng = EpropEngine(n, k, 4, B, alif=net.is_alif, chunk=chunk)
@@ -147,3 +148,31 @@ def test_raw_operand_multichunk_matches_xbar(kind, n, k, B, T, chunk, monkeypatc
         out[flag] = (eng.grad_w_acc.cpu().numpy().copy(), eng.loss.cpu().numpy().copy())
     assert np.array_equal(out["1"][1], out["0"][1])
     assert _rel(out["1"][0], out["0"][0]) < 1e-5
+
+
+@pytest.mark.parametrize("bits", [False, True])
+def test_pack_writes_raw_operand_bitwise(bits, monkeypatch):
+    """One chunk: the pack writing K5's raw-spike operand (spb_pack_spikes_xh) instead of
+    K4 -- the same bf16 rows, so the whole update is bitwise equal."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200.gradients import _neuron_kwargs
+    n, k, B, T = 256, 700, 6, 200
+    net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=n, n_inputs=k, n_classes=5,
+                                       precision="f32", seed=31))
+    x, y = poisson_batch(B, k, T, 5, seed=32)
+    xin = np.packbits(x, axis=-1, bitorder="little") if bits else x
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SPB_PACK_XH", flag)
+        eng = EpropEngine(n, k, 5, B, alif=True, chunk=255)
+        eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+        eng.run(torch.from_numpy(xin).cuda(), torch.from_numpy(y).cuda(), bits=bits,
+                **_neuron_kwargs(net))
+        torch.cuda.synchronize()
+        out[flag] = (eng.grad_w_acc.cpu().numpy().copy(), eng.xh.float().cpu().numpy().copy())
+    assert np.array_equal(out["1"][1], out["0"][1])
+    assert np.array_equal(out["1"][0], out["0"][0])
