@@ -58,8 +58,10 @@ constexpr int K1_THREADS = 128;  // 4 warps = 128 consecutive neurons of one sam
 // Templated on the per-launch flags so the per-step loop carries no flag branches and
 // walks its current / psi rows with pointer increments (the kernel is instruction-bound:
 // ~70 issued instructions per neuron-step before this specialisation).
+// (7 CTAs per SM, <= 73 registers: 2048 CTAs at C3 are two full waves; measured better
+// than 6 once K4 no longer shares the SMs: C3 K1 0.151 -> 0.147 ms)
 template <bool PASSA, bool PARK, bool RESET, bool SMOOTH>
-__global__ void __launch_bounds__(K1_THREADS, 6) forward_chunk_kernel(
+__global__ void __launch_bounds__(K1_THREADS, 7) forward_chunk_kernel(
     FwdParams P, const double* __restrict__ cur, double* __restrict__ u_st,
     double* __restrict__ a_st, double* __restrict__ zbar_st, double* __restrict__ zsum_st,
     uint32_t* __restrict__ raster, const float* __restrict__ wsig, float* __restrict__ psis) {
