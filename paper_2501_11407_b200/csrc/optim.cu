@@ -110,11 +110,13 @@ static int grid_for(long long total, int sm_count) {
 // CTA's own fresh writes, L1-hot) and emits the P digit planes, 4 inputs per thread so every
 // plane store is one 32-bit word.  do_sgd = 0 is plain slicing (spb_slice_weights).
 // ------------------------------------------------------------------------------------
-__device__ __forceinline__ void slice_one(double wv, int s, int P, int8_t (&q)[8]) {
+// scale46 = 2^(46-s) (P = 6): the product is exact, so w * scale46 == ldexp(w, 46 - s)
+__device__ __forceinline__ void slice_one(double wv, int s, int P, int8_t (&q)[8],
+                                          double scale46 = 0.0) {
   if (P == 6) {
     // balanced radix-256 digits of R = rint(w 2^(46-s)), |R| < 2^46, least significant
     // first: q = ((R + 128) mod 256) - 128 in [-128, 127], R <- (R - q) / 256 (exact)
-    long long R = (long long)rint(ldexp(wv, 46 - s));
+    long long R = __double2ll_rn(wv * scale46);
 #pragma unroll
     for (int p = 5; p >= 0; --p) {
       const long long d = ((R + 128) & 255) - 128;
@@ -165,6 +167,8 @@ __global__ void __launch_bounds__(SS_THREADS) sgd_slice_kernel(T* __restrict__ w
   int s = 0;
   if (mx > 0.0) frexp(mx, &s);  // mx = f * 2^s, f in [0.5, 1)  =>  |w| < 2^s
   if (tid == 0 && i < n) sexp[i] = s;
+  // 2^(46-s) (f32 weights: 46 - s in [-82, 195], a normal double)
+  const double sc46 = (P == 6) ? __longlong_as_double((long long)(46 - s + 1023) << 52) : 0.0;
   for (int j0 = 4 * tid; j0 < Kpad; j0 += 4 * SS_THREADS) {
     uint32_t word[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
@@ -172,7 +176,7 @@ __global__ void __launch_bounds__(SS_THREADS) sgd_slice_kernel(T* __restrict__ w
       const int j = j0 + e;
       const double wv = (i < n && j < k) ? (double)row[j] : 0.0;
       int8_t q[8];
-      slice_one(wv, s, P, q);
+      slice_one(wv, s, P, q, sc46);
       for (int p = 0; p < P; ++p) word[p] |= (uint32_t)(uint8_t)q[p] << (8 * e);
     }
     for (int p = 0; p < P; ++p)
