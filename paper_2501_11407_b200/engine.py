@@ -409,13 +409,15 @@ class EpropEngine:
         # Several chunks: the same on every chunk (scan pass 4 / 3), with the entry state
         # xbar_{t0-1} of each later chunk handled apart -- K4 writes it to xs_hi/lo, a
         # K = B GEMM adds Ct_0 (x) xbar_{t0-1} and K6 adds Wt_0 xbar_{t0-1} in its epilogue.
-        filt = (not self.reset and not self.recurrent and not forward_only and self.filt)
+        # (the recurrent extension: one chunk only -- its x~ operand is built in pass B)
+        filt = (not self.reset and (one or not self.recurrent) and not forward_only
+                and self.filt)
         if filt and one:
             x_alpha = 0.0   # K4 = byte -> bf16 copy (the filter state is never needed)
-        raw_x = (filt or self.reset) and not self.recurrent
+        raw_x = (filt or self.reset) and (filt or not self.recurrent)
         xl_ptr = None if raw_x else v(self.xl.data_ptr())
         # one chunk: the pack writes the raw-spike GEMM operand itself (no K4 at all)
-        pack_xh = (filt and one and not self.fused and self.pack_xh
+        pack_xh = (filt and one and not self.fused and not self.recurrent and self.pack_xh
                    and (bits or (self.k % 4 == 0 and x.data_ptr() % 4 == 0)))
 
         def timed(name, meta, fn, *args):
@@ -589,8 +591,7 @@ class EpropEngine:
                      v(self.xq2.data_ptr()), st)
                 call("spb_xbar_chunk_seg", v(self.xq2.data_ptr()), Tc * self.Kx2, self.Kx2, B,
                      self.kx, self.kp, KR, ln, int(c == 0 or self.reset), x_alpha,
-                     v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()), v(self.xl.data_ptr()),
-                     st)
+                     v(self.xbar_state.data_ptr()), v(self.xh.data_ptr()), xl_ptr, st)
                 self.launches += 2
             elif pack_xh:
                 pass   # the pass-A pack wrote the raw-spike operand

@@ -40,7 +40,7 @@ def _run(net, x, y, chunk, recurrent=True):
                       reset=net.neuron.reset, recurrent=recurrent)
     # the recurrent path keeps the filtered-input (xbar) GEMM operand; compare it with the
     # feed-forward engine on that same operand (the raw-spike fold sums in another order)
-    eng.filt = recurrent
+    eng.filt = False
     eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out),
                     w_rec=torch.from_numpy(net.neuron.w_rec) if recurrent else None)
     r = torch.zeros((B, T, (net.n + 31) // 32), dtype=torch.int32, device="cuda")
