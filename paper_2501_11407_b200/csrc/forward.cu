@@ -418,9 +418,16 @@ constexpr int K1S_THREADS = 128;  // 4 warps = 256 consecutive neurons of one sa
 // coefficients -- sum_rho C_rho xbar_{rho-1} = sum_rho Ct_rho x_{rho-1} (+ Ct_0 xbar_{-1}
 // = 0) with Ct_rho = C_rho + alpha Ct_{rho+1} -- so the gradient GEMM runs on the RAW
 // spikes, exact in bf16 (2 MMAs instead of 3, half the operand bytes, no filter kernel).
-// (7 CTAs per SM, <= 73 registers: the C3 grid of B x n/256 = 1024 CTAs is one wave)
+// (7 CTAs per SM, <= 73 registers: the C3 grid of B x n/256 = 1024 CTAs is one wave;
+// blocks of 8 rows -- 12 or 16 spill and measured slower: C3 0.7036 vs 0.715 / 0.733 ms)
+#ifndef SCAN_BLK
+#define SCAN_BLK 8
+#endif
+#ifndef SCAN_OCC
+#define SCAN_OCC 7
+#endif
 template <bool ALIF, bool CARRY, bool FILT = false>
-__global__ void __launch_bounds__(K1S_THREADS, 7) chunk_scan_kernel(
+__global__ void __launch_bounds__(K1S_THREADS, SCAN_OCC) chunk_scan_kernel(
     FwdParams P, const float* __restrict__ wsig, const float* __restrict__ ctab,
     uint32_t* __restrict__ c_hi, uint32_t* __restrict__ c_lo, uint32_t* __restrict__ w_hi,
     uint32_t* __restrict__ w_lo, int ldc, float2* __restrict__ mdt,
@@ -467,20 +474,20 @@ __global__ void __launch_bounds__(K1S_THREADS, 7) chunk_scan_kernel(
   float lam0 = 0.f, dcum0 = 1.f, an0 = 0.f, lam1 = 0.f, dcum1 = 1.f, an1 = 0.f;
   float ft0 = 0.f, ft1 = 0.f, fw0 = 0.f, fw1 = 0.f;  // FILT: running Ct, Wt
   const float falpha = (float)P.alpha;
-  // rows in blocks of 8: the next block's 8 psi loads are issued before this block is
-  // processed (8-16 rows in flight per thread, no register shifting)
-  float2 nxt[8];
+  // rows in blocks of SCAN_BLK: the next block's psi loads are issued before this block
+  // is processed (1-2 blocks in flight per thread, no register shifting)
+  float2 nxt[SCAN_BLK];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) nxt[u] = ldpsi(L - u);
+  for (int u = 0; u < SCAN_BLK; ++u) nxt[u] = ldpsi(L - u);
   float2 up = make_float2(0.f, 0.f);  // psi row r+1
-  for (int r8 = L; r8 >= 0; r8 -= 8) {
-    float2 blk[8];
+  for (int r8 = L; r8 >= 0; r8 -= SCAN_BLK) {
+    float2 blk[SCAN_BLK];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) blk[u] = nxt[u];
+    for (int u = 0; u < SCAN_BLK; ++u) blk[u] = nxt[u];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) nxt[u] = ldpsi(r8 - 8 - u);
+    for (int u = 0; u < SCAN_BLK; ++u) nxt[u] = ldpsi(r8 - SCAN_BLK - u);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < SCAN_BLK; ++u) {
     const int r = r8 - u;
     if (r < 0) break;
     const float2 cur = blk[u];  // psi row r = psi_{r-1}
