@@ -407,3 +407,28 @@ def test_bit_packed_inputs_match_byte_inputs(k, T):
         outs.append((eng.grad_w(torch.float64).cpu().numpy(), eng.loss.cpu().numpy()))
     for o in outs[1:]:
         assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
+
+
+@pytest.mark.parametrize("bits", [False, True])
+def test_one_chunk_streamed_inputs_match_resident(bits):
+    """One chunk (the pack also writes K5's raw operand) from pinned host memory, bytes and
+    bit-packed: bitwise the resident-input update."""
+    _need_gpu()
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200.gradients import _neuron_kwargs
+    net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=256, n_inputs=700, n_classes=20,
+                                       precision="f32", seed=2))
+    B = 12
+    x, y = poisson_batch(B, 700, 100, 20, seed=7)
+    xin = np.packbits(x, axis=-1, bitorder="little") if bits else x
+    yd = torch.from_numpy(y).cuda()
+    outs = []
+    for dev_in in (torch.from_numpy(xin).cuda(), torch.from_numpy(xin).pin_memory()):
+        eng = EpropEngine(256, 700, 20, B, alif=True, chunk=127)
+        eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+        eng.run(dev_in, yd, bits=bits, **_neuron_kwargs(net))
+        torch.cuda.synchronize()
+        outs.append((eng.grad_w_acc.cpu().numpy().copy(), eng.loss.cpu().numpy().copy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
