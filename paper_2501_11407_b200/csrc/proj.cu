@@ -502,6 +502,9 @@ __device__ __forceinline__ uint32_t expand4(uint32_t nib) {  // 4 bits -> 4 byte
 // Byte-count rows with k, the row stride and x 4-byte aligned (the common case): CTA per 4
 // rows, thread per 4 output bytes of each -- each warp moves 128 contiguous bytes in and
 // out per row (coalesced u32), the 4 rows' loads in flight together.
+#ifndef PACK_GRID
+#define PACK_GRID (148 * 16)  // grid-stride pack: C3 0.7038 -> 0.6996 ms (148 * 4: 0.701)
+#endif
 constexpr int PACK_R = 4;  // byte-input pack: rows per CTA (2: 0.7136, 4: 0.7106, 8: 0.7125 ms at C3)
 
 // bf16 of four spike counts (0..255, exact): the upper halves of their fp32 encodings
@@ -524,31 +527,33 @@ __global__ void __launch_bounds__(256) pack_bytes4_kernel(const uint8_t* __restr
                                                           int KR = 0) {
   const int wpr = Kpad >> 2;  // output words per row
   const int rows = B * Tc;
-  constexpr int R = PACK_R;   // rows per CTA, their loads issued together
-  const int row0 = blockIdx.x * R;
-  for (int w = threadIdx.x; w < wpr; w += blockDim.x) {
-    uint32_t v[R];
+  constexpr int R = PACK_R;   // rows per iteration, their loads issued together
+  // grid-stride over row groups (a persistent-size grid instead of one tiny CTA per group)
+  for (int row0 = blockIdx.x * R; row0 < rows; row0 += gridDim.x * R) {
+    int sq[R], bq[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const int row = row0 + q;
-      const int s = tmajor ? row / B : row % Tc;
-      const int b = tmajor ? row % B : row / Tc;
-      v[q] = (row < rows && s < len && 4 * w < k)
-                 ? __ldg(reinterpret_cast<const uint32_t*>(x + (long long)b * stride_b +
-                                                           (long long)s * k) + w)
-                 : 0u;
+      sq[q] = tmajor ? row / B : row % Tc;
+      bq[q] = tmajor ? row % B : row / Tc;
     }
+    for (int w = threadIdx.x; w < wpr; w += blockDim.x) {
+      uint32_t v[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q)
-      if (row0 + q < rows) reinterpret_cast<uint32_t*>(xq + (long long)(row0 + q) * Kpad)[w] = v[q];
-    if (xh != nullptr) {
+      for (int q = 0; q < R; ++q)
+        v[q] = (row0 + q < rows && sq[q] < len && 4 * w < k)
+                   ? __ldg(reinterpret_cast<const uint32_t*>(x + (long long)bq[q] * stride_b +
+                                                             (long long)sq[q] * k) + w)
+                   : 0u;
 #pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int row = row0 + q;
-        if (row < rows) {
-          const int s = row % Tc, b = row / Tc;
-          xh[((long long)b * KR + s + 1) * (Kpad >> 2) + w] = bf16x4_of_bytes(v[q]);
-        }
+      for (int q = 0; q < R; ++q)
+        if (row0 + q < rows)
+          reinterpret_cast<uint32_t*>(xq + (long long)(row0 + q) * Kpad)[w] = v[q];
+      if (xh != nullptr) {
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+          if (row0 + q < rows)
+            xh[((long long)bq[q] * KR + sq[q] + 1) * (Kpad >> 2) + w] = bf16x4_of_bytes(v[q]);
       }
     }
   }
@@ -666,7 +671,7 @@ int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits
   const long long want = (rows + 7) / 8;
   const int blocks = (int)(want < 148LL * 16 ? want : 148LL * 16);
   if (!bits && (k & 3) == 0 && (stride_b & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0) {
-    const int b4 = (int)((rows + proj::PACK_R - 1) / proj::PACK_R);
+    const int b4 = (int)std::min<long long>((rows + proj::PACK_R - 1) / proj::PACK_R, PACK_GRID);
     const int t4 = std::min(256, ((Kpad / 4 + 31) / 32) * 32);
     proj::pack_bytes4_kernel<<<b4, t4, 0, stream>>>(x, stride_b, k, len, Tc, Kpad, B, time_major,
                                                      xq);
@@ -705,7 +710,7 @@ int spb_pack_spikes_xh(const uint8_t* x, long long stride_b, int B, int k, int b
   SPB_CHECK_ARG((k & 3) == 0 && (stride_b & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0,
                 "spb_pack_spikes_xh: byte rows must be 4-byte aligned");
   const int t4 = std::min(256, ((Kpad / 4 + 31) / 32) * 32);
-  proj::pack_bytes4_kernel<<<(int)((rows + proj::PACK_R - 1) / proj::PACK_R), t4, 0, stream>>>(
+  proj::pack_bytes4_kernel<<<(int)std::min<long long>((rows + proj::PACK_R - 1) / proj::PACK_R, PACK_GRID), t4, 0, stream>>>(
       x, stride_b, k, len, Tc, Kpad, B, 0, xq, static_cast<uint2*>(xh), KR);
   SPB_CHECK_LAUNCH("pack_bytes4_xh");
   return 0;
