@@ -571,40 +571,45 @@ __global__ void __launch_bounds__(128) pack_bits8_kernel(const uint8_t* __restri
   const int wpr = Kpad >> 3;     // output 8-byte words per row
   const int rows = B * Tc;
   constexpr int R = 4;
-  const int row0 = blockIdx.x * R;
-  for (int w = threadIdx.x; w < wpr; w += blockDim.x) {
-    uint32_t v[R];
+  // grid-stride over row groups (as pack_bytes4_kernel)
+  for (int row0 = blockIdx.x * R; row0 < rows; row0 += gridDim.x * R) {
+    int sq[R], bq[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const int row = row0 + q;
-      const int s = tmajor ? row / B : row % Tc;
-      const int b = tmajor ? row % B : row / Tc;
-      uint32_t byte = 0u;
-      if (row < rows && s < len && w < kb) {
-        byte = __ldg(x + (long long)b * stride_b + (long long)s * kb + w);
-        const int left = k - 8 * w;  // valid channels in this byte
-        if (left < 8) byte &= (1u << left) - 1u;
-      }
-      v[q] = byte;
+      sq[q] = tmajor ? row / B : row % Tc;
+      bq[q] = tmajor ? row % B : row / Tc;
     }
-#pragma unroll
-    for (int q = 0; q < R; ++q)
-      if (row0 + q < rows)
-        reinterpret_cast<uint2*>(xq + (long long)(row0 + q) * Kpad)[w] =
-            make_uint2(expand4(v[q] & 0xfu), expand4(v[q] >> 4));
-    if (xh != nullptr) {
+    for (int w = threadIdx.x; w < wpr; w += blockDim.x) {
+      uint32_t v[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        const int row = row0 + q;
-        if (row < rows) {
-          const int s = row % Tc, b = row / Tc;
-          // 8 spikes -> 8 bf16 (0x3F80 = 1.0)
-          uint32_t o[4];
+        uint32_t byte = 0u;
+        if (row0 + q < rows && sq[q] < len && w < kb) {
+          byte = __ldg(x + (long long)bq[q] * stride_b + (long long)sq[q] * kb + w);
+          const int left = k - 8 * w;  // valid channels in this byte
+          if (left < 8) byte &= (1u << left) - 1u;
+        }
+        v[q] = byte;
+      }
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            o[e] = (((v[q] >> (2 * e)) & 1u) ? 0x3F80u : 0u) |
-                   (((v[q] >> (2 * e + 1)) & 1u) ? 0x3F800000u : 0u);
-          xh[((long long)b * KR + s + 1) * (Kpad >> 3) + w] = make_uint4(o[0], o[1], o[2], o[3]);
+      for (int q = 0; q < R; ++q)
+        if (row0 + q < rows)
+          reinterpret_cast<uint2*>(xq + (long long)(row0 + q) * Kpad)[w] =
+              make_uint2(expand4(v[q] & 0xfu), expand4(v[q] >> 4));
+      if (xh != nullptr) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          if (row0 + q < rows) {
+            // 8 spikes -> 8 bf16 (0x3F80 = 1.0)
+            uint32_t o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              o[e] = (((v[q] >> (2 * e)) & 1u) ? 0x3F80u : 0u) |
+                     (((v[q] >> (2 * e + 1)) & 1u) ? 0x3F800000u : 0u);
+            xh[((long long)bq[q] * KR + sq[q] + 1) * (Kpad >> 3) + w] =
+                make_uint4(o[0], o[1], o[2], o[3]);
+          }
         }
       }
     }
@@ -679,7 +684,7 @@ int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits
     return 0;
   }
   if (bits) {
-    const int b8 = (int)((rows + 3) / 4);
+    const int b8 = (int)std::min<long long>((rows + 3) / 4, PACK_GRID);
     const int t8 = std::min(128, ((Kpad / 8 + 31) / 32) * 32);
     proj::pack_bits8_kernel<<<b8, t8, 0, stream>>>(x, stride_b, k, len, Tc, Kpad, B, time_major,
                                                     xq);
@@ -702,7 +707,7 @@ int spb_pack_spikes_xh(const uint8_t* x, long long stride_b, int B, int k, int b
   const long long rows = (long long)B * Tc;
   if (bits) {
     const int t8 = std::min(128, ((Kpad / 8 + 31) / 32) * 32);
-    proj::pack_bits8_kernel<<<(int)((rows + 3) / 4), t8, 0, stream>>>(
+    proj::pack_bits8_kernel<<<(int)std::min<long long>((rows + 3) / 4, PACK_GRID), t8, 0, stream>>>(
         x, stride_b, k, len, Tc, Kpad, B, 0, xq, static_cast<uint4*>(xh), KR);
     SPB_CHECK_LAUNCH("pack_bits8_xh");
     return 0;
