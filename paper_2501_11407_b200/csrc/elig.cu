@@ -43,7 +43,13 @@ constexpr int SMEM = ETILE + STAGES * STAGE + 1024 + 256;
 // raw-spike operand (RAW): no xbar-lo tiles, 2 MMAs per K step, 6 stages of 3 tiles
 constexpr int STAGES_R = 6;
 constexpr int STAGE_R = 3 * TILE;
-constexpr int SMEM_R = ETILE + STAGES_R * STAGE_R + 1024 + 256;
+// RAW: the 2-MMA operand stages are 24 KB, so two eps tiles fit beside 4 of them
+#ifndef K6_RAW_EB
+#define K6_RAW_EB 2
+#endif
+constexpr int EB_R = K6_RAW_EB;
+constexpr int STAGES_RB = (EB_R == 2) ? 4 : STAGES_R;
+constexpr int SMEM_R = EB_R * ETILE + STAGES_RB * STAGE_R + 1024 + 256;
 // A = W, B = xbar, both MN-major (neurons / channels contiguous, written by K1s / K4)
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -108,21 +114,22 @@ __global__ void __launch_bounds__(THREADS, 1)
                       const __nv_bfloat16* __restrict__ wl_g, int ldw,
                       const __nv_bfloat16* __restrict__ xs_hi,
                       const __nv_bfloat16* __restrict__ xs_lo) {
-  constexpr int NST = RAW ? STAGES_R : STAGES;
+  constexpr int NST = RAW ? STAGES_RB : STAGES;
+  constexpr int EB = RAW ? EB_R : 1;   // eps tile buffers
   constexpr int SB = RAW ? STAGE_R : STAGE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* esm = smem;                             // [4 boxes][128 rows][128 B]
-  uint8_t* osm = smem + ETILE;                     // [NST][4 or 3][TILE]
+  uint8_t* esm = smem;                             // [EB][4 boxes][128 rows][128 B]
+  uint8_t* osm = smem + EB * ETILE;                // [NST][4 or 3][TILE]
   uint64_t* bars = reinterpret_cast<uint64_t*>(osm + NST * SB);
   uint64_t* full = bars;
   uint64_t* empty = bars + NST;
   uint64_t* tfull = bars + 2 * NST;
   uint64_t* tempty = bars + 2 * NST + 2;
-  uint64_t* efull = bars + 2 * NST + 4;
-  uint64_t* eempty = bars + 2 * NST + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 6);
+  uint64_t* efull = bars + 2 * NST + 4;            // [EB]
+  uint64_t* eempty = bars + 2 * NST + 4 + EB;      // [EB]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 4 + 2 * EB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
@@ -139,8 +146,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(smem_u32(&tfull[a]), 1);
       mbar_init(smem_u32(&tempty[a]), EPI_WARPS);
     }
-    mbar_init(smem_u32(efull), 1);
-    mbar_init(smem_u32(eempty), 1);  // the epilogue's storing thread, once per sample
+    for (int e = 0; e < EB; ++e) {
+      mbar_init(smem_u32(&efull[e]), 1);
+      mbar_init(smem_u32(&eempty[e]), 1);  // the epilogue's storing thread, once per use
+    }
     mbar_fence_init();
     if (do_mma) {
       tma_prefetch_desc(&tm_wh);
@@ -193,12 +202,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 2) {
     if (lane == 0 && load_eps) {  // each sample's eps~ tile E0, 4 boxes of 32 columns
       for (int lb = 0; lb < nb; ++lb) {
-        mbar_wait(smem_u32(eempty), (lb & 1) ^ 1);
-        const uint32_t fb = smem_u32(efull);
+        const int eb = lb % EB, eu = lb / EB;   // buffer, its use count
+        mbar_wait(smem_u32(&eempty[eb]), (eu & 1) ^ 1);
+        const uint32_t fb = smem_u32(&efull[eb]);
         mbar_expect_tx(fb, ETILE);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          tma_load_2d(smem_u32(esm + q * (ETILE / 4)), &tm_eps, fb, j0 + 32 * q,
+          tma_load_2d(smem_u32(esm + eb * ETILE + q * (ETILE / 4)), &tm_eps, fb, j0 + 32 * q,
                       (b0 + lb) * n_pad + i0);
       }
     }
@@ -251,9 +261,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const long long o = (long long)b * KR * ldw + i;
         w0e = __bfloat162float(wh_g[o]) + __bfloat162float(wl_g[o]);
       }
-      const uint32_t erow = smem_u32(esm + cg * (ETILE / 4) + r * 128);
-      if (load_eps) mbar_wait(smem_u32(efull), lb & 1);
-      else if (store_eps && lb > 0) mbar_wait(smem_u32(eempty), (lb - 1) & 1);  // tile reusable
+      const int eb = lb % EB, eu = lb / EB;
+      const uint32_t erow = smem_u32(esm + eb * ETILE + cg * (ETILE / 4) + r * 128);
+      if (load_eps) mbar_wait(smem_u32(&efull[eb]), eu & 1);
+      else if (store_eps && eu > 0) mbar_wait(smem_u32(&eempty[eb]), (eu - 1) & 1);  // reusable
       if (do_mma) {
         mbar_wait(smem_u32(&tfull[a]), (lb >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -314,12 +325,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (store_eps) {
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4)
-              tma_store_2d(&tm_eps, smem_u32(esm + q4 * (ETILE / 4)), j0 + 32 * q4,
+              tma_store_2d(&tm_eps, smem_u32(esm + eb * ETILE + q4 * (ETILE / 4)), j0 + 32 * q4,
                            b * n_pad + i0);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           }
-          arrive(smem_u32(eempty));
+          arrive(smem_u32(&eempty[eb]));
         }
       }
     }
