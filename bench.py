@@ -196,6 +196,9 @@ def main():
                     help="split the batch over this many concurrently streamed engines")
     ap.add_argument("--mb-sms", type=int, default=0,
                     help="SMs the persistent kernels of each micro-batch may occupy (0 = all)")
+    ap.add_argument("--park-gb", type=float, default=0.0,
+                    help="opt-in: park every chunk's psi in pass A when it fits this many GB "
+                         "(pass B skips the projection and dynamics; memory then grows with T)")
     ap.add_argument("--no-e2e-graph", dest="e2e_graph", action="store_false",
                     help="eager launches in the e2e loop (default: each step replays the "
                          "update's CUDA graph; measured 77-79 -> 79-81 M at C3)")
@@ -251,6 +254,9 @@ def main():
                           device=dev, recurrent=args.recurrent)
     eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out),
                     w_rec=torch.from_numpy(net.neuron.w_rec) if args.recurrent else None)
+    if args.park_gb > 0:
+        for e in getattr(eng, "engines", [eng]):
+            e.park_budget = int(args.park_gb * (1 << 30))
     xd = torch.from_numpy(x_np).to(dev)
     yd = torch.from_numpy(y_np).to(dev)
     packer = GradPacker(n, k, m, dev)  # (recurrent: grad W_rec stays in the accumulator)
@@ -563,6 +569,7 @@ def main():
                        "forward_precision": "fp64 state/current (bit-exact spikes)",
                        "forward_kernel": "K21 fused projection+dynamics" if eng.fused else "K2 projection + K1 dynamics",
                        "step": "e-prop gradient (+ allreduce when N > 1) + fused SGD on W/W_out + W re-slice",
+                       "psi_parking_gb": args.park_gb,
                        "l2": "512 MiB flush between timed steps (outside events)",
                        "launch": "CUDA graph replay of the whole update" if graph is not None
                                  else "eager launches"},

@@ -190,6 +190,11 @@ class EpropEngine:
         # fold the input filter into the one-chunk coefficients (SPB_FILT=0: xbar operand)
         self.filt = os.environ.get("SPB_FILT", "1") != "0"
         self.pack_xh = os.environ.get("SPB_PACK_XH", "1") != "0"
+        # opt-in memory-for-time trade (off by default: memory then grows with T): park the
+        # psi of every chunk in pass A when all of it fits `park_budget` bytes, so pass B
+        # skips the projection and the dynamics recompute.  SPB_PARK_GB sets it too.
+        self.park_budget = int(float(os.environ.get("SPB_PARK_GB", "0")) * (1 << 30))
+        self.psi_park = None
         self.kf_sync = torch.zeros(1 + 2 * B, dtype=torch.int32, device=dev)
         self.kf_part = torch.empty(B * ((n + 127) // 128) * m, dtype=f64, device=dev)
         self.ldc = _round_up(n, 8)   # C/W are MN-major [K][ldc] (neurons contiguous)
@@ -390,6 +395,16 @@ class EpropEngine:
         ctab = self._gains(T, float(kappa))
         nchunks = (T + Tc - 1) // Tc
         one = nchunks == 1
+        slab = B * (self.KR + 1) * n
+        park = (not one and not forward_only and not self.fused and not self.recurrent
+                and self.park_budget > 0 and 4 * slab * nchunks <= self.park_budget
+                and self.device.type == "cuda")
+        if park and (self.psi_park is None or self.psi_park.shape[0] < nchunks):
+            self.psi_park = torch.empty((nchunks, B, self.KR + 1, n), dtype=torch.float32,
+                                        device=self.device)
+
+        def psi_ptr(c):
+            return v(self.psi_park[c].data_ptr()) if park else v(self.psi.data_ptr())
         # K1f: pass A + readout + scan of a one-chunk sequence in one kernel
         kf = (one and self.k1f and self.filt and not forward_only and not self.fused
               and not self.recurrent and not self.reset and self.device.type == "cuda")
@@ -530,7 +545,7 @@ class EpropEngine:
                   v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
                   v(raster.data_ptr()) if raster is not None else None,
                   None, None, None, None, None, None, None, None, 0, None,
-                  v(self.psi.data_ptr()) if (one and not forward_only) else None, st)
+                  psi_ptr(c) if (park or (one and not forward_only)) else None, st)
             self.launches += 3
         # ---------------- readout / loss (inside K1f when it ran) ----------------
         if not kf:
@@ -556,7 +571,10 @@ class EpropEngine:
             ln = min(Tc, T - t0)
             last = c == nchunks - 1
             carry_out = bool(self.ntr) and not last   # only a later chunk needs the trace
-            if not one:  # one chunk: xq and cur of pass A are still valid (same W, same x)
+            if park:     # psi of this chunk was parked in pass A: spikes (for K4) only
+                pack_chunk(c, ln)
+                self.launches += 1
+            elif not one:  # one chunk: xq and cur of pass A are still valid (same W, same x)
                 pack_chunk(c, ln)
                 if self.fused:
                     self._fused(1, ln, t0, T, common, None, self.psi, st, timed,
@@ -569,7 +587,7 @@ class EpropEngine:
                         self.launches += 1
                 self.launches += 2
             # one chunk (pass A parked psi) or K21 / K1rec (park psi themselves): scan only
-            pid = 2 if (one or self.fused or self.recurrent) else 1
+            pid = 2 if (one or park or self.fused or self.recurrent) else 1
             if filt:
                 pid = 3 if pid == 2 else 4
             if not kf:
@@ -582,7 +600,7 @@ class EpropEngine:
                       v(self.w_lo.data_ptr()) if carry_out else None,
                       v(self.wa_hi.data_ptr()) if carry_out and self.ntr == 2 else None,
                       v(self.wa_lo.data_ptr()) if carry_out and self.ntr == 2 else None, self.ldc,
-                      v(self.mdt.data_ptr()) if self.ntr else None, v(self.psi.data_ptr()), st)
+                      v(self.mdt.data_ptr()) if self.ntr else None, psi_ptr(c), st)
                 self.launches += 1 if pid >= 2 else 2
             if self.recurrent:
                 # x~ = [x_t, z_{t-1}] bytes, then the usual filter over kx columns

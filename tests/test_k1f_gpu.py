@@ -176,3 +176,31 @@ def test_pack_writes_raw_operand_bitwise(bits, monkeypatch):
         out[flag] = (eng.grad_w_acc.cpu().numpy().copy(), eng.xh.float().cpu().numpy().copy())
     assert np.array_equal(out["1"][1], out["0"][1])
     assert np.array_equal(out["1"][0], out["0"][0])
+
+
+@pytest.mark.parametrize("kind,T,chunk", [("alif", 300, 63), ("lif", 400, 127)])
+def test_parked_psi_is_bitwise_the_recompute(kind, T, chunk):
+    """Opt-in psi parking (park_budget): pass B reads the psi pass A parked instead of
+    re-running the projection and the dynamics -- the same psi, so bitwise the same update."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200.gradients import _neuron_kwargs
+    n, k, B = 200, 96, 6
+    net = P.init_network(P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=4,
+                                       precision="f32", seed=41))
+    x, y = poisson_batch(B, k, T, 4, seed=42)
+    out = {}
+    for budget in (0, 1 << 30):
+        eng = EpropEngine(n, k, 4, B, alif=net.is_alif, chunk=chunk)
+        eng.park_budget = budget
+        eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+        eng.run(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), **_neuron_kwargs(net))
+        torch.cuda.synchronize()
+        assert (eng.psi_park is not None) == (budget > 0)
+        out[budget] = (eng.grad_w_acc.cpu().numpy().copy(), eng.loss.cpu().numpy().copy(),
+                       eng.grad_wout.cpu().numpy().copy())
+    for a, b in zip(out[0], out[1 << 30]):
+        assert np.array_equal(a, b)
