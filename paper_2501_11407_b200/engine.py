@@ -6,7 +6,7 @@ hidden n, inputs k, classes m, chunk length Tc) and replays the update
     weights   K2s  slice W into exact INT8 digits (once per update)
     pass A    per chunk: pack x -> K2 INT8 tcgen05 current I = W x_t -> K1 dynamics(A)
     readout   K3 loss / g / w_sig ; K7 grad W_out
-    pass B    per chunk: pack -> K2 -> K1 dynamics(B) + backward chunk scan -> K4 xbar
+    pass B    per chunk: pack -> K2 -> K1 dynamics(B) + backward chunk scan -> K4 operand
                          -> K5 tcgen05 chunk-gradient GEMM   (all intra-chunk terms)
                          -> K6 tcgen05 ALIF trace carry      (inter-chunk terms, ALIF)
                          -> fixed-order reduction of the split partials
@@ -15,9 +15,12 @@ which is the reference's per-sample online loop (gradients.py:157-176) restated 
 batch: the learning signal L_t = c_t W_out^T (softmax - onehot) is only known after the
 whole sequence (gradients.py:177-182), so pass B recomputes the (deterministic) forward
 with L_t known (two-pass form), and the per-synapse ALIF trace is
-carried chunk to chunk (forward.cu / elig.cu headers give the algebra).  Memory is
-independent of T: state is per (sample, neuron[, input]) and chunk buffers are sized by
-Tc.
+carried chunk to chunk (forward.cu / elig.cu headers give the algebra).  With reset=False
+the presynaptic filter is folded into the scan's coefficients, so K5 / K6 run on the raw
+spikes (2 MMAs); a one-chunk sequence reuses pass A's current and parked psi (pass B =
+scan + K5), and its pack also writes K5's operand.  Memory is independent of T: state is
+per (sample, neuron[, input]) and chunk buffers are sized by Tc (opt-in `park_budget`
+trades that for skipping pass B's recompute).
 
 All work is enqueued on torch's current CUDA stream through the C-ABI (``_lib``); the
 engine never synchronises.  PyTorch provides allocation and streams only.
@@ -245,9 +248,11 @@ class EpropEngine:
         self._ctab_T = None
         self.ctab = None
         self.launches = 0
-        # where K4 (xbar of a one-chunk sequence) runs: "fa" (default, measured best: C4
-        # 1.66 -> 1.59 ms) = side stream after K2, overlapping K1; "proj" = side stream from
-        # the start of pass A, overlapping K2; "main" = serially before K5
+        # where K4 of a one-chunk sequence runs when the pack does not write K5's operand
+        # itself (SPB_PACK_XH=0, unaligned byte rows, fused / recurrent engines): "fa"
+        # (default, measured best: C4 1.66 -> 1.59 ms) = side stream after K2, overlapping
+        # K1; "proj" = side stream from the start of pass A, overlapping K2; "main" =
+        # serially before K5
         self.xbar_sched = os.environ.get("SPB_XBAR_SCHED", "fa")
         # side stream for work off the critical path (K4 xbar of a one-chunk sequence, K7)
         if self.device.type == "cuda":
