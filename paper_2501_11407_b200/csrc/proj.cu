@@ -138,6 +138,35 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se
                                                    int i0, uint32_t tempty_bar, int lane,
                                                    int probe = 0) {
   long long g0[NH], g1[NH];
+  if constexpr (P == 6 && BIN && sizeof(SE) == sizeof(double)) {
+    // binary spikes, k <= 768: every digit sum |S_p| <= 768*128 < 2^17, so digit PAIRS
+    // combine in int32 (|S_a 256 + S_b| < 2^26) and g = P01 2^32 + P23 2^16 + P45 needs
+    // only two 64-bit adds -- the same integer as (g0 << 24) + g1, half the instructions
+    int32_t p01[NH], r2v[NH];
+    {
+      int32_t r[3][NH];
+#pragma unroll
+      for (int p = 0; p < 3; ++p) tmem_ld16_nowait(tbase + p * NT, r[p]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < NH; ++c) {
+        p01[c] = r[0][c] * 256 + r[1][c];
+        r2v[c] = r[2][c];
+      }
+    }
+    {
+      int32_t r[3][NH];
+#pragma unroll
+      for (int p = 3; p < 6; ++p) tmem_ld16_nowait(tbase + p * NT, r[p - 3]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < NH; ++c) {
+        const int32_t p23 = r2v[c] * 256 + r[0][c], p45 = r[1][c] * 256 + r[2][c];
+        g0[c] = ((long long)p01[c] << 32) + ((long long)p23 << 16) + (long long)p45;
+        g1[c] = 0;
+      }
+    }
+  } else {
   {
     int32_t r[3][NH];
 #pragma unroll
@@ -159,6 +188,7 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se
       g1[c] = v;
     }
   }
+  }
   // the TMEM buffer is free once every epilogue warp has pulled its lanes
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncwarp();
@@ -170,7 +200,9 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se
     double v[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      if constexpr (sizeof(SE) == sizeof(double))
+      if constexpr (P == 6 && BIN && sizeof(SE) == sizeof(double))
+        v[h] = (double)g0[c + h] * se[c + h];   // g0 holds the whole integer g
+      else if constexpr (sizeof(SE) == sizeof(double))
         v[h] = digits_current_scaled<P, BIN>(g0[c + h], g1[c + h], se[c + h]);
       else
         v[h] = digits_current<P, BIN>(g0[c + h], g1[c + h], se[c + h]);
