@@ -213,6 +213,43 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se
     if (ch[0].x == 1.2345e-300 && row < M) out[(long long)row * n + i0] = ch[0].y;
     return;
   }
+  if ((n & 3) == 0) {
+    // 4x4 transpose of 32-byte quads (4 neurons) inside each group of 4 lanes (2 xor-
+    // butterfly stages): lane p of the group then holds quad p of the group's 4 rows and
+    // each 256-bit store instruction writes 8 rows x 128 contiguous bytes (full lines) --
+    // two thirds of the shuffles and half the store instructions of the 8x8 scheme below.
+    const int p4 = lane & 3;
+#pragma unroll
+    for (int sh = 2; sh >= 1; sh >>= 1) {
+      const bool up = (p4 & sh) != 0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        if (m & sh) continue;
+        const int ms = m | sh;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double2 send = up ? ch[2 * m + e] : ch[2 * ms + e];
+          double2 recv;
+          recv.x = __shfl_xor_sync(0xffffffffu, send.x, sh);
+          recv.y = __shfl_xor_sync(0xffffffffu, send.y, sh);
+          if (up) ch[2 * m + e] = recv; else ch[2 * ms + e] = recv;
+        }
+      }
+    }
+    const int row0 = row - p4;
+    const int col = i0 + 4 * p4;
+#pragma unroll
+    for (int kq = 0; kq < 4; ++kq) {
+      const int r = row0 + kq;
+      if (r < M && col < n) {  // n % 4 == 0: a quad is all in or all out
+        double* o = out + (long long)r * n + col;
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o), "d"(ch[2 * kq].x),
+                     "d"(ch[2 * kq].y), "d"(ch[2 * kq + 1].x), "d"(ch[2 * kq + 1].y)
+                     : "memory");
+      }
+    }
+    return;
+  }
   // 8x8 transpose of 16-byte chunks inside each group of 8 lanes (3 xor-butterfly
   // stages): afterwards lane p of the group holds chunk p of the group's 8 rows, so each
   // store instruction writes 4 rows x 128 contiguous bytes (full lines) instead of 32
