@@ -177,6 +177,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     float* prow = partial + (long long)blockIdx.z * slice_stride + (long long)row * ldp;
+    // the slice holds every row of the tile grid (n_pad rows) and 32-byte aligned rows:
+    // coalesced transposed stores are allowed
+    const bool rows_padded = slice_stride >= (long long)gridDim.y * BM * ldp && (ldp % 8) == 0;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
       uint32_t r[32];
@@ -192,16 +195,54 @@ __global__ void __launch_bounds__(THREADS, 1)
             "=r"(r[31])
           : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < M) {
+      if (!have_work) {
+#pragma unroll
+        for (int v = 0; v < 32; ++v) r[v] = 0u;
+      }
+      if (rows_padded) {
+        // 4x4 transpose of 32-byte chunks (8 columns) inside each group of 4 lanes, then
+        // 256-bit stores: each instruction writes 8 rows x 128 contiguous bytes instead of
+        // 32 rows x 16 bytes (rows past M are padding rows of the partial slice)
+        const int p4 = lane & 3;
+#pragma unroll
+        for (int sh = 2; sh >= 1; sh >>= 1) {
+          const bool up = (p4 & sh) != 0;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            if (m & sh) continue;
+            const int ms = m | sh;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const uint32_t send = up ? r[8 * m + e] : r[8 * ms + e];
+              const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, sh);
+              if (up) r[8 * m + e] = recv; else r[8 * ms + e] = recv;
+            }
+          }
+        }
+        const int col = n0 + c0 + 8 * p4;
+        float* base = partial + (long long)blockIdx.z * slice_stride +
+                      (long long)(m0 + q * 32 + (lane & ~3)) * ldp + col;
+#pragma unroll
+        for (int kq = 0; kq < 4; ++kq) {
+          if (col < ldp) {
+            float* o = base + (long long)kq * ldp;
+            asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(o),
+                         "r"(r[8 * kq + 0]), "r"(r[8 * kq + 1]), "r"(r[8 * kq + 2]),
+                         "r"(r[8 * kq + 3]), "r"(r[8 * kq + 4]), "r"(r[8 * kq + 5]),
+                         "r"(r[8 * kq + 6]), "r"(r[8 * kq + 7])
+                         : "memory");
+          }
+        }
+      } else if (row < M) {
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
           const int col = n0 + c0 + v * 4;
           if (col < ldp) {
             float4 o;
-            o.x = have_work ? __uint_as_float(r[v * 4 + 0]) : 0.f;
-            o.y = have_work ? __uint_as_float(r[v * 4 + 1]) : 0.f;
-            o.z = have_work ? __uint_as_float(r[v * 4 + 2]) : 0.f;
-            o.w = have_work ? __uint_as_float(r[v * 4 + 3]) : 0.f;
+            o.x = __uint_as_float(r[v * 4 + 0]);
+            o.y = __uint_as_float(r[v * 4 + 1]);
+            o.z = __uint_as_float(r[v * 4 + 2]);
+            o.w = __uint_as_float(r[v * 4 + 3]);
             *reinterpret_cast<float4*>(prow + col) = o;
           }
         }
