@@ -336,13 +336,35 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if (store_eps && warp == EPI0 && lane == 0)
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // E_end written
-    if (vi) {
-      float* prow = partial + ((long long)blockIdx.z * n_pad + i) * kp + c0;
+    {
+      // grad tile through a 4x4 lane transpose of 32-byte chunks and 256-bit stores: each
+      // instruction writes 8 rows x 128 contiguous bytes (rows past n are zero padding)
+      const int p4 = lane & 3;
 #pragma unroll
-      for (int v4 = 0; v4 < 8; ++v4)
-        if (c0 + v4 * 4 < kp)
-          *reinterpret_cast<float4*>(prow + v4 * 4) =
-              make_float4(g[v4 * 4], g[v4 * 4 + 1], g[v4 * 4 + 2], g[v4 * 4 + 3]);
+      for (int sh = 2; sh >= 1; sh >>= 1) {
+        const bool up = (p4 & sh) != 0;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          if (m & sh) continue;
+          const int ms = m | sh;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float send = up ? g[8 * m + e] : g[8 * ms + e];
+            const float recv = __shfl_xor_sync(0xffffffffu, send, sh);
+            if (up) g[8 * m + e] = recv; else g[8 * ms + e] = recv;
+          }
+        }
+      }
+      float* base = partial + ((long long)blockIdx.z * n_pad + i0 + q * 32 + (lane & ~3)) * kp +
+                    c0 + 8 * p4;
+#pragma unroll
+      for (int kq = 0; kq < 4; ++kq)
+        asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(
+                         base + (long long)kq * kp),
+                     "f"(g[8 * kq + 0]), "f"(g[8 * kq + 1]), "f"(g[8 * kq + 2]),
+                     "f"(g[8 * kq + 3]), "f"(g[8 * kq + 4]), "f"(g[8 * kq + 5]),
+                     "f"(g[8 * kq + 6]), "f"(g[8 * kq + 7])
+                     : "memory");
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
