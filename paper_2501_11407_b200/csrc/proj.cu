@@ -606,23 +606,31 @@ __global__ void __launch_bounds__(256) pack_bytes4_kernel(const uint8_t* __restr
       sq[q] = tmajor ? row / B : row % Tc;
       bq[q] = tmajor ? row % B : row / Tc;
     }
-    for (int w = threadIdx.x; w < wpr; w += blockDim.x) {
-      uint32_t v[R];
+    // thread per 8 channels: two 32-bit loads, one 8-byte xq store, one 16-byte xh store
+    for (int w2 = threadIdx.x; 2 * w2 < wpr; w2 += blockDim.x) {
+      const int w = 2 * w2;
+      uint32_t v[R][2];
 #pragma unroll
-      for (int q = 0; q < R; ++q)
-        v[q] = (row0 + q < rows && sq[q] < len && 4 * w < k)
-                   ? __ldg(reinterpret_cast<const uint32_t*>(x + (long long)bq[q] * stride_b +
-                                                             (long long)sq[q] * k) + w)
-                   : 0u;
+      for (int q = 0; q < R; ++q) {
+        const bool live = row0 + q < rows && sq[q] < len;
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(x + (long long)bq[q] * stride_b +
+                                                                (long long)sq[q] * k);
+        v[q][0] = (live && 4 * w < k) ? __ldg(src + w) : 0u;
+        v[q][1] = (live && 4 * (w + 1) < k) ? __ldg(src + w + 1) : 0u;
+      }
 #pragma unroll
       for (int q = 0; q < R; ++q)
         if (row0 + q < rows)
-          reinterpret_cast<uint32_t*>(xq + (long long)(row0 + q) * Kpad)[w] = v[q];
+          reinterpret_cast<uint2*>(xq + (long long)(row0 + q) * Kpad)[w2] =
+              make_uint2(v[q][0], v[q][1]);
       if (xh != nullptr) {
 #pragma unroll
         for (int q = 0; q < R; ++q)
-          if (row0 + q < rows)
-            xh[((long long)bq[q] * KR + sq[q] + 1) * (Kpad >> 2) + w] = bf16x4_of_bytes(v[q]);
+          if (row0 + q < rows) {
+            const uint2 a = bf16x4_of_bytes(v[q][0]), b = bf16x4_of_bytes(v[q][1]);
+            reinterpret_cast<uint4*>(xh)[((long long)bq[q] * KR + sq[q] + 1) * (Kpad >> 3) + w2] =
+                make_uint4(a.x, a.y, b.x, b.y);
+          }
       }
     }
   }
@@ -746,7 +754,7 @@ int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits
   const int blocks = (int)(want < 148LL * 16 ? want : 148LL * 16);
   if (!bits && (k & 3) == 0 && (stride_b & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0) {
     const int b4 = (int)std::min<long long>((rows + proj::PACK_R - 1) / proj::PACK_R, PACK_GRID);
-    const int t4 = std::min(256, ((Kpad / 4 + 31) / 32) * 32);
+    const int t4 = std::min(256, ((Kpad / 8 + 31) / 32) * 32);
     proj::pack_bytes4_kernel<<<b4, t4, 0, stream>>>(x, stride_b, k, len, Tc, Kpad, B, time_major,
                                                      xq);
     SPB_CHECK_LAUNCH("pack_bytes4");
@@ -783,7 +791,7 @@ int spb_pack_spikes_xh(const uint8_t* x, long long stride_b, int B, int k, int b
   }
   SPB_CHECK_ARG((k & 3) == 0 && (stride_b & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 3) == 0,
                 "spb_pack_spikes_xh: byte rows must be 4-byte aligned");
-  const int t4 = std::min(256, ((Kpad / 4 + 31) / 32) * 32);
+  const int t4 = std::min(256, ((Kpad / 8 + 31) / 32) * 32);
   proj::pack_bytes4_kernel<<<(int)std::min<long long>((rows + proj::PACK_R - 1) / proj::PACK_R, PACK_GRID), t4, 0, stream>>>(
       x, stride_b, k, len, Tc, Kpad, B, 0, xq, static_cast<uint2*>(xh), KR);
   SPB_CHECK_LAUNCH("pack_bytes4_xh");
