@@ -134,7 +134,7 @@ __device__ __forceinline__ void slice_one(double wv, int s, int P, int8_t (&q)[8
   }
 }
 
-constexpr int SS_THREADS = 128;  // one CTA per row of W
+constexpr int SS_THREADS = 256;  // one CTA per row of W
 
 template <typename T>
 __global__ void __launch_bounds__(SS_THREADS) sgd_slice_kernel(T* __restrict__ w, GradSrc gs,
