@@ -1,6 +1,7 @@
 // C-ABI bookkeeping: error reporting and library identification.
 #include "common.cuh"
 #include <cstdarg>
+#include <cstdlib>
 
 namespace spb {
 static thread_local char g_err[512] = "";
@@ -9,6 +10,13 @@ void set_error(const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SPB_PDL");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return on;
 }
 }  // namespace spb
 

@@ -31,6 +31,31 @@ void set_error(const char* fmt, ...);
     }                                                                           \
   } while (0)
 
+// Programmatic dependent launch (PDL) between the kernels of one update on the main stream:
+// a kernel launched by pdl_launch may be scheduled while its predecessor drains; it calls
+// pdl_enter() first thing, which waits for the predecessor grid to complete (and its memory
+// to be visible) and then lets its own dependent launch early.  Both instructions are
+// no-ops for kernels launched without the attribute.  SPB_PDL=0 turns the attribute off.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... K, typename... A>
+inline cudaError_t pdl_launch(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<A&&>(args)...);
+}
+
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 __host__ __device__ inline int round_up(int a, int b) { return ceil_div(a, b) * b; }
 

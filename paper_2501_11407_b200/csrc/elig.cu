@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                       const __nv_bfloat16* __restrict__ wl_g, int ldw,
                       const __nv_bfloat16* __restrict__ xs_hi,
                       const __nv_bfloat16* __restrict__ xs_lo) {
+  pdl_enter();
   constexpr int NST = RAW ? STAGES_RB : STAGES;
   constexpr int EB = RAW ? EB_R : 1;   // eps tile buffers
   constexpr int SB = RAW ? STAGE_R : STAGE;
@@ -379,6 +380,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // the fixed-order fp64 sums), k_pad % 4 == 0.
 __global__ void reduce_partials_kernel(const float* __restrict__ partial, int S, int n, int n_pad,
                                        int k_pad, int accumulate, double* __restrict__ grad) {
+  pdl_enter();
   const long long idx = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
   if (idx >= (long long)n * k_pad) return;
   const long long stride = (long long)n_pad * k_pad;
@@ -529,14 +531,14 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
   if (raw) {
     cudaFuncSetAttribute(carry::alif_carry_kernel<true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, carry::SMEM_R);
-    carry::alif_carry_kernel<true><<<grid, carry::THREADS, carry::SMEM_R, stream>>>(
+    pdl_launch(carry::alif_carry_kernel<true>, grid, carry::THREADS, carry::SMEM_R, stream,
         mwh, mwl, mxh, mxl, meps, reinterpret_cast<const float2*>(mdt), eps, partial, B, n,
         n_pad, ke, kp, KR, bps, do_mma, load_eps, store_eps, carry_probe(), whb, wlb, ldw, xsh,
         xsl);
   } else {
     cudaFuncSetAttribute(carry::alif_carry_kernel<false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, carry::SMEM);
-    carry::alif_carry_kernel<false><<<grid, carry::THREADS, carry::SMEM, stream>>>(
+    pdl_launch(carry::alif_carry_kernel<false>, grid, carry::THREADS, carry::SMEM, stream,
         mwh, mwl, mxh, mxl, meps, reinterpret_cast<const float2*>(mdt), eps, partial, B, n,
         n_pad, ke, kp, KR, bps, do_mma, load_eps, store_eps, carry_probe(), whb, wlb, ldw,
         nullptr, nullptr);
@@ -550,7 +552,7 @@ int spb_reduce_partials(const float* partial, int splits, int n, int n_pad, int 
   SPB_CHECK_ARG(partial && grad && splits > 0 && n > 0 && n <= n_pad && k_pad % 4 == 0,
                 "spb_reduce_partials: bad args (k_pad %% 4 == 0)");
   const long long total = (long long)n * k_pad;
-  reduce_partials_kernel<<<(unsigned)((total / 4 + 255) / 256), 256, 0, stream>>>(
+  pdl_launch(reduce_partials_kernel, (unsigned)((total / 4 + 255) / 256), 256, 0, stream,
       partial, splits, n, n_pad, k_pad, accumulate, grad);
   SPB_CHECK_LAUNCH("reduce_partials");
   return 0;

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(K1_THREADS, 7) forward_chunk_kernel(
     FwdParams P, const double* __restrict__ cur, double* __restrict__ u_st,
     double* __restrict__ a_st, double* __restrict__ zbar_st, double* __restrict__ zsum_st,
     uint32_t* __restrict__ raster, const float* __restrict__ wsig, float* __restrict__ psis) {
+  pdl_enter();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // CTA = one sample x 128 consecutive neurons: every step it streams 1 KB of current
   // and writes 512 B of psi contiguously (DRAM-friendly), warp = 32 neurons
@@ -158,9 +159,8 @@ static void launch_forward(const FwdParams& P, dim3 grid, cudaStream_t stream, c
                            const float* wsig, float* psis) {
   const bool reset = P.reset != 0, smooth = P.smooth != 0;
 #define SPB_K1(R, S)                                                                          \
-  forward_chunk_kernel<PASSA, PARK, R, S><<<grid, K1_THREADS, 0, stream>>>(P, cur, u, a, zbar, \
-                                                                          zsum, raster, wsig, \
-                                                                          psis)
+  pdl_launch(forward_chunk_kernel<PASSA, PARK, R, S>, grid, K1_THREADS, 0, stream, P, cur, u, a, \
+             zbar, zsum, raster, wsig, psis)
   if (reset && smooth) SPB_K1(true, true);
   else if (reset) SPB_K1(true, false);
   else if (smooth) SPB_K1(false, true);
@@ -432,6 +432,7 @@ __global__ void __launch_bounds__(K1S_THREADS, SCAN_OCC) chunk_scan_kernel(
     uint32_t* __restrict__ c_hi, uint32_t* __restrict__ c_lo, uint32_t* __restrict__ w_hi,
     uint32_t* __restrict__ w_lo, int ldc, float2* __restrict__ mdt,
     const float* __restrict__ psis) {
+  pdl_enter();
   extern __shared__ float cs[];  // cs[r] = c_{t0+r-1}, r = 0..L
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int L = P.len;
@@ -1239,7 +1240,7 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
       SPB_CHECK_LAUNCH("chunk_scan_seg");
       return 0;
     }
-    kfn<<<sgrid, K1S_THREADS, (len + 1) * sizeof(float), stream>>>(
+    pdl_launch(kfn, sgrid, K1S_THREADS, (len + 1) * sizeof(float), stream,
         P, wsig, ctab, reinterpret_cast<uint32_t*>(c_hi), reinterpret_cast<uint32_t*>(c_lo),
         reinterpret_cast<uint32_t*>(w_hi), reinterpret_cast<uint32_t*>(w_lo), ldc,
         reinterpret_cast<float2*>(mdt), psi_scratch);

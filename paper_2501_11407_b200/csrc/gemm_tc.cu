@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const __grid_constant__ CUtensorMap tm_bl, int M, int N, int K,
                         int kb_per_split, float* __restrict__ partial, int ldp,
                         long long slice_stride) {
+  pdl_enter();
   constexpr int NST = BLO ? STAGES : STAGES_NL;
   constexpr int SB = BLO ? STAGE_BYTES : STAGE_BYTES_NL;
   extern __shared__ uint8_t smem_raw[];
@@ -334,12 +335,12 @@ int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* 
   if (blo) {
     cudaFuncSetAttribute(tc::grad_gemm_tc_kernel<true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
-    tc::grad_gemm_tc_kernel<true><<<grid, tc::THREADS, tc::SMEM_BYTES, stream>>>(
+    pdl_launch(tc::grad_gemm_tc_kernel<true>, grid, tc::THREADS, tc::SMEM_BYTES, stream,
         mah, mal, mbh, mbl, M, N_rows, K, kbps, partial, ldp, slice_stride);
   } else {
     cudaFuncSetAttribute(tc::grad_gemm_tc_kernel<false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES_NL);
-    tc::grad_gemm_tc_kernel<false><<<grid, tc::THREADS, tc::SMEM_BYTES_NL, stream>>>(
+    pdl_launch(tc::grad_gemm_tc_kernel<false>, grid, tc::THREADS, tc::SMEM_BYTES_NL, stream,
         mah, mal, mbh, mbl, M, N_rows, K, kbps, partial, ldp, slice_stride);
   }
   SPB_CHECK_LAUNCH("grad_gemm_tc");

@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(SS_THREADS) sgd_slice_kernel(T* __restrict__ w
                                                                int Kpad, int n_pad32, int P,
                                                                int8_t* __restrict__ wq,
                                                                int* __restrict__ sexp) {
+  pdl_enter();
   using O = Op<T>;
   __shared__ double red[SS_THREADS / 32];
   const int i = blockIdx.x;
@@ -195,10 +196,10 @@ extern "C" __attribute__((visibility("hidden"))) int spb_launch_sgd_slice(void* 
   const GradSrc gs{g, g_is_f64, ld_g, g_scale};
   const int blocks = n_pad32;
   if (w_is_f64)
-    sgd_slice_kernel<double><<<blocks, SS_THREADS, 0, stream>>>(static_cast<double*>(w), gs, n, k, lr,
+    pdl_launch(sgd_slice_kernel<double>, blocks, SS_THREADS, 0, stream, static_cast<double*>(w), gs, n, k, lr,
                                                          do_sgd, Kpad, n_pad32, P, wq, sexp);
   else
-    sgd_slice_kernel<float><<<blocks, SS_THREADS, 0, stream>>>(static_cast<float*>(w), gs, n, k,
+    pdl_launch(sgd_slice_kernel<float>, blocks, SS_THREADS, 0, stream, static_cast<float*>(w), gs, n, k,
                                                         (float)lr, do_sgd, Kpad, n_pad32, P, wq,
                                                         sexp);
   SPB_CHECK_LAUNCH("sgd_slice");

@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                            const __grid_constant__ CUtensorMap tm_w, const int* __restrict__ sexp,
                            double* __restrict__ out, int M, int n, int n_pad32, int nkb,
                            int probe) {
+  pdl_enter();
   using C = ResCfg<P, XS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -594,6 +595,7 @@ __global__ void __launch_bounds__(256) pack_bytes4_kernel(const uint8_t* __restr
                                                           uint8_t* __restrict__ xq,
                                                           uint2* __restrict__ xh = nullptr,
                                                           int KR = 0) {
+  pdl_enter();
   const int wpr = Kpad >> 2;  // output words per row
   const int rows = B * Tc;
   constexpr int R = PACK_R;   // rows per iteration, their loads issued together
@@ -644,6 +646,7 @@ __global__ void __launch_bounds__(128) pack_bits8_kernel(const uint8_t* __restri
                                                          uint8_t* __restrict__ xq,
                                                          uint4* __restrict__ xh = nullptr,
                                                          int KR = 0) {
+  pdl_enter();
   const int kb = (k + 7) >> 3;   // input bytes per row
   const int wpr = Kpad >> 3;     // output 8-byte words per row
   const int rows = B * Tc;
@@ -852,17 +855,17 @@ int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, i
       auto kfn = bin ? proj::input_proj_wres_kernel<6, 5, true> : proj::input_proj_wres_kernel<6, 5, false>;
       constexpr int sm = proj::ResCfg<6, 5>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      kfn<<<grid, proj::THREADS, sm, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
+      pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
     } else if (P == 7) {
       auto kfn = bin ? proj::input_proj_wres_kernel<7, 3, true> : proj::input_proj_wres_kernel<7, 3, false>;
       constexpr int sm = proj::ResCfg<7, 3>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      kfn<<<grid, proj::THREADS, sm, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
+      pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
     } else {
       auto kfn = proj::input_proj_wres_kernel<8, 2, false>;
       constexpr int sm = proj::ResCfg<8, 2>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      kfn<<<grid, proj::THREADS, sm, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
+      pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
     }
   } else if (P == 6) {
     auto kfn = bin ? proj::input_proj_kernel<6, true> : proj::input_proj_kernel<6, false>;

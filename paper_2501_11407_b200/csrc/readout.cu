@@ -16,6 +16,7 @@ __global__ void readout_loss_kernel(const double* __restrict__ wout, const doubl
                                     double* __restrict__ s_out, double* __restrict__ loss,
                                     double* __restrict__ g_out, float* __restrict__ wsig,
                                     int* __restrict__ correct) {
+  pdl_enter();
   extern __shared__ double sm[];  // [m] logits + [m] g (exps, then dL/ds)
   double* s = sm;
   double* g = sm + m;
@@ -161,7 +162,7 @@ int spb_readout_loss(const double* wout, const double* zsum, const long long* la
   const size_t smem = (size_t)(2 * m + 32) * sizeof(double);
   // one warp per class (up to 32 warps): the class dot products run in one round
   const int threads = 32 * (m < 8 ? 8 : (m > 32 ? 32 : m));
-  readout_loss_kernel<<<B, threads, smem, stream>>>(wout, zsum, labels, n, m, s_out, loss, g,
+  pdl_launch(readout_loss_kernel, B, threads, smem, stream, wout, zsum, labels, n, m, s_out, loss, g,
                                                     wsig, correct);
   SPB_CHECK_LAUNCH("readout_loss");
   return 0;
