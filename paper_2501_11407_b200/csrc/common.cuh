@@ -39,6 +39,10 @@ void set_error(const char* fmt, ...);
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+// explicit early trigger: the dependent grid may be scheduled before this one drains
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 bool pdl_enabled();
 template <typename... K, typename... A>
 inline cudaError_t pdl_launch(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem,

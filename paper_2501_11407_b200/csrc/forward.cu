@@ -433,6 +433,7 @@ __global__ void __launch_bounds__(K1S_THREADS, SCAN_OCC) chunk_scan_kernel(
     uint32_t* __restrict__ w_lo, int ldc, float2* __restrict__ mdt,
     const float* __restrict__ psis) {
   pdl_enter();
+  pdl_trigger();
   extern __shared__ float cs[];  // cs[r] = c_{t0+r-1}, r = 0..L
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int L = P.len;

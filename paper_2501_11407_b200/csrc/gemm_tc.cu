@@ -81,7 +81,6 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const __grid_constant__ CUtensorMap tm_bl, int M, int N, int K,
                         int kb_per_split, float* __restrict__ partial, int ldp,
                         long long slice_stride) {
-  pdl_enter();
   constexpr int NST = BLO ? STAGES : STAGES_NL;
   constexpr int SB = BLO ? STAGE_BYTES : STAGE_BYTES_NL;
   extern __shared__ uint8_t smem_raw[];
@@ -122,6 +121,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  pdl_enter();  // the prologue above touches only shared memory, TMEM and the params
 
   if (warp == 0) {
     if (lane == 0) {
