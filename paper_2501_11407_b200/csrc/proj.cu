@@ -304,7 +304,6 @@ __global__ void __launch_bounds__(THREADS, 1)
                            const __grid_constant__ CUtensorMap tm_w, const int* __restrict__ sexp,
                            double* __restrict__ out, int M, int n, int n_pad32, int nkb,
                            int probe) {
-  pdl_enter();
   using C = ResCfg<P, XS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -352,6 +351,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  pdl_enter();  // the prologue above touches only shared memory, TMEM and the params
 
   if (warp == 0) {
     if (lane == 0) {
@@ -596,6 +596,7 @@ __global__ void __launch_bounds__(256) pack_bytes4_kernel(const uint8_t* __restr
                                                           uint2* __restrict__ xh = nullptr,
                                                           int KR = 0) {
   pdl_enter();
+  pdl_trigger();
   const int wpr = Kpad >> 2;  // output words per row
   const int rows = B * Tc;
   constexpr int R = PACK_R;   // rows per iteration, their loads issued together
@@ -647,6 +648,7 @@ __global__ void __launch_bounds__(128) pack_bits8_kernel(const uint8_t* __restri
                                                          uint4* __restrict__ xh = nullptr,
                                                          int KR = 0) {
   pdl_enter();
+  pdl_trigger();
   const int kb = (k + 7) >> 3;   // input bytes per row
   const int wpr = Kpad >> 3;     // output 8-byte words per row
   const int rows = B * Tc;
