@@ -445,7 +445,7 @@ def main():
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        n_e2e = max(5, args.steps // 2)
+        n_e2e = max(10, args.steps)
         e0.record(main)
         run_e2e(n_e2e)
         e1.record(main)
