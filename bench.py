@@ -149,6 +149,60 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+def parity_block(eng, net, x_np, y_np, kw, kind, recurrent=False):
+    """One update of the timed configuration (the same engine, inputs and initial
+    weights) checked against the f64 oracle -- the reference's BPTT engine batched in
+    GEMM form (oracle/eprop_ref.bptt_batch, pinned to the reference's own outputs in
+    tests/test_oracle.py).  Runs after the timed region; the oracle is only the checker.
+    The full batch is checked when its [B, T, n] f64 oracle state fits 2^27 entries,
+    else the first samples of the batch through a second engine of that size."""
+    import torch
+    from oracle import eprop_ref as O
+    from paper_2501_11407_b200.engine import EpropEngine
+    if recurrent:
+        return {"checked": False, "why": "recurrent extension: parity unpinned (no reference)"}
+    B, T, k = x_np.shape
+    n = eng.n
+    bs = B if B * T * n <= (1 << 27) else max(1, (1 << 27) // (T * n))
+    e = eng
+    if bs < B:
+        e = EpropEngine(n, k, eng.m, bs, alif=kind == "alif", w_f64=False, chunk=eng.Tc,
+                        device=eng.device)
+    xs, ys = np.ascontiguousarray(x_np[:bs]), y_np[:bs]
+    e.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+    raster = torch.zeros((bs, T, (n + 31) // 32), dtype=torch.int32, device=eng.device)
+    e.run(torch.from_numpy(xs).to(eng.device), torch.from_numpy(ys).to(eng.device),
+          raster=raster, binary=True, **kw)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ref = O.bptt_batch(net.neuron.w, net.readout.w_out, O.Params(alif=kind == "alif"), xs, ys)
+    t_or = time.perf_counter() - t0
+    r = raster.cpu().numpy().view(np.uint32)
+    got = ((r[..., None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool)
+    got = got.reshape(bs, T, -1)[..., :n]
+    gw = e.grad_w(torch.float64).cpu().numpy().ravel()
+    gwo = e.grad_wout.cpu().numpy().ravel()
+    rw, ro = ref.grad_w.ravel(), ref.grad_w_out.ravel()
+    rel = float(np.linalg.norm(gw - rw) / np.linalg.norm(rw))
+    cos = float(gw @ rw / (np.linalg.norm(gw) * np.linalg.norm(rw)))
+    out = {
+        "checked": True,
+        "oracle": "f64 BPTT (reference gradients.py:188-231, batched GEMM form) on the "
+                  "same inputs and initial weights",
+        "samples": bs, "of_batch": B, "steps": T,
+        "spike_flips": int((got != ref.raster).sum()),
+        "spikes": int(ref.raster.sum()),
+        "grad_w_rel_l2": rel, "grad_w_cos": cos,
+        "grad_w_out_rel_l2": float(np.linalg.norm(gwo - ro) / np.linalg.norm(ro)),
+        "loss_max_rel": float(np.max(np.abs(e.loss.cpu().numpy() - ref.loss)
+                                     / np.maximum(np.abs(ref.loss), 1e-300))),
+        "tolerance": "spikes bit-exact; grad rel <= 1e-4, cos >= 0.9999",
+        "oracle_s": round(t_or, 2),
+    }
+    out["pass"] = bool(out["spike_flips"] == 0 and rel <= 1e-4 and cos >= 0.9999)
+    return out
+
+
 def cpu_reference_line(args, cfg_name):
     """--impl reference: the reference algorithm (oracle port) on the host cores."""
     from oracle.cpu_bench import _pool, cores, time_cpu
@@ -192,6 +246,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the post-timing parity check of one update vs the f64 oracle")
     ap.add_argument("--microbatch", type=int, default=1,
                     help="split the batch over this many concurrently streamed engines")
     ap.add_argument("--mb-sms", type=int, default=0,
@@ -543,6 +599,14 @@ def main():
                      "kernel_ms_per_step": e["ms_per_step"],
                      "share_of_step": e["share_of_step"]})
 
+    # ---- parity of the timed configuration (after the timed region; rank 0) ----
+    parity = None
+    if rank == 0 and not args.no_parity and not args.profile:
+        try:
+            parity = parity_block(eng, net, x_np, y_np, kw, kind, args.recurrent)
+        except Exception as exc:  # noqa: BLE001
+            parity = {"checked": False, "error": repr(exc)}
+
     # ---- CPU baseline (rank 0, N=1 only) ----
     cpu = None
     if world == 1 and not args.no_cpu and not args.profile:
@@ -578,6 +642,7 @@ def main():
             "roofline": roof,
             "kernels": kernels,
             "cpu_baseline": cpu,
+            "parity": parity,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

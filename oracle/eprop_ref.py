@@ -330,6 +330,74 @@ def eprop_two_pass_batch(w, w_out, p: Params, x, labels, dtype=np.float64) -> Ba
     return BatchResult(loss, s, grad_w, grad_w_out, raster, zsum)
 
 
+def bptt_batch(w, w_out, p: Params, x, labels, dtype=np.float64, smooth=False) -> BatchResult:
+    """Batched ``bptt_gradient`` (gradients.py:188-231) in GEMM form: the checker for the
+    benched configurations (C3 at B=256, C4 at B=128), where the per-synapse e-prop
+    restatement would take hours in numpy.
+
+    For the reference's feed-forward layer e-prop is the exact gradient (the reference
+    pins sparse e-prop == BPTT to <=1e-10 in f64, test_gradients.py:157-194, reset on and
+    off), so this is an oracle for ``eprop_sparse_gradient`` summed over the batch.
+    Forward: one [B*T, k] x [k, n] GEMM for every step's current (x is integer counts,
+    so the f64 sums differ from the reference's matvec only in the last ulp), then the
+    per-step state update of gradients.py:118-129 over [B, n].  Reverse sweep exactly as
+    gradients.py:216-230, storing lambda_u per step; grad_W = one [n, B*T] x [B*T, k] GEMM.
+    """
+    w = np.asarray(w).astype(dtype)
+    w_out = np.asarray(w_out).astype(dtype)
+    B, T, k = x.shape
+    n, m = w.shape[0], w_out.shape[0]
+    beta, rho = p.beta_eff, p.rho_eff
+    xf = x.reshape(B * T, k).astype(dtype)
+    cur = (xf @ w.T).reshape(B, T, n)                  # every step's W x_t
+    sgs = np.empty((B, T, n), dtype)
+    raster = np.zeros((B, T, n), dtype=bool)
+    u = np.zeros((B, n), dtype)
+    a = np.zeros((B, n), dtype)
+    v = np.zeros((B, m), dtype)
+    s = np.zeros((B, m), dtype)
+    zbar = np.zeros((B, n), dtype)
+    zsum = np.zeros((B, n), dtype)
+    for t in range(T):                                  # gradients.py:118-129
+        z_prev = _spike(u - p.theta - beta * a, p.slope, smooth)
+        a = rho * a + z_prev
+        u = p.alpha * u + cur[:, t]
+        if p.reset:
+            u = u - p.theta * z_prev
+        d = u - p.theta - beta * a
+        z = _spike(d, p.slope, smooth)
+        sgs[:, t] = surrogate_grad(d, p.slope)
+        raster[:, t] = z > 0.5
+        cur[:, t] = z                                   # z_t kept for the readout grad
+        v = p.kappa * v + z @ w_out.T
+        s = s + v
+        zbar = p.kappa * zbar + z
+        zsum = zsum + zbar
+    loss = np.zeros(B)
+    g = np.zeros((B, m), dtype)
+    for b in range(B):
+        loss[b], g[b] = softmax_cross_entropy(s[b], int(labels[b]))
+    lam_u = np.zeros((B, n), dtype)
+    lam_a = np.zeros((B, n), dtype)
+    c_t = 0.0
+    mu0 = g @ w_out                                      # W_out^T g per sample
+    for t in range(T - 1, -1, -1):                      # gradients.py:216-230
+        c_t = 1.0 + p.kappa * c_t
+        xi = c_t * mu0
+        if p.alif:
+            xi = xi + lam_a
+        if p.reset:
+            xi = xi - p.theta * lam_u
+        new_lam_u = p.alpha * lam_u + xi * sgs[:, t]
+        if p.alif:
+            lam_a = rho * lam_a - beta * xi * sgs[:, t]
+        lam_u = new_lam_u
+        sgs[:, t] = lam_u                               # lambda_u,t overwrites psi_t
+    grad_w = sgs.reshape(B * T, n).T @ xf               # sum_{b,t} lambda_u (x) x_t
+    grad_w_out = g.T @ zsum                             # sum_t c_t g (x) z_t = g (x) zsum
+    return BatchResult(loss, s, grad_w, grad_w_out, raster, zsum)
+
+
 # --------------------------------------------------------------------------------------
 # parity inputs (training.py:35-50, datasets.py:60-83)
 # --------------------------------------------------------------------------------------

@@ -104,6 +104,48 @@ def test_two_pass_batch_large_shapes(name):
     assert np.allclose(r.loss, g["loss"], rtol=1e-12)
 
 
+@pytest.mark.parametrize("name", [n for n in SMALL if "f64" in n])
+def test_bptt_batch_matches_reference(name):
+    """The batched GEMM-form BPTT (checker of the benched configs) against the
+    reference's per-sample e-prop and BPTT, summed over the batch (reset on and off)."""
+    g = load_golden(name)
+    p, w, w_out, x, labels = _setup(g)
+    r = O.bptt_batch(w, w_out, p, x, labels)
+    for key in ("eprop_w", "bptt_w"):
+        ref = g[key].sum(0)
+        assert np.linalg.norm(r.grad_w - ref) <= 1e-11 * np.linalg.norm(ref)
+    ref_o = g["eprop_w_out"].sum(0)
+    assert np.linalg.norm(r.grad_w_out - ref_o) <= 1e-11 * np.linalg.norm(ref_o)
+    assert np.allclose(r.loss, g["loss"], rtol=1e-12, atol=1e-12)
+    assert np.array_equal(np.packbits(r.raster, axis=-1), g["raster_packed"])
+
+
+@pytest.mark.parametrize("name", ["c2_lif_f64", "c3_alif_f64", "c4_alif_f64"])
+def test_bptt_batch_large_shapes(name):
+    """SHD/SSC shapes: bit-exact rasters and the reference's gradient samples."""
+    g = load_golden(name)
+    p, w, w_out, x, labels = _setup(g)
+    r = O.bptt_batch(w, w_out, p, x, labels)
+    assert np.array_equal(np.packbits(r.raster, axis=-1), g["raster_packed"])
+    ref = g["eprop_w_batch_sum"]
+    got = r.grad_w.ravel()[g["grad_idx"]]
+    assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref)
+    assert np.allclose(r.loss, g["loss"], rtol=1e-12)
+
+
+def test_bptt_batch_equals_two_pass_long_horizon():
+    """Long horizon (T = 3000, ALIF, the regime of the >= 10-chunk GPU tests): the
+    GEMM-form BPTT and the per-synapse two-pass e-prop restatement agree in f64."""
+    p = O.Params(alif=True)
+    x, labels = O.poisson_batch(3, 24, 3000, 3, seed=5)
+    w, w_out = O.init_network_arrays(16, 24, 3, seed=2)
+    w = w * 4.0   # enough drive that neurons spike and adapt over the whole horizon
+    a = O.bptt_batch(w, w_out, p, x, labels)
+    b = O.eprop_two_pass_batch(w, w_out, p, x, labels)
+    assert a.raster.any() and np.array_equal(a.raster, b.raster)
+    assert np.linalg.norm(a.grad_w - b.grad_w) <= 1e-10 * np.linalg.norm(b.grad_w)
+
+
 def test_poisson_generator_statistics():
     x, labels = O.poisson_batch(4, 700, 50, 20, seed=0)
     assert x.dtype == np.uint8 and set(np.unique(x)) <= {0, 1}
