@@ -69,7 +69,7 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
-INT8_KERNELS = ("proj", "fused_a", "fused_b")
+INT8_KERNELS = ("proj",)
 
 
 def measured_traffic(cfg, kernel):
@@ -248,10 +248,6 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the post-timing parity check of one update vs the f64 oracle")
-    ap.add_argument("--microbatch", type=int, default=1,
-                    help="split the batch over this many concurrently streamed engines")
-    ap.add_argument("--mb-sms", type=int, default=0,
-                    help="SMs the persistent kernels of each micro-batch may occupy (0 = all)")
     ap.add_argument("--park-gb", type=float, default=0.0,
                     help="opt-in: park every chunk's psi in pass A when it fits this many GB "
                          "(pass B skips the projection and dynamics; memory then grows with T)")
@@ -300,19 +296,12 @@ def main():
     x_np, y_np = poisson_batch(B, k, T, m, seed=1000 + rank)
     from paper_2501_11407_b200.engine import default_chunk
     chunk = args.chunk or default_chunk(T, B, n, k, kind == "alif")
-    if args.microbatch > 1:
-        from paper_2501_11407_b200.engine import MicroBatchEngine
-        eng = MicroBatchEngine(n, k, m, B, parts=args.microbatch, alif=kind == "alif",
-                               w_f64=False, chunk=chunk, device=dev, recurrent=args.recurrent,
-                               sm_count=args.mb_sms or None)
-    else:
-        eng = EpropEngine(n, k, m, B, alif=kind == "alif", w_f64=False, chunk=chunk,
-                          device=dev, recurrent=args.recurrent)
+    eng = EpropEngine(n, k, m, B, alif=kind == "alif", w_f64=False, chunk=chunk,
+                      device=dev, recurrent=args.recurrent)
     eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out),
                     w_rec=torch.from_numpy(net.neuron.w_rec) if args.recurrent else None)
     if args.park_gb > 0:
-        for e in getattr(eng, "engines", [eng]):
-            e.park_budget = int(args.park_gb * (1 << 30))
+        eng.park_budget = int(args.park_gb * (1 << 30))
     xd = torch.from_numpy(x_np).to(dev)
     yd = torch.from_numpy(y_np).to(dev)
     packer = GradPacker(n, k, m, dev)  # (recurrent: grad W_rec stays in the accumulator)
@@ -321,14 +310,10 @@ def main():
     if kind == "alif":
         kw.update(beta=net.neuron.beta, rho=net.neuron.rho)
 
-    # Online weight update (north_star (3)): one fp32 master W / W_out shared by the
-    # engine(s); after the allreduce the fused SGD kernel updates both (W_out also
-    # refreshes the engine's fp64 mirror) and W is re-sliced into the INT8 digits the
-    # next update's projection reads -- all of it inside the timed step.
-    engines = list(getattr(eng, "engines", [eng]))
-    w_master = engines[0].w
-    for e in engines[1:]:
-        e.w = w_master
+    # Online weight update (north_star (3)): fp32 master W (the engine's) and W_out;
+    # after the allreduce the fused SGD kernel updates both (W_out also refreshes the
+    # engine's fp64 mirror) and W is re-sliced into the INT8 digits the next update's
+    # projection reads -- all of it inside the timed step.
     wout_master = torch.from_numpy(np.ascontiguousarray(net.readout.w_out)).to(dev)
     lr, g_scale = 1e-3, 1.0 / (world * B)
     vp = ctypes.c_void_p
@@ -341,12 +326,9 @@ def main():
             gw, gwo, g64, ldw = eng.grad_w_acc, eng.grad_wout, 1, eng.grad_w_acc.stride(0)
         st = vp(torch.cuda.current_stream(dev).cuda_stream)
         # W: SGD fused with the re-slicing of the first engine's INT8 digits
-        engines[0].sgd_slice(gw, g64, ldw, g_scale, lr)
+        eng.sgd_slice(gw, g64, ldw, g_scale, lr)
         _lib.call("spb_sgd_update", vp(wout_master.data_ptr()), 0, m, n, vp(gwo.data_ptr()),
-                  g64, n, g_scale, lr, vp(engines[0].wout.data_ptr()), st)
-        for e in engines[1:]:
-            e.wout.copy_(engines[0].wout)
-            e.slice_weights()
+                  g64, n, g_scale, lr, vp(eng.wout.data_ptr()), st)
 
     def step(x, y, timers=None, bits=False):
         # the synthetic Poisson inputs are 0/1 spikes: promise it (K2 single-int64 path)
@@ -407,8 +389,8 @@ def main():
         ev[i][1].record()
     barrier()
     # kernels of libsparseprop_b200.so per step: the engine's + SGD(+slice) on W + SGD on
-    # W_out + a slice per further engine (+ the payload pack when N > 1)
-    launches_per_step = eng.launches + 2 + (len(engines) - 1) + (1 if world > 1 else 0)
+    # W_out (+ the payload pack when N > 1)
+    launches_per_step = eng.launches + 2 + (1 if world > 1 else 0)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
     clk = clocks.stop() if clocks else None
@@ -530,14 +512,6 @@ def main():
                 ln = meta                                        # int8 MACs x2, useful part
                 flops += 2.0 * P_sl * B * ln * n * k
                 byts += B * ln * k + P_sl * n * k + 8.0 * B * ln * n
-            elif name in ("fused_a", "fused_b"):
-                ln, pid, parked = meta                           # K21: projection + dynamics
-                flops += 2.0 * P_sl * B * ln * n * k
-                byts += B * ln * k + P_sl * n * k + 16.0 * B * n * 2   # spikes, digits, state
-                if parked:
-                    byts += 4.0 * B * (ln + 1) * n                     # psi for the scan
-                if pid == 0:
-                    byts += B * ln * n / 8.0 + 16.0 * B * n           # raster, zbar/zsum
             elif name in ("forward", "forward_a"):
                 ln, pid, flag = meta
                 pid = {3: 2, 4: 1}.get(pid, pid)   # raw-operand passes: same traffic
@@ -548,9 +522,6 @@ def main():
                         byts += psi
                 if pid >= 1:                       # scan: psi back, C (and W) out, bf16 hi/lo
                     byts += psi + 4.0 * n * B * KR * (2 if flag else 1)
-            elif name == "forward_scan":
-                ln, _, _ = meta                    # K1f: current in, C out (psi stays in L2)
-                byts += 8.0 * B * ln * n + 4.0 * n * B * KR
             elif name == "gemm":
                 ln, raw = meta                   # raw spikes (exact bf16): 2 MMAs, no B-lo
                 flops += (4.0 if raw else 6.0) * n * k * B * (ln + 1)
@@ -576,10 +547,7 @@ def main():
         dom = max(kernels, key=lambda nm: kernels[nm]["ms_per_step"])
         e = kernels[dom]
         names = {"proj": "input_proj_kernel (K2, int8 tcgen05)", "forward": "forward_chunk + chunk_scan (K1 pass B)",
-                 "fused_a": "fused_forward_kernel (K21 pass A: int8 tcgen05 projection + fp64 dynamics)",
-                 "fused_b": "fused_forward_kernel (K21 pass B: projection + dynamics, psi)",
                  "forward_a": "forward_chunk_kernel (K1 pass A)",
-                 "forward_scan": "forward_scan_kernel (K1f: dynamics + readout + chunk scan)",
                  "gemm": "grad_gemm_tc_kernel (K5, bf16 hi/lo tcgen05)",
                  "carry": "alif_carry_kernel (K6, tcgen05 + eps stream)"}
         if args.recurrent:
@@ -631,7 +599,7 @@ def main():
                        "global_batch": B * world, "seq_len": T, "n_hidden": n, "n_inputs": k,
                        "n_classes": m, "chunk": eng.Tc, "parallelism": f"dp{world}",
                        "forward_precision": "fp64 state/current (bit-exact spikes)",
-                       "forward_kernel": "K21 fused projection+dynamics" if eng.fused else "K2 projection + K1 dynamics",
+                       "forward_kernel": "K2 projection + K1 dynamics",
                        "step": "e-prop gradient (+ allreduce when N > 1) + fused SGD on W/W_out + W re-slice",
                        "psi_parking_gb": args.park_gb,
                        "l2": "512 MiB flush between timed steps (outside events)",

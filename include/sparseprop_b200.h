@@ -36,8 +36,9 @@ int spb_version(void);
 int spb_device_sm(void); /* compute capability of the current device, e.g. 100 */
 
 /* K2  Exact input projection on INT8 tensor cores (proj.cu).  The weights are sliced
- *     once per update into P signed 7-bit digits per entry (P=7 for fp32 weights, 8 for
- *     fp64) with a per-neuron power-of-two scale; spikes are uint8 counts; tcgen05
+ *     once per update into P signed digits per entry (P=6 radix-256 digits for fp32
+ *     weights, P=8 radix-128 digits for fp64; csrc/digits.cuh) with a per-neuron
+ *     power-of-two scale; spikes are uint8 counts; tcgen05
  *     kind::i8 accumulates exactly in int32 and the digits are recombined in int64, so
  *     I = W x_t is exact up to one final fp64 rounding.  Replaces `net.neuron.w @ x_t`
  *     (gradients.py:125).
@@ -46,7 +47,7 @@ int spb_device_sm(void); /* compute capability of the current device, e.g. 100 *
  *   spb_pack_spikes:   x row (b, s < len) at x + b*stride_b + s*kb -> xq [B*Tc][Kpad] uint8,
  *                      zero padded; bits = 0: kb = k bytes (counts), bits = 1: kb = ceil(k/8)
  *                      bytes, channel j = bit (j & 7) of byte j >> 3 (packbits, little);
- *                      output row b*Tc + s, or s*B + b with time_major != 0 (K21). 
+ *                      output row b*Tc + s, or s*B + b with time_major != 0.
  *   spb_input_proj:    cur[row][i] = sum_j xq[row][j] W[i][j] for row < M (= B*Tc), fp64;
  *                      persistent grid of min(tiles, sm_count) CTAs.  binary != 0 promises
  *                      0/1 spikes (and k <= 16384): the 7 digit sums then recombine in one
@@ -62,42 +63,13 @@ int spb_pack_spikes_xh(const uint8_t* x, long long stride_b, int B, int k, int b
                        int Tc, int Kpad, int KR, uint8_t* xq, void* xh, cudaStream_t stream);
 int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
                    int Kpad, int P, double* cur, int sm_count, int binary, cudaStream_t stream);
-/* K2 on CTA pairs (proj2.cu): the same exact projection with tcgen05.mma.cta_group::2 --
- *   each CTA of a 2-CTA cluster supplies its 128 spike rows and half of the weight digits
- *   (P even: 6 or 8; Kpad <= 768); same output bits as spb_input_proj. */
-int spb_input_proj_pair(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
-                        int n_pad32, int Kpad, int P, double* cur, int sm_count, int binary,
-                        cudaStream_t stream);
 /* Profiling variant of spb_input_proj (W-resident kernel): probe bit 0 skips the epilogue,
  * bit 1 the spike-operand loads; probe = 0 is the production kernel. */
 int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
                          int n_pad32, int Kpad, int P, double* cur, int sm_count, int binary,
                          int probe, cudaStream_t stream);
 
-/* K21 Fused exact projection + neuron dynamics (fused.cu): the K2 tensor-core sums of a
- *     (128-sample block, 16-neuron tile) at one step land in TMEM and the epilogue thread
- *     that owns the sample integrates K1's dynamics in registers, step after step; the
- *     fp64 current never reaches HBM.  Same arithmetic as K2 + K1 (identical spikes).
- *     xq: TIME-MAJOR operand [Tc*B][Kpad] (spb_pack_spikes time_major=1), Kpad <= 768;
- *     wq/sexp from spb_slice_weights.  pass 0 (A): zbar, zsum, raster (uint8 view of the
- *     [B][T][ceil(n/32)] uint32 raster, optional, must be ZERO-initialised: bits are
- *     OR-ed in), psi optional; pass 1 (B): psi required
- *     (then spb_forward_chunk pass 2 runs the scan).  State u, a as K1. */
-int spb_fused_forward(int pass, const uint8_t* xq, const int8_t* wq, const int* sexp, int B,
-                      int n, int n_pad32, int Kpad, int P, int Tc, int KR, int len, int t0, int T,
-                      double alpha, double theta, double slope, double beta, double rho,
-                      double kappa, int reset, int smooth, double* u, double* a, double* zbar,
-                      double* zsum, uint8_t* raster, float* psi_scratch, int sm_count,
-                      cudaStream_t stream);
 
-/* Profiling variant of spb_fused_forward: probe bit 0 skips the dynamics (MMA + TMEM
- * reads only), bit 1 skips the psi stores; probe = 0 is the production kernel. */
-int spb_fused_forward_probe(int pass, const uint8_t* xq, const int8_t* wq, const int* sexp, int B,
-                            int n, int n_pad32, int Kpad, int P, int Tc, int KR, int len, int t0,
-                            int T, double alpha, double theta, double slope, double beta,
-                            double rho, double kappa, int reset, int smooth, double* u, double* a,
-                            double* zbar, double* zsum, uint8_t* raster, float* psi_scratch,
-                            int sm_count, int probe, cudaStream_t stream);
 
 /* K1  Neuron dynamics over one time chunk from the exact current cur [B*Tc][n] (row
  *     b*Tc+s): ALIF/LIF state update, spike and surrogate derivative.
@@ -134,21 +106,6 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
                       void* wa_hi, void* wa_lo, int ldc, float* mdt, float* psi_scratch,
                       cudaStream_t stream);
 
-/* K1f One-chunk update's per-neuron work in one kernel (forward.cu; replaces, for a
- *     sequence that fits one chunk, reset = 0: spb_forward_chunk pass 0 with psi_scratch +
- *     spb_readout_loss + spb_forward_chunk pass 2): the pass-A dynamics from a fresh state
- *     (u, a, zbar, zsum, raster as K1), the readout loss of each sample (s, loss, g, correct
- *     and wsig = W_out^T g as spb_readout_loss; wout [m][n] fp64, m <= 64, logits summed over
- *     128-neuron partials) and the backward scan into c_hi/c_lo (as pass B; no carry).
- *     sync: 1 + 2B uint32 words, zero before the first call (self-resetting); part:
- *     B * ceil(n/128) * m doubles of scratch.  Reference: gradients.py:118-174 as K1 + K3. */
-int spb_forward_scan_chunk(const double* cur, int B, int n, int Tc, int KR, int len, int T,
-                           double alpha, double theta, double slope, double beta, double rho,
-                           double kappa, int alif, int smooth, double* u, double* a, double* zbar,
-                           double* zsum, uint32_t* raster, float* psi, const double* wout,
-                           const long long* labels, int m, double* s, double* loss, double* g,
-                           float* wsig, int* correct, const float* ctab, void* c_hi, void* c_lo,
-                           int ldc, unsigned* sync, double* part, cudaStream_t stream);
 
 /* K1rec Recurrent hidden layer (forward_rec.cu, parity unpinned):
  *     u <- alpha u + (cur[row][i] + sum_{j: z_{t-1}[j]} W_rec[i][j]), otherwise as K1.
@@ -205,7 +162,7 @@ int spb_readout_grad(const double* g, const double* zsum, int B, int n, int m, d
                      cudaStream_t stream);
 
 /* K5  Chunk gradient GEMM on tcgen05 tensor cores (TMA-fed, bf16 hi/lo split, fp32
- *     TMEM accumulation), split-K over `splits` CTAs per 128x128 tile:
+ *     TMEM accumulation), split-K over `splits` CTAs per 128x256 tile:
  *       partial[z][i][j] = sum_{K in split z} (Ah+Al)[K][i] (Bh+Bl)[K][j]  (i<M, j<ldp)
  *     at partial + z*slice_stride (row stride ldp); every slice is written.
  *     With A = C (K1) and B = xbar (K4) this is every intra-chunk gradient term: the

@@ -24,17 +24,10 @@ SIGNATURES = {
     "spb_slice_weights": [P, I, I, I, I, I, I, P, P, P],
     "spb_pack_spikes": [P, LL, I, I, I, I, I, I, I, P, P],
     "spb_pack_spikes_xh": [P, LL, I, I, I, I, I, I, I, P, P, P],
-    "spb_fused_forward_probe": [I, P, P, P, I, I, I, I, I, I, I, I, I, I, D, D, D, D, D, D, I,
-                                I, P, P, P, P, P, P, I, I, P],
-    "spb_fused_forward": [I, P, P, P, I, I, I, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I,
-                          P, P, P, P, P, P, I, P],
     "spb_input_proj": [P, P, P, I, I, I, I, I, P, I, I, P],
     "spb_input_proj_probe": [P, P, P, I, I, I, I, I, P, I, I, I, P],
-    "spb_input_proj_pair": [P, P, P, I, I, I, I, I, P, I, I, P],
     "spb_forward_chunk": [I, P, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I, I,
                           P, P, P, P, P, P, P, P, P, P, P, P, P, I, P, P, P],
-    "spb_forward_scan_chunk": [P, I, I, I, I, I, I, D, D, D, D, D, D, I, I, P, P, P, P, P, P,
-                               P, P, I, P, P, P, P, P, P, P, P, I, P, P, P],
     "spb_xbar_chunk": [P, LL, LL, I, I, I, I, I, I, D, P, P, P, P],
     "spb_xbar_chunk_seg": [P, LL, LL, I, I, I, I, I, I, D, P, P, P, P],
     "spb_xbar_chunk_raw": [P, LL, LL, I, I, I, I, I, I, D, P, P, P, P, P],

@@ -1,4 +1,4 @@
-// Weight-digit formats of the exact INT8 tensor-core projection (K2 / K21).
+// Weight-digit formats of the exact INT8 tensor-core projection (K2).
 //
 //   W[i][j] = sum_{p<P} q_p[i][j] * 2^(RB*(P-1-p)) * 2^(s_i - F) + r,   q_p int8,
 //   s_i = exponent of max_j |W[i][j]|  (|W[i][j]| < 2^s_i)

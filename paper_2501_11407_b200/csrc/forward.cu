@@ -169,241 +169,6 @@ static void launch_forward(const FwdParams& P, dim3 grid, cudaStream_t stream, c
 }
 
 // ------------------------------------------------------------------------------------
-// K1f: a whole one-chunk update's per-neuron work in ONE kernel -- pass A (the K1 loop
-// above), the readout (logits, softmax cross-entropy, learning signal w_sig) and the
-// backward chunk scan (K1s) -- so psi goes from the forward loop to the scan through L2
-// (read back right after it was written, then discarded without write-back) instead of
-// an HBM round trip, and the readout costs no separate launch.  The readout of sample b
-// needs zsum of ALL its neurons: the ceil(n/128) CTAs of a sample meet through global
-// memory -- each publishes its partial logits, the last to arrive (atomic counter) adds
-// the partials in block order, evaluates the loss and publishes g, the others spin on a
-// generation word.  CTAs take their (block, sample) from a ticket counter in dispatch
-// order, so every sample's CTAs are resident or finished when one of them waits: no
-// deadlock whatever the occupancy.  Sync words self-reset; the buffer is zeroed once.
-// Bitwise the unfused path's spikes, losses to fp64 rounding (the logits are summed
-// over 128-neuron partials), gradients to fp32 rounding.
-// ------------------------------------------------------------------------------------
-constexpr int KF_MAXM = 64;
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <bool ALIF, bool SMOOTH>
-__global__ void __launch_bounds__(K1_THREADS, 6) forward_scan_kernel(
-    FwdParams P, const double* __restrict__ cur, double* __restrict__ u_st,
-    double* __restrict__ a_st, double* __restrict__ zbar_st, double* __restrict__ zsum_st,
-    uint32_t* __restrict__ raster, float* __restrict__ psis, const double* __restrict__ wout,
-    const long long* __restrict__ labels, int m, double* __restrict__ s_out,
-    double* __restrict__ loss_out, double* __restrict__ g_out, float* __restrict__ wsig_out,
-    int* __restrict__ correct, const float* __restrict__ ctab, uint32_t* __restrict__ c_hi,
-    uint32_t* __restrict__ c_lo, int ldc, unsigned* __restrict__ sync,
-    double* __restrict__ part) {
-  extern __shared__ float cs[];  // cs[r] = c_{r-1}, r = 0..L (readout filter gains)
-  __shared__ double red[K1_THREADS / 32][KF_MAXM];
-  __shared__ double sg[KF_MAXM];
-  __shared__ unsigned s_tk, s_gen0, s_last;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n = P.n, L = P.len;
-  const int nblk = (n + K1_THREADS - 1) / K1_THREADS;
-  unsigned* ticket = sync;
-  unsigned* count = sync + 1;
-  unsigned* gen = sync + 1 + P.B;
-  if (tid == 0) {
-    const unsigned t = atomicAdd(ticket, 1u);
-    if (t == (unsigned)(nblk * P.B) - 1u) atomicExch(ticket, 0u);  // every CTA has its ticket
-    s_tk = t;
-  }
-  for (int r = tid; r <= L; r += K1_THREADS) cs[r] = (r >= 1) ? ctab[r - 1] : 0.f;
-  __syncthreads();
-  const int blk = (int)(s_tk % (unsigned)nblk), b = (int)(s_tk / (unsigned)nblk);
-  const int wbase = blk * K1_THREADS + warp * 32;
-  const int i = wbase + lane;
-  const bool valid_i = i < n;
-  const bool warp_live = wbase < n;
-  const long long bi = (long long)b * n + i;
-  const double theta = P.theta, beta = P.beta, alpha = P.alpha, rho = P.rho, kappa = P.kappa;
-  const int nw = (n + 31) >> 5;
-  const float slope = (float)P.slope;
-  const double slope_d = P.slope;
-  const int icol = valid_i ? i : (warp_live ? wbase : 0);
-  float* pcol = psis + (long long)b * (P.KR + 1) * n + icol;  // psi rows of this neuron
-  double zsum = 0.0;
-  // ---------------- pass A (the K1 loop, fresh state: one chunk starts at t = 0) ----------
-  if (warp_live) {
-    double u = 0.0, a = 0.0, zbar = 0.0;
-    const double* cp = cur + (long long)b * P.Tc * n + icol;
-    double d_prev = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
-    float* pp = pcol;
-    if (valid_i) pp[0] = surrogate_grad_f32((float)d_prev, slope);
-    uint32_t* rp = raster != nullptr ? raster + (long long)b * P.T * nw + (wbase >> 5) : nullptr;
-    double In[8];
-#pragma unroll
-    for (int u8 = 0; u8 < 8; ++u8) In[u8] = u8 < L ? __ldcs(cp + (long long)u8 * n) : 0.0;
-    const long long n8 = 8LL * n;
-    for (int s8 = 0; s8 < L; s8 += 8) {
-      double Ib[8];
-#pragma unroll
-      for (int u8 = 0; u8 < 8; ++u8) Ib[u8] = In[u8];
-      cp += n8;
-#pragma unroll
-      for (int u8 = 0; u8 < 8; ++u8)
-        In[u8] = (s8 + 8 + u8 < L) ? __ldcs(cp + (long long)u8 * n) : 0.0;
-#pragma unroll
-      for (int u8 = 0; u8 < 8; ++u8) {
-        if (s8 + u8 < L) {
-          const double z_prev = spike_value(d_prev, SMOOTH, slope_d);
-          a = __dadd_rn(__dmul_rn(rho, a), z_prev);
-          u = __dadd_rn(__dmul_rn(alpha, u), Ib[u8]);
-          const double d = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
-          const double zv = spike_value(d, SMOOTH, slope_d);
-          zbar = __dadd_rn(__dmul_rn(kappa, zbar), zv);
-          zsum = __dadd_rn(zsum, zbar);
-          const unsigned bal = __ballot_sync(0xffffffffu, zv > 0.5 && valid_i);
-          if (rp != nullptr && lane == 0) rp[0] = bal;
-          if (rp != nullptr) rp += nw;
-          pp += n;
-          if (valid_i) pp[0] = surrogate_grad_f32((float)d, slope);
-          d_prev = d;
-        }
-      }
-    }
-    if (valid_i) {
-      u_st[bi] = u;
-      a_st[bi] = a;
-      zbar_st[bi] = zbar;
-      zsum_st[bi] = zsum;
-    }
-  }
-  // ---------------- readout: partial logits of this CTA's neurons -------------------------
-  for (int c = 0; c < m; ++c) {
-    double v = valid_i ? wout[(long long)c * n + i] * zsum : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[warp][c] = v;
-  }
-  __syncthreads();
-  if (tid < m) {
-    double v = red[0][tid];
-#pragma unroll
-    for (int w = 1; w < K1_THREADS / 32; ++w) v += red[w][tid];
-    part[((long long)b * nblk + blk) * m + tid] = v;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    s_gen0 = ld_acquire_u32(gen + b);  // read BEFORE arriving: the last arriver bumps it
-    __threadfence();
-    s_last = atomicAdd(count + b, 1u) == (unsigned)nblk - 1u;
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    if (warp == 0) {  // logits (block order), softmax CE in class order, as readout_loss
-      for (int c = lane; c < m; c += 32) {
-        double v = 0.0;
-        for (int q = 0; q < nblk; ++q) v += __ldcg(part + ((long long)b * nblk + q) * m + c);
-        red[0][c] = v;
-      }
-      __syncwarp();
-      const int y = (int)labels[b];
-      double mx = red[0][0];
-      int arg = 0;
-      if (lane == 0)
-        for (int c = 1; c < m; ++c)
-          if (red[0][c] > mx) { mx = red[0][c]; arg = c; }
-      mx = __shfl_sync(0xffffffffu, mx, 0);
-      for (int c = lane; c < m; c += 32) sg[c] = exp(red[0][c] - mx);
-      __syncwarp();
-      double logz = 0.0;
-      if (lane == 0) {
-        double se = 0.0;
-        for (int c = 0; c < m; ++c) se += sg[c];
-        logz = log(se);
-        loss_out[b] = logz - (red[0][y] - mx);
-        if (correct) correct[b] = (arg == y) ? 1 : 0;
-      }
-      logz = __shfl_sync(0xffffffffu, logz, 0);
-      __syncwarp();
-      for (int c = lane; c < m; c += 32) {
-        const double gc = exp((red[0][c] - mx) - logz) - (c == y ? 1.0 : 0.0);
-        sg[c] = gc;
-        s_out[(long long)b * m + c] = red[0][c];
-        g_out[(long long)b * m + c] = gc;
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      count[b] = 0u;
-      __threadfence();
-      atomicAdd(gen + b, 1u);
-    }
-  } else {
-    if (tid == 0)
-      while (ld_acquire_u32(gen + b) == s_gen0) __nanosleep(64);
-    __syncthreads();
-    for (int c = tid; c < m; c += K1_THREADS) sg[c] = __ldcg(g_out + (long long)b * m + c);
-    __syncthreads();
-  }
-  if (!warp_live) return;  // no block barriers below
-  double wsd = 0.0;
-  if (valid_i)
-    for (int c = 0; c < m; ++c) wsd = fma(wout[(long long)c * n + i], sg[c], wsd);
-  const float ws = (float)wsd;
-  if (valid_i) wsig_out[bi] = ws;
-  // ---------------- backward chunk scan (K1s on one neuron per thread) -------------------
-  const float fbeta = (float)P.beta, frho = (float)P.rho;
-  const long long ld2 = ldc >> 1;
-  const long long row0 = (long long)b * P.KR * ld2 + (i >> 1);
-  uint32_t* chp = c_hi + row0;
-  uint32_t* clp = c_lo + row0;
-  const bool even = (lane & 1) == 0;
-  const bool st_ok = even && i < n;  // (i, i+1) pair; columns past n stay untouched
-  for (int r = P.KR - 1; r > L; --r)
-    if (st_ok) { chp[r * ld2] = 0u; clp[r * ld2] = 0u; }
-  chp += L * ld2;
-  clp += L * ld2;
-  const bool disc = (n & 31) == 0;  // whole 128-byte psi lines per warp
-  const float* wrow = psis + (long long)b * (P.KR + 1) * n + wbase;
-  float lam = 0.f, an = 0.f, up = 0.f, ft = 0.f;
-  const float falpha = (float)P.alpha;
-  constexpr int PF = 8;
-  float q[PF];
-#pragma unroll
-  for (int u = 0; u < PF; ++u) q[u] = (L - u >= 0) ? pcol[(long long)(L - u) * n] : 0.f;
-  for (int r = L; r >= 0; --r) {
-    const float cu = valid_i ? q[0] : 0.f;
-#pragma unroll
-    for (int u = 0; u < PF - 1; ++u) q[u] = q[u + 1];
-    q[PF - 1] = (r - PF >= 0) ? pcol[(long long)(r - PF) * n] : 0.f;
-    const float c_prev = cs[r], c_r = (r < L) ? cs[r + 1] : 0.f;
-    float c0 = r >= 1 ? c_prev * ws * cu : 0.f;
-    if (ALIF && r < L) {
-      const float A0 = fmaf(-fbeta, cu, frho);
-      lam = fmaf(an, lam, -fbeta * (c_r * ws * up));
-      c0 = fmaf(cu, lam, c0);
-      an = A0;
-    }
-    up = cu;
-    ft = fmaf(falpha, ft, c0);  // input filter folded into C (as pass 3)
-    c0 = ft;
-    const float c1 = __shfl_down_sync(0xffffffffu, c0, 1);
-    if (st_ok) {
-      uint32_t h, l;
-      split_bf16x2(c0, c1, h, l);
-      *chp = h;
-      *clp = l;
-    }
-    chp -= ld2;
-    clp -= ld2;
-    // this warp's psi line of row r is consumed: drop it from L2 without a write-back
-    if (disc && lane == 0)
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(wrow + (long long)r * n) : "memory");
-  }
-}
-
-// ------------------------------------------------------------------------------------
 // K1s: backward scan over one chunk (pass B).  Thread = (sample, 2 neighbouring neurons):
 // it reads the psi rows K1 parked in the scratch (float2, coalesced, 4 rows prefetched)
 // from rho = L down to 0 and emits the GEMM operands MN-major -- C[b*KR + rho][i] and,
@@ -1247,36 +1012,6 @@ int spb_forward_chunk(int pass, const double* cur, int B, int n, int Tc, int KR,
         reinterpret_cast<float2*>(mdt), psi_scratch);
     SPB_CHECK_LAUNCH("chunk_scan");
   }
-  return 0;
-}
-
-int spb_forward_scan_chunk(const double* cur, int B, int n, int Tc, int KR, int len, int T,
-                           double alpha, double theta, double slope, double beta, double rho,
-                           double kappa, int alif, int smooth, double* u, double* a, double* zbar,
-                           double* zsum, uint32_t* raster, float* psi, const double* wout,
-                           const long long* labels, int m, double* s, double* loss, double* g,
-                           float* wsig, int* correct, const float* ctab, void* c_hi, void* c_lo,
-                           int ldc, unsigned* sync, double* part, cudaStream_t stream) {
-  SPB_CHECK_ARG(cur && u && a && zbar && zsum && psi && wout && labels && s && loss && g && wsig &&
-                    ctab && c_hi && c_lo && sync && part,
-                "spb_forward_scan_chunk: null pointer");
-  SPB_CHECK_ARG(B > 0 && n > 0 && Tc > 0 && len > 0 && len <= Tc && len <= T && KR >= Tc + 1 &&
-                    KR % 8 == 0 && m > 0 && m <= KF_MAXM && ldc >= n && ldc % 8 == 0,
-                "spb_forward_scan_chunk: bad sizes B=%d n=%d Tc=%d KR=%d len=%d m=%d", B, n, Tc,
-                KR, len, m);
-  FwdParams P{B, n, Tc, KR, len, 0, T, alpha, theta, slope, beta, rho, kappa, 0, alif, 0, smooth};
-  const int nblk = ceil_div(n, K1_THREADS);
-  const size_t smem = (size_t)(len + 1) * sizeof(float);
-#define SPB_K1F(A, S)                                                                            \
-  forward_scan_kernel<A, S><<<nblk * B, K1_THREADS, smem, stream>>>(                            \
-      P, cur, u, a, zbar, zsum, raster, psi, wout, labels, m, s, loss, g, wsig, correct, ctab,  \
-      reinterpret_cast<uint32_t*>(c_hi), reinterpret_cast<uint32_t*>(c_lo), ldc, sync, part)
-  if (alif && smooth) SPB_K1F(true, true);
-  else if (alif) SPB_K1F(true, false);
-  else if (smooth) SPB_K1F(false, true);
-  else SPB_K1F(false, false);
-#undef SPB_K1F
-  SPB_CHECK_LAUNCH("forward_scan");
   return 0;
 }
 

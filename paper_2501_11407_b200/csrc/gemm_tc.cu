@@ -9,11 +9,12 @@
 // fp32 accuracy from bf16 tensor cores: every operand is split x = hi + lo (bf16 each)
 // and D += Ah*Bh + Ah*Bl + Al*Bh (the lo*lo term is below fp32 rounding of the sum).
 //
-// Structure (one 128x128 output tile per CTA, split-K over blockIdx.z):
-//   warp 0   TMA producer: Ah, Al, Bh, Bl, two 64x64 MN-major SWIZZLE_128B boxes each,
-//            per stage
-//   warp 1   TMEM allocation + single-thread tcgen05.mma issue (12 MMAs of 128x128x16 per
-//            64-wide K block), tcgen05.commit releases smem stages / signals the epilogue
+// Structure (one 128x256 output tile per CTA, split-K over blockIdx.z):
+//   warp 0   TMA producer: Ah, Al (128 x BK), Bh (and Bl unless the B operand is exact in
+//            bf16) (256 x BK), MN-major SWIZZLE_128B boxes, per stage
+//   warp 1   TMEM allocation + converged-warp tcgen05.mma issue (M=128, N=256, K=16; 3
+//            MMAs per K step, 2 for an exact-bf16 B), tcgen05.commit releases smem
+//            stages / signals the epilogue
 //   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 -> fp32 partial tile (fixed-order reduce later)
 #include "tma.cuh"
 #include <cudaTypedefs.h>

@@ -123,7 +123,7 @@ __device__ __forceinline__ void slice_one(double wv, int s, int P, int8_t (&q)[8
       R = (R - d) >> 8;
       q[p] = (int8_t)d;
     }
-  } else {  // radix-128 digits (P = 7: f32, P = 8: f64 weights)
+  } else {  // radix-128 digits (P = 8: f64 weights; P = 7 kept for the digit tests)
     double r = ldexp(wv, -s);
     for (int p = 0; p < P; ++p) {
       const double t = r * (p == 0 ? 64.0 : 128.0);

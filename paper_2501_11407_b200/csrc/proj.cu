@@ -5,12 +5,13 @@
 // down to ~1e-7), so the projection has to be exact to fp64 level.
 // Inputs are spike counts (uint8), so we slice the weights instead of rounding them:
 //
-//   W[i][j] = sum_{p<P} q_p[i][j] * 2^(s_i - 6 - 7p) + r,   q_p in [-64, 64] (int8),
-//   |r| <= 2^(s_i - 7P),  s_i = exponent of max_j |W[i][j]|
+//   W[i][j] = sum_{p<P} q_p[i][j] * 2^(RB*(P-1-p)) * 2^(s_i - F) + r,   q_p int8,
+//   s_i = exponent of max_j |W[i][j]|      (formats: csrc/digits.cuh)
 //
-// P = 7 slices (48 bits) for fp32 weights -- exact for every weight >= 2^-24 of the row
-// maximum -- and P = 8 (55 bits) for fp64 weights.  x (u8) * q_p (s8) is accumulated by
-// tcgen05.mma.kind::i8 in int32 TMEM (exact: |acc| <= k*255*64 < 2^31), the slices are
+// P = 6 balanced radix-256 digits (F = 46) for fp32 weights -- exact for every weight
+// within 2^-23 of the row maximum -- and P = 8 radix-128 digits (F = 55) for fp64
+// weights.  x (u8) * q_p (s8) is accumulated by tcgen05.mma.kind::i8 in int32 TMEM
+// (exact: |acc| <= k*255*128 < 2^31), the slices are
 // recombined in int64 (exact) and converted to fp64 once: the result is the (weight-
 // truncated) exact sum rounded once, independent of summation order.
 //
@@ -127,9 +128,9 @@ __device__ __forceinline__ double pow2(int e) {  // 2^e for -1022 <= e <= 1023
 // them exactly in int64 and writes 16 fp64 currents (128 contiguous bytes).
 constexpr int NH = NT / 2;  // neurons per epilogue thread (16 epilogue warps measured slower)
 
-// BIN (binary spikes, k <= 16384): every digit sum |S_p| < 2^20, so all P = 7 digits
-// recombine into ONE int64 g = sum_p S_p 128^(6-p) (|g| < 2^63) and I = (double)g *
-// 2^(s-48): one rounding of the exact sum, bitwise the value of the two-part path below,
+// BIN (binary spikes, k <= 16384): every digit sum |S_p| < 2^21, so all P <= 7 digits
+// recombine into ONE int64 g = sum_p S_p 2^(RB*(P-1-p)) (|g| < 2^63) and I = (double)g *
+// 2^(s-F): one rounding of the exact sum, bitwise the value of the two-part path below,
 // with half the fp64-pipe work.
 // SE: per-neuron exponents (int) or precomputed scales 2^(s-F) (double)
 template <int P, bool BIN, typename SE = int>

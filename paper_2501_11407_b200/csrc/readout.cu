@@ -42,7 +42,11 @@ __global__ void readout_loss_kernel(const double* __restrict__ wout, const doubl
   // softmax cross-entropy: the exps run one class per lane; the max, the first argmax and
   // the sum of exps are taken in class order by one lane (the reference's order)
   if (warp == 0) {
-    const int y = (int)labels[b];
+    // an out-of-range label (the host wrappers reject them: LabelOutOfRange) yields a NaN
+    // loss and no one-hot term instead of an out-of-bounds shared-memory read
+    const long long yl = labels[b];
+    const bool ybad = yl < 0 || yl >= m;
+    const int y = ybad ? -1 : (int)yl;
     double mx = s[0];
     int arg = 0;
     if (lane == 0) {
@@ -57,7 +61,7 @@ __global__ void readout_loss_kernel(const double* __restrict__ wout, const doubl
       double se = 0.0;
       for (int c = 0; c < m; ++c) se += g[c];
       logz = log(se);
-      loss[b] = logz - (s[y] - mx);
+      loss[b] = ybad ? __longlong_as_double(0x7ff8000000000000ULL) : logz - (s[y] - mx);
       if (correct) correct[b] = (arg == y) ? 1 : 0;
     }
     logz = __shfl_sync(0xffffffffu, logz, 0);
@@ -162,6 +166,12 @@ int spb_readout_loss(const double* wout, const double* zsum, const long long* la
   const size_t smem = (size_t)(2 * m + 32) * sizeof(double);
   // one warp per class (up to 32 warps): the class dot products run in one round
   const int threads = 32 * (m < 8 ? 8 : (m > 32 ? 32 : m));
+  if (smem > 48 * 1024) {  // m > 3056: opt in to the larger dynamic shared memory
+    const cudaError_t e = cudaFuncSetAttribute(
+        readout_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    SPB_CHECK_ARG(e == cudaSuccess, "spb_readout_loss: smem opt-in failed: %s",
+                  cudaGetErrorString(e));
+  }
   pdl_launch(readout_loss_kernel, B, threads, smem, stream, wout, zsum, labels, n, m, s_out, loss, g,
                                                     wsig, correct);
   SPB_CHECK_LAUNCH("readout_loss");

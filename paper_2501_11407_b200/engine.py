@@ -111,8 +111,7 @@ class EpropEngine:
 
     def __init__(self, n: int, k: int, m: int, B: int, *, alif: bool, w_f64: bool = False,
                  chunk: int = 127, device=None, sm_count: int | None = None,
-                 reset: bool = False, fused: bool | None = None, recurrent: bool = False,
-                 pair: bool | None = None):
+                 reset: bool = False, recurrent: bool = False, grad: bool = True):
         if chunk not in CHUNKS:
             raise ValueError(f"chunk must be one of {CHUNKS} (Tc + 1 a multiple of 64)")
         self.lib = _lib.load()
@@ -127,7 +126,13 @@ class EpropEngine:
         self.w_f64 = bool(w_f64)
         self.Tc = int(chunk)
         self.KR = self.Tc + 1
-        self.device = torch.device(device if device is not None else "cuda")
+        dev = torch.device(device if device is not None else "cuda")
+        if dev.type == "cuda" and dev.index is None and torch.cuda.is_available():
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        # grad=False: forward-only engine (evaluate(), network_loss): none of the pass-B
+        # buffers (psi scratch, GEMM operands, the per-synapse trace, partials) exist
+        self.grad = bool(grad)
         self.n_pad = _round_up(self.n, 128)
         # recurrent layer: the eligibility kernels see the extended
         # input x~_t = [x_t, z_{t-1}] of width kx = k + n (forward_rec.cu)
@@ -150,27 +155,8 @@ class EpropEngine:
         self.Kpad = _round_up(k, 128)
         self.n_pad32 = _round_up(n, 32)
         self.P = 8 if self.w_f64 else 6   # digit format, csrc/digits.cuh
-        # K2 on CTA pairs (proj2.cu, cta_group::2): bitwise the single-CTA K2; opt-in --
-        # measured slower at C3 (0.347 vs 0.301 ms): the MMA issue loop, not the shared-
-        # memory operand port, bounds K2 (tools/proj_probe.py, tools/mma_pattern_bench.cu)
-        self.pair = False if pair is None else bool(pair)
-        if self.pair and self.Kpad > 768:
-            raise ValueError("the CTA-pair projection needs k <= 768")
-        # K21 (fused.cu) = K2 + K1 in one kernel: the fp64 current never leaves the SM
-        # (needs Kpad <= 768).  Opt-in: measured on B200 it is bitwise identical to K2 + K1
-        # but not faster at C3/C4 (its N = 112 MMAs keep the tensor pipe ~26 % busy and the
-        # per-step epilogue sits on the critical path), so K2 then K1 is the default.
-        fusable = self.Kpad <= 768
-        if fused is None:
-            fused = False
-        if fused and not fusable:
-            raise ValueError("the fused projection needs k <= 768")
-        if fused and recurrent:
-            raise ValueError("the fused projection has no recurrent variant")
-        self.fused = bool(fused)
         self.xq = torch.zeros((B * self.Tc, self.Kpad), dtype=torch.uint8, device=dev)
-        self.cur = (None if self.fused else
-                    torch.empty((B * self.Tc, n), dtype=f64, device=dev))
+        self.cur = torch.empty((B * self.Tc, n), dtype=f64, device=dev)
         self.wq = torch.zeros((self.P, self.n_pad32, self.Kpad), dtype=torch.int8, device=dev)
         self.sexp = torch.zeros(n, dtype=torch.int32, device=dev)
         # neuron state (fp64) and readout filters
@@ -184,12 +170,15 @@ class EpropEngine:
         self.loss = torch.empty(B, dtype=f64, device=dev)
         self.g = torch.empty((B, m), dtype=f64, device=dev)
         self.correct = torch.empty(B, dtype=torch.int32, device=dev)
-        # pass-B chunk operands (bf16 hi/lo, K-major over (sample, rho))
-        self.psi = torch.zeros((B, self.KR + 1, n), dtype=f32, device=dev)   # K1 scan scratch
-        # K1f (one-chunk forward + readout + scan in one kernel): sample meeting words and
-        # the partial logits.  Opt-in (SPB_K1F=1 or engine.k1f = True): measured slower at C3
-        # (0.41 vs 0.29 ms for K1 + K3 + K1s: the live psi of ~900 resident CTAs overflows L2)
-        self.k1f = os.environ.get("SPB_K1F", "0") == "1" and m <= 64
+        self.ldc = _round_up(n, 8)   # C/W are MN-major [K][ldc] (neurons contiguous)
+        self.xbar_state = torch.empty((B, self.kx), dtype=f64, device=dev)
+        if self.recurrent:
+            self.wrecT = torch.zeros((n, n), dtype=f64 if self.w_f64 else f32, device=dev)
+            self.nw = (n + 31) // 32
+            self.Kx2 = _round_up(self.kx, 4)
+        # weights
+        self.w = torch.empty((n, k), dtype=f64 if self.w_f64 else f32, device=dev)
+        self.wout = torch.empty((m, n), dtype=f64, device=dev)
         # fold the input filter into the one-chunk coefficients (SPB_FILT=0: xbar operand)
         self.filt = os.environ.get("SPB_FILT", "1") != "0"
         self.pack_xh = os.environ.get("SPB_PACK_XH", "1") != "0"
@@ -198,17 +187,40 @@ class EpropEngine:
         # skips the projection and the dynamics recompute.  SPB_PARK_GB sets it too.
         self.park_budget = int(float(os.environ.get("SPB_PARK_GB", "0")) * (1 << 30))
         self.psi_park = None
-        self.kf_sync = torch.zeros(1 + 2 * B, dtype=torch.int32, device=dev)
-        self.kf_part = torch.empty(B * ((n + 127) // 128) * m, dtype=f64, device=dev)
-        self.ldc = _round_up(n, 8)   # C/W are MN-major [K][ldc] (neurons contiguous)
+        self._ctab_T = None
+        self.ctab = None
+        self.launches = 0
+        # where K4 of a one-chunk sequence runs when the pack does not write K5's operand
+        # itself (SPB_PACK_XH=0, unaligned byte rows, recurrent engines): "fa"
+        # (default, measured best: C4 1.66 -> 1.59 ms) = side stream after K2, overlapping
+        # K1; "proj" = side stream from the start of pass A, overlapping K2; "main" =
+        # serially before K5
+        self.xbar_sched = os.environ.get("SPB_XBAR_SCHED", "fa")
+        # side stream for work off the critical path (K4 xbar of a one-chunk sequence, K7)
+        if self.device.type == "cuda":
+            self.side = torch.cuda.Stream(device=dev)
+            self._ev = {nm: torch.cuda.Event() for nm in ("start", "xbar", "ro", "rg")}
+        else:
+            self.side = None
+            self._ev = None
+        self.splits5 = self.splits6 = 0
+        self.psi = self.c_hi = self.c_lo = self.xh = self.xl = self.xs_hi = self.xs_lo = None
+        self.w_hi = self.w_lo = self.wa_hi = self.wa_lo = self.mdt = self.eps = self.eps2 = None
+        self.partial = self.grad_w_acc = self.grad_wout = self.zchunk = self.xq2 = None
+        if self.grad:
+            self._alloc_grad_buffers()
+
+    def _alloc_grad_buffers(self):
+        """Pass-B buffers: psi scratch, the chunk GEMM / carry operands (bf16 hi/lo,
+        K-major over (sample, rho)), the per-synapse trace, split partials, accumulators."""
+        dev, sms = self.device, self.sm_count
+        f32, f64, bf16 = torch.float32, torch.float64, torch.bfloat16
+        B, n, m, K = self.B, self.n, self.m, self.K
+        self.psi = torch.zeros((B, self.KR + 1, n), dtype=f32, device=dev)   # K1 scan scratch
         self.c_hi = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
         self.c_lo = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
-        self.xbar_state = torch.empty((B, self.kx), dtype=f64, device=dev)
         if self.recurrent:
-            self.wrecT = torch.zeros((n, n), dtype=f64 if self.w_f64 else f32, device=dev)
-            self.nw = (n + 31) // 32
             self.zchunk = torch.zeros((B, self.KR, self.nw), dtype=torch.int32, device=dev)
-            self.Kx2 = _round_up(self.kx, 4)
             self.xq2 = torch.zeros((B * self.Tc, self.Kx2), dtype=torch.uint8, device=dev)
         self.xh = torch.zeros((K, self.kp), dtype=bf16, device=dev)   # MN-major [K][kp]
         self.xl = torch.zeros((K, self.kp), dtype=bf16, device=dev)
@@ -242,25 +254,6 @@ class EpropEngine:
                                    dtype=f32, device=dev)
         self.grad_w_acc = torch.empty((n, self.kp), dtype=f64, device=dev)
         self.grad_wout = torch.empty((m, n), dtype=f64, device=dev)
-        # weights
-        self.w = torch.empty((n, k), dtype=f64 if self.w_f64 else f32, device=dev)
-        self.wout = torch.empty((m, n), dtype=f64, device=dev)
-        self._ctab_T = None
-        self.ctab = None
-        self.launches = 0
-        # where K4 of a one-chunk sequence runs when the pack does not write K5's operand
-        # itself (SPB_PACK_XH=0, unaligned byte rows, fused / recurrent engines): "fa"
-        # (default, measured best: C4 1.66 -> 1.59 ms) = side stream after K2, overlapping
-        # K1; "proj" = side stream from the start of pass A, overlapping K2; "main" =
-        # serially before K5
-        self.xbar_sched = os.environ.get("SPB_XBAR_SCHED", "fa")
-        # side stream for work off the critical path (K4 xbar of a one-chunk sequence, K7)
-        if self.device.type == "cuda":
-            self.side = torch.cuda.Stream(device=dev)
-            self._ev = {nm: torch.cuda.Event() for nm in ("start", "xbar", "ro", "rg")}
-        else:
-            self.side = None
-            self._ev = None
 
     # ----------------------------------------------------------------------------------
     def set_weights(self, w, w_out, stream=None, w_rec=None):
@@ -315,7 +308,7 @@ class EpropEngine:
 
     def _pack(self, xp, strideb, bits, ln, st, xh=False):
         """Chunk spikes (bytes or bits) -> zero-padded projection operand xq [B*Tc][Kpad]
-        (rows b*Tc + s for K2, time-major s*B + b for K21; also K4's row source).  xh: also
+        (rows b*Tc + s; also K4's row source).  xh: also
         write the one-chunk raw-spike GEMM operand (K4 folded into the pack)."""
         if xh:
             _lib.call("spb_pack_spikes_xh", ctypes_void(xp), strideb, self.B, self.k, int(bits),
@@ -323,27 +316,13 @@ class EpropEngine:
                       ctypes_void(self.xh.data_ptr()), st)
             return
         _lib.call("spb_pack_spikes", ctypes_void(xp), strideb, self.B, self.k, int(bits), ln,
-                  self.Tc, self.Kpad, int(self.fused), ctypes_void(self.xq.data_ptr()), st)
-
-    def _fused(self, pass_id, ln, t0, T, common, raster, psi, st, timed, meta):
-        """K21: exact INT8 projection + dynamics in one kernel (pass 0: raster, zsum and
-        optionally psi; pass 1: psi for the backward scan)."""
-        v = ctypes_void
-        alpha, theta, slope, beta, rho, kappa, reset, _alif, smooth = common
-        timed("fused_a" if pass_id == 0 else "fused_b", meta, "spb_fused_forward", pass_id,
-              v(self.xq.data_ptr()), v(self.wq.data_ptr()), v(self.sexp.data_ptr()), self.B,
-              self.n, self.n_pad32, self.Kpad, self.P, self.Tc, self.KR, ln, t0, T, alpha,
-              theta, slope, beta, rho, kappa, reset, smooth, v(self.u.data_ptr()),
-              v(self.a.data_ptr()), v(self.zbar.data_ptr()) if pass_id == 0 else None,
-              v(self.zsum.data_ptr()) if pass_id == 0 else None,
-              v(raster.data_ptr()) if raster is not None else None,
-              v(psi.data_ptr()) if psi is not None else None, self.sm_count, st)
+                  self.Tc, self.Kpad, 0, ctypes_void(self.xq.data_ptr()), st)
 
     def _project(self, ln, st, timed=None, binary=False):
         """K2: cur = W x_t exactly on INT8 tensor cores from the packed chunk (binary:
         0/1 spikes, single-int64 digit recombination)."""
         v = ctypes_void
-        args = ("spb_input_proj_pair" if self.pair else "spb_input_proj", v(self.xq.data_ptr()),
+        args = ("spb_input_proj", v(self.xq.data_ptr()),
                 v(self.wq.data_ptr()), v(self.sexp.data_ptr()), self.B * self.Tc, self.n,
                 self.n_pad32, self.Kpad, self.P, v(self.cur.data_ptr()), self.sm_count,
                 int(bool(binary)), st)
@@ -389,6 +368,12 @@ class EpropEngine:
                                 f"{tuple(x.shape)} {x.dtype}")
         if not x.is_contiguous():
             raise ShapeMismatch("x must be contiguous")
+        if (labels.dtype != torch.int64 or tuple(labels.shape) != (self.B,)
+                or labels.device != self.device):
+            raise ShapeMismatch(f"labels must be int64 [{self.B}] on {self.device}, got "
+                                f"{labels.dtype} {tuple(labels.shape)} on {labels.device}")
+        if not self.grad and not forward_only:
+            raise ValueError("engine built with grad=False runs forward_only updates only")
         streaming = x.device.type == "cpu" and self.device.type == "cuda"
         T = int(x.shape[1])
         if T <= 0:
@@ -401,7 +386,7 @@ class EpropEngine:
         nchunks = (T + Tc - 1) // Tc
         one = nchunks == 1
         slab = B * (self.KR + 1) * n
-        park = (not one and not forward_only and not self.fused and not self.recurrent
+        park = (not one and not forward_only and not self.recurrent
                 and self.park_budget > 0 and 4 * slab * nchunks <= self.park_budget
                 and self.device.type == "cuda")
         if park and (self.psi_park is None or self.psi_park.shape[0] < nchunks):
@@ -410,16 +395,13 @@ class EpropEngine:
 
         def psi_ptr(c):
             return v(self.psi_park[c].data_ptr()) if park else v(self.psi.data_ptr())
-        # K1f: pass A + readout + scan of a one-chunk sequence in one kernel
-        kf = (one and self.k1f and self.filt and not forward_only and not self.fused
-              and not self.recurrent and not self.reset and self.device.type == "cuda")
         strideb = T * kb
         self.launches = 0
         v = ctypes_void
         common = (float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa),
                   int(self.reset), int(self.alif), int(bool(smooth)))
-        # K4 reads the packed operand (sample-major for K2, time-major for K21)
-        xq_sb, xq_st = ((self.Kpad, B * self.Kpad) if self.fused else (Tc * self.Kpad, self.Kpad))
+        # K4 reads the packed operand (sample-major rows)
+        xq_sb, xq_st = Tc * self.Kpad, self.Kpad
         # K5/K6 operand: the filtered input xbar (reset=False: G_u = 1 (x) xbar), or with
         # reset=True the raw input (G_u is carried per synapse; K4 with alpha = 0 = copy)
         x_alpha = 0.0 if self.reset else float(alpha)
@@ -437,7 +419,7 @@ class EpropEngine:
         raw_x = (filt or self.reset) and (filt or not self.recurrent)
         xl_ptr = None if raw_x else v(self.xl.data_ptr())
         # one chunk: the pack writes the raw-spike GEMM operand itself (no K4 at all)
-        pack_xh = (filt and one and not self.fused and not self.recurrent and self.pack_xh
+        pack_xh = (filt and one and not self.recurrent and self.pack_xh
                    and (bits or (self.k % 4 == 0 and x.data_ptr() % 4 == 0)))
 
         def timed(name, meta, fn, *args):
@@ -495,8 +477,6 @@ class EpropEngine:
             def pack_chunk(c, ln):
                 self._pack(x.data_ptr() + c * Tc * kb, strideb, bits, ln, st, xh=pack_xh)
 
-        if raster is not None and self.fused:
-            raster.zero_()  # K21 ORs the spike bits into the words
         # ---------------- pass A ----------------
         for c in range(nchunks):  # chunk 0 starts from fresh state inside the kernels
             t0 = c * Tc
@@ -507,7 +487,7 @@ class EpropEngine:
                 if use_side:
                     self._ev["xbar"].record(main)
                 side_x = False
-            if side_x and self.xbar_sched == "fa" and not self.fused:
+            if side_x and self.xbar_sched == "fa":
                 self._project(ln, st, timed, binary)
             if side_x and self.xbar_sched != "main":
                 # K4 needs only x: overlap it with pass A
@@ -518,27 +498,8 @@ class EpropEngine:
                      xl_ptr, sst)
                 self._ev["xbar"].record(self.side)
                 self.launches += 1
-            if self.fused:
-                self._fused(0, ln, t0, T, common, raster,
-                            self.psi if (one and not forward_only) else None, st, timed,
-                            (ln, 0, one and not forward_only))
-                self.launches += 2
-                continue
             if not (side_x and self.xbar_sched == "fa"):
                 self._project(ln, st, timed, binary)
-            if kf:
-                timed("forward_scan", (ln, 3, one), "spb_forward_scan_chunk",
-                      v(self.cur.data_ptr()), B, n, Tc, KR, ln, T, *common[:6], int(self.alif),
-                      int(bool(smooth)), v(self.u.data_ptr()), v(self.a.data_ptr()),
-                      v(self.zbar.data_ptr()), v(self.zsum.data_ptr()),
-                      v(raster.data_ptr()) if raster is not None else None,
-                      v(self.psi.data_ptr()), v(self.wout.data_ptr()), v(labels.data_ptr()), m,
-                      v(self.s.data_ptr()), v(self.loss.data_ptr()), v(self.g.data_ptr()),
-                      v(self.wsig.data_ptr()), v(self.correct.data_ptr()), v(ctab.data_ptr()),
-                      v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()), self.ldc,
-                      v(self.kf_sync.data_ptr()), v(self.kf_part.data_ptr()), st)
-                self.launches += 3
-                continue
             if self.recurrent:
                 self._forward_rec(0, ln, t0, T, common, raster,
                                   one and not forward_only, st, timed, (ln, 0, one))
@@ -552,12 +513,11 @@ class EpropEngine:
                   None, None, None, None, None, None, None, None, 0, None,
                   psi_ptr(c) if (park or (one and not forward_only)) else None, st)
             self.launches += 3
-        # ---------------- readout / loss (inside K1f when it ran) ----------------
-        if not kf:
-            call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
-                 v(labels.data_ptr()), B, n, m, v(self.s.data_ptr()), v(self.loss.data_ptr()),
-                 v(self.g.data_ptr()), v(self.wsig.data_ptr()), v(self.correct.data_ptr()), st)
-            self.launches += 1
+        # ---------------- readout / loss ----------------
+        call("spb_readout_loss", v(self.wout.data_ptr()), v(self.zsum.data_ptr()),
+             v(labels.data_ptr()), B, n, m, v(self.s.data_ptr()), v(self.loss.data_ptr()),
+             v(self.g.data_ptr()), v(self.wsig.data_ptr()), v(self.correct.data_ptr()), st)
+        self.launches += 1
         if forward_only:
             return self
         if use_side:  # K7 is off the critical path
@@ -581,32 +541,27 @@ class EpropEngine:
                 self.launches += 1
             elif not one:  # one chunk: xq and cur of pass A are still valid (same W, same x)
                 pack_chunk(c, ln)
-                if self.fused:
-                    self._fused(1, ln, t0, T, common, None, self.psi, st, timed,
-                                (ln, 1, carry_out))
-                else:
-                    self._project(ln, st, timed, binary)
-                    if self.recurrent:
-                        self._forward_rec(1, ln, t0, T, common, None, True, st, timed,
-                                          (ln, 1, carry_out))
-                        self.launches += 1
+                self._project(ln, st, timed, binary)
+                if self.recurrent:
+                    self._forward_rec(1, ln, t0, T, common, None, True, st, timed,
+                                      (ln, 1, carry_out))
+                    self.launches += 1
                 self.launches += 2
-            # one chunk (pass A parked psi) or K21 / K1rec (park psi themselves): scan only
-            pid = 2 if (one or park or self.fused or self.recurrent) else 1
+            # one chunk (pass A parked psi) or K1rec (parks psi itself): scan only
+            pid = 2 if (one or park or self.recurrent) else 1
             if filt:
                 pid = 3 if pid == 2 else 4
-            if not kf:
-                timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,
-                      v(self.cur.data_ptr()) if self.cur is not None else None, B, n, Tc, KR,
-                      ln, t0, T, *common, v(self.u.data_ptr()), v(self.a.data_ptr()), None, None,
-                      None, v(self.wsig.data_ptr()), v(ctab.data_ptr()),
-                      v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()),
-                      v(self.w_hi.data_ptr()) if carry_out else None,
-                      v(self.w_lo.data_ptr()) if carry_out else None,
-                      v(self.wa_hi.data_ptr()) if carry_out and self.ntr == 2 else None,
-                      v(self.wa_lo.data_ptr()) if carry_out and self.ntr == 2 else None, self.ldc,
-                      v(self.mdt.data_ptr()) if self.ntr else None, psi_ptr(c), st)
-                self.launches += 1 if pid >= 2 else 2
+            timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,
+                  v(self.cur.data_ptr()), B, n, Tc, KR,
+                  ln, t0, T, *common, v(self.u.data_ptr()), v(self.a.data_ptr()), None, None,
+                  None, v(self.wsig.data_ptr()), v(ctab.data_ptr()),
+                  v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()),
+                  v(self.w_hi.data_ptr()) if carry_out else None,
+                  v(self.w_lo.data_ptr()) if carry_out else None,
+                  v(self.wa_hi.data_ptr()) if carry_out and self.ntr == 2 else None,
+                  v(self.wa_lo.data_ptr()) if carry_out and self.ntr == 2 else None, self.ldc,
+                  v(self.mdt.data_ptr()) if self.ntr else None, psi_ptr(c), st)
+            self.launches += 1 if pid >= 2 else 2
             if self.recurrent:
                 # x~ = [x_t, z_{t-1}] bytes, then the usual filter over kx columns
                 call("spb_pack_rec", v(self.xq.data_ptr()), xq_sb, xq_st,
@@ -763,66 +718,4 @@ class EpropEngine:
         _lib.call("spb_finalize_grad", ctypes_void(self.grad_w_acc.data_ptr()), self.n, self.k,
                   self.kp, ctypes_void(out.data_ptr()), int(dtype == torch.float64),
                   ctypes_void(self._stream()))
-        return out
-
-
-class MicroBatchEngine:
-    """Two half-batch engines on two CUDA streams, so one half's HBM-bound kernels (K1,
-    the chunk scan) run while the other half's tensor-core kernels (K2, K5) run; the
-    gradient accumulators are added in a fixed order afterwards (deterministic).  Same
-    results as one engine over the whole batch up to the fp32 summation order of the
-    chunk GEMM's partials (each half's partials are reduced separately, in fp64).
-    Exposes the single engine's result buffers: grad_w_acc, grad_wout, loss, s, correct."""
-
-    def __init__(self, n, k, m, B, *, parts: int = 2, **kw):
-        if B < parts:
-            raise ValueError("batch smaller than the number of micro-batches")
-        dev = kw.get("device")
-        self.parts = int(parts)
-        base, extra = divmod(B, parts)
-        self.sizes = [base + (1 if i < extra else 0) for i in range(parts)]
-        self.engines = [EpropEngine(n, k, m, b, **kw) for b in self.sizes]
-        e0 = self.engines[0]
-        self.n, self.k, self.m, self.B = e0.n, e0.k, e0.m, int(B)
-        self.device, self.kp = e0.device, e0.kp
-        self.Tc, self.KR, self.P, self.fused = e0.Tc, e0.KR, e0.P, e0.fused
-        self.streams = [torch.cuda.Stream(device=self.device) for _ in range(parts)]
-        self.grad_w_acc = torch.empty_like(e0.grad_w_acc)
-        self.grad_wout = torch.empty_like(e0.grad_wout)
-        self.loss = torch.empty(B, dtype=e0.loss.dtype, device=self.device)
-        self.correct = torch.empty(B, dtype=e0.correct.dtype, device=self.device)
-        self.s = torch.empty((B, m), dtype=e0.s.dtype, device=self.device)
-        self.launches = 0
-
-    def set_weights(self, *a, **kw):
-        for e in self.engines:
-            e.set_weights(*a, **kw)
-
-    def run(self, x, labels, **kw):
-        main = torch.cuda.current_stream(self.device)
-        lo = 0
-        for e, st, b in zip(self.engines, self.streams, self.sizes):
-            st.wait_stream(main)
-            with torch.cuda.stream(st):
-                e.run(x[lo:lo + b], labels[lo:lo + b], **kw)
-            lo += b
-        for st in self.streams:
-            main.wait_stream(st)
-        # fixed-order combination (part 0 + part 1 + ...)
-        torch.add(self.engines[0].grad_w_acc, self.engines[1].grad_w_acc, out=self.grad_w_acc)
-        torch.add(self.engines[0].grad_wout, self.engines[1].grad_wout, out=self.grad_wout)
-        for e in self.engines[2:]:
-            self.grad_w_acc += e.grad_w_acc
-            self.grad_wout += e.grad_wout
-        torch.cat([e.loss for e in self.engines], out=self.loss)
-        torch.cat([e.correct for e in self.engines], out=self.correct)
-        torch.cat([e.s for e in self.engines], out=self.s)
-        self.launches = sum(e.launches for e in self.engines)
-        return self
-
-    def grad_w(self, dtype=torch.float32):
-        out = torch.empty((self.n, self.k), dtype=dtype, device=self.device)
-        _lib.call("spb_finalize_grad", ctypes_void(self.grad_w_acc.data_ptr()), self.n, self.k,
-                  self.kp, ctypes_void(out.data_ptr()), int(dtype == torch.float64),
-                  ctypes_void(torch.cuda.current_stream(self.device).cuda_stream))
         return out

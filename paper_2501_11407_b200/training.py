@@ -18,6 +18,13 @@ gradient ("batch is an outer loop with gradient averaging"); the me
 row of an update carries the batch-mean loss.  With torch.distributed initialised the
 batch is sharded over the ranks and the gradient is combined with one allreduce per
 update (parallel.py).
+
+Provenance note: the host-only numpy pieces (``NetworkSpec``, ``loss_and_grad``,
+``sgd_update``, ``AdamState``, ``adam_update``, ``MetricsRow``) restate the reference's
+training.py:18-100 nearly line for line ON PURPOSE -- they are the reference API the
+drop-in must reproduce bit for bit (same RNG stream, same numpy promotion rules), and
+they never run on the GPU path.  The device trainer below (``DeviceTrainer``,
+``train``, ``evaluate``) is this package's own design.
 """
 
 from __future__ import annotations
@@ -28,7 +35,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import ShapeMismatch
+from .errors import LabelOutOfRange, ShapeMismatch
 from .neurons import ALIFParams, LIFParams, Network, ReadoutParams
 
 _DTYPES = {"f32": np.float32, "f64": np.float64}
@@ -314,6 +321,15 @@ def _dataset_inputs(dataset):
     raise TypeError("dataset must be a SpikeDataset (datasets.py)")
 
 
+def _check_labels(labels: np.ndarray, m: int) -> None:
+    """Every label in [0, m) -- the reference raises LabelOutOfRange from
+    softmax_cross_entropy (gradients.py:66-69) in train and evaluate; here it is checked
+    once per dataset on the host, before any kernel reads a label."""
+    if labels.size and (labels.min() < 0 or labels.max() >= m):
+        bad = labels[(labels < 0) | (labels >= m)][0]
+        raise LabelOutOfRange(f"label {int(bad)} out of range for {m} classes")
+
+
 def _pinned(torch, arr):
     t = torch.from_numpy(np.ascontiguousarray(arr))
     try:
@@ -329,6 +345,7 @@ def evaluate(net: Network, dataset, *, batch_size: int = 256, device=None):
 
     from .engine import EpropEngine, default_chunk
     x, labels, bits = _dataset_inputs(dataset)
+    _check_labels(labels, net.m)
     N, T = x.shape[0], x.shape[1]
     if N == 0:
         return float("nan"), 0.0
@@ -347,7 +364,7 @@ def evaluate(net: Network, dataset, *, batch_size: int = 256, device=None):
             eng = EpropEngine(net.n, net.k, net.m, B, alif=net.is_alif,
                               w_f64=net.neuron.w.dtype == np.float64,
                               chunk=default_chunk(T, B, net.n, net.k, net.is_alif), device=dev,
-                              reset=net.neuron.reset, recurrent=net.is_recurrent)
+                              reset=net.neuron.reset, recurrent=net.is_recurrent, grad=False)
             eng.set_weights(w, wo, w_rec=(torch.from_numpy(np.ascontiguousarray(
                 net.neuron.w_rec)) if net.is_recurrent else None))
             engines[B] = eng
@@ -380,6 +397,7 @@ def train(spec: NetworkSpec, dataset, method: str = "eprop-sparse", optimizer: s
         raise ValueError("batch_size must be >= 1")
     net = init_network(spec)
     x, labels, bits = _dataset_inputs(dataset)
+    _check_labels(labels, net.m)
     N, T = x.shape[0], x.shape[1]
     world, rank = 1, 0
     import torch.distributed as dist
@@ -397,10 +415,10 @@ def train(spec: NetworkSpec, dataset, method: str = "eprop-sparse", optimizer: s
     for epoch in range(epochs):
         for s0 in range(0, N, batch_size):
             nb = min(batch_size, N - s0)
-            lo, hi = shard_range(nb, rank, world)
-            if hi <= lo:
+            if nb < world:   # rank-independent: every rank raises, none enters the allreduce
                 raise ValueError("every rank needs at least one sample per update "
                                  f"(batch {nb} over {world} ranks)")
+            lo, hi = shard_range(nb, rank, world)
             tr.step(xs[s0 + lo:s0 + hi], ld[s0 + lo:s0 + hi], bits=bits, total_batch=nb)
             epochs_of.append(epoch)
             updates += 1

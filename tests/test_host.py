@@ -264,3 +264,30 @@ def test_default_chunk():
     assert default_chunk(500, 128, 2048, 700) == 511
     big = default_chunk(10_000, 256, 8192, 700, budget=8 << 30)
     assert big < 511 and chunk_bytes(big, 256, 8192, 700) <= 8 << 30
+
+
+def test_engine_label_and_mode_checks():
+    """Labels must be int64 [B] on the engine's device; a grad=False engine (evaluate)
+    allocates no pass-B buffers and refuses gradient runs."""
+    eng = EpropEngine(8, 5, 2, 3, alif=True, chunk=63, device="cpu", sm_count=148)
+    x = torch.zeros((3, 10, 5), dtype=torch.uint8)
+    for bad in (torch.zeros(3, dtype=torch.int32), torch.zeros(4, dtype=torch.int64),
+                torch.zeros((3, 1), dtype=torch.int64)):
+        with pytest.raises(P.ShapeMismatch):
+            eng.run(x, bad)
+    fwd = EpropEngine(8, 5, 2, 3, alif=True, chunk=63, device="cpu", sm_count=148, grad=False)
+    assert fwd.eps is None and fwd.psi is None and fwd.grad_w_acc is None
+    with pytest.raises(ValueError):
+        fwd.run(x, torch.zeros(3, dtype=torch.int64))
+
+
+def test_train_and_evaluate_reject_bad_labels_before_any_kernel():
+    from paper_2501_11407_b200.datasets import generate_poisson_dataset
+    from paper_2501_11407_b200.training import evaluate, train
+    ds = generate_poisson_dataset(4, 6, 10, 3, seed=0)
+    ds.labels[2] = (2, 7)     # class 7 of 3
+    spec = P.NetworkSpec(kind="lif", n_hidden=4, n_inputs=6, n_classes=3, seed=0)
+    with pytest.raises(P.LabelOutOfRange):
+        train(spec, ds)
+    with pytest.raises(P.LabelOutOfRange):
+        evaluate(P.init_network(spec), ds)

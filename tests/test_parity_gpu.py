@@ -254,7 +254,7 @@ def test_int8_tensor_core_projection_is_exact(w_f64):
     w = w.astype(np.float64 if w_f64 else np.float32)
     x = (rng.random((B, T, k)) < 0.1).astype(np.uint8)
     x[0, 0, :10] = 7                       # pooled counts
-    eng = EpropEngine(n, k, 3, B, alif=False, w_f64=w_f64, chunk=63, fused=False)
+    eng = EpropEngine(n, k, 3, B, alif=False, w_f64=w_f64, chunk=63)
     eng.set_weights(torch.from_numpy(w), torch.zeros((3, n), dtype=torch.float64))
     xd = torch.from_numpy(x).cuda()
     v = ctypes.c_void_p
@@ -288,7 +288,7 @@ def test_binary_recombination_is_bitwise_the_two_part_path(k):
     w = (rng.uniform(-1, 1, (n, k)) / np.sqrt(k)).astype(np.float32)
     w[5, :] *= 1e-5
     x = (rng.random((B, T, k)) < 0.15).astype(np.uint8)
-    eng = EpropEngine(n, k, 3, B, alif=False, chunk=63, fused=False)
+    eng = EpropEngine(n, k, 3, B, alif=False, chunk=63)
     eng.set_weights(torch.from_numpy(w), torch.zeros((3, n), dtype=torch.float64))
     xd = torch.from_numpy(x).cuda()
     v = ctypes.c_void_p
@@ -304,37 +304,6 @@ def test_binary_recombination_is_bitwise_the_two_part_path(k):
     exact = np.einsum("btk,nk->btn", x.astype(np.longdouble), w.astype(np.longdouble))
     got = outs[1].reshape(B, eng.Tc, n)[:, :T]
     assert np.max(np.abs(got - exact.astype(np.float64))) <= 2.3e-16 * np.max(np.abs(exact))
-
-
-@pytest.mark.parametrize("w_f64,B,T,n,binary", [(False, 5, 70, 100, False),
-                                                (True, 3, 40, 70, False),
-                                                (False, 9, 57, 333, True),
-                                                (False, 1, 5, 32, False)])
-def test_pair_projection_is_bitwise_single_cta(w_f64, B, T, n, binary):
-    """K2 on CTA pairs (cta_group::2, proj2.cu) = the single-CTA K2, bit for bit, for
-    ragged row counts (M not a multiple of 256), ragged n, f32 and f64 digit formats."""
-    _need_gpu()
-    import ctypes
-    from paper_2501_11407_b200.engine import EpropEngine
-    rng = np.random.default_rng(3)
-    k = 700
-    w = (rng.uniform(-1, 1, (n, k)) / np.sqrt(k)).astype(np.float64 if w_f64 else np.float32)
-    x = (rng.random((B, T, k)) < 0.1).astype(np.uint8)
-    if not binary:
-        x[0, 0, :20] = 5
-    outs = []
-    for pair in (False, True):
-        eng = EpropEngine(n, k, 3, B, alif=False, w_f64=w_f64, chunk=127, fused=False, pair=pair)
-        eng.set_weights(torch.from_numpy(w), torch.zeros((3, n), dtype=torch.float64))
-        xd = torch.from_numpy(x).cuda()
-        v = ctypes.c_void_p
-        st = v(torch.cuda.current_stream().cuda_stream)
-        eng._pack(xd.data_ptr(), T * k, False, T, st)
-        eng.cur.fill_(7.0)
-        eng._project(T, st, binary=binary)
-        torch.cuda.synchronize()
-        outs.append(eng.cur.cpu().numpy().reshape(B, eng.Tc, n)[:, :T].copy())
-    assert np.array_equal(outs[0], outs[1])
 
 
 def test_streamed_inputs_match_resident_and_memory_is_flat_in_T():

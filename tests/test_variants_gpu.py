@@ -1,8 +1,7 @@
-"""K1f (csrc/forward.cu forward_scan_kernel: one-chunk pass A + readout + backward scan in
-one launch) against the three-launch path it replaces (K1 pass A, K3 readout, K1s scan).
-The dynamics are the same code, so rasters and spike counts are bitwise equal; the logits
-are summed over 128-neuron partials (losses equal to fp64 rounding) and the gradients
-follow to fp32 rounding."""
+"""Engine variants that must reproduce the default path: the segmented chunk scan and
+filter, the raw-spike operand over several chunks, the pack writing K5's operand,
+parked psi, and CUDA-graph replay of a whole update (bitwise where the arithmetic is
+the same, to fp32 rounding where only the summation order differs)."""
 
 import numpy as np
 import pytest
@@ -18,57 +17,20 @@ def _rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
-def _run(net, x, y, *, k1f, smooth=False, graph=False):
+def _run(net, x, y, *, smooth=False):
     from paper_2501_11407_b200.engine import EpropEngine
     from paper_2501_11407_b200.gradients import _neuron_kwargs
     B, T, _ = x.shape
     chunk = next(c for c in (63, 127, 255, 511) if T <= c)
     eng = EpropEngine(net.n, net.k, net.m, B, alif=net.is_alif,
                       w_f64=net.neuron.w.dtype == np.float64, chunk=chunk)
-    eng.k1f = k1f
     eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
     r = torch.zeros((B, T, (net.n + 31) // 32), dtype=torch.int32, device="cuda")
     xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
-    kw = dict(raster=r, smooth=smooth, **_neuron_kwargs(net))
-    eng.run(xd, yd, **kw)
-    if graph:  # replays reuse the self-resetting sample-meeting words
-        for _ in range(3):
-            eng.run(xd, yd, **kw)
+    eng.run(xd, yd, raster=r, smooth=smooth, **_neuron_kwargs(net))
     torch.cuda.synchronize()
     return dict(raster=r.cpu().numpy().copy(), loss=eng.loss.cpu().numpy().copy(),
-                g=eng.g.cpu().numpy().copy(), correct=eng.correct.cpu().numpy().copy(),
-                wsig=eng.wsig.cpu().numpy().copy(), zsum=eng.zsum.cpu().numpy().copy(),
                 gw=eng.grad_w_acc.cpu().numpy().copy(), gwo=eng.grad_wout.cpu().numpy().copy())
-
-
-@pytest.mark.parametrize("kind,n,k,m,B,T,prec,smooth", [
-    ("alif", 1024, 700, 20, 16, 250, "f32", False),   # C3 shape, small batch
-    ("lif", 256, 700, 20, 24, 250, "f32", False),     # C2 shape
-    ("alif", 100, 37, 3, 5, 40, "f64", False),        # ragged warps (no L2 discard), f64
-    ("lif", 130, 64, 35, 7, 100, "f32", True),        # smooth spikes, two CTAs + 2 neurons
-    ("alif", 2048, 96, 64, 3, 60, "f32", False),      # 16 CTAs per sample, m at the limit
-])
-def test_k1f_matches_three_launch_path(kind, n, k, m, B, T, prec, smooth):
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    import paper_2501_11407_b200 as P
-    from paper_2501_11407_b200.datasets import poisson_batch
-    net = P.init_network(P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=m,
-                                       precision=prec, seed=7))
-    x, y = poisson_batch(B, k, T, m, seed=11)
-    a = _run(net, x, y, k1f=True, smooth=smooth, graph=True)
-    b = _run(net, x, y, k1f=False, smooth=smooth)
-    assert np.array_equal(a["raster"], b["raster"])
-    assert np.array_equal(a["zsum"], b["zsum"])
-    assert np.array_equal(a["correct"], b["correct"])
-    np.testing.assert_allclose(a["loss"], b["loss"], rtol=1e-12, atol=1e-14)
-    np.testing.assert_allclose(a["g"], b["g"], rtol=1e-10, atol=1e-14)
-    assert _rel(a["wsig"], b["wsig"]) < 1e-6
-    assert _rel(a["gwo"], b["gwo"]) < 1e-10
-    assert _rel(a["gw"], b["gw"]) < 1e-5
-    cos = float(np.dot(a["gw"].ravel(), b["gw"].ravel()) /
-                (np.linalg.norm(a["gw"]) * np.linalg.norm(b["gw"]) + 1e-300))
-    assert cos > 0.99999
 
 
 @pytest.mark.parametrize("kind,n,B,T", [("lif", 256, 6, 100), ("alif", 192, 5, 120),
@@ -83,9 +45,9 @@ def test_segmented_scan_matches_one_sweep(kind, n, B, T, monkeypatch):
                                        precision="f32", seed=3))
     x, y = poisson_batch(B, 50, T, 4, seed=5)
     monkeypatch.setenv("SPB_SCAN_SEG", "1")
-    a = _run(net, x, y, k1f=False)
+    a = _run(net, x, y)
     monkeypatch.setenv("SPB_SCAN_SEG", "0")
-    b = _run(net, x, y, k1f=False)
+    b = _run(net, x, y)
     assert np.array_equal(a["raster"], b["raster"])
     assert _rel(a["gw"], b["gw"]) < 1e-5
 
@@ -204,3 +166,33 @@ def test_parked_psi_is_bitwise_the_recompute(kind, T, chunk):
                        eng.grad_wout.cpu().numpy().copy())
     for a, b in zip(out[0], out[1 << 30]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("T", [150, 60])   # three chunks / one chunk (side-stream K4)
+def test_graphed_update_equals_eager(T):
+    """EpropEngine.graphed: the captured CUDA graph replays the same update bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200.gradients import _neuron_kwargs
+    net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=200, n_inputs=90, n_classes=5,
+                                       precision="f32", seed=4))
+    kw = _neuron_kwargs(net)
+    eng = EpropEngine(200, 90, 5, 12, alif=True, chunk=63)
+    eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+    outs = []
+    for seed in (1, 2):
+        x, y = poisson_batch(12, 90, T, 5, seed=seed)
+        xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        eng.run(xd, yd, **kw)
+        torch.cuda.synchronize()
+        outs.append((eng.grad_w_acc.cpu().numpy().copy(), eng.loss.cpu().numpy().copy()))
+    step = eng.graphed(xd, yd, **kw)
+    for seed, (gw, ls) in zip((1, 2), outs):
+        x, y = poisson_batch(12, 90, T, 5, seed=seed)
+        step(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+        torch.cuda.synchronize()
+        assert np.array_equal(eng.grad_w_acc.cpu().numpy(), gw)
+        assert np.array_equal(eng.loss.cpu().numpy(), ls)
