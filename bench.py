@@ -203,35 +203,98 @@ def parity_block(eng, net, x_np, y_np, kw, kind, recurrent=False):
     return out
 
 
-def cpu_reference_line(args, cfg_name):
-    """--impl reference: the reference algorithm (oracle port) on the host cores."""
-    from oracle.cpu_bench import _pool, cores, time_cpu
-    kind, n, k, m, T, B = CONFIGS[cfg_name]
+def dropin_e2e(P, net, x_np, y_np, chunk, calls=6):
+    """The drop-in call a reference user makes, timed end to end on the host clock:
+    ``eprop_batch_gradient(net, x, labels)`` with numpy uint8 spike counts in and numpy
+    gradients out (and the same with bit-packed spikes, ``packed=True``).  Every call
+    includes the host staging, the host-to-device input copy, the update and the
+    device-to-host copies of the gradients, losses and readouts."""
+    import torch
+    from paper_2501_11407_b200.gradients import eprop_batch_gradient
+    B, T, k = x_np.shape
+    n, m = net.n, net.m
+    out = {"input": "numpy uint8 spike counts [B, T, k]", "unit": UNIT}
+    xb = np.packbits(x_np, axis=-1, bitorder="little")
+    for tag, xin, kw in (("counts", x_np, {}), ("packed", xb, {"packed": True})):
+        for _ in range(2):
+            eprop_batch_gradient(net, xin, y_np, chunk=chunk, **kw)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(calls):
+            r = eprop_batch_gradient(net, xin, y_np, chunk=chunk, **kw)
+        dt = (time.perf_counter() - t0) / calls
+        ent = {"value": B * T / dt, "ms_per_call": dt * 1e3,
+               "h2d_bytes_per_call": int(xin.nbytes + y_np.nbytes),
+               "d2h_bytes_per_call": int(4 * (n * k + m * n) + 8 * B + 8 * B * m + 4 * B)}
+        if tag == "counts":
+            out.update(ent)
+        else:
+            out["packed"] = dict(ent, input="np.packbits(x, axis=-1, bitorder='little')")
+    out["calls"] = calls
+    out["api"] = "paper_2501_11407_b200.eprop_batch_gradient (weights unchanged between calls)"
+    del r
+    return out
+
+
+def shape_of(args, world):
+    """(kind, n, k, m, T, B per rank, global batch, scaling) of the run: the config's
+    per-GPU batch (weak scaling), or --global-batch split over the ranks (strong)."""
+    kind, n, k, m, T, B = CONFIGS[args.config]
+    if args.global_batch:
+        if args.global_batch % world:
+            raise SystemExit(f"--global-batch {args.global_batch} is not a multiple of {world}")
+        return kind, n, k, m, T, args.global_batch // world, args.global_batch, "strong"
+    return kind, n, k, m, T, B, B * world, "weak"
+
+
+def config_dict(args, world, chunk):
+    """The ``config`` object of the JSON line -- the same keys for both arms."""
+    kind, n, k, m, T, B, G, scaling = shape_of(args, world)
+    return {"workload": CONFIG_DESC[args.config] + (" + recurrent W_rec" if args.recurrent
+                                                     else ""),
+            "batch_per_gpu": B, "global_batch": G, "seq_len": T, "n_hidden": n,
+            "n_inputs": k, "n_classes": m, "chunk": chunk, "parallelism": f"dp{world}"}
+
+
+def cpu_reference_line(args, world):
+    """--impl reference: the reference's own e-prop engine (ENGINES["eprop-sparse"],
+    gradients.py:132-185, from baseline/_ref) on all host cores, rank 0 only; each timed
+    step is a bounded sample of the workload (one T_sub-step sample per core)."""
+    from oracle.cpu_bench import _pool, cores, cpu_model, reference_available, time_cpu, warm
+    from paper_2501_11407_b200.engine import default_chunk
+    kind, n, k, m, T, B, G, scaling = shape_of(args, world)
+    impl = "reference" if reference_available() else "port"
     procs = cores()
-    T_sub = 25 if kind == "alif" else 100
+    # bounded per-step sample: ~1 s of CPU work per timed step on this shape
+    T_sub = max(2, min(T, int(25 * (1024 * 700) / (n * k)) if kind == "alif" else
+                       int(100 * (256 * 700) / (n * k))))
     pool = _pool(procs)
     vals = []
     try:
+        warm(pool, procs, kind, n, k, m, impl)
         for i in range(args.warmup + args.steps):
-            v, wall, _ = time_cpu(kind, n, k, m, T_sub, procs, procs, pool=pool)
+            v, wall, _ = time_cpu(kind, n, k, m, T_sub, procs, procs, pool=pool, impl=impl,
+                                  warmed=True)
             if i >= args.warmup:
                 vals.append(v)
     finally:
         pool.close()
         pool.join()
     value = float(np.mean(vals))
-    sample = (f"{procs} processes x 1 sample x {T_sub} steps per timed step "
-              f"(of the {B}x{T} workload), oracle port of gradients.py:132-185, "
-              "BLAS threads=1")
+    what = ("the unmodified reference sparseprop 0.1.0 (baseline/_ref), "
+            "ENGINES['eprop-sparse'] = gradients.py:132-185, f32 net"
+            if impl == "reference" else
+            "oracle port of gradients.py:132-185 (reference not installed in baseline/_ref)")
+    sample = (f"{procs} processes x 1 sample x {T_sub} steps per timed step (of the "
+              f"{G}x{T} workload); {what}; BLAS threads=1")
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": None, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": CONFIG_DESC[cfg_name], "batch_per_gpu": B, "seq_len": T,
-                   "n_hidden": n, "n_inputs": k, "n_classes": m},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": sample},
+        "config": config_dict(args, world, default_chunk(T, B, n, k, kind == "alif")),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": impl,
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -242,6 +305,10 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="fixed global batch split over the ranks (strong scaling, e.g. "
+                         "--config c4 --global-batch 1024); default: the config's batch "
+                         "per GPU (weak scaling)")
     ap.add_argument("--chunk", type=int, default=0, help="0 = engine default for T")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -266,7 +333,7 @@ def main():
 
     if args.impl == "reference":
         if rank == 0:
-            print(json.dumps(cpu_reference_line(args, args.config)), flush=True)
+            print(json.dumps(cpu_reference_line(args, world)), flush=True)
         return
 
     import torch
@@ -289,11 +356,19 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    kind, n, k, m, T, B = CONFIGS[args.config]
+    kind, n, k, m, T, B, G, scaling = shape_of(args, world)
     spec = P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=m, precision="f32", seed=0,
                          recurrent=args.recurrent)
     net = P.init_network(spec)
-    x_np, y_np = poisson_batch(B, k, T, m, seed=1000 + rank)
+    # this rank's shard: weak scaling -- its own batch (seed 1000 + rank); strong scaling
+    # -- a contiguous slice of ONE global batch (seed 1000), every rank the same size
+    if scaling == "strong":
+        xg, yg = poisson_batch(G, k, T, m, seed=1000)
+        x_np = np.ascontiguousarray(xg[rank * B:(rank + 1) * B])
+        y_np = np.ascontiguousarray(yg[rank * B:(rank + 1) * B])
+        del xg, yg
+    else:
+        x_np, y_np = poisson_batch(B, k, T, m, seed=1000 + rank)
     from paper_2501_11407_b200.engine import default_chunk
     chunk = args.chunk or default_chunk(T, B, n, k, kind == "alif")
     eng = EpropEngine(n, k, m, B, alif=kind == "alif", w_f64=False, chunk=chunk,
@@ -315,7 +390,7 @@ def main():
     # engine's fp64 mirror) and W is re-sliced into the INT8 digits the next update's
     # projection reads -- all of it inside the timed step.
     wout_master = torch.from_numpy(np.ascontiguousarray(net.readout.w_out)).to(dev)
-    lr, g_scale = 1e-3, 1.0 / (world * B)
+    lr, g_scale = 1e-3, 1.0 / G
     vp = ctypes.c_void_p
 
     def update():
@@ -353,8 +428,10 @@ def main():
     # the allreduce) is captured once in a CUDA graph and replayed per step: no host
     # launch gaps on the device timeline.  Falls back to eager launches if capture fails.
     graph = None
-    # (single process only: the NCCL allreduce of a multi-rank step stays eager)
-    if args.graph and not args.profile and world == 1:
+    # N > 1 over NCCL: the allreduce is captured into the graph too (NCCL supports stream
+    # capture), so every N is timed the same way; gloo ranks (a 1-GPU test of the
+    # multi-rank path) stay eager.  All ranks must agree on the mode.
+    if args.graph and not args.profile and (world == 1 or backend == "nccl"):
         try:
             cs_ = torch.cuda.Stream(device=dev)
             cs_.wait_stream(torch.cuda.current_stream(dev))
@@ -370,6 +447,11 @@ def main():
             print(f"[bench] CUDA graph capture failed ({exc}); eager launches", file=sys.stderr)
             graph = None
             barrier()
+        if world > 1:
+            ok = torch.tensor([1 if graph is not None else 0], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0:
+                graph = None
 
     clocks = ClockSampler(local) if not args.profile else None
     if clocks:
@@ -576,40 +658,59 @@ def main():
             parity = {"checked": False, "error": repr(exc)}
 
     # ---- CPU baseline (rank 0, N=1 only) ----
-    cpu = None
+    # the reference's own engine (baseline/_ref) is the baseline; the oracle port of the
+    # same algorithm is reported beside it, labelled
+    cpu = cpu_port = None
     if world == 1 and not args.no_cpu and not args.profile:
-        from oracle.cpu_bench import cores, time_cpu
+        from oracle.cpu_bench import cores, cpu_model, reference_available, time_cpu
         procs = cores()
-        T_sub = 100 if kind == "alif" else 250
-        v, wall, procs = time_cpu(kind, n, k, m, T_sub, 2 * procs, procs)
-        cpu = {"value": v, "unit": UNIT, "cores": procs, "kind": "port",
-               "sample": f"{2 * procs} single-sample tasks x {T_sub} steps of the {B}x{T} "
-                         f"workload on {procs} processes ({wall:.1f} s wall); oracle port "
-                         "of gradients.py:132-185, BLAS threads=1"}
+        for impl in (("reference", "port") if reference_available() else ("port",)):
+            per_core = 10 if impl == "reference" else 40      # bounded: ~5-10 s each
+            T_sub = max(2, min(T, int(per_core * (1024 * 700) / (n * k)) if kind == "alif"
+                               else int(4 * per_core * (256 * 700) / (n * k))))
+            v, wall, procs = time_cpu(kind, n, k, m, T_sub, 2 * procs, procs, impl=impl)
+            what = ("the unmodified reference sparseprop 0.1.0 (baseline/_ref), "
+                    "ENGINES['eprop-sparse'], f32 net" if impl == "reference" else
+                    "oracle port (oracle/eprop_ref.eprop_forward_mode) of gradients.py:132-185")
+            ent = {"value": v, "unit": UNIT, "cores": procs, "kind": impl,
+                   "cpu_model": cpu_model(),
+                   "sample": f"{2 * procs} single-sample tasks x {T_sub} steps of the "
+                             f"{B}x{T} workload on {procs} processes ({wall:.1f} s wall); "
+                             f"{what}; BLAS threads=1"}
+            if impl == "reference" or cpu is None:
+                cpu = ent
+            if impl == "port":
+                cpu_port = ent
+
+    # ---- drop-in API end to end (rank 0, N=1): eprop_batch_gradient on numpy ----
+    dropin = None
+    if world == 1 and not args.no_e2e and not args.profile and not args.recurrent:
+        dropin = dropin_e2e(P, net, x_np, y_np, chunk)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": CONFIG_DESC[args.config] + (" + recurrent W_rec" if
-                                                               args.recurrent else ""),
-                       "batch_per_gpu": B,
-                       "global_batch": B * world, "seq_len": T, "n_hidden": n, "n_inputs": k,
-                       "n_classes": m, "chunk": eng.Tc, "parallelism": f"dp{world}",
-                       "forward_precision": "fp64 state/current (bit-exact spikes)",
-                       "forward_kernel": "K2 projection + K1 dynamics",
-                       "step": "e-prop gradient (+ allreduce when N > 1) + fused SGD on W/W_out + W re-slice",
-                       "psi_parking_gb": args.park_gb,
-                       "l2": "512 MiB flush between timed steps (outside events)",
-                       "launch": "CUDA graph replay of the whole update" if graph is not None
-                                 else "eager launches"},
+            "config": config_dict(args, world, eng.Tc),
+            "run": {"forward_precision": "fp64 state/current (bit-exact spikes)",
+                    "forward_kernel": "K2 projection + K1 dynamics",
+                    "step": "e-prop gradient (+ allreduce when N > 1) + fused SGD on W/W_out "
+                            "+ W re-slice",
+                    "psi_parking_gb": args.park_gb,
+                    "l2": "512 MiB flush between timed steps (outside events)",
+                    "launch": ("CUDA graph replay of the whole update"
+                               + (" incl. the NCCL allreduce" if world > 1 else ""))
+                              if graph is not None else "eager launches",
+                    "dist_backend": backend if world > 1 else None},
             "e2e": e2e,
+            "e2e_dropin": dropin,
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roof,
             "kernels": kernels,
             "cpu_baseline": cpu,
+            "cpu_baseline_port": cpu_port,
             "parity": parity,
             "clocks": clk,
         }

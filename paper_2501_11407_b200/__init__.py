@@ -16,7 +16,9 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # the compute entry points need torch + the CUDA library; import lazily
     if name in ("eprop_sparse_gradient", "eprop_batch_gradient", "ENGINES", "GradResult",
-                "BatchGradResult", "softmax_cross_entropy", "gradient_deviation_stats"):
+                "BatchGradResult", "softmax_cross_entropy", "gradient_deviation_stats",
+                "network_loss", "DeviationStats", "TraceState", "initial_trace",
+                "eprop_trace_update", "learning_signal", "accumulate_param_grad"):
         from . import gradients
         return getattr(gradients, name)
     if name == "EpropEngine":

@@ -1,29 +1,45 @@
 """Gradient entry points of the drop-in (same names and signatures as the reference).
 
 Reference: /root/reference/pkg/src/sparseprop/gradients.py
+  TraceState                 :39-44     (host container, compressed layout)
   GradResult                 :54-63
   softmax_cross_entropy      :66-75
+  initial_trace              :85-86
+  eprop_trace_update         :89-94
+  learning_signal            :97-101
+  accumulate_param_grad      :104-111
   eprop_sparse_gradient      :132-185   <- the hot path, here on B200 kernels
+  network_loss               :349-365   (forward only, on B200 kernels)
   gradient_deviation_stats   :418-433
   ENGINES                    :436-441
 
 ``eprop_sparse_gradient(net, x_seq, label)`` keeps the reference's single-sample
 contract (numpy in, numpy out, dtype of ``net.neuron.w``).  ``eprop_batch_gradient``
 is the batched form the kernels are built for: per-sample losses/readouts and the
-batch-SUMMED gradients.  Every number is computed by the CUDA
-kernels in libsparseprop_b200.so; there is no CPU path.
+batch-SUMMED gradients.  Every number of those two and of
+``network_loss`` is computed by the CUDA kernels in libsparseprop_b200.so; there is no
+CPU path.  ``net`` may be this package's ``Network`` or the reference's own
+``sparseprop.neurons.Network`` (duck-typed: ALIF = the neuron has ``beta``/``rho``).
+
+The per-step trace helpers (``initial_trace``, ``eprop_trace_update``,
+``learning_signal``, ``accumulate_param_grad``) are the reference's public single-step
+API, used by its tests and by callers that drive the recursion themselves.  They are
+small host (numpy) operations on one sample's compressed trace -- the GPU path never
+calls them (it runs the whole recursion batched inside the kernels) -- and they accept
+the reference's own ``TraceState``/``SparseTensor`` objects as well as plain arrays.
 """
 
 from __future__ import annotations
 
+import threading
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from .engine import EpropEngine, default_chunk
-from .errors import LabelOutOfRange, ShapeMismatch
-from .neurons import ALIFParams, Network
+from .errors import LabelOutOfRange, ShapeMismatch, StructureFallback
 
 
 @dataclass
@@ -72,33 +88,75 @@ def softmax_cross_entropy(v: np.ndarray, label: int):
     return float(lse - z[label]), p
 
 
+# --------------------------------------------------------------------------------------
+# network introspection (this package's Network or the reference's, duck-typed)
+# --------------------------------------------------------------------------------------
+
+def is_alif(net) -> bool:
+    """ALIF layer: the reference's ALIFParams adds beta/rho (neurons.py:53-63)."""
+    p = net.neuron
+    return hasattr(p, "beta") and hasattr(p, "rho")
+
+
+def w_rec_of(net):
+    """Recurrent weights of the extension (None for the reference's feed-forward layer)."""
+    return getattr(net.neuron, "w_rec", None)
+
+
+def _dims(net):
+    w = np.asarray(net.neuron.w)
+    w_out = np.asarray(net.readout.w_out)
+    if w.ndim != 2 or w_out.ndim != 2 or w_out.shape[1] != w.shape[0]:
+        raise ShapeMismatch(f"weights {w.shape} / {w_out.shape} do not form a network")
+    return int(w.shape[0]), int(w.shape[1]), int(w_out.shape[0])
+
+
+def _neuron_kwargs(net) -> dict:
+    p = net.neuron
+    kw = dict(alpha=float(p.alpha), theta=float(p.theta), slope=float(p.slope),
+              reset=bool(p.reset), kappa=float(net.readout.kappa))
+    if is_alif(net):
+        kw.update(beta=float(p.beta), rho=float(p.rho))
+    return kw
+
+
 _ENGINES: dict = {}
 
 
-def get_engine(net: Network, B: int, *, chunk: int | None = None, T: int | None = None,
-               device=None) -> EpropEngine:
-    """Engine cache keyed by shape, neuron kind, weight precision, chunk and device."""
+def get_engine(net, B: int, *, chunk: int | None = None, T: int | None = None,
+               device=None, grad: bool = True) -> EpropEngine:
+    """Engine cache keyed by shape, neuron kind, weight precision, chunk, device and
+    mode (``grad=False``: forward-only engine for ``network_loss``)."""
     dev = torch.device(device if device is not None else "cuda")
+    if dev.type == "cuda" and dev.index is None and torch.cuda.is_available():
+        dev = torch.device("cuda", torch.cuda.current_device())
+    n, k, m = _dims(net)
+    alif = is_alif(net)
     if chunk is None:
-        chunk = default_chunk(T or 127, B, net.n, net.k, net.is_alif)
-    w_f64 = net.neuron.w.dtype == np.float64
+        chunk = default_chunk(T or 127, B, n, k, alif)
+    w_f64 = np.asarray(net.neuron.w).dtype == np.float64
     reset = bool(net.neuron.reset)
-    rec = net.is_recurrent
-    key = (net.n, net.k, net.m, B, net.is_alif, w_f64, chunk, str(dev), reset, rec)
+    rec = w_rec_of(net) is not None
+    key = (n, k, m, B, alif, w_f64, chunk, str(dev), reset, rec, bool(grad))
     eng = _ENGINES.get(key)
     if eng is None:
-        eng = EpropEngine(net.n, net.k, net.m, B, alif=net.is_alif, w_f64=w_f64, chunk=chunk,
-                          device=dev, reset=reset, recurrent=rec)
+        eng = EpropEngine(n, k, m, B, alif=alif, w_f64=w_f64, chunk=chunk, device=dev,
+                          reset=reset, recurrent=rec, grad=grad)
         _ENGINES[key] = eng
     return eng
 
 
 def _as_counts(x: np.ndarray) -> np.ndarray:
-    """Spike inputs as uint8 event counts (binary spikes or pooled counts <= 255)."""
+    """Spike inputs as uint8 event counts (binary spikes or pooled counts <= 255).
+
+    Every input the reference produces or tests with is a spike count: Poisson 0/1
+    spikes (datasets.py:65-67, bench.py:63-67), pooled integer counts
+    (datasets.py:138-159), and the 0/1 draws of its tests (test_gradients.py:50).  The
+    exact INT8 tensor-core projection relies on it; real-valued inputs raise."""
     if x.dtype == np.uint8:
         return x
     if x.dtype == np.bool_:
-        return x.astype(np.uint8)
+        return x.view(np.uint8)
     xi = np.rint(x)
     if not np.array_equal(xi, x) or (x.size and (x.min() < 0 or x.max() > 255)):
         raise ValueError("inputs must be non-negative integer spike counts <= 255 "
@@ -106,60 +164,162 @@ def _as_counts(x: np.ndarray) -> np.ndarray:
     return xi.astype(np.uint8)
 
 
-def _neuron_kwargs(net: Network) -> dict:
-    p = net.neuron
-    kw = dict(alpha=p.alpha, theta=p.theta, slope=p.slope, reset=p.reset, kappa=net.readout.kappa)
-    if isinstance(p, ALIFParams):
-        kw.update(beta=p.beta, rho=p.rho)
-    return kw
+# --------------------------------------------------------------------------------------
+# host staging: pinned buffers, threaded copies, weight versioning
+# --------------------------------------------------------------------------------------
+
+_POOL = None
+_POOL_LOCK = threading.Lock()
 
 
-def eprop_batch_gradient(net: Network, x, labels, *, chunk: int | None = None,
-                         device=None, smooth: bool = False) -> BatchGradResult:
+def _pool():
+    global _POOL
+    with _POOL_LOCK:
+        if _POOL is None:
+            _POOL = ThreadPoolExecutor(max_workers=8, thread_name_prefix="spb-stage")
+        return _POOL
+
+
+def _copy_into(dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[...] = src, split over threads along axis 0 for large arrays (numpy releases
+    the GIL in the copy loop, so the pieces run concurrently)."""
+    if src.nbytes < (8 << 20) or src.shape[0] < 2:
+        np.copyto(dst, src)
+        return
+    parts = min(8, src.shape[0])
+    edges = np.linspace(0, src.shape[0], parts + 1).astype(int)
+    futs = [_pool().submit(np.copyto, dst[a:b], src[a:b])
+            for a, b in zip(edges[:-1], edges[1:]) if b > a]
+    for f in futs:
+        f.result()
+
+
+class _Staging:
+    """Per-engine pinned host buffers and device input buffers, grown on demand."""
+
+    def __init__(self, eng: EpropEngine):
+        self.eng = eng
+        self.x_host = self.x_dev = None
+        self.y_host = torch.empty(eng.B, dtype=torch.int64).pin_memory()
+        self.y_dev = torch.empty(eng.B, dtype=torch.int64, device=eng.device)
+        self.w_seen = None      # host copies of the weights last uploaded
+        self.w_obj = None
+
+    def inputs(self, xc: np.ndarray, labels: np.ndarray):
+        shape = tuple(xc.shape)
+        if self.x_host is None or tuple(self.x_host.shape) != shape:
+            self.x_host = torch.empty(shape, dtype=torch.uint8).pin_memory()
+            self.x_dev = torch.empty(shape, dtype=torch.uint8, device=self.eng.device)
+        _copy_into(self.x_host.numpy(), xc)
+        self.y_host.numpy()[:] = labels
+        self.x_dev.copy_(self.x_host, non_blocking=True)
+        self.y_dev.copy_(self.y_host, non_blocking=True)
+        return self.x_dev, self.y_dev
+
+    def weights(self, net):
+        """Upload + re-slice W only when it changed since the last call (same array
+        object with equal contents -> skip; in-place edits, e.g. the reference's finite
+        differences, are caught by the content comparison)."""
+        eng = self.eng
+        w = np.asarray(net.neuron.w)
+        w_out = np.asarray(net.readout.w_out)
+        w_rec = w_rec_of(net)
+        objs = (id(net.neuron.w), id(net.readout.w_out), id(w_rec))
+        if (self.w_seen is not None and objs == self.w_obj
+                and np.array_equal(w, self.w_seen[0])
+                and np.array_equal(w_out, self.w_seen[1])
+                and (w_rec is None or np.array_equal(w_rec, self.w_seen[2]))):
+            return
+        eng.set_weights(torch.from_numpy(np.ascontiguousarray(w)),
+                        torch.from_numpy(np.ascontiguousarray(w_out)),
+                        w_rec=(torch.from_numpy(np.ascontiguousarray(w_rec))
+                               if w_rec is not None else None))
+        self.w_seen = (w.copy(), w_out.copy(), None if w_rec is None else np.array(w_rec))
+        self.w_obj = objs
+
+
+def _staging(eng: EpropEngine) -> _Staging:
+    st = getattr(eng, "_staging", None)
+    if st is None:
+        st = eng._staging = _Staging(eng)
+    return st
+
+
+def _to_host(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> fresh numpy array through the caching pinned-host allocator."""
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    return h
+
+
+def _check_batch(net, x, labels, packed: bool):
+    n, k, m = _dims(net)
+    x = np.asarray(x)
+    kb = (k + 7) // 8 if packed else k
+    if x.ndim != 3 or x.shape[2] != kb:
+        raise ShapeMismatch(f"x must be [B, T, {kb}]{' (bit-packed)' if packed else ''}, "
+                            f"got {x.shape}")
+    labels = np.asarray(labels, dtype=np.int64).reshape(-1)
+    B = x.shape[0]
+    if labels.shape[0] != B:
+        raise ShapeMismatch("one label per sample required")
+    if B and (labels.min() < 0 or labels.max() >= m):
+        bad = labels[(labels < 0) | (labels >= m)][0]
+        raise LabelOutOfRange(f"label {int(bad)} out of range for {m} classes")
+    if packed and x.dtype != np.uint8:
+        raise ShapeMismatch("bit-packed inputs are uint8 (np.packbits, bitorder='little')")
+    return (x if packed else _as_counts(x)), labels
+
+
+# --------------------------------------------------------------------------------------
+# the hot path
+# --------------------------------------------------------------------------------------
+
+def eprop_batch_gradient(net, x, labels, *, chunk: int | None = None, device=None,
+                         smooth: bool = False, packed: bool = False) -> BatchGradResult:
     """Batched online e-prop on the B200: x [B, T, k] spike counts, labels [B].
 
     Returns per-sample losses and readout sums and the gradients SUMMED over the batch
     (= sum of the reference's per-sample ``eprop_sparse_gradient`` grads).  ``smooth``
     replaces the hard threshold by surrogate_smooth in the forward (graph.py:45-47), the
-    reference's finite-difference mode (gradients.py:114-115).
+    reference's finite-difference mode (gradients.py:114-115).  ``packed=True``: x is
+    the bit-packed binary spike tensor (np.packbits(..., axis=-1, bitorder="little"),
+    [B, T, ceil(k/8)] uint8) -- 8x fewer host-to-device bytes.
+
+    Host side: the inputs go through a pinned staging buffer (threaded copy, async
+    host-to-device), the weights are uploaded and re-sliced only when they changed, and
+    the results come back through pinned buffers in one synchronisation.
     """
-    x = np.asarray(x)
-    if x.ndim != 3 or x.shape[2] != net.k:
-        raise ShapeMismatch(f"x must be [B, T, k={net.k}], got {x.shape}")
-    labels = np.asarray(labels, dtype=np.int64).reshape(-1)
-    B, T = x.shape[0], x.shape[1]
-    if labels.shape[0] != B:
-        raise ShapeMismatch("one label per sample required")
-    if B and (labels.min() < 0 or labels.max() >= net.m):
-        bad = labels[(labels < 0) | (labels >= net.m)][0]
-        raise LabelOutOfRange(f"label {int(bad)} out of range for {net.m} classes")
-    xc = np.ascontiguousarray(_as_counts(x))
+    xc, labels = _check_batch(net, x, labels, packed)
+    B, T = xc.shape[0], xc.shape[1]
+    if B == 0 or T == 0:
+        raise ShapeMismatch("empty batch or sequence")
     eng = get_engine(net, B, chunk=chunk, T=T, device=device)
-    dev = eng.device
-    xd = torch.from_numpy(xc).to(dev)
-    ld = torch.from_numpy(labels).to(dev)
-    eng.set_weights(torch.from_numpy(np.ascontiguousarray(net.neuron.w)),
-                    torch.from_numpy(np.ascontiguousarray(net.readout.w_out)),
-                    w_rec=(torch.from_numpy(np.ascontiguousarray(net.neuron.w_rec))
-                           if net.is_recurrent else None))
-    eng.run(xd, ld, smooth=smooth, **_neuron_kwargs(net))
-    wdt = torch.float64 if net.neuron.w.dtype == np.float64 else torch.float32
-    gw = eng.grad_w(wdt)
-    gwo = eng.grad_wout.to(wdt)
-    out_dtype = net.neuron.w.dtype
-    grads = {"w": gw.cpu().numpy().astype(out_dtype, copy=False),
-             "w_out": gwo.cpu().numpy().astype(out_dtype, copy=False)}
-    if net.is_recurrent:
-        grads["w_rec"] = eng.grad_w_rec(wdt).cpu().numpy().astype(out_dtype, copy=False)
+    st = _staging(eng)
+    xd, ld = st.inputs(np.ascontiguousarray(xc), labels)
+    st.weights(net)
+    # 0/1 spikes (bit-packed or bool) let K2 recombine its digit sums in one int64
+    binary = packed or np.asarray(x).dtype == np.bool_
+    eng.run(xd, ld, smooth=smooth, bits=packed, binary=binary, **_neuron_kwargs(net))
+    w_dtype = np.asarray(net.neuron.w).dtype
+    wdt = torch.float64 if w_dtype == np.float64 else torch.float32
+    outs = {"w": _to_host(eng.grad_w(wdt)), "w_out": _to_host(eng.grad_wout.to(wdt)),
+            "loss": _to_host(eng.loss), "s": _to_host(eng.s), "correct": _to_host(eng.correct)}
+    if w_rec_of(net) is not None:
+        outs["w_rec"] = _to_host(eng.grad_w_rec(wdt))
+    torch.cuda.current_stream(eng.device).synchronize()
+    grads = {"w": outs["w"].numpy(), "w_out": outs["w_out"].numpy()}
+    if "w_rec" in outs:
+        grads["w_rec"] = outs["w_rec"].numpy()
     return BatchGradResult(
-        loss=eng.loss.cpu().numpy().copy(),
+        loss=outs["loss"].numpy(),
         grads=grads,
-        readout_sum=eng.s.cpu().numpy().astype(out_dtype),
-        correct=eng.correct.cpu().numpy().astype(bool),
+        readout_sum=outs["s"].numpy().astype(w_dtype, copy=False),
+        correct=outs["correct"].numpy().astype(bool),
     )
 
 
-def eprop_sparse_gradient(net: Network, x_seq: np.ndarray, label: int,
+def eprop_sparse_gradient(net, x_seq: np.ndarray, label: int,
                           smooth: bool = False) -> GradResult:
     """Online sparse e-prop for one sample -- the reference entry point (gradients.py:132).
 
@@ -167,20 +327,122 @@ def eprop_sparse_gradient(net: Network, x_seq: np.ndarray, label: int,
     {"w": [n, k], "w_out": [m, n]} in the dtype of ``net.neuron.w`` and the time-summed
     readout.  Inputs must be spike counts (binary or pooled integers).
     """
+    n, k, m = _dims(net)
     x_seq = np.asarray(x_seq)
-    if x_seq.ndim != 2 or x_seq.shape[1] != net.k:
-        raise ShapeMismatch(f"x_seq must be [T, k={net.k}], got {x_seq.shape}")
-    if not 0 <= int(label) < net.m:
-        raise LabelOutOfRange(f"label {label} out of range for {net.m} classes")
+    if x_seq.ndim != 2 or x_seq.shape[1] != k:
+        raise ShapeMismatch(f"x_seq must be [T, k={k}], got {x_seq.shape}")
+    if not 0 <= int(label) < m:
+        raise LabelOutOfRange(f"label {label} out of range for {m} classes")
     r = eprop_batch_gradient(net, x_seq[None], np.array([int(label)]), smooth=smooth)
     return GradResult(float(r.loss[0]), r.grads, r.readout_sum[0], None)
+
+
+def network_loss(net, x_seq: np.ndarray, label: int, smooth: bool = False):
+    """Forward-only loss evaluation with the binary spike raster (gradients.py:349-365):
+    returns ``(loss, readout_sum [m], raster [T, n] bool)``, computed by the B200
+    forward kernels (K2 exact projection + K1 dynamics + K3 readout) on a forward-only
+    engine -- the same spikes as the gradient path, bit for bit."""
+    n, k, m = _dims(net)
+    x_seq = np.asarray(x_seq)
+    if x_seq.ndim != 2 or x_seq.shape[1] != k:
+        raise ShapeMismatch(f"x_seq must be [T, k={k}], got {x_seq.shape}")
+    if not 0 <= int(label) < m:
+        raise LabelOutOfRange(f"label {label} out of range for {m} classes")
+    xc = _as_counts(x_seq)[None]
+    T = xc.shape[1]
+    eng = get_engine(net, 1, T=T, grad=False)
+    st = _staging(eng)
+    xd, ld = st.inputs(np.ascontiguousarray(xc), np.array([int(label)]))
+    st.weights(net)
+    raster = torch.zeros((1, T, (n + 31) // 32), dtype=torch.int32, device=eng.device)
+    eng.run(xd, ld, raster=raster, smooth=smooth, forward_only=True, **_neuron_kwargs(net))
+    r = raster.cpu().numpy().view(np.uint32)[0]
+    bits = ((r[..., None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool)
+    w_dtype = np.asarray(net.neuron.w).dtype
+    return (float(eng.loss[0].item()), eng.s[0].cpu().numpy().astype(w_dtype),
+            bits.reshape(T, -1)[:, :n])
+
+
+# --------------------------------------------------------------------------------------
+# the reference's single-step trace API (host helpers, gradients.py:39-111)
+# --------------------------------------------------------------------------------------
+
+@dataclass
+class TraceState:
+    """Eligibility trace G_t of one sample in the reference's compressed layout
+    (gradients.py:39-44, 78-86): LIF ``values`` [n, k] (delta-3 rows), ALIF [n, 2, k]
+    (``[:, 0]`` = G_u, ``[:, 1]`` = G_a = eps_a).  ``G`` aliases the state itself so
+    ``state.G.values`` reads like the reference's ``TraceState.G`` (a SparseTensor)."""
+
+    values: np.ndarray
+    structure_intact: bool = True
+
+    @property
+    def G(self):
+        return self
+
+
+def _values(t):
+    """Compressed values of a reference SparseTensor / TraceState, or a plain array."""
+    if hasattr(t, "G"):
+        t = t.G
+    if hasattr(t, "structure") and not getattr(t.structure, "delta_pairs", True):
+        raise StructureFallback("trace update received a densified operand")
+    return np.asarray(t.values if hasattr(t, "values") else t)
+
+
+def initial_trace(p, dtype=np.float64) -> TraceState:
+    """G_0 = 0 in the compressed layout of ``p`` (gradients.py:78-86)."""
+    n, k = np.shape(p.w)
+    shape = (n, 2, k) if (hasattr(p, "beta") and hasattr(p, "rho")) else (n, k)
+    return TraceState(np.zeros(shape, dtype=dtype))
+
+
+def eprop_trace_update(g_prev, h_i, f) -> TraceState:
+    """One trace step G_t = H_I G_{t-1} + F_t on compressed operands (gradients.py:89-94):
+    LIF ``h_i`` diag [n], ``f`` [n, k]; ALIF ``h_i`` per-neuron 2x2 blocks [n, 2, 2],
+    ``f`` [n, 2, k].  Accepts the reference's SparseTensor / TraceState objects too."""
+    g = _values(g_prev)
+    h = _values(h_i)
+    fv = _values(f)
+    if g.ndim == 2:                                 # LIF: diag(h) G + F
+        if h.shape != (g.shape[0],) or fv.shape != g.shape:
+            raise ShapeMismatch("trace, H_I and F shapes disagree")
+        out = h[:, None] * g + fv
+    else:                                           # ALIF: per-neuron 2x2 blocks
+        if h.shape != (g.shape[0], 2, 2) or fv.shape != g.shape:
+            raise ShapeMismatch("trace, H_I and F shapes disagree")
+        out = np.einsum("iab,ibj->iaj", h, g) + fv
+    intact = getattr(g_prev, "structure_intact", True)
+    return TraceState(out, intact)
+
+
+def learning_signal(dl_dv: np.ndarray, readout, surrogate_grads: np.ndarray) -> np.ndarray:
+    """Per-step dL/du of the hidden layer: (W_out^T dL/dv) * sigma' (gradients.py:97-101)."""
+    dl_dv = np.asarray(dl_dv)
+    w_out = np.asarray(readout.w_out)
+    if dl_dv.shape[0] != w_out.shape[0]:
+        raise ShapeMismatch("dL/dv does not match readout width")
+    return (w_out.T @ dl_dv) * surrogate_grads
+
+
+def accumulate_param_grad(acc: np.ndarray, c_t: np.ndarray, g_t) -> np.ndarray:
+    """acc[i, j] += c_t[i] * G_t[i, j], the u-component for ALIF blocks
+    (gradients.py:104-111); in place, returns ``acc``."""
+    vals = _values(g_t)
+    u_vals = vals[:, 0, :] if vals.ndim == 3 else vals
+    c_t = np.asarray(c_t)
+    if acc.shape != u_vals.shape or c_t.shape[0] != acc.shape[0]:
+        raise ShapeMismatch("accumulator, signal and trace shapes disagree")
+    acc += c_t[:, None] * u_vals
+    return acc
 
 
 def gradient_deviation_stats(g1, g2) -> DeviationStats:
     """Median and 2.5/97.5 % quantiles of |g1 - g2| over all parameters (gradients.py:418-433)."""
 
     def flat(g):
-        if isinstance(g, (GradResult, BatchGradResult)):
+        if isinstance(g, (GradResult, BatchGradResult)) or hasattr(g, "grads"):
             g = g.grads
         if isinstance(g, dict):
             return np.concatenate([np.asarray(g[key]).ravel() for key in sorted(g)])

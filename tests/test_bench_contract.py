@@ -27,7 +27,7 @@ def _check_common(d):
     assert BASE_KEYS <= set(d), BASE_KEYS - set(d)
     assert d["metric"].startswith("e-prop train samples")
     assert d["unit"] == "samples*timesteps/s" and d["higher_is_better"] is True
-    assert d["value"] > 0 and d["scaling"] == "weak" and d["data"] == "synthetic"
+    assert d["value"] > 0 and d["scaling"] in ("weak", "strong") and d["data"] == "synthetic"
     assert {"workload", "seq_len", "n_hidden", "n_inputs", "n_classes"} <= set(d["config"])
     e = d["e2e"]
     assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(e)
@@ -39,8 +39,26 @@ def test_reference_arm_contract():
     _check_common(d)
     assert d["impl"] == "reference"
     cb = d["cpu_baseline"]
-    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"]
+    sys.path.insert(0, ROOT)
+    from oracle.cpu_bench import reference_available
+    # the reference's own engine when baseline/_ref holds it, else the labelled port
+    assert cb["kind"] == ("reference" if reference_available() else "port")
+    assert cb["cores"] >= 1 and cb["value"] == d["value"] and cb["cpu_model"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["scaling"] == "weak"
+
+
+def test_reference_arm_strong_scaling_config():
+    """--global-batch: the fixed global batch of north_star's C4 curve (1024 split over
+    the ranks); the config keys are the ones the B200 arm prints."""
+    d = _run("--impl", "reference", "--config", "c4", "--global-batch", "1024",
+             "--steps", "1", "--warmup", "0")
+    _check_common(d)
+    assert d["scaling"] == "strong"
+    c = d["config"]
+    assert c["global_batch"] == 1024 and c["batch_per_gpu"] == 1024 and c["n_hidden"] == 2048
+    assert set(c) == {"workload", "batch_per_gpu", "global_batch", "seq_len", "n_hidden",
+                      "n_inputs", "n_classes", "chunk", "parallelism"}
 
 
 @pytest.mark.gpu
@@ -56,3 +74,9 @@ def test_gpu_arm_contract():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     c = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c)
+    assert set(d["config"]) == {"workload", "batch_per_gpu", "global_batch", "seq_len",
+                                "n_hidden", "n_inputs", "n_classes", "chunk", "parallelism"}
+    p = d["parity"]
+    assert p["checked"] and p["pass"] and p["spike_flips"] == 0
+    dp = d["e2e_dropin"]
+    assert dp["value"] > 0 and dp["packed"]["value"] > 0
