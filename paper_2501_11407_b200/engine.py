@@ -39,7 +39,11 @@ from . import _lib
 from .errors import LabelOutOfRange, ShapeMismatch
 
 SM_COUNT_DEFAULT = 148
-CHUNKS = (63, 127, 255, 511)  # Tc with Tc + 1 a multiple of the 64-wide K block
+# Tc with Tc + 1 a multiple of the 64-wide K block.  Longer chunks are strictly less work
+# (one per-synapse trace round trip per chunk; a sequence that fits one chunk never
+# materialises the trace and skips pass B's recompute); the chunk buffers grow with Tc,
+# never with T.
+CHUNKS = (63, 127, 255, 511, 1023, 2047)
 
 
 def ctypes_void(p):
@@ -91,7 +95,7 @@ def chunk_bytes(Tc: int, B: int, n: int, k: int, alif: bool = True) -> int:
 
 
 def default_chunk(T: int, B: int | None = None, n: int | None = None, k: int | None = None,
-                  alif: bool = True, budget: int = 24 << 30) -> int:
+                  alif: bool = True, budget: int = 32 << 30) -> int:
     """Chunk length Tc for a sequence of T steps: the smallest Tc covering the whole
     sequence, else the longest one whose chunk buffers fit ``budget`` bytes.  Longer
     chunks are strictly less work (the per-synapse ALIF trace makes one HBM round trip per

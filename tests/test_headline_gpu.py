@@ -137,3 +137,39 @@ def test_alif_long_horizon(chunk, precision):
     assert ref.raster.mean() > 0.005
     rel, cos = _check(eng, raster, ref, n)
     print(f"T={T} chunk={chunk} {precision}: rel {rel:.2e} cos {cos:.10f}")
+
+
+@pytest.mark.parametrize("chunk,T", [(1023, 900), (1023, 2500), (2047, 2000), (2047, 4500)])
+@pytest.mark.parametrize("kind", ["alif", "lif"])
+def test_long_chunks(chunk, T, kind):
+    """Tc = 1023 / 2047: one chunk (the trace never materialised, pass B reuses pass A)
+    and several chunks (the carry path with K = 1024 / 2048 per-sample GEMMs)."""
+    _need_gpu()
+    n, k, m, B = 72, 40, 4, 5
+    w, w_out = O.init_network_arrays(n, k, m, seed=5, dtype=np.float32)
+    w_out = (w_out * 2e-3).astype(np.float32)
+    x, y = O.poisson_batch(B, k, T, m, seed=9)
+    eng, raster = _run(kind, n, k, m, x, y, w, w_out, chunk)
+    ref = O.bptt_batch(w, w_out, O.Params(alif=kind == "alif"), x, y)
+    _check(eng, raster, ref, n)
+
+
+@pytest.mark.parametrize("chunk", [1023, 2047])
+@pytest.mark.parametrize("kind", ["alif", "lif"])
+def test_long_chunks_reset(chunk, kind):
+    """reset=True (the per-synapse G_u, K1r + K6 / K6r) with the long chunks."""
+    _need_gpu()
+    from paper_2501_11407_b200.engine import EpropEngine
+    n, k, m, B, T = 48, 30, 3, 4, 2500
+    w, w_out = O.init_network_arrays(n, k, m, seed=6, dtype=np.float64)
+    w_out = w_out * 2e-3
+    x, y = O.poisson_batch(B, k, T, m, seed=10)
+    eng = EpropEngine(n, k, m, B, alif=kind == "alif", w_f64=True, chunk=chunk,
+                      device="cuda", reset=True)
+    eng.set_weights(torch.from_numpy(w), torch.from_numpy(w_out))
+    raster = torch.zeros((B, T, (n + 31) // 32), dtype=torch.int32, device="cuda")
+    eng.run(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), raster=raster,
+            reset=True, binary=True)
+    torch.cuda.synchronize()
+    ref = O.bptt_batch(w, w_out, O.Params(alif=kind == "alif", reset=True), x, y)
+    _check(eng, _unpack_raster(raster, n), ref, n)

@@ -258,7 +258,8 @@ def test_input_count_conversion():
 
 def test_default_chunk():
     assert default_chunk(10) == 63 and default_chunk(100) == 127 and default_chunk(250) == 255
-    assert default_chunk(500) == 511 and default_chunk(10_000) == 511
+    assert default_chunk(500) == 511 and default_chunk(10_000) == 2047
+    assert default_chunk(2000) == 2047 and default_chunk(1000) == 1023
     # the chunk buffers are sized by Tc only; a budget caps Tc for huge layers
     from paper_2501_11407_b200.engine import chunk_bytes
     assert default_chunk(500, 128, 2048, 700) == 511
