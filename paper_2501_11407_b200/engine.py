@@ -421,7 +421,7 @@ class EpropEngine:
         if filt and one:
             x_alpha = 0.0   # K4 = byte -> bf16 copy (the filter state is never needed)
         raw_x = (filt or self.reset) and (filt or not self.recurrent)
-        xl_ptr = None if raw_x else v(self.xl.data_ptr())
+        xl_ptr = None if (raw_x or self.xl is None) else v(self.xl.data_ptr())
         # one chunk: the pack writes the raw-spike GEMM operand itself (no K4 at all)
         pack_xh = (filt and one and not self.recurrent and self.pack_xh
                    and (bits or (self.k % 4 == 0 and x.data_ptr() % 4 == 0)))
