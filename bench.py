@@ -69,7 +69,7 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
-INT8_KERNELS = ("proj",)
+INT8_KERNELS = ("proj", "proj_dyn_a", "proj_dyn_b")
 
 
 def measured_traffic(cfg, kernel):
@@ -594,6 +594,12 @@ def main():
                 ln = meta                                        # int8 MACs x2, useful part
                 flops += 2.0 * P_sl * B * ln * n * k
                 byts += B * ln * k + P_sl * n * k + 8.0 * B * ln * n
+            elif name in ("proj_dyn_a", "proj_dyn_b"):
+                ln, mode, flag = meta                          # K2D: projection + dynamics
+                flops += 2.0 * P_sl * B * ln * n * k
+                byts += B * ln * k + P_sl * n * k + 32.0 * B * n   # spikes, digits, state
+                if mode >= 1:
+                    byts += 4.0 * B * (ln + 1) * n                # psi parked for the scan
             elif name in ("forward", "forward_a"):
                 ln, pid, flag = meta
                 pid = {3: 2, 4: 1}.get(pid, pid)   # raw-operand passes: same traffic
@@ -629,6 +635,8 @@ def main():
         dom = max(kernels, key=lambda nm: kernels[nm]["ms_per_step"])
         e = kernels[dom]
         names = {"proj": "input_proj_kernel (K2, int8 tcgen05)", "forward": "forward_chunk + chunk_scan (K1 pass B)",
+                 "proj_dyn_a": "input_proj_dyn_kernel (K2D pass A: int8 tcgen05 projection + fp64 dynamics)",
+                 "proj_dyn_b": "input_proj_dyn_kernel (K2D pass B: projection + dynamics, psi)",
                  "forward_a": "forward_chunk_kernel (K1 pass A)",
                  "gemm": "grad_gemm_tc_kernel (K5, bf16 hi/lo tcgen05)",
                  "carry": "alif_carry_kernel (K6, tcgen05 + eps stream)"}

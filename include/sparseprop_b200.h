@@ -68,11 +68,23 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
 int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
                          int n_pad32, int Kpad, int P, double* cur, int sm_count, int binary,
                          int probe, cudaStream_t stream);
+/* K2D Exact projection with the K1 dynamics fused (proj.cu input_proj_dyn_kernel): the
+ *     K2 tiles of a sample are followed, inside the same persistent CTA, by 4 chain warps
+ *     that integrate u, a (fp64, the reference's operation order) over the fresh currents
+ *     while they are in L2 and then discard them -- the current never makes a DRAM round
+ *     trip.  Rows of xq / cur are sample-aligned: row b*KR + s (KR % 64 == 0, len <= Tc <
+ *     KR); Kpad <= 768; P = 6 (fp32 weights) or 8 (fp64).  mode 0: pass A (zbar, zsum,
+ *     raster optional); 1: pass A with psi parked in psi [B][KR+1][n] (row 0 = psi_{t0-1});
+ *     2: pass B (psi parked, no readout filters).  Outputs as spb_forward_chunk. */
+int spb_input_proj_dyn(int mode, const uint8_t* xq, const int8_t* wq, const int* sexp, int B,
+                       int n, int n_pad32, int Kpad, int P, int Tc, int KR, int len, int t0,
+                       int T, double alpha, double theta, double slope, double beta, double rho,
+                       double kappa, int reset, int smooth, double* cur, double* u, double* a,
+                       double* zbar, double* zsum, uint32_t* raster, float* psi, int sm_count,
+                       int binary, cudaStream_t stream);
 
-
-
-/* K1  Neuron dynamics over one time chunk from the exact current cur [B*Tc][n] (row
- *     b*Tc+s): ALIF/LIF state update, spike and surrogate derivative.
+/* K1  Neuron dynamics over one time chunk from the exact current cur [B*KR][n] (row
+ *     b*KR+s, sample-aligned): ALIF/LIF state update, spike and surrogate derivative.
  *     Replaces _step_state (gradients.py:118-129) + heaviside/surrogate_grad
  *     (graph.py:40-52) + the readout spike filter (gradients.py:173-174).
  *     smooth != 0: spikes are 0.5 + d/(1+slope|d|) (surrogate_smooth, graph.py:45-47; the

@@ -90,6 +90,14 @@ __device__ __forceinline__ float surrogate_grad_f32(float d, float slope) {
   return r * r;
 }
 
+// z = spike(d): Theta(d) = [d >= 0] (graph.py:50-52) or, with smooth=True (the reference's
+// finite-difference mode, gradients.py:114-115), 0.5 + d / (1 + slope |d|) in the
+// reference's operation order.
+__device__ __forceinline__ double spike_value(double d, bool smooth, double slope) {
+  if (!smooth) return d >= 0.0 ? 1.0 : 0.0;
+  return __dadd_rn(0.5, __ddiv_rn(d, __dadd_rn(1.0, __dmul_rn(slope, fabs(d)))));
+}
+
 // bf16 hi/lo split of an fp32 value: x ~= hi + lo with |x - hi - lo| <= 2^-16 |x|.
 __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
   hi = __float2bfloat16_rn(x);

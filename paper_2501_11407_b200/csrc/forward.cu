@@ -36,13 +36,6 @@ struct FwdParams {
   int smooth;             // 1: spikes are surrogate_smooth(d) (graph.py:45-47), not Theta(d)
 };
 
-// z = spike(d): Theta(d) = [d >= 0] (graph.py:50-52) or, with smooth=True (the reference's
-// finite-difference mode, gradients.py:114-115), 0.5 + d / (1 + slope |d|) in the
-// reference's operation order.
-__device__ __forceinline__ double spike_value(double d, bool smooth, double slope) {
-  if (!smooth) return d >= 0.0 ? 1.0 : 0.0;
-  return __dadd_rn(0.5, __ddiv_rn(d, __dadd_rn(1.0, __dmul_rn(slope, fabs(d)))));
-}
 
 constexpr int K1_THREADS = 128;  // 4 warps = 128 consecutive neurons of one sample
 
@@ -88,7 +81,8 @@ __global__ void __launch_bounds__(K1_THREADS, 7) forward_chunk_kernel(
   const int n = P.n;
   const int nw = (n + 31) >> 5;
   // invalid lanes read a valid address (their own row start) and discard the value
-  const double* cp = cur + (long long)b * P.Tc * n + (valid_i ? i : wbase);
+  // current rows are sample-aligned: row b*KR + s (K2's layout)
+  const double* cp = cur + (long long)b * P.KR * n + (valid_i ? i : wbase);
   // d_prev of step t is the drive d of step t-1 (the reference recomputes the same
   // expression from the same state, gradients.py:159): carry it.
   double d_prev = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1) forward_rec_kernel(
   uint32_t* zrow = zchunk != nullptr ? zchunk + (long long)b * P.KR * nw : nullptr;
   if (zrow != nullptr)  // chunk row 0 = z_{t0-1}
     for (int w = tid; w < nw; w += REC_THREADS) zrow[w] = mask[0][w];
-  const double* crow = cur + (long long)b * P.Tc * n;
+  const double* crow = cur + (long long)b * P.KR * n;   // sample-aligned rows b*KR + s
   for (int s = 0; s < P.len; ++s) {
     const uint32_t* mprev = mask[s & 1];
     uint32_t* mnext = mask[(s + 1) & 1];

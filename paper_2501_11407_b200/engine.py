@@ -91,7 +91,7 @@ def chunk_bytes(Tc: int, B: int, n: int, k: int, alif: bool = True) -> int:
     kp = _round_up(k, 128)
     ldc = _round_up(n, 8)
     ops = 2 * (2 if alif else 1) * 2 * B * KR * ldc
-    return (8 * B * Tc * n + B * Tc * kp + 4 * B * (KR + 1) * n + ops + 4 * B * KR * kp)
+    return (8 * B * KR * n + B * KR * kp + 4 * B * (KR + 1) * n + ops + 4 * B * KR * kp)
 
 
 def default_chunk(T: int, B: int | None = None, n: int | None = None, k: int | None = None,
@@ -159,8 +159,11 @@ class EpropEngine:
         self.Kpad = _round_up(k, 128)
         self.n_pad32 = _round_up(n, 32)
         self.P = 8 if self.w_f64 else 6   # digit format, csrc/digits.cuh
-        self.xq = torch.zeros((B * self.Tc, self.Kpad), dtype=torch.uint8, device=dev)
-        self.cur = torch.empty((B * self.Tc, n), dtype=f64, device=dev)
+        # sample-aligned rows b*KR + s (KR = Tc + 1, a multiple of 64): a sample's rows
+        # start on a 128-row tile (or share one with one other sample), so the fused
+        # projection + dynamics kernel (K2D) never splits a sample across CTAs
+        self.xq = torch.zeros((B * self.KR, self.Kpad), dtype=torch.uint8, device=dev)
+        self.cur = torch.empty((B * self.KR, n), dtype=f64, device=dev)
         self.wq = torch.zeros((self.P, self.n_pad32, self.Kpad), dtype=torch.int8, device=dev)
         self.sexp = torch.zeros(n, dtype=torch.int32, device=dev)
         # neuron state (fp64) and readout filters
@@ -183,6 +186,10 @@ class EpropEngine:
         # weights
         self.w = torch.empty((n, k), dtype=f64 if self.w_f64 else f32, device=dev)
         self.wout = torch.empty((m, n), dtype=f64, device=dev)
+        # K2D (projection + dynamics fused, proj.cu) unless SPB_FUSE_DYN=0; the recurrent
+        # layer keeps K2 + K1rec, the fp64-weight digits (P = 8) need Kpad <= 768 too
+        self.fuse_dyn = (os.environ.get("SPB_FUSE_DYN", "1") != "0" and not self.recurrent
+                         and self.Kpad <= 768)
         # fold the input filter into the one-chunk coefficients (SPB_FILT=0: xbar operand)
         self.filt = os.environ.get("SPB_FILT", "1") != "0"
         self.pack_xh = os.environ.get("SPB_PACK_XH", "1") != "0"
@@ -311,23 +318,37 @@ class EpropEngine:
         return self.ctab
 
     def _pack(self, xp, strideb, bits, ln, st, xh=False):
-        """Chunk spikes (bytes or bits) -> zero-padded projection operand xq [B*Tc][Kpad]
-        (rows b*Tc + s; also K4's row source).  xh: also
+        """Chunk spikes (bytes or bits) -> zero-padded projection operand xq [B*KR][Kpad]
+        (rows b*KR + s, rows s >= len zero; also K4's row source).  xh: also
         write the one-chunk raw-spike GEMM operand (K4 folded into the pack)."""
         if xh:
             _lib.call("spb_pack_spikes_xh", ctypes_void(xp), strideb, self.B, self.k, int(bits),
-                      ln, self.Tc, self.Kpad, self.KR, ctypes_void(self.xq.data_ptr()),
+                      ln, self.KR, self.Kpad, self.KR, ctypes_void(self.xq.data_ptr()),
                       ctypes_void(self.xh.data_ptr()), st)
             return
         _lib.call("spb_pack_spikes", ctypes_void(xp), strideb, self.B, self.k, int(bits), ln,
-                  self.Tc, self.Kpad, 0, ctypes_void(self.xq.data_ptr()), st)
+                  self.KR, self.Kpad, 0, ctypes_void(self.xq.data_ptr()), st)
+
+    def _project_dyn(self, mode, ln, t0, T, common, raster, psi, st, timed, binary, tag):
+        """K2D: the exact projection with the K1 dynamics fused (proj.cu
+        input_proj_dyn_kernel); mode 0 = pass A, 1 = pass A + psi parked, 2 = pass B."""
+        v = ctypes_void
+        alpha, theta, slope, beta, rho, kappa, reset, _alif, smooth = common
+        timed(tag[0], tag[1], "spb_input_proj_dyn", int(mode), v(self.xq.data_ptr()),
+              v(self.wq.data_ptr()), v(self.sexp.data_ptr()), self.B, self.n, self.n_pad32,
+              self.Kpad, self.P, self.Tc, self.KR, ln, t0, T, alpha, theta, slope, beta, rho,
+              kappa, reset, smooth, v(self.cur.data_ptr()), v(self.u.data_ptr()),
+              v(self.a.data_ptr()), v(self.zbar.data_ptr()) if mode < 2 else None,
+              v(self.zsum.data_ptr()) if mode < 2 else None,
+              v(raster.data_ptr()) if raster is not None else None, psi, self.sm_count,
+              int(bool(binary)), st)
 
     def _project(self, ln, st, timed=None, binary=False):
         """K2: cur = W x_t exactly on INT8 tensor cores from the packed chunk (binary:
         0/1 spikes, single-int64 digit recombination)."""
         v = ctypes_void
         args = ("spb_input_proj", v(self.xq.data_ptr()),
-                v(self.wq.data_ptr()), v(self.sexp.data_ptr()), self.B * self.Tc, self.n,
+                v(self.wq.data_ptr()), v(self.sexp.data_ptr()), self.B * self.KR, self.n,
                 self.n_pad32, self.Kpad, self.P, v(self.cur.data_ptr()), self.sm_count,
                 int(bool(binary)), st)
         if timed is not None:
@@ -405,7 +426,7 @@ class EpropEngine:
         common = (float(alpha), float(theta), float(slope), beta_e, rho_e, float(kappa),
                   int(self.reset), int(self.alif), int(bool(smooth)))
         # K4 reads the packed operand (sample-major rows)
-        xq_sb, xq_st = Tc * self.Kpad, self.Kpad
+        xq_sb, xq_st = KR * self.Kpad, self.Kpad
         # K5/K6 operand: the filtered input xbar (reset=False: G_u = 1 (x) xbar), or with
         # reset=True the raw input (G_u is carried per synapse; K4 with alpha = 0 = copy)
         x_alpha = 0.0 if self.reset else float(alpha)
@@ -502,6 +523,15 @@ class EpropEngine:
                      xl_ptr, sst)
                 self._ev["xbar"].record(self.side)
                 self.launches += 1
+            if self.fuse_dyn:
+                # K2D: projection + dynamics in one kernel (psi parked for the scan when
+                # pass B will not recompute this chunk)
+                mode = 1 if (park or (one and not forward_only)) else 0
+                self._project_dyn(mode, ln, t0, T, common, raster,
+                                  psi_ptr(c) if mode else None, st, timed, binary,
+                                  ("proj_dyn_a", (ln, mode, one)))
+                self.launches += 2
+                continue
             if not (side_x and self.xbar_sched == "fa"):
                 self._project(ln, st, timed, binary)
             if self.recurrent:
@@ -545,14 +575,18 @@ class EpropEngine:
                 self.launches += 1
             elif not one:  # one chunk: xq and cur of pass A are still valid (same W, same x)
                 pack_chunk(c, ln)
-                self._project(ln, st, timed, binary)
+                if self.fuse_dyn:   # K2D pass B: the chunk's psi parked for the scan
+                    self._project_dyn(2, ln, t0, T, common, None, psi_ptr(c), st, timed,
+                                      binary, ("proj_dyn_b", (ln, 2, carry_out)))
+                else:
+                    self._project(ln, st, timed, binary)
                 if self.recurrent:
                     self._forward_rec(1, ln, t0, T, common, None, True, st, timed,
                                       (ln, 1, carry_out))
                     self.launches += 1
                 self.launches += 2
-            # one chunk (pass A parked psi) or K1rec (parks psi itself): scan only
-            pid = 2 if (one or park or self.recurrent) else 1
+            # one chunk (pass A parked psi), K2D or K1rec (park psi themselves): scan only
+            pid = 2 if (one or park or self.recurrent or self.fuse_dyn) else 1
             if filt:
                 pid = 3 if pid == 2 else 4
             timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,

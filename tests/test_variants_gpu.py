@@ -196,3 +196,45 @@ def test_graphed_update_equals_eager(T):
         torch.cuda.synchronize()
         assert np.array_equal(eng.grad_w_acc.cpu().numpy(), gw)
         assert np.array_equal(eng.loss.cpu().numpy(), ls)
+
+
+@pytest.mark.parametrize("kind,n,k,B,T,chunk,prec,reset,smooth", [
+    ("alif", 1024, 700, 12, 250, 255, "f32", False, False),   # C3 shape, one chunk
+    ("alif", 256, 700, 7, 300, 127, "f32", False, False),     # 3 chunks (pass B fused too)
+    ("lif", 96, 60, 5, 200, 63, "f64", False, False),         # KR = 64: two samples per tile, P = 8
+    ("alif", 200, 90, 3, 150, 63, "f32", True, False),        # reset, ragged n (no discard)
+    ("lif", 130, 64, 4, 100, 127, "f32", False, True),        # smooth spikes, partial tile
+    ("alif", 2048, 700, 2, 500, 511, "f32", False, False),    # C4 shape
+    ("alif", 48, 30, 1, 2100, 1023, "f64", False, False),     # long chunks, B = 1
+])
+def test_fused_projection_dynamics_is_bitwise_the_two_kernel_path(
+        kind, n, k, B, T, chunk, prec, reset, smooth, monkeypatch):
+    """K2D (projection + dynamics in one kernel) against K2 then K1: the same arithmetic in
+    the same order, so rasters, losses, readouts and the gradient accumulators are equal
+    bit for bit, for pass A, pass B (several chunks), both digit formats, reset, smooth,
+    two samples per 128-row tile and ragged neuron tiles."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.engine import EpropEngine
+    from paper_2501_11407_b200.gradients import _neuron_kwargs
+    net = P.init_network(P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=5,
+                                       precision=prec, reset=reset, seed=12))
+    x, y = poisson_batch(B, k, T, 5, seed=13)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SPB_FUSE_DYN", flag)
+        eng = EpropEngine(n, k, 5, B, alif=kind == "alif", w_f64=prec == "f64", chunk=chunk,
+                          reset=reset)
+        assert eng.fuse_dyn == (flag == "1")
+        eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+        r = torch.zeros((B, T, (n + 31) // 32), dtype=torch.int32, device="cuda")
+        eng.run(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), raster=r,
+                smooth=smooth, **_neuron_kwargs(net))
+        torch.cuda.synchronize()
+        out[flag] = [r.cpu().numpy(), eng.loss.cpu().numpy(), eng.s.cpu().numpy(),
+                     eng.grad_w_acc.cpu().numpy(), eng.grad_wout.cpu().numpy(),
+                     eng.u.cpu().numpy(), eng.a.cpu().numpy()]
+    for a, b in zip(out["1"], out["0"]):
+        assert np.array_equal(a, b)
