@@ -46,7 +46,7 @@ CONFIG_DESC = {
     "c2": "SHD-shaped LIF e-prop 700->256->20, T=250",
     "c3": "SHD-shaped ALIF e-prop 700->1024->20, T=250",
     "c4": "SSC-shaped ALIF e-prop 700->2048->35, T=500 (per-GPU shard of the 1024 batch at 8 GPUs)",
-    "c5": "C5 sweep point: ALIF e-prop 700->1024->20, T=2000 (4 chunks: per-synapse trace carried)",
+    "c5": "C5 sweep point: ALIF e-prop 700->1024->20, T=2000",
 }
 METRIC = "e-prop train samples·timesteps/s (SHD-shape ALIF); HBM GB/s vs roofline"
 UNIT = "samples*timesteps/s"
@@ -69,7 +69,7 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
-INT8_KERNELS = ("proj", "proj_dyn_a", "proj_dyn_b")
+INT8_KERNELS = ("proj",)
 
 
 def measured_traffic(cfg, kernel):
@@ -240,6 +240,8 @@ def shape_of(args, world):
     """(kind, n, k, m, T, B per rank, global batch, scaling) of the run: the config's
     per-GPU batch (weak scaling), or --global-batch split over the ranks (strong)."""
     kind, n, k, m, T, B = CONFIGS[args.config]
+    n = getattr(args, "hidden", 0) or n          # C5 sweep points (--hidden / --seq-len)
+    T = getattr(args, "seq_len", 0) or T
     if args.global_batch:
         if args.global_batch % world:
             raise SystemExit(f"--global-batch {args.global_batch} is not a multiple of {world}")
@@ -250,8 +252,10 @@ def shape_of(args, world):
 def config_dict(args, world, chunk):
     """The ``config`` object of the JSON line -- the same keys for both arms."""
     kind, n, k, m, T, B, G, scaling = shape_of(args, world)
-    return {"workload": CONFIG_DESC[args.config] + (" + recurrent W_rec" if args.recurrent
-                                                     else ""),
+    desc = CONFIG_DESC[args.config]
+    if args.config == "c5":
+        desc = f"C5 sweep point: ALIF e-prop 700->{n}->{m}, T={T}"
+    return {"workload": desc + (" + recurrent W_rec" if args.recurrent else ""),
             "batch_per_gpu": B, "global_batch": G, "seq_len": T, "n_hidden": n,
             "n_inputs": k, "n_classes": m, "chunk": chunk, "parallelism": f"dp{world}"}
 
@@ -310,6 +314,10 @@ def main():
                          "--config c4 --global-batch 1024); default: the config's batch "
                          "per GPU (weak scaling)")
     ap.add_argument("--chunk", type=int, default=0, help="0 = engine default for T")
+    ap.add_argument("--hidden", type=int, default=0,
+                    help="C5 sweep: hidden size override (BASELINE configs[4]: 256-8192)")
+    ap.add_argument("--seq-len", type=int, default=0,
+                    help="C5 sweep: sequence length override (BASELINE configs[4]: 100-10000)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -594,12 +602,6 @@ def main():
                 ln = meta                                        # int8 MACs x2, useful part
                 flops += 2.0 * P_sl * B * ln * n * k
                 byts += B * ln * k + P_sl * n * k + 8.0 * B * ln * n
-            elif name in ("proj_dyn_a", "proj_dyn_b"):
-                ln, mode, flag = meta                          # K2D: projection + dynamics
-                flops += 2.0 * P_sl * B * ln * n * k
-                byts += B * ln * k + P_sl * n * k + 32.0 * B * n   # spikes, digits, state
-                if mode >= 1:
-                    byts += 4.0 * B * (ln + 1) * n                # psi parked for the scan
             elif name in ("forward", "forward_a"):
                 ln, pid, flag = meta
                 pid = {3: 2, 4: 1}.get(pid, pid)   # raw-operand passes: same traffic
@@ -635,8 +637,6 @@ def main():
         dom = max(kernels, key=lambda nm: kernels[nm]["ms_per_step"])
         e = kernels[dom]
         names = {"proj": "input_proj_kernel (K2, int8 tcgen05)", "forward": "forward_chunk + chunk_scan (K1 pass B)",
-                 "proj_dyn_a": "input_proj_dyn_kernel (K2D pass A: int8 tcgen05 projection + fp64 dynamics)",
-                 "proj_dyn_b": "input_proj_dyn_kernel (K2D pass B: projection + dynamics, psi)",
                  "forward_a": "forward_chunk_kernel (K1 pass A)",
                  "gemm": "grad_gemm_tc_kernel (K5, bf16 hi/lo tcgen05)",
                  "carry": "alif_carry_kernel (K6, tcgen05 + eps stream)"}
@@ -712,6 +712,11 @@ def main():
                                + (" incl. the NCCL allreduce" if world > 1 else ""))
                               if graph is not None else "eager launches",
                     "dist_backend": backend if world > 1 else None},
+            "memory": {"engine_device_bytes": eng.device_bytes(),
+                       "peak_allocated_bytes": int(torch.cuda.max_memory_allocated(dev)),
+                       "note": "engine_device_bytes = every buffer of the update (sized by "
+                               "B, n, k and the chunk, not by T); the peak also holds the "
+                               "device-resident input batch [B, T, k] and the L2 flush buffer"},
             "e2e": e2e,
             "e2e_dropin": dropin,
             "gpu_launches": launches_per_step * args.steps,

@@ -68,20 +68,6 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
 int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
                          int n_pad32, int Kpad, int P, double* cur, int sm_count, int binary,
                          int probe, cudaStream_t stream);
-/* K2D Exact projection with the K1 dynamics fused (proj.cu input_proj_dyn_kernel): the
- *     K2 tiles of a sample are followed, inside the same persistent CTA, by 4 chain warps
- *     that integrate u, a (fp64, the reference's operation order) over the fresh currents
- *     while they are in L2 and then discard them -- the current never makes a DRAM round
- *     trip.  Rows of xq / cur are sample-aligned: row b*KR + s (KR % 64 == 0, len <= Tc <
- *     KR); Kpad <= 768; P = 6 (fp32 weights) or 8 (fp64).  mode 0: pass A (zbar, zsum,
- *     raster optional); 1: pass A with psi parked in psi [B][KR+1][n] (row 0 = psi_{t0-1});
- *     2: pass B (psi parked, no readout filters).  Outputs as spb_forward_chunk. */
-int spb_input_proj_dyn(int mode, const uint8_t* xq, const int8_t* wq, const int* sexp, int B,
-                       int n, int n_pad32, int Kpad, int P, int Tc, int KR, int len, int t0,
-                       int T, double alpha, double theta, double slope, double beta, double rho,
-                       double kappa, int reset, int smooth, double* cur, double* u, double* a,
-                       double* zbar, double* zsum, uint32_t* raster, float* psi, int sm_count,
-                       int binary, cudaStream_t stream);
 
 /* K1  Neuron dynamics over one time chunk from the exact current cur [B*KR][n] (row
  *     b*KR+s, sample-aligned): ALIF/LIF state update, spike and surrogate derivative.
@@ -207,6 +193,15 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
                          int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
                          int store_eps, const void* xs_hi, const void* xs_lo,
                          cudaStream_t stream);
+/* K6p The same carry on CTA pairs (tcgen05.mma.cta_group::2, 256 neurons x 256 inputs per
+ *     pair; eps streamed in 128 x 32 TMA boxes through an 8-slot ring): same arguments and
+ *     results as spb_alif_carry_chunk; each of the `splits` sample ranges runs on
+ *     2 * ceil(kp/256) * ceil(n_pad/256) CTAs.  n_pad % 128 == 0, KR % 32 == 0. */
+int spb_alif_carry_pair(const void* wh, const void* wl, int ldw, const void* xh, const void* xl,
+                        const float* mdt, float* eps, float* partial, int B, int n, int n_pad,
+                        int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
+                        int store_eps, const void* xs_hi, const void* xs_lo,
+                        cudaStream_t stream);
 
 /* K6r The ALIF trace PAIR (G_u, G_a) of reset=True carried across chunks on tcgen05
  *     (elig_reset.cu): with (W_u, W_a), M, Dt from K1r and the raw input x (K4, alpha=0)

@@ -26,8 +26,6 @@ SIGNATURES = {
     "spb_pack_spikes_xh": [P, LL, I, I, I, I, I, I, I, P, P, P],
     "spb_input_proj": [P, P, P, I, I, I, I, I, P, I, I, P],
     "spb_input_proj_probe": [P, P, P, I, I, I, I, I, P, I, I, I, P],
-    "spb_input_proj_dyn": [I, P, P, P, I, I, I, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I,
-                           P, P, P, P, P, P, P, I, I, P],
     "spb_forward_chunk": [I, P, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I, I,
                           P, P, P, P, P, P, P, P, P, P, P, P, P, I, P, P, P],
     "spb_xbar_chunk": [P, LL, LL, I, I, I, I, I, I, D, P, P, P, P],
@@ -38,6 +36,8 @@ SIGNATURES = {
     "spb_grad_gemm_partials": [P, P, I, P, P, I, I, I, I, I, P, I, LL, P],
     "spb_grad_gemm_simt": [P, P, I, P, P, I, I, I, I, P, I, P],
     "spb_alif_carry_chunk": [P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I, I, P, P,
+                             P],
+    "spb_alif_carry_pair": [P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I, I, P, P,
                              P],
     "spb_reset_carry_chunk": [P, P, P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I,
                               I, P],

@@ -451,308 +451,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
 }
 
-// ------------------------------------------------------------------------------------
-// K2D: the exact projection with the neuron dynamics fused in (K2 + K1 in one kernel).
-//
-// Rows are laid out sample-aligned (row b*KR + s, KR = Tc + 1 a multiple of 64), so a
-// unit of work -- one sample's tiles for one 32-neuron tile (KR >= 128: KR/128 tiles) or
-// one tile holding two samples (KR = 64) -- never straddles CTAs.  Each persistent CTA
-// walks a contiguous range of units; warps 0-9 are K2 unchanged (TMA, MMA issue, 8
-// epilogue warps writing the fp64 currents), and 4 chain warps run the dynamics of K1
-// (gradients.py:118-129 in the reference's operation order, fp64) over the tiles the
-// epilogue has finished: lane = neuron, one sample's steps in order, the current read
-// back while it is still in L2 and the lines then discarded (no DRAM write-back, no
-// DRAM re-read: the 8 B/neuron-step round trip of K2 -> K1 disappears).  Chain warp w
-// takes the CTA's units w, w+4, ... (independent samples), so 4 dependency chains are in
-// flight per SM.  The epilogue publishes finished tiles through a monotonic shared
-// counter (release / acquire, CTA scope); it never waits for the chains.
-// MODE 0: pass A (raster, zbar, zsum);  1: pass A + psi parked for the scan;
-//      2: pass B (psi parked).  reset / smooth are runtime flags (warp-uniform).
-// ------------------------------------------------------------------------------------
-struct DynParams {
-  int B, n, Tc, KR, len, t0, T;
-  double alpha, theta, slope, beta, rho, kappa;
-  int reset, smooth;
-};
-
-constexpr int CHAIN_WARPS = 4;
-constexpr int THREADS_D = THREADS + CHAIN_WARPS * 32;
-
-__device__ __forceinline__ void red_release_add(uint32_t saddr, uint32_t v) {
-  asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_shared(uint32_t saddr) {
-  uint32_t v;
-  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
-  return v;
-}
-
-template <int MODE>
-__device__ __forceinline__ void chain_sample(const DynParams& P, const double* __restrict__ cur,
-                                             int b, int i0, int lane, int s_lo, int s_hi,
-                                             double& u, double& a, double& zbar, double& zsum,
-                                             double& d_prev, uint32_t* __restrict__ raster,
-                                             float* __restrict__ psis, bool discard) {
-  constexpr bool PASSA = MODE <= 1, PARK = MODE >= 1;
-  const int n = P.n;
-  const int i = i0 + lane;
-  const bool valid = i < n;
-  const int nw = (n + 31) >> 5;
-  const double theta = P.theta, beta = P.beta, alpha = P.alpha, rho = P.rho, kappa = P.kappa;
-  const double slope_d = P.slope;
-  const float slope = (float)P.slope;
-  const bool reset = P.reset != 0, smooth = P.smooth != 0;
-  const double* cp = cur + ((long long)b * P.KR + s_lo) * n + (valid ? i : i0);
-  float* pp = PARK ? psis + ((long long)b * (P.KR + 1) + s_lo + 1) * n + (valid ? i : i0) : nullptr;
-  uint32_t* rp = (PASSA && raster != nullptr)
-                     ? raster + ((long long)b * P.T + P.t0 + s_lo) * nw + (i0 >> 5) : nullptr;
-  // lanes 0 / 16 discard the two 128-byte lines of the row once it is consumed
-  const bool dl = discard && (lane & 15) == 0 && i0 + lane + 16 <= n;
-  const int len = s_hi - s_lo;
-  double In[8];
-#pragma unroll
-  for (int u8 = 0; u8 < 8; ++u8) In[u8] = u8 < len ? cp[(long long)u8 * n] : 0.0;
-  const long long n8 = 8LL * n;
-  for (int s8 = 0; s8 < len; s8 += 8) {
-    double Ib[8];
-#pragma unroll
-    for (int u8 = 0; u8 < 8; ++u8) Ib[u8] = In[u8];
-    const double* cq = cp;
-    cp += n8;
-#pragma unroll
-    for (int u8 = 0; u8 < 8; ++u8) In[u8] = (s8 + 8 + u8 < len) ? cp[(long long)u8 * n] : 0.0;
-#pragma unroll
-    for (int u8 = 0; u8 < 8; ++u8) {
-      if (s8 + u8 < len) {
-        const double z_prev = spike_value(d_prev, smooth, slope_d);
-        a = __dadd_rn(__dmul_rn(rho, a), z_prev);
-        u = __dadd_rn(__dmul_rn(alpha, u), Ib[u8]);
-        if (reset) u = __dsub_rn(u, __dmul_rn(theta, z_prev));
-        const double d = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
-        if (PASSA) {
-          const double zv = spike_value(d, smooth, slope_d);
-          zbar = __dadd_rn(__dmul_rn(kappa, zbar), zv);
-          zsum = __dadd_rn(zsum, zbar);
-          const unsigned bal = __ballot_sync(0xffffffffu, zv > 0.5 && valid);
-          if (rp != nullptr) {
-            if (lane == 0) rp[0] = bal;
-            rp += nw;
-          }
-        }
-        if (PARK) {
-          if (valid) pp[0] = surrogate_grad_f32((float)d, slope);
-          pp += n;
-        }
-        d_prev = d;
-        if (dl)
-          asm volatile("discard.global.L2 [%0], 128;" ::"l"(cq + (long long)u8 * n) : "memory");
-      }
-    }
-  }
-}
-
-template <int P, int XS, bool BIN, int MODE>
-__global__ void __launch_bounds__(THREADS_D, 1)
-    input_proj_dyn_kernel(const __grid_constant__ CUtensorMap tm_x,
-                          const __grid_constant__ CUtensorMap tm_w, const int* __restrict__ sexp,
-                          double* __restrict__ out, int n_pad32, int nkb, DynParams D,
-                          double* __restrict__ u_st, double* __restrict__ a_st,
-                          double* __restrict__ zbar_st, double* __restrict__ zsum_st,
-                          uint32_t* __restrict__ raster, float* __restrict__ psis) {
-  using C = ResCfg<P, XS>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* wsm = smem;
-  uint8_t* xsm = smem + C::W_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xsm + XS * TILE_A);
-  uint64_t* xfull = bars;
-  uint64_t* xempty = bars + XS;
-  uint64_t* tfull = bars + 2 * XS;
-  uint64_t* tempty = bars + 2 * XS + 2;
-  uint64_t* wfull = bars + 2 * XS + 4;
-  uint64_t* wempty = bars + 2 * XS + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * XS + 6);
-  uint32_t* stored = tmem_slot + 1;   // epilogue threads x finished tiles (monotonic)
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = D.n, M = D.B * D.KR;
-  const int G = D.KR >= BM ? D.KR / BM : 1;          // tiles per unit
-  const int S = D.KR >= BM ? 1 : BM / D.KR;          // samples per unit
-  const int upn = (D.B + S - 1) / S;                 // units per neuron tile
-  const int n_tiles = (n + NT - 1) / NT;
-  const long long total = (long long)upn * n_tiles;
-  const int u_begin = (int)(total * blockIdx.x / gridDim.x);
-  const int u_end = (int)(total * (blockIdx.x + 1) / gridDim.x);
-  const int ntl = (u_end - u_begin) * G;             // local tiles
-  auto tile_of = [&](int lt, int& nt, int& mt) {
-    const int u = u_begin + lt / G;
-    nt = u / upn;
-    mt = (u % upn) * G + lt % G;
-  };
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < XS; ++s) {
-      mbar_init(smem_u32(&xfull[s]), 1);
-      mbar_init(smem_u32(&xempty[s]), 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(smem_u32(&tfull[a]), 1);
-      mbar_init(smem_u32(&tempty[a]), EPI_WARPS);
-    }
-    mbar_init(smem_u32(wfull), 1);
-    mbar_init(smem_u32(wempty), 1);
-    *stored = 0u;
-    mbar_fence_init();
-    tma_prefetch_desc(&tm_x);
-    tma_prefetch_desc(&tm_w);
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem_base = *tmem_slot;
-  pdl_enter();
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int it = 0, cur_nt = -1, wl = 0;
-      for (int lt = 0; lt < ntl; ++lt) {
-        int nt, mt;
-        tile_of(lt, nt, mt);
-        if (nt != cur_nt) {
-          mbar_wait(smem_u32(wempty), (wl & 1) ^ 1);
-          const uint32_t fb = smem_u32(wfull);
-          mbar_expect_tx(fb, nkb * C::WBLK);
-          for (int kb = 0; kb < nkb; ++kb)
-#pragma unroll
-            for (int p = 0; p < P; ++p)
-              tma_load_2d(smem_u32(wsm + kb * C::WBLK + p * NT * BK), &tm_w, fb, kb * BK,
-                          p * n_pad32 + nt * NT);
-          cur_nt = nt;
-          ++wl;
-        }
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % XS;
-          mbar_wait(smem_u32(&xempty[s]), ((it / XS) & 1) ^ 1);
-          const uint32_t fb = smem_u32(&xfull[s]);
-          mbar_expect_tx(fb, TILE_A);
-          tma_load_2d(smem_u32(xsm + s * TILE_A), &tm_x, fb, kb * BK, mt * BM);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    int it = 0, cur_nt = -1, wl = 0;
-    for (int lt = 0; lt < ntl; ++lt) {
-      int nt, mt;
-      tile_of(lt, nt, mt);
-      if (nt != cur_nt) {
-        mbar_wait(smem_u32(wfull), wl & 1);
-        cur_nt = nt;
-        ++wl;
-      }
-      const int a = lt & 1;
-      mbar_wait(smem_u32(&tempty[a]), ((lt >> 1) & 1) ^ 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t dacc = tmem_base + (uint32_t)(a * 256);
-      for (int kb = 0; kb < nkb; ++kb, ++it) {
-        const int s = it % XS;
-        mbar_wait(smem_u32(&xfull[s]), (it / XS) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        mma_i8_x4(dacc, desc_k_sw128(smem_u32(xsm + s * TILE_A)),
-                  desc_k_sw128(smem_u32(wsm + kb * C::WBLK)), Cfg<P>::IDESC, kb ? 1u : 0u);
-        commit(smem_u32(&xempty[s]));
-      }
-      commit(smem_u32(&tfull[a]));
-      int nt2 = -1, mt2;
-      if (lt + 1 < ntl) tile_of(lt + 1, nt2, mt2);
-      if (nt2 != nt) commit(smem_u32(wempty));
-    }
-  } else if (warp < 2 + EPI_WARPS) {
-    const int q = warp & 3;
-    const int hh = (warp - 2) >> 2;
-    int sc_nt = -1;
-    double sc[NH];
-    for (int lt = 0; lt < ntl; ++lt) {
-      int nt, mt;
-      tile_of(lt, nt, mt);
-      const int a = lt & 1;
-      const int i0 = nt * NT + hh * NH;
-      if (nt != sc_nt) {
-#pragma unroll
-        for (int c = 0; c < NH; ++c)
-          sc[c] = digits_pow2(((i0 + c < n) ? __ldg(sexp + i0 + c) : 0) - Digits<P>::F);
-        sc_nt = nt;
-      }
-      mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      proj_epilogue_tile<P, BIN>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH),
-                                 sc, out, M, n, mt * BM + q * 32 + lane, i0, smem_u32(&tempty[a]),
-                                 lane);
-      // publish: this thread's current stores of the tile precede the release
-      red_release_add(smem_u32(stored), 1u);
-    }
-  } else {
-    // chain warps: the dynamics of K1 over finished tiles, one sample chain per lane
-    const int cw = warp - 2 - EPI_WARPS;
-    const uint32_t st_addr = smem_u32(stored);
-    const bool discard = (n & 15) == 0;
-    const int nu = u_end - u_begin;
-    for (int lu = cw; lu < nu; lu += CHAIN_WARPS) {
-      const int u = u_begin + lu;
-      const int nt = u / upn, mu = u % upn;
-      const int i0 = nt * NT;
-      const int i = i0 + lane;
-      const bool valid = i < n;
-      for (int si = 0; si < S; ++si) {
-        const int b = mu * S + si;
-        if (b >= D.B) break;
-        const long long bi = (long long)b * n + (valid ? i : i0);
-        double uu = 0.0, aa = 0.0, zbar = 0.0, zsum = 0.0;
-        if (D.t0 > 0 && valid) {
-          uu = u_st[bi];
-          aa = a_st[bi];
-          if (MODE <= 1) {
-            zbar = zbar_st[bi];
-            zsum = zsum_st[bi];
-          }
-        }
-        double d_prev = __dsub_rn(__dsub_rn(uu, D.theta), __dmul_rn(D.beta, aa));
-        if (MODE >= 1 && valid)
-          psis[(long long)b * (D.KR + 1) * n + i] = surrogate_grad_f32((float)d_prev, (float)D.slope);
-        for (int g = 0; g < G; ++g) {
-          const int lt = lu * G + g;
-          const int s_lo = D.KR >= BM ? g * BM : 0;
-          const int s_hi = min(D.len, D.KR >= BM ? s_lo + BM : D.KR);
-          // wait for all epilogue threads to have published tile lt
-          const uint32_t need = (uint32_t)(lt + 1) * (EPI_WARPS * 32);
-          while (ld_acquire_shared(st_addr) < need) __nanosleep(64);
-          if (s_lo < s_hi)
-            chain_sample<MODE>(D, out, b, i0, lane, s_lo, s_hi, uu, aa, zbar, zsum, d_prev,
-                               raster, psis, discard);
-        }
-        if (valid) {
-          u_st[bi] = uu;
-          a_st[bi] = aa;
-          if (MODE <= 1) {
-            zbar_st[bi] = zbar;
-            zsum_st[bi] = zsum;
-          }
-        }
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
-}
-
 template <int P, bool BIN>
 __global__ void __launch_bounds__(THREADS, 1)
     input_proj_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
@@ -1192,65 +890,3 @@ int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, i
 }
 
 }  // extern "C"
-
-// K2D launcher (see input_proj_dyn_kernel): exact projection + K1 dynamics in one kernel.
-extern "C" int spb_input_proj_dyn(int mode, const uint8_t* xq, const int8_t* wq, const int* sexp,
-                                  int B, int n, int n_pad32, int Kpad, int P, int Tc, int KR,
-                                  int len, int t0, int T, double alpha, double theta,
-                                  double slope, double beta, double rho, double kappa, int reset,
-                                  int smooth, double* cur, double* u, double* a, double* zbar,
-                                  double* zsum, uint32_t* raster, float* psi, int sm_count,
-                                  int binary, cudaStream_t stream) {
-  using namespace spb;
-  SPB_CHECK_ARG(mode >= 0 && mode <= 2, "spb_input_proj_dyn: mode must be 0, 1 or 2");
-  SPB_CHECK_ARG(xq && wq && sexp && cur && u && a && B > 0 && n > 0 && n_pad32 >= n &&
-                    n_pad32 % proj::NT == 0 && Kpad % proj::BK == 0 &&
-                    Kpad <= 768 && (P == 6 || P == 8),
-                "spb_input_proj_dyn: bad args (P 6 / 8, Kpad <= 768)");
-  SPB_CHECK_ARG(KR % 64 == 0 && KR >= Tc + 1 && len >= 1 && len <= Tc && t0 >= 0 && t0 + len <= T,
-                "spb_input_proj_dyn: bad sizes (KR %% 64, len <= Tc < KR)");
-  SPB_CHECK_ARG(mode == 2 || (zbar && zsum), "spb_input_proj_dyn: pass A needs zbar/zsum");
-  SPB_CHECK_ARG(mode == 0 || psi, "spb_input_proj_dyn: psi scratch required");
-  SPB_CHECK_ARG((reinterpret_cast<uintptr_t>(xq) | reinterpret_cast<uintptr_t>(wq)) % 16 == 0,
-                "spb_input_proj_dyn: operands must be 16-byte aligned");
-  const int M = B * KR;
-  CUtensorMap mx, mw;
-  const bool ok =
-      make_tmap_2d(&mx, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, Kpad, M, Kpad, proj::BK, proj::BM,
-                   CU_TENSOR_MAP_SWIZZLE_128B) &&
-      make_tmap_2d(&mw, wq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, Kpad, (uint64_t)P * n_pad32, Kpad,
-                   proj::BK, proj::NT, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!ok) {
-    set_error("spb_input_proj_dyn: cuTensorMapEncodeTiled failed");
-    return 3;
-  }
-  proj::DynParams D{B, n, Tc, KR, len, t0, T, alpha, theta, slope, beta, rho, kappa, reset, smooth};
-  const int S = KR >= proj::BM ? 1 : proj::BM / KR;
-  const long long units = (long long)((B + S - 1) / S) * ceil_div(n, proj::NT);
-  const int grid = (int)std::max<long long>(1, std::min<long long>(units, sm_count > 0 ? sm_count : 148));
-  const int nkb = Kpad / proj::BK;
-  const bool bin = binary != 0 && P == 6;
-#define SPB_K2D(PP, XS, BN, MD)                                                                 \
-  do {                                                                                          \
-    auto kfn = proj::input_proj_dyn_kernel<PP, XS, BN, MD>;                                     \
-    constexpr int sm = proj::ResCfg<PP, XS>::SMEM;                                              \
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                 \
-    pdl_launch(kfn, grid, proj::THREADS_D, sm, stream, mx, mw, sexp, cur, n_pad32, nkb, D, u, a, \
-               zbar, zsum, raster, psi);                                                         \
-  } while (0)
-#define SPB_K2D_MODES(PP, XS, BN)            \
-  if (mode == 0) SPB_K2D(PP, XS, BN, 0);     \
-  else if (mode == 1) SPB_K2D(PP, XS, BN, 1); \
-  else SPB_K2D(PP, XS, BN, 2)
-  if (P == 6 && bin) {
-    SPB_K2D_MODES(6, 5, true);
-  } else if (P == 6) {
-    SPB_K2D_MODES(6, 5, false);
-  } else {
-    SPB_K2D_MODES(8, 2, false);
-  }
-#undef SPB_K2D_MODES
-#undef SPB_K2D
-  SPB_CHECK_LAUNCH("input_proj_dyn");
-  return 0;
-}

@@ -159,9 +159,7 @@ class EpropEngine:
         self.Kpad = _round_up(k, 128)
         self.n_pad32 = _round_up(n, 32)
         self.P = 8 if self.w_f64 else 6   # digit format, csrc/digits.cuh
-        # sample-aligned rows b*KR + s (KR = Tc + 1, a multiple of 64): a sample's rows
-        # start on a 128-row tile (or share one with one other sample), so the fused
-        # projection + dynamics kernel (K2D) never splits a sample across CTAs
+        # sample-aligned rows b*KR + s (KR = Tc + 1, a multiple of 64; rows s >= len zero)
         self.xq = torch.zeros((B * self.KR, self.Kpad), dtype=torch.uint8, device=dev)
         self.cur = torch.empty((B * self.KR, n), dtype=f64, device=dev)
         self.wq = torch.zeros((self.P, self.n_pad32, self.Kpad), dtype=torch.int8, device=dev)
@@ -186,12 +184,11 @@ class EpropEngine:
         # weights
         self.w = torch.empty((n, k), dtype=f64 if self.w_f64 else f32, device=dev)
         self.wout = torch.empty((m, n), dtype=f64, device=dev)
-        # K2D (projection + dynamics fused, proj.cu) unless SPB_FUSE_DYN=0; the recurrent
-        # layer keeps K2 + K1rec, the fp64-weight digits (P = 8) need Kpad <= 768 too
-        self.fuse_dyn = (os.environ.get("SPB_FUSE_DYN", "1") != "0" and not self.recurrent
-                         and self.Kpad <= 768)
         # fold the input filter into the one-chunk coefficients (SPB_FILT=0: xbar operand)
         self.filt = os.environ.get("SPB_FILT", "1") != "0"
+        # the single-trace carry (ALIF, or LIF with reset) on CTA pairs (K6p, elig.cu)
+        # unless SPB_CARRY_PAIR=0 (single-CTA K6)
+        self.carry_pair = os.environ.get("SPB_CARRY_PAIR", "1") != "0" and self.ntr == 1
         self.pack_xh = os.environ.get("SPB_PACK_XH", "1") != "0"
         # opt-in memory-for-time trade (off by default: memory then grows with T): park the
         # psi of every chunk in pass A when all of it fits `park_budget` bytes, so pass B
@@ -220,6 +217,17 @@ class EpropEngine:
         self.partial = self.grad_w_acc = self.grad_wout = self.zchunk = self.xq2 = None
         if self.grad:
             self._alloc_grad_buffers()
+
+    def device_bytes(self) -> int:
+        """Device memory held by the engine's buffers (each tensor counted once)."""
+        seen, total = set(), 0
+        for v in vars(self).values():
+            if isinstance(v, torch.Tensor) and v.device.type == "cuda":
+                key = v.untyped_storage().data_ptr()
+                if key not in seen:
+                    seen.add(key)
+                    total += v.untyped_storage().nbytes()
+        return total
 
     def _alloc_grad_buffers(self):
         """Pass-B buffers: psi scratch, the chunk GEMM / carry operands (bf16 hi/lo,
@@ -254,8 +262,11 @@ class EpropEngine:
                 self.wa_hi = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
                 self.wa_lo = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
                 self.eps2 = torch.zeros((B, self.n_pad, self.ke), dtype=f32, device=dev)
-            bn6 = 128 if self.ntr == 1 else 64
-            tiles6 = (self.kp // bn6) * (self.n_pad // 128)
+            if self.carry_pair:   # K6p: CTA pairs over 256 x 256 synapse tiles
+                tiles6 = 2 * math.ceil(self.kp / 256) * math.ceil(self.n_pad / 256)
+            else:
+                bn6 = 128 if self.ntr == 1 else 64
+                tiles6 = (self.kp // bn6) * (self.n_pad // 128)
             self.splits6 = _wave_split(tiles6, B, sms)
         else:
             self.w_hi = self.w_lo = self.mdt = self.eps = None
@@ -328,20 +339,6 @@ class EpropEngine:
             return
         _lib.call("spb_pack_spikes", ctypes_void(xp), strideb, self.B, self.k, int(bits), ln,
                   self.KR, self.Kpad, 0, ctypes_void(self.xq.data_ptr()), st)
-
-    def _project_dyn(self, mode, ln, t0, T, common, raster, psi, st, timed, binary, tag):
-        """K2D: the exact projection with the K1 dynamics fused (proj.cu
-        input_proj_dyn_kernel); mode 0 = pass A, 1 = pass A + psi parked, 2 = pass B."""
-        v = ctypes_void
-        alpha, theta, slope, beta, rho, kappa, reset, _alif, smooth = common
-        timed(tag[0], tag[1], "spb_input_proj_dyn", int(mode), v(self.xq.data_ptr()),
-              v(self.wq.data_ptr()), v(self.sexp.data_ptr()), self.B, self.n, self.n_pad32,
-              self.Kpad, self.P, self.Tc, self.KR, ln, t0, T, alpha, theta, slope, beta, rho,
-              kappa, reset, smooth, v(self.cur.data_ptr()), v(self.u.data_ptr()),
-              v(self.a.data_ptr()), v(self.zbar.data_ptr()) if mode < 2 else None,
-              v(self.zsum.data_ptr()) if mode < 2 else None,
-              v(raster.data_ptr()) if raster is not None else None, psi, self.sm_count,
-              int(bool(binary)), st)
 
     def _project(self, ln, st, timed=None, binary=False):
         """K2: cur = W x_t exactly on INT8 tensor cores from the packed chunk (binary:
@@ -523,15 +520,6 @@ class EpropEngine:
                      xl_ptr, sst)
                 self._ev["xbar"].record(self.side)
                 self.launches += 1
-            if self.fuse_dyn:
-                # K2D: projection + dynamics in one kernel (psi parked for the scan when
-                # pass B will not recompute this chunk)
-                mode = 1 if (park or (one and not forward_only)) else 0
-                self._project_dyn(mode, ln, t0, T, common, raster,
-                                  psi_ptr(c) if mode else None, st, timed, binary,
-                                  ("proj_dyn_a", (ln, mode, one)))
-                self.launches += 2
-                continue
             if not (side_x and self.xbar_sched == "fa"):
                 self._project(ln, st, timed, binary)
             if self.recurrent:
@@ -575,18 +563,14 @@ class EpropEngine:
                 self.launches += 1
             elif not one:  # one chunk: xq and cur of pass A are still valid (same W, same x)
                 pack_chunk(c, ln)
-                if self.fuse_dyn:   # K2D pass B: the chunk's psi parked for the scan
-                    self._project_dyn(2, ln, t0, T, common, None, psi_ptr(c), st, timed,
-                                      binary, ("proj_dyn_b", (ln, 2, carry_out)))
-                else:
-                    self._project(ln, st, timed, binary)
+                self._project(ln, st, timed, binary)
                 if self.recurrent:
                     self._forward_rec(1, ln, t0, T, common, None, True, st, timed,
                                       (ln, 1, carry_out))
                     self.launches += 1
                 self.launches += 2
-            # one chunk (pass A parked psi), K2D or K1rec (park psi themselves): scan only
-            pid = 2 if (one or park or self.recurrent or self.fuse_dyn) else 1
+            # one chunk (pass A parked psi) or K1rec (parks psi itself): scan only
+            pid = 2 if (one or park or self.recurrent) else 1
             if filt:
                 pid = 3 if pid == 2 else 4
             timed("forward", (ln, pid, carry_out), "spb_forward_chunk", pid,
@@ -641,7 +625,8 @@ class EpropEngine:
             if self.ntr and (c > 0 or not last):
                 # first chunk: E0 = 0 (nothing to add, only carry); last chunk: no carry
                 if self.ntr == 1:
-                    timed("carry", (ln, c > 0, not last), "spb_alif_carry_chunk",
+                    timed("carry", (ln, c > 0, not last),
+                          "spb_alif_carry_pair" if self.carry_pair else "spb_alif_carry_chunk",
                           v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()), self.ldc,
                           v(self.xh.data_ptr()), xl_ptr, v(self.mdt.data_ptr()),
                           v(self.eps.data_ptr()), v(part6), B, n, self.n_pad, self.kx, self.ke,

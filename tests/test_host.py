@@ -108,21 +108,19 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     eng.run(x, y)
     names = [c[0] for c in rec.calls]
     nch = (T + chunk - 1) // chunk
-    assert eng.fuse_dyn   # K2D: projection + dynamics in one launch per chunk and pass
-    assert names.count("spb_forward_chunk") == nch        # pass B: the chunk scans only
-    assert names.count("spb_input_proj_dyn") == (2 * nch if nch > 1 else 1)
+    assert names.count("spb_forward_chunk") == 2 * nch
     # a single chunk reuses pass A's packed spikes and current in pass B
     # one chunk: the pack also writes K5's raw-spike operand (spb_pack_spikes_xh, no K4)
     packs = names.count("spb_pack_spikes") + names.count("spb_pack_spikes_xh")
     assert packs == (2 * nch if nch > 1 else 1)
     pack_xh = nch == 1 and 30 % 4 == 0          # byte rows must be 4-byte aligned (k = 30)
     assert names.count("spb_pack_spikes_xh") == (1 if pack_xh else 0)
-    assert names.count("spb_input_proj") == 0
+    assert names.count("spb_input_proj") == (2 * nch if nch > 1 else 1)
     assert names.count("spb_slice_weights") == 0
     assert sum(names.count(x) for x in XB) == (0 if pack_xh else nch)
     # K5 per chunk, plus the K = B GEMM of the carried filter state for chunks after the first
     assert names.count("spb_grad_gemm_partials") == nch + (nch - 1)
-    carries = [c[1] for c in rec.calls if c[0] == "spb_alif_carry_chunk"]
+    carries = [c[1] for c in rec.calls if c[0] in ("spb_alif_carry_chunk", "spb_alif_carry_pair")]
     if alif:
         # no carry launch for a single chunk; chunk 0 only carries, the last only adds M E0
         assert len(carries) == (nch if nch > 1 else 0)
@@ -135,12 +133,9 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
         assert not carries
     assert names.count("spb_readout_loss") == 1
     # spb_forward_chunk pass B launches two kernels (dynamics + chunk scan)
-    passb = sum(1 for c in rec.calls if c[0] == "spb_forward_chunk" and c[1][0] in (1, 4))
-    assert passb == 0
-    modes = [c[1][0] for c in rec.calls if c[0] == "spb_input_proj_dyn"]
+    passb = sum(1 for c in rec.calls if c[0] == "spb_forward_chunk" and c[1][0] == 1)
     if nch == 1:  # pass A parks psi, pass B runs the scan only, input filter folded in
-        assert modes == [1]
-        assert [c[1][0] for c in rec.calls if c[0] == "spb_forward_chunk"] == [3]
+        assert [c[1][0] for c in rec.calls if c[0] == "spb_forward_chunk"] == [0, 3]
         # the raw-spike operand: written by the pack, K5 gets no B-lo
         gm = [c[1] for c in rec.calls if c[0] == "spb_grad_gemm_partials"]
         assert all(a[4] is None for a in gm)
@@ -162,8 +157,8 @@ def test_engine_reset_dry_run(monkeypatch, alif):
     assert xb and all(a[8] == 1 and a[9] == 0.0 for a in xb)      # fresh, alpha = 0
     fw = [c[1] for c in rec.calls if c[0] == "spb_forward_chunk"]
     assert all(a[15] == 1 for a in fw)                              # reset flag
-    carry = "spb_reset_carry_chunk" if alif else "spb_alif_carry_chunk"
-    other = "spb_alif_carry_chunk" if alif else "spb_reset_carry_chunk"
+    carry = "spb_reset_carry_chunk" if alif else "spb_alif_carry_pair"
+    other = "spb_alif_carry_pair" if alif else "spb_reset_carry_chunk"
     names = [c[0] for c in rec.calls]
     assert names.count(carry) == 4 and names.count(other) == 0     # 4 chunks
     assert eng.mdt.shape[-1] == (8 if alif else 2)
@@ -196,14 +191,13 @@ def test_engine_forward_only_dry_run(monkeypatch):
     eng.run(torch.zeros((6, 150, 30), dtype=torch.uint8), torch.zeros(6, dtype=torch.int64),
             forward_only=True, smooth=True)
     names = [c[0] for c in rec.calls]
-    assert names.count("spb_input_proj_dyn") == 3 and names.count("spb_forward_chunk") == 0
+    assert names.count("spb_forward_chunk") == 3 and names.count("spb_input_proj") == 3
     assert names[-1] == "spb_readout_loss"
-    for n in ("spb_xbar_chunk", "spb_xbar_chunk_seg", "spb_grad_gemm_partials", "spb_alif_carry_chunk",
+    for n in ("spb_xbar_chunk", "spb_xbar_chunk_seg", "spb_grad_gemm_partials", "spb_alif_carry_pair",
               "spb_readout_grad"):
         assert n not in names
-    # smooth flag reaches the kernel; pass A mode 0 (nothing parked)
-    dyn = [c[1] for c in rec.calls if c[0] == "spb_input_proj_dyn"]
-    assert all(a[21] == 1 and a[0] == 0 for a in dyn)
+    # smooth flag reaches the kernel (argument after `alif`)
+    assert all(c[1][17] == 1 for c in rec.calls if c[0] == "spb_forward_chunk")
 
 
 def test_engine_rejects_bad_inputs():

@@ -262,7 +262,7 @@ def test_int8_tensor_core_projection_is_exact(w_f64):
     eng._pack(xd.data_ptr(), T * k, False, T, st)
     eng._project(T, st)
     torch.cuda.synchronize()
-    got = eng.cur.cpu().numpy().reshape(B, eng.Tc, n)[:, :T]
+    got = eng.cur.cpu().numpy().reshape(B, eng.KR, n)[:, :T]
     exact = np.einsum("btk,nk->btn", x.astype(np.longdouble), w.astype(np.longdouble))
     err = np.abs(got.astype(np.longdouble) - exact)
     # one fp64 rounding of the exact sum (half an ulp) + the digit truncation: every
@@ -302,7 +302,7 @@ def test_binary_recombination_is_bitwise_the_two_part_path(k):
         outs.append(eng.cur.cpu().numpy().copy())
     assert np.array_equal(outs[0], outs[1])
     exact = np.einsum("btk,nk->btn", x.astype(np.longdouble), w.astype(np.longdouble))
-    got = outs[1].reshape(B, eng.Tc, n)[:, :T]
+    got = outs[1].reshape(B, eng.KR, n)[:, :T]
     assert np.max(np.abs(got - exact.astype(np.float64))) <= 2.3e-16 * np.max(np.abs(exact))
 
 
