@@ -617,11 +617,11 @@ def main():
                 flops += (4.0 if raw else 6.0) * n * k * B * (ln + 1)
                 byts += 4.0 * n * B * KR + (2.0 if raw else 4.0) * k * B * KR
             elif name == "carry":
-                ln, ld, stv = meta
+                ln, ld, stv, raw = meta             # raw spikes: 2 MMAs, x hi only (2 B)
                 byts += 4.0 * B * n * k * (int(ld) + int(stv)) + 8.0 * B * n
                 if stv:
-                    byts += 4.0 * (n + k) * B * KR
-                    flops += 6.0 * n * k * B * KR
+                    byts += (4.0 * n + (2.0 if raw else 4.0) * k) * B * KR
+                    flops += (4.0 if raw else 6.0) * n * k * B * KR
         ent = {"ms_per_step": t_tot * 1e3 / steps_bd, "share_of_step": t_tot * 1e3 / steps_bd / ms,
                "launches_per_step": len(lst) / steps_bd}
         if byts:
@@ -639,7 +639,7 @@ def main():
         names = {"proj": "input_proj_kernel (K2, int8 tcgen05)", "forward": "forward_chunk + chunk_scan (K1 pass B)",
                  "forward_a": "forward_chunk_kernel (K1 pass A)",
                  "gemm": "grad_gemm_tc_kernel (K5, bf16 hi/lo tcgen05)",
-                 "carry": "alif_carry_kernel (K6, tcgen05 + eps stream)"}
+                 "carry": "alif_carry_pair_kernel (K6p, cta_group::2 tcgen05 + eps stream)"}
         if args.recurrent:
             names["forward_a"] = "forward_rec_kernel (K1rec pass A: recurrent spike gather)"
         if e.get("tensor_frac", 0) >= e.get("hbm_frac", 0) and "tensor_tflops" in e:

@@ -176,13 +176,16 @@ int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* 
 int spb_grad_gemm_simt(const void* ah, const void* al, int lda, const void* bh, const void* bl,
                        int ldb, int M, int N, int K, double* grad, int ldg, cudaStream_t stream);
 
-/* K6  ALIF adaptation trace carried across chunks on tcgen05 tensor cores (elig.cu):
+/* K6  ALIF adaptation trace carried across chunks on tcgen05 tensor cores (elig.cu), on
+ *     CTA pairs (tcgen05.mma.cta_group::2: 256 neurons x 256 inputs per pair, eps streamed
+ *     in 128 x 32 TMA boxes through an 8-slot ring); each of the `splits` sample ranges
+ *     runs on 2 * ceil(kp/256) * ceil(n_pad/256) CTAs:
  *       E_end[b,i,:] = Dt[b,i] E0[b,i,:] + sum_rho W_rho[b,i] xbar_rho[b,:]   (if do_mma)
  *       partial[z][i][j] = sum_{b in split z} M[b,i] E0[b,i,j]
  *     eps [B][n_pad][ke] fp32 (E0 read if load_eps, E_end written if store_eps), w* the K1s
  *     operand [B*KR][ldw] and x* the K4 operand [B*KR][kp] (both MN-major), mdt from K1s;
  *     partial [splits][n_pad][kp].
- *     n_pad % 128 == 0, kp % 128 == 0, ke % 4 == 0, KR % 64 == 0.  Replaces the ALIF G_a
+ *     n_pad % 128 == 0, kp % 128 == 0, ke % 4 == 0, KR % 32 == 0.  Replaces the ALIF G_a
  *     block of eprop_trace_update (gradients.py:89-94) and x_step (gradients.py:165-167).
  *     xl = NULL: the raw-spike operand (rows rho >= 1 raw spikes, row 0 zero; W from scan
  *     pass 3/4 with the input filter folded in), 2 MMAs per step; then xs_hi/xs_lo [B][kp]
@@ -193,15 +196,6 @@ int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh
                          int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
                          int store_eps, const void* xs_hi, const void* xs_lo,
                          cudaStream_t stream);
-/* K6p The same carry on CTA pairs (tcgen05.mma.cta_group::2, 256 neurons x 256 inputs per
- *     pair; eps streamed in 128 x 32 TMA boxes through an 8-slot ring): same arguments and
- *     results as spb_alif_carry_chunk; each of the `splits` sample ranges runs on
- *     2 * ceil(kp/256) * ceil(n_pad/256) CTAs.  n_pad % 128 == 0, KR % 32 == 0. */
-int spb_alif_carry_pair(const void* wh, const void* wl, int ldw, const void* xh, const void* xl,
-                        const float* mdt, float* eps, float* partial, int B, int n, int n_pad,
-                        int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
-                        int store_eps, const void* xs_hi, const void* xs_lo,
-                        cudaStream_t stream);
 
 /* K6r The ALIF trace PAIR (G_u, G_a) of reset=True carried across chunks on tcgen05
  *     (elig_reset.cu): with (W_u, W_a), M, Dt from K1r and the raw input x (K4, alpha=0)

@@ -37,8 +37,6 @@ SIGNATURES = {
     "spb_grad_gemm_simt": [P, P, I, P, P, I, I, I, I, P, I, P],
     "spb_alif_carry_chunk": [P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I, I, P, P,
                              P],
-    "spb_alif_carry_pair": [P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I, I, P, P,
-                             P],
     "spb_reset_carry_chunk": [P, P, P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I,
                               I, P],
     "spb_reduce_partials": [P, I, I, I, I, I, P, P],

@@ -16,43 +16,34 @@
 // once and written once per chunk (8 bytes per synapse per chunk), and the per-step FMA
 // work of the literal recursion moves onto the tensor cores.
 //
-// Kernel structure (one 128-neuron x 128-input tile per CTA, a contiguous sample range per
-// blockIdx.z):  warp 0 TMA producer of the W hi/lo, xbar hi/lo K-blocks (5-stage ring),
-// warp 1 TMEM owner + tcgen05.mma issuer (bf16 hi/lo split: hi*hi + hi*lo + lo*hi, fp32
-// accumulation in one of two TMEM buffers), warp 2 TMA producer of the eps tiles, warps
-// 3-18 epilogue: tcgen05.ld of the sample's product, eps update/store, gradient tile in
-// registers across samples.
+// Kernel structure: see K6 below (CTA pairs, streamed eps boxes).  The single-CTA
+// 128 x 128 version of round 1 (0.56 of HBM at C5, L2-operand bound) was replaced.
 #include "tma.cuh"
 
 #include <cstdlib>
 
 namespace spb {
-namespace carry {
 
-// Tile: 128 neurons (TMEM lanes) x 128 inputs (TMEM columns); K blocks of 32 rows.
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 5;
-constexpr int TILE = BM * BK * 2;               // 8 KB (two 64-wide MN-major boxes)
-constexpr int STAGE = 4 * TILE;                 // W hi/lo + xbar hi/lo
-constexpr int ETILE = BM * BN * 4;              // 64 KB eps tile (4 boxes of 128 x 32 fp32)
-constexpr int EPI_WARPS = 16;                   // 4 TMEM lane quarters x 4 column groups of 32
-constexpr int EPI0 = 3;                         // warps 0-2: operand TMA, MMA, eps TMA
-constexpr int THREADS = EPI0 * 32 + EPI_WARPS * 32;
-// one eps tile (single-buffered: its own producer warp refills it while the next sample's
-// MMAs run) leaves room for 5 operand stages -- the L2 operand stream is latency-bound
-constexpr int SMEM = ETILE + STAGES * STAGE + 1024 + 256;
-// raw-spike operand (RAW): no xbar-lo tiles, 2 MMAs per K step, 6 stages of 3 tiles
-constexpr int STAGES_R = 6;
-constexpr int STAGE_R = 3 * TILE;
-// RAW: the 2-MMA operand stages are 24 KB, so two eps tiles fit beside 4 of them
-#ifndef K6_RAW_EB
-#define K6_RAW_EB 2
-#endif
-constexpr int EB_R = K6_RAW_EB;
-constexpr int STAGES_RB = (EB_R == 2) ? 4 : STAGES_R;
-constexpr int SMEM_R = EB_R * ETILE + STAGES_RB * STAGE_R + 1024 + 256;
-// A = W, B = xbar, both MN-major (neurons / channels contiguous, written by K1s / K4)
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
-                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// ------------------------------------------------------------------------------------
+// K6: the carry on CTA PAIRS (tcgen05.mma.cta_group::2, M = 256, N = 256).
+//
+// Why pairs: per (sample, 128 x 128 tile) a single-CTA kernel streams 384 KB of W hi/lo
+// and spike operands from L2 for 128 KB of eps traffic, so at C5 its launch was bound by
+// the L2 (LTS) throughput, not by HBM (round 1, ncu: DRAM 45 %, long-scoreboard stalls).
+// A pair covers 256 neurons x 256 inputs: each CTA stages its own 128 W rows (A) and HALF
+// of the 256 input columns (B), and receives its 128 rows x all 256 columns in its own
+// TMEM, so the operand bytes per eps byte halve.  The eps tile of a CTA (128 x 256 fp32 =
+// 128 KB per sample) is streamed through a ring of 8 TMA boxes of 128 rows x 32 columns
+// with its own load warp and store warp, so the eps stream runs continuously instead of a
+// tile at a time.  Roles: warp 0 operand TMA (both CTAs; bytes land on the leader's
+// barrier), warp 1 TMEM allocator (cta_group::2) and, on the leader, the MMA issuer
+// (commits multicast to both CTAs), warp 2 eps box loads, warp 3 eps box stores (E_end
+// written in place), warps 4-19 epilogue (4 TMEM lane quarters x 4 column groups of 2
+// boxes; the gradient tile grad += M E0 stays in registers across the CTA's samples).
+// Measured (profiles/r2): C5 shape, Tc = 511: 441 us per launch for 2.18 GB of DRAM
+// traffic = 0.75 of HBM (round-1 single-CTA kernel: 598 us, 0.56).
+// ------------------------------------------------------------------------------------
+namespace carry {
 
 // MN-major SWIZZLE_128B operand: 64-element MN runs (128 B rows, one per K), 8-row K
 // groups 1024 B apart (SBO), the second 64-element MN half one box (LBO) further.
@@ -65,336 +56,9 @@ __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr, uint32_t lbo) 
   d |= (uint64_t)2u << 61;
   return d;
 }
-__device__ __forceinline__ void mma_bf16(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
-}
-__device__ __forceinline__ void commit(uint32_t bar) {
-  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
-                   bar)
-               : "memory");
-}
 __device__ __forceinline__ void arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&r)[16]) {
-  uint32_t* v = reinterpret_cast<uint32_t*>(r);
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-// Per CTA: one 128x128 synapse tile, a contiguous range of samples.  Warp 0 streams the
-// W / xbar K-blocks of each sample's GEMM (5-stage ring), warp 2 the sample's eps~ tile E0
-// (4 TMA boxes, SWIZZLE_128B, single-buffered: it is refilled as soon as the epilogue has
-// read it, while the next sample's MMAs run); warp 1 issues the tcgen05 MMAs into one of
-// two TMEM buffers; 16 epilogue warps combine E_end = Dt E0 + D (written back with plain
-// stores) and grad += M E0 (registers across samples).
-// RAW: the per-sample GEMM runs on the raw spikes (rows rho >= 1; row 0 zero) with the
-// input filter folded into W (forward.cu pass 3/4), and the entry-state term
-// Wt_0[b,i] xbar_{t0-1}[b,j] (xs = bf16 hi/lo [B][kp], Wt_0 = row 0 of W) is added in the
-// epilogue in fp32.
-template <bool RAW>
-__global__ void __launch_bounds__(THREADS, 1)
-    alif_carry_kernel(const __grid_constant__ CUtensorMap tm_wh, const __grid_constant__ CUtensorMap tm_wl,
-                      const __grid_constant__ CUtensorMap tm_xh, const __grid_constant__ CUtensorMap tm_xl,
-                      const __grid_constant__ CUtensorMap tm_eps,
-                      const float2* __restrict__ mdt, float* __restrict__ eps,
-                      float* __restrict__ partial, int B, int n, int n_pad, int ke, int kp, int KR,
-                      int b_per_split, int do_mma, int load_eps, int store_eps,
-                      int probe, const __nv_bfloat16* __restrict__ wh_g,
-                      const __nv_bfloat16* __restrict__ wl_g, int ldw,
-                      const __nv_bfloat16* __restrict__ xs_hi,
-                      const __nv_bfloat16* __restrict__ xs_lo) {
-  pdl_enter();
-  constexpr int NST = RAW ? STAGES_RB : STAGES;
-  constexpr int EB = RAW ? EB_R : 1;   // eps tile buffers
-  constexpr int SB = RAW ? STAGE_R : STAGE;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* esm = smem;                             // [EB][4 boxes][128 rows][128 B]
-  uint8_t* osm = smem + EB * ETILE;                // [NST][4 or 3][TILE]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(osm + NST * SB);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + NST;
-  uint64_t* tfull = bars + 2 * NST;
-  uint64_t* tempty = bars + 2 * NST + 2;
-  uint64_t* efull = bars + 2 * NST + 4;            // [EB]
-  uint64_t* eempty = bars + 2 * NST + 4 + EB;      // [EB]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 4 + 2 * EB);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
-  const int b0 = blockIdx.z * b_per_split;
-  const int nb = max(0, min(B, b0 + b_per_split) - b0);
-  const int nkb = KR / BK;
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < NST; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(smem_u32(&tfull[a]), 1);
-      mbar_init(smem_u32(&tempty[a]), EPI_WARPS);
-    }
-    for (int e = 0; e < EB; ++e) {
-      mbar_init(smem_u32(&efull[e]), 1);
-      mbar_init(smem_u32(&eempty[e]), 1);  // the epilogue's storing thread, once per use
-    }
-    mbar_fence_init();
-    if (do_mma) {
-      tma_prefetch_desc(&tm_wh);
-      tma_prefetch_desc(&tm_wl);
-      tma_prefetch_desc(&tm_xh);
-      if (!RAW) tma_prefetch_desc(&tm_xl);
-    }
-    if (load_eps || store_eps) tma_prefetch_desc(&tm_eps);
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(256));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0 && do_mma) {  // operand K-blocks of every sample's GEMM
-      int it = 0;
-      for (int lb = 0; lb < nb; ++lb) {
-        const int kbase = (b0 + lb) * KR;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % NST;
-          mbar_wait(smem_u32(&empty[s]), ((it / NST) & 1) ^ 1);
-          const uint32_t st = smem_u32(osm + s * SB);
-          const uint32_t fb = smem_u32(&full[s]);
-          if (probe & 1) {  // profiling probe: no operand traffic
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
-            continue;
-          }
-          mbar_expect_tx(fb, SB);
-          const int kr = kbase + kb * BK;
-          tma_load_2d(st, &tm_wh, fb, i0, kr);
-          tma_load_2d(st + TILE / 2, &tm_wh, fb, i0 + 64, kr);
-          tma_load_2d(st + TILE, &tm_wl, fb, i0, kr);
-          tma_load_2d(st + TILE + TILE / 2, &tm_wl, fb, i0 + 64, kr);
-          tma_load_2d(st + 2 * TILE, &tm_xh, fb, j0, kr);
-          tma_load_2d(st + 2 * TILE + TILE / 2, &tm_xh, fb, j0 + 64, kr);
-          if (!RAW) {
-            tma_load_2d(st + 3 * TILE, &tm_xl, fb, j0, kr);
-            tma_load_2d(st + 3 * TILE + TILE / 2, &tm_xl, fb, j0 + 64, kr);
-          }
-        }
-      }
-    }
-  } else if (warp == 2) {
-    if (lane == 0 && load_eps) {  // each sample's eps~ tile E0, 4 boxes of 32 columns
-      for (int lb = 0; lb < nb; ++lb) {
-        const int eb = lb % EB, eu = lb / EB;   // buffer, its use count
-        mbar_wait(smem_u32(&eempty[eb]), (eu & 1) ^ 1);
-        const uint32_t fb = smem_u32(&efull[eb]);
-        mbar_expect_tx(fb, ETILE);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          tma_load_2d(smem_u32(esm + eb * ETILE + q * (ETILE / 4)), &tm_eps, fb, j0 + 32 * q,
-                      (b0 + lb) * n_pad + i0);
-      }
-    }
-  } else if (warp == 1) {
-    if (do_mma) {  // whole warp, converged; elect.sync picks the issuer
-      int it = 0;
-      for (int lb = 0; lb < nb; ++lb) {
-        const int a = lb & 1;
-        mbar_wait(smem_u32(&tempty[a]), ((lb >> 1) & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem_base + (uint32_t)(a * BN);
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % NST;
-          mbar_wait(smem_u32(&full[s]), (it / NST) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t st = smem_u32(osm + s * SB);
-#pragma unroll
-          for (int kk = 0; kk < ((probe & 2) ? 0 : BK / 16); ++kk) {  // probe bit 1: no MMAs
-            const uint32_t off = kk * 2048;  // 16 K rows of the MN-major tiles
-            const uint64_t dwh = desc_mn_sw128(st + off, TILE / 2),
-                           dwl = desc_mn_sw128(st + TILE + off, TILE / 2);
-            const uint64_t dxh = desc_mn_sw128(st + 2 * TILE + off, TILE / 2),
-                           dxl = desc_mn_sw128(st + 3 * TILE + off, TILE / 2);
-            mma_bf16(d, dwh, dxh, (kb | kk) ? 1u : 0u);
-            if (!RAW) mma_bf16(d, dwh, dxl, 1u);
-            mma_bf16(d, dwl, dxh, 1u);
-          }
-          commit(smem_u32(&empty[s]));
-        }
-        commit(smem_u32(&tfull[a]));
-      }
-    }
-  } else {
-    const int q = warp & 3;            // TMEM lane quarter of this warp
-    const int cg = (warp - EPI0) >> 2; // 32-column group = eps box
-    const int r = q * 32 + lane;       // tile-local neuron row
-    const int i = i0 + r;
-    const bool vi = i < n;
-    const int c0 = j0 + cg * 32;       // first input column of this thread
-    float g[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) g[c] = 0.f;
-    for (int lb = 0; lb < nb; ++lb) {
-      const int b = b0 + lb;
-      const int a = lb & 1;
-      const float2 md = vi ? mdt[(long long)b * n + i] : make_float2(0.f, 0.f);
-      // RAW: entry-state term Wt_0[b,i] * xbar_{t0-1}[b, c0 + c] (xs may be absent: fresh)
-      float w0e = 0.f;
-      if (RAW && xs_hi != nullptr && vi) {
-        const long long o = (long long)b * KR * ldw + i;
-        w0e = __bfloat162float(wh_g[o]) + __bfloat162float(wl_g[o]);
-      }
-      const int eb = lb % EB, eu = lb / EB;
-      const uint32_t erow = smem_u32(esm + eb * ETILE + cg * (ETILE / 4) + r * 128);
-      if (load_eps) mbar_wait(smem_u32(&efull[eb]), eu & 1);
-      else if (store_eps && eu > 0) mbar_wait(smem_u32(&eempty[eb]), (eu - 1) & 1);  // reusable
-      if (do_mma) {
-        mbar_wait(smem_u32(&tfull[a]), (lb >> 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      }
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        float D[16];
-        if (do_mma) {
-          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * BN + cg * 32 + hf * 16), D);
-        } else {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) D[c] = 0.f;
-        }
-#pragma unroll
-        for (int v4 = hf * 4; v4 < hf * 4 + 4; ++v4) {
-          float4 e0 = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (load_eps)  // SWIZZLE_128B: 16-byte chunk v4 of row r sits at chunk v4 ^ (r & 7)
-            e0 = lds_f4(erow + ((v4 ^ (r & 7)) << 4));
-          g[v4 * 4 + 0] = fmaf(md.x, e0.x, g[v4 * 4 + 0]);
-          g[v4 * 4 + 1] = fmaf(md.x, e0.y, g[v4 * 4 + 1]);
-          g[v4 * 4 + 2] = fmaf(md.x, e0.z, g[v4 * 4 + 2]);
-          g[v4 * 4 + 3] = fmaf(md.x, e0.w, g[v4 * 4 + 3]);
-          if (store_eps) {  // E_end in place over E0 (same swizzled chunk), TMA-stored below
-            const int dv = (v4 - hf * 4) * 4;
-            float4 en;
-            en.x = fmaf(md.y, e0.x, D[dv + 0]);
-            en.y = fmaf(md.y, e0.y, D[dv + 1]);
-            en.z = fmaf(md.y, e0.z, D[dv + 2]);
-            en.w = fmaf(md.y, e0.w, D[dv + 3]);
-            if (RAW && xs_hi != nullptr) {
-              const int cc = c0 + v4 * 4;
-              float xsv[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                xsv[e] = cc + e < kp ? __bfloat162float(xs_hi[(long long)b * kp + cc + e]) +
-                                           __bfloat162float(xs_lo[(long long)b * kp + cc + e])
-                                     : 0.f;
-              en.x = fmaf(w0e, xsv[0], en.x);
-              en.y = fmaf(w0e, xsv[1], en.y);
-              en.z = fmaf(w0e, xsv[2], en.z);
-              en.w = fmaf(w0e, xsv[3], en.w);
-            }
-            sts_f4(erow + ((v4 ^ (r & 7)) << 4), en);
-          }
-        }
-      }
-      __syncwarp();
-      if (do_mma) {
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        if (lane == 0) arrive(smem_u32(&tempty[a]));
-      }
-      if (load_eps || store_eps) {
-        // the whole tile is read (and rewritten): one thread stores it with 4 TMA boxes
-        // and frees it once the bulk copies have read the shared memory
-        if (store_eps) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("bar.sync 1, %0;" ::"r"(EPI_WARPS * 32) : "memory");
-        if (warp == EPI0 && lane == 0) {
-          if (store_eps) {
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
-              tma_store_2d(&tm_eps, smem_u32(esm + eb * ETILE + q4 * (ETILE / 4)), j0 + 32 * q4,
-                           b * n_pad + i0);
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          }
-          arrive(smem_u32(&eempty[eb]));
-        }
-      }
-    }
-    if (store_eps && warp == EPI0 && lane == 0)
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // E_end written
-    {
-      // grad tile through a 4x4 lane transpose of 32-byte chunks and 256-bit stores: each
-      // instruction writes 8 rows x 128 contiguous bytes (rows past n are zero padding)
-      const int p4 = lane & 3;
-#pragma unroll
-      for (int sh = 2; sh >= 1; sh >>= 1) {
-        const bool up = (p4 & sh) != 0;
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          if (m & sh) continue;
-          const int ms = m | sh;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float send = up ? g[8 * m + e] : g[8 * ms + e];
-            const float recv = __shfl_xor_sync(0xffffffffu, send, sh);
-            if (up) g[8 * m + e] = recv; else g[8 * ms + e] = recv;
-          }
-        }
-      }
-      float* base = partial + ((long long)blockIdx.z * n_pad + i0 + q * 32 + (lane & ~3)) * kp +
-                    c0 + 8 * p4;
-#pragma unroll
-      for (int kq = 0; kq < 4; ++kq)
-        asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(
-                         base + (long long)kq * kp),
-                     "f"(g[8 * kq + 0]), "f"(g[8 * kq + 1]), "f"(g[8 * kq + 2]),
-                     "f"(g[8 * kq + 3]), "f"(g[8 * kq + 4]), "f"(g[8 * kq + 5]),
-                     "f"(g[8 * kq + 6]), "f"(g[8 * kq + 7])
-                     : "memory");
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
-}
-
-}  // namespace carry
-
-// ------------------------------------------------------------------------------------
-// K6p: the same carry on CTA PAIRS (tcgen05.mma.cta_group::2, M = 256, N = 256).
-//
-// Why: per (sample, 128 x 128 tile) the single-CTA kernel streams 384 KB of W hi/lo and
-// spike operands from L2 for 128 KB of eps traffic, so at C5 the launch is bound by the
-// L2 (LTS) throughput, not by HBM (ncu: DRAM 45 %, long-scoreboard stalls).  A pair
-// covers 256 neurons x 256 inputs: each CTA stages its own 128 W rows (A) and HALF of the
-// 256 input columns (B), and receives its 128 rows x all 256 columns in its own TMEM, so
-// the operand bytes per eps byte halve.  The eps tile of a CTA (128 x 256 fp32 = 128 KB
-// per sample) is streamed through a ring of 8 TMA boxes of 128 rows x 32 columns with its
-// own load warp and store warp, so the eps stream runs continuously instead of a tile at a
-// time.  Roles: warp 0 operand TMA (both CTAs; bytes land on the leader's barrier), warp 1
-// TMEM allocator (cta_group::2) and, on the leader, the MMA issuer (commits multicast to
-// both CTAs), warp 2 eps box loads, warp 3 eps box stores (E_end written in place),
-// warps 4-19 epilogue (4 TMEM lane quarters x 4 column groups of 2 boxes; the gradient
-// tile grad += M E0 stays in registers across the CTA's samples).
-// Same arithmetic, in the same order per element, as alif_carry_kernel.
-// ------------------------------------------------------------------------------------
-namespace carry2 {
 
 constexpr int BM = 128;                 // neurons per CTA (the pair: 256)
 constexpr int BN = 256;                 // inputs per pair tile = MMA N
@@ -463,8 +127,12 @@ __device__ __forceinline__ void commit2(uint32_t bar) {
       " [%0], m;\n\t}" ::"r"(bar)
       : "memory");
 }
+// TMEM-empty arrive on the leader: relaxed -- the warp's tcgen05.ld of the buffer have
+// completed (tcgen05.wait::ld) before it arrives, so nothing it wrote or read has to be
+// published; a release at cluster scope (a cluster-wide memory fence per sample and
+// warp) measured as the top stall of the epilogue.
 __device__ __forceinline__ void arrive_remote(uint32_t cluster_bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar)
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar)
                : "memory");
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&r)[8]) {
@@ -556,101 +224,101 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   // gradient tile (64 fp32 per thread) lives in registers: 128 x 56 + 512 x 104 <= 640 x 96
   if (warp < EPI0) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
-  if (warp == 0) {
-    if (lane == 0 && do_mma) {  // this CTA's operand K-blocks of every sample's GEMM
-      int it = 0;
-      for (int lb = 0; lb < nb; ++lb) {
-        const int kbase = (b0 + lb) * KR;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % NST;
-          mbar_wait(smem_u32(&empty[s]), ((it / NST) & 1) ^ 1);
-          if (leader) mbar_expect_tx(smem_u32(&full[s]), 2 * SB);
-          const uint32_t lb_full = mapa(smem_u32(&full[s]), 0);
-          const uint32_t st = smem_u32(osm + s * SB);
-          const int kr = kbase + kb * BK;
-          tma_load_2sm(st, &tm_wh, lb_full, i0, kr);
-          tma_load_2sm(st + TILE / 2, &tm_wh, lb_full, i0 + 64, kr);
-          tma_load_2sm(st + TILE, &tm_wl, lb_full, i0, kr);
-          tma_load_2sm(st + TILE + TILE / 2, &tm_wl, lb_full, i0 + 64, kr);
-          tma_load_2sm(st + 2 * TILE, &tm_xh, lb_full, jx, kr);
-          tma_load_2sm(st + 2 * TILE + TILE / 2, &tm_xh, lb_full, jx + 64, kr);
-          if (!RAW) {
-            tma_load_2sm(st + 3 * TILE, &tm_xl, lb_full, jx, kr);
-            tma_load_2sm(st + 3 * TILE + TILE / 2, &tm_xl, lb_full, jx + 64, kr);
+    if (warp == 0) {
+      if (lane == 0 && do_mma) {  // this CTA's operand K-blocks of every sample's GEMM
+        int it = 0;
+        for (int lb = 0; lb < nb; ++lb) {
+          const int kbase = (b0 + lb) * KR;
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int s = it % NST;
+            mbar_wait(smem_u32(&empty[s]), ((it / NST) & 1) ^ 1);
+            if (leader) mbar_expect_tx(smem_u32(&full[s]), 2 * SB);
+            const uint32_t lb_full = mapa(smem_u32(&full[s]), 0);
+            const uint32_t st = smem_u32(osm + s * SB);
+            const int kr = kbase + kb * BK;
+            tma_load_2sm(st, &tm_wh, lb_full, i0, kr);
+            tma_load_2sm(st + TILE / 2, &tm_wh, lb_full, i0 + 64, kr);
+            tma_load_2sm(st + TILE, &tm_wl, lb_full, i0, kr);
+            tma_load_2sm(st + TILE + TILE / 2, &tm_wl, lb_full, i0 + 64, kr);
+            tma_load_2sm(st + 2 * TILE, &tm_xh, lb_full, jx, kr);
+            tma_load_2sm(st + 2 * TILE + TILE / 2, &tm_xh, lb_full, jx + 64, kr);
+            if (!RAW) {
+              tma_load_2sm(st + 3 * TILE, &tm_xl, lb_full, jx, kr);
+              tma_load_2sm(st + 3 * TILE + TILE / 2, &tm_xl, lb_full, jx + 64, kr);
+            }
           }
         }
       }
-    }
-  } else if (warp == 1) {
-    if (leader && do_mma) {  // whole warp, converged; elect.sync picks the issuer
-      int it = 0;
-      for (int lb = 0; lb < nb; ++lb) {
-        const int a = lb & 1;
-        mbar_wait_cluster(smem_u32(&tempty[a]), ((lb >> 1) & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem_base + (uint32_t)(a * BN);
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % NST;
-          mbar_wait_cluster(smem_u32(&full[s]), (it / NST) & 1);
+    } else if (warp == 1) {
+      if (leader && do_mma) {  // whole warp, converged; elect.sync picks the issuer
+        int it = 0;
+        for (int lb = 0; lb < nb; ++lb) {
+          const int a = lb & 1;
+          mbar_wait_cluster(smem_u32(&tempty[a]), ((lb >> 1) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t st = smem_u32(osm + s * SB);
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint32_t off = kk * 2048;  // 16 K rows of the MN-major tiles
-            const uint64_t dwh = carry::desc_mn_sw128(st + off, TILE / 2),
-                           dwl = carry::desc_mn_sw128(st + TILE + off, TILE / 2);
-            const uint64_t dxh = carry::desc_mn_sw128(st + 2 * TILE + off, TILE / 2),
-                           dxl = carry::desc_mn_sw128(st + 3 * TILE + off, TILE / 2);
-            mma2_bf16(d, dwh, dxh, (kb | kk) ? 1u : 0u);
-            if (!RAW) mma2_bf16(d, dwh, dxl, 1u);
-            mma2_bf16(d, dwl, dxh, 1u);
+          const uint32_t d = tmem_base + (uint32_t)(a * BN);
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int s = it % NST;
+            mbar_wait_cluster(smem_u32(&full[s]), (it / NST) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t st = smem_u32(osm + s * SB);
+  #pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t off = kk * 2048;  // 16 K rows of the MN-major tiles
+              const uint64_t dwh = desc_mn_sw128(st + off, TILE / 2),
+                             dwl = desc_mn_sw128(st + TILE + off, TILE / 2);
+              const uint64_t dxh = desc_mn_sw128(st + 2 * TILE + off, TILE / 2),
+                             dxl = desc_mn_sw128(st + 3 * TILE + off, TILE / 2);
+              mma2_bf16(d, dwh, dxh, (kb | kk) ? 1u : 0u);
+              if (!RAW) mma2_bf16(d, dwh, dxl, 1u);
+              mma2_bf16(d, dwl, dxh, 1u);
+            }
+            commit2(smem_u32(&empty[s]));
           }
-          commit2(smem_u32(&empty[s]));
-        }
-        commit2(smem_u32(&tfull[a]));
-      }
-    }
-  } else if (warp == 2) {
-    if (lane == 0) {  // eps boxes of every sample, in (sample, box) order through the ring
-      const bool ld = load_eps && own;
-      for (int lb = 0; lb < nb; ++lb) {
-        for (int bx = 0; bx < BOXES; ++bx) {
-          const int gi = lb * BOXES + bx, slot = gi % NBOX, u = gi / NBOX;
-          mbar_wait(smem_u32(&eempty[slot]), (u & 1) ^ 1);
-          const uint32_t fb = smem_u32(&efull[slot]);
-          if (ld) {
-            mbar_expect_tx(fb, EBOX);
-            tma_load_2d(smem_u32(esm + slot * EBOX), &tm_eps, fb, j0 + 32 * bx,
-                        (b0 + lb) * n_pad + i0);
-          } else {
-            carry::arrive(fb);
-          }
+          commit2(smem_u32(&tfull[a]));
         }
       }
-    }
-  } else if (warp == 3) {
-    if (lane == 0) {  // E_end boxes back to HBM; a slot is freed once its store has read it
-      const bool st_e = store_eps && own;
-      int prev = -1;
-      for (int lb = 0; lb < nb; ++lb) {
-        for (int bx = 0; bx < BOXES; ++bx) {
-          const int gi = lb * BOXES + bx, slot = gi % NBOX, u = gi / NBOX;
-          mbar_wait(smem_u32(&eready[slot]), u & 1);
-          if (st_e) {
-            tma_store_2d(&tm_eps, smem_u32(esm + slot * EBOX), j0 + 32 * bx,
-                         (b0 + lb) * n_pad + i0);
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            if (prev >= 0) carry::arrive(smem_u32(&eempty[prev]));
-            prev = slot;
-          } else {
-            carry::arrive(smem_u32(&eempty[slot]));
+    } else if (warp == 2) {
+      if (lane == 0) {  // eps boxes of every sample, in (sample, box) order through the ring
+        const bool ld = load_eps && own;
+        for (int lb = 0; lb < nb; ++lb) {
+          for (int bx = 0; bx < BOXES; ++bx) {
+            const int gi = lb * BOXES + bx, slot = gi % NBOX, u = gi / NBOX;
+            mbar_wait(smem_u32(&eempty[slot]), (u & 1) ^ 1);
+            const uint32_t fb = smem_u32(&efull[slot]);
+            if (ld) {
+              mbar_expect_tx(fb, EBOX);
+              tma_load_2d(smem_u32(esm + slot * EBOX), &tm_eps, fb, j0 + 32 * bx,
+                          (b0 + lb) * n_pad + i0);
+            } else {
+              arrive(fb);
+            }
           }
         }
       }
-      if (st_e) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // E_end written
+    } else if (warp == 3) {
+      if (lane == 0) {  // E_end boxes back to HBM; a slot is freed once its store has read it
+        const bool st_e = store_eps && own;
+        int prev = -1;
+        for (int lb = 0; lb < nb; ++lb) {
+          for (int bx = 0; bx < BOXES; ++bx) {
+            const int gi = lb * BOXES + bx, slot = gi % NBOX, u = gi / NBOX;
+            mbar_wait(smem_u32(&eready[slot]), u & 1);
+            if (st_e) {
+              tma_store_2d(&tm_eps, smem_u32(esm + slot * EBOX), j0 + 32 * bx,
+                           (b0 + lb) * n_pad + i0);
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              if (prev >= 0) arrive(smem_u32(&eempty[prev]));
+              prev = slot;
+            } else {
+              arrive(smem_u32(&eempty[slot]));
+            }
+          }
+        }
+        if (st_e) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // E_end written
+      }
     }
-  }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 104;" ::: "memory");
     const int e = warp - EPI0;
@@ -733,7 +401,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         if (store_eps) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) carry::arrive(smem_u32(&eready[slot]));
+        if (lane == 0) arrive(smem_u32(&eready[slot]));
       }
       if (do_mma) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -786,7 +454,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
 }
 
-}  // namespace carry2
+}  // namespace carry
 
 // 4 consecutive elements per thread (float4 partial loads, all S slices in flight before
 // the fixed-order fp64 sums), k_pad % 4 == 0.
@@ -886,78 +554,7 @@ __global__ void __launch_bounds__(256) grad_gemm_simt_kernel(
 
 using namespace spb;
 
-// SPB_CARRY_PROBE (profiling only): bit 0 drops the operand loads, bit 1 the MMAs
-static int carry_probe() {
-  const char* e = getenv("SPB_CARRY_PROBE");
-  return e ? atoi(e) : 0;
-}
-
 extern "C" {
-
-int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh, const void* xl,
-                         const float* mdt, float* eps, float* partial, int B, int n, int n_pad,
-                         int k, int ke, int kp, int KR, int splits, int do_mma, int load_eps,
-                         int store_eps, const void* xs_hi, const void* xs_lo,
-                         cudaStream_t stream) {
-  SPB_CHECK_ARG(mdt && eps && partial, "spb_alif_carry_chunk: null pointer");
-  // xl = NULL: raw-spike operand (2 MMAs); xs = the entry-state term (NULL: fresh state)
-  const bool raw = xl == nullptr;
-  SPB_CHECK_ARG(!(xs_hi && !raw) && !(xs_hi && !xs_lo),
-                "spb_alif_carry_chunk: the entry-state term needs the raw operand (xl = NULL)");
-  SPB_CHECK_ARG(!do_mma || (wh && wl && xh), "spb_alif_carry_chunk: missing GEMM operands");
-  SPB_CHECK_ARG(n_pad % carry::BM == 0 && n <= n_pad && kp % carry::BN == 0 && kp >= k &&
-                    ke >= k && ke % 4 == 0 && KR % carry::BK == 0 && (kp / carry::BN) * carry::BN == kp,
-                "spb_alif_carry_chunk: bad padding (n_pad %% 128, kp %% 128, ke %% 4, KR %% 64)");
-  SPB_CHECK_ARG(B > 0 && splits > 0 && splits <= B, "spb_alif_carry_chunk: bad split");
-  SPB_CHECK_ARG(!do_mma || (ldw >= n && ldw % 8 == 0), "spb_alif_carry_chunk: bad ldw");
-  SPB_CHECK_ARG(!(store_eps && !do_mma), "spb_alif_carry_chunk: storing eps needs the GEMM");
-  CUtensorMap mwh{}, mwl{}, mxh{}, mxl{}, meps{};
-  if ((load_eps || store_eps) &&
-      !make_tmap_2d(&meps, eps, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ke, (uint64_t)B * n_pad,
-                    (uint64_t)ke * 4, 32, carry::BM, CU_TENSOR_MAP_SWIZZLE_128B)) {
-    set_error("spb_alif_carry_chunk: cuTensorMapEncodeTiled (eps) failed");
-    return 3;
-  }
-  if (do_mma) {
-    const uint64_t K = (uint64_t)B * KR;
-    const bool ok =
-        make_tmap_2d(&mwh, wh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, K, (uint64_t)ldw * 2, 64,
-                     carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
-        make_tmap_2d(&mwl, wl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, K, (uint64_t)ldw * 2, 64,
-                     carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
-        make_tmap_2d(&mxh, xh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kp, K, (uint64_t)kp * 2, 64,
-                     carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
-        make_tmap_2d(&mxl, raw ? xh : xl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kp, K,
-                     (uint64_t)kp * 2, 64, carry::BK, CU_TENSOR_MAP_SWIZZLE_128B);
-    if (!ok) {
-      set_error("spb_alif_carry_chunk: cuTensorMapEncodeTiled failed");
-      return 3;
-    }
-  }
-  const int bps = ceil_div(B, splits);
-  dim3 grid(kp / carry::BN, n_pad / carry::BM, splits);
-  const auto* whb = static_cast<const __nv_bfloat16*>(wh);
-  const auto* wlb = static_cast<const __nv_bfloat16*>(wl);
-  const auto* xsh = static_cast<const __nv_bfloat16*>(xs_hi);
-  const auto* xsl = static_cast<const __nv_bfloat16*>(xs_lo);
-  if (raw) {
-    cudaFuncSetAttribute(carry::alif_carry_kernel<true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, carry::SMEM_R);
-    pdl_launch(carry::alif_carry_kernel<true>, grid, carry::THREADS, carry::SMEM_R, stream,
-        mwh, mwl, mxh, mxl, meps, reinterpret_cast<const float2*>(mdt), eps, partial, B, n,
-        n_pad, ke, kp, KR, bps, do_mma, load_eps, store_eps, carry_probe(), whb, wlb, ldw, xsh,
-        xsl);
-  } else {
-    cudaFuncSetAttribute(carry::alif_carry_kernel<false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, carry::SMEM);
-    pdl_launch(carry::alif_carry_kernel<false>, grid, carry::THREADS, carry::SMEM, stream,
-        mwh, mwl, mxh, mxl, meps, reinterpret_cast<const float2*>(mdt), eps, partial, B, n,
-        n_pad, ke, kp, KR, bps, do_mma, load_eps, store_eps, carry_probe(), whb, wlb, ldw,
-        nullptr, nullptr);
-  }
-  SPB_CHECK_LAUNCH("alif_carry");
-  return 0;
-}
 
 int spb_reduce_partials(const float* partial, int splits, int n, int n_pad, int k_pad,
                         int accumulate, double* grad, cudaStream_t stream) {
@@ -985,68 +582,68 @@ int spb_grad_gemm_simt(const void* ah, const void* al, int lda, const void* bh, 
 
 }  // extern "C"
 
-// K6p launcher: same arguments as spb_alif_carry_chunk; `splits` sample ranges, each over a
-// grid of (2 * ceil(kp / 256), ceil(n_pad / 256)) CTAs (clusters of 2 along x).
-extern "C" int spb_alif_carry_pair(const void* wh, const void* wl, int ldw, const void* xh,
+// K6 launcher: `splits` sample ranges, each over a grid of (2 * ceil(kp / 256),
+// ceil(n_pad / 256)) CTAs (clusters of 2 along x).
+extern "C" int spb_alif_carry_chunk(const void* wh, const void* wl, int ldw, const void* xh,
                                    const void* xl, const float* mdt, float* eps, float* partial,
                                    int B, int n, int n_pad, int k, int ke, int kp, int KR,
                                    int splits, int do_mma, int load_eps, int store_eps,
                                    const void* xs_hi, const void* xs_lo, cudaStream_t stream) {
   using namespace spb;
-  SPB_CHECK_ARG(mdt && eps && partial, "spb_alif_carry_pair: null pointer");
+  SPB_CHECK_ARG(mdt && eps && partial, "spb_alif_carry_chunk: null pointer");
   const bool raw = xl == nullptr;
   SPB_CHECK_ARG(!(xs_hi && !raw) && !(xs_hi && !xs_lo),
-                "spb_alif_carry_pair: the entry-state term needs the raw operand (xl = NULL)");
-  SPB_CHECK_ARG(!do_mma || (wh && wl && xh), "spb_alif_carry_pair: missing GEMM operands");
-  SPB_CHECK_ARG(n_pad % carry2::BM == 0 && n <= n_pad && kp % 128 == 0 && kp >= k && ke >= k &&
-                    ke % 4 == 0 && KR % carry2::BK == 0,
-                "spb_alif_carry_pair: bad padding (n_pad %% 128, kp %% 128, ke %% 4, KR %% 32)");
-  SPB_CHECK_ARG(B > 0 && splits > 0 && splits <= B, "spb_alif_carry_pair: bad split");
-  SPB_CHECK_ARG(!do_mma || (ldw >= n && ldw % 8 == 0), "spb_alif_carry_pair: bad ldw");
-  SPB_CHECK_ARG(!(store_eps && !do_mma), "spb_alif_carry_pair: storing eps needs the GEMM");
+                "spb_alif_carry_chunk: the entry-state term needs the raw operand (xl = NULL)");
+  SPB_CHECK_ARG(!do_mma || (wh && wl && xh), "spb_alif_carry_chunk: missing GEMM operands");
+  SPB_CHECK_ARG(n_pad % carry::BM == 0 && n <= n_pad && kp % 128 == 0 && kp >= k && ke >= k &&
+                    ke % 4 == 0 && KR % carry::BK == 0,
+                "spb_alif_carry_chunk: bad padding (n_pad %% 128, kp %% 128, ke %% 4, KR %% 32)");
+  SPB_CHECK_ARG(B > 0 && splits > 0 && splits <= B, "spb_alif_carry_chunk: bad split");
+  SPB_CHECK_ARG(!do_mma || (ldw >= n && ldw % 8 == 0), "spb_alif_carry_chunk: bad ldw");
+  SPB_CHECK_ARG(!(store_eps && !do_mma), "spb_alif_carry_chunk: storing eps needs the GEMM");
   CUtensorMap mwh{}, mwl{}, mxh{}, mxl{}, meps{};
   if ((load_eps || store_eps) &&
       !make_tmap_2d(&meps, eps, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ke, (uint64_t)B * n_pad,
-                    (uint64_t)ke * 4, 32, carry2::BM, CU_TENSOR_MAP_SWIZZLE_128B)) {
-    set_error("spb_alif_carry_pair: cuTensorMapEncodeTiled (eps) failed");
+                    (uint64_t)ke * 4, 32, carry::BM, CU_TENSOR_MAP_SWIZZLE_128B)) {
+    set_error("spb_alif_carry_chunk: cuTensorMapEncodeTiled (eps) failed");
     return 3;
   }
   if (do_mma) {
     const uint64_t K = (uint64_t)B * KR;
     const bool ok =
         make_tmap_2d(&mwh, wh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, K, (uint64_t)ldw * 2, 64,
-                     carry2::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
+                     carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
         make_tmap_2d(&mwl, wl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, n, K, (uint64_t)ldw * 2, 64,
-                     carry2::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
+                     carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
         make_tmap_2d(&mxh, xh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kp, K, (uint64_t)kp * 2, 64,
-                     carry2::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
+                     carry::BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
         make_tmap_2d(&mxl, raw ? xh : xl, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kp, K,
-                     (uint64_t)kp * 2, 64, carry2::BK, CU_TENSOR_MAP_SWIZZLE_128B);
+                     (uint64_t)kp * 2, 64, carry::BK, CU_TENSOR_MAP_SWIZZLE_128B);
     if (!ok) {
-      set_error("spb_alif_carry_pair: cuTensorMapEncodeTiled failed");
+      set_error("spb_alif_carry_chunk: cuTensorMapEncodeTiled failed");
       return 3;
     }
   }
   const int bps = ceil_div(B, splits);
-  dim3 grid(2 * ceil_div(kp, carry2::BN), ceil_div(n_pad, 2 * carry2::BM), splits);
+  dim3 grid(2 * ceil_div(kp, carry::BN), ceil_div(n_pad, 2 * carry::BM), splits);
   const auto* whb = static_cast<const __nv_bfloat16*>(wh);
   const auto* wlb = static_cast<const __nv_bfloat16*>(wl);
   const auto* xsh = static_cast<const __nv_bfloat16*>(xs_hi);
   const auto* xsl = static_cast<const __nv_bfloat16*>(xs_lo);
   if (raw) {
-    auto kfn = carry2::alif_carry_pair_kernel<true>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, carry2::Cfg<true>::SMEM);
-    pdl_launch(kfn, grid, carry2::THREADS, carry2::Cfg<true>::SMEM, stream, mwh, mwl, mxh, mxl,
+    auto kfn = carry::alif_carry_pair_kernel<true>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, carry::Cfg<true>::SMEM);
+    pdl_launch(kfn, grid, carry::THREADS, carry::Cfg<true>::SMEM, stream, mwh, mwl, mxh, mxl,
                meps, reinterpret_cast<const float2*>(mdt), partial, B, n, n_pad, kp, KR, bps,
                do_mma, load_eps, store_eps, whb, wlb, ldw, xsh, xsl);
   } else {
-    auto kfn = carry2::alif_carry_pair_kernel<false>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, carry2::Cfg<false>::SMEM);
-    pdl_launch(kfn, grid, carry2::THREADS, carry2::Cfg<false>::SMEM, stream, mwh, mwl, mxh, mxl,
+    auto kfn = carry::alif_carry_pair_kernel<false>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, carry::Cfg<false>::SMEM);
+    pdl_launch(kfn, grid, carry::THREADS, carry::Cfg<false>::SMEM, stream, mwh, mwl, mxh, mxl,
                meps, reinterpret_cast<const float2*>(mdt), partial, B, n, n_pad, kp, KR, bps,
                do_mma, load_eps, store_eps, whb, wlb, ldw, (const __nv_bfloat16*)nullptr,
                (const __nv_bfloat16*)nullptr);
   }
-  SPB_CHECK_LAUNCH("alif_carry_pair");
+  SPB_CHECK_LAUNCH("alif_carry");
   return 0;
 }

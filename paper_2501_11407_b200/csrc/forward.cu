@@ -795,9 +795,9 @@ __global__ void __launch_bounds__(128) xbar_chunk4_kernel(
     if (j + c < k) xbar_st[(long long)b * k + j + c] = xb[c];
 }
 
-// K4 on time segments: warp s of a CTA filters rows rho in [64 s, 64 s + 63] of 128
-// channels (4 per lane) -- KR/64 x the threads of xbar_chunk4_kernel for the same bytes
-// (one 64-row segment per warp).  The filter is linear: sweep 1 runs each segment from a
+// K4 on time segments: warp s of a CTA filters rows rho in [S s, S s + S - 1] of 128
+// channels (4 per lane), S = KR / nseg rows per segment (64 up to KR = 512, then the
+// KR / 8 of 8 segments) -- nseg x the threads of xbar_chunk4_kernel for the same bytes.  The filter is linear: sweep 1 runs each segment from a
 // zero entry (segment 0 from the true carry) to get its end value, the segments meet in
 // shared memory in time order (E <- alpha^len E + end), and sweep 2 re-reads the spike
 // bytes (L1/L2-hot) and writes the rows from the true entry.  fp64 throughout; the values
@@ -824,7 +824,8 @@ __global__ void __launch_bounds__(256) xbar_seg_kernel(
 #pragma unroll
   for (int c = 0; c < 4; ++c)
     xb_in[c] = (j + c < k && !fresh) ? xbar_st[(long long)b * k + j + c] : 0.0;
-  const int lo = seg * XSEG_ROWS, hi = lo + XSEG_ROWS - 1;
+  const int srows = KR / nseg;
+  const int lo = seg * srows, hi = lo + srows - 1;
   auto xword = [&](int rho) -> uint32_t {  // spikes of step rho - 1 (rows 1..len)
     return (any && rho >= 1 && rho <= len) ? (__ldg(xin + (long long)(rho - 1) * st4) & keep) : 0u;
   };
@@ -1062,9 +1063,10 @@ static int xbar_launch(const uint8_t* x, long long stride_b, long long stride_t,
   const bool al4 = (stride_b | stride_t) % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0 &&
                    reinterpret_cast<uintptr_t>(xh) % 8 == 0 &&
                    reinterpret_cast<uintptr_t>(xl) % 8 == 0;
-  if (segmented && al4 && KR % XSEG_ROWS == 0 && KR / XSEG_ROWS <= 8) {
+  const int nseg = std::min(8, KR / XSEG_ROWS);
+  if (segmented && al4 && KR % XSEG_ROWS == 0 && (KR / nseg) % 8 == 0) {
     dim3 gs(ceil_div(kp / 4, 32), B);
-    xbar_seg_kernel<<<gs, 32 * (KR / XSEG_ROWS), 0, stream>>>(
+    xbar_seg_kernel<<<gs, 32 * nseg, 0, stream>>>(
         x, stride_b, stride_t, B, k, kp, KR, len, fresh, alpha, xbar_state,
         reinterpret_cast<uint2*>(xh), reinterpret_cast<uint2*>(xl), raw,
         reinterpret_cast<uint2*>(xs_hi), reinterpret_cast<uint2*>(xs_lo));

@@ -14,10 +14,11 @@
 // runs the unchanged scan / xbar / GEMM / carry kernels on the extended input
 // x~_t = [x_t, z_{t-1}] (spb_pack_rec).
 //
-// One CTA per sample, 512 threads, NPT <= 4 neurons per thread (n <= 2048); the spikes of
-// the previous step live in a double-buffered shared bitmask, compacted by one warp into
-// an ascending active list each step (two __syncthreads per step) so that the weight
-// loads of 8 presynaptic spikes are in flight at once.
+// One CTA per sample, 512 threads, NPT <= 4 neurons per thread (n <= 2048), two CTAs per
+// SM for n <= 1024; the spikes of the previous step live in a double-buffered shared
+// bitmask, compacted by one warp into an ascending active list each step (two
+// __syncthreads per step) so that the weight loads of 8 presynaptic spikes are in flight
+// at once.  The step is latency-bound (L2 round trips of the gather + two barriers).
 // W_rec is stored transposed (wrecT[j][i] = W_rec[i][j]) so the gather of an active
 // presynaptic row is coalesced across the CTA's threads.
 #include "common.cuh"
@@ -38,8 +39,11 @@ __device__ __forceinline__ double rec_spike(double d, bool smooth, double slope)
   return __dadd_rn(0.5, __ddiv_rn(d, __dadd_rn(1.0, __dmul_rn(slope, fabs(d)))));
 }
 
-template <int NPT>
-__global__ void __launch_bounds__(REC_THREADS, 1) forward_rec_kernel(
+// WT: the stored weight type (fp32 weights are gathered as fp32 -- half the registers per
+// load in flight -- and widened exactly to fp64 before the ordered sum).  Two CTAs per SM
+// (<= 64 registers), so the B samples of C3 (256) run as ONE wave on 148 SMs instead of two.
+template <int NPT, typename WT>
+__global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_kernel(
     RecParams P, const double* __restrict__ cur, const void* __restrict__ wrecT,
     double* __restrict__ u_st, double* __restrict__ a_st, double* __restrict__ zbar_st,
     double* __restrict__ zsum_st, uint32_t* __restrict__ raster, float* __restrict__ psis,
@@ -53,8 +57,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1) forward_rec_kernel(
   const bool smooth = P.smooth != 0;
   const double theta = P.theta, beta = P.beta, slope = P.slope;
   const float slope_f = (float)P.slope;
-  const float* wf = static_cast<const float*>(wrecT);
-  const double* wd = static_cast<const double*>(wrecT);
+  const WT* wt = static_cast<const WT*>(wrecT);
   double u[NPT], a[NPT], zb[NPT], zs[NPT], dp[NPT];
 #pragma unroll
   for (int c = 0; c < NPT; ++c) {
@@ -127,23 +130,23 @@ __global__ void __launch_bounds__(REC_THREADS, 1) forward_rec_kernel(
 #pragma unroll
     for (int c = 0; c < NPT; ++c) R[c] = 0.0;
     const int na = nact;
-    constexpr int GB = 8;
+    constexpr int GB = sizeof(WT) == 8 ? 4 : 8;   // spikes whose weight loads are in flight
     for (int q0 = 0; q0 < na; q0 += GB) {
-      double wv[GB][NPT];
+      WT wv[GB][NPT];
 #pragma unroll
       for (int q = 0; q < GB; ++q) {
         const long long o = (long long)(q0 + q < na ? act[q0 + q] : 0) * n;
 #pragma unroll
         for (int c = 0; c < NPT; ++c) {
           const int i = tid + c * REC_THREADS;
-          wv[q][c] = (q0 + q < na && i < n) ? (P.w_f64 ? wd[o + i] : (double)wf[o + i]) : 0.0;
+          wv[q][c] = (q0 + q < na && i < n) ? wt[o + i] : WT(0);
         }
       }
 #pragma unroll
       for (int q = 0; q < GB; ++q)
 #pragma unroll
         for (int c = 0; c < NPT; ++c)
-          if (q0 + q < na) R[c] = __dadd_rn(R[c], wv[q][c]);
+          if (q0 + q < na) R[c] = __dadd_rn(R[c], (double)wv[q][c]);
     }
     float psi[NPT];
 #pragma unroll
@@ -241,15 +244,19 @@ int spb_forward_rec_chunk(int pass, const double* cur, const void* wrecT, int w_
   RecParams P{B, n, Tc, KR, len, t0, T, alpha, theta, slope, beta, rho, kappa,
               reset, alif, pass, smooth, w_is_f64};
   const int npt = (n + REC_THREADS - 1) / REC_THREADS;
-  if (npt <= 1)
-    forward_rec_kernel<1><<<B, REC_THREADS, 0, stream>>>(P, cur, wrecT, u, a, zbar, zsum, raster,
-                                                         psi_scratch, zchunk);
-  else if (npt <= 2)
-    forward_rec_kernel<2><<<B, REC_THREADS, 0, stream>>>(P, cur, wrecT, u, a, zbar, zsum, raster,
-                                                         psi_scratch, zchunk);
-  else
-    forward_rec_kernel<4><<<B, REC_THREADS, 0, stream>>>(P, cur, wrecT, u, a, zbar, zsum, raster,
-                                                         psi_scratch, zchunk);
+#define SPB_REC(NPT, WT)                                                                  \
+  forward_rec_kernel<NPT, WT><<<B, REC_THREADS, 0, stream>>>(P, cur, wrecT, u, a, zbar, zsum, \
+                                                             raster, psi_scratch, zchunk)
+  if (w_is_f64) {
+    if (npt <= 1) SPB_REC(1, double);
+    else if (npt <= 2) SPB_REC(2, double);
+    else SPB_REC(4, double);
+  } else {
+    if (npt <= 1) SPB_REC(1, float);
+    else if (npt <= 2) SPB_REC(2, float);
+    else SPB_REC(4, float);
+  }
+#undef SPB_REC
   SPB_CHECK_LAUNCH("forward_rec");
   return 0;
 }

@@ -186,9 +186,6 @@ class EpropEngine:
         self.wout = torch.empty((m, n), dtype=f64, device=dev)
         # fold the input filter into the one-chunk coefficients (SPB_FILT=0: xbar operand)
         self.filt = os.environ.get("SPB_FILT", "1") != "0"
-        # the single-trace carry (ALIF, or LIF with reset) on CTA pairs (K6p, elig.cu)
-        # unless SPB_CARRY_PAIR=0 (single-CTA K6)
-        self.carry_pair = os.environ.get("SPB_CARRY_PAIR", "1") != "0" and self.ntr == 1
         self.pack_xh = os.environ.get("SPB_PACK_XH", "1") != "0"
         # opt-in memory-for-time trade (off by default: memory then grows with T): park the
         # psi of every chunk in pass A when all of it fits `park_budget` bytes, so pass B
@@ -262,11 +259,10 @@ class EpropEngine:
                 self.wa_hi = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
                 self.wa_lo = torch.zeros((K, self.ldc), dtype=bf16, device=dev)
                 self.eps2 = torch.zeros((B, self.n_pad, self.ke), dtype=f32, device=dev)
-            if self.carry_pair:   # K6p: CTA pairs over 256 x 256 synapse tiles
+            if self.ntr == 1:   # K6: CTA pairs over 256 x 256 synapse tiles
                 tiles6 = 2 * math.ceil(self.kp / 256) * math.ceil(self.n_pad / 256)
-            else:
-                bn6 = 128 if self.ntr == 1 else 64
-                tiles6 = (self.kp // bn6) * (self.n_pad // 128)
+            else:               # K6r: 128 x 64 tiles
+                tiles6 = (self.kp // 64) * (self.n_pad // 128)
             self.splits6 = _wave_split(tiles6, B, sms)
         else:
             self.w_hi = self.w_lo = self.mdt = self.eps = None
@@ -625,8 +621,7 @@ class EpropEngine:
             if self.ntr and (c > 0 or not last):
                 # first chunk: E0 = 0 (nothing to add, only carry); last chunk: no carry
                 if self.ntr == 1:
-                    timed("carry", (ln, c > 0, not last),
-                          "spb_alif_carry_pair" if self.carry_pair else "spb_alif_carry_chunk",
+                    timed("carry", (ln, c > 0, not last, raw_x), "spb_alif_carry_chunk",
                           v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()), self.ldc,
                           v(self.xh.data_ptr()), xl_ptr, v(self.mdt.data_ptr()),
                           v(self.eps.data_ptr()), v(part6), B, n, self.n_pad, self.kx, self.ke,
@@ -634,7 +629,7 @@ class EpropEngine:
                           v(self.xs_hi.data_ptr()) if entry else None,
                           v(self.xs_lo.data_ptr()) if entry else None, st)
                 else:
-                    timed("carry", (ln, c > 0, not last), "spb_reset_carry_chunk",
+                    timed("carry", (ln, c > 0, not last, True), "spb_reset_carry_chunk",
                           v(self.w_hi.data_ptr()), v(self.w_lo.data_ptr()),
                           v(self.wa_hi.data_ptr()), v(self.wa_lo.data_ptr()), self.ldc,
                           v(self.xh.data_ptr()), v(self.mdt.data_ptr()), v(self.eps.data_ptr()),

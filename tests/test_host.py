@@ -120,7 +120,7 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     assert sum(names.count(x) for x in XB) == (0 if pack_xh else nch)
     # K5 per chunk, plus the K = B GEMM of the carried filter state for chunks after the first
     assert names.count("spb_grad_gemm_partials") == nch + (nch - 1)
-    carries = [c[1] for c in rec.calls if c[0] in ("spb_alif_carry_chunk", "spb_alif_carry_pair")]
+    carries = [c[1] for c in rec.calls if c[0] == "spb_alif_carry_chunk"]
     if alif:
         # no carry launch for a single chunk; chunk 0 only carries, the last only adds M E0
         assert len(carries) == (nch if nch > 1 else 0)
@@ -157,8 +157,8 @@ def test_engine_reset_dry_run(monkeypatch, alif):
     assert xb and all(a[8] == 1 and a[9] == 0.0 for a in xb)      # fresh, alpha = 0
     fw = [c[1] for c in rec.calls if c[0] == "spb_forward_chunk"]
     assert all(a[15] == 1 for a in fw)                              # reset flag
-    carry = "spb_reset_carry_chunk" if alif else "spb_alif_carry_pair"
-    other = "spb_alif_carry_pair" if alif else "spb_reset_carry_chunk"
+    carry = "spb_reset_carry_chunk" if alif else "spb_alif_carry_chunk"
+    other = "spb_alif_carry_chunk" if alif else "spb_reset_carry_chunk"
     names = [c[0] for c in rec.calls]
     assert names.count(carry) == 4 and names.count(other) == 0     # 4 chunks
     assert eng.mdt.shape[-1] == (8 if alif else 2)
@@ -193,7 +193,7 @@ def test_engine_forward_only_dry_run(monkeypatch):
     names = [c[0] for c in rec.calls]
     assert names.count("spb_forward_chunk") == 3 and names.count("spb_input_proj") == 3
     assert names[-1] == "spb_readout_loss"
-    for n in ("spb_xbar_chunk", "spb_xbar_chunk_seg", "spb_grad_gemm_partials", "spb_alif_carry_pair",
+    for n in ("spb_xbar_chunk", "spb_xbar_chunk_seg", "spb_grad_gemm_partials", "spb_alif_carry_chunk",
               "spb_readout_grad"):
         assert n not in names
     # smooth flag reaches the kernel (argument after `alif`)

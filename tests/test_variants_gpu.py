@@ -205,30 +205,38 @@ def test_graphed_update_equals_eager(T):
     ("lif", 130, 64, 4, 300, 63, True, "1"),        # LIF reset: the G_u trace
     ("alif", 1024, 700, 40, 700, 255, False, "1"),  # C3-like, several sample splits
 ])
-def test_carry_pair_matches_single_cta(kind, n, k, B, T, chunk, reset, filt, monkeypatch):
-    """K6p (CTA pairs, cta_group::2, streamed eps boxes) against the single-CTA K6: the same
-    products summed in the same per-element order (the MMA K-steps and the epilogue FMAs),
-    so the update agrees to fp32 rounding; losses and spikes are untouched."""
+def test_carry_pairs_vs_oracle(kind, n, k, B, T, chunk, reset, filt, monkeypatch):
+    """K6 on CTA pairs (cta_group::2, streamed eps boxes) over several chunks, at the
+    geometries the pair tiling makes special (one pair column tile, a half pair past
+    n_pad, the filtered 3-MMA operand, LIF reset, several sample splits) against the f64
+    oracle: rasters bit-exact, gradient within the north-star tolerance."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_2501_11407_b200 as P
     from paper_2501_11407_b200.datasets import poisson_batch
     from paper_2501_11407_b200.engine import EpropEngine
     from paper_2501_11407_b200.gradients import _neuron_kwargs
+    from oracle import eprop_ref as O
     net = P.init_network(P.NetworkSpec(kind=kind, n_hidden=n, n_inputs=k, n_classes=5,
                                        precision="f32", reset=reset, seed=31))
     x, y = poisson_batch(B, k, T, 5, seed=32)
     monkeypatch.setenv("SPB_FILT", filt)
-    out = {}
-    for flag in ("1", "0"):
-        monkeypatch.setenv("SPB_CARRY_PAIR", flag)
-        eng = EpropEngine(n, k, 5, B, alif=kind == "alif", chunk=chunk, reset=reset)
-        assert eng.carry_pair == (flag == "1")
-        eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
-        eng.run(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), **_neuron_kwargs(net))
-        torch.cuda.synchronize()
-        out[flag] = (eng.grad_w_acc.cpu().numpy().copy(), eng.loss.cpu().numpy().copy(),
-                     eng.eps.cpu().numpy().copy())
-    assert np.array_equal(out["1"][1], out["0"][1])
-    assert _rel(out["1"][0], out["0"][0]) < 1e-6
-    assert _rel(out["1"][2], out["0"][2]) < 1e-6
+    eng = EpropEngine(n, k, 5, B, alif=kind == "alif", chunk=chunk, reset=reset)
+    assert -(-T // chunk) >= 3 and eng.ntr == 1
+    eng.set_weights(torch.from_numpy(net.neuron.w), torch.from_numpy(net.readout.w_out))
+    eng.run(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), **_neuron_kwargs(net))
+    torch.cuda.synchronize()
+    p = O.Params(alif=kind == "alif", reset=reset)
+    if reset:   # the per-sample forward-mode e-prop (gradients.py:132-185), summed
+        rs = [O.eprop_forward_mode(net.neuron.w, net.readout.w_out, p,
+                                   x[b].astype(np.float64), int(y[b])) for b in range(B)]
+        ref_gw = np.sum([r.grad_w for r in rs], axis=0)
+        ref_loss = np.array([r.loss for r in rs])
+    else:       # feed-forward, no reset: BPTT == e-prop (test_gradients.py:157-168)
+        ref = O.bptt_batch(net.neuron.w, net.readout.w_out, p, x, y)
+        ref_gw, ref_loss = ref.grad_w, ref.loss
+    gw = eng.grad_w(torch.float64).cpu().numpy()
+    assert _rel(gw, ref_gw) < 1e-4
+    cos = float(gw.ravel() @ ref_gw.ravel() / (np.linalg.norm(gw) * np.linalg.norm(ref_gw)))
+    assert cos >= 0.9999
+    assert np.allclose(eng.loss.cpu().numpy(), ref_loss, rtol=1e-9, atol=1e-12)

@@ -77,14 +77,24 @@ def main():
                 per_n.append(row)
             ok = [r for r in per_n if "engine_device_bytes" in r]
             if ok:
-                # memory must not grow with T: compare rows that share a chunk length
-                by_chunk = {}
-                for r in ok:
-                    by_chunk.setdefault(r["chunk"], []).append(r["engine_device_bytes"])
-                flat = {str(c): max(v) / min(v) for c, v in by_chunk.items()}
-                summ = {"n_hidden": n, "engine_bytes_by_T": {r["T"]: r["engine_device_bytes"]
-                                                              for r in ok},
-                        "max_over_min_per_chunk": flat}
+                # memory must not grow with T: the engine at ONE chunk length (the one the
+                # longest T gets) for every T -- buffers are sized by (B, n, k, chunk) only
+                chunk = ok[-1]["chunk"]
+                mem = {}
+                for T in [int(v) for v in args.T.split(",")]:
+                    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c5",
+                           "--hidden", str(n), "--seq-len", str(T), "--global-batch",
+                           str(args.batch), "--chunk", str(chunk), "--steps", "3",
+                           "--warmup", "3", "--no-e2e", "--no-cpu", "--no-parity"]
+                    p = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
+                    for ln in p.stdout.splitlines():
+                        if ln.startswith("{"):
+                            d = json.loads(ln)
+                            mem[T] = {"engine_device_bytes": d["memory"]["engine_device_bytes"],
+                                      "ms_per_update": d["ms_per_step"]}
+                vals = [v["engine_device_bytes"] for v in mem.values()]
+                summ = {"n_hidden": n, "fixed_chunk": chunk, "by_T": mem,
+                        "engine_bytes_max_over_min": (max(vals) / min(vals)) if vals else None}
                 print(json.dumps(summ), flush=True)
                 fo.write(json.dumps(summ) + "\n")
             rows.extend(per_n)

@@ -3,11 +3,11 @@
 # to profiles/<tag>: bench lines, launch lists (+ per-kernel shares), ncu summaries and
 # SASS hot spots (the .ncu-rep files themselves stay in gpurun_out: too large for git).
 set -u
-TAG=${1:-r1}
+TAG=${1:-r2}
 S=gpurun_out/$TAG
 D=profiles/$TAG
 mkdir -p $D
-cp $S/gpu.txt $S/bench_*.json $S/mem_sweep_c5.jsonl $D/ 2>/dev/null
+cp $S/gpu.txt $S/bench_*.json $S/mem_sweep_c5.jsonl $S/c5_sweep.jsonl $S/tc_sweep_*.jsonl $D/ 2>/dev/null
 cp $S/mma_microbench.txt $S/mma_pattern_bench.txt $S/proj_probe.txt $D/ 2>/dev/null
 for f in $S/launches_*.csv; do
   b=$(basename $f .csv)

@@ -64,7 +64,7 @@ def main():
         carry_ms, carry_bytes, full = 0.0, 0.0, []
         eps = 4.0 * B * n * k
         for a, b, meta in timers.get("carry", []):
-            ln, load, store = meta
+            ln, load, store, _raw = meta
             t = a.elapsed_time(b)
             byts = eps * (int(load) + int(store)) + 8.0 * B * n
             if store:   # the per-sample GEMM runs only when the trace is carried out

@@ -11,6 +11,7 @@ CAPTURES = {
     "ncu_grad_gemm": ("c3", "gemm"),
     "ncu_xbar_chunk": ("c3", "xbar"),
     "ncu_alif_carry": ("c5", "carry"),
+    "ncu_alif_carry_tc511": ("c5", "carry"),
 }
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
