@@ -253,6 +253,8 @@ def config_dict(args, world, chunk):
     """The ``config`` object of the JSON line -- the same keys for both arms."""
     kind, n, k, m, T, B, G, scaling = shape_of(args, world)
     desc = CONFIG_DESC[args.config]
+    if scaling == "strong":
+        desc = desc.split(" (")[0] + f" (global batch {G} split over {world} rank(s))"
     if args.config == "c5":
         desc = f"C5 sweep point: ALIF e-prop 700->{n}->{m}, T={T}"
     return {"workload": desc + (" + recurrent W_rec" if args.recurrent else ""),
@@ -413,13 +415,45 @@ def main():
         _lib.call("spb_sgd_update", vp(wout_master.data_ptr()), 0, m, n, vp(gwo.data_ptr()),
                   g64, n, g_scale, lr, vp(eng.wout.data_ptr()), st)
 
-    def step(x, y, timers=None, bits=False):
+    def local_part(x, y, timers=None, bits=False):
         # the synthetic Poisson inputs are 0/1 spikes: promise it (K2 single-int64 path)
         eng.run(x, y, timers=timers, bits=bits, binary=True, **kw)
-        if world > 1:  # the update's single collective
+        if world > 1:
             packer.pack(eng.grad_w_acc, eng.grad_wout, eng.loss, eng.correct)
+
+    def step(x, y, timers=None, bits=False):
+        local_part(x, y, timers=timers, bits=bits)
+        if world > 1:  # the update's single collective
             packer.allreduce()
         update()
+
+    def captured_step(x, y, bits=False):
+        """The step as CUDA-graph replays on these input buffers: one graph at N = 1; at
+        N > 1 the graph of the rank-local part (every kernel of the update and the payload
+        pack), the allreduce launched eagerly on the same stream (collectives are not
+        captured: a capture that succeeded on one rank but hung in replay on another would
+        deadlock the job), then the graph of the optimizer step."""
+        cs_ = torch.cuda.Stream(device=dev)
+        cs_.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(cs_):
+            step(x, y, bits=bits)                   # warm the capture stream
+        torch.cuda.current_stream(dev).wait_stream(cs_)
+        g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1, stream=cs_):
+            local_part(x, y, bits=bits)
+            if world == 1:
+                update()
+        if world == 1:
+            return g1.replay
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2, stream=cs_):
+            update()
+
+        def replay():
+            g1.replay()
+            packer.allreduce()
+            g2.replay()
+        return replay
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
@@ -436,20 +470,13 @@ def main():
     # the allreduce) is captured once in a CUDA graph and replayed per step: no host
     # launch gaps on the device timeline.  Falls back to eager launches if capture fails.
     graph = None
-    # N > 1 over NCCL: the allreduce is captured into the graph too (NCCL supports stream
-    # capture), so every N is timed the same way; gloo ranks (a 1-GPU test of the
-    # multi-rank path) stay eager.  All ranks must agree on the mode.
-    if args.graph and not args.profile and (world == 1 or backend == "nccl"):
+    # N > 1: the rank-local part and the optimizer step are graphs, the allreduce between
+    # them an eager collective (captured_step), so every N replays the same kernels.  All
+    # ranks must agree on the mode.
+    if args.graph and not args.profile:
         try:
-            cs_ = torch.cuda.Stream(device=dev)
-            cs_.wait_stream(torch.cuda.current_stream(dev))
-            with torch.cuda.stream(cs_):
-                step(xd, yd)                     # warm the capture stream
-            torch.cuda.current_stream(dev).wait_stream(cs_)
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=cs_):
-                step(xd, yd)
-            graph.replay()
+            graph = captured_step(xd, yd)
+            graph()
             barrier()
         except Exception as exc:  # noqa: BLE001
             print(f"[bench] CUDA graph capture failed ({exc}); eager launches", file=sys.stderr)
@@ -473,7 +500,7 @@ def main():
         flush.zero_()
         ev[i][0].record()
         if graph is not None:
-            graph.replay()
+            graph()
         else:
             step(xd, yd, timers=timers)
         ev[i][1].record()
@@ -540,17 +567,7 @@ def main():
                     xb[i].copy_(torch.from_numpy(x_bits).to(dev))
                     yb[i].copy_(yd)
                 torch.cuda.synchronize()
-                gsteps = []
-                for i in range(2):
-                    cs2 = torch.cuda.Stream(device=dev)
-                    cs2.wait_stream(torch.cuda.current_stream(dev))
-                    with torch.cuda.stream(cs2):
-                        step(xb[i], yb[i], bits=True)          # warm the capture stream
-                    torch.cuda.current_stream(dev).wait_stream(cs2)
-                    g_i = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(g_i, stream=cs2):
-                        step(xb[i], yb[i], bits=True)
-                    gsteps.append(g_i.replay)
+                gsteps = [captured_step(xb[i], yb[i], bits=True) for i in range(2)]
                 barrier()
             except Exception as exc:  # noqa: BLE001
                 print(f"[bench] e2e graph capture failed ({exc}); eager", file=sys.stderr)
@@ -708,9 +725,10 @@ def main():
                             "+ W re-slice",
                     "psi_parking_gb": args.park_gb,
                     "l2": "512 MiB flush between timed steps (outside events)",
-                    "launch": ("CUDA graph replay of the whole update"
-                               + (" incl. the NCCL allreduce" if world > 1 else ""))
-                              if graph is not None else "eager launches",
+                    "launch": (("CUDA graph replay of the whole update" if world == 1 else
+                                "CUDA graph replays of the rank-local update and of the "
+                                "optimizer step around one eager allreduce")
+                               if graph is not None else "eager launches"),
                     "dist_backend": backend if world > 1 else None},
             "memory": {"engine_device_bytes": eng.device_bytes(),
                        "peak_allocated_bytes": int(torch.cuda.max_memory_allocated(dev)),
