@@ -172,6 +172,15 @@ int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* 
                            int ldb, int M, int N_rows, int K, int splits, float* partial, int ldp,
                            long long slice_stride, cudaStream_t stream);
 
+/* K5p The same GEMM on CTA pairs (tcgen05.mma.cta_group::2, 256 neurons x 256 inputs per
+ *     pair; each CTA stages its 128 A rows and half of the B columns): same arguments and
+ *     results; each of the `splits` K ranges runs on 2*ceil(ldp/256)*ceil(M/256) CTAs.
+ *     Requires ldp % 8 == 0 and slice_stride >= round_up(M, 128) * ldp. */
+int spb_grad_gemm_pair_partials(const void* ah, const void* al, int lda, const void* bh,
+                                const void* bl, int ldb, int M, int N_rows, int K, int splits,
+                                float* partial, int ldp, long long slice_stride,
+                                cudaStream_t stream);
+
 /* K5s CUDA-core version of K5 on the same operands (test cross-check only). */
 int spb_grad_gemm_simt(const void* ah, const void* al, int lda, const void* bh, const void* bl,
                        int ldb, int M, int N, int K, double* grad, int ldg, cudaStream_t stream);

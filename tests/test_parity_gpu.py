@@ -214,6 +214,44 @@ def test_tcgen05_gemm_matches_cuda_core_gemm():
     assert float((got - exact).norm() / exact.norm()) < 1e-4
 
 
+@pytest.mark.parametrize("blo,M,N,K", [(True, 300, 320, 1024), (False, 1024, 768, 2048),
+                                        (False, 130, 128, 96)])
+def test_pair_gemm_matches_single_cta_gemm(blo, M, N, K):
+    """K5 on CTA pairs (cta_group::2) against the single-CTA K5 on the same operands: the
+    same products in the same per-element K order (fp32 accumulation), including a half
+    pair past the partial slice (M = 300, 1 neuron tile of 128 over n_pad) and the raw
+    exact-bf16 B operand (bl = NULL)."""
+    _need_gpu()
+    import ctypes
+    from paper_2501_11407_b200 import _lib
+    torch.manual_seed(1)
+    lda = (M + 7) // 8 * 8
+    mp = (M + 127) // 128 * 128
+    at = torch.zeros(K, lda, device="cuda")
+    at[:, :M] = torch.randn(K, M, device="cuda")
+    ah = at.to(torch.bfloat16); al = (at - ah.float()).to(torch.bfloat16)
+    if blo:
+        bt = torch.randn(K, N, device="cuda")
+    else:
+        bt = (torch.rand(K, N, device="cuda") < 0.1).float()
+    bh = bt.to(torch.bfloat16); bl = (bt - bh.float()).to(torch.bfloat16)
+    v = ctypes.c_void_p
+    out = {}
+    for fn in ("spb_grad_gemm_partials", "spb_grad_gemm_pair_partials"):
+        splits = 3
+        part = torch.full((splits + 1, mp, N), 7.0, device="cuda")   # +1: guard slice
+        _lib.call(fn, v(ah.data_ptr()), v(al.data_ptr()), lda, v(bh.data_ptr()),
+                  v(bl.data_ptr()) if blo else None, N, M, N, K, splits, v(part.data_ptr()), N,
+                  mp * N, None)
+        torch.cuda.synchronize()
+        assert bool((part[splits] == 7.0).all())        # nothing written past the slices
+        out[fn] = part[:splits, :M].double().sum(0)
+    a, b = out["spb_grad_gemm_pair_partials"], out["spb_grad_gemm_partials"]
+    assert float((a - b).norm() / b.norm()) < 1e-6
+    exact = at[:, :M].double().t() @ bt.double()
+    assert float((a - exact).norm() / exact.norm()) < 1e-4
+
+
 def test_label_out_of_range_raises():
     _need_gpu()
     import paper_2501_11407_b200 as P
