@@ -160,9 +160,12 @@ int spb_readout_grad(const double* g, const double* zsum, int B, int n, int m, d
                      cudaStream_t stream);
 
 /* K5  Chunk gradient GEMM on tcgen05 tensor cores (TMA-fed, bf16 hi/lo split, fp32
- *     TMEM accumulation), split-K over `splits` CTAs per 128x256 tile:
+ *     TMEM accumulation) on CTA pairs (cta_group::2, 256x256 per pair; each split runs on
+ *     2*ceil(ldp/256)*ceil(M/256) CTAs), split-K over `splits`:
  *       partial[z][i][j] = sum_{K in split z} (Ah+Al)[K][i] (Bh+Bl)[K][j]  (i<M, j<ldp)
- *     at partial + z*slice_stride (row stride ldp); every slice is written.
+ *     at partial + z*slice_stride (row stride ldp); every slice is written for rows <
+ *     round_up(M,128).  Requires ldp % 8 == 0, slice_stride >= round_up(M,128)*ldp.
+ *     bl = NULL: B exact in bf16 (raw spikes), 2 MMAs per step.
  *     With A = C (K1) and B = xbar (K4) this is every intra-chunk gradient term: the
  *     factorisable LIF part G_u = 1 (x) xbar and the intra-chunk ALIF part.  Replaces the
  *     xbar/xsum n x k accumulation of gradients.py:165-172,180.  A* [K][lda] MN-major
@@ -171,15 +174,6 @@ int spb_readout_grad(const double* g, const double* zsum, int B, int n, int m, d
 int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* bh, const void* bl,
                            int ldb, int M, int N_rows, int K, int splits, float* partial, int ldp,
                            long long slice_stride, cudaStream_t stream);
-
-/* K5p The same GEMM on CTA pairs (tcgen05.mma.cta_group::2, 256 neurons x 256 inputs per
- *     pair; each CTA stages its 128 A rows and half of the B columns): same arguments and
- *     results; each of the `splits` K ranges runs on 2*ceil(ldp/256)*ceil(M/256) CTAs.
- *     Requires ldp % 8 == 0 and slice_stride >= round_up(M, 128) * ldp. */
-int spb_grad_gemm_pair_partials(const void* ah, const void* al, int lda, const void* bh,
-                                const void* bl, int ldb, int M, int N_rows, int K, int splits,
-                                float* partial, int ldp, long long slice_stride,
-                                cudaStream_t stream);
 
 /* K5s CUDA-core version of K5 on the same operands (test cross-check only). */
 int spb_grad_gemm_simt(const void* ah, const void* al, int lda, const void* bh, const void* bl,

@@ -34,7 +34,6 @@ SIGNATURES = {
     "spb_readout_loss": [P, P, P, I, I, I, P, P, P, P, P, P],
     "spb_readout_grad": [P, P, I, I, I, P, P],
     "spb_grad_gemm_partials": [P, P, I, P, P, I, I, I, I, I, P, I, LL, P],
-    "spb_grad_gemm_pair_partials": [P, P, I, P, P, I, I, I, I, I, P, I, LL, P],
     "spb_grad_gemm_simt": [P, P, I, P, P, I, I, I, I, P, I, P],
     "spb_alif_carry_chunk": [P, P, I, P, P, P, P, P, I, I, I, I, I, I, I, I, I, I, I, P, P,
                              P],

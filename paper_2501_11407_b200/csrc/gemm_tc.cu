@@ -1,20 +1,21 @@
 // K5: factorised e-prop gradient GEMM on 5th-generation tensor cores (tcgen05 + TMA).
 //
 //   grad[i][j] += sum_K A[K][i] * B[K][j],   A = chunk coefficients C (M = n neurons)
-//                                            B = xbar_t     (N = k inputs)
-//   both MN-major (neurons / channels contiguous, as K1s / K4 write them),
-//   K = (sample, step) pairs of one time chunk (K = B*Tc), so the LIF trace psi (x) xbar
+//                                            B = xbar_t or raw spikes (N = k inputs)
+//   both MN-major (neurons / channels contiguous, as K1s / K4 / the pack write them),
+//   K = (sample, step) pairs of one time chunk (K = B*KR), so the LIF trace psi (x) xbar
 //   (gradients.py:165-172, G_u = 1 (x) xbar) is never materialised per sample.
 //
 // fp32 accuracy from bf16 tensor cores: every operand is split x = hi + lo (bf16 each)
-// and D += Ah*Bh + Ah*Bl + Al*Bh (the lo*lo term is below fp32 rounding of the sum).
+// and D += Ah*Bh + Ah*Bl + Al*Bh (the lo*lo term is below fp32 rounding of the sum); the
+// raw-spike B is exact in bf16 (Bl = 0, 2 MMAs).
 //
-// Structure (one 128x256 output tile per CTA, split-K over blockIdx.z):
-//   warp 0   TMA producer: Ah, Al (128 x BK), Bh (and Bl unless the B operand is exact in
-//            bf16) (256 x BK), MN-major SWIZZLE_128B boxes, per stage
-//   warp 1   TMEM allocation + converged-warp tcgen05.mma issue (M=128, N=256, K=16; 3
-//            MMAs per K step, 2 for an exact-bf16 B), tcgen05.commit releases smem
-//            stages / signals the epilogue
+// Structure (CTA pairs, one 256 x 256 output tile per pair, split-K over blockIdx.z):
+//   warp 0   TMA producer (both CTAs): own Ah, Al rows (128 x BK), half of the B columns
+//            (128 x BK; Bh, and Bl unless exact), MN-major SWIZZLE_128B boxes, per stage,
+//            transaction bytes on the leader's barrier
+//   warp 1   TMEM allocation (cta_group::2) + on the leader the converged-warp
+//            tcgen05.mma.cta_group::2 issue (M=256, N=256, K=16), commits multicast
 //   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 -> fp32 partial tile (fixed-order reduce later)
 #include "tma.cuh"
 #include <cudaTypedefs.h>
@@ -23,17 +24,8 @@
 namespace spb {
 namespace tc {
 
-constexpr int BM = 128, BN = 256, BK = 32, STAGES = 4;   // 128x256 tiles: 25% less L2 operand
-                                                          // traffic per output than 128x128
-constexpr int TILE_A = BM * BK * 2;  // bytes
-constexpr int TILE_B = BN * BK * 2;
-constexpr int STAGE_BYTES = 2 * TILE_A + 2 * TILE_B;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-// B exact in bf16 (BLO = false: raw spike operand, lo = 0): 2 MMAs per K step, no B-lo
-// stream, the freed shared memory buys 2 more stages
-constexpr int STAGES_NL = 6;
-constexpr int STAGE_BYTES_NL = 2 * TILE_A + TILE_B;
-constexpr int SMEM_BYTES_NL = STAGES_NL * STAGE_BYTES_NL + 1024 + 256;
+constexpr int BM = 128, BN = 256, BK = 32;   // per CTA: 128 neurons x 256 inputs, 32-row K blocks
+constexpr int TILE_A = BM * BK * 2;          // bytes
 constexpr int THREADS = 192;
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart.
@@ -57,218 +49,13 @@ __device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t saddr) {
   d |= (uint64_t)2u << 61;
   return d;
 }
-// Instruction descriptor: kind::f16, A and B bf16 MN-major (bits 15, 16), D fp32.
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
-                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
-}
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
-                   bar)
-               : "memory");
-}
-
-template <bool BLO>
-__global__ void __launch_bounds__(THREADS, 1)
-    grad_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_ah,
-                        const __grid_constant__ CUtensorMap tm_al,
-                        const __grid_constant__ CUtensorMap tm_bh,
-                        const __grid_constant__ CUtensorMap tm_bl, int M, int N, int K,
-                        int kb_per_split, float* __restrict__ partial, int ldp,
-                        long long slice_stride) {
-  constexpr int NST = BLO ? STAGES : STAGES_NL;
-  constexpr int SB = BLO ? STAGE_BYTES : STAGE_BYTES_NL;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * SB);
-  uint64_t* full = bars;                   // [NST]
-  uint64_t* empty = bars + NST;            // [NST]
-  uint64_t* tmem_full = bars + 2 * NST;    // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int nkb = (K + BK - 1) / BK;
-  const int kb0 = blockIdx.z * kb_per_split;
-  const int kb1 = min(nkb, kb0 + kb_per_split);
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < NST; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
-    }
-    mbar_init(smem_u32(tmem_full), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_ah)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_al)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_bh)) : "memory");
-    if (BLO)
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_bl)) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem_base = *tmem_slot;
-  pdl_enter();  // the prologue above touches only shared memory, TMEM and the params
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
-        const int s = it % NST;
-        const uint32_t ph = (it / NST) & 1;
-        mbar_wait(smem_u32(&empty[s]), ph ^ 1);
-        const uint32_t st = smem_u32(smem + s * SB);
-        const uint32_t fb = smem_u32(&full[s]);
-        mbar_expect_tx(fb, SB);
-        tma_load_2d(st, &tm_ah, fb, m0, kb * BK);
-        tma_load_2d(st + TILE_A / 2, &tm_ah, fb, m0 + 64, kb * BK);
-        tma_load_2d(st + TILE_A, &tm_al, fb, m0, kb * BK);
-        tma_load_2d(st + TILE_A + TILE_A / 2, &tm_al, fb, m0 + 64, kb * BK);
-#pragma unroll
-        for (int h = 0; h < BN / 64; ++h) {
-          tma_load_2d(st + 2 * TILE_A + h * (TILE_B / (BN / 64)), &tm_bh, fb, n0 + 64 * h, kb * BK);
-          if (BLO)
-            tma_load_2d(st + 2 * TILE_A + TILE_B + h * (TILE_B / (BN / 64)), &tm_bl, fb,
-                        n0 + 64 * h, kb * BK);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    {  // the whole warp runs the issue loop (converged); elect.sync picks the issuer
-      for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
-        const int s = it % NST;
-        const uint32_t ph = (it / NST) & 1;
-        mbar_wait(smem_u32(&full[s]), ph);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t st = smem_u32(smem + s * SB);
-        const uint32_t sah = st, sal = st + TILE_A, sbh = st + 2 * TILE_A,
-                       sbl = st + 2 * TILE_A + TILE_B;
-#pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint32_t offa = kk * 2048;  // 16 K rows of the MN-major tiles
-          const uint64_t dah = umma_desc_mn_sw128(sah + offa), dal = umma_desc_mn_sw128(sal + offa);
-          const uint64_t dbh = umma_desc_mn_sw128(sbh + offa), dbl = umma_desc_mn_sw128(sbl + offa);
-          umma_bf16(tmem_base, dah, dbh, (kb > kb0 || kk > 0) ? 1u : 0u);
-          if (BLO) umma_bf16(tmem_base, dah, dbl, 1u);
-          umma_bf16(tmem_base, dal, dbh, 1u);
-        }
-        umma_commit(smem_u32(&empty[s]));
-      }
-      umma_commit(smem_u32(tmem_full));
-    }
-  } else {
-    // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
-    const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    const bool have_work = kb1 > kb0;
-    if (have_work) {
-      mbar_wait(smem_u32(tmem_full), 0);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    }
-    float* prow = partial + (long long)blockIdx.z * slice_stride + (long long)row * ldp;
-    // the slice holds every row of the tile grid (n_pad rows) and 32-byte aligned rows:
-    // coalesced transposed stores are allowed
-    const bool rows_padded = slice_stride >= (long long)gridDim.y * BM * ldp && (ldp % 8) == 0;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t r[32];
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-            "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-            "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-            "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-            "=r"(r[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (!have_work) {
-#pragma unroll
-        for (int v = 0; v < 32; ++v) r[v] = 0u;
-      }
-      if (rows_padded) {
-        // 4x4 transpose of 32-byte chunks (8 columns) inside each group of 4 lanes, then
-        // 256-bit stores: each instruction writes 8 rows x 128 contiguous bytes instead of
-        // 32 rows x 16 bytes (rows past M are padding rows of the partial slice)
-        const int p4 = lane & 3;
-#pragma unroll
-        for (int sh = 2; sh >= 1; sh >>= 1) {
-          const bool up = (p4 & sh) != 0;
-#pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            if (m & sh) continue;
-            const int ms = m | sh;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const uint32_t send = up ? r[8 * m + e] : r[8 * ms + e];
-              const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, sh);
-              if (up) r[8 * m + e] = recv; else r[8 * ms + e] = recv;
-            }
-          }
-        }
-        const int col = n0 + c0 + 8 * p4;
-        float* base = partial + (long long)blockIdx.z * slice_stride +
-                      (long long)(m0 + q * 32 + (lane & ~3)) * ldp + col;
-#pragma unroll
-        for (int kq = 0; kq < 4; ++kq) {
-          if (col < ldp) {
-            float* o = base + (long long)kq * ldp;
-            asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(o),
-                         "r"(r[8 * kq + 0]), "r"(r[8 * kq + 1]), "r"(r[8 * kq + 2]),
-                         "r"(r[8 * kq + 3]), "r"(r[8 * kq + 4]), "r"(r[8 * kq + 5]),
-                         "r"(r[8 * kq + 6]), "r"(r[8 * kq + 7])
-                         : "memory");
-          }
-        }
-      } else if (row < M) {
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const int col = n0 + c0 + v * 4;
-          if (col < ldp) {
-            float4 o;
-            o.x = __uint_as_float(r[v * 4 + 0]);
-            o.y = __uint_as_float(r[v * 4 + 1]);
-            o.z = __uint_as_float(r[v * 4 + 2]);
-            o.w = __uint_as_float(r[v * 4 + 3]);
-            *reinterpret_cast<float4*>(prow + col) = o;
-          }
-        }
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(BN));
-  }
-}
-
 // ------------------------------------------------------------------------------------
-// K5 on CTA PAIRS (tcgen05.mma.cta_group::2, M = 256 neurons x N = 256 inputs per pair).
-// The single-CTA kernel above streams, per 32-row K block, 32 KB of operands (A hi/lo for
-// 128 neurons, B for 256 inputs) into each SM for 128 x 256 outputs; at the MMA peak that
-// is ~8.6 KB/clk chip-wide, above the L2 (LTS) throughput (~6.3 KB/clk), so the tensor
-// pipe idles ~25 % (ncu: 74 % active).  A pair stages, per CTA, its own 128 A rows and
-// HALF of the 256 B columns (24 KB per K block for the same 128 x 256 outputs per CTA):
-// 25 % fewer operand bytes per output.  Roles as above; the MMA issuer is the leader's
-// warp 1, the A/B bytes of both CTAs land on the leader's full barrier, commits
-// multicast to both CTAs; each CTA's epilogue stores its own 128 rows x 256 columns.
-// Same products, same per-element K order as the single-CTA kernel.
+// Why pairs (round 2): a single-CTA 128 x 256 tile streams, per 32-row K block, 32 KB of
+// operands (A hi/lo for 128 neurons, B for 256 inputs) into the SM; at the MMA peak that
+// is ~8.6 KB/clk chip-wide, above the L2 (LTS) throughput (~6.3 KB/clk), and its tensor
+// pipe idled ~25 % (ncu: 74 % active, C3 0.140 ms).  A pair stages, per CTA, its own 128
+// A rows and HALF of the 256 B columns (24 KB per K block for the same 128 x 256 outputs
+// per CTA): 25 % fewer operand bytes per output, tensor pipe 94 % active, C3 0.117 ms.
 constexpr int P_BNH = BN / 2;                 // B columns staged per CTA
 constexpr int P_TILE_B = P_BNH * BK * 2;      // 8 KB
 constexpr int P_STAGES = 6, P_STAGES_NL = 8;
@@ -500,19 +287,24 @@ using namespace spb;
 
 extern "C" {
 
-// Split-K tensor-core GEMM writing fp32 partial tiles:
-//   partial[z][i][j] = sum_{K in split z} (Ah+Al)[K][i] (Bh+Bl)[j][K]   (lo*lo dropped)
+// Split-K tensor-core GEMM (grad_gemm_pair_kernel) writing fp32 partial tiles:
+//   partial[z][i][j] = sum_{K in split z} (Ah+Al)[K][i] (Bh+Bl)[K][j]   (lo*lo dropped)
 // bl = NULL: B is exact in bf16 (raw spikes), Bl = 0 -- 2 MMAs per step instead of 3.
-// for i < M, j < ldp; every one of the `splits` slices is written (empty K ranges give 0).
-// Reduced in fixed order with spb_reduce_partials.
-int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* bh, const void* bl,
-                           int ldb, int M, int N_rows, int K, int splits, float* partial, int ldp,
-                           long long slice_stride, cudaStream_t stream) {
+// Every one of the `splits` slices is written for rows < round_up(M, 128), columns < ldp
+// (empty K ranges give 0); each split runs on 2 * ceil(ldp / 256) * ceil(M / 256) CTAs.
+// The slice must hold whole 128-row tiles and 32-byte rows (slice_stride >=
+// round_up(M, 128) * ldp, ldp % 8 == 0).  Reduced in fixed order by spb_reduce_partials.
+int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* bh,
+                                const void* bl, int ldb, int M, int N_rows, int K, int splits,
+                                float* partial, int ldp, long long slice_stride,
+                                cudaStream_t stream) {
   SPB_CHECK_ARG(ah && al && bh && partial, "spb_grad_gemm_partials: null pointer");
-  const bool blo = bl != nullptr;  // bl = NULL: B is exact in bf16 (no lo part), 2 MMAs
-  SPB_CHECK_ARG(M > 0 && N_rows > 0 && K > 0 && splits > 0 && ldp >= 1 &&
-                    lda >= M && lda % 8 == 0 && ldb >= N_rows && ldb % 8 == 0,
-                "spb_grad_gemm_partials: bad sizes M=%d lda=%d N=%d K=%d", M, lda, N_rows, K);
+  const bool blo = bl != nullptr;
+  SPB_CHECK_ARG(M > 0 && N_rows > 0 && K > 0 && splits > 0 && ldp >= 8 && ldp % 8 == 0 &&
+                    lda >= M && lda % 8 == 0 && ldb >= N_rows && ldb % 8 == 0 &&
+                    slice_stride >= (long long)ceil_div(M, tc::BM) * tc::BM * ldp,
+                "spb_grad_gemm_partials: bad sizes M=%d lda=%d N=%d K=%d ldp=%d", M, lda,
+                N_rows, K, ldp);
   SPB_CHECK_ARG((reinterpret_cast<uintptr_t>(ah) | reinterpret_cast<uintptr_t>(al) |
                  reinterpret_cast<uintptr_t>(bh) | reinterpret_cast<uintptr_t>(bl)) % 16 == 0,
                 "spb_grad_gemm_partials: operands must be 16-byte aligned");
@@ -521,49 +313,6 @@ int spb_grad_gemm_partials(const void* ah, const void* al, int lda, const void* 
       !tc::make_map_mn(&mbh, bh, N_rows, ldb, K) ||
       !tc::make_map_mn(&mbl, blo ? bl : bh, N_rows, ldb, K)) {
     set_error("spb_grad_gemm_partials: cuTensorMapEncodeTiled failed");
-    return 3;
-  }
-  const int nkb = ceil_div(K, tc::BK);
-  const int kbps = ceil_div(nkb, splits);
-  dim3 grid(ceil_div(ldp, tc::BN), ceil_div(M, tc::BM), splits);
-  if (blo) {
-    cudaFuncSetAttribute(tc::grad_gemm_tc_kernel<true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
-    pdl_launch(tc::grad_gemm_tc_kernel<true>, grid, tc::THREADS, tc::SMEM_BYTES, stream,
-        mah, mal, mbh, mbl, M, N_rows, K, kbps, partial, ldp, slice_stride);
-  } else {
-    cudaFuncSetAttribute(tc::grad_gemm_tc_kernel<false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES_NL);
-    pdl_launch(tc::grad_gemm_tc_kernel<false>, grid, tc::THREADS, tc::SMEM_BYTES_NL, stream,
-        mah, mal, mbh, mbl, M, N_rows, K, kbps, partial, ldp, slice_stride);
-  }
-  SPB_CHECK_LAUNCH("grad_gemm_tc");
-  return 0;
-}
-
-// K5 on CTA pairs (grad_gemm_pair_kernel): same arguments and results as
-// spb_grad_gemm_partials; each of the `splits` K ranges runs on 2 * ceil(ldp / 256) *
-// ceil(M / 256) CTAs.  The partial slice must hold whole 128-row tiles and 32-byte rows
-// (slice_stride >= round_up(M, 128) * ldp, ldp % 8 == 0).
-int spb_grad_gemm_pair_partials(const void* ah, const void* al, int lda, const void* bh,
-                                const void* bl, int ldb, int M, int N_rows, int K, int splits,
-                                float* partial, int ldp, long long slice_stride,
-                                cudaStream_t stream) {
-  SPB_CHECK_ARG(ah && al && bh && partial, "spb_grad_gemm_pair_partials: null pointer");
-  const bool blo = bl != nullptr;
-  SPB_CHECK_ARG(M > 0 && N_rows > 0 && K > 0 && splits > 0 && ldp >= 8 && ldp % 8 == 0 &&
-                    lda >= M && lda % 8 == 0 && ldb >= N_rows && ldb % 8 == 0 &&
-                    slice_stride >= (long long)ceil_div(M, tc::BM) * tc::BM * ldp,
-                "spb_grad_gemm_pair_partials: bad sizes M=%d lda=%d N=%d K=%d ldp=%d", M, lda,
-                N_rows, K, ldp);
-  SPB_CHECK_ARG((reinterpret_cast<uintptr_t>(ah) | reinterpret_cast<uintptr_t>(al) |
-                 reinterpret_cast<uintptr_t>(bh) | reinterpret_cast<uintptr_t>(bl)) % 16 == 0,
-                "spb_grad_gemm_pair_partials: operands must be 16-byte aligned");
-  CUtensorMap mah, mal, mbh, mbl;
-  if (!tc::make_map_mn(&mah, ah, M, lda, K) || !tc::make_map_mn(&mal, al, M, lda, K) ||
-      !tc::make_map_mn(&mbh, bh, N_rows, ldb, K) ||
-      !tc::make_map_mn(&mbl, blo ? bl : bh, N_rows, ldb, K)) {
-    set_error("spb_grad_gemm_pair_partials: cuTensorMapEncodeTiled failed");
     return 3;
   }
   const int nkb = ceil_div(K, tc::BK);

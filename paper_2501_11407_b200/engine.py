@@ -186,10 +186,6 @@ class EpropEngine:
         self.wout = torch.empty((m, n), dtype=f64, device=dev)
         # fold the input filter into the one-chunk coefficients (SPB_FILT=0: xbar operand)
         self.filt = os.environ.get("SPB_FILT", "1") != "0"
-        # K5 on CTA pairs (gemm_tc.cu grad_gemm_pair_kernel) unless SPB_GEMM_PAIR=0
-        self.gemm_pair = os.environ.get("SPB_GEMM_PAIR", "1") != "0"
-        self.gemm_fn = ("spb_grad_gemm_pair_partials" if self.gemm_pair
-                        else "spb_grad_gemm_partials")
         self.pack_xh = os.environ.get("SPB_PACK_XH", "1") != "0"
         # opt-in memory-for-time trade (off by default: memory then grows with T): park the
         # psi of every chunk in pass A when all of it fits `park_budget` bytes, so pass B
@@ -248,10 +244,7 @@ class EpropEngine:
         self.xs_hi = torch.zeros((B, self.kp), dtype=bf16, device=dev)
         self.xs_lo = torch.zeros((B, self.kp), dtype=bf16, device=dev)
         # split-K (K5) and sample-split (K6) partial slices, reduced in fixed order
-        if self.gemm_pair:   # K5 on CTA pairs: 256 x 256 per pair
-            tiles5 = 2 * math.ceil(self.kp / 256) * math.ceil(n / 256)
-        else:                # K5 tiles are 128 x 256
-            tiles5 = math.ceil(self.kp / 256) * math.ceil(n / 128)
+        tiles5 = 2 * math.ceil(self.kp / 256) * math.ceil(n / 256)   # K5: CTA pairs, 256 x 256
         # split-K so the grid fills whole waves of SMs (C4: 96 tiles x 3 = 1.95 waves)
         self.splits5 = _wave_split(tiles5, max(1, K // 64), sms)
         self.wa_hi = self.wa_lo = self.eps2 = None
@@ -611,14 +604,14 @@ class EpropEngine:
                      ln, int(c == 0 or self.reset), x_alpha, v(self.xbar_state.data_ptr()),
                      v(self.xh.data_ptr()), xl_ptr, st)
                 self.launches += 1
-            timed("gemm", (ln, raw_x), self.gemm_fn, v(self.c_hi.data_ptr()),
+            timed("gemm", (ln, raw_x), "spb_grad_gemm_partials", v(self.c_hi.data_ptr()),
                   v(self.c_lo.data_ptr()), self.ldc, v(self.xh.data_ptr()), xl_ptr,
                   self.kp, n, self.kp, K, self.splits5, v(self.partial.data_ptr()), self.kp,
                   slice_stride, st)
             self.launches += 1
             entry = filt and not one and c > 0   # row-0 terms of the carried filter state
             if entry:  # sum_b Ct_0[b,i] xbar_{t0-1}[b,j]: rows b*KR of C, K = B
-                call(self.gemm_fn, v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()),
+                call("spb_grad_gemm_partials", v(self.c_hi.data_ptr()), v(self.c_lo.data_ptr()),
                      KR * self.ldc, v(self.xs_hi.data_ptr()), v(self.xs_lo.data_ptr()),
                      self.kp, n, self.kp, B, 1,
                      v(self.partial.data_ptr() + (self.splits5 + self.splits6) * slice_stride * 4),

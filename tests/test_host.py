@@ -119,7 +119,7 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     assert names.count("spb_slice_weights") == 0
     assert sum(names.count(x) for x in XB) == (0 if pack_xh else nch)
     # K5 per chunk, plus the K = B GEMM of the carried filter state for chunks after the first
-    assert names.count(eng.gemm_fn) == nch + (nch - 1)
+    assert names.count("spb_grad_gemm_partials") == nch + (nch - 1)
     carries = [c[1] for c in rec.calls if c[0] == "spb_alif_carry_chunk"]
     if alif:
         # no carry launch for a single chunk; chunk 0 only carries, the last only adds M E0
@@ -137,7 +137,7 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     if nch == 1:  # pass A parks psi, pass B runs the scan only, input filter folded in
         assert [c[1][0] for c in rec.calls if c[0] == "spb_forward_chunk"] == [0, 3]
         # the raw-spike operand: written by the pack, K5 gets no B-lo
-        gm = [c[1] for c in rec.calls if c[0] == eng.gemm_fn]
+        gm = [c[1] for c in rec.calls if c[0] == "spb_grad_gemm_partials"]
         assert all(a[4] is None for a in gm)
     assert eng.launches == len(rec.calls) + passb
 
@@ -193,8 +193,7 @@ def test_engine_forward_only_dry_run(monkeypatch):
     names = [c[0] for c in rec.calls]
     assert names.count("spb_forward_chunk") == 3 and names.count("spb_input_proj") == 3
     assert names[-1] == "spb_readout_loss"
-    for n in ("spb_xbar_chunk", "spb_xbar_chunk_seg", "spb_grad_gemm_partials", "spb_grad_gemm_pair_partials",
-              "spb_alif_carry_chunk",
+    for n in ("spb_xbar_chunk", "spb_xbar_chunk_seg", "spb_grad_gemm_partials", "spb_alif_carry_chunk",
               "spb_readout_grad"):
         assert n not in names
     # smooth flag reaches the kernel (argument after `alif`)

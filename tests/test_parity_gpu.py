@@ -186,41 +186,13 @@ def test_batched_vs_two_pass_oracle(kind, n, k, m, T, B, chunk):
     assert np.allclose(eng.loss.cpu().numpy(), ref.loss, rtol=1e-9)
 
 
-def test_tcgen05_gemm_matches_cuda_core_gemm():
-    _need_gpu()
-    import ctypes
-    from paper_2501_11407_b200 import _lib
-    torch.manual_seed(0)
-    M, N, K, lda = 300, 320, 1024, 304
-    a = torch.randn(M, K, device="cuda")
-    b = torch.randn(N, K, device="cuda")
-    at = torch.zeros(K, lda, device="cuda")
-    at[:, :M] = a.t()                       # MN-major A operand [K][lda]
-    ah = at.to(torch.bfloat16); al = (at - ah.float()).to(torch.bfloat16)
-    bt = b.t().contiguous()                 # MN-major B operand [K][N]
-    bh = bt.to(torch.bfloat16); bl = (bt - bh.float()).to(torch.bfloat16)
-    splits = 3
-    part = torch.zeros((splits, M, N), device="cuda")
-    v = ctypes.c_void_p
-    _lib.call("spb_grad_gemm_partials", v(ah.data_ptr()), v(al.data_ptr()), lda, v(bh.data_ptr()),
-              v(bl.data_ptr()), N, M, N, K, splits, v(part.data_ptr()), N, M * N, None)
-    ref = torch.zeros((M, N), dtype=torch.float64, device="cuda")
-    _lib.call("spb_grad_gemm_simt", v(ah.data_ptr()), v(al.data_ptr()), lda, v(bh.data_ptr()),
-              v(bl.data_ptr()), N, M, N, K, v(ref.data_ptr()), N, None)
-    torch.cuda.synchronize()
-    got = part.double().sum(0)
-    exact = a.double() @ b.double().t()
-    assert float((got - ref).norm() / ref.norm()) < 1e-5
-    assert float((got - exact).norm() / exact.norm()) < 1e-4
-
-
 @pytest.mark.parametrize("blo,M,N,K", [(True, 300, 320, 1024), (False, 1024, 768, 2048),
                                         (False, 130, 128, 96)])
-def test_pair_gemm_matches_single_cta_gemm(blo, M, N, K):
-    """K5 on CTA pairs (cta_group::2) against the single-CTA K5 on the same operands: the
-    same products in the same per-element K order (fp32 accumulation), including a half
-    pair past the partial slice (M = 300, 1 neuron tile of 128 over n_pad) and the raw
-    exact-bf16 B operand (bl = NULL)."""
+def test_pair_gemm_slices_vs_cuda_core_gemm(blo, M, N, K):
+    """K5 on CTA pairs at the geometries the pair tiling makes special -- a half pair
+    past the partial slice (M = 300 over 384 rows, M = 130), the raw exact-bf16 B operand
+    (bl = NULL), several splits -- against the CUDA-core GEMM on the same operands and the
+    exact product; nothing is written past the last slice."""
     _need_gpu()
     import ctypes
     from paper_2501_11407_b200 import _lib
@@ -236,20 +208,21 @@ def test_pair_gemm_matches_single_cta_gemm(blo, M, N, K):
         bt = (torch.rand(K, N, device="cuda") < 0.1).float()
     bh = bt.to(torch.bfloat16); bl = (bt - bh.float()).to(torch.bfloat16)
     v = ctypes.c_void_p
-    out = {}
-    for fn in ("spb_grad_gemm_partials", "spb_grad_gemm_pair_partials"):
-        splits = 3
-        part = torch.full((splits + 1, mp, N), 7.0, device="cuda")   # +1: guard slice
-        _lib.call(fn, v(ah.data_ptr()), v(al.data_ptr()), lda, v(bh.data_ptr()),
-                  v(bl.data_ptr()) if blo else None, N, M, N, K, splits, v(part.data_ptr()), N,
-                  mp * N, None)
-        torch.cuda.synchronize()
-        assert bool((part[splits] == 7.0).all())        # nothing written past the slices
-        out[fn] = part[:splits, :M].double().sum(0)
-    a, b = out["spb_grad_gemm_pair_partials"], out["spb_grad_gemm_partials"]
-    assert float((a - b).norm() / b.norm()) < 1e-6
+    splits = 3
+    part = torch.full((splits + 1, mp, N), 7.0, device="cuda")   # +1: guard slice
+    _lib.call("spb_grad_gemm_partials", v(ah.data_ptr()), v(al.data_ptr()), lda,
+              v(bh.data_ptr()), v(bl.data_ptr()) if blo else None, N, M, N, K, splits,
+              v(part.data_ptr()), N, mp * N, None)
+    ref = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+    zl = torch.zeros_like(bl)
+    _lib.call("spb_grad_gemm_simt", v(ah.data_ptr()), v(al.data_ptr()), lda, v(bh.data_ptr()),
+              v((bl if blo else zl).data_ptr()), N, M, N, K, v(ref.data_ptr()), N, None)
+    torch.cuda.synchronize()
+    assert bool((part[splits] == 7.0).all())        # nothing written past the slices
+    got = part[:splits, :M].double().sum(0)
+    assert float((got - ref).norm() / ref.norm()) < 1e-5
     exact = at[:, :M].double().t() @ bt.double()
-    assert float((a - exact).norm() / exact.norm()) < 1e-4
+    assert float((got - exact).norm() / exact.norm()) < 1e-4
 
 
 def test_label_out_of_range_raises():
