@@ -97,46 +97,65 @@ __global__ void __launch_bounds__(K1_THREADS, 7) forward_chunk_kernel(
                      ? raster + ((long long)b * P.T + P.t0) * nw + (wbase >> 5) : nullptr;
   const int len = P.len;
   // software pipeline: the current of steps s8+8..s8+15 is in flight while steps
-  // s8..s8+7 integrate (16 outstanding 8-byte loads per thread)
+  // s8..s8+7 integrate (16 outstanding 8-byte loads per thread).  Blocks of 8 steps that
+  // lie entirely inside the chunk run without per-step bounds checks (the guards were a
+  // third of the loop's integer instructions; the kernel is issue-bound).
+  auto step = [&](double I) {
+    // gradients.py:121-129 (u - theta - beta*a evaluates as (u - theta) - (beta*a))
+    const double z_prev = spike_value(d_prev, SMOOTH, slope_d);
+    a = __dadd_rn(__dmul_rn(rho, a), z_prev);
+    u = __dadd_rn(__dmul_rn(alpha, u), I);
+    if (RESET) u = __dsub_rn(u, __dmul_rn(theta, z_prev));
+    const double d = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
+    if (PASSA) {
+      const double zv = spike_value(d, SMOOTH, slope_d);
+      zbar = __dadd_rn(__dmul_rn(kappa, zbar), zv);
+      zsum = __dadd_rn(zsum, zbar);
+      // raster = z > 0.5 (gradients.py:362)
+      const unsigned bal = __ballot_sync(0xffffffffu, zv > 0.5 && valid_i);
+      if (rp != nullptr) {
+        if (lane == 0) rp[0] = bal;
+        rp += nw;
+      }
+    }
+    // the surrogate only scales fp32 eligibilities: evaluate it in fp32
+    if (PARK) {
+      pp += n;
+      if (park) pp[0] = surrogate_grad_f32((float)d, slope);
+    }
+    d_prev = d;
+  };
   double In[8];
+  if (len >= 8) {
 #pragma unroll
-  for (int u8 = 0; u8 < 8; ++u8) In[u8] = u8 < len ? __ldcs(cp + (long long)u8 * n) : 0.0;
+    for (int u8 = 0; u8 < 8; ++u8) In[u8] = __ldcs(cp + (long long)u8 * n);
+  } else {
+#pragma unroll
+    for (int u8 = 0; u8 < 8; ++u8) In[u8] = u8 < len ? __ldcs(cp + (long long)u8 * n) : 0.0;
+  }
   const long long n8 = 8LL * n;
-  for (int s8 = 0; s8 < len; s8 += 8) {
+  const int full = len & ~7;   // steps in complete blocks of 8
+  int s8 = 0;
+  for (; s8 < full; s8 += 8) {
     double Ib[8];
 #pragma unroll
     for (int u8 = 0; u8 < 8; ++u8) Ib[u8] = In[u8];
     cp += n8;
+    if (s8 + 16 <= len) {
 #pragma unroll
-    for (int u8 = 0; u8 < 8; ++u8)
-      In[u8] = (s8 + 8 + u8 < len) ? __ldcs(cp + (long long)u8 * n) : 0.0;
+      for (int u8 = 0; u8 < 8; ++u8) In[u8] = __ldcs(cp + (long long)u8 * n);
+    } else {
 #pragma unroll
-    for (int u8 = 0; u8 < 8; ++u8) {
-      if (s8 + u8 < len) {
-        // gradients.py:121-129 (u - theta - beta*a evaluates as (u - theta) - (beta*a))
-        const double z_prev = spike_value(d_prev, SMOOTH, slope_d);
-        a = __dadd_rn(__dmul_rn(rho, a), z_prev);
-        u = __dadd_rn(__dmul_rn(alpha, u), Ib[u8]);
-        if (RESET) u = __dsub_rn(u, __dmul_rn(theta, z_prev));
-        const double d = __dsub_rn(__dsub_rn(u, theta), __dmul_rn(beta, a));
-        if (PASSA) {
-          const double zv = spike_value(d, SMOOTH, slope_d);
-          zbar = __dadd_rn(__dmul_rn(kappa, zbar), zv);
-          zsum = __dadd_rn(zsum, zbar);
-          // raster = z > 0.5 (gradients.py:362)
-          const unsigned bal = __ballot_sync(0xffffffffu, zv > 0.5 && valid_i);
-          if (rp != nullptr && lane == 0) rp[0] = bal;
-          if (rp != nullptr) rp += nw;
-        }
-        // the surrogate only scales fp32 eligibilities: evaluate it in fp32
-        if (PARK) {
-          pp += n;
-          if (park) pp[0] = surrogate_grad_f32((float)d, slope);
-        }
-        d_prev = d;
-      }
+      for (int u8 = 0; u8 < 8; ++u8)
+        In[u8] = (s8 + 8 + u8 < len) ? __ldcs(cp + (long long)u8 * n) : 0.0;
     }
+#pragma unroll
+    for (int u8 = 0; u8 < 8; ++u8) step(Ib[u8]);
   }
+  // the last partial block (its current is already in In)
+#pragma unroll
+  for (int u8 = 0; u8 < 7; ++u8)
+    if (s8 + u8 < len) step(In[u8]);
   if (valid_i) {
     u_st[bi] = u;
     a_st[bi] = a;
