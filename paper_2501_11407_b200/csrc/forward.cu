@@ -24,6 +24,7 @@
 //   C_rho = R_rho [rho < L] + Lpsi_{rho-1} [rho >= 1]          (LIF: R = 0)
 // plus the elementwise M E0 term, and the carried trace is a per-sample GEMM with W.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -254,29 +255,18 @@ __global__ void __launch_bounds__(K1S_THREADS, SCAN_OCC) chunk_scan_kernel(
   float lam0 = 0.f, dcum0 = 1.f, an0 = 0.f, lam1 = 0.f, dcum1 = 1.f, an1 = 0.f;
   float ft0 = 0.f, ft1 = 0.f, fw0 = 0.f, fw1 = 0.f;  // FILT: running Ct, Wt
   const float falpha = (float)P.alpha;
-  // rows in blocks of SCAN_BLK: the next block's psi loads are issued before this block
-  // is processed (1-2 blocks in flight per thread, no register shifting)
-  float2 nxt[SCAN_BLK];
-#pragma unroll
-  for (int u = 0; u < SCAN_BLK; ++u) nxt[u] = ldpsi(L - u);
+  // one row r (psi row r = psi_{r-1}); MID: 1 <= r < L, i.e. no boundary case -- rows L
+  // and 0 and the last partial block take the checked path
   float2 up = make_float2(0.f, 0.f);  // psi row r+1
-  for (int r8 = L; r8 >= 0; r8 -= SCAN_BLK) {
-    float2 blk[SCAN_BLK];
-#pragma unroll
-    for (int u = 0; u < SCAN_BLK; ++u) blk[u] = nxt[u];
-#pragma unroll
-    for (int u = 0; u < SCAN_BLK; ++u) nxt[u] = ldpsi(r8 - SCAN_BLK - u);
-#pragma unroll
-    for (int u = 0; u < SCAN_BLK; ++u) {
-    const int r = r8 - u;
-    if (r < 0) break;
-    const float2 cur = blk[u];  // psi row r = psi_{r-1}
-    const float c_prev = cs[r], c_r = (r < L) ? cs[r + 1] : 0.f;
+  auto row = [&](const int r, const float2 cur, auto mid_tag) {
+    constexpr bool MID = decltype(mid_tag)::value;
+    const float c_prev = cs[r];
+    const float c_r = (MID || r < L) ? cs[r + 1] : 0.f;
     // L_{r-1} psi_{r-1} (row r >= 1) [+ R_r = P_r Lambda_r, ALIF]; W_r = P_r D(L-1, r)
-    float c0 = r >= 1 ? c_prev * ws0 * cur.x : 0.f;
-    float c1 = r >= 1 ? c_prev * ws1 * cur.y : 0.f;
+    float c0 = (MID || r >= 1) ? c_prev * ws0 * cur.x : 0.f;
+    float c1 = (MID || r >= 1) ? c_prev * ws1 * cur.y : 0.f;
     float w0 = 0.f, w1 = 0.f;
-    if (ALIF && r < L) {
+    if (ALIF && (MID || r < L)) {
       const float A0 = fmaf(-beta, cur.x, rho), A1 = fmaf(-beta, cur.y, rho);
       lam0 = fmaf(an0, lam0, -beta * (c_r * ws0 * up.x));
       lam1 = fmaf(an1, lam1, -beta * (c_r * ws1 * up.y));
@@ -315,8 +305,30 @@ __global__ void __launch_bounds__(K1S_THREADS, SCAN_OCC) chunk_scan_kernel(
       wlp -= ld2;
     }
     up = cur;
-    }
+  };
+  using checked = std::integral_constant<bool, false>;
+  using mid = std::integral_constant<bool, true>;
+  row(L, ldpsi(L), checked{});
+  // rows L-1 .. 1 in blocks of SCAN_BLK: the next block's psi loads are issued before
+  // this block is processed (1-2 blocks in flight per thread, no register shifting);
+  // complete blocks run without per-row boundary checks (the loop is issue-bound)
+  int r8 = L - 1;
+  float2 nxt[SCAN_BLK];
+#pragma unroll
+  for (int u = 0; u < SCAN_BLK; ++u) nxt[u] = ldpsi(r8 - u);
+  for (; r8 - (SCAN_BLK - 1) >= 1; r8 -= SCAN_BLK) {
+    float2 blk[SCAN_BLK];
+#pragma unroll
+    for (int u = 0; u < SCAN_BLK; ++u) blk[u] = nxt[u];
+#pragma unroll
+    for (int u = 0; u < SCAN_BLK; ++u) nxt[u] = ldpsi(r8 - SCAN_BLK - u);
+#pragma unroll
+    for (int u = 0; u < SCAN_BLK; ++u) row(r8 - u, blk[u], mid{});
   }
+  // the last rows (r8 .. 0, at most SCAN_BLK of them, already loaded)
+#pragma unroll
+  for (int u = 0; u < SCAN_BLK; ++u)
+    if (r8 - u >= 0) row(r8 - u, nxt[u], checked{});
   if (ALIF && mdt != nullptr) {  // M also feeds the last chunk's inter-chunk term
     mdt[bi] = make_float2(an0 * lam0, dcum0);  // M = A_0 Lambda_0, Dt = prod A
     if (has2) mdt[bi + 1] = make_float2(an1 * lam1, dcum1);
