@@ -49,7 +49,9 @@ int spb_device_sm(void); /* compute capability of the current device, e.g. 100 *
  *                      bytes, channel j = bit (j & 7) of byte j >> 3 (packbits, little);
  *                      output row b*Tc + s, or s*B + b with time_major != 0.
  *   spb_input_proj:    cur[row][i] = sum_j xq[row][j] W[i][j] for row < M (= B*Tc), fp64;
- *                      persistent grid of min(tiles, sm_count) CTAs.  binary != 0 promises
+ *                      persistent grid of min(tiles, sm_count) CTAs.  k = the real input
+ *                      count (columns k..Kpad-1 of xq/wq are zero): when the last partial
+ *                      128-byte K block holds <= 64 inputs it runs as a 64-byte block.  binary != 0 promises
  *                      0/1 spikes (and k <= 16384): the 7 digit sums then recombine in one
  *                      int64 (same bits, half the fp64 work). */
 int spb_slice_weights(const void* w, int w_is_f64, int n, int k, int Kpad, int n_pad32, int P,
@@ -62,12 +64,13 @@ int spb_pack_spikes(const uint8_t* x, long long stride_b, int B, int k, int bits
 int spb_pack_spikes_xh(const uint8_t* x, long long stride_b, int B, int k, int bits, int len,
                        int Tc, int Kpad, int KR, uint8_t* xq, void* xh, cudaStream_t stream);
 int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
-                   int Kpad, int P, double* cur, int sm_count, int binary, cudaStream_t stream);
+                   int k, int Kpad, int P, double* cur, int sm_count, int binary,
+                   cudaStream_t stream);
 /* Profiling variant of spb_input_proj (W-resident kernel): probe bit 0 skips the epilogue,
  * bit 1 the spike-operand loads; probe = 0 is the production kernel. */
 int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
-                         int n_pad32, int Kpad, int P, double* cur, int sm_count, int binary,
-                         int probe, cudaStream_t stream);
+                         int n_pad32, int k, int Kpad, int P, double* cur, int sm_count,
+                         int binary, int probe, cudaStream_t stream);
 
 /* K1  Neuron dynamics over one time chunk from the exact current cur [B*KR][n] (row
  *     b*KR+s, sample-aligned): ALIF/LIF state update, spike and surrogate derivative.

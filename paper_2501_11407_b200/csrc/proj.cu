@@ -79,6 +79,29 @@ __device__ __forceinline__ void mma_i8_x4(uint32_t tmem_d, uint64_t a, uint64_t 
       "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %3, 1;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc0));
 }
+// K-major SWIZZLE_64B operand (the 64-byte tail K block of the spikes): 8-row groups 512 B
+// apart, swizzle mode 4
+__device__ __forceinline__ uint64_t desc_k_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(512u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)4u << 61;
+  return d;
+}
+// The 2 MMAs of the 64-byte tail K block under one elect.sync (A: SW64, B: SW128 rows).
+__device__ __forceinline__ void mma_i8_x2(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                          uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, b1;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 b1, %2, 2;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, 1;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc0));
+}
 __device__ __forceinline__ void commit(uint32_t bar) {
   asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
                "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
@@ -302,9 +325,12 @@ struct ResCfg {
 template <int P, int XS, bool BIN>
 __global__ void __launch_bounds__(THREADS, 1)
     input_proj_wres_kernel(const __grid_constant__ CUtensorMap tm_x,
-                           const __grid_constant__ CUtensorMap tm_w, const int* __restrict__ sexp,
+                           const __grid_constant__ CUtensorMap tm_w,
+                           const __grid_constant__ CUtensorMap tm_xt, const int* __restrict__ sexp,
                            double* __restrict__ out, int M, int n, int n_pad32, int nkb,
-                           int probe) {
+                           int tail, int probe) {
+  // nkb full 128-byte K blocks, then (tail) one 64-byte block: k = 700 runs 704 bytes of
+  // K instead of 768 (8 % fewer MMAs and spike-operand bytes)
   using C = ResCfg<P, XS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -362,8 +388,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (nt != cur_nt) {  // (re)load this neuron tile's weight slices, all K blocks
           mbar_wait(smem_u32(wempty), (wl & 1) ^ 1);
           const uint32_t fb = smem_u32(wfull);
-          mbar_expect_tx(fb, nkb * C::WBLK);
-          for (int kb = 0; kb < nkb; ++kb)
+          mbar_expect_tx(fb, (nkb + tail) * C::WBLK);
+          for (int kb = 0; kb < nkb + tail; ++kb)
 #pragma unroll
             for (int p = 0; p < P; ++p)
               tma_load_2d(smem_u32(wsm + kb * C::WBLK + p * NT * BK), &tm_w, fb, kb * BK,
@@ -381,6 +407,18 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           mbar_expect_tx(fb, TILE_A);
           tma_load_2d(smem_u32(xsm + s * TILE_A), &tm_x, fb, kb * BK, mt * BM);
+        }
+        if (tail) {  // the 64-byte tail block (SWIZZLE_64B box) into the next stage
+          const int s = it % XS;
+          mbar_wait(smem_u32(&xempty[s]), ((it / XS) & 1) ^ 1);
+          const uint32_t fb = smem_u32(&xfull[s]);
+          if (probe & 2) {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
+          } else {
+            mbar_expect_tx(fb, TILE_A / 2);
+            tma_load_2d(smem_u32(xsm + s * TILE_A), &tm_xt, fb, nkb * BK, mt * BM);
+          }
+          ++it;
         }
       }
     }
@@ -407,6 +445,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           static_assert(BK / 32 == 4, "four K steps per block");
           mma_i8_x4(dacc, desc_k_sw128(xa), desc_k_sw128(wa), Cfg<P>::IDESC, kb ? 1u : 0u);
           commit(smem_u32(&xempty[s]));
+        }
+        if (tail) {
+          const int s = it % XS;
+          mbar_wait(smem_u32(&xfull[s]), (it / XS) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          mma_i8_x2(dacc, desc_k_sw64(smem_u32(xsm + s * TILE_A)),
+                    desc_k_sw128(smem_u32(wsm + nkb * C::WBLK)), Cfg<P>::IDESC, nkb ? 1u : 0u);
+          commit(smem_u32(&xempty[s]));
+          ++it;
         }
         commit(smem_u32(&tfull[a]));
         // last tile of this neuron tile: the weight region may be refilled afterwards
@@ -822,27 +869,35 @@ int spb_slice_weights(const void* w, int w_is_f64, int n, int k, int Kpad, int n
 }
 
 int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
-                         int n_pad32, int Kpad, int P, double* out, int sm_count, int binary,
-                         int probe, cudaStream_t stream);
+                         int n_pad32, int k, int Kpad, int P, double* out, int sm_count,
+                         int binary, int probe, cudaStream_t stream);
 
 int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
-                   int Kpad, int P, double* out, int sm_count, int binary, cudaStream_t stream) {
-  return spb_input_proj_probe(xq, wq, sexp, M, n, n_pad32, Kpad, P, out, sm_count, binary, 0,
+                   int k, int Kpad, int P, double* out, int sm_count, int binary,
+                   cudaStream_t stream) {
+  return spb_input_proj_probe(xq, wq, sexp, M, n, n_pad32, k, Kpad, P, out, sm_count, binary, 0,
                               stream);
+}
+
+// SPB_K2_TAIL=0: the zero-padded last K block instead of the 64-byte tail (A/B, tests)
+static bool k2_tail() {
+  const char* e = getenv("SPB_K2_TAIL");
+  return !(e && e[0] == '0');
 }
 
 // spb_input_proj with a profiling probe for the W-resident kernel: bit 0 skips the
 // epilogue, bit 1 the spike-operand loads (probe = 0 is the production kernel).
 int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
-                         int n_pad32, int Kpad, int P, double* out, int sm_count, int binary,
-                         int probe, cudaStream_t stream) {
+                         int n_pad32, int k, int Kpad, int P, double* out, int sm_count,
+                         int binary, int probe, cudaStream_t stream) {
   const bool bin = binary != 0 && P <= 7 && Kpad <= 8192;
   SPB_CHECK_ARG(xq && wq && sexp && out && M > 0 && n > 0 && n_pad32 >= n &&
                     n_pad32 % proj::NT == 0 && Kpad % proj::BK == 0 && (P == 6 || P == 7 || P == 8),
                 "spb_input_proj: bad args");
   SPB_CHECK_ARG((reinterpret_cast<uintptr_t>(xq) | reinterpret_cast<uintptr_t>(wq)) % 16 == 0,
                 "spb_input_proj: operands must be 16-byte aligned");
-  CUtensorMap mx, mw;
+  SPB_CHECK_ARG(k > 0 && k <= Kpad, "spb_input_proj: need 0 < k <= Kpad");
+  CUtensorMap mx, mw, mxt;
   const bool ok =
       make_tmap_2d(&mx, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, Kpad, M, Kpad, proj::BK, proj::BM,
                    CU_TENSOR_MAP_SWIZZLE_128B) &&
@@ -855,22 +910,35 @@ int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, i
   const int tiles = ceil_div(M, proj::BM) * ceil_div(n, proj::NT);
   const int grid = max(1, min(tiles, sm_count > 0 ? sm_count : 148));
   const int nkb = Kpad / proj::BK;
+  // W-resident kernel: the inputs past the last full 128-byte K block, if they fit in 64
+  // bytes, run as a 64-byte tail block (SWIZZLE_64B) instead of a zero-padded full block
+  const int rem = k % proj::BK;
+  const int tail = (rem > 0 && rem <= proj::BK / 2 && k2_tail()) ? 1 : 0;
+  const int nkb_res = tail ? k / proj::BK : nkb;
+  if (!make_tmap_2d(&mxt, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, Kpad, M, Kpad, proj::BK / 2,
+                    proj::BM, CU_TENSOR_MAP_SWIZZLE_64B)) {
+    set_error("spb_input_proj: cuTensorMapEncodeTiled (tail) failed");
+    return 3;
+  }
   if (nkb <= proj::ResCfg<7, 3>::MAXKB) {  // weights of a neuron tile fit in shared memory
     if (P == 6) {
       auto kfn = bin ? proj::input_proj_wres_kernel<6, 5, true> : proj::input_proj_wres_kernel<6, 5, false>;
       constexpr int sm = proj::ResCfg<6, 5>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
+      pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, mxt, sexp, out, M, n, n_pad32,
+                 nkb_res, tail, probe);
     } else if (P == 7) {
       auto kfn = bin ? proj::input_proj_wres_kernel<7, 3, true> : proj::input_proj_wres_kernel<7, 3, false>;
       constexpr int sm = proj::ResCfg<7, 3>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
+      pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, mxt, sexp, out, M, n, n_pad32,
+                 nkb_res, tail, probe);
     } else {
       auto kfn = proj::input_proj_wres_kernel<8, 2, false>;
       constexpr int sm = proj::ResCfg<8, 2>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, sexp, out, M, n, n_pad32, nkb, probe);
+      pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, mxt, sexp, out, M, n, n_pad32,
+                 nkb_res, tail, probe);
     }
   } else if (P == 6) {
     auto kfn = bin ? proj::input_proj_kernel<6, true> : proj::input_proj_kernel<6, false>;

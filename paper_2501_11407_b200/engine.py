@@ -342,7 +342,7 @@ class EpropEngine:
         v = ctypes_void
         args = ("spb_input_proj", v(self.xq.data_ptr()),
                 v(self.wq.data_ptr()), v(self.sexp.data_ptr()), self.B * self.KR, self.n,
-                self.n_pad32, self.Kpad, self.P, v(self.cur.data_ptr()), self.sm_count,
+                self.n_pad32, self.k, self.Kpad, self.P, v(self.cur.data_ptr()), self.sm_count,
                 int(bool(binary)), st)
         if timed is not None:
             timed("proj", ln, *args)

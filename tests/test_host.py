@@ -71,7 +71,7 @@ def test_bad_arguments_are_rejected_without_gpu():
                   0.95, 1.0, 10.0, 0.0, 0.0, 0.95, 0, 0, 0, None, None, None, None, None, None, None, None,
                   None, None, None, None, None, 8, None, None, None)
     with pytest.raises(P.ShapeMismatch):
-        _lib.call("spb_input_proj", None, None, None, 1, 1, 32, 100, 7, None, 148, 0, None)
+        _lib.call("spb_input_proj", None, None, None, 1, 1, 32, 100, 100, 7, None, 148, 0, None)
     with pytest.raises(P.ShapeMismatch):
         _lib.call("spb_alif_carry_chunk", None, None, 8, None, None, None, None, None, 1, 1, 100,
                   1, 4, 128, 64, 1, 0, 0, 0, None, None, None)

@@ -225,6 +225,35 @@ def test_pair_gemm_slices_vs_cuda_core_gemm(blo, M, N, K):
     assert float((got - exact).norm() / exact.norm()) < 1e-4
 
 
+@pytest.mark.parametrize("k", [20, 60, 64, 65, 129, 700, 768])
+def test_projection_tail_block_is_bitwise_the_padded_block(k, monkeypatch):
+    """K2 runs the last <= 64 inputs past a 128-byte K block as a 64-byte SWIZZLE_64B
+    block; integer MMA accumulation is exact, so the fp64 currents equal the zero-padded
+    full-block path bit for bit (k = 20: the tail is the whole K; 768: no tail)."""
+    _need_gpu()
+    import ctypes
+    from paper_2501_11407_b200.engine import EpropEngine
+    rng = np.random.default_rng(k)
+    B, T, n = 3, 40, 96
+    w = (rng.uniform(-1, 1, (n, k)) / np.sqrt(k)).astype(np.float32)
+    x = (rng.random((B, T, k)) < 0.2).astype(np.uint8)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SPB_K2_TAIL", flag)
+        eng = EpropEngine(n, k, 3, B, alif=False, w_f64=False, chunk=63)
+        eng.set_weights(torch.from_numpy(w), torch.zeros((3, n), dtype=torch.float64))
+        xd = torch.from_numpy(x).cuda()
+        st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        eng._pack(xd.data_ptr(), T * k, False, T, st)
+        eng.cur.zero_()
+        eng._project(T, st, binary=True)
+        torch.cuda.synchronize()
+        out[flag] = eng.cur.cpu().numpy().reshape(B, eng.KR, n)[:, :T].copy()
+    assert np.array_equal(out["1"], out["0"])
+    exact = np.einsum("btk,nk->btn", x.astype(np.longdouble), w.astype(np.longdouble))
+    assert np.max(np.abs(out["1"] - exact.astype(np.float64))) <= 2.3e-16 * np.max(np.abs(exact))
+
+
 def test_label_out_of_range_raises():
     _need_gpu()
     import paper_2501_11407_b200 as P

@@ -24,27 +24,12 @@ for binary, probe in ((0, 0), (1, 0), (0, 1), (0, 2), (0, 3), (0, 4), (1, 4)):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         _lib.call("spb_input_proj_probe", v(eng.xq.data_ptr()), v(eng.wq.data_ptr()),
-                  v(eng.sexp.data_ptr()), B * eng.Tc, n, eng.n_pad32, eng.Kpad, eng.P,
+                  v(eng.sexp.data_ptr()), B * eng.KR, n, eng.n_pad32, k, eng.Kpad, eng.P,
                   v(eng.cur.data_ptr()), eng.sm_count, binary, probe, st)
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    ops = 2.0 * eng.P * B * eng.Tc * n * eng.Kpad
+    ops = 2.0 * eng.P * B * eng.KR * n * k
     ms = float(np.median(ts[2:]))
     print(f"binary={binary} probe={probe} (bit0: no epilogue, bit1: no x loads, bit2: no stores): {ms:.4f} ms, "
           f"{ops / ms / 1e9:.0f} TOPS issued", flush=True)
-
-# CTA-pair kernel (proj2.cu) on the same operands
-for binary in (0, 1):
-    ts = []
-    for rep in range(8):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        _lib.call("spb_input_proj_pair", v(eng.xq.data_ptr()), v(eng.wq.data_ptr()),
-                  v(eng.sexp.data_ptr()), B * eng.Tc, n, eng.n_pad32, eng.Kpad, eng.P,
-                  v(eng.cur.data_ptr()), eng.sm_count, binary, st)
-        e1.record()
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    ms = float(np.median(ts[2:]))
-    print(f"pair binary={binary}: {ms:.4f} ms, {2.0 * eng.P * B * eng.Tc * n * eng.Kpad / ms / 1e9:.0f} TOPS issued", flush=True)
