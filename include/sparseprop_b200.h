@@ -226,6 +226,13 @@ int spb_reduce_partials(const float* partial, int splits, int n, int n_pad, int 
 int spb_copy_chunk_h2d(void* dst, long long dst_pitch, const void* src, long long src_pitch,
                        long long row_bytes, int rows, cudaStream_t stream);
 
+/* HOST helper of the drop-in's staging (host.cu; x and out are HOST pointers, no stream):
+ * uint8 counts x [rows][k] -> out [rows][ceil(k/8)] bit-packed like
+ * np.packbits(x, axis=-1, bitorder="little").  Returns 0 when every count is 0 or 1, 1
+ * when some count is > 1 (out then partial; the caller stages the bytes instead), 2 on
+ * bad arguments.  Thread-safe on disjoint row ranges. */
+int spb_host_pack_bits(const uint8_t* x, long long rows, int k, uint8_t* out);
+
 /* out[r][c] = acc[r*ld + c] cast to fp32 (out_is_f64=0) or fp64. */
 int spb_finalize_grad(const double* acc, int rows, int cols, int ld, void* out, int out_is_f64,
                       cudaStream_t stream);

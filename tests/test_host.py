@@ -292,3 +292,21 @@ def test_train_and_evaluate_reject_bad_labels_before_any_kernel():
         train(spec, ds)
     with pytest.raises(P.LabelOutOfRange):
         evaluate(P.init_network(spec), ds)
+
+
+@pytest.mark.parametrize("k", [1, 7, 8, 16, 700, 701])
+def test_host_pack_bits_matches_numpy_packbits(k):
+    """The drop-in's native packer (host code, no GPU) = np.packbits(bitorder='little'),
+    and it reports counts > 1 anywhere in a row (full words and the tail bytes)."""
+    rng = np.random.default_rng(k)
+    x = (rng.random((5, 9, k)) < 0.3).astype(np.uint8)
+    kb = (k + 7) // 8
+    out = np.zeros((5, 9, kb), np.uint8)
+    lib = _lib.load()
+    assert lib.spb_host_pack_bits(x.ctypes.data, 45, k, out.ctypes.data) == 0
+    np.testing.assert_array_equal(out, np.packbits(x, axis=-1, bitorder="little"))
+    for j in {0, k // 2, k - 1}:
+        y = x.copy()
+        y[3, 4, j] = 2
+        assert lib.spb_host_pack_bits(y.ctypes.data, 45, k, out.ctypes.data) == 1
+    assert lib.spb_host_pack_bits(x.ctypes.data, 45, 0, out.ctypes.data) == 2

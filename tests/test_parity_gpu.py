@@ -441,3 +441,36 @@ def test_one_chunk_streamed_inputs_match_resident(bits):
         torch.cuda.synchronize()
         outs.append((eng.grad_w_acc.cpu().numpy().copy(), eng.loss.cpu().numpy().copy()))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_dropin_binary_counts_travel_bit_packed():
+    """uint8 0/1 counts through the drop-in are bit-packed on the host (spb_host_pack_bits)
+    and give bitwise the update of packed=True input and of the byte-staged path; a count
+    > 1 falls back to byte staging."""
+    _need_gpu()
+    import paper_2501_11407_b200 as P
+    from paper_2501_11407_b200.datasets import poisson_batch
+    from paper_2501_11407_b200.gradients import _staging, get_engine
+    net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=160, n_inputs=700, n_classes=5,
+                                       precision="f32", seed=4))
+    B, T = 64, 120   # 5.4 MB of counts: the threaded, sliced packing path
+    x, y = poisson_batch(B, 700, T, 5, seed=11)
+    r_counts = P.eprop_batch_gradient(net, x, y)
+    st = _staging(get_engine(net, B, T=T))
+    assert not st.counts_nonbinary and len(st.bufs) == 1 and \
+        next(iter(st.bufs))[2] == 88                       # staged bit-packed
+    r_packed = P.eprop_batch_gradient(net, np.packbits(x, axis=-1, bitorder="little"), y,
+                                      packed=True)
+    st.counts_nonbinary = True                               # force the byte staging
+    r_bytes = P.eprop_batch_gradient(net, x, y)
+    for r in (r_packed, r_bytes):
+        assert np.array_equal(r.grads["w"], r_counts.grads["w"])
+        assert np.array_equal(r.grads["w_out"], r_counts.grads["w_out"])
+        assert np.array_equal(r.loss, r_counts.loss)
+    st.counts_nonbinary = False
+    x2 = x.copy()
+    x2[B - 1, T - 1, 699] = 2
+    r2 = P.eprop_batch_gradient(net, x2, y)
+    assert st.counts_nonbinary
+    ref = O.eprop_two_pass_batch(net.neuron.w, net.readout.w_out, O.Params(alif=True), x2, y)
+    assert _rel(r2.grads["w"], ref.grad_w) <= REL_TOL
