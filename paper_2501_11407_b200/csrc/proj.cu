@@ -22,6 +22,8 @@
 //   spb_input_proj       persistent warp-specialised tcgen05 GEMM -> I [B*Tc][n] fp64
 #include "tma.cuh"
 #include "digits.cuh"
+#include <algorithm>
+#include <cstdlib>
 
 namespace spb {
 namespace proj {
@@ -309,6 +311,37 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se
   }
 }
 
+// The tile sequence of one persistent CTA of the W-resident kernel.  The m-tiles (rows =
+// (sample, step)) are cut into `bands` consecutive bands; inside a band the tiles run
+// neuron-major and every CTA takes the same fraction of them, so all CTAs work in the same
+// band at the same time and the band's spike tiles are read from DRAM once and then hit
+// L2 for the other neuron tiles (bands = 1: one band over all rows -- each spike tile is
+// then re-read from DRAM by the neuron tiles at different times).  Odd bands are walked
+// backwards, so a CTA enters the next band on the neuron tile it just finished (one
+// weight reload per band instead of two).
+struct TileWalk {
+  int m_tiles, n_tiles, bands, cta, ncta;
+  int g = -1, k = 0, kb = 0, ke = 0, bw = 1, mb0 = 0;
+  __device__ TileWalk(int m_tiles_, int n_tiles_, int bands_, int cta_, int ncta_)
+      : m_tiles(m_tiles_), n_tiles(n_tiles_), bands(bands_), cta(cta_), ncta(ncta_) {}
+  __device__ bool next(int& nt, int& mt) {
+    while (k >= ke) {
+      if (++g >= bands) return false;
+      mb0 = (int)((long long)m_tiles * g / bands);
+      bw = (int)((long long)m_tiles * (g + 1) / bands) - mb0;
+      const long long tot = (long long)bw * n_tiles;
+      kb = (int)(tot * cta / ncta);
+      ke = (int)(tot * (cta + 1) / ncta);
+      k = kb;
+    }
+    const int u = (g & 1) ? ke - 1 - (k - kb) : k;
+    ++k;
+    nt = u / bw;
+    mt = mb0 + u - nt * bw;
+    return true;
+  }
+};
+
 // W-resident variant (Kpad <= 768): each persistent CTA walks a contiguous range of tiles
 // in neuron-major order, keeps the sliced weights of its current neuron tile (all K) in
 // shared memory and streams only the spike tiles -- operand traffic drops from
@@ -328,7 +361,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                            const __grid_constant__ CUtensorMap tm_w,
                            const __grid_constant__ CUtensorMap tm_xt, const int* __restrict__ sexp,
                            double* __restrict__ out, int M, int n, int n_pad32, int nkb,
-                           int tail, int probe) {
+                           int tail, int probe, int bands) {
   // nkb full 128-byte K blocks, then (tail) one 64-byte block: k = 700 runs 704 bytes of
   // K instead of 768 (8 % fewer MMAs and spike-operand bytes)
   using C = ResCfg<P, XS>;
@@ -349,9 +382,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (M + BM - 1) / BM;
   const int n_tiles = (n + NT - 1) / NT;
-  const long long total = (long long)m_tiles * n_tiles;
-  const int t_begin = (int)(total * blockIdx.x / gridDim.x);
-  const int t_end = (int)(total * (blockIdx.x + 1) / gridDim.x);
+  const int nbands = max(1, min(bands, m_tiles));
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < XS; ++s) {
@@ -382,9 +413,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int it = 0, cur_nt = -1, wl = 0;
-      for (int t = t_begin; t < t_end; ++t) {
-        const int nt = t / m_tiles, mt = t % m_tiles;
+      int it = 0, cur_nt = -1, wl = 0, nt, mt;
+      TileWalk tw(m_tiles, n_tiles, nbands, blockIdx.x, gridDim.x);
+      while (tw.next(nt, mt)) {
         if (nt != cur_nt) {  // (re)load this neuron tile's weight slices, all K blocks
           mbar_wait(smem_u32(wempty), (wl & 1) ^ 1);
           const uint32_t fb = smem_u32(wfull);
@@ -424,9 +455,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 1) {
     {  // the whole warp runs the issue loop (converged); elect.sync picks the issuer
-      int it = 0, lt = 0, cur_nt = -1, wl = 0;
-      for (int t = t_begin; t < t_end; ++t, ++lt) {
-        const int nt = t / m_tiles;
+      int it = 0, lt = 0, cur_nt = -1, wl = 0, nt, mt, nnt, nmt;
+      TileWalk tw(m_tiles, n_tiles, nbands, blockIdx.x, gridDim.x);
+      bool have = tw.next(nt, mt);
+      while (have) {
+        const bool more = tw.next(nnt, nmt);  // one tile ahead: the weight region's last use
         if (nt != cur_nt) {
           mbar_wait(smem_u32(wfull), wl & 1);
           cur_nt = nt;
@@ -443,32 +476,38 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t xa = smem_u32(xsm + s * TILE_A);
           const uint32_t wa = smem_u32(wsm + kb * C::WBLK);
           static_assert(BK / 32 == 4, "four K steps per block");
-          mma_i8_x4(dacc, desc_k_sw128(xa), desc_k_sw128(wa), Cfg<P>::IDESC, kb ? 1u : 0u);
+          if (!(probe & 8))  // profiling probe: no MMAs (the epilogue alone)
+            mma_i8_x4(dacc, desc_k_sw128(xa), desc_k_sw128(wa), Cfg<P>::IDESC, kb ? 1u : 0u);
           commit(smem_u32(&xempty[s]));
         }
         if (tail) {
           const int s = it % XS;
           mbar_wait(smem_u32(&xfull[s]), (it / XS) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          mma_i8_x2(dacc, desc_k_sw64(smem_u32(xsm + s * TILE_A)),
-                    desc_k_sw128(smem_u32(wsm + nkb * C::WBLK)), Cfg<P>::IDESC, nkb ? 1u : 0u);
+          if (!(probe & 8))
+            mma_i8_x2(dacc, desc_k_sw64(smem_u32(xsm + s * TILE_A)),
+                      desc_k_sw128(smem_u32(wsm + nkb * C::WBLK)), Cfg<P>::IDESC, nkb ? 1u : 0u);
           commit(smem_u32(&xempty[s]));
           ++it;
         }
         commit(smem_u32(&tfull[a]));
         // last tile of this neuron tile: the weight region may be refilled afterwards
-        if (t + 1 == t_end || (t + 1) / m_tiles != nt) commit(smem_u32(wempty));
+        if (!more || nnt != nt) commit(smem_u32(wempty));
+        nt = nnt;
+        mt = nmt;
+        have = more;
+        ++lt;
       }
     }
   } else {
     const int q = warp & 3;          // TMEM lane quarter
     const int hh = (warp - 2) >> 2;  // neuron half of the tile
     int lt = 0;
-    // tile coordinates advanced incrementally (no per-tile division); the per-neuron
-    // scales 2^(s-F) change only with the neuron tile
-    int nt = t_begin / m_tiles, mt = t_begin % m_tiles, sc_nt = -1;
+    // the per-neuron scales 2^(s-F) change only with the neuron tile
+    int nt, mt, sc_nt = -1;
     double sc[NH];
-    for (int t = t_begin; t < t_end; ++t, ++lt) {
+    TileWalk tw(m_tiles, n_tiles, nbands, blockIdx.x, gridDim.x);
+    for (; tw.next(nt, mt); ++lt) {
       const int a = lt & 1;
       const int i0 = nt * NT + hh * NH;
       if (nt != sc_nt) {
@@ -483,13 +522,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&tempty[a]));
-        if (++mt == m_tiles) { mt = 0; ++nt; }
         continue;
       }
       proj_epilogue_tile<P, BIN>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH),
                             sc, out, M, n, mt * BM + q * 32 + lane, i0, smem_u32(&tempty[a]),
                             lane, probe);
-      if (++mt == m_tiles) { mt = 0; ++nt; }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -879,14 +916,26 @@ int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, 
                               stream);
 }
 
+// Row bands of the W-resident kernel's tile walk (TileWalk): about 30 tiles per CTA per
+// band (measured, tools/k2_bands.py: C3 4 bands 0.246 -> 0.227 ms with DRAM reads 383 ->
+// 70 MB; C4 0.473 -> 0.422; C5 Tc = 2047 1.84 -> 1.71; C2 stays at one band).
+// SPB_K2_BANDS=g overrides (A/B).
+static int k2_bands(long long tiles, int grid) {
+  const char* e = getenv("SPB_K2_BANDS");
+  if (e) return max(1, atoi(e));
+  return (int)max(1LL, (tiles + 15LL * grid) / (30LL * grid));
+}
 // SPB_K2_TAIL=0: the zero-padded last K block instead of the 64-byte tail (A/B, tests)
 static bool k2_tail() {
   const char* e = getenv("SPB_K2_TAIL");
   return !(e && e[0] == '0');
 }
 
+
+
 // spb_input_proj with a profiling probe for the W-resident kernel: bit 0 skips the
-// epilogue, bit 1 the spike-operand loads (probe = 0 is the production kernel).
+// epilogue, bit 1 the spike-operand loads, bit 2 the current stores, bit 3 the MMAs
+// (probe = 0 is the production kernel).
 int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
                          int n_pad32, int k, int Kpad, int P, double* out, int sm_count,
                          int binary, int probe, cudaStream_t stream) {
@@ -926,19 +975,19 @@ int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, i
       constexpr int sm = proj::ResCfg<6, 5>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, mxt, sexp, out, M, n, n_pad32,
-                 nkb_res, tail, probe);
+                 nkb_res, tail, probe, k2_bands(tiles, grid));
     } else if (P == 7) {
       auto kfn = bin ? proj::input_proj_wres_kernel<7, 3, true> : proj::input_proj_wres_kernel<7, 3, false>;
       constexpr int sm = proj::ResCfg<7, 3>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, mxt, sexp, out, M, n, n_pad32,
-                 nkb_res, tail, probe);
+                 nkb_res, tail, probe, k2_bands(tiles, grid));
     } else {
       auto kfn = proj::input_proj_wres_kernel<8, 2, false>;
       constexpr int sm = proj::ResCfg<8, 2>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, mxt, sexp, out, M, n, n_pad32,
-                 nkb_res, tail, probe);
+                 nkb_res, tail, probe, k2_bands(tiles, grid));
     }
   } else if (P == 6) {
     auto kfn = bin ? proj::input_proj_kernel<6, true> : proj::input_proj_kernel<6, false>;

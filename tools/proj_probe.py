@@ -18,7 +18,7 @@ eng.run(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
 torch.cuda.synchronize()
 v = ctypes.c_void_p
 st = v(torch.cuda.current_stream().cuda_stream)
-for binary, probe in ((0, 0), (1, 0), (0, 1), (0, 2), (0, 3), (0, 4), (1, 4)):
+for binary, probe in ((1, 0), (1, 1), (1, 2), (1, 3), (1, 4), (1, 8), (1, 10), (1, 12), (1, 14)):
     ts = []
     for rep in range(8):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -31,5 +31,5 @@ for binary, probe in ((0, 0), (1, 0), (0, 1), (0, 2), (0, 3), (0, 4), (1, 4)):
         ts.append(e0.elapsed_time(e1))
     ops = 2.0 * eng.P * B * eng.KR * n * k
     ms = float(np.median(ts[2:]))
-    print(f"binary={binary} probe={probe} (bit0: no epilogue, bit1: no x loads, bit2: no stores): {ms:.4f} ms, "
+    print(f"binary={binary} probe={probe} (bit0: no epilogue, bit1: no x loads, bit2: no stores, bit3: no MMAs): {ms:.4f} ms, "
           f"{ops / ms / 1e9:.0f} TOPS issued", flush=True)
