@@ -12,7 +12,8 @@ import os
 from .errors import KernelError, ShapeMismatch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsparseprop_b200.so")
+# SPB_LIB: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("SPB_LIB") or os.path.join(_HERE, "libsparseprop_b200.so")
 
 P = ctypes.c_void_p
 I = ctypes.c_int

@@ -12,10 +12,26 @@
 // g0 = digits 0-2 and g1 = digits 3..P-1 (both exact in int64 and in double) with ONE
 // rounding:  I = fma(g0, 2^(s-F+RB*(P-3)), g1 * 2^(s-F)).  With binary spikes all digits
 // fit one int64 g = g0 * 2^(RB*(P-3)) + g1 and I = (double)g * 2^(s-F) (same bits).
+//
+// Row order of the sliced weights wq [P][n_pad32][Kpad]: inside every group of 16 neurons
+// the rows are permuted, storage slot c holding neuron perm16(c).  K2's MMA puts slot c of
+// a tile in TMEM column c, and a tcgen05.ld.16x256b gives thread q (of a lane quad) the
+// columns 2q, 2q+1, 8+2q, 9+2q -- under this order the four consecutive neurons 4q..4q+3,
+// so each thread stores 32 contiguous bytes of a current row without any lane shuffles.
 #pragma once
 #include "common.cuh"
 
 namespace spb {
+
+__host__ __device__ constexpr int perm16(int c) {  // storage slot -> neuron (mod 16)
+  return ((c & 7) >> 1) * 4 + (c >> 3) * 2 + (c & 1);
+}
+__host__ __device__ constexpr int pinv16(int j) {  // neuron -> storage slot (mod 16)
+  return ((j & 3) >> 1) * 8 + (j >> 2) * 2 + (j & 1);
+}
+__host__ __device__ constexpr int wq_slot(int i) { return (i & ~15) | pinv16(i & 15); }
+static_assert(perm16(pinv16(5)) == 5 && perm16(pinv16(14)) == 14 && pinv16(perm16(9)) == 9,
+              "perm16 / pinv16 are inverse");
 
 template <int P>
 struct Digits {

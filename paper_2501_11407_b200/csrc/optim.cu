@@ -18,6 +18,7 @@
 // in fp64 (the readout weights the loss kernel reads).  Elementwise, HBM-bound: one
 // thread per parameter, grid-stride.
 #include "common.cuh"
+#include "digits.cuh"
 
 namespace spb {
 
@@ -181,7 +182,8 @@ __global__ void __launch_bounds__(SS_THREADS) sgd_slice_kernel(T* __restrict__ w
       for (int p = 0; p < P; ++p) word[p] |= (uint32_t)(uint8_t)q[p] << (8 * e);
     }
     for (int p = 0; p < P; ++p)
-      *reinterpret_cast<uint32_t*>(wq + ((long long)p * n_pad32 + i) * Kpad + j0) = word[p];
+      *reinterpret_cast<uint32_t*>(wq + ((long long)p * n_pad32 + wq_slot(i)) * Kpad + j0) =
+          word[p];
   }
 }
 

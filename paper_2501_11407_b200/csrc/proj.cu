@@ -164,35 +164,6 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se
                                                    int i0, uint32_t tempty_bar, int lane,
                                                    int probe = 0) {
   long long g0[NH], g1[NH];
-  if constexpr (P == 6 && BIN && sizeof(SE) == sizeof(double)) {
-    // binary spikes, k <= 768: every digit sum |S_p| <= 768*128 < 2^17, so digit PAIRS
-    // combine in int32 (|S_a 256 + S_b| < 2^26) and g = P01 2^32 + P23 2^16 + P45 needs
-    // only two 64-bit adds -- the same integer as (g0 << 24) + g1, half the instructions
-    int32_t p01[NH], r2v[NH];
-    {
-      int32_t r[3][NH];
-#pragma unroll
-      for (int p = 0; p < 3; ++p) tmem_ld16_nowait(tbase + p * NT, r[p]);
-      tmem_wait_ld();
-#pragma unroll
-      for (int c = 0; c < NH; ++c) {
-        p01[c] = r[0][c] * 256 + r[1][c];
-        r2v[c] = r[2][c];
-      }
-    }
-    {
-      int32_t r[3][NH];
-#pragma unroll
-      for (int p = 3; p < 6; ++p) tmem_ld16_nowait(tbase + p * NT, r[p - 3]);
-      tmem_wait_ld();
-#pragma unroll
-      for (int c = 0; c < NH; ++c) {
-        const int32_t p23 = r2v[c] * 256 + r[0][c], p45 = r[1][c] * 256 + r[2][c];
-        g0[c] = ((long long)p01[c] << 32) + ((long long)p23 << 16) + (long long)p45;
-        g1[c] = 0;
-      }
-    }
-  } else {
   {
     int32_t r[3][NH];
 #pragma unroll
@@ -214,24 +185,23 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se
       g1[c] = v;
     }
   }
-  }
   // the TMEM buffer is free once every epilogue warp has pulled its lanes
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncwarp();
   if (lane == 0) mbar_arrive(tempty_bar);
-  // values of this thread's row: 16 doubles = 8 double2 chunks
+  // values of this thread's row in NEURON order: 16 doubles = 8 double2 chunks (TMEM
+  // column c holds neuron perm16(c) of the 16-neuron group, digits.cuh)
   double2 ch[NH / 2];
 #pragma unroll
   for (int c = 0; c < NH; c += 2) {
     double v[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      if constexpr (P == 6 && BIN && sizeof(SE) == sizeof(double))
-        v[h] = (double)g0[c + h] * se[c + h];   // g0 holds the whole integer g
-      else if constexpr (sizeof(SE) == sizeof(double))
-        v[h] = digits_current_scaled<P, BIN>(g0[c + h], g1[c + h], se[c + h]);
+      const int sl = pinv16(c + h);
+      if constexpr (sizeof(SE) == sizeof(double))
+        v[h] = digits_current_scaled<P, BIN>(g0[sl], g1[sl], se[c + h]);
       else
-        v[h] = digits_current<P, BIN>(g0[c + h], g1[c + h], se[c + h]);
+        v[h] = digits_current<P, BIN>(g0[sl], g1[sl], se[c + h]);
     }
     ch[c / 2] = make_double2(v[0], v[1]);
   }
@@ -309,6 +279,84 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se
       }
     }
   }
+}
+
+// tcgen05.ld.16x256b.x2: 16 TMEM lanes x 16 columns per warp.  Thread t holds lanes
+// t/4 (registers 0, 1, 4, 5) and t/4 + 8 (2, 3, 6, 7), columns 2(t%4), 2(t%4)+1 (0-3) and
+// 8 + 2(t%4), 9 + 2(t%4) (4-7) -- measured, tools/tmem_layout_probe.cu.
+__device__ __forceinline__ void tmem_ld16x256b_x2_nowait(uint32_t taddr, int32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+
+// Epilogue of one 32-row x 16-neuron quarter-tile, P = 6 digits, binary spikes, k <= 768
+// (every digit sum |S_p| <= 768 * 128 < 2^17, so digit PAIRS combine in int32 and
+// g = P01 2^32 + P23 2^16 + P45 is the exact integer sum of all six).  The digits are
+// read in the 16x256b shape: with the slot order of the sliced weights (digits.cuh) each
+// thread gets 4 rows x the 4 consecutive neurons 4q..4q+3 (q = lane % 4), so a row's
+// 4 currents go out as one 32-byte store and a warp's store instruction covers 8 rows x
+// 128 contiguous bytes -- no lane transposes.  sc4 = 2^(s-F) of those 4 neurons.
+__device__ __forceinline__ void proj_epilogue_p6bin(uint32_t tbase, const double (&sc4)[4],
+                                                    double* __restrict__ out, int M, int n,
+                                                    int row0, int i0, uint32_t tempty_bar,
+                                                    int lane, int probe) {
+  const int t4 = lane >> 2, q4 = lane & 3;
+  double v[2][2][4];  // [lane half][row +0 / +8][neuron 4 q4 + j]
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int32_t r[6][8];
+    if (probe & 16) {  // profiling probe: no TMEM loads
+#pragma unroll
+      for (int p = 0; p < 6; ++p)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) r[p][e] = lane * (p + 1) + e;
+    } else {
+#pragma unroll
+      for (int p = 0; p < 6; ++p)
+        tmem_ld16x256b_x2_nowait(tbase + ((uint32_t)(16 * h) << 16) + (uint32_t)(p * NT), r[p]);
+      tmem_wait_ld();
+    }
+    if (h == 1) {  // the TMEM buffer is free once every epilogue warp has pulled its lanes
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int32_t p01 = r[0][e] * 256 + r[1][e];
+      const int32_t p23 = r[2][e] * 256 + r[3][e];
+      const int32_t p45 = r[4][e] * 256 + r[5][e];
+      const long long g = ((long long)p01 << 32) + ((long long)p23 << 16) + (long long)p45;
+      const int j = (e & 1) + 2 * (e >> 2);   // register e -> neuron 4 q4 + j
+      v[h][(e >> 1) & 1][j] = (double)g * sc4[j];
+    }
+  }
+  const int col = i0 + 4 * q4;
+  if (probe & 4) {  // profiling probe: no global stores
+    if (v[0][0][0] == 1.2345e-300 && row0 < M) out[(long long)row0 * n + col] = v[0][0][1];
+    return;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int rh = 0; rh < 2; ++rh) {
+      const int r = row0 + 16 * h + 8 * rh + t4;
+      if (r >= M) continue;
+      double* o = out + (long long)r * n + col;
+      const double* w = v[h][rh];
+      if ((n & 3) == 0) {  // 32-byte aligned quads, all in or all out
+        if (col < n)
+          asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o), "d"(w[0]),
+                       "d"(w[1]), "d"(w[2]), "d"(w[3])
+                       : "memory");
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (col + j < n) o[j] = w[j];
+      }
+    }
 }
 
 // The tile sequence of one persistent CTA of the W-resident kernel.  The m-tiles (rows =
@@ -413,7 +461,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int it = 0, cur_nt = -1, wl = 0, nt, mt;
+      int s = 0, ph = 0, cur_nt = -1, wl = 0, nt, mt;
       TileWalk tw(m_tiles, n_tiles, nbands, blockIdx.x, gridDim.x);
       while (tw.next(nt, mt)) {
         if (nt != cur_nt) {  // (re)load this neuron tile's weight slices, all K blocks
@@ -428,34 +476,33 @@ __global__ void __launch_bounds__(THREADS, 1)
           cur_nt = nt;
           ++wl;
         }
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % XS;
-          mbar_wait(smem_u32(&xempty[s]), ((it / XS) & 1) ^ 1);
+        for (int kb = 0; kb < nkb + tail; ++kb) {  // stage s, ring phase ph (incremental)
+          mbar_wait(smem_u32(&xempty[s]), ph ^ 1);
           const uint32_t fb = smem_u32(&xfull[s]);
           if (probe & 2) {  // profiling probe: no spike-operand traffic
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
-            continue;
-          }
-          mbar_expect_tx(fb, TILE_A);
-          tma_load_2d(smem_u32(xsm + s * TILE_A), &tm_x, fb, kb * BK, mt * BM);
-        }
-        if (tail) {  // the 64-byte tail block (SWIZZLE_64B box) into the next stage
-          const int s = it % XS;
-          mbar_wait(smem_u32(&xempty[s]), ((it / XS) & 1) ^ 1);
-          const uint32_t fb = smem_u32(&xfull[s]);
-          if (probe & 2) {
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
-          } else {
+          } else if (kb < nkb) {
+            mbar_expect_tx(fb, TILE_A);
+            tma_load_2d(smem_u32(xsm + s * TILE_A), &tm_x, fb, kb * BK, mt * BM);
+          } else {  // the 64-byte tail block (SWIZZLE_64B box)
             mbar_expect_tx(fb, TILE_A / 2);
             tma_load_2d(smem_u32(xsm + s * TILE_A), &tm_xt, fb, nkb * BK, mt * BM);
           }
-          ++it;
+          if (++s == XS) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
     }
   } else if (warp == 1) {
     {  // the whole warp runs the issue loop (converged); elect.sync picks the issuer
-      int it = 0, lt = 0, cur_nt = -1, wl = 0, nt, mt, nnt, nmt;
+      long long c0 = 0, g0 = 0;  // probe & 32: clock / global-timer record of the issue loop
+      if (probe & 32) {
+        c0 = clock64();
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+      }
+      int s = 0, ph = 0, lt = 0, cur_nt = -1, wl = 0, nt, mt, nnt, nmt;
       TileWalk tw(m_tiles, n_tiles, nbands, blockIdx.x, gridDim.x);
       bool have = tw.next(nt, mt);
       while (have) {
@@ -469,9 +516,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(smem_u32(&tempty[a]), ((lt >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dacc = tmem_base + (uint32_t)(a * 256);
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % XS;
-          mbar_wait(smem_u32(&xfull[s]), (it / XS) & 1);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(smem_u32(&xfull[s]), ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t xa = smem_u32(xsm + s * TILE_A);
           const uint32_t wa = smem_u32(wsm + kb * C::WBLK);
@@ -479,16 +525,22 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (!(probe & 8))  // profiling probe: no MMAs (the epilogue alone)
             mma_i8_x4(dacc, desc_k_sw128(xa), desc_k_sw128(wa), Cfg<P>::IDESC, kb ? 1u : 0u);
           commit(smem_u32(&xempty[s]));
+          if (++s == XS) {
+            s = 0;
+            ph ^= 1;
+          }
         }
-        if (tail) {
-          const int s = it % XS;
-          mbar_wait(smem_u32(&xfull[s]), (it / XS) & 1);
+        if (tail) {  // the 64-byte tail block: A in SWIZZLE_64B
+          mbar_wait(smem_u32(&xfull[s]), ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           if (!(probe & 8))
             mma_i8_x2(dacc, desc_k_sw64(smem_u32(xsm + s * TILE_A)),
                       desc_k_sw128(smem_u32(wsm + nkb * C::WBLK)), Cfg<P>::IDESC, nkb ? 1u : 0u);
           commit(smem_u32(&xempty[s]));
-          ++it;
+          if (++s == XS) {
+            s = 0;
+            ph ^= 1;
+          }
         }
         commit(smem_u32(&tfull[a]));
         // last tile of this neuron tile: the weight region may be refilled afterwards
@@ -498,22 +550,38 @@ __global__ void __launch_bounds__(THREADS, 1)
         have = more;
         ++lt;
       }
+      if (probe & 32) {  // wait for the last tile's MMAs, then record (cycles, ns, tiles)
+        mbar_wait(smem_u32(&tfull[(lt - 1) & 1]), ((lt - 1) >> 1) & 1);
+        long long g1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+        if (lane == 0) {
+          out[3 * blockIdx.x] = (double)(clock64() - c0);
+          out[3 * blockIdx.x + 1] = (double)(g1 - g0);
+          out[3 * blockIdx.x + 2] = (double)lt;
+        }
+      }
     }
   } else {
     const int q = warp & 3;          // TMEM lane quarter
     const int hh = (warp - 2) >> 2;  // neuron half of the tile
     int lt = 0;
     // the per-neuron scales 2^(s-F) change only with the neuron tile
+    // P = 6 with binary spikes: the shuffle-free 16x256b epilogue (4 neurons per thread)
+    constexpr bool FAST = (P == 6 && BIN);
+    constexpr int NS = FAST ? 4 : NH;
+    const int ns0 = FAST ? 4 * (lane & 3) : 0;
     int nt, mt, sc_nt = -1;
-    double sc[NH];
+    double sc[NS];
     TileWalk tw(m_tiles, n_tiles, nbands, blockIdx.x, gridDim.x);
     for (; tw.next(nt, mt); ++lt) {
       const int a = lt & 1;
       const int i0 = nt * NT + hh * NH;
       if (nt != sc_nt) {
 #pragma unroll
-        for (int c = 0; c < NH; ++c)
-          sc[c] = digits_pow2(((i0 + c < n) ? __ldg(sexp + i0 + c) : 0) - Digits<P>::F);
+        for (int c = 0; c < NS; ++c) {
+          const int i = i0 + ns0 + c;
+          sc[c] = digits_pow2(((i < n) ? __ldg(sexp + i) : 0) - Digits<P>::F);
+        }
         sc_nt = nt;
       }
       mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
@@ -524,9 +592,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) mbar_arrive(smem_u32(&tempty[a]));
         continue;
       }
-      proj_epilogue_tile<P, BIN>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH),
-                            sc, out, M, n, mt * BM + q * 32 + lane, i0, smem_u32(&tempty[a]),
-                            lane, probe);
+      const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH);
+      if constexpr (FAST)
+        proj_epilogue_p6bin(tb, sc, out, M, n, mt * BM + q * 32, i0, smem_u32(&tempty[a]), lane,
+                            probe);
+      else
+        proj_epilogue_tile<P, BIN>(tb, sc, out, M, n, mt * BM + q * 32 + lane, i0,
+                                   smem_u32(&tempty[a]), lane, probe);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -42,7 +42,11 @@ def test_sgd_slice_matches_two_launches(w_f64, g_f64, n, k):
     assert torch.equal(eng_a.wq, eng_b.wq)
     # and the digits reconstruct the updated weights (digits.cuh format)
     P = eng_a.P
-    wq = eng_a.wq.cpu().numpy().astype(np.float64)[:, :n, :k]
+    # rows are stored in slot order within groups of 16 neurons (digits.cuh wq_slot)
+    i = np.arange(n)
+    j = i & 15
+    slot = (i & ~15) | (((j & 3) >> 1) * 8 + (j >> 2) * 2 + (j & 1))
+    wq = eng_a.wq.cpu().numpy().astype(np.float64)[:, slot, :k]
     s = eng_a.sexp.cpu().numpy()[:n].astype(np.float64)
     if P == 6:
         rec = sum(wq[p] * 2.0 ** (8 * (5 - p)) for p in range(6)) * (2.0 ** (s - 46))[:, None]

@@ -1,3 +1,2 @@
-python -m pytest tests/test_parity_gpu.py tests/test_headline_gpu.py -q -x -p no:cacheprovider 2>&1 | tail -2
-for c in c3 c4 c5; do python bench.py --config $c --no-cpu > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; python tools/bench_summary.py gpurun_out/bench_$c.json | head -3; done
-SPB_K2_BANDS=1 python bench.py --no-cpu > gpurun_out/bench_c3_b1.json 2>/dev/null; python tools/bench_summary.py gpurun_out/bench_c3_b1.json | head -2
+for r in 1 2 3; do for L in oldloop new; do echo -n "$L: "; SPB_LIB=ab/lib_$L.so python tools/k2_bands.py 4 12 2>&1 | grep bands; done; done
+for L in oldloop new; do SPB_LIB=ab/lib_$L.so python bench.py --no-cpu > gpurun_out/bench_$L.json 2>/dev/null; echo $L; python tools/bench_summary.py gpurun_out/bench_$L.json 2>/dev/null| head -2; done

@@ -34,20 +34,23 @@ __device__ __forceinline__ void commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 constexpr int XS = 5;
-__global__ void __launch_bounds__(128, 1) bench(int mode, int stages_total, unsigned long long* cyc, int N) {
+__global__ void __launch_bounds__(320, 1) bench(int mode, int stages_total, unsigned long long* cyc, int N, int fill) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t full[XS], empty[XS], done;
+  __shared__ uint64_t full[XS], empty[XS], done, tfull[2], tempty[2];
   __shared__ uint32_t slot;
   const int tid = threadIdx.x;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
-  for (int i = tid; i < 180 * 1024; i += blockDim.x) base[i] = 0;
+  // fill = 1: pseudo-random operand bytes (tensor-core power depends on the data)
+  for (int i = tid; i < 180 * 1024; i += blockDim.x)
+    base[i] = fill ? (uint8_t)((i * 2654435761u) >> 13) : 0;
   if (tid == 0) {
     for (int s = 0; s < XS; ++s) { mbar_init(su32(&full[s]), 1); mbar_init(su32(&empty[s]), 1); }
     mbar_init(su32(&done), 1);
+    for (int a = 0; a < 2; ++a) { mbar_init(su32(&tfull[a]), 1); mbar_init(su32(&tempty[a]), mode == 7 ? 8 : 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid < 32) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -97,6 +100,52 @@ __global__ void __launch_bounds__(128, 1) bench(int mode, int stages_total, unsi
                  "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&done)) : "memory");
     mbar_wait(su32(&done), 0);
     if (tid == 0) cyc[blockIdx.x] = clock64() - t0;
+  } else if (mode >= 6 && tid < 32) {
+    // K2-like: tiles of 5.5 K blocks (22 MMAs), two TMEM accumulators (cols 0 / 256),
+    // tfull commit per tile, the MMA warp waits the epilogue's tempty before reusing one
+    const unsigned long long t0 = clock64();
+    const int tiles = stages_total / 6;
+    int it = 0;
+    for (int t = 0; t < tiles; ++t) {
+      const int a = t & 1;
+      if (t >= 2) mbar_wait(su32(&tempty[a]), ((t >> 1) - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int kb = 0; kb < 6; ++kb, ++it) {
+        const int s = it % XS;
+        mbar_wait(su32(&full[s]), (it / XS) & 1);
+        const uint32_t xa = xa0 + s * 16384;
+        const uint32_t wa = wa0 + kb * (N * 128) % (4 * N * 128);
+        const int nk = kb < 5 ? 4 : 2;
+        for (int kk = 0; kk < nk; ++kk) {
+          asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "elect.sync _|e, 0xffffffff;\n\t"
+                       "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + a * 256),
+                       "l"(desc_k_sw128(xa + kk * 32)), "l"(desc_k_sw128(wa + kk * 32)), "r"(idesc), "r"(kb | kk));
+        }
+        asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&empty[s])) : "memory");
+      }
+      asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                   "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(&tfull[a])) : "memory");
+    }
+    mbar_wait(su32(&tfull[(tiles - 1) & 1]), ((tiles - 1) >> 1) & 1);
+    if (tid == 0) cyc[blockIdx.x] = clock64() - t0;
+  } else if (mode >= 6 && tid >= 64 && (mode == 7 || tid < 96)) {
+    // "epilogue": wait tfull, arrive tempty (mode 6: one warp, mode 7: 8 warps like K2)
+    const int tiles = stages_total / 6;
+    for (int t = 0; t < tiles; ++t) {
+      const int a = t & 1;
+      mbar_wait(su32(&tfull[a]), (t >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if ((tid & 31) == 0) arrive(su32(&tempty[a]));
+      __syncwarp();
+    }
+  } else if (tid == 32 && mode >= 6) {
+    for (int it = 0; it < (stages_total / 6) * 6; ++it) {
+      const int s = it % XS;
+      if (it >= XS) mbar_wait(su32(&empty[s]), ((it / XS) - 1) & 1);
+      arrive(su32(&full[s]));
+    }
   } else if (tid == 32 && mode == 5) {
     for (int it = 0; it < stages_total; ++it) {
       const int s = it % XS;
@@ -131,7 +180,7 @@ __global__ void __launch_bounds__(128, 1) bench(int mode, int stages_total, unsi
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 int main() {
@@ -142,21 +191,21 @@ int main() {
   const int smem = 180 * 1024 + 1024;
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int stages = 4000;
-  for (int N : {128, 192}) for (int mode = 3; mode < 6; ++mode) {
+  for (int fill : {0, 1}) for (int N : {192}) for (int mode = 5; mode < 8; ++mode) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     float ms = 0;
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0);
-      bench<<<sms, 128, smem>>>(mode, stages, d, N);
+      bench<<<sms, 320, smem>>>(mode, stages, d, N, fill);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       cudaEventElapsedTime(&ms, e0, e1);
     }
     unsigned long long c0 = 0;
     cudaMemcpy(&c0, d, 8, cudaMemcpyDeviceToHost);
-    const double ops = 2.0 * 128 * N * 32 * 4.0 * stages * sms;
-    printf("N=%d mode %d: %.1f cyc/MMA, %.0f TOPS  err=%s\n", N, mode, (double)c0 / (4.0 * stages),
+    const double ops = 2.0 * 128 * N * 32 * (mode >= 6 ? 22.0 / 6.0 : 4.0) * stages * sms;
+    printf("fill=%d N=%d mode %d: %.1f cyc/MMA, %.0f TOPS  err=%s\n", fill, N, mode, (double)c0 / ((mode >= 6 ? 22.0 / 6.0 : 4.0) * stages),
            ops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
