@@ -16,6 +16,9 @@ timeout 300 python bench.py --config c5 --no-cpu --steps 5 > $O/bench_c5.json 2>
 timeout 600 python bench.py --config c5 --seq-len 10000 --no-cpu --steps 3 > $O/bench_c5_T10000.json 2>&1
 timeout 300 python bench.py --impl reference --steps 3 > $O/bench_ref.json 2>&1
 timeout 300 python bench.py --recurrent --no-cpu --steps 5 > $O/bench_c3_recurrent.json 2>&1
+timeout 300 python tools/proj_probe.py > $O/proj_probe.txt 2>&1
+timeout 300 python tools/k2_bands.py 1,2,3,4,6,8 8 > $O/k2_bands_c3.txt 2>&1
+timeout 300 python tools/dropin_profile.py > $O/dropin_profile.txt 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $O/launches_c3.csv python bench.py --steps 2 --warmup 3 --profile > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
