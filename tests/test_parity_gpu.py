@@ -254,6 +254,40 @@ def test_projection_tail_block_is_bitwise_the_padded_block(k, monkeypatch):
     assert np.max(np.abs(out["1"] - exact.astype(np.float64))) <= 2.3e-16 * np.max(np.abs(exact))
 
 
+@pytest.mark.parametrize("B,T,n,k,binary", [(40, 250, 1024, 700, True), (7, 300, 200, 90, True),
+                                              (5, 120, 96, 700, False), (64, 250, 2048, 130, True)])
+def test_projection_banded_walk_is_bitwise_the_plain_walk(B, T, n, k, binary, monkeypatch):
+    """K2's banded tile walk (TileWalk: row bands, odd bands reversed, one weight reload per
+    band) visits every (row, neuron) tile exactly once: the currents equal the one-band walk
+    bit for bit for any band count (also more bands than row tiles, which are clamped)."""
+    _need_gpu()
+    import ctypes
+    from paper_2501_11407_b200.engine import EpropEngine
+    rng = np.random.default_rng(n + k)
+    w = (rng.uniform(-1, 1, (n, k)) / np.sqrt(k)).astype(np.float32)
+    x = (rng.random((B, T, k)) < 0.1).astype(np.uint8)
+    if not binary:
+        x[0, :, :5] = 3
+    eng = EpropEngine(n, k, 3, B, alif=False, w_f64=False, chunk=255 if T < 256 else 511)
+    eng.set_weights(torch.from_numpy(w), torch.zeros((3, n), dtype=torch.float64))
+    xd = torch.from_numpy(x).cuda()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    eng._pack(xd.data_ptr(), T * k, False, T, st)
+    out = {}
+    for bands in ("1", "2", "3", "7", "1000", None):
+        if bands is None:
+            monkeypatch.delenv("SPB_K2_BANDS", raising=False)   # the default band count
+        else:
+            monkeypatch.setenv("SPB_K2_BANDS", bands)
+        eng.cur.fill_(float("nan"))
+        eng._project(T, st, binary=binary)
+        torch.cuda.synchronize()
+        out[bands] = eng.cur.cpu().numpy().reshape(B, eng.KR, n)[:, :T].copy()
+    for bands, cur in out.items():
+        assert np.isfinite(cur).all(), bands
+        assert np.array_equal(cur.view(np.int64), out["1"].view(np.int64)), bands
+
+
 def test_label_out_of_range_raises():
     _need_gpu()
     import paper_2501_11407_b200 as P
