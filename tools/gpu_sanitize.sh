@@ -10,3 +10,6 @@ echo "memcheck k5 rc=$?"; grep -E "ERROR SUMMARY|passed|failed|Invalid" gpurun_o
 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 7 --print-limit 20 \
   python -m pytest tests/test_recurrent_gpu.py tests/test_reset_gpu.py -q -x -p no:cacheprovider > gpurun_out/san/memcheck_rec.log 2>&1
 echo "memcheck rec/reset rc=$?"; grep -E "ERROR SUMMARY|passed|failed|Invalid" gpurun_out/san/memcheck_rec.log | head -5
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 7 --print-limit 20 \
+  python -m pytest tests/test_parity_gpu.py -q -x -p no:cacheprovider -k "projection or int8 or binary or pooled" > gpurun_out/san/memcheck_k2.log 2>&1
+echo "memcheck k2 rc=$?"; grep -E "ERROR SUMMARY|passed|failed|Invalid" gpurun_out/san/memcheck_k2.log | head -5
