@@ -18,7 +18,7 @@ eng.run(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
 torch.cuda.synchronize()
 v = ctypes.c_void_p
 st = v(torch.cuda.current_stream().cuda_stream)
-for binary, probe in ((1, 0), (1, 1), (1, 2), (1, 3), (1, 4), (1, 8), (1, 10), (1, 12), (1, 14), (1, 30), (1, 15)):
+for binary, probe in ((1, 0), (1, 1), (1, 2), (1, 3), (1, 4), (1, 8), (1, 10), (1, 12), (1, 14), (1, 15)):
     ts = []
     for rep in range(8):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -31,7 +31,7 @@ for binary, probe in ((1, 0), (1, 1), (1, 2), (1, 3), (1, 4), (1, 8), (1, 10), (
         ts.append(e0.elapsed_time(e1))
     ops = 2.0 * eng.P * B * eng.KR * n * k
     ms = float(np.median(ts[2:]))
-    print(f"binary={binary} probe={probe} (bit0: no epilogue, bit1: no x loads, bit2: no stores, bit3: no MMAs, bit4: no TMEM loads): {ms:.4f} ms, "
+    print(f"binary={binary} probe={probe} (bit0: no epilogue, bit1: no x loads, bit2: no stores, bit3: no MMAs): {ms:.4f} ms, "
           f"{ops / ms / 1e9:.0f} TOPS issued", flush=True)
 
 # issue-loop clock record (probe bit 5, with the stores off): SM cycles and ns per CTA
