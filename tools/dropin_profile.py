@@ -12,11 +12,15 @@ import paper_2501_11407_b200 as P  # noqa: E402
 from paper_2501_11407_b200.datasets import poisson_batch  # noqa: E402
 from paper_2501_11407_b200 import gradients as G  # noqa: E402
 
-net = P.init_network(P.NetworkSpec(kind="alif", n_hidden=1024, n_inputs=700, n_classes=20,
+# python tools/dropin_profile.py [kind n B]   (default: C3 = alif 1024 256)
+KIND = sys.argv[1] if len(sys.argv) > 1 else "alif"
+N_H = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+BATCH = int(sys.argv[3]) if len(sys.argv) > 3 else 256
+net = P.init_network(P.NetworkSpec(kind=KIND, n_hidden=N_H, n_inputs=700, n_classes=20,
                                    precision="f32", seed=0))
-x, y = poisson_batch(256, 700, 250, 20, seed=1000)
+x, y = poisson_batch(BATCH, 700, 250, 20, seed=1000)
 xb = np.packbits(x, axis=-1, bitorder="little")
-eng = G.get_engine(net, 256, T=250)
+eng = G.get_engine(net, BATCH, T=250)
 st = G._staging(eng)
 
 
@@ -40,7 +44,7 @@ st.counts_nonbinary = False
 sync = torch.cuda.synchronize
 print("phase: pack+H2D (counts)  %.3f" % timeit(lambda: (st.inputs_packed_from_counts(x, y), sync())))
 print("phase: pack only (1 thr)  %.3f" % timeit(lambda: P._lib.load().spb_host_pack_bits(
-    x.ctypes.data, 256 * 250, 700, st.bufs[(256, 250, 88)][0].numpy().ctypes.data)))
+    x.ctypes.data, BATCH * 250, 700, st.bufs[(BATCH, 250, 88)][0].numpy().ctypes.data)))
 print("phase: copy+H2D (packed)  %.3f" % timeit(lambda: (st.inputs(xb, y), sync())))
 print("phase: weights check      %.3f" % timeit(lambda: st.weights(net)))
 kw = dict(smooth=False, bits=True, binary=True, **G._neuron_kwargs(net))
@@ -67,5 +71,5 @@ for pp in (2, 4, 8, 16, 32):
     print("counts pack parts %d: ms/call %.3f, pack+H2D %.3f" % (
         pp, timeit(lambda: G.eprop_batch_gradient(net, x, y)),
         timeit(lambda: (st.inputs_packed_from_counts(x, y), sync()))))
-hb = st.bufs[(256, 250, 88)]
+hb = st.bufs[(BATCH, 250, 88)]
 print("H2D 5.6 MB pinned alone %.3f" % timeit(lambda: (hb[1].copy_(hb[0], non_blocking=True), sync())))

@@ -1,3 +1,1 @@
-for r in 1 2 3; do for L in base sets; do echo -n "$L: "; SPB_LIB=ab/lib_$L.so python tools/k2_bands.py 4 12 2>&1 | grep bands | cut -c1-80; done; done
-for L in base sets; do SPB_LIB=ab/lib_$L.so timeout 300 python bench.py --no-cpu --steps 30 > gpurun_out/ab.json 2>/dev/null; echo -n "$L "; python tools/bench_summary.py gpurun_out/ab.json 2>/dev/null | grep -E "ms=|proj" | sed -E 's/.*ms=([0-9.]+).*/ms=\1/; s/, .share.*//' | tr '\n' ' '; echo; done
-for L in base sets; do SPB_LIB=ab/lib_$L.so timeout 300 python bench.py --config c4 --no-cpu --steps 20 > gpurun_out/ab.json 2>/dev/null; echo -n "c4 $L "; python tools/bench_summary.py gpurun_out/ab.json 2>/dev/null | grep -E "ms=|proj" | sed -E 's/.*ms=([0-9.]+).*/ms=\1/; s/, .share.*//' | tr '\n' ' '; echo; done
+timeout 600 python bench.py --no-cpu --no-parity 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['e2e_dropin'])"
