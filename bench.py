@@ -70,6 +70,9 @@ def peaks():
 
 
 INT8_KERNELS = ("proj",)
+# issue-rate peaks of the MMA kinds measured on this B200 (tools/mma_microbench.cu,
+# profiles/r1/mma_microbench.txt: M = 128, N >= 128, one CTA per SM, burst clock)
+MMA_ISSUE_PEAK_TOPS = {"proj": 4484.0, "gemm": 2196.0, "carry": 2196.0}
 
 
 def measured_traffic(cfg, kernel):
@@ -678,6 +681,11 @@ def main():
             roof = {"kernel": names[dom], "bound": "hbm", "achieved": e["hbm_gbs"],
                     "peak": hbm_peak, "unit": "GB/s", "frac": e["hbm_frac"]}
         tr = measured_traffic(args.config + ("_rec" if args.recurrent else ""), dom)
+        if roof["bound"] == "tensor" and dom in MMA_ISSUE_PEAK_TOPS:
+            # the same achieved rate against the MMA kind's own measured issue peak
+            roof["frac_of_mma_issue_peak"] = roof["achieved"] / MMA_ISSUE_PEAK_TOPS[dom]
+            roof["mma_issue_peak_source"] = ("tools/mma_microbench.cu "
+                                             "(profiles/r1/mma_microbench.txt), burst clock")
         roof.update({"peak_source": peak_kind + (" (int8 = 2x bf16)" if dom in INT8_KERNELS else ""),
                      "traffic": (tr or {}).get("bytes_per_launch"),
                      "traffic_unit": "bytes per launch (DRAM read + write)",
