@@ -238,17 +238,18 @@ class DeviceTrainer:
         st = ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
         v = ctypes.c_void_p
         stats = torch.stack([eng.loss.sum(), eng.correct.sum().to(torch.float64)])
-        if self._world() > 1 and self.w_rec is not None:
-            raise NotImplementedError("multi-rank training of the recurrent extension")
+        # the accumulator holds grad W in columns [0, k) and, for the recurrent
+        # extension, grad W_rec in columns [k, k + n): both travel in the one payload
+        kx = eng.k + (eng.n if self.w_rec is not None else 0)
         if self._world() > 1:
             from .parallel import GradPacker
             if self._packer is None:
-                self._packer = GradPacker(eng.n, eng.k, eng.m, self.device,
+                self._packer = GradPacker(eng.n, kx, eng.m, self.device,
                                           dtype=torch.float64 if self.is_f64 else torch.float32)
             self._packer.pack(eng.grad_w_acc, eng.grad_wout, eng.loss, eng.correct)
             gw, gwo, ls, nc = self._packer.allreduce(self.group)
             stats = torch.stack([ls.to(torch.float64), nc.to(torch.float64)])
-            g_w, g_w_f64, ld_w = gw, int(self.is_f64), eng.k
+            g_w, g_w_f64, ld_w = gw, int(self.is_f64), kx
             g_wo, g_wo_f64 = gwo, int(self.is_f64)
         else:
             g_w, g_w_f64, ld_w = eng.grad_w_acc, 1, eng.kp
@@ -270,15 +271,15 @@ class DeviceTrainer:
                           v(self.v_wo.data_ptr()), f64, m, n, v(g_wo.data_ptr()), g_wo_f64, n,
                           scale, self.lr, self.beta1, self.beta2, self.eps, self.t,
                           v(eng.wout.data_ptr()), st)
-        if self.w_rec is not None:  # columns k .. k+n of the accumulator
-            g_wr = ctypes.c_void_p(eng.grad_w_acc.data_ptr() + 8 * k)
+        if self.w_rec is not None:  # columns k .. k+n of the accumulator / payload
+            g_wr = ctypes.c_void_p(g_w.data_ptr() + g_w.element_size() * k)
             if self.optimizer == "sgd":
-                self.lib.call("spb_sgd_update", v(self.w_rec.data_ptr()), f64, n, n, g_wr, 1,
-                              eng.kp, scale, self.lr, None, st)
+                self.lib.call("spb_sgd_update", v(self.w_rec.data_ptr()), f64, n, n, g_wr,
+                              g_w_f64, ld_w, scale, self.lr, None, st)
             else:
                 self.lib.call("spb_adam_update", v(self.w_rec.data_ptr()),
                               v(self.m_wr.data_ptr()), v(self.v_wr.data_ptr()), f64, n, n, g_wr,
-                              1, eng.kp, scale, self.lr, self.beta1, self.beta2, self.eps,
+                              g_w_f64, ld_w, scale, self.lr, self.beta1, self.beta2, self.eps,
                               self.t, None, st)
             eng.wrecT.copy_(self.w_rec.t())
         # this engine's digits follow the new W right away (the next update's K2; the

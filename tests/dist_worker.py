@@ -44,6 +44,12 @@ def main(out):
     res.update(w=net2.neuron.w, w_out=net2.readout.w_out,
                row_loss=np.array([r.loss for r in rows]),
                row_acc=np.array([r.accuracy for r in rows]))
+    # the recurrent extension: grad W and grad W_rec travel in the one payload
+    net3, rows3 = train(P.NetworkSpec(**SPEC, recurrent=True), ds, batch_size=8, epochs=1,
+                        lr=0.05)
+    res.update(rec_w=net3.neuron.w, rec_w_out=net3.readout.w_out, rec_w_rec=net3.neuron.w_rec,
+               rec_row_loss=np.array([r.loss for r in rows3]),
+               rec_row_acc=np.array([r.accuracy for r in rows3]))
     if rank == 0:
         np.savez(os.path.join(out, "dist.npz"), **res)
     dist.barrier()

@@ -71,3 +71,12 @@ def test_two_ranks_equal_one_rank(tmp_path):
     # accumulators directly: the weights agree to the fp32 rounding of 4 updates)
     assert _rel(d["w"], net1.neuron.w) <= 5e-5
     assert _rel(d["w_out"], net1.readout.w_out) <= 5e-5
+    # recurrent extension (W_rec): sharded training = one rank on the whole batch
+    net3, rows3 = train(P.NetworkSpec(**W.SPEC, recurrent=True), ds, batch_size=8, epochs=1,
+                        lr=0.05)
+    assert np.array_equal(d["rec_row_acc"], [r.accuracy for r in rows3])
+    np.testing.assert_allclose(d["rec_row_loss"], [r.loss for r in rows3], rtol=1e-5)
+    assert _rel(d["rec_w"], net3.neuron.w) <= 5e-5
+    assert _rel(d["rec_w_out"], net3.readout.w_out) <= 5e-5
+    assert _rel(d["rec_w_rec"], net3.neuron.w_rec) <= 5e-5
+    assert _rel(d["rec_w_rec"], P.init_network(P.NetworkSpec(**W.SPEC, recurrent=True)).neuron.w_rec) > 0
