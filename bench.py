@@ -403,7 +403,9 @@ def main():
         eng.park_budget = int(args.park_gb * (1 << 30))
     xd = torch.from_numpy(x_np).to(dev)
     yd = torch.from_numpy(y_np).to(dev)
-    packer = GradPacker(n, k, m, dev)  # (recurrent: grad W_rec stays in the accumulator)
+    # the payload: grad W columns [0, k) (+ grad W_rec columns [k, k + n), recurrent)
+    kx = k + (n if args.recurrent else 0)
+    packer = GradPacker(n, kx, m, dev)
     kw = dict(alpha=net.neuron.alpha, theta=net.neuron.theta, slope=net.neuron.slope,
               kappa=net.readout.kappa)
     if kind == "alif":
@@ -414,13 +416,15 @@ def main():
     # engine's fp64 mirror) and W is re-sliced into the INT8 digits the next update's
     # projection reads -- all of it inside the timed step.
     wout_master = torch.from_numpy(np.ascontiguousarray(net.readout.w_out)).to(dev)
+    wrec_master = (torch.from_numpy(np.ascontiguousarray(net.neuron.w_rec)).to(dev)
+                   if args.recurrent else None)
     lr, g_scale = 1e-3, 1.0 / G
     vp = ctypes.c_void_p
 
     def update():
         if world > 1:  # the allreduced fp32 payload
             gw, gwo, _, _ = packer.views()
-            g64, ldw = 0, k
+            g64, ldw = 0, kx
         else:          # one rank: straight from the engine's fp64 accumulators
             gw, gwo, g64, ldw = eng.grad_w_acc, eng.grad_wout, 1, eng.grad_w_acc.stride(0)
         st = vp(torch.cuda.current_stream(dev).cuda_stream)
@@ -428,6 +432,14 @@ def main():
         eng.sgd_slice(gw, g64, ldw, g_scale, lr)
         _lib.call("spb_sgd_update", vp(wout_master.data_ptr()), 0, m, n, vp(gwo.data_ptr()),
                   g64, n, g_scale, lr, vp(eng.wout.data_ptr()), st)
+        if wrec_master is not None:  # W_rec (columns k .. k+n) and its transposed copy
+            # (a small step size keeps the recurrent activity -- the gather work -- at its
+            # initial level over the timed steps; at lr = 1e-3 the synthetic network's
+            # recurrent excitation grows step by step.  Same kernels, same work per step.)
+            _lib.call("spb_sgd_update", vp(wrec_master.data_ptr()), 0, n, n,
+                      vp(gw.data_ptr() + gw.element_size() * k), g64, ldw, g_scale, 1e-6,
+                      None, st)
+            eng.wrecT.copy_(wrec_master.t())
 
     def local_part(x, y, timers=None, bits=False):
         # the synthetic Poisson inputs are 0/1 spikes: promise it (K2 single-int64 path)
@@ -521,7 +533,7 @@ def main():
     barrier()
     # kernels of libsparseprop_b200.so per step: the engine's + SGD(+slice) on W + SGD on
     # W_out (+ the payload pack when N > 1)
-    launches_per_step = eng.launches + 2 + (1 if world > 1 else 0)
+    launches_per_step = eng.launches + 2 + (1 if world > 1 else 0) + (1 if args.recurrent else 0)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
     clk = clocks.stop() if clocks else None
@@ -743,7 +755,8 @@ def main():
             "run": {"forward_precision": "fp64 state/current (bit-exact spikes)",
                     "forward_kernel": "K2 projection + K1 dynamics",
                     "step": "e-prop gradient (+ allreduce when N > 1) + fused SGD on W/W_out "
-                            "+ W re-slice",
+                            "+ W re-slice" + (" + SGD on W_rec (+ its transposed copy)"
+                                              if args.recurrent else ""),
                     "psi_parking_gb": args.park_gb,
                     "l2": "512 MiB flush between timed steps (outside events)",
                     "launch": (("CUDA graph replay of the whole update" if world == 1 else

@@ -1,5 +1,3 @@
-mkdir -p gpurun_out/r2b
-timeout 600 python bench.py > gpurun_out/r2b/bench_c3.json 2> gpurun_out/r2b/bench_c3.err
-timeout 300 python bench.py --config c4 --no-cpu --steps 10 > gpurun_out/r2b/bench_c4.json 2>&1
-timeout 300 python bench.py --config c2 --no-cpu --steps 20 > gpurun_out/r2b/bench_c2.json 2>&1
-for c in c3 c4 c2; do python -c "import json; d=json.loads(open('gpurun_out/r2b/bench_$c.json').read().strip().splitlines()[-1]); print('$c', d['ms_per_step'], d['e2e']['value'], d['e2e_dropin']['ms_per_call'], d['e2e_dropin']['packed']['ms_per_call'])"; done
+timeout 300 python bench.py --recurrent --no-cpu --steps 10 > gpurun_out/r2b/bench_c3_recurrent.json 2>gpurun_out/r2b/rec.err; tail -2 gpurun_out/r2b/rec.err
+python tools/bench_summary.py gpurun_out/r2b/bench_c3_recurrent.json | head -3
+SPB_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --recurrent --steps 3 --warmup 3 --no-cpu 2>&1 | tail -1 | cut -c1-200
