@@ -226,6 +226,14 @@ int spb_reduce_partials(const float* partial, int splits, int n, int n_pad, int 
 int spb_copy_chunk_h2d(void* dst, long long dst_pitch, const void* src, long long src_pitch,
                        long long row_bytes, int rows, cudaStream_t stream);
 
+/* Real-valued (non-count) inputs, one chunk: x [B][len][k] fp32 (x_is_f64 = 0) / fp64 with
+ * sample stride stride_b (elements) -> the raw-input GEMM operand as bf16 hi/lo pairs
+ * xh, xl [B*KR][ld] (row b*KR + s + 1 = step s; rows s >= len zero; row b*KR untouched),
+ * x = hi + lo to ~2^-16 relative.  The projection of such inputs is an fp64 GEMM (the
+ * exact INT8 path needs integer counts). */
+int spb_pack_real(const void* x, int x_is_f64, long long stride_b, int B, int k, int len, int KR,
+                  int ld, void* xh, void* xl, cudaStream_t stream);
+
 /* HOST helper of the drop-in's staging (host.cu; x and out are HOST pointers, no stream):
  * uint8 counts x [rows][k] -> out [rows][ceil(k/8)] bit-packed like
  * np.packbits(x, axis=-1, bitorder="little").  Returns 0 when every count is 0 or 1, 1

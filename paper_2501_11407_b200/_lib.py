@@ -45,6 +45,7 @@ SIGNATURES = {
     "spb_pack_grads": [P, I, I, I, P, I, P, P, I, P, I, P],
     "spb_copy_chunk_h2d": [P, LL, P, LL, LL, I, P],
     "spb_host_pack_bits": [P, LL, I, P],
+    "spb_pack_real": [P, I, LL, I, I, I, I, I, P, P, P],
     "spb_sgd_slice_update": [P, I, I, I, P, I, I, D, D, I, I, I, P, P, P],
     "spb_sgd_update": [P, I, I, I, P, I, I, D, D, P, P],
     "spb_adam_update": [P, P, P, I, I, I, P, I, I, D, D, D, D, D, I, P, P],

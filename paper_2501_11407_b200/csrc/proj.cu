@@ -959,6 +959,65 @@ int spb_pack_spikes_xh(const uint8_t* x, long long stride_b, int B, int k, int b
   return 0;
 }
 
+}  // extern "C"
+namespace spb {
+namespace proj {
+// Real-valued inputs (the drop-in's non-count x): the one-chunk raw-input GEMM operand as
+// bf16 hi/lo pairs, x = hi + lo to ~2^-16, in the row layout of spb_pack_spikes_xh (row
+// b*KR + s + 1 = step s, rows s >= len zero, row b*KR untouched).  Thread per 2 columns.
+template <typename T>
+__global__ void pack_real_kernel(const T* __restrict__ x, long long stride_b, int B, int k,
+                                 int len, int KR, int ld, __nv_bfloat162* __restrict__ xh,
+                                 __nv_bfloat162* __restrict__ xl) {
+  pdl_enter();
+  const int hw = ld >> 1;                                  // bf16 pairs per row
+  const long long total = (long long)B * (KR - 1) * hw;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int c2 = (int)(idx % hw);
+    const long long rs = idx / hw;
+    const int s = (int)(rs % (KR - 1));
+    const int b = (int)(rs / (KR - 1));
+    float hi[2], lo[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = 2 * c2 + e;
+      const double v = (s < len && j < k) ? (double)x[(long long)b * stride_b + (long long)s * k + j]
+                                           : 0.0;
+      const __nv_bfloat16 h = __double2bfloat16(v);
+      hi[e] = __bfloat162float(h);
+      lo[e] = (float)(v - (double)hi[e]);
+    }
+    const long long o = ((long long)b * KR + s + 1) * hw + c2;
+    xh[o] = __floats2bfloat162_rn(hi[0], hi[1]);
+    xl[o] = __floats2bfloat162_rn(lo[0], lo[1]);
+  }
+}
+}  // namespace proj
+}  // namespace spb
+extern "C" {
+
+// Real-valued (non-count) inputs of one chunk: x [B][len][k] fp32 (x_is_f64 = 0) / fp64,
+// sample stride stride_b elements -> xh, xl bf16 [B*KR][ld] (see pack_real_kernel).
+int spb_pack_real(const void* x, int x_is_f64, long long stride_b, int B, int k, int len, int KR,
+                  int ld, void* xh, void* xl, cudaStream_t stream) {
+  SPB_CHECK_ARG(x && xh && xl && B > 0 && k > 0 && ld >= k && ld % 2 == 0 && len >= 0 &&
+                    len < KR && stride_b >= (long long)len * k,
+                "spb_pack_real: bad args");
+  const long long pairs = (long long)B * (KR - 1) * (ld / 2);
+  const int blocks = (int)std::min<long long>((pairs + 255) / 256, 148LL * 8);
+  if (x_is_f64)
+    pdl_launch(proj::pack_real_kernel<double>, blocks, 256, 0, stream,
+               static_cast<const double*>(x), stride_b, B, k, len, KR, ld,
+               static_cast<__nv_bfloat162*>(xh), static_cast<__nv_bfloat162*>(xl));
+  else
+    pdl_launch(proj::pack_real_kernel<float>, blocks, 256, 0, stream,
+               static_cast<const float*>(x), stride_b, B, k, len, KR, ld,
+               static_cast<__nv_bfloat162*>(xh), static_cast<__nv_bfloat162*>(xl));
+  SPB_CHECK_LAUNCH("pack_real");
+  return 0;
+}
+
 int spb_launch_sgd_slice(void* w, int w_is_f64, int n, int k, const void* g, int g_is_f64,
                          int ld_g, double g_scale, double lr, int do_sgd, int Kpad, int n_pad32,
                          int P, int8_t* wq, int* sexp, cudaStream_t stream);  // optim.cu

@@ -380,10 +380,13 @@ class EpropEngine:
         if bool(reset) != self.reset:
             raise ValueError(f"engine built for reset={self.reset}, called with reset={reset}")
         kb = (self.k + 7) // 8 if bits else self.k
-        if x.dtype != torch.uint8 or x.dim() != 3 or x.shape[0] != self.B or x.shape[2] != kb:
+        # real-valued inputs (fp32/fp64, not spike counts): fp64 projection, hi/lo operand
+        real = x.dtype in (torch.float32, torch.float64) and not bits
+        if ((x.dtype != torch.uint8 and not real) or x.dim() != 3 or x.shape[0] != self.B
+                or x.shape[2] != kb):
             raise ShapeMismatch(f"x must be uint8 [B={self.B}, T, {kb}] "
-                                f"({'bit-packed' if bits else 'counts'}), got "
-                                f"{tuple(x.shape)} {x.dtype}")
+                                f"({'bit-packed' if bits else 'counts'}) or fp32/fp64 "
+                                f"[B, T, k], got {tuple(x.shape)} {x.dtype}")
         if not x.is_contiguous():
             raise ShapeMismatch("x must be contiguous")
         if (labels.dtype != torch.int64 or tuple(labels.shape) != (self.B,)
@@ -396,6 +399,13 @@ class EpropEngine:
         T = int(x.shape[1])
         if T <= 0:
             raise ShapeMismatch("T must be positive")
+        if real and (streaming or T > self.Tc or self.recurrent or self.reset
+                     or stream is not None or x.device != self.device
+                     or self.device.type != "cuda"):
+            raise ValueError("real-valued (non-count) inputs are supported for one-chunk "
+                             f"sequences (T <= {self.Tc}) on the engine's device, reset=False, "
+                             "without the recurrent extension; spike-count inputs have no "
+                             "such limits")
         call = _lib.call
         st = ctypes_void(stream if stream is not None else self._stream())
         beta_e, rho_e = (float(beta), float(rho)) if self.alif else (0.0, 0.0)
@@ -436,9 +446,13 @@ class EpropEngine:
             x_alpha = 0.0   # K4 = byte -> bf16 copy (the filter state is never needed)
         raw_x = (filt or self.reset) and (filt or not self.recurrent)
         xl_ptr = None if (raw_x or self.xl is None) else v(self.xl.data_ptr())
+        if real and self.xl is not None:
+            xl_ptr = v(self.xl.data_ptr())   # real inputs are not exact in bf16: hi + lo
         # one chunk: the pack writes the raw-spike GEMM operand itself (no K4 at all)
         pack_xh = (filt and one and not self.recurrent and self.pack_xh
                    and (bits or (self.k % 4 == 0 and x.data_ptr() % 4 == 0)))
+        if real:
+            pack_xh = True   # spb_pack_real writes the operand (hi and lo)
 
         def timed(name, meta, fn, *args):
             if timers is None:
@@ -491,6 +505,17 @@ class EpropEngine:
                 self._pack(xs[u % 2].data_ptr(), Tc * kb, bits, ln, st, xh=pack_xh)
                 self._sev_free[u % 2].record(main)
                 state["u"] += 1
+        elif real:
+            def pack_chunk(c, ln):
+                # operand: bf16 hi/lo rows; projection I = x W^T in fp64 (cuBLAS DGEMM via
+                # torch, on this stream): the exact INT8 path needs integer counts
+                if self.xh is not None:   # (forward-only engines have no GEMM operand)
+                    call("spb_pack_real", v(x.data_ptr()), int(x.dtype == torch.float64),
+                         T * k, B, k, ln, KR, self.kp, v(self.xh.data_ptr()),
+                         v(self.xl.data_ptr()), st)
+                cur3 = self.cur.view(B, KR, n)
+                cur3[:, :ln].copy_(torch.matmul(x[:, :ln].to(torch.float64),
+                                                self.w.to(torch.float64).t()))
         else:
             def pack_chunk(c, ln):
                 self._pack(x.data_ptr() + c * Tc * kb, strideb, bits, ln, st, xh=pack_xh)
@@ -516,7 +541,7 @@ class EpropEngine:
                      xl_ptr, sst)
                 self._ev["xbar"].record(self.side)
                 self.launches += 1
-            if not (side_x and self.xbar_sched == "fa"):
+            if not (side_x and self.xbar_sched == "fa") and not real:
                 self._project(ln, st, timed, binary)
             if self.recurrent:
                 self._forward_rec(0, ln, t0, T, common, raster,

@@ -148,21 +148,33 @@ def get_engine(net, B: int, *, chunk: int | None = None, T: int | None = None,
 
 
 def _as_counts(x: np.ndarray) -> np.ndarray:
-    """Spike inputs as uint8 event counts (binary spikes or pooled counts <= 255).
+    """Spike inputs as uint8 event counts (binary spikes or pooled counts <= 255), or None
+    when ``x`` is not such a count tensor (real-valued inputs, see ``_as_inputs``).
 
     Every input the reference produces or tests with is a spike count: Poisson 0/1
     spikes (datasets.py:65-67, bench.py:63-67), pooled integer counts
-    (datasets.py:138-159), and the 0/1 draws of its tests (test_gradients.py:50).  The
-    exact INT8 tensor-core projection relies on it; real-valued inputs raise."""
+    (datasets.py:138-159), and the 0/1 draws of its tests (test_gradients.py:50); the
+    exact INT8 tensor-core projection relies on it."""
     if x.dtype == np.uint8:
         return x
     if x.dtype == np.bool_:
         return x.view(np.uint8)
     xi = np.rint(x)
     if not np.array_equal(xi, x) or (x.size and (x.min() < 0 or x.max() > 255)):
-        raise ValueError("inputs must be non-negative integer spike counts <= 255 "
-                         "(binary spikes or pooled counts, datasets.py:46-52/138-159)")
+        return None
     return xi.astype(np.uint8)
+
+
+def _as_inputs(x: np.ndarray):
+    """(array, real): spike counts as uint8 (the exact INT8 projection), anything else
+    real-valued as float64 (the reference accepts any float x_seq, gradients.py:132; the
+    B200 path then projects in fp64 and feeds the gradient GEMM bf16 hi/lo pairs)."""
+    if x.dtype != np.bool_ and (not np.issubdtype(x.dtype, np.number) or np.iscomplexobj(x)):
+        raise ShapeMismatch(f"inputs must be real numbers, got {x.dtype}")
+    c = _as_counts(x)
+    if c is not None:
+        return c, False
+    return np.ascontiguousarray(x, dtype=np.float64), True
 
 
 # --------------------------------------------------------------------------------------
@@ -364,7 +376,10 @@ def _check_batch(net, x, labels, packed: bool):
         raise LabelOutOfRange(f"label {int(bad)} out of range for {m} classes")
     if packed and x.dtype != np.uint8:
         raise ShapeMismatch("bit-packed inputs are uint8 (np.packbits, bitorder='little')")
-    return (x if packed else _as_counts(x)), labels
+    if packed:
+        return x, labels, False
+    xc, real = _as_inputs(x)
+    return xc, labels, real
 
 
 # --------------------------------------------------------------------------------------
@@ -373,7 +388,8 @@ def _check_batch(net, x, labels, packed: bool):
 
 def eprop_batch_gradient(net, x, labels, *, chunk: int | None = None, device=None,
                          smooth: bool = False, packed: bool = False) -> BatchGradResult:
-    """Batched online e-prop on the B200: x [B, T, k] spike counts, labels [B].
+    """Batched online e-prop on the B200: x [B, T, k] spike counts (or real values, see
+    ``_as_inputs``), labels [B].
 
     Returns per-sample losses and readout sums and the gradients SUMMED over the batch
     (= sum of the reference's per-sample ``eprop_sparse_gradient`` grads).  ``smooth``
@@ -386,13 +402,15 @@ def eprop_batch_gradient(net, x, labels, *, chunk: int | None = None, device=Non
     host-to-device), the weights are uploaded and re-sliced only when they changed, and
     the results come back through pinned buffers in one synchronisation.
     """
-    xc, labels = _check_batch(net, x, labels, packed)
+    xc, labels, real = _check_batch(net, x, labels, packed)
     B, T = xc.shape[0], xc.shape[1]
     if B == 0 or T == 0:
         raise ShapeMismatch("empty batch or sequence")
     eng = get_engine(net, B, chunk=chunk, T=T, device=device)
     st = _staging(eng)
     xc = np.ascontiguousarray(xc)
+    if real:
+        return _real_batch_gradient(net, eng, st, xc, labels, smooth)
     # the weight comparison runs on a staging thread while the inputs are staged
     w_check = _pool().submit(st.weights_unchanged, net)
     binary = packed
@@ -407,7 +425,11 @@ def eprop_batch_gradient(net, x, labels, *, chunk: int | None = None, device=Non
     binary = binary or np.asarray(x).dtype == np.bool_
     kw = dict(smooth=bool(smooth), bits=bool(packed), binary=bool(binary), **_neuron_kwargs(net))
     st.run(tuple(sorted(kw.items())) + (T,), **kw)
-    w_dtype = np.asarray(net.neuron.w).dtype
+    return _collect(eng, net, np.asarray(net.neuron.w).dtype)
+
+
+def _collect(eng, net, w_dtype):
+    """Results of the last update as numpy (pinned buffers, one synchronisation)."""
     wdt = torch.float64 if w_dtype == np.float64 else torch.float32
     outs = {"w": _to_host(eng.grad_w(wdt)), "w_out": _to_host(eng.grad_wout.to(wdt)),
             "loss": _to_host(eng.loss), "s": _to_host(eng.s), "correct": _to_host(eng.correct)}
@@ -425,13 +447,25 @@ def eprop_batch_gradient(net, x, labels, *, chunk: int | None = None, device=Non
     )
 
 
+def _real_batch_gradient(net, eng, st, xr, labels, smooth):
+    """Real-valued inputs: one chunk, reset=False, no W_rec (EpropEngine.run checks it);
+    the projection is an fp64 GEMM instead of the exact INT8 one, so spikes equal an fp64
+    reference up to its own summation-order rounding rather than bit for bit."""
+    st._labels(labels)
+    st.weights(net)
+    xd = torch.from_numpy(xr).to(eng.device)
+    eng.run(xd, st.y_dev, smooth=bool(smooth), **_neuron_kwargs(net))
+    return _collect(eng, net, np.asarray(net.neuron.w).dtype)
+
+
 def eprop_sparse_gradient(net, x_seq: np.ndarray, label: int,
                           smooth: bool = False) -> GradResult:
     """Online sparse e-prop for one sample -- the reference entry point (gradients.py:132).
 
     Same contract: ``x_seq`` [T, k], integer ``label``; returns the loss, the gradients
     {"w": [n, k], "w_out": [m, n]} in the dtype of ``net.neuron.w`` and the time-summed
-    readout.  Inputs must be spike counts (binary or pooled integers).
+    readout.  Spike counts take the exact INT8 projection; other real values the fp64 one
+    (one-chunk sequences, reset=False).
     """
     n, k, m = _dims(net)
     x_seq = np.asarray(x_seq)
@@ -454,11 +488,16 @@ def network_loss(net, x_seq: np.ndarray, label: int, smooth: bool = False):
         raise ShapeMismatch(f"x_seq must be [T, k={k}], got {x_seq.shape}")
     if not 0 <= int(label) < m:
         raise LabelOutOfRange(f"label {label} out of range for {m} classes")
-    xc = _as_counts(x_seq)[None]
+    xc, real = _as_inputs(x_seq)
+    xc = xc[None]
     T = xc.shape[1]
     eng = get_engine(net, 1, T=T, grad=False)
     st = _staging(eng)
-    xd, ld = st.inputs(np.ascontiguousarray(xc), np.array([int(label)]))
+    if real:
+        st._labels(np.array([int(label)]))
+        xd, ld = torch.from_numpy(np.ascontiguousarray(xc)).to(eng.device), st.y_dev
+    else:
+        xd, ld = st.inputs(np.ascontiguousarray(xc), np.array([int(label)]))
     st.weights(net)
     raster = torch.zeros((1, T, (n + 31) // 32), dtype=torch.int32, device=eng.device)
     eng.run(xd, ld, raster=raster, smooth=smooth, forward_only=True, **_neuron_kwargs(net))

@@ -205,6 +205,10 @@ def test_engine_rejects_bad_inputs():
     with pytest.raises(P.ShapeMismatch):
         eng.run(torch.zeros((3, 10, 4), dtype=torch.uint8), torch.zeros(3, dtype=torch.int64))
     with pytest.raises(P.ShapeMismatch):
+        eng.run(torch.zeros((3, 10, 5), dtype=torch.int32), torch.zeros(3, dtype=torch.int64))
+    with pytest.raises(P.ShapeMismatch):
+        eng.run(torch.zeros((3, 10, 4), dtype=torch.float32), torch.zeros(3, dtype=torch.int64))
+    with pytest.raises(ValueError):   # real-valued inputs: one chunk on a CUDA engine only
         eng.run(torch.zeros((3, 10, 5), dtype=torch.float32), torch.zeros(3, dtype=torch.int64))
     with pytest.raises(ValueError):
         eng.run(torch.zeros((3, 10, 5), dtype=torch.uint8), torch.zeros(3, dtype=torch.int64),
@@ -247,13 +251,18 @@ def test_init_network_matches_oracle_and_reference_seed_stream():
 
 
 def test_input_count_conversion():
-    from paper_2501_11407_b200.gradients import _as_counts
+    """Integer-valued inputs in [0, 255] go the exact INT8 way as uint8 counts; anything
+    else real-valued is kept as float64 (the fp64-projection path); non-numbers raise."""
+    from paper_2501_11407_b200.gradients import _as_counts, _as_inputs
     x = np.array([[0.0, 1.0, 3.0]])
     assert _as_counts(x).dtype == np.uint8
-    with pytest.raises(ValueError):
-        _as_counts(np.array([[0.5]]))
-    with pytest.raises(ValueError):
-        _as_counts(np.array([[-1.0]]))
+    assert _as_inputs(x)[1] is False and _as_inputs(x)[0].dtype == np.uint8
+    for v in (0.5, -1.0, 300.0):
+        assert _as_counts(np.array([[v]])) is None
+        xr, real = _as_inputs(np.array([[v]], dtype=np.float32))
+        assert real and xr.dtype == np.float64 and xr[0, 0] == v
+    with pytest.raises(P.ShapeMismatch):
+        _as_inputs(np.array([["a"]]))
 
 
 def test_default_chunk():

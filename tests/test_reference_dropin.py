@@ -160,6 +160,46 @@ def test_reference_network_objects_vs_reference_engines(kind, n, T):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["lif", "alif"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_real_valued_inputs_vs_reference(kind, dtype):
+    """Inputs that are not spike counts (any float x_seq, as the reference accepts,
+    gradients.py:132): the B200 path projects them in fp64 and feeds the gradient GEMM
+    bf16 hi/lo pairs -- the reference's own e-prop and BPTT on its own Network objects
+    are matched to the fp32 gradient tolerance, the forward raster and loss exactly."""
+    _need_gpu()
+    sp = _sparseprop()
+    from sparseprop.gradients import bptt_gradient, eprop_sparse_gradient, network_loss
+
+    from paper_2501_11407_b200 import gradients as G
+    for seed in range(3):
+        net = _ref_network(sp, kind, n=32, k=12, seed=seed, dtype=dtype)
+        rng = np.random.default_rng(seed + 7)
+        x = (rng.random((90, 12)) * 1.3 * (rng.random((90, 12)) < 0.4)).astype(dtype)
+        label = int(rng.integers(net.m))
+        a = G.eprop_sparse_gradient(net, x, label)
+        for ref in (eprop_sparse_gradient(net, x, label), bptt_gradient(net, x, label)):
+            for key in ("w", "w_out"):
+                assert a.grads[key].dtype == net.neuron.w.dtype
+                g, r = a.grads[key].astype(np.float64), ref.grads[key].astype(np.float64)
+                rel = np.linalg.norm(g - r) / max(np.linalg.norm(r), 1e-300)
+                assert rel <= (1e-4 if dtype == np.float64 else 2e-4), (key, rel)
+        l_ours, s_ours, r_ours = G.network_loss(net, x, label)
+        l_ref, s_ref, r_ref = network_loss(net, x, label)
+        assert np.array_equal(r_ours, r_ref)
+        # (the reference runs an f32 net in f32 arithmetic, the B200 path in fp64)
+        assert l_ours == pytest.approx(l_ref, rel=1e-4 if dtype == np.float32 else 1e-10)
+    # the batched entry point with a float batch (B = 5, T = 90)
+    xb = (np.random.default_rng(3).random((5, 90, 12)) * 0.9).astype(dtype)
+    yb = np.arange(5) % net.m
+    rb = G.eprop_batch_gradient(net, xb, yb)
+    gs = sum(eprop_sparse_gradient(net, xb[i], int(yb[i])).grads["w"].astype(np.float64)
+             for i in range(5))
+    rel = np.linalg.norm(rb.grads["w"] - gs) / np.linalg.norm(gs)
+    assert rel <= 2e-4, rel
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("kind,precision,optimizer", [("lif", "f64", "sgd"),
                                                      ("alif", "f64", "adam"),
                                                      ("alif", "f32", "sgd")])
