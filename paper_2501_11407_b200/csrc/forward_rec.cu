@@ -14,8 +14,8 @@
 // runs the unchanged scan / xbar / GEMM / carry kernels on the extended input
 // x~_t = [x_t, z_{t-1}] (spb_pack_rec).
 //
-// One CTA per sample, 512 threads, NPT <= 4 neurons per thread (n <= 2048), two CTAs per
-// SM for n <= 1024; the spikes of the previous step live in a double-buffered shared
+// One CTA per sample, 512 threads, NPT <= 4 consecutive neurons per thread (n <= 2048),
+// two CTAs per SM for n <= 1024; the spikes of the previous step live in a double-buffered shared
 // bitmask, compacted by one warp into an ascending active list each step (two
 // __syncthreads per step) so that the weight loads of 8 presynaptic spikes are in flight
 // at once.  The step is latency-bound (L2 round trips of the gather + two barriers).
@@ -39,10 +39,52 @@ __device__ __forceinline__ double rec_spike(double d, bool smooth, double slope)
   return __dadd_rn(0.5, __ddiv_rn(d, __dadd_rn(1.0, __dmul_rn(slope, fabs(d)))));
 }
 
+// The NPT neurons of a thread are consecutive (i = NPT*tid + c), so a gathered row of
+// W_rec^T is one vector load per thread (float2 / float4 / double2 pairs) when n % NPT == 0
+// (VEC), and a warp's spikes form NPT consecutive mask words, assembled with one OR-
+// reduction per word.
+template <int NPT, typename WT, bool VEC>
+__device__ __forceinline__ void rec_load_row(const WT* __restrict__ row, int i0, int n,
+                                             WT (&w)[NPT]) {
+  if constexpr (VEC && NPT == 1) {
+    w[0] = i0 < n ? __ldg(row + i0) : WT(0);
+  } else if constexpr (VEC && sizeof(WT) == 4 && NPT == 2) {
+    const float2 v = i0 < n ? __ldg(reinterpret_cast<const float2*>(row + i0)) : make_float2(0.f, 0.f);
+    w[0] = v.x;
+    w[1] = v.y;
+  } else if constexpr (VEC && sizeof(WT) == 4 && NPT == 4) {
+    const float4 v = i0 < n ? __ldg(reinterpret_cast<const float4*>(row + i0))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    w[0] = v.x;
+    w[1] = v.y;
+    w[2] = v.z;
+    w[3] = v.w;
+  } else if constexpr (VEC && sizeof(WT) == 8) {
+#pragma unroll
+    for (int c = 0; c < NPT; c += 2) {
+      const double2 v = i0 < n ? __ldg(reinterpret_cast<const double2*>(row + i0 + c))
+                               : make_double2(0.0, 0.0);
+      w[c] = v.x;
+      w[c + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < NPT; ++c) w[c] = (i0 + c < n) ? row[i0 + c] : WT(0);
+  }
+}
+
+// this warp's NPT mask words from each lane's NPT spike bits (bit c = neuron NPT*lane + c)
+template <int NPT>
+__device__ __forceinline__ uint32_t rec_mask_word(uint32_t nib, int lane, int q) {
+  constexpr int LPW = 32 / NPT;  // lanes per word
+  const uint32_t v = nib << (NPT * (lane % LPW));
+  return __reduce_or_sync(0xffffffffu, (lane / LPW == q) ? v : 0u);
+}
+
 // WT: the stored weight type (fp32 weights are gathered as fp32 -- half the registers per
 // load in flight -- and widened exactly to fp64 before the ordered sum).  Two CTAs per SM
 // (<= 64 registers), so the B samples of C3 (256) run as ONE wave on 148 SMs instead of two.
-template <int NPT, typename WT>
+template <int NPT, typename WT, bool VEC>
 __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_kernel(
     RecParams P, const double* __restrict__ cur, const void* __restrict__ wrecT,
     double* __restrict__ u_st, double* __restrict__ a_st, double* __restrict__ zbar_st,
@@ -51,17 +93,19 @@ __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_ker
   __shared__ uint32_t mask[2][REC_MAX_N / 32];
   __shared__ uint16_t act[REC_MAX_N];
   __shared__ int nact;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x;
   const int n = P.n, nw = (n + 31) >> 5;
   const bool smooth = P.smooth != 0;
   const double theta = P.theta, beta = P.beta, slope = P.slope;
   const float slope_f = (float)P.slope;
   const WT* wt = static_cast<const WT*>(wrecT);
+  const int i0 = NPT * tid;            // this thread's first neuron
+  const int wbase = NPT * warp;        // this warp's first mask word
   double u[NPT], a[NPT], zb[NPT], zs[NPT], dp[NPT];
 #pragma unroll
   for (int c = 0; c < NPT; ++c) {
-    const int i = tid + c * REC_THREADS;
+    const int i = i0 + c;
     const bool v = i < n;
     const long long bi = (long long)b * n + i;
     u[c] = (v && P.t0 > 0) ? u_st[bi] : 0.0;
@@ -71,18 +115,22 @@ __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_ker
     dp[c] = __dsub_rn(__dsub_rn(u[c], theta), __dmul_rn(beta, a[c]));
   }
   // z_{t0-1} from the carried state (the expression the reference re-evaluates)
+  {
+    uint32_t nib = 0;
 #pragma unroll
-  for (int c = 0; c < NPT; ++c) {
-    const int i = tid + c * REC_THREADS;
-    const bool zv = (i < n) && rec_spike(dp[c], smooth, slope) > 0.5;
-    const unsigned bal = __ballot_sync(0xffffffffu, zv);
-    if (lane == 0 && (c * REC_THREADS + (tid & ~31)) < n) mask[0][(c * REC_THREADS + (tid & ~31)) >> 5] = bal;
+    for (int c = 0; c < NPT; ++c)
+      if (i0 + c < n && rec_spike(dp[c], smooth, slope) > 0.5) nib |= 1u << c;
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      const uint32_t wd = rec_mask_word<NPT>(nib, lane, q);
+      if (lane == q && wbase + q < nw) mask[0][wbase + q] = wd;
+    }
   }
   float* prow = psis != nullptr ? psis + (long long)b * (P.KR + 1) * n : nullptr;
   if (prow != nullptr) {
 #pragma unroll
     for (int c = 0; c < NPT; ++c) {
-      const int i = tid + c * REC_THREADS;
+      const int i = i0 + c;
       if (i < n) prow[i] = surrogate_grad_f32((float)dp[c], slope_f);  // psi_{t0-1}
     }
   }
@@ -98,7 +146,7 @@ __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_ker
     double I[NPT];
 #pragma unroll
     for (int c = 0; c < NPT; ++c) {
-      const int i = tid + c * REC_THREADS;
+      const int i = i0 + c;
       I[c] = i < n ? __ldcs(crow + (long long)s * n + i) : 0.0;
     }
     // active list of z_{t-1} (ascending), built by warp 0 from the bitmask
@@ -135,11 +183,11 @@ __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_ker
       WT wv[GB][NPT];
 #pragma unroll
       for (int q = 0; q < GB; ++q) {
-        const long long o = (long long)(q0 + q < na ? act[q0 + q] : 0) * n;
+        if (q0 + q < na) {
+          rec_load_row<NPT, WT, VEC>(wt + (long long)act[q0 + q] * n, i0, n, wv[q]);
+        } else {
 #pragma unroll
-        for (int c = 0; c < NPT; ++c) {
-          const int i = tid + c * REC_THREADS;
-          wv[q][c] = (q0 + q < na && i < n) ? wt[o + i] : WT(0);
+          for (int c = 0; c < NPT; ++c) wv[q][c] = WT(0);
         }
       }
 #pragma unroll
@@ -149,9 +197,10 @@ __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_ker
           if (q0 + q < na) R[c] = __dadd_rn(R[c], (double)wv[q][c]);
     }
     float psi[NPT];
+    uint32_t nib = 0;
 #pragma unroll
     for (int c = 0; c < NPT; ++c) {
-      const int i = tid + c * REC_THREADS;
+      const int i = i0 + c;
       const double z_prev = rec_spike(dp[c], smooth, slope);
       a[c] = __dadd_rn(__dmul_rn(P.rho, a[c]), z_prev);
       u[c] = __dadd_rn(__dmul_rn(P.alpha, u[c]), __dadd_rn(I[c], R[c]));
@@ -164,19 +213,23 @@ __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_ker
       }
       psi[c] = surrogate_grad_f32((float)d, slope_f);
       dp[c] = d;
-      const unsigned bal = __ballot_sync(0xffffffffu, zv > 0.5 && i < n);
-      const int wi = (c * REC_THREADS + (tid & ~31)) >> 5;
-      if (lane == 0 && wi < nw) {
-        mnext[wi] = bal;
+      if (zv > 0.5 && i < n) nib |= 1u << c;
+    }
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      const uint32_t wd = rec_mask_word<NPT>(nib, lane, q);
+      const int wi = wbase + q;
+      if (lane == q && wi < nw) {
+        mnext[wi] = wd;
         if (P.pass == 0 && raster != nullptr)
-          raster[((long long)b * P.T + P.t0 + s) * nw + wi] = bal;
-        if (zrow != nullptr) zrow[(long long)(s + 1) * nw + wi] = bal;
+          raster[((long long)b * P.T + P.t0 + s) * nw + wi] = wd;
+        if (zrow != nullptr) zrow[(long long)(s + 1) * nw + wi] = wd;
       }
     }
     if (prow != nullptr) {
 #pragma unroll
       for (int c = 0; c < NPT; ++c) {
-        const int i = tid + c * REC_THREADS;
+        const int i = i0 + c;
         if (i < n) prow[(long long)(s + 1) * n + i] = psi[c];
       }
     }
@@ -184,7 +237,7 @@ __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_ker
   }
 #pragma unroll
   for (int c = 0; c < NPT; ++c) {
-    const int i = tid + c * REC_THREADS;
+    const int i = i0 + c;
     if (i < n) {
       const long long bi = (long long)b * n + i;
       u_st[bi] = u[c];
@@ -244,9 +297,15 @@ int spb_forward_rec_chunk(int pass, const double* cur, const void* wrecT, int w_
   RecParams P{B, n, Tc, KR, len, t0, T, alpha, theta, slope, beta, rho, kappa,
               reset, alif, pass, smooth, w_is_f64};
   const int npt = (n + REC_THREADS - 1) / REC_THREADS;
-#define SPB_REC(NPT, WT)                                                                  \
-  forward_rec_kernel<NPT, WT><<<B, REC_THREADS, 0, stream>>>(P, cur, wrecT, u, a, zbar, zsum, \
-                                                             raster, psi_scratch, zchunk)
+#define SPB_REC(NPT, WT)                                                                    \
+  do {                                                                                      \
+    if (n % NPT == 0)                                                                       \
+      forward_rec_kernel<NPT, WT, true><<<B, REC_THREADS, 0, stream>>>(                     \
+          P, cur, wrecT, u, a, zbar, zsum, raster, psi_scratch, zchunk);                    \
+    else                                                                                    \
+      forward_rec_kernel<NPT, WT, false><<<B, REC_THREADS, 0, stream>>>(                    \
+          P, cur, wrecT, u, a, zbar, zsum, raster, psi_scratch, zchunk);                    \
+  } while (0)
   if (w_is_f64) {
     if (npt <= 1) SPB_REC(1, double);
     else if (npt <= 2) SPB_REC(2, double);
