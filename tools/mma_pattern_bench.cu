@@ -6,6 +6,7 @@
 //           barrier the MMA thread waits on (the K2 ring without TMA), depth 5
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_pattern_bench tools/mma_pattern_bench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -41,12 +42,12 @@ __global__ void __launch_bounds__(320, 1) bench(int mode, int stages_total, unsi
   const int tid = threadIdx.x;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
   // fill = 1: pseudo-random operand bytes (tensor-core power depends on the data)
-  for (int i = tid; i < 180 * 1024; i += blockDim.x)
+  for (int i = tid; i < 224 * 1024; i += blockDim.x)
     base[i] = fill ? (uint8_t)((i * 2654435761u) >> 13) : 0;
   if (tid == 0) {
     for (int s = 0; s < XS; ++s) { mbar_init(su32(&full[s]), 1); mbar_init(su32(&empty[s]), 1); }
     mbar_init(su32(&done), 1);
-    for (int a = 0; a < 2; ++a) { mbar_init(su32(&tfull[a]), 1); mbar_init(su32(&tempty[a]), mode == 7 ? 8 : 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(su32(&tfull[a]), 1); mbar_init(su32(&tempty[a]), mode >= 7 ? 8 : 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid < 32) {
@@ -58,7 +59,10 @@ __global__ void __launch_bounds__(320, 1) bench(int mode, int stages_total, unsi
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = slot;
   const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  const uint32_t xa0 = su32(base), wa0 = su32(base + XS * 16384);
+  // mode 9: K2's shared-memory layout -- six 192-row weight blocks (144 KB) first, the
+  // five 16 KB spike stages after them
+  const uint32_t xa0 = mode == 9 ? su32(base + 6 * 24576) : su32(base);
+  const uint32_t wa0 = mode == 9 ? su32(base) : su32(base + XS * 16384);
   if (mode == 4 && tid < 32) {
     // warp-converged issue: every lane runs the loop, one elected lane issues (no R2UR /
     // divergent-uniform loop around each tcgen05.mma)
@@ -114,8 +118,22 @@ __global__ void __launch_bounds__(320, 1) bench(int mode, int stages_total, unsi
         const int s = it % XS;
         mbar_wait(su32(&full[s]), (it / XS) & 1);
         const uint32_t xa = xa0 + s * 16384;
-        const uint32_t wa = wa0 + kb * (N * 128) % (4 * N * 128);
+        const uint32_t wa = mode == 9 ? wa0 + kb * (N * 128) : wa0 + kb * (N * 128) % (4 * N * 128);
         const int nk = kb < 5 ? 4 : 2;
+        if (mode >= 8 && nk == 4) {   // K2's pattern: the 4 MMAs of a K block under one elect
+          const uint64_t a0 = desc_k_sw128(xa), b0 = desc_k_sw128(wa);
+          asm volatile(
+              "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+              "setp.ne.b32 p, %4, 0;\n\t"
+              "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+              "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+              "elect.sync _|e, 0xffffffff;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, 1;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a2, b2, %3, 1;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %3, 1;\n\t}" ::"r"(tmem + a * 256),
+              "l"(a0), "l"(b0), "r"(idesc), "r"(kb));
+        } else
         for (int kk = 0; kk < nk; ++kk) {
           asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                        "elect.sync _|e, 0xffffffff;\n\t"
@@ -130,7 +148,7 @@ __global__ void __launch_bounds__(320, 1) bench(int mode, int stages_total, unsi
     }
     mbar_wait(su32(&tfull[(tiles - 1) & 1]), ((tiles - 1) >> 1) & 1);
     if (tid == 0) cyc[blockIdx.x] = clock64() - t0;
-  } else if (mode >= 6 && tid >= 64 && (mode == 7 || tid < 96)) {
+  } else if (mode >= 6 && tid >= 64 && (mode >= 7 || tid < 96)) {
     // "epilogue": wait tfull, arrive tempty (mode 6: one warp, mode 7: 8 warps like K2)
     const int tiles = stages_total / 6;
     for (int t = 0; t < tiles; ++t) {
@@ -188,10 +206,10 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   unsigned long long* d;
   cudaMalloc(&d, sms * sizeof(unsigned long long));
-  const int smem = 180 * 1024 + 1024;
+  const int smem = 224 * 1024 + 1024;
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const int stages = 4000;
-  for (int fill : {0, 1}) for (int N : {192}) for (int mode = 5; mode < 8; ++mode) {
+  const int stages = getenv("MMA_STAGES") ? atoi(getenv("MMA_STAGES")) : 4000;
+  for (int fill : {0, 1}) for (int N : {192}) for (int mode = 7; mode < 10; ++mode) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     float ms = 0;
