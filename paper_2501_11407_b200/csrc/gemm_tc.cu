@@ -238,11 +238,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(BN));
 }
 
-// 2-D bf16 K-major operand [rows][K] with a 64 x box_rows box, 128-byte swizzle.
-static bool make_map(CUtensorMap* map, const void* ptr, int K, int rows, int box_rows) {
-  return make_tmap_2d(map, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)K, (uint64_t)rows,
-                      (uint64_t)K * 2, BK, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
-}
 // 2-D bf16 MN-major operand [K][ld] (M contiguous) with 64 x 64 boxes, 128-byte swizzle.
 static bool make_map_mn(CUtensorMap* map, const void* ptr, int M, int ld, int K) {
   return make_tmap_2d(map, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)M, (uint64_t)K,
