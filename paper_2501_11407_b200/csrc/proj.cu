@@ -25,6 +25,19 @@
 #include <algorithm>
 #include <cstdlib>
 
+// K2 producer warp: SPB_K2_ELECT=1 runs the spike-stage loop on the whole (converged) warp
+// with expect_tx + TMA under elect.sync; 0 keeps it on lane 0 alone.
+#ifndef SPB_K2_ELECT
+#define SPB_K2_ELECT 1
+#endif
+#if SPB_K2_ELECT
+#define SPB_K2_PRODUCER_LANES true
+#define SPB_K2_LANE0 (lane == 0)
+#else
+#define SPB_K2_PRODUCER_LANES (lane == 0)
+#define SPB_K2_LANE0 true
+#endif
+
 namespace spb {
 namespace proj {
 
@@ -457,25 +470,41 @@ __global__ void __launch_bounds__(THREADS, 1)
   pdl_enter();  // the prologue above touches only shared memory, TMEM and the params
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (SPB_K2_PRODUCER_LANES) {
       int s = 0, ph = 0, cur_nt = -1, wl = 0, nt, mt;
       TileWalk tw(m_tiles, n_tiles, nbands, blockIdx.x, gridDim.x);
       while (tw.next(nt, mt)) {
         if (nt != cur_nt) {  // (re)load this neuron tile's weight slices, all K blocks
           mbar_wait(smem_u32(wempty), (wl & 1) ^ 1);
           const uint32_t fb = smem_u32(wfull);
-          mbar_expect_tx(fb, (nkb + tail) * C::WBLK);
-          for (int kb = 0; kb < nkb + tail; ++kb)
+          if (SPB_K2_LANE0) {
+            mbar_expect_tx(fb, (nkb + tail) * C::WBLK);
+            for (int kb = 0; kb < nkb + tail; ++kb)
 #pragma unroll
-            for (int p = 0; p < P; ++p)
-              tma_load_2d(smem_u32(wsm + kb * C::WBLK + p * NT * BK), &tm_w, fb, kb * BK,
-                          p * n_pad32 + nt * NT);
+              for (int p = 0; p < P; ++p)
+                tma_load_2d(smem_u32(wsm + kb * C::WBLK + p * NT * BK), &tm_w, fb, kb * BK,
+                            p * n_pad32 + nt * NT);
+          }
+#if SPB_K2_ELECT
+          __syncwarp();
+#endif
           cur_nt = nt;
           ++wl;
         }
         for (int kb = 0; kb < nkb + tail; ++kb) {  // stage s, ring phase ph (incremental)
           mbar_wait(smem_u32(&xempty[s]), ph ^ 1);
           const uint32_t fb = smem_u32(&xfull[s]);
+#if SPB_K2_ELECT
+          if (probe & 2) {
+            if (lane == 0)
+              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
+          } else if (kb < nkb) {
+            tma_load_2d_elect(smem_u32(xsm + s * TILE_A), &tm_x, fb, kb * BK, mt * BM, TILE_A);
+          } else {
+            tma_load_2d_elect(smem_u32(xsm + s * TILE_A), &tm_xt, fb, nkb * BK, mt * BM,
+                              TILE_A / 2);
+          }
+#else
           if (probe & 2) {  // profiling probe: no spike-operand traffic
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
           } else if (kb < nkb) {
@@ -485,6 +514,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_expect_tx(fb, TILE_A / 2);
             tma_load_2d(smem_u32(xsm + s * TILE_A), &tm_xt, fb, nkb * BK, mt * BM);
           }
+#endif
           if (++s == XS) {
             s = 0;
             ph ^= 1;

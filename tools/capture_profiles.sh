@@ -19,6 +19,7 @@ timeout 300 python bench.py --recurrent --no-cpu --steps 5 > $O/bench_c3_recurre
 timeout 300 python tools/proj_probe.py > $O/proj_probe.txt 2>&1
 timeout 300 python tools/k2_bands.py 1,2,3,4,6,8 8 > $O/k2_bands_c3.txt 2>&1
 timeout 300 python tools/dropin_profile.py > $O/dropin_profile.txt 2>&1
+timeout 300 python tools/step_timeline.py --out $O/step_timeline_c3.json > $O/step_timeline_c3.txt 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $O/launches_c3.csv python bench.py --steps 2 --warmup 3 --profile > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \

@@ -8,7 +8,7 @@ S=gpurun_out/$TAG
 D=profiles/$TAG
 mkdir -p $D
 cp $S/gpu.txt $S/bench_*.json $S/mem_sweep_c5.jsonl $S/c5_sweep.jsonl $S/tc_sweep_*.jsonl $D/ 2>/dev/null
-cp $S/mma_microbench.txt $S/mma_pattern_bench.txt $S/proj_probe.txt $S/k2_bands_c3.txt $S/dropin_profile.txt $D/ 2>/dev/null
+cp $S/mma_microbench.txt $S/mma_pattern_bench.txt $S/proj_probe.txt $S/k2_bands_c3.txt $S/dropin_profile.txt $S/step_timeline_c3.txt $D/ 2>/dev/null
 for f in $S/launches_*.csv; do
   b=$(basename $f .csv)
   cp $f $D/
