@@ -123,6 +123,14 @@ __device__ __forceinline__ void commit(uint32_t bar) {
                    bar)
                : "memory");
 }
+// commit arriving on the barrier at this offset in every CTA of the cluster in mask
+__device__ __forceinline__ void commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster"
+               ".multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(bar),
+               "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -413,7 +421,11 @@ struct ResCfg {
   static constexpr int SMEM = W_BYTES + XS * TILE_A + 1024 + 256;
 };
 
-template <int P, int XS, bool BIN>
+// MC: launched as clusters of 2 CTAs working on neuron tiles 2j and 2j + 1 of the same
+// spike tiles; each CTA loads one half (64 rows) of every spike stage and multicasts it
+// to both, so the spike operand leaves L2 once per neuron-tile pair (tm_x / tm_xt then
+// have 64-row boxes) and a stage is refilled once both CTAs' MMAs released it.
+template <int P, int XS, bool BIN, bool MC = false>
 __global__ void __launch_bounds__(THREADS, 1)
     input_proj_wres_kernel(const __grid_constant__ CUtensorMap tm_x,
                            const __grid_constant__ CUtensorMap tm_w,
@@ -441,11 +453,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int m_tiles = (M + BM - 1) / BM;
   const int n_tiles = (n + NT - 1) / NT;
   const int nbands = max(1, min(bands, m_tiles));
+  // the tile walk: over neuron-tile pairs per cluster (MC), else over neuron tiles per CTA
+  const int rank = MC ? (int)cluster_rank() : 0;
+  const int w_nt = MC ? n_tiles >> 1 : n_tiles;
+  const int w_cta = MC ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int w_n = MC ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < XS; ++s) {
       mbar_init(smem_u32(&xfull[s]), 1);
-      mbar_init(smem_u32(&xempty[s]), 1);
+      mbar_init(smem_u32(&xempty[s]), MC ? 2 : 1);  // MC: both CTAs' MMAs release a stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&tfull[a]), 1);
@@ -465,6 +482,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if constexpr (MC) cluster_sync_all();  // the peer's barriers exist before any multicast
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
   pdl_enter();  // the prologue above touches only shared memory, TMEM and the params
@@ -472,8 +490,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     if (SPB_K2_PRODUCER_LANES) {
       int s = 0, ph = 0, cur_nt = -1, wl = 0, nt, mt;
-      TileWalk tw(m_tiles, n_tiles, nbands, blockIdx.x, gridDim.x);
+      TileWalk tw(m_tiles, w_nt, nbands, w_cta, w_n);
       while (tw.next(nt, mt)) {
+        if (MC) nt = 2 * nt + rank;
         if (nt != cur_nt) {  // (re)load this neuron tile's weight slices, all K blocks
           mbar_wait(smem_u32(wempty), (wl & 1) ^ 1);
           const uint32_t fb = smem_u32(wfull);
@@ -492,12 +511,21 @@ __global__ void __launch_bounds__(THREADS, 1)
           ++wl;
         }
         for (int kb = 0; kb < nkb + tail; ++kb) {  // stage s, ring phase ph (incremental)
-          mbar_wait(smem_u32(&xempty[s]), ph ^ 1);
+          if (MC)  // released by both CTAs' MMAs (the peer's commit is a remote arrive)
+            mbar_wait_cluster(smem_u32(&xempty[s]), ph ^ 1);
+          else
+            mbar_wait(smem_u32(&xempty[s]), ph ^ 1);
           const uint32_t fb = smem_u32(&xfull[s]);
 #if SPB_K2_ELECT
           if (probe & 2) {
             if (lane == 0)
               asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
+          } else if (MC) {  // this CTA's 64 rows of the stage, into both CTAs
+            const bool full = kb < nkb;
+            const uint32_t half = full ? TILE_A / 2 : TILE_A / 4;
+            tma_load_2d_mc_elect(smem_u32(xsm + s * TILE_A) + rank * half, full ? &tm_x : &tm_xt,
+                                 fb, kb * BK, mt * BM + rank * (BM / 2),
+                                 full ? TILE_A : TILE_A / 2, (uint16_t)3);
           } else if (kb < nkb) {
             tma_load_2d_elect(smem_u32(xsm + s * TILE_A), &tm_x, fb, kb * BK, mt * BM, TILE_A);
           } else {
@@ -530,10 +558,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
       }
       int s = 0, ph = 0, lt = 0, cur_nt = -1, wl = 0, nt, mt, nnt, nmt;
-      TileWalk tw(m_tiles, n_tiles, nbands, blockIdx.x, gridDim.x);
+      TileWalk tw(m_tiles, w_nt, nbands, w_cta, w_n);
       bool have = tw.next(nt, mt);
       while (have) {
         const bool more = tw.next(nnt, nmt);  // one tile ahead: the weight region's last use
+        // (the walk's neuron index is a pair index under MC: equality tests are unchanged)
         if (nt != cur_nt) {
           mbar_wait(smem_u32(wfull), wl & 1);
           cur_nt = nt;
@@ -551,7 +580,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           static_assert(BK / 32 == 4, "four K steps per block");
           if (!(probe & 8))  // profiling probe: no MMAs (the epilogue alone)
             mma_i8_x4(dacc, desc_k_sw128(xa), desc_k_sw128(wa), Cfg<P>::IDESC, kb ? 1u : 0u);
-          commit(smem_u32(&xempty[s]));
+          if (MC)
+            commit_mc(smem_u32(&xempty[s]), 3);
+          else
+            commit(smem_u32(&xempty[s]));
           if (++s == XS) {
             s = 0;
             ph ^= 1;
@@ -563,7 +595,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (!(probe & 8))
             mma_i8_x2(dacc, desc_k_sw64(smem_u32(xsm + s * TILE_A)),
                       desc_k_sw128(smem_u32(wsm + nkb * C::WBLK)), Cfg<P>::IDESC, nkb ? 1u : 0u);
-          commit(smem_u32(&xempty[s]));
+          if (MC)
+            commit_mc(smem_u32(&xempty[s]), 3);
+          else
+            commit(smem_u32(&xempty[s]));
           if (++s == XS) {
             s = 0;
             ph ^= 1;
@@ -599,8 +634,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int ns0 = FAST ? 4 * (lane & 3) : 0;
     int nt, mt, sc_nt = -1;
     double sc[NS];
-    TileWalk tw(m_tiles, n_tiles, nbands, blockIdx.x, gridDim.x);
+    TileWalk tw(m_tiles, w_nt, nbands, w_cta, w_n);
     for (; tw.next(nt, mt); ++lt) {
+      if (MC) nt = 2 * nt + rank;
       const int a = lt & 1;
       const int i0 = nt * NT + hh * NH;
       if (nt != sc_nt) {
@@ -630,6 +666,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  // MC: the peer's last multicast writes and stage releases target this CTA's shared
+  // memory; neither CTA leaves before both are done
+  if constexpr (MC) cluster_sync_all();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
 }
@@ -782,6 +821,9 @@ __global__ void __launch_bounds__(256) pack_bytes4_kernel(const uint8_t* __restr
   pdl_enter();
   pdl_trigger();
   const int wpr = Kpad >> 2;  // output words per row
+  // 8-column groups up to the last input column; the pad past it is never written and
+  // stays zero from the buffers' allocation (C3: 704 of 768 columns, 12 MB less per update)
+  const int wl = min(wpr >> 1, (k + 7) >> 3);
   const int rows = B * Tc;
   constexpr int R = PACK_R;   // rows per iteration, their loads issued together
   // grid-stride over row groups (a persistent-size grid instead of one tiny CTA per group)
@@ -794,7 +836,7 @@ __global__ void __launch_bounds__(256) pack_bytes4_kernel(const uint8_t* __restr
       bq[q] = tmajor ? row % B : row / Tc;
     }
     // thread per 8 channels: two 32-bit loads, one 8-byte xq store, one 16-byte xh store
-    for (int w2 = threadIdx.x; 2 * w2 < wpr; w2 += blockDim.x) {
+    for (int w2 = threadIdx.x; w2 < wl; w2 += blockDim.x) {
       const int w = 2 * w2;
       uint32_t v[R][2];
 #pragma unroll
@@ -835,6 +877,9 @@ __global__ void __launch_bounds__(128) pack_bits8_kernel(const uint8_t* __restri
   pdl_trigger();
   const int kb = (k + 7) >> 3;   // input bytes per row
   const int wpr = Kpad >> 3;     // output 8-byte words per row
+  // columns past the last input byte are never written: they stay zero from the buffers'
+  // allocation (no packer writes them), so the pad is not rewritten every update
+  const int wl = min(wpr, kb);
   const int rows = B * Tc;
   constexpr int R = 4;
   // grid-stride over row groups (as pack_bytes4_kernel)
@@ -846,7 +891,7 @@ __global__ void __launch_bounds__(128) pack_bits8_kernel(const uint8_t* __restri
       sq[q] = tmajor ? row / B : row % Tc;
       bq[q] = tmajor ? row % B : row / Tc;
     }
-    for (int w = threadIdx.x; w < wpr; w += blockDim.x) {
+    for (int w = threadIdx.x; w < wl; w += blockDim.x) {
       uint32_t v[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
@@ -1088,6 +1133,41 @@ static bool k2_tail() {
   const char* e = getenv("SPB_K2_TAIL");
   return !(e && e[0] == '0');
 }
+// SPB_K2_MC=1: CTA pairs multicasting the spike stages (bitwise equal; measured no faster
+// at C3 -- 0.2218 vs 0.2184 ms, DESIGN.md §6 -- so the single-CTA kernel is the default)
+static bool k2_mc() {
+  const char* e = getenv("SPB_K2_MC");
+  return e && e[0] == '1';
+}
+}  // extern "C" (the launcher below is a template)
+// the W-resident projection launch: PDL, and clusters of 2 for the multicast variant
+template <typename... K, typename... A>
+static cudaError_t launch_wres(void (*kernel)(K...), int grid, size_t smem, cudaStream_t stream,
+                               bool mc, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(proj::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (mc) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<A&&>(args)...);
+}
+extern "C" {
 
 
 
@@ -1127,8 +1207,28 @@ int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, i
     set_error("spb_input_proj: cuTensorMapEncodeTiled (tail) failed");
     return 3;
   }
+  // spike multicast across CTA pairs (P = 6): neuron tiles in pairs, an even grid
+  const int n_tiles = ceil_div(n, proj::NT);
+  const bool mc = P == 6 && nkb <= proj::ResCfg<6, 5>::MAXKB && k2_mc() && n_tiles % 2 == 0 &&
+                  grid >= 2;
   if (nkb <= proj::ResCfg<7, 3>::MAXKB) {  // weights of a neuron tile fit in shared memory
-    if (P == 6) {
+    if (P == 6 && mc) {
+      const int g2 = grid & ~1;
+      CUtensorMap hx, hxt;  // 64-row boxes: each CTA of a pair loads one half of a stage
+      if (!make_tmap_2d(&hx, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, Kpad, M, Kpad, proj::BK,
+                        proj::BM / 2, CU_TENSOR_MAP_SWIZZLE_128B) ||
+          !make_tmap_2d(&hxt, xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, Kpad, M, Kpad, proj::BK / 2,
+                        proj::BM / 2, CU_TENSOR_MAP_SWIZZLE_64B)) {
+        set_error("spb_input_proj: cuTensorMapEncodeTiled (multicast halves) failed");
+        return 3;
+      }
+      auto kfn = bin ? proj::input_proj_wres_kernel<6, 5, true, true>
+                     : proj::input_proj_wres_kernel<6, 5, false, true>;
+      constexpr int sm = proj::ResCfg<6, 5>::SMEM;
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      launch_wres(kfn, g2, sm, stream, true, hx, mw, hxt, sexp, out, M, n, n_pad32, nkb_res,
+                  tail, probe, k2_bands(tiles, g2));
+    } else if (P == 6) {
       auto kfn = bin ? proj::input_proj_wres_kernel<6, 5, true> : proj::input_proj_wres_kernel<6, 5, false>;
       constexpr int sm = proj::ResCfg<6, 5>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);

@@ -48,6 +48,20 @@ __device__ __forceinline__ void tma_load_2d_elect(uint32_t dst, const CUtensorMa
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "r"(bytes)
       : "memory");
 }
+// As tma_load_2d_elect, the box multicast to the CTAs of the cluster in ctaMask (same
+// shared-memory offset and barrier offset in each): every destination's barrier receives
+// the box's bytes as complete_tx; expect_tx is armed on this CTA's barrier only.
+__device__ __forceinline__ void tma_load_2d_mc_elect(uint32_t dst, const CUtensorMap* map,
+                                                     uint32_t bar, int c0, int c1,
+                                                     uint32_t bytes, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%4], %5;\n\t"
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %6;\n\t}" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "r"(bytes), "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

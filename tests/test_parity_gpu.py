@@ -288,6 +288,46 @@ def test_projection_banded_walk_is_bitwise_the_plain_walk(B, T, n, k, binary, mo
         assert np.array_equal(cur.view(np.int64), out["1"].view(np.int64)), bands
 
 
+@pytest.mark.parametrize("B,T,n,k,binary", [(40, 250, 1024, 700, True), (64, 250, 2048, 130, True),
+                                              (5, 120, 96, 700, False), (2, 50, 64, 700, True),
+                                              (3, 100, 128, 700, False), (1, 20, 64, 64, True)])
+def test_projection_pair_multicast_is_bitwise_single_cta(B, T, n, k, binary, monkeypatch):
+    """K2 on CTA pairs (each loads half of every spike stage and multicasts it to both;
+    a stage is refilled once both CTAs' MMAs released it) gives the single-CTA kernel's
+    currents bit for bit -- also with a single cluster, fewer pair tiles than clusters,
+    odd band counts, and an odd neuron-tile count (which takes the single-CTA kernel)."""
+    _need_gpu()
+    import ctypes
+    from paper_2501_11407_b200.engine import EpropEngine
+    rng = np.random.default_rng(7 * n + k)
+    w = (rng.uniform(-1, 1, (n, k)) / np.sqrt(k)).astype(np.float32)
+    x = (rng.random((B, T, k)) < 0.1).astype(np.uint8)
+    if not binary:
+        x[0, :, :5] = 3
+    eng = EpropEngine(n, k, 3, B, alif=False, w_f64=False, chunk=255 if T < 256 else 511)
+    eng.set_weights(torch.from_numpy(w), torch.zeros((3, n), dtype=torch.float64))
+    xd = torch.from_numpy(x).cuda()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    eng._pack(xd.data_ptr(), T * k, False, T, st)
+    out = {}
+    for mc, bands in (("0", None), ("1", None), ("1", "1"), ("1", "3"), ("1", "1000")):
+        monkeypatch.setenv("SPB_K2_MC", mc)
+        if bands is None:
+            monkeypatch.delenv("SPB_K2_BANDS", raising=False)
+        else:
+            monkeypatch.setenv("SPB_K2_BANDS", bands)
+        eng.cur.fill_(float("nan"))
+        eng._project(T, st, binary=binary)
+        torch.cuda.synchronize()
+        out[(mc, bands)] = eng.cur.cpu().numpy().reshape(B, eng.KR, n)[:, :T].copy()
+    ref = out[("0", None)]
+    assert np.isfinite(ref).all()
+    for key, cur in out.items():
+        assert np.array_equal(cur.view(np.int64), ref.view(np.int64)), key
+    exact = np.einsum("btk,nk->btn", x.astype(np.longdouble), w.astype(np.longdouble))
+    assert np.max(np.abs(ref - exact.astype(np.float64))) <= 2.3e-16 * np.max(np.abs(exact))
+
+
 def test_label_out_of_range_raises():
     _need_gpu()
     import paper_2501_11407_b200 as P
