@@ -656,9 +656,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         continue;
       }
       const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH);
-      if constexpr (FAST)
-        proj_epilogue_p6bin(tb, sc, out, M, n, mt * BM + q * 32, i0, smem_u32(&tempty[a]), lane,
-                            probe);
+      if constexpr (FAST) {
+        if (probe & 64)  // profiling probe: tile-contiguous output blocks (32 KB per tile)
+          proj_epilogue_p6bin(tb, sc, out + (long long)(mt * n_tiles + nt) * (BM * NT), BM, NT,
+                              q * 32, hh * NH, smem_u32(&tempty[a]), lane, probe);
+        else
+          proj_epilogue_p6bin(tb, sc, out, M, n, mt * BM + q * 32, i0, smem_u32(&tempty[a]),
+                              lane, probe);
+      }
       else
         proj_epilogue_tile<P, BIN>(tb, sc, out, M, n, mt * BM + q * 32 + lane, i0,
                                    smem_u32(&tempty[a]), lane, probe);
@@ -1172,7 +1177,8 @@ extern "C" {
 
 
 // spb_input_proj with a profiling probe for the W-resident kernel: bit 0 skips the
-// epilogue, bit 1 the spike-operand loads, bit 2 the current stores, bit 3 the MMAs
+// epilogue, bit 1 the spike-operand loads, bit 2 the current stores, bit 3 the MMAs,
+// bit 5 records the issue loop's clock, bit 6 stores tile-contiguous blocks (layout probe)
 // (probe = 0 is the production kernel).
 int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
                          int n_pad32, int k, int Kpad, int P, double* out, int sm_count,

@@ -1,5 +1,6 @@
 """Time K2 (W-resident INT8 projection) at the C3 shape with the epilogue and/or the
-spike-operand loads switched off (spb_input_proj_probe) to locate its bottleneck."""
+spike-operand loads switched off (spb_input_proj_probe) to locate its bottleneck
+(bit 6 = 64: the stores go to tile-contiguous 32 KB blocks instead of the row layout)."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -18,7 +19,7 @@ eng.run(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
 torch.cuda.synchronize()
 v = ctypes.c_void_p
 st = v(torch.cuda.current_stream().cuda_stream)
-for binary, probe in ((1, 0), (1, 1), (1, 2), (1, 3), (1, 4), (1, 8), (1, 10), (1, 12), (1, 14), (1, 15)):
+for binary, probe in ((1, 0), (1, 64), (1, 0), (1, 64), (1, 1), (1, 2), (1, 3), (1, 4), (1, 8), (1, 10), (1, 12), (1, 14), (1, 15)):
     ts = []
     for rep in range(8):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
