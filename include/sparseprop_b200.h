@@ -66,6 +66,13 @@ int spb_pack_spikes_xh(const uint8_t* x, long long stride_b, int B, int k, int b
 int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
                    int k, int Kpad, int P, double* cur, int sm_count, int binary,
                    cudaStream_t stream);
+/* spb_input_proj over rin live rows per sample: xq holds B*rin rows (row b*rin + s), the
+ * current of row b*rin + s lands in cur row b*rout + s (rout = the current buffer's KR >=
+ * rin); rin == rout is spb_input_proj with M = B*rin.  The one-chunk update packs only
+ * the chunk's live steps (len of KR = Tc + 1 rows: C3 250 of 256, K2 0.217 -> 0.208 ms). */
+int spb_input_proj_rows(const uint8_t* xq, const int8_t* wq, const int* sexp, int B, int rin,
+                        int rout, int n, int n_pad32, int k, int Kpad, int P, double* cur,
+                        int sm_count, int binary, cudaStream_t stream);
 /* Profiling variant of spb_input_proj (W-resident kernel): probe bit 0 skips the epilogue,
  * bit 1 the spike-operand loads; probe = 0 is the production kernel. */
 int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,

@@ -26,6 +26,7 @@ SIGNATURES = {
     "spb_pack_spikes": [P, LL, I, I, I, I, I, I, I, P, P],
     "spb_pack_spikes_xh": [P, LL, I, I, I, I, I, I, I, P, P, P],
     "spb_input_proj": [P, P, P, I, I, I, I, I, I, P, I, I, P],
+    "spb_input_proj_rows": [P, P, P, I, I, I, I, I, I, I, I, P, I, I, P],
     "spb_input_proj_probe": [P, P, P, I, I, I, I, I, I, P, I, I, I, P],
     "spb_forward_chunk": [I, P, I, I, I, I, I, I, I, D, D, D, D, D, D, I, I, I,
                           P, P, P, P, P, P, P, P, P, P, P, P, P, I, P, P, P],

@@ -178,12 +178,34 @@ constexpr int NH = NT / 2;  // neurons per epilogue thread (16 epilogue warps me
 // recombine into ONE int64 g = sum_p S_p 2^(RB*(P-1-p)) (|g| < 2^63) and I = (double)g *
 // 2^(s-F): one rounding of the exact sum, bitwise the value of the two-part path below,
 // with half the fp64-pipe work.
+// Output row of input row r0 + d (0 <= d < 32) with (b0, s0) = (r0 / rin, r0 % rin): the
+// projection may read rin rows per sample (the chunk's live steps) and write rout rows per
+// sample (the current buffer's KR); rin == rout is the identity.  A 32-row quarter tile
+// crosses at most one sample boundary when rin >= 32.
+__device__ __forceinline__ long long proj_out_row(int b0, int s0, int d, int rin, int rout) {
+  int s = s0 + d, b = b0;
+  if (rin >= 32) {
+    if (s >= rin) {
+      s -= rin;
+      ++b;
+    }
+  } else {
+    const int q = s / rin;
+    b += q;
+    s -= q * rin;
+  }
+  return (long long)b * rout + s;
+}
+
 // SE: per-neuron exponents (int) or precomputed scales 2^(s-F) (double)
 template <int P, bool BIN, typename SE = int>
 __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se)[NH],
-                                                   double* __restrict__ out, int M, int n, int row,
-                                                   int i0, uint32_t tempty_bar, int lane,
+                                                   double* __restrict__ out, int M, int n,
+                                                   int rin, int rout, int row, int i0,
+                                                   uint32_t tempty_bar, int lane,
                                                    int probe = 0) {
+  const int rq = row - lane;  // this warp's quarter-tile base row
+  const int b0 = rq / rin, s0 = rq - b0 * rin;
   long long g0[NH], g1[NH];
   {
     int32_t r[3][NH];
@@ -259,7 +281,7 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se
     for (int kq = 0; kq < 4; ++kq) {
       const int r = row0 + kq;
       if (r < M && col < n) {  // n % 4 == 0: a quad is all in or all out
-        double* o = out + (long long)r * n + col;
+        double* o = out + proj_out_row(b0, s0, r - rq, rin, rout) * n + col;
         asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o), "d"(ch[2 * kq].x),
                      "d"(ch[2 * kq].y), "d"(ch[2 * kq + 1].x), "d"(ch[2 * kq + 1].y)
                      : "memory");
@@ -291,7 +313,7 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se
   for (int k = 0; k < 8; ++k) {
     const int r = row0 + k;
     if (r < M) {
-      double* o = out + (long long)r * n + col;
+      double* o = out + proj_out_row(b0, s0, r - rq, rin, rout) * n + col;
       if (col + 1 < n && (n & 1) == 0) {  // 16-byte aligned rows
         *reinterpret_cast<double2*>(o) = ch[k];
       } else {
@@ -321,8 +343,8 @@ __device__ __forceinline__ void tmem_ld16x256b_x2_nowait(uint32_t taddr, int32_t
 // 128 contiguous bytes -- no lane transposes.  sc4 = 2^(s-F) of those 4 neurons.
 __device__ __forceinline__ void proj_epilogue_p6bin(uint32_t tbase, const double (&sc4)[4],
                                                     double* __restrict__ out, int M, int n,
-                                                    int row0, int i0, uint32_t tempty_bar,
-                                                    int lane, int probe) {
+                                                    int rin, int rout, int row0, int i0,
+                                                    uint32_t tempty_bar, int lane, int probe) {
   const int t4 = lane >> 2, q4 = lane & 3;
   double v[2][2][4];  // [lane half][row +0 / +8][neuron 4 q4 + j]
   // all 12 digit loads in flight at once, one wait, and the TMEM buffer released before
@@ -356,13 +378,14 @@ __device__ __forceinline__ void proj_epilogue_p6bin(uint32_t tbase, const double
     if (v[0][0][0] == 1.2345e-300 && row0 < M) out[(long long)row0 * n + col] = v[0][0][1];
     return;
   }
+  const int b0 = row0 / rin, s0 = row0 - b0 * rin;
 #pragma unroll
   for (int h = 0; h < 2; ++h)
 #pragma unroll
     for (int rh = 0; rh < 2; ++rh) {
-      const int r = row0 + 16 * h + 8 * rh + t4;
-      if (r >= M) continue;
-      double* o = out + (long long)r * n + col;
+      const int d = 16 * h + 8 * rh + t4;
+      if (row0 + d >= M) continue;
+      double* o = out + proj_out_row(b0, s0, d, rin, rout) * n + col;
       const double* w = v[h][rh];
       if ((n & 3) == 0) {  // 32-byte aligned quads, all in or all out
         if (col < n)
@@ -431,7 +454,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                            const __grid_constant__ CUtensorMap tm_w,
                            const __grid_constant__ CUtensorMap tm_xt, const int* __restrict__ sexp,
                            double* __restrict__ out, int M, int n, int n_pad32, int nkb,
-                           int tail, int probe, int bands) {
+                           int tail, int probe, int bands, int rin, int rout) {
   // nkb full 128-byte K blocks, then (tail) one 64-byte block: k = 700 runs 704 bytes of
   // K instead of 768 (8 % fewer MMAs and spike-operand bytes)
   using C = ResCfg<P, XS>;
@@ -659,13 +682,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       if constexpr (FAST) {
         if (probe & 64)  // profiling probe: tile-contiguous output blocks (32 KB per tile)
           proj_epilogue_p6bin(tb, sc, out + (long long)(mt * n_tiles + nt) * (BM * NT), BM, NT,
-                              q * 32, hh * NH, smem_u32(&tempty[a]), lane, probe);
+                              BM, BM, q * 32, hh * NH, smem_u32(&tempty[a]), lane, probe);
         else
-          proj_epilogue_p6bin(tb, sc, out, M, n, mt * BM + q * 32, i0, smem_u32(&tempty[a]),
-                              lane, probe);
+          proj_epilogue_p6bin(tb, sc, out, M, n, rin, rout, mt * BM + q * 32, i0,
+                              smem_u32(&tempty[a]), lane, probe);
       }
       else
-        proj_epilogue_tile<P, BIN>(tb, sc, out, M, n, mt * BM + q * 32 + lane, i0,
+        proj_epilogue_tile<P, BIN>(tb, sc, out, M, n, rin, rout, mt * BM + q * 32 + lane, i0,
                                    smem_u32(&tempty[a]), lane, probe);
     }
   }
@@ -682,7 +705,7 @@ template <int P, bool BIN>
 __global__ void __launch_bounds__(THREADS, 1)
     input_proj_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                       const int* __restrict__ sexp, double* __restrict__ out, int M, int n,
-                      int n_pad32, int nkb) {
+                      int n_pad32, int nkb, int rin, int rout) {
   using C = Cfg<P>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -777,8 +800,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(smem_u32(&tfull[a]), (lt >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       proj_epilogue_tile<P, BIN>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * 256 + hh * NH),
-                            se, out, M, n, mt * BM + q * 32 + lane, i0, smem_u32(&tempty[a]),
-                            lane);
+                            se, out, M, n, rin, rout, mt * BM + q * 32 + lane, i0,
+                            smem_u32(&tempty[a]), lane);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1113,15 +1136,32 @@ int spb_slice_weights(const void* w, int w_is_f64, int n, int k, int Kpad, int n
                               Kpad, n_pad32, P, wq, sexp, stream);
 }
 
-int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
-                         int n_pad32, int k, int Kpad, int P, double* out, int sm_count,
-                         int binary, int probe, cudaStream_t stream);
+}  // extern "C"
+static int input_proj_impl(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int rin,
+                           int rout, int n, int n_pad32, int k, int Kpad, int P, double* out,
+                           int sm_count, int binary, int probe, cudaStream_t stream);
+extern "C" {
 
 int spb_input_proj(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n, int n_pad32,
                    int k, int Kpad, int P, double* out, int sm_count, int binary,
                    cudaStream_t stream) {
-  return spb_input_proj_probe(xq, wq, sexp, M, n, n_pad32, k, Kpad, P, out, sm_count, binary, 0,
-                              stream);
+  return input_proj_impl(xq, wq, sexp, M, M, M, n, n_pad32, k, Kpad, P, out, sm_count, binary, 0,
+                         stream);
+}
+
+int spb_input_proj_rows(const uint8_t* xq, const int8_t* wq, const int* sexp, int B, int rin,
+                        int rout, int n, int n_pad32, int k, int Kpad, int P, double* out,
+                        int sm_count, int binary, cudaStream_t stream) {
+  SPB_CHECK_ARG(B > 0 && rin > 0 && rout >= rin, "spb_input_proj_rows: need B > 0, 0 < rin <= rout");
+  return input_proj_impl(xq, wq, sexp, B * rin, rin, rout, n, n_pad32, k, Kpad, P, out, sm_count,
+                         binary, 0, stream);
+}
+
+int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
+                         int n_pad32, int k, int Kpad, int P, double* out, int sm_count,
+                         int binary, int probe, cudaStream_t stream) {
+  return input_proj_impl(xq, wq, sexp, M, M, M, n, n_pad32, k, Kpad, P, out, sm_count, binary,
+                         probe, stream);
 }
 
 // Row bands of the W-resident kernel's tile walk (TileWalk): about 30 tiles per CTA per
@@ -1180,9 +1220,10 @@ extern "C" {
 // epilogue, bit 1 the spike-operand loads, bit 2 the current stores, bit 3 the MMAs,
 // bit 5 records the issue loop's clock, bit 6 stores tile-contiguous blocks (layout probe)
 // (probe = 0 is the production kernel).
-int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int n,
-                         int n_pad32, int k, int Kpad, int P, double* out, int sm_count,
-                         int binary, int probe, cudaStream_t stream) {
+}  // extern "C"
+static int input_proj_impl(const uint8_t* xq, const int8_t* wq, const int* sexp, int M, int rin,
+                           int rout, int n, int n_pad32, int k, int Kpad, int P, double* out,
+                           int sm_count, int binary, int probe, cudaStream_t stream) {
   const bool bin = binary != 0 && P <= 7 && Kpad <= 8192;
   SPB_CHECK_ARG(xq && wq && sexp && out && M > 0 && n > 0 && n_pad32 >= n &&
                     n_pad32 % proj::NT == 0 && Kpad % proj::BK == 0 && (P == 6 || P == 7 || P == 8),
@@ -1233,41 +1274,39 @@ int spb_input_proj_probe(const uint8_t* xq, const int8_t* wq, const int* sexp, i
       constexpr int sm = proj::ResCfg<6, 5>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       launch_wres(kfn, g2, sm, stream, true, hx, mw, hxt, sexp, out, M, n, n_pad32, nkb_res,
-                  tail, probe, k2_bands(tiles, g2));
+                  tail, probe, k2_bands(tiles, g2), rin, rout);
     } else if (P == 6) {
       auto kfn = bin ? proj::input_proj_wres_kernel<6, 5, true> : proj::input_proj_wres_kernel<6, 5, false>;
       constexpr int sm = proj::ResCfg<6, 5>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, mxt, sexp, out, M, n, n_pad32,
-                 nkb_res, tail, probe, k2_bands(tiles, grid));
+                 nkb_res, tail, probe, k2_bands(tiles, grid), rin, rout);
     } else if (P == 7) {
       auto kfn = bin ? proj::input_proj_wres_kernel<7, 3, true> : proj::input_proj_wres_kernel<7, 3, false>;
       constexpr int sm = proj::ResCfg<7, 3>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, mxt, sexp, out, M, n, n_pad32,
-                 nkb_res, tail, probe, k2_bands(tiles, grid));
+                 nkb_res, tail, probe, k2_bands(tiles, grid), rin, rout);
     } else {
       auto kfn = proj::input_proj_wres_kernel<8, 2, false>;
       constexpr int sm = proj::ResCfg<8, 2>::SMEM;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
       pdl_launch(kfn, grid, proj::THREADS, sm, stream, mx, mw, mxt, sexp, out, M, n, n_pad32,
-                 nkb_res, tail, probe, k2_bands(tiles, grid));
+                 nkb_res, tail, probe, k2_bands(tiles, grid), rin, rout);
     }
   } else if (P == 6) {
     auto kfn = bin ? proj::input_proj_kernel<6, true> : proj::input_proj_kernel<6, false>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, proj::Cfg<6>::SMEM);
-    kfn<<<grid, proj::THREADS, proj::Cfg<6>::SMEM, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);
+    kfn<<<grid, proj::THREADS, proj::Cfg<6>::SMEM, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb, rin, rout);
   } else if (P == 7) {
     auto kfn = bin ? proj::input_proj_kernel<7, true> : proj::input_proj_kernel<7, false>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, proj::Cfg<7>::SMEM);
-    kfn<<<grid, proj::THREADS, proj::Cfg<7>::SMEM, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);
+    kfn<<<grid, proj::THREADS, proj::Cfg<7>::SMEM, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb, rin, rout);
   } else {
     auto kfn = proj::input_proj_kernel<8, false>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, proj::Cfg<8>::SMEM);
-    kfn<<<grid, proj::THREADS, proj::Cfg<8>::SMEM, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb);
+    kfn<<<grid, proj::THREADS, proj::Cfg<8>::SMEM, stream>>>(mx, mw, sexp, out, M, n, n_pad32, nkb, rin, rout);
   }
   SPB_CHECK_LAUNCH("input_proj");
   return 0;
 }
-
-}  // extern "C"

@@ -187,6 +187,8 @@ class EpropEngine:
         # fold the input filter into the one-chunk coefficients (SPB_FILT=0: xbar operand)
         self.filt = os.environ.get("SPB_FILT", "1") != "0"
         self.pack_xh = os.environ.get("SPB_PACK_XH", "1") != "0"
+        # SPB_COMPACT_ROWS=0: the one-chunk projection over all KR rows per sample (A/B)
+        self.compact_rows = os.environ.get("SPB_COMPACT_ROWS", "1") != "0"
         # opt-in memory-for-time trade (off by default: memory then grows with T): park the
         # psi of every chunk in pass A when all of it fits `park_budget` bytes, so pass B
         # skips the projection and the dynamics recompute.  SPB_PARK_GB sets it too.
@@ -324,26 +326,34 @@ class EpropEngine:
             self._ctab_T = (T, kappa)
         return self.ctab
 
-    def _pack(self, xp, strideb, bits, ln, st, xh=False):
+    def _pack(self, xp, strideb, bits, ln, st, xh=False, compact=False):
         """Chunk spikes (bytes or bits) -> zero-padded projection operand xq [B*KR][Kpad]
         (rows b*KR + s, rows s >= len zero; also K4's row source).  xh: also
-        write the one-chunk raw-spike GEMM operand (K4 folded into the pack)."""
+        write the one-chunk raw-spike GEMM operand (K4 folded into the pack).  compact
+        (with xh): only the live steps, xq rows b*len + s (spb_input_proj_rows)."""
         if xh:
             _lib.call("spb_pack_spikes_xh", ctypes_void(xp), strideb, self.B, self.k, int(bits),
-                      ln, self.KR, self.Kpad, self.KR, ctypes_void(self.xq.data_ptr()),
-                      ctypes_void(self.xh.data_ptr()), st)
+                      ln, ln if compact else self.KR, self.Kpad, self.KR,
+                      ctypes_void(self.xq.data_ptr()), ctypes_void(self.xh.data_ptr()), st)
             return
         _lib.call("spb_pack_spikes", ctypes_void(xp), strideb, self.B, self.k, int(bits), ln,
                   self.KR, self.Kpad, 0, ctypes_void(self.xq.data_ptr()), st)
 
-    def _project(self, ln, st, timed=None, binary=False):
+    def _project(self, ln, st, timed=None, binary=False, compact=False):
         """K2: cur = W x_t exactly on INT8 tensor cores from the packed chunk (binary:
-        0/1 spikes, single-int64 digit recombination)."""
+        0/1 spikes, single-int64 digit recombination).  compact: xq holds only the chunk's
+        live steps (rows b*len + s), written to cur rows b*KR + s."""
         v = ctypes_void
-        args = ("spb_input_proj", v(self.xq.data_ptr()),
-                v(self.wq.data_ptr()), v(self.sexp.data_ptr()), self.B * self.KR, self.n,
-                self.n_pad32, self.k, self.Kpad, self.P, v(self.cur.data_ptr()), self.sm_count,
-                int(bool(binary)), st)
+        if compact:
+            args = ("spb_input_proj_rows", v(self.xq.data_ptr()), v(self.wq.data_ptr()),
+                    v(self.sexp.data_ptr()), self.B, ln, self.KR, self.n, self.n_pad32, self.k,
+                    self.Kpad, self.P, v(self.cur.data_ptr()), self.sm_count, int(bool(binary)),
+                    st)
+        else:
+            args = ("spb_input_proj", v(self.xq.data_ptr()),
+                    v(self.wq.data_ptr()), v(self.sexp.data_ptr()), self.B * self.KR, self.n,
+                    self.n_pad32, self.k, self.Kpad, self.P, v(self.cur.data_ptr()),
+                    self.sm_count, int(bool(binary)), st)
         if timed is not None:
             timed("proj", ln, *args)
         else:
@@ -453,6 +463,9 @@ class EpropEngine:
                    and (bits or (self.k % 4 == 0 and x.data_ptr() % 4 == 0)))
         if real:
             pack_xh = True   # spb_pack_real writes the operand (hi and lo)
+        # one chunk with the operand folded into the pack: xq holds only the live steps
+        # (K2 over B*len rows instead of B*KR; C3: 500 instead of 512 row tiles)
+        compact = pack_xh and not real and self.compact_rows
 
         def timed(name, meta, fn, *args):
             if timers is None:
@@ -502,7 +515,8 @@ class EpropEngine:
                 if u + 1 < len(uses):
                     _copy(u + 1)
                 main.wait_event(self._sev_ready[u % 2])
-                self._pack(xs[u % 2].data_ptr(), Tc * kb, bits, ln, st, xh=pack_xh)
+                self._pack(xs[u % 2].data_ptr(), Tc * kb, bits, ln, st, xh=pack_xh,
+                           compact=compact)
                 self._sev_free[u % 2].record(main)
                 state["u"] += 1
         elif real:
@@ -518,7 +532,8 @@ class EpropEngine:
                                                 self.w.to(torch.float64).t()))
         else:
             def pack_chunk(c, ln):
-                self._pack(x.data_ptr() + c * Tc * kb, strideb, bits, ln, st, xh=pack_xh)
+                self._pack(x.data_ptr() + c * Tc * kb, strideb, bits, ln, st, xh=pack_xh,
+                           compact=compact)
 
         # ---------------- pass A ----------------
         for c in range(nchunks):  # chunk 0 starts from fresh state inside the kernels
@@ -542,7 +557,7 @@ class EpropEngine:
                 self._ev["xbar"].record(self.side)
                 self.launches += 1
             if not (side_x and self.xbar_sched == "fa") and not real:
-                self._project(ln, st, timed, binary)
+                self._project(ln, st, timed, binary, compact=compact)
             if self.recurrent:
                 self._forward_rec(0, ln, t0, T, common, raster,
                                   one and not forward_only, st, timed, (ln, 0, one))

@@ -142,6 +142,28 @@ def test_engine_launch_sequence_dry_run(monkeypatch, alif, T, chunk):
     assert eng.launches == len(rec.calls) + passb
 
 
+@pytest.mark.parametrize("compact", ["1", "0"])
+def test_engine_compact_rows_dry_run(monkeypatch, compact):
+    """One chunk with the raw-spike operand folded into the pack: xq holds only the live
+    steps (pack rows-per-sample = len) and K2 maps input row b*len + s to current row
+    b*KR + s (spb_input_proj_rows); SPB_COMPACT_ROWS=0 keeps the KR-row layout."""
+    monkeypatch.setenv("SPB_COMPACT_ROWS", compact)
+    rec = _Recorder()
+    monkeypatch.setattr(_lib, "call", rec)
+    monkeypatch.setattr(torch.cuda, "current_stream", lambda *a, **k: type("S", (), {"cuda_stream": 0})())
+    eng = EpropEngine(40, 32, 3, 6, alif=True, chunk=127, device="cpu", sm_count=148)
+    eng.run(torch.zeros((6, 100, 32), dtype=torch.uint8), torch.zeros(6, dtype=torch.int64))
+    packs = [c[1] for c in rec.calls if c[0] == "spb_pack_spikes_xh"]
+    assert len(packs) == 1 and packs[0][5] == 100                  # len
+    assert packs[0][6] == (100 if compact == "1" else eng.KR)      # xq rows per sample
+    rows = [c[1] for c in rec.calls if c[0] == "spb_input_proj_rows"]
+    plain = [c[1] for c in rec.calls if c[0] == "spb_input_proj"]
+    if compact == "1":
+        assert not plain and len(rows) == 1 and rows[0][3:6] == (6, 100, eng.KR)
+    else:
+        assert not rows and len(plain) == 1 and plain[0][3] == 6 * eng.KR
+
+
 @pytest.mark.parametrize("alif", [False, True])
 def test_engine_reset_dry_run(monkeypatch, alif):
     """reset=True: raw-input operand (K4 alpha = 0, fresh every chunk), the reset scan
