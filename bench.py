@@ -152,6 +152,12 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+# SPB_WOUT_SIDE=1: the W_out update after K7 on the engine's side stream, beside K5 (A/B,
+# tools/wout_side_ab.sh): 2.5 us less device time per update (0.6028 vs 0.6056 ms) but a
+# slower e2e loop (97.8 vs 101.8 M), so the default keeps it on the main stream
+WOUT_SIDE = os.environ.get("SPB_WOUT_SIDE", "0") == "1"
+
+
 def parity_block(eng, net, x_np, y_np, kw, kind, recurrent=False):
     """One update of the timed configuration (the same engine, inputs and initial
     weights) checked against the f64 oracle -- the reference's BPTT engine batched in
@@ -427,11 +433,19 @@ def main():
             g64, ldw = 0, kx
         else:          # one rank: straight from the engine's fp64 accumulators
             gw, gwo, g64, ldw = eng.grad_w_acc, eng.grad_wout, 1, eng.grad_w_acc.stride(0)
-        st = vp(torch.cuda.current_stream(dev).cuda_stream)
+        main = torch.cuda.current_stream(dev)
+        st = vp(main.cuda_stream)
         # W: SGD fused with the re-slicing of the first engine's INT8 digits
         eng.sgd_slice(gw, g64, ldw, g_scale, lr)
+        # W_out: on one rank its gradient comes from K7 on the engine's side stream, so the
+        # update follows K7 there (beside K5) and the step joins it at the end
+        side = eng.side if (world == 1 and WOUT_SIDE) else None
         _lib.call("spb_sgd_update", vp(wout_master.data_ptr()), 0, m, n, vp(gwo.data_ptr()),
-                  g64, n, g_scale, lr, vp(eng.wout.data_ptr()), st)
+                  g64, n, g_scale, lr, vp(eng.wout.data_ptr()),
+                  vp(side.cuda_stream) if side is not None else st)
+        if side is not None:
+            wo_done.record(side)
+            main.wait_event(wo_done)
         if wrec_master is not None:  # W_rec (columns k .. k+n) and its transposed copy
             # (a small step size keeps the recurrent activity -- the gather work -- at its
             # initial level over the timed steps; at lr = 1e-3 the synthetic network's
@@ -440,6 +454,8 @@ def main():
                       vp(gw.data_ptr() + gw.element_size() * k), g64, ldw, g_scale, 1e-6,
                       None, st)
             eng.wrecT.copy_(wrec_master.t())
+
+    wo_done = torch.cuda.Event()
 
     def local_part(x, y, timers=None, bits=False):
         # the synthetic Poisson inputs are 0/1 spikes: promise it (K2 single-int64 path)

@@ -22,6 +22,8 @@ ap.add_argument("--replays", type=int, default=10)
 ap.add_argument("--B", type=int, default=256)
 ap.add_argument("--T", type=int, default=250)
 ap.add_argument("--out", default="gpurun_out/step_timeline.json")
+ap.add_argument("--no-side", dest="side", action="store_false",
+                help="W_out update on the main stream instead of after K7 on the side stream")
 args = ap.parse_args()
 
 n, k, m, T, B = 1024, 700, 20, args.T, args.B
@@ -39,12 +41,21 @@ kw = dict(alpha=net.neuron.alpha, theta=net.neuron.theta, slope=net.neuron.slope
 vp = ctypes.c_void_p
 
 
-def step():
+wo_done = torch.cuda.Event()
+
+
+def step():  # as bench.py's update at one rank
     eng.run(xd, yd, binary=True, **kw)
-    st = vp(torch.cuda.current_stream(dev).cuda_stream)
+    main = torch.cuda.current_stream(dev)
+    st = vp(main.cuda_stream)
     eng.sgd_slice(eng.grad_w_acc, 1, eng.grad_w_acc.stride(0), 1.0 / B, 1e-3)
+    side = eng.side if args.side else None
     _lib.call("spb_sgd_update", vp(wout.data_ptr()), 0, m, n, vp(eng.grad_wout.data_ptr()), 1,
-              n, 1.0 / B, 1e-3, vp(eng.wout.data_ptr()), st)
+              n, 1.0 / B, 1e-3, vp(eng.wout.data_ptr()),
+              vp(side.cuda_stream) if side is not None else st)
+    if side is not None:
+        wo_done.record(side)
+        main.wait_event(wo_done)
 
 
 cs = torch.cuda.Stream(device=dev)
