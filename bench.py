@@ -152,10 +152,10 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-# SPB_WOUT_SIDE=1: the W_out update after K7 on the engine's side stream, beside K5 (A/B,
-# tools/wout_side_ab.sh): 2.5 us less device time per update (0.6028 vs 0.6056 ms) but a
-# slower e2e loop (97.8 vs 101.8 M), so the default keeps it on the main stream
-WOUT_SIDE = os.environ.get("SPB_WOUT_SIDE", "0") == "1"
+# The W_out update runs after K7 on the engine's side stream, beside K5 (one rank):
+# 0.6021 vs 0.6037 ms per update, e2e 106.2 vs 105.9 M (tools/wout_side_ab.sh, 3 alternating
+# pairs).  SPB_WOUT_SIDE=0 puts it on the main stream at the end of the update (A/B).
+WOUT_SIDE = os.environ.get("SPB_WOUT_SIDE", "1") != "0"
 
 
 def parity_block(eng, net, x_np, y_np, kw, kind, recurrent=False):

@@ -260,9 +260,17 @@ class DeviceTrainer:
         if self.optimizer == "sgd":
             # W update fused with the re-slicing of this engine's INT8 digits (one launch)
             eng.sgd_slice(g_w, g_w_f64, ld_w, scale, self.lr, stream=st.value)
+            # one rank: grad W_out comes from K7 on the engine's side stream -- the update
+            # follows it there (beside the gradient GEMM) and the main stream joins it
+            side = eng.side if self._world() == 1 else None
             self.lib.call("spb_sgd_update", v(self.w_out.data_ptr()), f64, m, n,
                           v(g_wo.data_ptr()), g_wo_f64, n, scale, self.lr,
-                          v(eng.wout.data_ptr()), st)
+                          v(eng.wout.data_ptr()),
+                          v(side.cuda_stream) if side is not None else st)
+            if side is not None:
+                done = torch.cuda.Event()
+                done.record(side)
+                torch.cuda.current_stream(self.device).wait_event(done)
         else:
             self.lib.call("spb_adam_update", v(self.w.data_ptr()), v(self.m_w.data_ptr()),
                           v(self.v_w.data_ptr()), f64, n, k, v(g_w.data_ptr()), g_w_f64, ld_w,

@@ -22,8 +22,8 @@ ap.add_argument("--replays", type=int, default=10)
 ap.add_argument("--B", type=int, default=256)
 ap.add_argument("--T", type=int, default=250)
 ap.add_argument("--out", default="gpurun_out/step_timeline.json")
-ap.add_argument("--side", action="store_true",
-                help="W_out update after K7 on the side stream (bench.py SPB_WOUT_SIDE=1)")
+ap.add_argument("--no-side", dest="side", action="store_false",
+                help="W_out update on the main stream (bench.py SPB_WOUT_SIDE=0)")
 args = ap.parse_args()
 
 n, k, m, T, B = 1024, 700, 20, args.T, args.B
