@@ -9,39 +9,65 @@
 
 #include "common.cuh"
 
+#ifndef K3_SB
+#define K3_SB 2  // samples per K3 CTA (A/B builds: -DK3_SB=1)
+#endif
+
 namespace spb {
 
+// SB samples per CTA: every W_out element loaded serves SB samples (W_out is re-read from
+// L2 by every CTA; at one sample per CTA that stream was most of K3's time inside the
+// update).  Per sample the arithmetic and its order are those of one sample per CTA.
+template <int SB>
 __global__ void readout_loss_kernel(const double* __restrict__ wout, const double* __restrict__ zsum,
-                                    const long long* __restrict__ labels, int n, int m,
+                                    const long long* __restrict__ labels, int B, int n, int m,
                                     double* __restrict__ s_out, double* __restrict__ loss,
                                     double* __restrict__ g_out, float* __restrict__ wsig,
                                     int* __restrict__ correct) {
   pdl_enter();
-  extern __shared__ double sm[];  // [m] logits + [m] g (exps, then dL/ds)
-  double* s = sm;
-  double* g = sm + m;
-  const int b = blockIdx.x;
+  extern __shared__ double sm[];  // [SB][m] logits + [SB][m] g (exps, then dL/ds)
+  const int b0 = blockIdx.x * SB;
+  const int nb = min(SB, B - b0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const double* z = zsum + (long long)b * n;
   // one warp per class (round robin): s_c = sum_i W_out[c][i] zsum[b][i], no block barriers
   for (int c = warp; c < m; c += nwarps) {
     const double* wr = wout + (long long)c * n;
-    double a0 = 0.0, a1 = 0.0;
+    double a0[SB], a1[SB];
+#pragma unroll
+    for (int q = 0; q < SB; ++q) a0[q] = a1[q] = 0.0;
+    const double* z[SB];
+#pragma unroll
+    for (int q = 0; q < SB; ++q) z[q] = zsum + (long long)(b0 + (q < nb ? q : 0)) * n;
     int i = lane;
 #pragma unroll 4
     for (; i + 32 < n; i += 64) {
-      a0 = fma(wr[i], z[i], a0);
-      a1 = fma(wr[i + 32], z[i + 32], a1);
+      const double w0 = wr[i], w1 = wr[i + 32];
+#pragma unroll
+      for (int q = 0; q < SB; ++q) {
+        a0[q] = fma(w0, z[q][i], a0[q]);
+        a1[q] = fma(w1, z[q][i + 32], a1[q]);
+      }
     }
-    if (i < n) a0 = fma(wr[i], z[i], a0);
-    double acc = a0 + a1;
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) s[c] = acc;
+    if (i < n) {
+      const double w0 = wr[i];
+#pragma unroll
+      for (int q = 0; q < SB; ++q) a0[q] = fma(w0, z[q][i], a0[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < SB; ++q) {
+      double acc = a0[q] + a1[q];
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) sm[q * m + c] = acc;
+    }
   }
   __syncthreads();
-  // softmax cross-entropy: the exps run one class per lane; the max, the first argmax and
-  // the sum of exps are taken in class order by one lane (the reference's order)
-  if (warp == 0) {
+  // softmax cross-entropy (warp q: sample b0 + q): the exps run one class per lane; the
+  // max, the first argmax and the sum of exps are taken in class order by one lane (the
+  // reference's order)
+  if (warp < nb) {
+    const int b = b0 + warp;
+    double* s = sm + warp * m;
+    double* g = sm + (SB + warp) * m;
     // an out-of-range label (the host wrappers reject them: LabelOutOfRange) yields a NaN
     // loss and no one-hot term instead of an out-of-bounds shared-memory read
     const long long yl = labels[b];
@@ -74,10 +100,19 @@ __global__ void readout_loss_kernel(const double* __restrict__ wout, const doubl
     }
   }
   __syncthreads();
+  const double* g = sm + SB * m;
   for (int i = tid; i < n; i += blockDim.x) {
-    double acc = 0.0;
-    for (int c = 0; c < m; ++c) acc = fma(wout[(long long)c * n + i], g[c], acc);
-    wsig[(long long)b * n + i] = (float)acc;
+    double acc[SB];
+#pragma unroll
+    for (int q = 0; q < SB; ++q) acc[q] = 0.0;
+    for (int c = 0; c < m; ++c) {
+      const double w = wout[(long long)c * n + i];
+#pragma unroll
+      for (int q = 0; q < SB; ++q) acc[q] = fma(w, g[q * m + c], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < SB; ++q)
+      if (q < nb) wsig[(long long)(b0 + q) * n + i] = (float)acc[q];
   }
 }
 
@@ -163,17 +198,23 @@ int spb_readout_loss(const double* wout, const double* zsum, const long long* la
   SPB_CHECK_ARG(wout && zsum && labels && s_out && loss && g && wsig,
                 "spb_readout_loss: null pointer");
   SPB_CHECK_ARG(B > 0 && n > 0 && m > 0 && m <= 4096, "spb_readout_loss: bad sizes");
-  const size_t smem = (size_t)(2 * m + 32) * sizeof(double);
+  // K3_SB samples per CTA (W_out read once per CTA for all of them) when that still
+  // leaves >= 64 CTAs; small batches keep one sample per CTA
+  constexpr int SB = K3_SB;
+  const bool multi = SB > 1 && B >= 64 * SB;
+  const int sb = multi ? SB : 1;
+  const size_t smem = (size_t)(2 * sb * m + 32) * sizeof(double);
   // one warp per class (up to 32 warps): the class dot products run in one round
   const int threads = 32 * (m < 8 ? 8 : (m > 32 ? 32 : m));
-  if (smem > 48 * 1024) {  // m > 3056: opt in to the larger dynamic shared memory
-    const cudaError_t e = cudaFuncSetAttribute(
-        readout_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kfn = multi ? readout_loss_kernel<SB> : readout_loss_kernel<1>;
+  if (smem > 48 * 1024) {  // large m: opt in to the larger dynamic shared memory
+    const cudaError_t e =
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     SPB_CHECK_ARG(e == cudaSuccess, "spb_readout_loss: smem opt-in failed: %s",
                   cudaGetErrorString(e));
   }
-  pdl_launch(readout_loss_kernel, B, threads, smem, stream, wout, zsum, labels, n, m, s_out, loss, g,
-                                                    wsig, correct);
+  pdl_launch(kfn, (B + sb - 1) / sb, threads, smem, stream, wout, zsum, labels, B, n, m, s_out,
+             loss, g, wsig, correct);
   SPB_CHECK_LAUNCH("readout_loss");
   return 0;
 }
