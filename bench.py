@@ -469,20 +469,32 @@ def main():
             packer.allreduce()
         update()
 
-    def captured_step(x, y, bits=False):
+    def captured_step(x, y, bits=False, loss_host=None):
         """The step as CUDA-graph replays on these input buffers: one graph at N = 1; at
         N > 1 the graph of the rank-local part (every kernel of the update and the payload
         pack), the allreduce launched eagerly on the same stream (collectives are not
         captured: a capture that succeeded on one rank but hung in replay on another would
-        deadlock the job), then the graph of the optimizer step."""
+        deadlock the job), then the graph of the optimizer step.  loss_host: the graph also
+        copies the per-sample losses to this pinned host buffer, on a branch that follows
+        the loss kernel (K3) and runs beside the rest of the update."""
         cs_ = torch.cuda.Stream(device=dev)
         cs_.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(cs_):
             step(x, y, bits=bits)                   # warm the capture stream
         torch.cuda.current_stream(dev).wait_stream(cs_)
         g1 = torch.cuda.CUDAGraph()
+        d2h = torch.cuda.Stream(device=dev) if loss_host is not None else None
         with torch.cuda.graph(g1, stream=cs_):
             local_part(x, y, bits=bits)
+            if d2h is not None:
+                ro = eng._ev.get("ro") if eng._ev else None
+                if ro is not None:     # K3 done (recorded by run() for K7's side stream)
+                    d2h.wait_event(ro)
+                else:
+                    d2h.wait_stream(cs_)
+                with torch.cuda.stream(d2h):
+                    loss_host.copy_(eng.loss, non_blocking=True)
+                cs_.wait_stream(d2h)
             if world == 1:
                 update()
         if world == 1:
@@ -583,9 +595,9 @@ def main():
         x_bits = np.packbits(x_np, axis=-1, bitorder="little")
         xh = torch.from_numpy(x_bits).pin_memory()
         yh = torch.from_numpy(y_np).pin_memory()
-        # the per-sample losses of step i: staged on the device (D2D, main stream) and read
-        # back to pinned host memory on the copy stream, so the D2H does not sit between two
-        # updates on the main stream (double-buffered, reuse waits for the earlier read)
+        # the per-sample losses of step i go to pinned host memory: inside the replayed
+        # graph on a branch after K3 (beside the rest of the update); eager steps stage them
+        # on the device and read them back on the copy stream (double-buffered)
         loss_h = [torch.empty(B, dtype=torch.float64).pin_memory() for _ in range(2)]
         loss_s = [torch.empty(B, dtype=torch.float64, device=dev) for _ in range(2)]
         staged = [torch.cuda.Event() for _ in range(2)]
@@ -615,7 +627,8 @@ def main():
                     xb[i].copy_(torch.from_numpy(x_bits).to(dev))
                     yb[i].copy_(yd)
                 torch.cuda.synchronize()
-                gsteps = [captured_step(xb[i], yb[i], bits=True) for i in range(2)]
+                gsteps = [captured_step(xb[i], yb[i], bits=True, loss_host=loss_h[i])
+                          for i in range(2)]
                 barrier()
             except Exception as exc:  # noqa: BLE001
                 print(f"[bench] e2e graph capture failed ({exc}); eager", file=sys.stderr)
@@ -632,20 +645,21 @@ def main():
                 else:
                     step(xb[i % 2], yb[i % 2], bits=True)
                 consumed[i % 2].record(main)
-                main.wait_event(read[i % 2])
-                loss_s[i % 2].copy_(eng.loss, non_blocking=True)
-                staged[i % 2].record(main)
-                with torch.cuda.stream(cs):
-                    cs.wait_event(staged[i % 2])
-                    loss_h[i % 2].copy_(loss_s[i % 2], non_blocking=True)
-                    read[i % 2].record(cs)
+                if gsteps is None:   # (the graph copies the losses itself)
+                    main.wait_event(read[i % 2])
+                    loss_s[i % 2].copy_(eng.loss, non_blocking=True)
+                    staged[i % 2].record(main)
+                    with torch.cuda.stream(cs):
+                        cs.wait_event(staged[i % 2])
+                        loss_h[i % 2].copy_(loss_s[i % 2], non_blocking=True)
+                        read[i % 2].record(cs)
             main.wait_stream(cs)   # the last read-back is inside the timed region
 
         run_e2e(3)
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        n_e2e = max(10, args.steps)
+        n_e2e = max(50, args.steps)   # short steps (C2) are host-jitter sensitive
         e0.record(main)
         run_e2e(n_e2e)
         e1.record(main)
@@ -659,8 +673,8 @@ def main():
                "d2h_bytes_per_step": int(B * 8),
                "ms_per_step": float(e2e_ms.item()),
                "pipeline": "H2D of step i+1 on a copy stream overlaps step i (double buffer); "
-                           "step i's losses are staged on the device and read back on the "
-                           "copy stream"
+                           "step i's losses are copied D2H right after its loss kernel, beside "
+                           "the rest of the update"
                            + ("; each step replays the whole update's CUDA graph"
                               if gsteps is not None else "")}
 
