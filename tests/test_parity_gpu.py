@@ -328,25 +328,28 @@ def test_projection_pair_multicast_is_bitwise_single_cta(B, T, n, k, binary, mon
     assert np.max(np.abs(ref - exact.astype(np.float64))) <= 2.3e-16 * np.max(np.abs(exact))
 
 
-@pytest.mark.parametrize("B,T,n,k,binary,chunk", [(40, 250, 1024, 700, True, 255),
-                                                    (5, 20, 96, 700, False, 63),
-                                                    (3, 31, 64, 128, True, 63),
-                                                    (2, 127, 200, 64, False, 127),
-                                                    (7, 33, 2048, 132, True, 63)])
-def test_projection_compact_rows_is_bitwise_kr_rows(B, T, n, k, binary, chunk):
+@pytest.mark.parametrize("B,T,n,k,binary,chunk,w64", [(40, 250, 1024, 700, True, 255, False),
+                                                        (5, 20, 96, 700, False, 63, False),
+                                                        (3, 31, 64, 128, True, 63, False),
+                                                        (2, 127, 200, 64, False, 127, False),
+                                                        (7, 33, 2048, 132, True, 63, False),
+                                                        (6, 45, 160, 900, True, 63, False),
+                                                        (4, 50, 96, 300, True, 63, True)])
+def test_projection_compact_rows_is_bitwise_kr_rows(B, T, n, k, binary, chunk, w64):
     """K2 over the chunk's live steps only (xq rows b*len + s, spb_input_proj_rows, the
     one-chunk default) writes the same currents to rows b*KR + s as the projection over
     all KR rows per sample -- bit for bit, incl. len < 32 (a quarter tile spanning several
-    samples) and the generic (non-binary / P != 6) epilogue."""
+    samples), the generic (non-binary / f64 weights, P = 8) epilogue and the streaming
+    kernel of K > 768 (k = 900)."""
     _need_gpu()
     import ctypes
     from paper_2501_11407_b200.engine import EpropEngine
     rng = np.random.default_rng(B * T + n)
-    w = (rng.uniform(-1, 1, (n, k)) / np.sqrt(k)).astype(np.float32)
+    w = (rng.uniform(-1, 1, (n, k)) / np.sqrt(k)).astype(np.float64 if w64 else np.float32)
     x = (rng.random((B, T, k)) < 0.1).astype(np.uint8)
     if not binary:
         x[0, :, :5] = 3
-    eng = EpropEngine(n, k, 3, B, alif=False, w_f64=False, chunk=chunk)
+    eng = EpropEngine(n, k, 3, B, alif=False, w_f64=w64, chunk=chunk)
     eng.set_weights(torch.from_numpy(w), torch.zeros((3, n), dtype=torch.float64))
     xd = torch.from_numpy(x).cuda()
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
