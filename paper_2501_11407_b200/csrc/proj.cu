@@ -182,6 +182,14 @@ constexpr int NH = NT / 2;  // neurons per epilogue thread (16 epilogue warps me
 // projection may read rin rows per sample (the chunk's live steps) and write rout rows per
 // sample (the current buffer's KR); rin == rout is the identity.  A 32-row quarter tile
 // crosses at most one sample boundary when rin >= 32.
+// r / rin (r >= 0, a quotient below 2^22: the sample index) without an integer division:
+// the float quotient is within one of the true one, corrected by one step either way
+__device__ __forceinline__ int proj_row_div(int r, int rin) {
+  int q = __float2int_rz(__fdividef((float)r, (float)rin));
+  if (q * rin > r) --q;
+  else if ((q + 1) * rin <= r) ++q;
+  return q;
+}
 __device__ __forceinline__ long long proj_out_row(int b0, int s0, int d, int rin, int rout) {
   int s = s0 + d, b = b0;
   if (rin >= 32) {
@@ -205,7 +213,7 @@ __device__ __forceinline__ void proj_epilogue_tile(uint32_t tbase, const SE (&se
                                                    uint32_t tempty_bar, int lane,
                                                    int probe = 0) {
   const int rq = row - lane;  // this warp's quarter-tile base row
-  const int b0 = rq / rin, s0 = rq - b0 * rin;
+  const int b0 = proj_row_div(rq, rin), s0 = rq - b0 * rin;
   long long g0[NH], g1[NH];
   {
     int32_t r[3][NH];
@@ -378,14 +386,14 @@ __device__ __forceinline__ void proj_epilogue_p6bin(uint32_t tbase, const double
     if (v[0][0][0] == 1.2345e-300 && row0 < M) out[(long long)row0 * n + col] = v[0][0][1];
     return;
   }
-  const int b0 = row0 / rin, s0 = row0 - b0 * rin;
+  const int b0 = proj_row_div(row0, rin), s0 = row0 - b0 * rin;
 #pragma unroll
   for (int h = 0; h < 2; ++h)
 #pragma unroll
     for (int rh = 0; rh < 2; ++rh) {
       const int d = 16 * h + 8 * rh + t4;
       if (row0 + d >= M) continue;
-      double* o = out + proj_out_row(b0, s0, d, rin, rout) * n + col;
+      double* o = out + (rin == rout ? (long long)(row0 + d) : proj_out_row(b0, s0, d, rin, rout)) * n + col;
       const double* w = v[h][rh];
       if ((n & 3) == 0) {  // 32-byte aligned quads, all in or all out
         if (col < n)
