@@ -834,7 +834,13 @@ __device__ __forceinline__ uint32_t expand4(uint32_t nib) {  // 4 bits -> 4 byte
 #ifndef PACK_GRID
 #define PACK_GRID (148 * 16)  // grid-stride pack: C3 0.7038 -> 0.6996 ms (148 * 4: 0.701)
 #endif
-constexpr int PACK_R = 4;  // byte-input pack: rows per CTA (2: 0.7136, 4: 0.7106, 8: 0.7125 ms at C3)
+#ifndef SPB_PACK_R
+#define SPB_PACK_R 8
+#endif
+// byte-input pack: rows per CTA iteration, their loads in flight together.  With the update
+// at 0.60 ms, 8 rows: pack 36.1 -> 33.6 us and the update's span 595.8 -> 592.5 us (device
+// timeline, tools/step_timeline.py); 16 rows: 42.8 us (round 1 at 0.71 ms: 4 rows best)
+constexpr int PACK_R = SPB_PACK_R;
 
 // bf16 of four spike counts (0..255, exact): the upper halves of their fp32 encodings
 __device__ __forceinline__ uint2 bf16x4_of_bytes(uint32_t w) {
