@@ -837,6 +837,9 @@ __device__ __forceinline__ uint32_t expand4(uint32_t nib) {  // 4 bits -> 4 byte
 #ifndef SPB_PACK_R
 #define SPB_PACK_R 8
 #endif
+#ifndef SPB_PACK_RB
+#define SPB_PACK_RB 4  // bit-packed input: rows per CTA iteration (8: same e2e, 16: -4 %)
+#endif
 // byte-input pack: rows per CTA iteration, their loads in flight together.  With the update
 // at 0.60 ms, 8 rows: pack 36.1 -> 33.6 us and the update's span 595.8 -> 592.5 us (device
 // timeline, tools/step_timeline.py); 16 rows: 42.8 us (round 1 at 0.71 ms: 4 rows best)
@@ -923,7 +926,7 @@ __global__ void __launch_bounds__(128) pack_bits8_kernel(const uint8_t* __restri
   // allocation (no packer writes them), so the pad is not rewritten every update
   const int wl = min(wpr, kb);
   const int rows = B * Tc;
-  constexpr int R = 4;
+  constexpr int R = SPB_PACK_RB;
   // grid-stride over row groups (as pack_bytes4_kernel)
   for (int row0 = blockIdx.x * R; row0 < rows; row0 += gridDim.x * R) {
     int sq[R], bq[R];
