@@ -73,6 +73,22 @@ __device__ __forceinline__ void rec_load_row(const WT* __restrict__ row, int i0,
   }
 }
 
+// Rows of -0.0 (the exact identity of IEEE addition, +0 + -0 = +0 included): the active
+// list is padded with them to a whole number of gather groups, so the gather runs without
+// per-row predicates or selects and the ordered sum is bitwise unchanged.
+#define SPB_NZ8 -0.0, -0.0, -0.0, -0.0, -0.0, -0.0, -0.0, -0.0
+#define SPB_NZ64 SPB_NZ8, SPB_NZ8, SPB_NZ8, SPB_NZ8, SPB_NZ8, SPB_NZ8, SPB_NZ8, SPB_NZ8
+#define SPB_NZ512 SPB_NZ64, SPB_NZ64, SPB_NZ64, SPB_NZ64, SPB_NZ64, SPB_NZ64, SPB_NZ64, SPB_NZ64
+#define SPB_NZ2048 SPB_NZ512, SPB_NZ512, SPB_NZ512, SPB_NZ512
+__device__ const double kNegZeroRowF64[REC_MAX_N] = {SPB_NZ2048};
+__device__ const float kNegZeroRowF32[REC_MAX_N] = {SPB_NZ2048};
+
+template <typename WT>
+__device__ __forceinline__ const WT* neg_zero_row() {
+  if constexpr (sizeof(WT) == 8) return reinterpret_cast<const WT*>(kNegZeroRowF64);
+  else return reinterpret_cast<const WT*>(kNegZeroRowF32);
+}
+
 // this warp's NPT mask words from each lane's NPT spike bits (bit c = neuron NPT*lane + c)
 template <int NPT>
 __device__ __forceinline__ uint32_t rec_mask_word(uint32_t nib, int lane, int q) {
@@ -91,7 +107,8 @@ __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_ker
     double* __restrict__ zsum_st, uint32_t* __restrict__ raster, float* __restrict__ psis,
     uint32_t* __restrict__ zchunk) {
   __shared__ uint32_t mask[2][REC_MAX_N / 32];
-  __shared__ uint16_t act[REC_MAX_N];
+  constexpr int GB = sizeof(WT) == 8 ? 4 : 8;   // spikes whose weight loads are in flight
+  __shared__ const WT* act[REC_MAX_N + GB];     // active rows of W_rec^T, -0.0 row padded
   __shared__ int nact;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x;
@@ -101,6 +118,7 @@ __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_ker
   const float slope_f = (float)P.slope;
   const WT* wt = static_cast<const WT*>(wrecT);
   const int i0 = NPT * tid;            // this thread's first neuron
+  const int iv = i0 < n ? i0 : 0;      // its gather offset (idle threads: the row start)
   const int wbase = NPT * warp;        // this warp's first mask word
   double u[NPT], a[NPT], zb[NPT], zs[NPT], dp[NPT];
 #pragma unroll
@@ -164,12 +182,14 @@ __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_ker
         }
         int pos = base + incl - cnt;
         while (bits) {
-          act[pos++] = (uint16_t)((w << 5) + __ffs(bits) - 1);
+          act[pos++] = wt + (long long)((w << 5) + __ffs(bits) - 1) * n;
           bits &= bits - 1;
         }
         base += __shfl_sync(0xffffffffu, incl, 31);
       }
-      if (lane == 0) nact = base;
+      const int padded = (base + GB - 1) / GB * GB;
+      if (base + lane < padded) act[base + lane] = neg_zero_row<WT>();
+      if (lane == 0) nact = padded;
     }
     __syncthreads();
     // recurrent current: sum over the active presynaptic j in ascending order, the
@@ -177,24 +197,23 @@ __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_ker
     double R[NPT];
 #pragma unroll
     for (int c = 0; c < NPT; ++c) R[c] = 0.0;
-    const int na = nact;
-    constexpr int GB = sizeof(WT) == 8 ? 4 : 8;   // spikes whose weight loads are in flight
+    const int na = nact;   // a multiple of GB (-0.0 rows at the end)
     for (int q0 = 0; q0 < na; q0 += GB) {
       WT wv[GB][NPT];
 #pragma unroll
       for (int q = 0; q < GB; ++q) {
-        if (q0 + q < na) {
-          rec_load_row<NPT, WT, VEC>(wt + (long long)act[q0 + q] * n, i0, n, wv[q]);
+        if constexpr (VEC) {
+          // n % NPT == 0: a valid thread's NPT weights lie inside the row; an idle thread
+          // (i0 >= n) reads the row start, its sums are never used
+          rec_load_row<NPT, WT, VEC>(act[q0 + q] + iv, 0, 1, wv[q]);
         } else {
-#pragma unroll
-          for (int c = 0; c < NPT; ++c) wv[q][c] = WT(0);
+          rec_load_row<NPT, WT, VEC>(act[q0 + q], i0, n, wv[q]);
         }
       }
 #pragma unroll
       for (int q = 0; q < GB; ++q)
 #pragma unroll
-        for (int c = 0; c < NPT; ++c)
-          if (q0 + q < na) R[c] = __dadd_rn(R[c], (double)wv[q][c]);
+        for (int c = 0; c < NPT; ++c) R[c] = __dadd_rn(R[c], (double)wv[q][c]);
     }
     float psi[NPT];
     uint32_t nib = 0;
