@@ -17,7 +17,7 @@
 // One CTA per sample, 512 threads, NPT <= 4 consecutive neurons per thread (n <= 2048),
 // two CTAs per SM for n <= 1024; the spikes of the previous step live in a double-buffered shared
 // bitmask, compacted by one warp into an ascending active list each step (two
-// __syncthreads per step) so that the weight loads of 8 presynaptic spikes are in flight
+// __syncthreads per step) and padded with a -0.0 row to whole groups of SPB_REC_GB rows in flight
 // at once.  The step is latency-bound (L2 round trips of the gather + two barriers).
 // W_rec is stored transposed (wrecT[j][i] = W_rec[i][j]) so the gather of an active
 // presynaptic row is coalesced across the CTA's threads.
@@ -107,7 +107,10 @@ __global__ void __launch_bounds__(REC_THREADS, NPT <= 2 ? 2 : 1) forward_rec_ker
     double* __restrict__ zsum_st, uint32_t* __restrict__ raster, float* __restrict__ psis,
     uint32_t* __restrict__ zchunk) {
   __shared__ uint32_t mask[2][REC_MAX_N / 32];
-  constexpr int GB = sizeof(WT) == 8 ? 4 : 8;   // spikes whose weight loads are in flight
+#ifndef SPB_REC_GB
+#define SPB_REC_GB 2
+#endif
+  constexpr int GB = sizeof(WT) == 8 ? SPB_REC_GB / 2 : SPB_REC_GB;   // spikes whose weight loads are in flight
   __shared__ const WT* act[REC_MAX_N + GB];     // active rows of W_rec^T, -0.0 row padded
   __shared__ int nact;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
